@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: certified reach-steps/s of the B200 DT reachability primitive.
+
+Workload (default, BASELINE.json configs[3]): the initial-set partition sweep
+-- 65,536 sub-boxes (8x8x8x8x4x4) of a 6-D system through a 3x128 ReLU
+one-step map, horizon 30 -- i.e. reach_with_splitting(dt_reach) (refine.hpp:
+121-160).  One "step" = one full sweep (65,536 sub-boxes x 30 DT steps) with
+the per-step hull; a reach-step is one sub-box advanced one DT step.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU, NCCL): weak scaling -- the global plan is
+N x 65,536 parts (first split count x N), each rank sweeps its own contiguous
+65,536 parts, and the per-step hull is combined with one NCCL all-reduce
+(min on lo / max on hi / min on the failure key), the path's only exchange.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified reference headers compiled -O2) on the host cores, each step a
+bounded sample of the same sweep.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "certified reach-steps/sec (batch x horizon)"
+UNIT = "reach-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-sample-parts", type=int, default=0, help="parts per CPU sample (0 = auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def algorithmic_flops_per_part(net_dims, n, m, H, window):
+    """Algorithmic FP64 flops of one sub-box's H-step dt_reach:
+    IBP (2 mul + 2 add per weight, hidden layers + prepend), the Lambda.W
+    contractions (2 per MAC), the prepend Lambda.A and shift, relaxation
+    chains (intercepts, scaling, shift: 7 per Lambda entry), and the fold
+    solve (~6 n^3 when it runs).  I . W_out is excluded (a copy)."""
+    L = len(net_dims) - 1
+    cap = window if window > 0 else 1
+    hidden = net_dims[1:L]
+    total = 0
+    nq = 0
+    for k in range(H):
+        nz = n * (1 + nq)
+        f = 2 * n * nz + 2 * n  # prepend IBP
+        f += 4 * n * net_dims[1] if L > 1 else 0  # layer 0 IBP (x columns)
+        f += 2 * m * net_dims[1] if (L > 1 and m) else 0  # action fold
+        for l in range(1, L - 1):
+            f += 4 * net_dims[l] * net_dims[l + 1]
+        # backward Lambda.W for l = L-2 .. 0
+        for l in range(L - 2, -1, -1):
+            cols = n if l == 0 else net_dims[l]
+            f += 2 * n * net_dims[l + 1] * cols
+        f += 7 * n * sum(hidden)  # relaxation chains
+        f += 2 * n * n * nz + 2 * n * n  # prepend Lambda.A + shift
+        nq += 1
+        if nq > cap:
+            f += 6 * n ** 3
+            nq -= 1
+        total += f
+    return total
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(w, parts: int, threads: int = 0):
+    """The reference itself (oracle/_ref) on `parts` sub-boxes of the sweep."""
+    from oracle_bind import ref_available, ref_split_hull, ref_lib
+    if not ref_available():
+        return None
+    lib = ref_lib()
+    lib.ref_hardware_threads.restype = C.c_int
+    cores = threads or int(lib.ref_hardware_threads())
+    t0 = time.perf_counter()
+    ref_split_hull(w.sys, w.x0_lo, w.x0_hi, w.plan, w.actions, begin=0, end=parts, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": parts * w.horizon / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{parts} of {w.plan.total_parts()} sub-boxes x {w.horizon} steps through the reference "
+                      f"reach_with_splitting pieces (oracle/_ref, g++ -O2), {dt:.2f} s"}
+
+
+def auto_cpu_parts():
+    cores = os.cpu_count() or 8
+    # ~15 ms per sub-box-horizon per core (survey probe) -> aim at ~10-15 s
+    return int(max(256, min(65536, cores * 800)))
+
+
+def run_reference(args):
+    from paper_2605_25346_b200.workloads import c4_partition_sweep
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    w = c4_partition_sweep()
+    parts = args.cpu_sample_parts or max(128, auto_cpu_parts() // 8)
+    times = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(w, parts)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libreach_ref.so not built"}))
+            return
+        if i >= args.warmup:
+            times.append(parts * w.horizon / r["value"])
+            cb = r
+    ms = 1e3 * float(np.mean(times))
+    value = parts * w.horizon / (ms / 1e3)
+    cb["value"] = value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c4_partition_sweep (BASELINE configs[3]) bounded CPU sample",
+                       "sub_boxes_per_step": parts, "horizon": w.horizon, "state_dim": 6,
+                       "net": "6->128x3->6 ReLU", "plan": "8x8x8x8x4x4"},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    from paper_2605_25346_b200 import _abi as A
+    from paper_2605_25346_b200._native import Context
+    from paper_2605_25346_b200.api import SplitPlan, reach_split_hull
+    from paper_2605_25346_b200.workloads import c4_partition_sweep
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = c4_partition_sweep()
+    per_rank = w.plan.total_parts()
+    counts = list(w.plan.counts)
+    counts[0] *= world
+    plan = SplitPlan(counts)
+    begin, end = rank * per_rank, (rank + 1) * per_rank
+    H, n, m = w.horizon, w.sys.n, w.sys.m
+
+    ctx = Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    netdims = [int(x) for x in w.sys.step.dims()]
+    flops_part = algorithmic_flops_per_part(netdims, n, m, H, 4)
+
+    # device-resident outputs; the X0 box / plan are kernel parameters
+    cnt = (H + 1) * n
+    d_lo = torch.empty(cnt, dtype=torch.float64, device=dev)
+    d_hi = torch.empty(cnt, dtype=torch.float64, device=dev)
+    d_div = torch.empty(H + 1, dtype=torch.int32, device=dev)
+    d_nb = torch.empty(1, dtype=torch.int32, device=dev)
+    d_key = torch.empty(1, dtype=torch.int64, device=dev)
+    d_act = torch.zeros(max(H * m, 1), dtype=torch.float64, device=dev)
+    x0lo = np.ascontiguousarray(w.x0_lo)
+    x0hi = np.ascontiguousarray(w.x0_hi)
+    cts = np.array(counts, dtype=np.int32)
+    args_c = A.SplitArgs(n, m, H, 4, 0, A.dptr(x0lo), A.dptr(x0hi), A.iptr(cts), A.dptr(d_act.data_ptr()),
+                         begin, end)
+    out_c = A.HullOut(A.dptr(d_lo.data_ptr()), A.dptr(d_hi.data_ptr()), A.iptr(d_div.data_ptr()),
+                      A.iptr(d_nb.data_ptr()), A.lptr(d_key.data_ptr()))
+    net = ctx.upload(w.sys.step)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def device_step():
+        ctx.check(ctx._lib.reach_split_hull(ctx.handle, net, C.byref(args_c), C.byref(out_c),
+                                            A.REACH_FLAG_DEVICE_PTRS), "reach_split_hull")
+        if world > 1:
+            lo_ = torch.where(torch.isnan(d_lo), torch.full_like(d_lo, float("inf")), d_lo)
+            dist.all_reduce(lo_, op=dist.ReduceOp.MIN)
+            dist.all_reduce(d_hi, op=dist.ReduceOp.MAX)
+            dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
+            dist.all_reduce(d_nb, op=dist.ReduceOp.MIN)
+            d_lo.copy_(lo_)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        device_step()
+    barrier()
+
+    # ---- timed region (device events per step, L2 flushed between steps)
+    ctx.enable_kernel_timing(True)
+    ctx.kernel_time()
+    launches0 = ctx.launch_count
+    clocks = ClockSampler(local)
+    clocks.start()
+    step_ms = []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        ev0.record(stream)
+        device_step()
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+    barrier()
+    clk = clocks.stop()
+    kern_ms, kern_n = ctx.kernel_time()
+    launches = ctx.launch_count - launches0
+    ctx.enable_kernel_timing(False)
+    t_local = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([t_local, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max, kern_max = float(t[0]), float(t[1])
+    else:
+        t_max, kern_max = t_local, kern_ms
+    reach_steps = per_rank * world * H
+    value = reach_steps * args.steps / (t_max / 1e3)
+
+    # ---- end to end through the public API (host X0/plan/actions in, host hull out)
+    from paper_2605_25346_b200.api import DTReachParams
+    ctx.set_stream(None)
+    e2e_t = []
+    for i in range(args.warmup + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        res = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, DTReachParams(), begin, end, ctx=ctx)
+        if world > 1:
+            hl = torch.tensor(np.where(np.isnan(res.lo), np.inf, res.lo), device=dev)
+            hh = torch.tensor(res.hi, device=dev)
+            dist.all_reduce(hl, op=dist.ReduceOp.MIN)
+            dist.all_reduce(hh, op=dist.ReduceOp.MAX)
+            hl.cpu(), hh.cpu()
+        dt_ = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_t.append(dt_)
+    e2e_local = float(np.sum(e2e_t))
+    if world > 1:
+        t = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_local = float(t[0])
+    e2e_value = reach_steps * args.steps / e2e_local
+    h2d = 2 * n * 8 + n * 4 + H * m * 8
+    d2h = 2 * (H + 1) * n * 8 + (H + 1) * 4 + 4 + 8
+
+    # ---- roofline of the dominant kernel (dt_horizon_kernel), FP64 pipe
+    tf_fma, tf_ma = ctx.fp64_peak()
+    ach = flops_part * per_rank / (kern_max / max(kern_n, 1) / 1e3) / 1e12
+    roof = {"bound": "fp64", "achieved": ach, "peak": tf_fma, "unit": "TFLOP/s", "frac": ach / tf_fma,
+            "traffic": None, "kernel": "rb::dt_horizon_kernel<6,4>",
+            "flops_per_launch": flops_part * per_rank,
+            "peak_source": "measured on this box by reach_measure_fp64_peak (DFMA chains, 2 flops/instr)",
+            "exact_mode_ceiling_tflops": tf_ma,
+            "frac_of_exact_mode_ceiling": ach / tf_ma if tf_ma else None,
+            "kernel_ms_per_launch": kern_max / max(kern_n, 1)}
+    prof = os.path.join(ROOT, "profiles", "c4_dram_traffic.json")
+    if os.path.exists(prof):
+        try:
+            roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    # ---- parity spot check vs the oracle (first 64 parts of this rank, bit-exact)
+    parity = None
+    if rank == 0:
+        try:
+            from oracle_bind import oracle_split_hull, same_bits
+            g = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=0, part_end=64, ctx=ctx)
+            e = oracle_split_hull(w.sys, w.x0_lo, w.x0_hi, plan, w.actions, begin=0, end=64)
+            parity = {"parts": 64, "bit_exact": bool(same_bits(g.lo, e.lo) and same_bits(g.hi, e.hi)
+                                                     and g.n_boxes == e.n_boxes)}
+        except Exception as ex:  # the checker is optional at bench time
+            parity = {"error": str(ex)}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(w, args.cpu_sample_parts or auto_cpu_parts())
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "c4_partition_sweep (BASELINE configs[3])", "sub_boxes_per_gpu": per_rank,
+                           "sub_boxes_total": per_rank * world, "plan": "x".join(map(str, counts)),
+                           "horizon": H, "state_dim": n, "net": "6->128x3->6 ReLU (residual synthetic)",
+                           "window": 4, "l2": "flushed between timed steps (256 MB write)",
+                           "parallelism": f"dp{world}"},
+                "roofline": roof, "cpu_baseline": cb,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches, "clocks": clk, "parity": parity,
+                "bit_exact_vs_reference": "ReLU path: identical operation order and roundings (tests/test_gpu_dt.py)"}
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

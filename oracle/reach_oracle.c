@@ -1,0 +1,511 @@
+/*
+ * TEST INFRASTRUCTURE ONLY -- the CPU oracle.  Never linked into, loaded by,
+ * or called from the product path (paper_2605_25346_b200/).  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline leg may use it.
+ *
+ * A plain-C restatement of the reference's discrete-time reachability path,
+ * operation for operation in the same order and rounding (no FMA contraction:
+ * built with -ffp-contract=off), so it is bit-identical to the reference
+ * compiled at -O2 on x86-64.  Pinned against oracle/_ref (the reference
+ * itself) and the reference's golden vectors in tests/test_oracle.py.
+ *
+ * Each function cites the reference file:line it restates
+ * (paths relative to /root/reference/proj/include/reach/).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "reach_b200.h"
+
+/* std::min / std::max semantics (first argument wins ties, NaN-asymmetric). */
+static double smin(double a, double b) { return (b < a) ? b : a; }
+static double smax(double a, double b) { return (a < b) ? b : a; }
+
+typedef struct { double lo, hi; } iv;
+
+/* iv_add (interval.hpp:60) in nearest rounding. */
+static iv iv_add(iv a, iv b) { iv r = {a.lo + b.lo, a.hi + b.hi}; return r; }
+/* iv_scale (interval.hpp:83). */
+static iv iv_scale(double a, iv x) {
+  iv r;
+  if (a >= 0.0) { r.lo = a * x.lo; r.hi = a * x.hi; }
+  else { r.lo = a * x.hi; r.hi = a * x.lo; }
+  return r;
+}
+static int iv_finite(iv x) { return isfinite(x.lo) && isfinite(x.hi); }
+
+typedef struct {
+  int rows, cols, act;
+  const double* w; /* row-major rows x cols */
+  const double* b;
+} layer_t;
+
+typedef struct {
+  int n_layers;
+  layer_t* layers;
+} net_t;
+
+static net_t net_from_desc(const reach_net_desc* d) {
+  net_t net;
+  net.n_layers = d->n_layers;
+  net.layers = (layer_t*)malloc(sizeof(layer_t) * (size_t)d->n_layers);
+  size_t k = 0;
+  for (int l = 0; l < d->n_layers; ++l) {
+    layer_t* L = &net.layers[l];
+    L->rows = d->dims[l + 1];
+    L->cols = d->dims[l];
+    L->act = d->acts[l];
+    L->w = d->params + k;
+    k += (size_t)L->rows * L->cols;
+    L->b = d->params + k;
+    k += (size_t)L->rows;
+  }
+  return net;
+}
+
+/* relax_activation (neural.hpp:166-227).  Returns 0, or 1 on a non-finite
+ * preactivation (the reference throws std::invalid_argument). */
+static int relax_activation(int act, iv pre, double* slope, double* li, double* ui) {
+  if (!iv_finite(pre)) return 1;
+  const double l = pre.lo, u = pre.hi;
+  *slope = 0.0; *li = 0.0; *ui = 0.0;
+  if (act == REACH_ACT_IDENTITY) {
+    *slope = 1.0;
+  } else if (act == REACH_ACT_RELU) {
+    if (l >= 0.0) {
+      *slope = 1.0;
+    } else if (u <= 0.0) {
+      *slope = 0.0;
+    } else {
+      double s = u / (u - l);
+      *slope = s;
+      *ui = -s * l;
+      *li = smin(0.0, smin(-s * l, u - s * u));
+    }
+  } else { /* tanh */
+    double tl = tanh(l), tu = tanh(u);
+    double s = smin(1.0 - tl * tl, 1.0 - tu * tu);
+    *slope = s;
+    double lo_int = tl - s * l, hi_int = lo_int;
+    double g = tu - s * u;
+    lo_int = smin(lo_int, g); hi_int = smax(hi_int, g);
+    if (s < 1.0 && s > 0.0) {
+      double xs = atanh(sqrt(1.0 - s));
+      if (l <= xs && xs <= u) { g = tanh(xs) - s * xs; lo_int = smin(lo_int, g); hi_int = smax(hi_int, g); }
+      if (l <= -xs && -xs <= u) { g = tanh(-xs) - s * -xs; lo_int = smin(lo_int, g); hi_int = smax(hi_int, g); }
+    }
+    double margin = (hi_int - lo_int) * 1e-12 + 1e-15;
+    *li = lo_int - margin;
+    *ui = hi_int + margin;
+  }
+  return 0;
+}
+
+/* act_interval (neural.hpp:229-241). */
+static iv act_interval(int act, iv p) {
+  iv r = p;
+  if (act == REACH_ACT_RELU) { r.lo = smax(p.lo, 0.0); r.hi = smax(p.hi, 0.0); }
+  else if (act == REACH_ACT_TANH) { r.lo = tanh(p.lo); r.hi = tanh(p.hi); }
+  return r;
+}
+
+/*
+ * certify_tm_input (neural.hpp:342-394) on the prepended wide network,
+ * with crown_backward (neural.hpp:290-335) and preactivation_bounds
+ * (neural.hpp:243-257) inlined.  Input TM: x = c + A z + r, z in [-1,1]^nz,
+ * r in ig (time_horizon = 0).  `net` layers 0..L-1 are the (frozen) network;
+ * layer 0 of `net` has n_i columns.  Outputs: out_c[n_o], out_A[n_o x nz]
+ * (ld nz), rem[n_o].  Returns 0 ok, 1 non-finite preactivation.
+ */
+static int certify_tm_input(const net_t* net, int n_i, int nz, const double* c, const double* A /* n_i x nz */,
+                            const iv* ig, double* out_c, double* out_A, iv* rem) {
+  const int L = net->n_layers;
+  const int n_o = net->layers[L - 1].rows;
+  const int wcols = nz + n_i;
+  int maxw = wcols;
+  for (int l = 0; l < L; ++l) { if (net->layers[l].rows > maxw) maxw = net->layers[l].rows; if (net->layers[l].cols > maxw) maxw = net->layers[l].cols; }
+  /* preactivation boxes: wide layer 0 (prepend) then net layers */
+  iv** pre = (iv**)malloc(sizeof(iv*) * (size_t)(L + 1));
+  pre[0] = (iv*)malloc(sizeof(iv) * (size_t)n_i);
+  for (int l = 0; l < L; ++l) pre[l + 1] = (iv*)malloc(sizeof(iv) * (size_t)net->layers[l].rows);
+  iv* h = (iv*)malloc(sizeof(iv) * (size_t)maxw);
+  iv* hn = (iv*)malloc(sizeof(iv) * (size_t)maxw);
+  /* prepend layer: W = [A | I], b = c, domain [-1,1]^nz x ig (neural.hpp:360-373),
+     box_affine_image (interval.hpp:284-295) */
+  for (int i = 0; i < n_i; ++i) {
+    iv acc = {0.0, 0.0};
+    const iv unit = {-1.0, 1.0};
+    for (int j = 0; j < nz; ++j) acc = iv_add(acc, iv_scale(A[(size_t)i * nz + j], unit));
+    for (int j = 0; j < n_i; ++j) acc = iv_add(acc, iv_scale(j == i ? 1.0 : 0.0, ig[j]));
+    iv bb = {c[i], c[i]};
+    pre[0][i] = iv_add(acc, bb);
+    h[i] = pre[0][i]; /* identity act */
+  }
+  int hw = n_i;
+  for (int l = 0; l < L; ++l) {
+    const layer_t* Ly = &net->layers[l];
+    for (int i = 0; i < Ly->rows; ++i) {
+      iv acc = {0.0, 0.0};
+      for (int j = 0; j < Ly->cols; ++j) acc = iv_add(acc, iv_scale(Ly->w[(size_t)i * Ly->cols + j], h[j]));
+      iv bb = {Ly->b[i], Ly->b[i]};
+      pre[l + 1][i] = iv_add(acc, bb);
+      hn[i] = act_interval(Ly->act, pre[l + 1][i]);
+    }
+    iv* t = h; h = hn; hn = t;
+    hw = Ly->rows;
+  }
+  (void)hw;
+
+  /* backward (neural.hpp:297-327), a = Lambda (n_o x width) row-major */
+  double* a = (double*)malloc(sizeof(double) * (size_t)n_o * (size_t)(maxw > n_o ? maxw : n_o));
+  double* an = (double*)malloc(sizeof(double) * (size_t)n_o * (size_t)(maxw > n_o ? maxw : n_o));
+  double* b_lo = (double*)calloc((size_t)n_o, sizeof(double));
+  double* b_up = (double*)calloc((size_t)n_o, sizeof(double));
+  double* shift = (double*)malloc(sizeof(double) * (size_t)n_o);
+  int acols = n_o;
+  for (int i = 0; i < n_o; ++i)
+    for (int j = 0; j < n_o; ++j) a[(size_t)i * n_o + j] = (i == j) ? 1.0 : 0.0;
+  int status = 0;
+  for (int l = L; l >= 0 && status == 0; --l) {
+    /* wide layer l: l == 0 is the prepend layer, else net layer l-1 */
+    int rows, cols, act;
+    const double* w = NULL; const double* bias = NULL;
+    if (l == 0) { rows = n_i; cols = wcols; act = REACH_ACT_IDENTITY; bias = c; }
+    else { const layer_t* Ly = &net->layers[l - 1]; rows = Ly->rows; cols = Ly->cols; act = Ly->act; w = Ly->w; bias = Ly->b; }
+    (void)rows;
+    if (act != REACH_ACT_IDENTITY) {
+      for (int j = 0; j < acols; ++j) {
+        double s, li, ui;
+        if (relax_activation(act, pre[l][j], &s, &li, &ui)) { status = 1; break; }
+        for (int i = 0; i < n_o; ++i) {
+          double aij = a[(size_t)i * acols + j];
+          if (aij >= 0.0) { b_lo[i] += aij * li; b_up[i] += aij * ui; }
+          else { b_lo[i] += aij * ui; b_up[i] += aij * li; }
+          a[(size_t)i * acols + j] = aij * s;
+        }
+      }
+      if (status) break;
+    }
+    /* shift = matvec(a, b) (linalg.hpp:40-51); b += shift (vadd) */
+    for (int i = 0; i < n_o; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < acols; ++j) acc += a[(size_t)i * acols + j] * bias[j];
+      shift[i] = acc;
+    }
+    for (int i = 0; i < n_o; ++i) { b_lo[i] = b_lo[i] + shift[i]; b_up[i] = b_up[i] + shift[i]; }
+    /* a = matmul(a, W) (linalg.hpp:53-63), i-k-j order */
+    for (int i = 0; i < n_o; ++i) {
+      double* crow = an + (size_t)i * cols;
+      for (int j = 0; j < cols; ++j) crow[j] = 0.0;
+      for (int k = 0; k < acols; ++k) {
+        double aik = a[(size_t)i * acols + k];
+        if (l == 0) {
+          for (int j = 0; j < nz; ++j) crow[j] += aik * A[(size_t)k * nz + j];
+          for (int j = 0; j < n_i; ++j) crow[nz + j] += aik * ((j == k) ? 1.0 : 0.0);
+        } else {
+          const double* wrow = w + (size_t)k * cols;
+          for (int j = 0; j < cols; ++j) crow[j] += aik * wrow[j];
+        }
+      }
+    }
+    double* t = a; a = an; an = t;
+    acols = cols;
+  }
+  if (status == 0) {
+    /* tail (neural.hpp:383-391) */
+    for (int i = 0; i < n_o; ++i) {
+      double mid = (b_lo[i] + b_up[i]) * 0.5;
+      out_c[i] = mid;
+      for (int j = 0; j < nz; ++j) out_A[(size_t)i * nz + j] = a[(size_t)i * wcols + j];
+      iv r = {b_lo[i] - mid, b_up[i] - mid};
+      for (int j = 0; j < n_i; ++j) r = iv_add(r, iv_scale(a[(size_t)i * wcols + nz + j], ig[j]));
+      rem[i] = r;
+    }
+  }
+  for (int l = 0; l <= L; ++l) free(pre[l]);
+  free(pre); free(h); free(hn); free(a); free(an); free(b_lo); free(b_up); free(shift);
+  return status;
+}
+
+/* mat_solve (linalg.hpp:96-132): A X = B, A n x n, B n x m, partial pivoting. */
+static int mat_solve(int n, int m, const double* A0, const double* B0, double* X) {
+  double* a = (double*)malloc(sizeof(double) * (size_t)n * n);
+  double* b = (double*)malloc(sizeof(double) * (size_t)n * m);
+  memcpy(a, A0, sizeof(double) * (size_t)n * n);
+  memcpy(b, B0, sizeof(double) * (size_t)n * m);
+  int ok = 1;
+  for (int k = 0; k < n && ok; ++k) {
+    int piv = k;
+    double best = fabs(a[(size_t)k * n + k]);
+    for (int i = k + 1; i < n; ++i) {
+      double cand = fabs(a[(size_t)i * n + k]);
+      if (cand > best) { best = cand; piv = i; }
+    }
+    if (!(best > 1e-12)) { ok = 0; break; }
+    if (piv != k) {
+      for (int j = 0; j < n; ++j) { double t = a[(size_t)k * n + j]; a[(size_t)k * n + j] = a[(size_t)piv * n + j]; a[(size_t)piv * n + j] = t; }
+      for (int j = 0; j < m; ++j) { double t = b[(size_t)k * m + j]; b[(size_t)k * m + j] = b[(size_t)piv * m + j]; b[(size_t)piv * m + j] = t; }
+    }
+    for (int i = k + 1; i < n; ++i) {
+      double f = a[(size_t)i * n + k] / a[(size_t)k * n + k];
+      for (int j = k; j < n; ++j) a[(size_t)i * n + j] -= f * a[(size_t)k * n + j];
+      for (int j = 0; j < m; ++j) b[(size_t)i * m + j] -= f * b[(size_t)k * m + j];
+    }
+  }
+  if (ok) {
+    for (int i = n - 1; i >= 0; --i)
+      for (int j = 0; j < m; ++j) {
+        double acc = b[(size_t)i * m + j];
+        for (int k = i + 1; k < n; ++k) acc -= a[(size_t)i * n + k] * X[(size_t)k * m + j];
+        X[(size_t)i * m + j] = acc / a[(size_t)i * n + i];
+      }
+  }
+  free(a); free(b);
+  return ok;
+}
+
+static double row_abs_sum(const double* M, int cols, int i) {
+  double acc = 0.0;
+  for (int j = 0; j < cols; ++j) acc += fabs(M[(size_t)i * cols + j]);
+  return acc;
+}
+
+/* SymbolicState (flowpipe_ct.hpp:286-300) for the DT path: every block is
+ * n x n (G0 from the diagonal init, fresh blocks n x n). blocks[0] = G0,
+ * blocks[1..nq] = queue oldest..newest. */
+typedef struct {
+  int n, nq, window;
+  double* c;      /* n */
+  double* blocks; /* (window+3) * n * n */
+} symstate;
+
+static int sym_cap(const symstate* s) { return s->window > 0 ? s->window : 1; }
+static double* blk(symstate* s, int b) { return s->blocks + (size_t)b * s->n * s->n; }
+
+/* init_symbolic_state (flowpipe_ct.hpp:303-309) */
+static void sym_init(symstate* s, const double* lo, const double* hi) {
+  const int n = s->n;
+  s->nq = 0;
+  double* g0 = blk(s, 0);
+  memset(g0, 0, sizeof(double) * (size_t)n * n);
+  for (int i = 0; i < n; ++i) {
+    s->c[i] = (lo[i] + hi[i]) * 0.5;          /* Interval::mid */
+    g0[(size_t)i * n + i] = (hi[i] - lo[i]) * 0.5; /* Interval::rad */
+  }
+}
+
+/* fold_overflow (flowpipe_ct.hpp:317-350) */
+static void fold_overflow(symstate* s) {
+  const int n = s->n;
+  double* x = (double*)malloc(sizeof(double) * (size_t)n * n);
+  double* e = (double*)malloc(sizeof(double) * (size_t)n * n);
+  double* r = (double*)malloc(sizeof(double) * (size_t)n);
+  while (s->nq > sym_cap(s)) {
+    double* a = blk(s, 1);
+    double* newest = blk(s, s->nq);
+    double* g0 = blk(s, 0);
+    int folded = 0;
+    if (mat_solve(n, n, g0, a, x)) {
+      double worst = 0.0;
+      for (int j = 0; j < n; ++j) {
+        r[j] = row_abs_sum(x, n, j) * (1.0 + 1e-12);
+        worst = smax(worst, r[j]); /* std::max(worst, value(r_j)) */
+      }
+      if (worst <= 1.0) {
+        for (int i = 0; i < n; ++i) {
+          for (int j = 0; j < n; ++j) e[(size_t)i * n + j] = 0.0;
+          for (int k = 0; k < n; ++k) {
+            double gik = g0[(size_t)i * n + k];
+            for (int j = 0; j < n; ++j) e[(size_t)i * n + j] += gik * x[(size_t)k * n + j];
+          }
+        }
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) e[(size_t)i * n + j] -= a[(size_t)i * n + j];
+        for (int j = 0; j < n; ++j)
+          for (int i = 0; i < n; ++i) g0[(size_t)i * n + j] *= 1.0 + r[j];
+        for (int i = 0; i < n; ++i) newest[(size_t)i * n + i] += row_abs_sum(e, n, i) * (1.0 + 1e-12);
+        folded = 1;
+      }
+    }
+    if (!folded)
+      for (int i = 0; i < n; ++i) newest[(size_t)i * n + i] += row_abs_sum(a, n, i);
+    /* pop_front */
+    memmove(blk(s, 1), blk(s, 2), sizeof(double) * (size_t)n * n * (size_t)(s->nq - 1));
+    s->nq -= 1;
+  }
+  free(x); free(e); free(r);
+}
+
+/*
+ * dt_reach (dt_reach.hpp:41-104) for one sample.  Writes boxes into lo/hi
+ * ([H+1][n]); returns n_boxes; *failed_step / *status per tube.hpp:30-34.
+ */
+static int dt_reach_one(const net_t* net, int n, int m, int H, int window, int rebuild,
+                        const double* x0lo, const double* x0hi, const double* actions,
+                        double* lo, double* hi, int* failed_step, int* status) {
+  const int cap = window > 0 ? window : 1;
+  const int nzmax = n * (cap + 2);
+  symstate s;
+  s.n = n; s.window = window; s.nq = 0;
+  s.c = (double*)malloc(sizeof(double) * (size_t)n);
+  s.blocks = (double*)calloc((size_t)(cap + 3) * n * n, sizeof(double));
+  double* A = (double*)malloc(sizeof(double) * (size_t)n * nzmax);
+  double* oc = (double*)malloc(sizeof(double) * (size_t)n);
+  double* oA = (double*)malloc(sizeof(double) * (size_t)n * nzmax);
+  iv* rem = (iv*)malloc(sizeof(iv) * (size_t)n);
+  iv* ig = (iv*)calloc((size_t)n, sizeof(iv));
+  double* bias = NULL;
+  /* frozen network copy (freeze_trailing_inputs, neural.hpp:398-413) */
+  net_t fz = *net;
+  fz.layers = (layer_t*)malloc(sizeof(layer_t) * (size_t)net->n_layers);
+  memcpy(fz.layers, net->layers, sizeof(layer_t) * (size_t)net->n_layers);
+  const layer_t* l0 = &net->layers[0];
+  double* w0 = NULL;
+  if (m > 0) {
+    w0 = (double*)malloc(sizeof(double) * (size_t)l0->rows * n);
+    for (int i = 0; i < l0->rows; ++i)
+      for (int j = 0; j < n; ++j) w0[(size_t)i * n + j] = l0->w[(size_t)i * l0->cols + j];
+    bias = (double*)malloc(sizeof(double) * (size_t)l0->rows);
+    fz.layers[0].w = w0;
+    fz.layers[0].cols = n;
+    fz.layers[0].b = bias;
+  }
+
+  int nb = 0;
+  *failed_step = -1;
+  *status = REACH_TUBE_OK;
+  for (int d = 0; d < n; ++d) { lo[d] = x0lo[d]; hi[d] = x0hi[d]; }
+  nb = 1;
+  sym_init(&s, x0lo, x0hi);
+  for (int k = 0; k < H; ++k) {
+    if (m > 0) {
+      const double* u = actions + (size_t)k * m;
+      for (int i = 0; i < l0->rows; ++i) {
+        double bi = l0->b[i];
+        for (int j = 0; j < m; ++j) bi += l0->w[(size_t)i * l0->cols + n + j] * u[j];
+        bias[i] = bi;
+      }
+    }
+    /* symbolic_seed (flowpipe_ct.hpp:353-370): A = [G0 | Q1 .. Qk] */
+    const int nz = n * (1 + s.nq);
+    for (int i = 0; i < n; ++i)
+      for (int b = 0; b <= s.nq; ++b)
+        for (int j = 0; j < n; ++j) A[(size_t)i * nz + b * n + j] = blk(&s, b)[(size_t)i * n + j];
+    if (certify_tm_input(&fz, n, nz, s.c, A, ig, oc, oA, rem)) {
+      *failed_step = k; *status = REACH_TUBE_NONFINITE_PREACT; break;
+    }
+    int fin = 1;
+    for (int i = 0; i < n; ++i) if (!iv_finite(rem[i])) fin = 0;
+    if (!fin) { *failed_step = k; *status = REACH_TUBE_DIVERGED_CERT; break; }
+    /* re-seed (dt_reach.hpp:69-92) */
+    for (int i = 0; i < n; ++i) s.c[i] = oc[i] + (rem[i].lo + rem[i].hi) * 0.5;
+    for (int b = 0; b <= s.nq; ++b)
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) blk(&s, b)[(size_t)i * n + j] = oA[(size_t)i * nz + b * n + j];
+    s.nq += 1;
+    double* fresh = blk(&s, s.nq);
+    memset(fresh, 0, sizeof(double) * (size_t)n * n);
+    for (int i = 0; i < n; ++i) fresh[(size_t)i * n + i] = (rem[i].hi - rem[i].lo) * 0.5;
+    fold_overflow(&s);
+    /* symbolic_box (flowpipe_ct.hpp:413-424) */
+    int bfin = 1;
+    double* blo = lo + (size_t)nb * n;
+    double* bhi = hi + (size_t)nb * n;
+    for (int i = 0; i < n; ++i) {
+      double r = row_abs_sum(blk(&s, 0), n, i);
+      for (int b = 1; b <= s.nq; ++b) r += row_abs_sum(blk(&s, b), n, i);
+      blo[i] = s.c[i] - r;
+      bhi[i] = s.c[i] + r;
+      if (!isfinite(blo[i]) || !isfinite(bhi[i])) bfin = 0;
+    }
+    nb += 1;
+    if (!bfin) { *failed_step = k; *status = REACH_TUBE_DIVERGED_BOX; break; }
+    if (rebuild) sym_init(&s, blo, bhi);
+  }
+  free(s.c); free(s.blocks); free(A); free(oc); free(oA); free(rem); free(ig);
+  free(fz.layers); free(w0); free(bias);
+  return nb;
+}
+
+int orc_dt_batch(const reach_net_desc* desc, const reach_dt_args* a, const reach_tube_out* out) {
+  if (!desc || !a || !out || a->n <= 0 || a->m < 0 || a->horizon < 0 || a->batch < 0) return REACH_E_INVALID_ARGUMENT;
+  if (desc->dims[0] != a->n + a->m || desc->dims[desc->n_layers] != a->n) return REACH_E_INVALID_ARGUMENT;
+  net_t net = net_from_desc(desc);
+  const int H = a->horizon, n = a->n, m = a->m;
+  for (int b = 0; b < a->batch; ++b) {
+    const double* act = a->actions_shared ? a->actions : a->actions + (size_t)b * H * m;
+    int fs, st;
+    int nb = dt_reach_one(&net, n, m, H, a->window, a->rebuild_from_box, a->x0_lo + (size_t)b * n,
+                          a->x0_hi + (size_t)b * n, act, out->lo + (size_t)b * (H + 1) * n,
+                          out->hi + (size_t)b * (H + 1) * n, &fs, &st);
+    out->n_boxes[b] = nb;
+    out->failed_step[b] = fs;
+    out->status[b] = st;
+  }
+  free(net.layers);
+  return REACH_OK;
+}
+
+/* split_box (refine.hpp:83-115) part p (last dim fastest) into lo/hi. */
+static void split_part(int n, const double* xlo, const double* xhi, const int32_t* counts, int64_t p,
+                       double* lo, double* hi) {
+  for (int d = n - 1; d >= 0; --d) {
+    int k = counts[d];
+    int i = (int)(p % k);
+    p /= k;
+    double e0 = (i == 0) ? xlo[d] : xlo[d] + (xhi[d] - xlo[d]) * ((double)i / k);
+    double e1 = (i + 1 == k) ? xhi[d] : xlo[d] + (xhi[d] - xlo[d]) * ((double)(i + 1) / k);
+    lo[d] = e0;
+    hi[d] = e1;
+  }
+}
+
+/* reach_with_splitting hull reduction (refine.hpp:133-158) over parts [begin,end). */
+int orc_split_hull(const reach_net_desc* desc, const reach_split_args* a, const reach_hull_out* out) {
+  const int n = a->n, H = a->horizon;
+  int64_t total = 1;
+  for (int d = 0; d < n; ++d) { if (a->counts[d] < 1) return REACH_E_INVALID_ARGUMENT; total *= a->counts[d]; }
+  int64_t begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
+  if (begin < 0 || begin >= end || end > total) return REACH_E_INVALID_ARGUMENT;
+  net_t net = net_from_desc(desc);
+  double* lo = (double*)malloc(sizeof(double) * (size_t)(H + 1) * n);
+  double* hi = (double*)malloc(sizeof(double) * (size_t)(H + 1) * n);
+  double plo[64], phi[64];
+  int steps = 0;
+  int64_t key = INT64_MAX;
+  for (int64_t p = begin; p < end; ++p) {
+    split_part(n, a->x0_lo, a->x0_hi, a->counts, p, plo, phi);
+    int fs, st;
+    int nb = dt_reach_one(&net, n, a->m, H, a->window, a->rebuild_from_box, plo, phi, a->actions, lo, hi, &fs, &st);
+    if (p == begin) {
+      steps = nb;
+      for (int k = 0; k < nb; ++k) {
+        for (int d = 0; d < n; ++d) { out->lo[k * n + d] = lo[k * n + d]; out->hi[k * n + d] = hi[k * n + d]; }
+      }
+      for (int k = 0; k <= H; ++k) out->box_diverged[k] = 0;
+    } else {
+      int upto = nb < steps ? nb : steps;
+      for (int k = 0; k < upto; ++k)
+        for (int d = 0; d < n; ++d) {
+          out->lo[k * n + d] = smin(out->lo[k * n + d], lo[k * n + d]);
+          out->hi[k * n + d] = smax(out->hi[k * n + d], hi[k * n + d]);
+        }
+      if (nb < steps) steps = nb;
+    }
+    for (int k = 0; k < nb; ++k) {
+      int fin = 1;
+      for (int d = 0; d < n; ++d) if (!isfinite(lo[k * n + d]) || !isfinite(hi[k * n + d])) fin = 0;
+      if (!fin) out->box_diverged[k] = 1;
+    }
+    if (st != REACH_TUBE_OK) {
+      int64_t kk = ((int64_t)(fs >= 0 ? fs : nb) << 40) | ((int64_t)p << 8) | (int64_t)(st & 0xff);
+      if (kk < key) key = kk;
+    }
+  }
+  out->n_boxes[0] = steps;
+  out->fail_key[0] = key;
+  free(lo); free(hi); free(net.layers);
+  return REACH_OK;
+}

@@ -1,0 +1,213 @@
+// TEST INFRASTRUCTURE ONLY -- never linked into the product library.
+//
+// C-ABI driver around the UNMODIFIED reference headers
+// (/root/reference/proj/include/reach/, compiled by include path, nothing
+// copied).  Built by oracle/Makefile into oracle/_ref/libreach_ref.so, which
+// the tests use as the ground truth and bench.py's `--impl reference` /
+// cpu_baseline legs time on the host cores.  Only tests/, __graft_entry__.smoke()
+// and bench.py's CPU legs may load it.
+//
+// Every call below is a reference entry point; the glue only converts the
+// flat C structs of include/reach_b200.h to/from reference types.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "reach/dt_reach.hpp"
+#include "reach/neural.hpp"
+#include "reach/parallel.hpp"
+#include "reach/refine.hpp"
+
+#include "reach_b200.h"
+
+using namespace reach;
+
+namespace {
+
+MLPNet<double> net_from_desc(const reach_net_desc* d) {
+  MLPNet<double> net;
+  size_t k = 0;
+  for (int l = 0; l < d->n_layers; ++l) {
+    Layer<double> layer;
+    int rows = d->dims[l + 1], cols = d->dims[l];
+    layer.w = Mat<double>(rows, cols);
+    for (int i = 0; i < rows * cols; ++i) layer.w.a[static_cast<size_t>(i)] = d->params[k++];
+    layer.b.resize(static_cast<size_t>(rows));
+    for (int i = 0; i < rows; ++i) layer.b[static_cast<size_t>(i)] = d->params[k++];
+    layer.act = d->acts[l] == REACH_ACT_RELU   ? Act::Relu
+                : d->acts[l] == REACH_ACT_TANH ? Act::Tanh
+                                               : Act::Identity;
+    net.layers.push_back(std::move(layer));
+  }
+  return net;
+}
+
+int32_t status_of(const ReachTube<double>& t) {
+  if (!t.diverged && t.failed_step < 0) return REACH_TUBE_OK;
+  if (t.failure_reason == "relax_activation: non-finite preactivation") return REACH_TUBE_NONFINITE_PREACT;
+  if (t.failure_reason == "diverged certification") return REACH_TUBE_DIVERGED_CERT;
+  if (t.failure_reason == "diverged box") return REACH_TUBE_DIVERGED_BOX;
+  return REACH_TUBE_OTHER;
+}
+
+Box box_at(const double* lo, const double* hi, int n) {
+  Box b(n);
+  for (int d = 0; d < n; ++d) b[d] = {lo[d], hi[d]};
+  return b;
+}
+
+std::vector<Vec<double>> actions_at(const double* a, int horizon, int m) {
+  std::vector<Vec<double>> out(static_cast<size_t>(horizon), Vec<double>(static_cast<size_t>(m)));
+  for (int k = 0; k < horizon; ++k)
+    for (int j = 0; j < m; ++j) out[static_cast<size_t>(k)][static_cast<size_t>(j)] = a[k * m + j];
+  return out;
+}
+
+DTSystem<double> make_sys(const reach_net_desc* desc, int n, int m) {
+  DTSystem<double> sys;
+  sys.step = net_from_desc(desc);
+  sys.n = n;
+  sys.m = m;
+  return sys;
+}
+
+}  // namespace
+
+extern "C" {
+
+// dt_reach (dt_reach.hpp:41) per sample inside the reference parallel_for
+// (parallel.hpp:17) with an explicit thread count (0 = hardware threads),
+// per-element exception isolation as dt_reach_batch (dt_reach.hpp:116-123).
+int ref_dt_batch(const reach_net_desc* desc, const reach_dt_args* a, const reach_tube_out* out,
+                 int32_t threads) {
+  try {
+    DTSystem<double> sys = make_sys(desc, a->n, a->m);
+    DTReachParams prm;
+    prm.window = a->window;
+    prm.rebuild_from_box = a->rebuild_from_box != 0;
+    const int H = a->horizon, n = a->n, m = a->m;
+    parallel_for(
+        a->batch,
+        [&](int b) {
+          ReachTube<double> tube;
+          try {
+            const double* act = a->actions_shared ? a->actions : a->actions + static_cast<size_t>(b) * H * m;
+            tube = dt_reach(sys, box_at(a->x0_lo + static_cast<size_t>(b) * n, a->x0_hi + static_cast<size_t>(b) * n, n),
+                            actions_at(act, H, m), prm);
+          } catch (const std::exception& e) {
+            tube.mark_failed(0, e.what());
+          }
+          out->n_boxes[b] = tube.steps();
+          out->failed_step[b] = tube.failed_step;
+          out->status[b] = status_of(tube);
+          for (int k = 0; k < tube.steps(); ++k)
+            for (int d = 0; d < n; ++d) {
+              size_t o = (static_cast<size_t>(b) * (H + 1) + k) * n + d;
+              out->lo[o] = tube.boxes[static_cast<size_t>(k)][d].lo;
+              out->hi[o] = tube.boxes[static_cast<size_t>(k)][d].hi;
+            }
+        },
+        threads);
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+
+// reach_with_splitting(dt_reach, x0, plan) (refine.hpp:121-160).  With the full
+// part range and threads == 0 this calls the reference driver verbatim; with
+// a sub-range (a bounded CPU sample / one shard) it runs the same reference
+// pieces -- split_box, dt_reach per part in parallel_for, box_hull in
+// ascending index order -- on parts [begin, end).
+int ref_split_hull(const reach_net_desc* desc, const reach_split_args* a, const reach_hull_out* out,
+                   int32_t threads) {
+  try {
+    DTSystem<double> sys = make_sys(desc, a->n, a->m);
+    DTReachParams prm;
+    prm.window = a->window;
+    prm.rebuild_from_box = a->rebuild_from_box != 0;
+    const int H = a->horizon, n = a->n;
+    auto actions = actions_at(a->actions, H, a->m);
+    Box x0 = box_at(a->x0_lo, a->x0_hi, n);
+    SplitPlan plan;
+    plan.counts.assign(a->counts, a->counts + n);
+    const long long total = plan.total_parts();
+    long long begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
+    if (begin < 0 || begin >= end || end > total) return REACH_E_INVALID_ARGUMENT;
+
+    auto engine = [&](const Box& b) { return dt_reach(sys, b, actions, prm); };
+    auto parts = split_box(x0, plan);
+    const int count = static_cast<int>(end - begin);
+    std::vector<ReachTube<double>> subs(static_cast<size_t>(count));
+    parallel_for(
+        count,
+        [&](int i) {
+          try {
+            subs[static_cast<size_t>(i)] = engine(parts[static_cast<size_t>(begin + i)]);
+          } catch (const std::exception& e) {
+            subs[static_cast<size_t>(i)].mark_failed(0, e.what());
+          }
+        },
+        threads);
+    // identical reduction to refine.hpp:133-158
+    int steps = subs.front().steps();
+    int64_t key = std::numeric_limits<int64_t>::max();
+    for (int i = 0; i < count; ++i) {
+      const auto& s = subs[static_cast<size_t>(i)];
+      steps = std::min(steps, s.steps());
+      if (s.diverged) {
+        int fs = s.failed_step >= 0 ? s.failed_step : s.steps();
+        int64_t k = (static_cast<int64_t>(fs) << 40) | (static_cast<int64_t>(begin + i) << 8) |
+                    static_cast<int64_t>(status_of(s) & 0xff);
+        key = std::min(key, k);
+      }
+    }
+    for (int k = 0; k < steps; ++k) {
+      Box b = subs.front().boxes[static_cast<size_t>(k)];
+      for (int i = 1; i < count; ++i) b = box_hull(b, subs[static_cast<size_t>(i)].boxes[static_cast<size_t>(k)]);
+      for (int d = 0; d < n; ++d) {
+        out->lo[static_cast<size_t>(k) * n + d] = b[d].lo;
+        out->hi[static_cast<size_t>(k) * n + d] = b[d].hi;
+      }
+      out->box_diverged[k] = b.diverged ? 1 : 0;
+    }
+    out->n_boxes[0] = steps;
+    out->fail_key[0] = key;
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+
+// The reference driver itself, for the `--impl reference` arm on full plans.
+int ref_reach_with_splitting(const reach_net_desc* desc, const reach_split_args* a, double* lo, double* hi,
+                             int32_t* n_boxes, int32_t* failed_step) {
+  try {
+    DTSystem<double> sys = make_sys(desc, a->n, a->m);
+    DTReachParams prm;
+    prm.window = a->window;
+    prm.rebuild_from_box = a->rebuild_from_box != 0;
+    auto actions = actions_at(a->actions, a->horizon, a->m);
+    SplitPlan plan;
+    plan.counts.assign(a->counts, a->counts + a->n);
+    auto hull = reach_with_splitting([&](const Box& b) { return dt_reach(sys, b, actions, prm); },
+                                     box_at(a->x0_lo, a->x0_hi, a->n), plan);
+    for (int k = 0; k < hull.steps(); ++k)
+      for (int d = 0; d < a->n; ++d) {
+        lo[static_cast<size_t>(k) * a->n + d] = hull.boxes[static_cast<size_t>(k)][d].lo;
+        hi[static_cast<size_t>(k) * a->n + d] = hull.boxes[static_cast<size_t>(k)][d].hi;
+      }
+    *n_boxes = hull.steps();
+    *failed_step = hull.failed_step;
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+
+int ref_hardware_threads(void) { return hardware_threads(); }
+
+}  // extern "C"

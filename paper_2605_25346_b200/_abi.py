@@ -1,0 +1,105 @@
+"""ctypes mirror of include/reach_b200.h (the C ABI).
+
+Struct layouts here must match the header field for field; tests/test_abi.py
+checks the exported symbols against the header declarations.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+REACH_OK = 0
+REACH_E_INVALID_ARGUMENT = 1
+REACH_E_CUDA = 2
+REACH_E_UNSUPPORTED = 3
+REACH_E_NO_DEVICE = 4
+REACH_E_OOM = 5
+
+REACH_FLAG_DEVICE_PTRS = 1
+
+ACT_RELU, ACT_TANH, ACT_IDENTITY = 0, 1, 2
+
+# reach_tube_status -> reference failure_reason strings (tube.hpp:30-34)
+TUBE_OK = 0
+TUBE_NONFINITE_PREACT = 1
+TUBE_DIVERGED_CERT = 2
+TUBE_DIVERGED_BOX = 3
+TUBE_OTHER = 99
+TUBE_REASON = {
+    TUBE_OK: "",
+    TUBE_NONFINITE_PREACT: "relax_activation: non-finite preactivation",
+    TUBE_DIVERGED_CERT: "diverged certification",
+    TUBE_DIVERGED_BOX: "diverged box",
+    TUBE_OTHER: "error",
+}
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_lp = C.POINTER(C.c_int64)
+
+
+class NetDesc(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("dims", _ip), ("acts", _ip), ("params", _dp)]
+
+
+class DTArgs(C.Structure):
+    _fields_ = [
+        ("batch", C.c_int32), ("horizon", C.c_int32), ("n", C.c_int32), ("m", C.c_int32),
+        ("window", C.c_int32), ("rebuild_from_box", C.c_int32),
+        ("x0_lo", _dp), ("x0_hi", _dp), ("actions", _dp), ("actions_shared", C.c_int32),
+    ]
+
+
+class TubeOut(C.Structure):
+    _fields_ = [("lo", _dp), ("hi", _dp), ("n_boxes", _ip), ("failed_step", _ip), ("status", _ip)]
+
+
+class SplitArgs(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("m", C.c_int32), ("horizon", C.c_int32), ("window", C.c_int32),
+        ("rebuild_from_box", C.c_int32),
+        ("x0_lo", _dp), ("x0_hi", _dp), ("counts", _ip), ("actions", _dp),
+        ("part_begin", C.c_int64), ("part_end", C.c_int64),
+    ]
+
+
+class HullOut(C.Structure):
+    _fields_ = [("lo", _dp), ("hi", _dp), ("box_diverged", _ip), ("n_boxes", _ip), ("fail_key", _lp)]
+
+
+def dptr(a) -> "C._Pointer":
+    """Pointer to a C-contiguous float64 numpy array, or a raw device address (int)."""
+    if a is None:
+        return C.cast(None, _dp)
+    if isinstance(a, int):
+        return C.cast(C.c_void_p(a), _dp)
+    assert a.dtype == np.float64 and a.flags.c_contiguous, (a.dtype, a.flags)
+    return a.ctypes.data_as(_dp)
+
+
+def iptr(a):
+    if a is None:
+        return C.cast(None, _ip)
+    if isinstance(a, int):
+        return C.cast(C.c_void_p(a), _ip)
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_ip)
+
+
+def lptr(a):
+    if isinstance(a, int):
+        return C.cast(C.c_void_p(a), _lp)
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_lp)
+
+
+FAIL_KEY_NONE = np.iinfo(np.int64).max
+
+
+def decode_fail_key(key: int):
+    """(div_step, part, status) of a hull fail key, or None."""
+    key = int(key)
+    if key == FAIL_KEY_NONE:
+        return None
+    return key >> 40, (key >> 8) & ((1 << 32) - 1), key & 0xFF

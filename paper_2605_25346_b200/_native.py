@@ -1,0 +1,153 @@
+"""Loader for the in-tree CUDA library (libreach_b200.so).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every compute call raises.  Build with `python -c "import
+__graft_entry__ as g; g.build()"` or `make -C paper_2605_25346_b200/csrc`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import _abi as A
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libreach_b200.so")
+
+_lib = None
+_lock = threading.Lock()
+
+
+class ReachError(RuntimeError):
+    pass
+
+
+class NativeMissing(ReachError):
+    pass
+
+
+def _declare(lib):
+    vp = C.c_void_p
+    lib.reach_abi_version.restype = C.c_int
+    lib.reach_tube_status_string.restype = C.c_char_p
+    lib.reach_tube_status_string.argtypes = [C.c_int32]
+    lib.reach_ctx_create.argtypes = [C.c_int32, C.POINTER(vp)]
+    lib.reach_ctx_destroy.argtypes = [vp]
+    lib.reach_ctx_set_stream.argtypes = [vp, vp]
+    lib.reach_ctx_synchronize.argtypes = [vp]
+    lib.reach_ctx_last_error.argtypes = [vp]
+    lib.reach_ctx_last_error.restype = C.c_char_p
+    lib.reach_ctx_launch_count.argtypes = [vp]
+    lib.reach_ctx_launch_count.restype = C.c_int64
+    lib.reach_net_upload.argtypes = [vp, C.POINTER(A.NetDesc), C.POINTER(vp)]
+    lib.reach_net_free.argtypes = [vp, vp]
+    lib.reach_dt_batch.argtypes = [vp, vp, C.POINTER(A.DTArgs), C.POINTER(A.TubeOut), C.c_int32]
+    lib.reach_split_hull.argtypes = [vp, vp, C.POINTER(A.SplitArgs), C.POINTER(A.HullOut), C.c_int32]
+    lib.reach_ctx_enable_kernel_timing.argtypes = [vp, C.c_int32]
+    lib.reach_ctx_kernel_time.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    lib.reach_measure_fp64_peak.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    for f in ("reach_ctx_create", "reach_ctx_destroy", "reach_ctx_set_stream", "reach_ctx_synchronize",
+              "reach_net_upload", "reach_net_free", "reach_dt_batch", "reach_split_hull",
+              "reach_ctx_enable_kernel_timing", "reach_ctx_kernel_time", "reach_measure_fp64_peak"):
+        getattr(lib, f).restype = C.c_int
+    return lib
+
+
+def lib():
+    """The loaded library; raises NativeMissing (loudly) if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeMissing(f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+            _lib = _declare(C.CDLL(LIB_PATH))
+            if _lib.reach_abi_version() != 1:
+                raise NativeMissing("ABI version mismatch")
+        return _lib
+
+
+class Context:
+    """reach_ctx: one CUDA device + stream + workspaces (one per host thread)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = lib()
+        h = C.c_void_p()
+        rc = self._lib.reach_ctx_create(int(device), C.byref(h))
+        if rc != A.REACH_OK:
+            raise ReachError(f"reach_ctx_create failed (code {rc}): no usable CUDA device {device}")
+        self.handle = h
+        self.device = device
+        self._nets = {}
+
+    def check(self, rc: int, what: str):
+        if rc == A.REACH_OK:
+            return
+        msg = self._lib.reach_ctx_last_error(self.handle).decode()
+        if rc == A.REACH_E_INVALID_ARGUMENT:
+            raise ValueError(f"{what}: {msg}")
+        raise ReachError(f"{what} failed (code {rc}): {msg}")
+
+    def set_stream(self, stream_handle: int | None):
+        self.check(self._lib.reach_ctx_set_stream(self.handle, C.c_void_p(stream_handle or 0)), "set_stream")
+
+    def synchronize(self):
+        self.check(self._lib.reach_ctx_synchronize(self.handle), "synchronize")
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.reach_ctx_launch_count(self.handle))
+
+    def enable_kernel_timing(self, on: bool = True):
+        self.check(self._lib.reach_ctx_enable_kernel_timing(self.handle, int(on)), "enable_kernel_timing")
+
+    def kernel_time(self):
+        """(total device ms, launches) of the main kernels since the last query."""
+        ms, n = C.c_double(), C.c_int64()
+        self.check(self._lib.reach_ctx_kernel_time(self.handle, C.byref(ms), C.byref(n)), "kernel_time")
+        return ms.value, n.value
+
+    def fp64_peak(self):
+        """(DFMA TFLOP/s, DMUL+DADD TFLOP/s) measured on this device."""
+        a, b = C.c_double(), C.c_double()
+        self.check(self._lib.reach_measure_fp64_peak(self.handle, C.byref(a), C.byref(b)), "fp64_peak")
+        return a.value, b.value
+
+    def upload(self, net) -> "C.c_void_p":
+        """Device handle of `net` (cached by content: nets are values, SPEC.md)."""
+        import hashlib
+        desc, keep = net.desc()
+        key = hashlib.blake2b(b"".join(a.tobytes() for a in keep), digest_size=16).digest()
+        hit = self._nets.get(key)
+        if hit is not None:
+            return hit[1]
+        h = C.c_void_p()
+        self.check(self._lib.reach_net_upload(self.handle, C.byref(desc), C.byref(h)), "reach_net_upload")
+        del keep
+        self._nets[key] = (net, h)
+        return h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            for _, (_, h) in list(self._nets.items()):
+                self._lib.reach_net_free(self.handle, h)
+            self._nets.clear()
+            self._lib.reach_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default = {}
+
+
+def default_context(device: int = 0) -> Context:
+    tid = (threading.get_ident(), device)
+    ctx = _default.get(tid)
+    if ctx is None:
+        ctx = Context(device)
+        _default[tid] = ctx
+    return ctx

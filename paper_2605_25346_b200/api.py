@@ -1,0 +1,363 @@
+"""Reference-facing host API (mirrors /root/reference/proj/include/reach/).
+
+Same names, argument meaning and error behaviour as the reference's C++
+templates for the DT reachability path:
+
+    MLPNet / Layer / Act            neural.hpp:18-88
+    affine_net                      neural.hpp:90-95
+    DTSystem, DTReachParams         dt_reach.hpp:17-36
+    dt_reach, dt_reach_batch        dt_reach.hpp:40-125
+    SplitPlan, split_box            refine.hpp:25-115
+    reach_with_splitting            refine.hpp:121-160  (engine = dt_reach)
+    ReachTube, tube_volume          tube.hpp:12-46
+    box_from_center, box_volume_proxy  interval.hpp:224-258
+
+Every compute call runs the CUDA kernels through the C ABI
+(include/reach_b200.h); there is no CPU path.  Shape errors raise
+ValueError where the reference throws std::invalid_argument.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi as A
+from ._native import Context, default_context
+
+
+class Act(enum.IntEnum):
+    Relu = A.ACT_RELU
+    Tanh = A.ACT_TANH
+    Identity = A.ACT_IDENTITY
+
+
+@dataclass
+class Layer:
+    w: np.ndarray  # out x in
+    b: np.ndarray
+    act: Act = Act.Identity
+
+
+@dataclass(eq=False)
+class MLPNet:
+    layers: List[Layer] = field(default_factory=list)
+
+    def input_dim(self) -> int:
+        return int(self.layers[0].w.shape[1])
+
+    def output_dim(self) -> int:
+        return int(self.layers[-1].w.shape[0])
+
+    def validate(self):
+        """MLPNet::validate (neural.hpp:49-56)."""
+        if not self.layers:
+            raise ValueError("MLPNet: empty")
+        for l in range(len(self.layers) - 1):
+            if self.layers[l + 1].w.shape[1] != self.layers[l].w.shape[0]:
+                raise ValueError("MLPNet: layer shapes do not chain")
+        if self.layers[-1].act != Act.Identity:
+            raise ValueError("MLPNet: final activation must be identity")
+
+    def forward(self, x: np.ndarray) -> np.ndarray:
+        """MLPNet::forward (neural.hpp:58-76) -- host-side rollout for checks; x is [in] or [in][S]."""
+        h = np.asarray(x, dtype=np.float64)
+        for L in self.layers:
+            h = L.w @ h + (L.b[:, None] if h.ndim == 2 else L.b)
+            if L.act == Act.Relu:
+                h = np.where(h < 0.0, 0.0, h)
+            elif L.act == Act.Tanh:
+                h = np.tanh(h)
+        return h
+
+    def params(self) -> np.ndarray:
+        """net_params order (neural.hpp:133-140): per layer W row-major then b."""
+        return np.concatenate([np.concatenate([L.w.ravel(), L.b.ravel()]) for L in self.layers]).astype(np.float64)
+
+    def dims(self) -> np.ndarray:
+        return np.array([self.layers[0].w.shape[1]] + [L.w.shape[0] for L in self.layers], dtype=np.int32)
+
+    def acts(self) -> np.ndarray:
+        return np.array([int(L.act) for L in self.layers], dtype=np.int32)
+
+    def desc(self):
+        """(reach_net_desc, keepalive) for the C ABI."""
+        self.validate()
+        dims, acts, params = self.dims(), self.acts(), np.ascontiguousarray(self.params())
+        d = A.NetDesc(len(self.layers), A.iptr(dims), A.iptr(acts), A.dptr(params))
+        return d, (dims, acts, params)
+
+
+def affine_net(m: np.ndarray, d: np.ndarray) -> MLPNet:
+    return MLPNet([Layer(np.asarray(m, np.float64), np.asarray(d, np.float64), Act.Identity)])
+
+
+@dataclass
+class DTSystem:
+    step: MLPNet
+    n: int
+    m: int = 0
+
+    def validate(self):
+        """DTSystem::validate (dt_reach.hpp:23-28)."""
+        self.step.validate()
+        if self.n <= 0 or self.m < 0:
+            raise ValueError("DTSystem: invalid dimensions")
+        if self.step.input_dim() != self.n + self.m or self.step.output_dim() != self.n:
+            raise ValueError("DTSystem: one-step map shape mismatch")
+
+
+@dataclass
+class DTReachParams:
+    window: int = 4
+    rebuild_from_box: bool = False
+
+
+@dataclass
+class ReachTube:
+    """ReachTube<double> (tube.hpp:12-35); box k = (lo[k], hi[k])."""
+    lo: np.ndarray
+    hi: np.ndarray
+    t_lo: np.ndarray
+    t_hi: np.ndarray
+    diverged: bool = False
+    failed_step: int = -1
+    failure_reason: str = ""
+
+    def steps(self) -> int:
+        return int(self.lo.shape[0])
+
+    def box_diverged(self, k: int) -> bool:
+        """IntervalBox::diverged after check_divergence (interval.hpp:215-218)."""
+        return not (np.all(np.isfinite(self.lo[k])) and np.all(np.isfinite(self.hi[k])))
+
+
+def box_volume_proxy(lo: np.ndarray, hi: np.ndarray) -> float:
+    """interval.hpp:252-258: width sum, +inf for a non-finite box."""
+    if not (np.all(np.isfinite(lo)) and np.all(np.isfinite(hi))):
+        return math.inf
+    acc = 0.0
+    for a, b in zip(lo, hi):
+        acc += b - a
+    return acc
+
+
+def tube_volume(t: ReachTube) -> float:
+    """tube.hpp:40-46."""
+    if t.diverged:
+        return math.inf
+    acc = 0.0
+    for k in range(t.steps()):
+        acc += box_volume_proxy(t.lo[k], t.hi[k])
+    return acc
+
+
+def box_from_center(center, radius):
+    """interval.hpp:224-240 -> (lo, hi)."""
+    c = np.asarray(center, dtype=np.float64)
+    r = np.broadcast_to(np.asarray(radius, dtype=np.float64), c.shape)
+    if np.any(r < 0.0):
+        raise ValueError("box_from_center: negative radius")
+    return c - r, c + r
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class TubeBatch:
+    """Batch output of dt_reach_batch in array form (the device layout)."""
+    lo: np.ndarray  # [B][H+1][n]
+    hi: np.ndarray
+    n_boxes: np.ndarray
+    failed_step: np.ndarray
+    status: np.ndarray
+
+    def tube(self, b: int) -> ReachTube:
+        k = int(self.n_boxes[b])
+        st = int(self.status[b])
+        t = np.arange(k, dtype=np.float64)
+        return ReachTube(self.lo[b, :k].copy(), self.hi[b, :k].copy(), t, t.copy(), diverged=st != A.TUBE_OK,
+                         failed_step=int(self.failed_step[b]), failure_reason=A.TUBE_REASON.get(st, "error"))
+
+    def tubes(self) -> List[ReachTube]:
+        return [self.tube(b) for b in range(self.lo.shape[0])]
+
+
+def _actions_array(seqs, B, H, m) -> np.ndarray:
+    a = np.zeros((B, H, m), dtype=np.float64)
+    for b, seq in enumerate(seqs):
+        if len(seq) != H:
+            raise ValueError("dt_reach_batch: ragged action sequences")
+        for k, u in enumerate(seq):
+            u = np.asarray(u, dtype=np.float64).ravel()
+            if u.size != m:
+                raise ValueError("dt_reach: action dimension mismatch")
+            a[b, k] = u
+    return a
+
+
+def dt_reach_batch_arrays(sys: DTSystem, x0_lo: np.ndarray, x0_hi: np.ndarray, actions: np.ndarray,
+                          prm: DTReachParams = DTReachParams(), ctx: Optional[Context] = None,
+                          actions_shared: bool = False) -> TubeBatch:
+    """dt_reach_batch (dt_reach.hpp:108-125) on arrays: x0 [B][n], actions [B][H][m] (or [H][m] shared)."""
+    sys.validate()
+    ctx = ctx or default_context()
+    x0_lo = np.ascontiguousarray(x0_lo, dtype=np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, dtype=np.float64)
+    B = x0_lo.shape[0]
+    if x0_lo.shape != (B, sys.n) or x0_hi.shape != (B, sys.n):
+        raise ValueError("dt_reach: X0 dimension mismatch")
+    actions = np.ascontiguousarray(actions, dtype=np.float64)
+    H = actions.shape[0] if actions_shared else actions.shape[1]
+    if actions.shape[-1] != sys.m and not (sys.m == 0 and actions.size == 0):
+        raise ValueError("dt_reach: action dimension mismatch")
+    out = TubeBatch(np.full((B, H + 1, sys.n), np.nan), np.full((B, H + 1, sys.n), np.nan),
+                    np.zeros(B, np.int32), np.zeros(B, np.int32), np.zeros(B, np.int32))
+    args = A.DTArgs(B, H, sys.n, sys.m, prm.window, int(prm.rebuild_from_box), A.dptr(x0_lo), A.dptr(x0_hi),
+                    A.dptr(actions if actions.size else np.zeros(1)), int(actions_shared))
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step),
+                   A.iptr(out.status))
+    net = ctx.upload(sys.step)
+    ctx.check(ctx._lib.reach_dt_batch(ctx.handle, net, C.byref(args), C.byref(to), 0), "dt_reach_batch")
+    return out
+
+
+def dt_reach_batch(sys: DTSystem, x0s: Sequence, action_seqs: Sequence, prm: DTReachParams = DTReachParams(),
+                   ctx: Optional[Context] = None) -> List[ReachTube]:
+    """dt_reach_batch (dt_reach.hpp:108-125): x0s = [(lo, hi), ...], action_seqs = [[u_0..u_{H-1}], ...]."""
+    if len(x0s) != len(action_seqs):
+        raise ValueError("dt_reach_batch: batch size mismatch")
+    if not x0s:
+        return []
+    B = len(x0s)
+    lo = np.array([np.asarray(b[0], np.float64) for b in x0s])
+    hi = np.array([np.asarray(b[1], np.float64) for b in x0s])
+    H = len(action_seqs[0])
+    acts = _actions_array(action_seqs, B, H, sys.m)
+    return dt_reach_batch_arrays(sys, lo, hi, acts, prm, ctx).tubes()
+
+
+def dt_reach(sys: DTSystem, x0, actions: Sequence, prm: DTReachParams = DTReachParams(),
+             ctx: Optional[Context] = None) -> ReachTube:
+    """dt_reach (dt_reach.hpp:40-104): x0 = (lo, hi)."""
+    return dt_reach_batch(sys, [x0], [actions], prm, ctx)[0]
+
+
+# ---------------------------------------------------------------------------
+class SplitPlan:
+    """SplitPlan (refine.hpp:25-78)."""
+    kMaxParts = 1 << 20
+
+    def __init__(self, counts):
+        self.counts = [int(c) for c in counts]
+
+    @staticmethod
+    def all_one(n_dims: int) -> "SplitPlan":
+        return SplitPlan([1] * n_dims)
+
+    @staticmethod
+    def parse(s: str) -> "SplitPlan":
+        toks = s.split("x")
+        if any(t == "" for t in toks):
+            raise ValueError(f'SplitPlan: empty count in "{s}"')
+        return SplitPlan([int(t) for t in toks])
+
+    @staticmethod
+    def rpy(n_dims: int, parts: int) -> "SplitPlan":
+        if n_dims < 9:
+            raise ValueError("SplitPlan::rpy: needs at least 9 dimensions")
+        k = int(round(parts ** (1.0 / 3.0)))
+        if k < 1 or k * k * k != parts:
+            raise ValueError("SplitPlan::rpy: parts must be a perfect cube")
+        p = SplitPlan.all_one(n_dims)
+        p.counts[6] = p.counts[7] = p.counts[8] = k
+        return p
+
+    def total_parts(self) -> int:
+        t = 1
+        for c in self.counts:
+            if c < 1:
+                raise ValueError("SplitPlan: counts must be >= 1")
+            t *= c
+            if t > self.kMaxParts:
+                raise ValueError("SplitPlan: total part count overflow")
+        return t
+
+    def validate(self, n_dims: int):
+        if len(self.counts) != n_dims:
+            raise ValueError("SplitPlan: dimension mismatch")
+        self.total_parts()
+
+
+def split_box(x0_lo, x0_hi, plan: SplitPlan):
+    """split_box (refine.hpp:83-115): [P][n] lo/hi, last dimension fastest."""
+    x0_lo = np.asarray(x0_lo, np.float64)
+    x0_hi = np.asarray(x0_hi, np.float64)
+    n = x0_lo.size
+    plan.validate(n)
+    edges = []
+    for d in range(n):
+        k = plan.counts[d]
+        e = [x0_lo[d] + (x0_hi[d] - x0_lo[d]) * (float(i) / k) for i in range(k + 1)]
+        e[0], e[k] = x0_lo[d], x0_hi[d]
+        edges.append(np.array(e))
+    grids = np.meshgrid(*[np.arange(c) for c in plan.counts], indexing="ij")
+    idx = np.stack([g.ravel() for g in grids], axis=1)
+    lo = np.stack([edges[d][idx[:, d]] for d in range(n)], axis=1)
+    hi = np.stack([edges[d][idx[:, d] + 1] for d in range(n)], axis=1)
+    return lo, hi
+
+
+@dataclass
+class HullResult:
+    """Partial or full hull of reach_with_splitting over a part range."""
+    lo: np.ndarray  # [H+1][n]
+    hi: np.ndarray
+    box_diverged: np.ndarray
+    n_boxes: int
+    fail_key: int
+
+    def tube(self) -> ReachTube:
+        k = self.n_boxes
+        t = np.arange(k, dtype=np.float64)
+        tube = ReachTube(self.lo[:k].copy(), self.hi[:k].copy(), t, t.copy())
+        f = A.decode_fail_key(self.fail_key)
+        tube.diverged = bool(np.any(self.box_diverged[:k])) or f is not None
+        if f is not None:
+            step, part, st = f
+            tube.failed_step = int(step)
+            tube.failure_reason = f"sub-box {part}: {A.TUBE_REASON.get(st, 'error')}"
+        return tube
+
+
+def reach_split_hull(sys: DTSystem, x0, plan: SplitPlan, actions, prm: DTReachParams = DTReachParams(),
+                     part_begin: int = 0, part_end: int = 0, ctx: Optional[Context] = None) -> HullResult:
+    """Hull over sub-boxes [part_begin, part_end) of reach_with_splitting (C ABI reach_split_hull)."""
+    sys.validate()
+    ctx = ctx or default_context()
+    lo0 = np.ascontiguousarray(x0[0], dtype=np.float64)
+    hi0 = np.ascontiguousarray(x0[1], dtype=np.float64)
+    plan.validate(sys.n)
+    acts = np.ascontiguousarray(np.asarray(actions, dtype=np.float64).reshape(-1, sys.m) if sys.m else np.zeros((0, 0)))
+    H = acts.shape[0] if sys.m else len(actions)
+    counts = np.array(plan.counts, dtype=np.int32)
+    out = HullResult(np.full((H + 1, sys.n), np.nan), np.full((H + 1, sys.n), np.nan), np.zeros(H + 1, np.int32), 0, 0)
+    nb = np.zeros(1, np.int32)
+    key = np.zeros(1, np.int64)
+    args = A.SplitArgs(sys.n, sys.m, H, prm.window, int(prm.rebuild_from_box), A.dptr(lo0), A.dptr(hi0),
+                       A.iptr(counts), A.dptr(acts if acts.size else np.zeros(1)), int(part_begin), int(part_end))
+    ho = A.HullOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.box_diverged), A.iptr(nb), A.lptr(key))
+    net = ctx.upload(sys.step)
+    ctx.check(ctx._lib.reach_split_hull(ctx.handle, net, C.byref(args), C.byref(ho), 0), "reach_with_splitting")
+    out.n_boxes = int(nb[0])
+    out.fail_key = int(key[0])
+    return out
+
+
+def reach_with_splitting(sys: DTSystem, x0, plan: SplitPlan, actions, prm: DTReachParams = DTReachParams(),
+                         ctx: Optional[Context] = None) -> ReachTube:
+    """reach_with_splitting(dt_reach engine, x0, plan) (refine.hpp:121-160)."""
+    return reach_split_hull(sys, x0, plan, actions, prm, ctx=ctx).tube()

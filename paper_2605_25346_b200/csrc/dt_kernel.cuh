@@ -1,0 +1,718 @@
+// Fused discrete-time reachability horizon kernel for B200 (sm_100a).
+//
+// One warp owns one sample (an initial-set sub-box or an MPC candidate) for
+// the WHOLE horizon; its symbolic state (c, G0, the windowed generator queue)
+// stays in shared memory across steps, so nothing but the final boxes ever
+// reaches HBM.  A dedicated producer warp streams the network's weight
+// matrices -- the only operand shared across samples -- through a ring of
+// shared-memory stages with the bulk-copy (TMA) engine and mbarriers; every
+// sample warp of the CTA consumes the same stream, so each weight byte is
+// read from L2 once per CTA per step and reused by all of its samples.
+//
+// Per step each warp runs the reference's dt_reach step (dt_reach.hpp:52-102):
+//   certify_tm_input (neural.hpp:342-394) on the symbolic seed:
+//     IBP preactivation bounds through the frozen net (neural.hpp:243-257),
+//     CROWN backward with shared slopes (neural.hpp:290-335): relaxation +
+//     intercept/shift chains, then the dense Lambda.W contraction,
+//     the prepended [A|I] layer and the remainder tail;
+//   re-seed (dt_reach.hpp:69-92), fold_overflow (flowpipe_ct.hpp:317-350)
+//   with a warp-parallel partial-pivot solve (linalg.hpp:96-132), and
+//   symbolic_box (flowpipe_ct.hpp:413-424).
+// Every floating-point reduction runs in the reference's order with separate
+// multiply and add roundings, so the result is bit-identical to the
+// reference's scalar C++ (ReLU networks; tanh uses CUDA's libm).
+#pragma once
+
+#include "dt_common.cuh"
+
+namespace rb {
+
+constexpr int kMaxLayers = 8;
+constexpr int kMaxSplitDims = 16;
+
+struct DevNet {
+  int L;
+  int dims[kMaxLayers + 1];
+  int acts[kMaxLayers];
+  long long w_off[kMaxLayers];   // W_l  : dims[l+1] rows x ldw[l]   (row-major, cols = dims[l])
+  long long wt_off[kMaxLayers];  // W_l^T: dims[l] rows x ldt[l]     (cols = dims[l+1])
+  long long b_off[kMaxLayers];
+  int ldw[kMaxLayers];
+  int ldt[kMaxLayers];
+  const double* blob;
+};
+
+struct DTParams {
+  DevNet net;
+  int B, H, n, m, window, rebuild;
+  // per-sample inputs (tube mode) -- or split mode (sub-box from the grid)
+  const double* x0_lo;
+  const double* x0_hi;
+  int split;
+  long long part_begin;
+  int counts[kMaxSplitDims];
+  double sx_lo[kMaxSplitDims];
+  double sx_hi[kMaxSplitDims];
+  const double* actions;
+  int actions_shared;
+  // tube outputs
+  double* out_lo;
+  double* out_hi;
+  int* n_boxes;
+  int* failed_step;
+  int* status;
+  // hull outputs (split mode)
+  unsigned long long* hull_lo;  // order keys [H+1][n]
+  unsigned long long* hull_hi;
+  int* hull_div;                // [H+1]
+  int* hull_nan0;               // [H+1][n][2], part-0 NaN rule
+  int* hull_nboxes;             // [1]
+  unsigned long long* hull_fail_key;  // [1]
+  // shared-memory layout (doubles)
+  int stage_doubles, nstage, warp_doubles;
+  int o_stA, o_c, o_pre, o_h, o_LT, o_R, o_bf0;
+  int nzs;       // stA row stride (n * (cap + 2))
+  int pre_off[kMaxLayers];
+};
+
+enum : int { ST_OK = 0, ST_PREACT = 1, ST_CERT = 2, ST_BOX = 3 };
+
+// Consumer side of the weight stream.
+struct WStream {
+  const double* stages;
+  uint64_t* full;
+  uint64_t* empty;
+  int nstage, stage_doubles;
+  uint32_t g;
+  __device__ __forceinline__ const double* acquire() {
+    const int s = g % nstage;
+    mbar_wait(&full[s], (g / nstage) & 1u);
+    return stages + static_cast<size_t>(s) * stage_doubles;
+  }
+  __device__ __forceinline__ void release(int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[g % nstage]);
+    ++g;
+  }
+};
+
+__device__ __forceinline__ int rows_per_chunk(int ld, int stage_doubles) {
+  int r = stage_doubles / ld;
+  return r < 1 ? 1 : r;
+}
+
+// Producer: issues one matrix (rows x ld doubles) as a sequence of chunks.
+__device__ __forceinline__ void produce_matrix(const double* src, int rows, int ld, double* stages, uint64_t* full,
+                                               uint64_t* empty, int nstage, int stage_doubles, uint32_t& g) {
+  const int rpc = rows_per_chunk(ld, stage_doubles);
+  for (int r0 = 0; r0 < rows; r0 += rpc) {
+    const int nr = min(rpc, rows - r0);
+    const int s = g % nstage;
+    mbar_wait(&empty[s], ((g / nstage) & 1u) ^ 1u);
+    const uint32_t bytes = static_cast<uint32_t>(nr) * ld * 8u;
+    mbar_arrive_expect_tx(&full[s], bytes);
+    bulk_g2s(stages + static_cast<size_t>(s) * stage_doubles, src + static_cast<size_t>(r0) * ld, bytes, &full[s]);
+    ++g;
+  }
+}
+
+// relax_activation (neural.hpp:166-227) for ReLU / tanh; identity never relaxed.
+__device__ __forceinline__ void relax(int act, double l, double u, double& s, double& li, double& ui) {
+  s = 0.0;
+  li = 0.0;
+  ui = 0.0;
+  if (act == 0) {  // relu
+    if (l >= 0.0) {
+      s = 1.0;
+    } else if (u <= 0.0) {
+      s = 0.0;
+    } else {
+      const double sl = __ddiv_rn(u, sub(u, l));
+      s = sl;
+      ui = mul(-sl, l);
+      li = smin(0.0, smin(mul(-sl, l), sub(u, mul(sl, u))));
+    }
+  } else {  // tanh
+    const double tl = tanh(l), tu = tanh(u);
+    const double sl = smin(sub(1.0, mul(tl, tl)), sub(1.0, mul(tu, tu)));
+    s = sl;
+    double lo = sub(tl, mul(sl, l));
+    double hi = lo;
+    double g = sub(tu, mul(sl, u));
+    lo = smin(lo, g);
+    hi = smax(hi, g);
+    if (sl < 1.0 && sl > 0.0) {
+      const double xs = atanh(__dsqrt_rn(sub(1.0, sl)));
+      if (l <= xs && xs <= u) {
+        g = sub(tanh(xs), mul(sl, xs));
+        lo = smin(lo, g);
+        hi = smax(hi, g);
+      }
+      if (l <= -xs && -xs <= u) {
+        g = sub(tanh(-xs), mul(sl, -xs));
+        lo = smin(lo, g);
+        hi = smax(hi, g);
+      }
+    }
+    const double margin = add(mul(sub(hi, lo), 1e-12), 1e-15);
+    li = sub(lo, margin);
+    ui = add(hi, margin);
+  }
+}
+
+__device__ __forceinline__ double act_apply(int act, double x) {
+  if (act == 0) return smax(x, 0.0);
+  if (act == 1) return tanh(x);
+  return x;
+}
+
+// split_box (refine.hpp:83-115): part p of the grid, last dimension fastest.
+__device__ __forceinline__ void split_edges(const DTParams& P, long long p, int d, double& lo, double& hi) {
+  long long q = p;
+  for (int e = P.n - 1; e > d; --e) q /= P.counts[e];
+  const int k = P.counts[d];
+  const int i = static_cast<int>(q % k);
+  const double xl = P.sx_lo[d], xh = P.sx_hi[d];
+  const double w = sub(xh, xl);
+  lo = (i == 0) ? xl : add(xl, mul(w, __ddiv_rn(static_cast<double>(i), static_cast<double>(k))));
+  hi = (i + 1 == k) ? xh : add(xl, mul(w, __ddiv_rn(static_cast<double>(i + 1), static_cast<double>(k))));
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.  NO: max state dim (= network output dim) of this family;
+// CPL: hidden units per lane (max hidden width <= 32 * CPL).
+template <int NO, int CPL>
+__global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
+  constexpr int NOP = (NO + 1) & ~1;  // Lambda^T row stride (16-byte rows)
+  constexpr int NZG = 2;              // 32-column groups of the generator matrix (nzs <= 64)
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int nwarps = blockDim.x / 32;
+  const int spc = nwarps - 1;  // sample warps per CTA; warp spc is the producer
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + P.nstage;
+  double* stages = reinterpret_cast<double*>(smem_raw + 128);
+  double* wbase = stages + static_cast<size_t>(P.nstage) * P.stage_doubles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], spc);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const DevNet& N = P.net;
+  const int L = N.L;
+  const int n = P.n, m = P.m, H = P.H;
+  const int cap = P.window > 0 ? P.window : 1;
+  const double* blob = N.blob;
+
+  // ------------------------------------------------------------ producer
+  if (warp == spc) {
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int k = 0; k < H; ++k) {
+        for (int l = 0; l + 1 < L; ++l)
+          produce_matrix(blob + N.wt_off[l], N.dims[l], N.ldt[l], stages, full, empty, P.nstage, P.stage_doubles, g);
+        for (int l = L - 1; l >= 0; --l)
+          produce_matrix(blob + N.w_off[l], N.dims[l + 1], N.ldw[l], stages, full, empty, P.nstage,
+                         P.stage_doubles, g);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ sample warp
+  const long long b = static_cast<long long>(blockIdx.x) * spc + warp;
+  const bool valid = b < P.B;
+  double* ws = wbase + static_cast<size_t>(warp) * P.warp_doubles;
+  double* stA = ws + P.o_stA;  // n x nzs: [G0 | Q1 .. Qnq | (fresh)]
+  double* cc = ws + P.o_c;     // n
+  double* pre = ws + P.o_pre;  // per hidden layer, (lo,hi) per unit
+  double* hb = ws + P.o_h;     // IBP layer input (lo,hi) per unit
+  double* LT = ws + P.o_LT;    // Lambda^T: [col][NOP]
+  double* R = ws + P.o_R;      // relaxation (s, li, ui) per unit
+  double* bf0 = ws + P.o_bf0;  // frozen first-layer bias (per sample: actions differ)
+  const int nzs = P.nzs;
+  WStream ws_in{stages, full, empty, P.nstage, P.stage_doubles, 0u};
+
+  const double* act_base = P.actions;
+  if (!P.actions_shared && m > 0) act_base += static_cast<size_t>(valid ? b : 0) * H * m;
+
+  // ---- X0 and init_symbolic_state (flowpipe_ct.hpp:303-309)
+  double x_lo = 0.0, x_hi = 0.0;
+  if (lane < n && valid) {
+    if (P.split) {
+      split_edges(P, P.part_begin + b, lane, x_lo, x_hi);
+    } else {
+      x_lo = P.x0_lo[b * n + lane];
+      x_hi = P.x0_hi[b * n + lane];
+    }
+  }
+  auto emit_box = [&](int k, double lo, double hi, bool fin) {
+    // lane < n holds dim `lane` of box k
+    if (!valid || lane >= n) return;
+    if (!P.split) {
+      const size_t o = (static_cast<size_t>(b) * (H + 1) + k) * n + lane;
+      P.out_lo[o] = lo;
+      P.out_hi[o] = hi;
+    } else {
+      if (lo == lo) atomicMin(&P.hull_lo[k * n + lane], order_key(lo));
+      if (hi == hi) atomicMax(&P.hull_hi[k * n + lane], order_key(hi));
+      if (P.part_begin + b == 0) {
+        if (lo != lo) P.hull_nan0[(k * n + lane) * 2 + 0] = 1;
+        if (hi != hi) P.hull_nan0[(k * n + lane) * 2 + 1] = 1;
+      }
+      if (!fin) atomicOr(&P.hull_div[k], 1);
+    }
+  };
+  auto init_state = [&](double lo, double hi) {
+    // lane i < n: c_i = mid, G0 = diag(rad); queue emptied
+    if (lane < n) {
+      cc[lane] = mul(add(lo, hi), 0.5);
+      for (int j = 0; j < n; ++j) stA[lane * nzs + j] = (j == lane) ? mul(sub(hi, lo), 0.5) : 0.0;
+    }
+    __syncwarp();
+  };
+  emit_box(0, x_lo, x_hi, finite(x_lo) && finite(x_hi));
+  init_state(x_lo, x_hi);
+  int nq = 0;
+  int status = ST_OK, failed_step = -1, nboxes = 1;
+  bool done = !valid;
+
+  for (int k = 0; k < H; ++k) {
+    const double* u = act_base + static_cast<size_t>(k) * m;
+    const int nz = n * (1 + nq);
+    bool preact_bad = false;
+
+    // ---- prepend layer IBP (neural.hpp:360-373 + interval.hpp:284-295):
+    // pre0_i = sum_j iv_scale(A_ij, [-1,1]) (+ [0,0] remainder block) + c_i
+    if (!done && lane < n) {
+      double lo = 0.0, hi = 0.0;
+      for (int j = 0; j < nz; ++j) {
+        const double a = stA[lane * nzs + j];
+        const double sl = (a >= 0.0) ? -a : a;  // a*-1 : a*1
+        const double sh = (a >= 0.0) ? a : -a;
+        lo = add(lo, sl);
+        hi = add(hi, sh);
+      }
+      const double c = cc[lane];
+      hb[2 * lane] = add(lo, c);
+      hb[2 * lane + 1] = add(hi, c);
+    }
+    __syncwarp();
+
+    // ---- IBP through the hidden layers (neural.hpp:243-257); output layer skipped
+    for (int l = 0; l + 1 < L; ++l) {
+      const int width = N.dims[l + 1];
+      const int nin = (l == 0) ? n : N.dims[l];  // frozen first layer: x columns only
+      const int rows = N.dims[l];
+      const int ld = N.ldt[l];
+      const int act = N.acts[l];
+      const double* bias = blob + N.b_off[l];
+      double alo[CPL], ahi[CPL], bfold[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        alo[c] = 0.0;
+        ahi[c] = 0.0;
+        const int o = c * 32 + lane;
+        bfold[c] = (o < width) ? bias[o] : 0.0;
+      }
+      const int rpc = rows_per_chunk(ld, P.stage_doubles);
+      for (int r0 = 0; r0 < rows; r0 += rpc) {
+        const double* ch = ws_in.acquire();
+        const int nr = min(rpc, rows - r0);
+        if (!done) {
+          for (int r = 0; r < nr; ++r) {
+            const int j = r0 + r;
+            const double* wrow = ch + r * ld;
+            if (j < nin) {
+              const double xl = hb[2 * j], xh = hb[2 * j + 1];
+#pragma unroll
+              for (int c = 0; c < CPL; ++c) {
+                const int o = c * 32 + lane;
+                if (o < width) {
+                  const double w = wrow[o];
+                  const bool pos = w >= 0.0;
+                  alo[c] = add(alo[c], mul(w, pos ? xl : xh));
+                  ahi[c] = add(ahi[c], mul(w, pos ? xh : xl));
+                }
+              }
+            } else {  // freeze_trailing_inputs (neural.hpp:410): b += W[:, n+j] * u_j
+              const double uj = u[j - n];
+#pragma unroll
+              for (int c = 0; c < CPL; ++c) {
+                const int o = c * 32 + lane;
+                if (o < width) bfold[c] = add(bfold[c], mul(wrow[o], uj));
+              }
+            }
+          }
+        }
+        ws_in.release(lane);
+      }
+      if (!done) {
+        __syncwarp();  // all lanes finished reading hb
+        double* pl = pre + P.pre_off[l];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int o = c * 32 + lane;
+          if (o < width) {
+            const double plo = add(alo[c], bfold[c]);
+            const double phi = add(ahi[c], bfold[c]);
+            pl[2 * o] = plo;
+            pl[2 * o + 1] = phi;
+            if (l == 0) bf0[o] = bfold[c];
+            if (act != 2 && !(finite(plo) && finite(phi))) preact_bad = true;
+            hb[2 * o] = act_apply(act, plo);
+            hb[2 * o + 1] = act_apply(act, phi);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (!done) preact_bad = __any_sync(0xffffffffu, preact_bad);
+
+    // ---- CROWN backward (neural.hpp:297-327)
+    // init: Lambda = I * W_{L-1} = W_{L-1}; b = 0 + I * b_{L-1}
+    double blo = 0.0, bup = 0.0;
+    {
+      const int l = L - 1;
+      const int rows = N.dims[l + 1];  // = n
+      const int ncols = (l == 0) ? n : N.dims[l];
+      const int ld = N.ldw[l];
+      const int rpc = rows_per_chunk(ld, P.stage_doubles);
+      for (int r0 = 0; r0 < rows; r0 += rpc) {
+        const double* ch = ws_in.acquire();
+        const int nr = min(rpc, rows - r0);
+        if (!done) {
+          for (int r = 0; r < nr; ++r) {
+            const int i = r0 + r;
+            for (int j = lane; j < ncols; j += 32) LT[j * NOP + i] = add(0.0, ch[r * ld + j]);
+          }
+        }
+        ws_in.release(lane);
+      }
+      if (!done && lane < n) {
+        const double* bias = blob + N.b_off[l];
+        double bi = bias[lane];
+        if (l == 0 && m > 0) {  // single-layer net: fold the action into the bias here
+          const double* w = blob + N.w_off[0] + static_cast<size_t>(lane) * N.ldw[0];
+          for (int j = 0; j < m; ++j) bi = add(bi, mul(w[n + j], u[j]));
+          bf0[lane] = bi;
+        }
+        blo = add(0.0, bi);
+        bup = blo;
+      }
+      __syncwarp();
+    }
+    for (int l = L - 2; l >= 0; --l) {
+      const int width = N.dims[l + 1];  // Lambda columns on entry
+      const int act = N.acts[l];
+      const double* bvec = (l == 0 && m > 0) ? bf0 : blob + N.b_off[l];
+      // relaxation + intercept chains + shift chain (lane i owns Lambda row i)
+      if (!done) {
+        if (act != 2) {
+          const double* pl = pre + P.pre_off[l];
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const int o = c * 32 + lane;
+            if (o < width) relax(act, pl[2 * o], pl[2 * o + 1], R[3 * o], R[3 * o + 1], R[3 * o + 2]);
+          }
+          __syncwarp();
+        }
+        if (lane < n) {
+          double shift = 0.0;
+          if (act != 2) {
+            for (int j = 0; j < width; ++j) {
+              const double a = LT[j * NOP + lane];
+              const double s = R[3 * j], li = R[3 * j + 1], ui = R[3 * j + 2];
+              const bool pos = a >= 0.0;
+              blo = add(blo, mul(a, pos ? li : ui));
+              bup = add(bup, mul(a, pos ? ui : li));
+              const double as = mul(a, s);
+              LT[j * NOP + lane] = as;
+              shift = add(shift, mul(as, bvec[j]));
+            }
+          } else {
+            for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
+          }
+          blo = add(blo, shift);
+          bup = add(bup, shift);
+        }
+        __syncwarp();
+      }
+      // dense contraction Lambda <- Lambda . W_l  (linalg.hpp:53-63, i-k-j order)
+      const int ncols = (l == 0) ? n : N.dims[l];
+      const int ld = N.ldw[l];
+      double acc[NO][CPL];
+#pragma unroll
+      for (int i = 0; i < NO; ++i)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[i][c] = 0.0;
+      const int rpc = rows_per_chunk(ld, P.stage_doubles);
+      for (int r0 = 0; r0 < width; r0 += rpc) {
+        const double* ch = ws_in.acquire();
+        const int nr = min(rpc, width - r0);
+        if (!done) {
+          for (int r = 0; r < nr; ++r) {
+            const int kk = r0 + r;
+            const double* wrow = ch + r * ld;
+            double lam[NOP];
+#pragma unroll
+            for (int i = 0; i < NOP; i += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(LT + kk * NOP + i);
+              lam[i] = v.x;
+              lam[i + 1] = v.y;
+            }
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+              const int jj = c * 32 + lane;
+              const double w = (jj < ncols) ? wrow[jj] : 0.0;
+#pragma unroll
+              for (int i = 0; i < NO; ++i) acc[i][c] = mac(acc[i][c], lam[i], w);
+            }
+          }
+        }
+        ws_in.release(lane);
+      }
+      if (!done) {
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int jj = c * 32 + lane;
+          if (jj < ncols)
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+              if (i < n) LT[jj * NOP + i] = acc[i][c];
+        }
+        __syncwarp();
+      }
+    }
+    if (done) continue;  // keep draining the weight stream in lockstep
+
+    // ---- prepended layer W = [A | I], b = c: shift chain and A_out = Lambda . A
+    if (lane < n) {
+      double shift = 0.0;
+      for (int kk = 0; kk < n; ++kk) shift = add(shift, mul(LT[kk * NOP + lane], cc[kk]));
+      blo = add(blo, shift);
+      bup = add(bup, shift);
+    }
+    double aout[NO][NZG];
+#pragma unroll
+    for (int g = 0; g < NZG; ++g) {
+      const int j = g * 32 + lane;
+#pragma unroll
+      for (int i = 0; i < NO; ++i) aout[i][g] = 0.0;
+      if (j < nz) {
+        for (int kk = 0; kk < n; ++kk) {
+          const double akj = stA[kk * nzs + j];
+#pragma unroll
+          for (int i = 0; i < NO; ++i) aout[i][g] = mac(aout[i][g], LT[kk * NOP + i], akj);
+        }
+      }
+    }
+
+    // ---- tail (neural.hpp:383-391), failure checks (dt_reach.hpp:58-67)
+    double mid = 0.0, rl = 0.0, rh = 0.0;
+    bool rem_ok = true;
+    if (lane < n) {
+      mid = mul(add(blo, bup), 0.5);
+      rl = sub(blo, mid);
+      rh = sub(bup, mid);
+      rem_ok = finite(rl) && finite(rh);
+    }
+    rem_ok = __all_sync(0xffffffffu, rem_ok);
+    if (preact_bad || !rem_ok) {
+      status = preact_bad ? ST_PREACT : ST_CERT;
+      failed_step = k;
+      done = true;
+      continue;
+    }
+    __syncwarp();
+    // ---- re-seed (dt_reach.hpp:69-92): c' = c + mid(rem), blocks <- A_out, fresh = diag(rad(rem))
+#pragma unroll
+    for (int g = 0; g < NZG; ++g) {
+      const int j = g * 32 + lane;
+      if (j < nz)
+#pragma unroll
+        for (int i = 0; i < NO; ++i)
+          if (i < n) stA[i * nzs + j] = aout[i][g];
+    }
+    if (lane < n) {
+      cc[lane] = add(mid, mul(add(rl, rh), 0.5));
+      const double rad = mul(sub(rh, rl), 0.5);
+      for (int j = 0; j < n; ++j) stA[lane * nzs + nz + j] = (j == lane) ? rad : 0.0;
+    }
+    ++nq;
+    __syncwarp();
+
+    // ---- fold_overflow (flowpipe_ct.hpp:317-350), warp-parallel
+    while (nq > cap) {
+      double* M = LT;           // [n][2n] augmented [G0 | a]
+      double* X = LT + 2 * n * n;  // [n][n]
+      double* E = X + n * n;       // [n][n]
+      double* rr = E + n * n;      // [n]
+      const int n2 = 2 * n;
+      if (lane < n2)
+        for (int i = 0; i < n; ++i) M[i * n2 + lane] = stA[i * nzs + lane];  // G0 | oldest block
+      __syncwarp();
+      bool ok = true;
+      for (int kk = 0; kk < n; ++kk) {
+        int piv = kk;
+        double best = fabs(M[kk * n2 + kk]);
+        for (int i = kk + 1; i < n; ++i) {
+          const double cand = fabs(M[i * n2 + kk]);
+          if (cand > best) {
+            best = cand;
+            piv = i;
+          }
+        }
+        if (!(best > 1e-12)) {
+          ok = false;
+          break;
+        }
+        if (piv != kk && lane < n2) {
+          const double t = M[kk * n2 + lane];
+          M[kk * n2 + lane] = M[piv * n2 + lane];
+          M[piv * n2 + lane] = t;
+        }
+        __syncwarp();
+        double f[NO];
+        const double akk = M[kk * n2 + kk];
+#pragma unroll
+        for (int i = 0; i < NO; ++i) f[i] = (i > kk && i < n) ? __ddiv_rn(M[i * n2 + kk], akk) : 0.0;
+        __syncwarp();
+        if (lane < n2 && (lane >= kk)) {
+          const double mk = M[kk * n2 + lane];
+#pragma unroll
+          for (int i = 0; i < NO; ++i)
+            if (i > kk && i < n) M[i * n2 + lane] = sub(M[i * n2 + lane], mul(f[i], mk));
+        }
+        __syncwarp();
+      }
+      bool folded = false;
+      double* newest = stA + n * nq;  // column offset of the newest block
+      if (ok) {
+        // back substitution, lane j owns RHS column j
+        if (lane < n) {
+          for (int i = n - 1; i >= 0; --i) {
+            double a = M[i * n2 + n + lane];
+            for (int kk = i + 1; kk < n; ++kk) a = sub(a, mul(M[i * n2 + kk], X[kk * n + lane]));
+            X[i * n + lane] = __ddiv_rn(a, M[i * n2 + i]);
+          }
+        }
+        __syncwarp();
+        if (lane < n) {
+          double s = 0.0;
+          for (int j = 0; j < n; ++j) s = add(s, fabs(X[lane * n + j]));
+          rr[lane] = mul(s, 1.0 + 1e-12);
+        }
+        __syncwarp();
+        double worst = 0.0;
+        for (int j = 0; j < n; ++j) worst = smax(worst, rr[j]);
+        if (worst <= 1.0) {
+          // residual e = G0 X - a, then scale G0 columns, box e into the newest block
+          if (lane < n) {
+            for (int i = 0; i < n; ++i) {
+              double e = 0.0;
+              for (int kk = 0; kk < n; ++kk) e = add(e, mul(stA[i * nzs + kk], X[kk * n + lane]));
+              E[i * n + lane] = sub(e, stA[i * nzs + n + lane]);
+            }
+          }
+          __syncwarp();
+          if (lane < n) {
+            const double sc = add(1.0, rr[lane]);
+            for (int i = 0; i < n; ++i) stA[i * nzs + lane] = mul(stA[i * nzs + lane], sc);
+          }
+          if (lane < n) {
+            double s = 0.0;
+            for (int j = 0; j < n; ++j) s = add(s, fabs(E[lane * n + j]));
+            newest[lane * nzs + lane] = add(newest[lane * nzs + lane], mul(s, 1.0 + 1e-12));
+          }
+          folded = true;
+        }
+      }
+      if (!folded && lane < n) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s = add(s, fabs(stA[lane * nzs + n + j]));
+        newest[lane * nzs + lane] = add(newest[lane * nzs + lane], s);
+      }
+      __syncwarp();
+      // pop the oldest block: columns [2n, n(nq+1)) -> [n, n nq)
+      const int span = n * (nq - 1);
+      for (int i = 0; i < n; ++i) {
+        for (int j0 = 0; j0 < span; j0 += 32) {
+          const int j = j0 + lane;
+          const double v = (j < span) ? stA[i * nzs + 2 * n + j] : 0.0;
+          __syncwarp();
+          if (j < span) stA[i * nzs + n + j] = v;
+          __syncwarp();
+        }
+      }
+      --nq;
+    }
+
+    // ---- symbolic_box (flowpipe_ct.hpp:413-424)
+    double lo = 0.0, hi = 0.0;
+    bool fin = true;
+    if (lane < n) {
+      double r = 0.0;
+      for (int j = 0; j < n; ++j) r = add(r, fabs(stA[lane * nzs + j]));
+      for (int q = 1; q <= nq; ++q) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s = add(s, fabs(stA[lane * nzs + q * n + j]));
+        r = add(r, s);
+      }
+      const double c = cc[lane];
+      lo = sub(c, r);
+      hi = add(c, r);
+      fin = finite(lo) && finite(hi);
+    }
+    fin = __all_sync(0xffffffffu, fin);
+    emit_box(k + 1, lo, hi, fin);
+    nboxes = k + 2;
+    if (!fin) {
+      status = ST_BOX;
+      failed_step = k;
+      done = true;
+      continue;
+    }
+    __syncwarp();
+    if (P.rebuild) {
+      init_state(lo, hi);
+      nq = 0;
+    }
+  }
+
+  if (!valid) return;
+  if (!P.split) {
+    if (lane == 0) {
+      P.n_boxes[b] = nboxes;
+      P.failed_step[b] = failed_step;
+      P.status[b] = status;
+    }
+  } else if (lane == 0) {
+    atomicMin(P.hull_nboxes, nboxes);
+    if (status != ST_OK) {
+      const unsigned long long key = (static_cast<unsigned long long>(failed_step >= 0 ? failed_step : nboxes) << 40) |
+                                     (static_cast<unsigned long long>(P.part_begin + b) << 8) |
+                                     static_cast<unsigned long long>(status & 0xff);
+      atomicMin(P.hull_fail_key, key);
+    }
+  }
+}
+
+// Converts the hull order keys back to doubles, applying the part-0 NaN rule.
+__global__ void hull_finalize_kernel(const unsigned long long* klo, const unsigned long long* khi, const int* nan0,
+                                     int count, double* lo, double* hi) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  lo[t] = nan0[2 * t] ? __longlong_as_double(0x7ff8000000000000ll) : from_order_key(klo[t]);
+  hi[t] = nan0[2 * t + 1] ? __longlong_as_double(0x7ff8000000000000ll) : from_order_key(khi[t]);
+}
+
+}  // namespace rb

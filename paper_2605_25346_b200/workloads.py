@@ -1,0 +1,127 @@
+"""Seeded synthetic workloads of the BASELINE.json configs.
+
+Plain `random_mlp` nets make tubes collapse or explode over the horizon, so the
+DT dynamics are near-identity residual ReLU maps: the first n+m hidden units
+of every layer carry (x, u) through relu(v + K) with K = 10 (stably active, so
+CROWN is exact on them); the remaining units are random features of (x, u);
+the output layer is x' = a x + dt Bu u + dt Bf features with the K offset
+cancelled in the biases.  Deterministic for a given seed (numpy PCG64).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List
+
+import numpy as np
+
+from .api import Act, DTSystem, Layer, MLPNet, SplitPlan
+
+MASTER_SEED = 20261017
+K_OFFSET = 10.0
+
+
+def residual_relu_dynamics(rng: np.random.Generator, n: int, m: int, hidden: List[int], dt: float,
+                           a: float = 0.95, mix: float = 0.3) -> MLPNet:
+    p = n + m
+    assert all(h >= p for h in hidden)
+    layers = []
+    prev = p
+    prev_feat = 0
+    for li, h in enumerate(hidden):
+        F = h - p
+        w = np.zeros((h, prev))
+        b = np.zeros(h)
+        # pass-through of (x, u): first layer adds K, deeper layers keep it
+        for i in range(p):
+            w[i, i] = 1.0
+        if li == 0:
+            b[:p] = K_OFFSET
+            w[p:, :p] = rng.normal(0.0, 1.0 / np.sqrt(p), size=(F, p))
+            b[p:] = rng.normal(0.0, 1.0, size=F)
+        else:
+            wx = rng.normal(0.0, 1.0 / np.sqrt(p), size=(F, p))
+            w[p:, :p] = wx
+            b[p:] = rng.normal(0.0, 1.0, size=F) - wx.sum(axis=1) * K_OFFSET  # cancel the K offset
+            if prev_feat > 0:
+                w[p:, p:prev] = rng.normal(0.0, mix / np.sqrt(prev_feat), size=(F, prev_feat))
+        layers.append(Layer(w, b, Act.Relu))
+        prev, prev_feat = h, F
+    # output layer: x' = a x + dt Bu u + dt Bf f   (inputs carry +K on the first p units)
+    w = np.zeros((n, prev))
+    b = np.zeros(n)
+    w[:, :n] = a * np.eye(n)
+    if m > 0:
+        bu = dt * rng.normal(0.0, 1.0, size=(n, m))
+        w[:, n:p] = bu
+    if prev_feat > 0:
+        w[:, p:prev] = dt * rng.normal(0.0, 1.0 / np.sqrt(prev_feat), size=(n, prev_feat))
+    b[:] = -w[:, :p].sum(axis=1) * K_OFFSET
+    layers.append(Layer(w, b, Act.Identity))
+    return MLPNet(layers)
+
+
+def random_mlp(rng: np.random.Generator, in_dim: int, hidden: List[int], out_dim: int, act: Act = Act.Relu,
+               scale: float = 1.0) -> MLPNet:
+    """Shape of random_mlp (neural.hpp:97-115) on a numpy stream."""
+    dims = [in_dim] + list(hidden) + [out_dim]
+    layers = []
+    for l in range(len(dims) - 1):
+        std = scale / np.sqrt(dims[l])
+        w = rng.normal(0.0, 1.0, size=(dims[l + 1], dims[l])) * std
+        b = rng.normal(0.0, 1.0, size=dims[l + 1]) * 0.05 * scale
+        layers.append(Layer(w, b, Act.Identity if l + 2 == len(dims) else act))
+    return MLPNet(layers)
+
+
+@dataclass
+class SplitWorkload:
+    sys: DTSystem
+    x0_lo: np.ndarray
+    x0_hi: np.ndarray
+    plan: SplitPlan
+    actions: np.ndarray  # [H][m]
+    horizon: int
+
+
+def c4_partition_sweep(seed: int = MASTER_SEED, counts=(8, 8, 8, 8, 4, 4), horizon: int = 30) -> SplitWorkload:
+    """BASELINE configs[3]: 65,536 sub-boxes of a 6D system, 3x128 ReLU, H = 30 (SURVEY §8 shape sheet C4)."""
+    rng = np.random.default_rng(seed + 4)
+    n = 6
+    net = residual_relu_dynamics(rng, n, 0, [128, 128, 128], dt=0.1)
+    c0 = rng.uniform(-0.5, 0.5, size=n)
+    return SplitWorkload(DTSystem(net, n, 0), c0 - 0.004, c0 + 0.004, SplitPlan(list(counts)),
+                         np.zeros((horizon, 0)), horizon)
+
+
+@dataclass
+class BatchWorkload:
+    sys: DTSystem
+    x0_lo: np.ndarray  # [B][n]
+    x0_hi: np.ndarray
+    actions: np.ndarray  # [B][H][m]
+
+
+def c3_mpc_candidates(seed: int = MASTER_SEED, batch: int = 4096, horizon: int = 20) -> BatchWorkload:
+    """BASELINE configs[2] tube leg: 4096 CEM candidates x H=20, 7->96x3->5 ReLU, eps 0.005, U=[-1,1]^2."""
+    rng = np.random.default_rng(seed + 3)
+    n, m = 5, 2
+    net = residual_relu_dynamics(rng, n, m, [96, 96, 96], dt=0.1)
+    x0 = np.zeros((batch, n))
+    acts = np.clip(rng.normal(0.0, 0.3, size=(batch, horizon, m)), -1.0, 1.0)
+    return BatchWorkload(DTSystem(net, n, m), x0 - 0.005, x0 + 0.005, acts)
+
+
+def small_batch(seed: int, n: int, m: int, hidden: List[int], batch: int, horizon: int, eps: float = 0.01,
+                act: Act = Act.Relu, residual: bool = True) -> BatchWorkload:
+    """Small seeded batch for parity tests."""
+    rng = np.random.default_rng(seed)
+    if residual and act == Act.Relu:
+        net = residual_relu_dynamics(rng, n, m, hidden, dt=0.1)
+    else:
+        net = random_mlp(rng, n + m, hidden, n, act, 0.6)
+        for L in net.layers[-1:]:
+            L.w *= 0.3
+    c = rng.uniform(-0.5, 0.5, size=(batch, n))
+    r = rng.uniform(0.2 * eps, eps, size=(batch, n))
+    acts = rng.uniform(-0.5, 0.5, size=(batch, horizon, m))
+    return BatchWorkload(DTSystem(net, n, m), c - r, c + r, acts)

@@ -1,0 +1,137 @@
+"""Test-side bindings of the CPU checkers (oracle/): the C restatement
+(oracle/liboracle.so) and the reference itself (oracle/_ref/libreach_ref.so).
+
+Only tests, __graft_entry__.smoke() and bench.py's CPU legs import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2605_25346_b200 import _abi as A
+from paper_2605_25346_b200.api import DTReachParams, DTSystem, HullResult, SplitPlan, TubeBatch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libreach_ref.so")
+
+
+def _build_oracle():
+    if not os.path.exists(ORACLE_SO):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "liboracle.so"], check=True,
+                       stdout=subprocess.DEVNULL)
+
+
+def _load(path, prefix):
+    lib = C.CDLL(path)
+    f = getattr(lib, prefix + "dt_batch")
+    f.argtypes = [C.POINTER(A.NetDesc), C.POINTER(A.DTArgs), C.POINTER(A.TubeOut)] + ([C.c_int32] if prefix == "ref_" else [])
+    f.restype = C.c_int
+    g = getattr(lib, prefix + "split_hull")
+    g.argtypes = [C.POINTER(A.NetDesc), C.POINTER(A.SplitArgs), C.POINTER(A.HullOut)] + ([C.c_int32] if prefix == "ref_" else [])
+    g.restype = C.c_int
+    return lib
+
+
+_cache = {}
+
+
+def oracle_lib():
+    if "orc" not in _cache:
+        _build_oracle()
+        _cache["orc"] = _load(ORACLE_SO, "orc_")
+    return _cache["orc"]
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref_lib():
+    if "ref" not in _cache:
+        _cache["ref"] = _load(REF_SO, "ref_")
+    return _cache["ref"]
+
+
+def _dt(lib, prefix, sys: DTSystem, x0_lo, x0_hi, actions, prm: DTReachParams, shared=False, threads=None):
+    x0_lo = np.ascontiguousarray(x0_lo, np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, np.float64)
+    B = x0_lo.shape[0]
+    actions = np.ascontiguousarray(actions, np.float64)
+    H = actions.shape[0] if shared else actions.shape[1]
+    out = TubeBatch(np.full((B, H + 1, sys.n), np.nan), np.full((B, H + 1, sys.n), np.nan),
+                    np.zeros(B, np.int32), np.zeros(B, np.int32), np.zeros(B, np.int32))
+    desc, keep = sys.step.desc()
+    args = A.DTArgs(B, H, sys.n, sys.m, prm.window, int(prm.rebuild_from_box), A.dptr(x0_lo), A.dptr(x0_hi),
+                    A.dptr(actions if actions.size else np.zeros(1)), int(shared))
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step), A.iptr(out.status))
+    fn = getattr(lib, prefix + "dt_batch")
+    rc = fn(C.byref(desc), C.byref(args), C.byref(to), *([threads or 0] if prefix == "ref_" else []))
+    assert rc == 0, rc
+    return out
+
+
+def oracle_dt_batch(sys, x0_lo, x0_hi, actions, prm=DTReachParams(), shared=False):
+    return _dt(oracle_lib(), "orc_", sys, x0_lo, x0_hi, actions, prm, shared)
+
+
+def ref_dt_batch(sys, x0_lo, x0_hi, actions, prm=DTReachParams(), shared=False, threads=0):
+    return _dt(ref_lib(), "ref_", sys, x0_lo, x0_hi, actions, prm, shared, threads)
+
+
+def _hull(lib, prefix, sys, x0_lo, x0_hi, plan: SplitPlan, actions, prm, begin=0, end=0, threads=None):
+    acts = np.ascontiguousarray(np.asarray(actions, np.float64).reshape(-1, sys.m) if sys.m else np.zeros((0, 0)))
+    H = acts.shape[0] if sys.m else len(actions)
+    lo0 = np.ascontiguousarray(x0_lo, np.float64)
+    hi0 = np.ascontiguousarray(x0_hi, np.float64)
+    counts = np.array(plan.counts, np.int32)
+    out = HullResult(np.full((H + 1, sys.n), np.nan), np.full((H + 1, sys.n), np.nan), np.zeros(H + 1, np.int32), 0, 0)
+    nb = np.zeros(1, np.int32)
+    key = np.zeros(1, np.int64)
+    desc, keep = sys.step.desc()
+    args = A.SplitArgs(sys.n, sys.m, H, prm.window, int(prm.rebuild_from_box), A.dptr(lo0), A.dptr(hi0),
+                       A.iptr(counts), A.dptr(acts if acts.size else np.zeros(1)), int(begin), int(end))
+    ho = A.HullOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.box_diverged), A.iptr(nb), A.lptr(key))
+    fn = getattr(lib, prefix + "split_hull")
+    rc = fn(C.byref(desc), C.byref(args), C.byref(ho), *([threads or 0] if prefix == "ref_" else []))
+    assert rc == 0, rc
+    out.n_boxes = int(nb[0])
+    out.fail_key = int(key[0])
+    return out
+
+
+def oracle_split_hull(sys, x0_lo, x0_hi, plan, actions, prm=DTReachParams(), begin=0, end=0):
+    return _hull(oracle_lib(), "orc_", sys, x0_lo, x0_hi, plan, actions, prm, begin, end)
+
+
+def ref_split_hull(sys, x0_lo, x0_hi, plan, actions, prm=DTReachParams(), begin=0, end=0, threads=0):
+    return _hull(ref_lib(), "ref_", sys, x0_lo, x0_hi, plan, actions, prm, begin, end, threads)
+
+
+def same_bits(a: np.ndarray, b: np.ndarray) -> bool:
+    """Bitwise equality up to the sign of zero (NaN == NaN)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.shape != b.shape:
+        return False
+    eq = (a == b) | (np.isnan(a) & np.isnan(b))
+    return bool(np.all(eq))
+
+
+def assert_tubes_equal(got: TubeBatch, exp: TubeBatch, exact=True, rtol=1e-12):
+    assert np.array_equal(got.n_boxes, exp.n_boxes), (got.n_boxes, exp.n_boxes)
+    assert np.array_equal(got.status, exp.status), (got.status, exp.status)
+    assert np.array_equal(got.failed_step, exp.failed_step)
+    for b in range(got.lo.shape[0]):
+        k = int(exp.n_boxes[b])
+        for arr_g, arr_e in ((got.lo, exp.lo), (got.hi, exp.hi)):
+            g, e = arr_g[b, :k], arr_e[b, :k]
+            if exact:
+                assert same_bits(g, e), (b, np.max(np.abs(g - e)))
+            else:
+                fin = np.isfinite(e)
+                scale = np.maximum(np.abs(e[fin]), 1e-300)
+                assert np.all(np.abs(g[fin] - e[fin]) <= rtol * np.maximum(scale, 1.0)), b
