@@ -219,7 +219,8 @@ def main():
     H, n, m = w.horizon, w.sys.n, w.sys.m
 
     ctx = Context(local)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # the library launches here; torch work joins it below
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     netdims = [int(x) for x in w.sys.step.dims()]
     flops_part = algorithmic_flops_per_part(netdims, n, m, H, 4)

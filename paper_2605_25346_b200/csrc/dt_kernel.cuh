@@ -34,13 +34,15 @@ struct DevNet {
   int L;
   int dims[kMaxLayers + 1];
   int acts[kMaxLayers];
-  long long w_off[kMaxLayers];   // W_l  : dims[l+1] rows x ldw[l]   (row-major, cols = dims[l])
-  long long wt_off[kMaxLayers];  // W_l^T: dims[l] rows x ldt[l]     (cols = dims[l+1])
-  long long b_off[kMaxLayers];
+  long long w_off[kMaxLayers];   // W_l  : dims[l+1] rows x ldw[l]   (row-major, cols = dims[l], zero-padded)
+  long long wt_off[kMaxLayers];  // W_l^T: dims[l] rows x ldt[l]     (cols = dims[l+1], zero-padded)
+  long long b_off[kMaxLayers];   // b_l padded with zeros to a multiple of 32
   int ldw[kMaxLayers];
   int ldt[kMaxLayers];
   const double* blob;
 };
+
+constexpr int kMaxChunks = 96;  // weight-stream chunks per DT step
 
 struct DTParams {
   DevNet net;
@@ -69,29 +71,54 @@ struct DTParams {
   int* hull_nboxes;             // [1]
   unsigned long long* hull_fail_key;  // [1]
   // shared-memory layout (doubles)
-  int stage_doubles, nstage, warp_doubles;
+  int stage_doubles, nstage, warp_doubles, bias_doubles;
   int o_stA, o_c, o_pre, o_h, o_LT, o_R, o_bf0;
-  int nzs;       // stA row stride (n * (cap + 2))
-  int pre_off[kMaxLayers];
+  int nzs;                      // stA row stride (n * (cap + 2))
+  int hp;                       // padded hidden width (32 * CPL)
+  int bias_s_off[kMaxLayers];   // per-layer bias offsets in the CTA bias copy
+  // weight stream: chunk table of one DT step (the sequence repeats every step)
+  int n_chunks_step;
+  long long ch_off[kMaxChunks];
+  unsigned ch_bytes[kMaxChunks];
 };
 
 enum : int { ST_OK = 0, ST_PREACT = 1, ST_CERT = 2, ST_BOX = 3 };
 
-// Consumer side of the weight stream.
+// Weight stream: a ring of shared-memory stages filled by the bulk-copy (TMA)
+// engine.  Every sample warp consumes every chunk in the same order; the LAST
+// warp to release a stage refills it with the chunk NSTAGE ahead, so no warp
+// is dedicated to producing and no warp blocks on a slow sibling to refill.
 struct WStream {
-  const double* stages;
+  const DTParams* P;
+  double* stages;
   uint64_t* full;
-  uint64_t* empty;
-  int nstage, stage_doubles;
+  int* cnt;
+  int spc;
   uint32_t g;
-  __device__ __forceinline__ const double* acquire() {
-    const int s = g % nstage;
-    mbar_wait(&full[s], (g / nstage) & 1u);
-    return stages + static_cast<size_t>(s) * stage_doubles;
+  uint32_t total;
+  __device__ __forceinline__ void issue(uint32_t gn, int s) const {
+    const int idx = static_cast<int>(gn % static_cast<uint32_t>(P->n_chunks_step));
+    const uint32_t bytes = P->ch_bytes[idx];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(&full[s], bytes);
+    bulk_g2s(stages + static_cast<size_t>(s) * P->stage_doubles, P->net.blob + P->ch_off[idx], bytes, &full[s]);
+  }
+  __device__ __forceinline__ const double* acquire() const {
+    const int s = g % P->nstage;
+    mbar_wait(&full[s], (g / P->nstage) & 1u);
+    return stages + static_cast<size_t>(s) * P->stage_doubles;
   }
   __device__ __forceinline__ void release(int lane) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[g % nstage]);
+    if (lane == 0) {
+      const int s = g % P->nstage;
+      __threadfence_block();
+      if (atomicAdd(&cnt[s], 1) == spc - 1) {
+        atomicExch(&cnt[s], 0);
+        const uint32_t gn = g + P->nstage;
+        if (gn < total) issue(gn, s);
+      }
+    }
     ++g;
   }
 };
@@ -99,21 +126,6 @@ struct WStream {
 __device__ __forceinline__ int rows_per_chunk(int ld, int stage_doubles) {
   int r = stage_doubles / ld;
   return r < 1 ? 1 : r;
-}
-
-// Producer: issues one matrix (rows x ld doubles) as a sequence of chunks.
-__device__ __forceinline__ void produce_matrix(const double* src, int rows, int ld, double* stages, uint64_t* full,
-                                               uint64_t* empty, int nstage, int stage_doubles, uint32_t& g) {
-  const int rpc = rows_per_chunk(ld, stage_doubles);
-  for (int r0 = 0; r0 < rows; r0 += rpc) {
-    const int nr = min(rpc, rows - r0);
-    const int s = g % nstage;
-    mbar_wait(&empty[s], ((g / nstage) & 1u) ^ 1u);
-    const uint32_t bytes = static_cast<uint32_t>(nr) * ld * 8u;
-    mbar_arrive_expect_tx(&full[s], bytes);
-    bulk_g2s(stages + static_cast<size_t>(s) * stage_doubles, src + static_cast<size_t>(r0) * ld, bytes, &full[s]);
-    ++g;
-  }
 }
 
 // relax_activation (neural.hpp:166-227) for ReLU / tanh; identity never relaxed.
@@ -178,67 +190,65 @@ __device__ __forceinline__ void split_edges(const DTParams& P, long long p, int 
   hi = (i + 1 == k) ? xh : add(xl, mul(w, __ddiv_rn(static_cast<double>(i + 1), static_cast<double>(k))));
 }
 
+
 // ---------------------------------------------------------------------------
 // The kernel.  NO: max state dim (= network output dim) of this family;
-// CPL: hidden units per lane (max hidden width <= 32 * CPL).
+// CPL: hidden units per lane (padded hidden width HP = 32 * CPL).
+// Block = kSampleWarps warps, one sample per warp.
+constexpr int kSampleWarps = 8;
+
 template <int NO, int CPL>
-__global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
+__global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const DTParams P) {
   constexpr int NOP = (NO + 1) & ~1;  // Lambda^T row stride (16-byte rows)
   constexpr int NZG = 2;              // 32-column groups of the generator matrix (nzs <= 64)
+  constexpr int HP = 32 * CPL;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int nwarps = blockDim.x / 32;
-  const int spc = nwarps - 1;  // sample warps per CTA; warp spc is the producer
+  const int spc = blockDim.x / 32;
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* empty = full + P.nstage;
+  int* cnt = reinterpret_cast<int*>(smem_raw + 64);
   double* stages = reinterpret_cast<double*>(smem_raw + 128);
-  double* wbase = stages + static_cast<size_t>(P.nstage) * P.stage_doubles;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < P.nstage; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], spc);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
+  double* bias_s = stages + static_cast<size_t>(P.nstage) * P.stage_doubles;
+  double* wbase = bias_s + P.bias_doubles;
 
   const DevNet& N = P.net;
   const int L = N.L;
   const int n = P.n, m = P.m, H = P.H;
   const int cap = P.window > 0 ? P.window : 1;
   const double* blob = N.blob;
+  const uint32_t total_chunks = static_cast<uint32_t>(P.n_chunks_step) * static_cast<uint32_t>(H);
 
-  // ------------------------------------------------------------ producer
-  if (warp == spc) {
-    if (lane == 0) {
-      uint32_t g = 0;
-      for (int k = 0; k < H; ++k) {
-        for (int l = 0; l + 1 < L; ++l)
-          produce_matrix(blob + N.wt_off[l], N.dims[l], N.ldt[l], stages, full, empty, P.nstage, P.stage_doubles, g);
-        for (int l = L - 1; l >= 0; --l)
-          produce_matrix(blob + N.w_off[l], N.dims[l + 1], N.ldw[l], stages, full, empty, P.nstage,
-                         P.stage_doubles, g);
-      }
+  WStream ws_in{&P, stages, full, cnt, spc, 0u, total_chunks};
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      cnt[s] = 0;
     }
-    return;
+    fence_mbar_init();
   }
+  // CTA copy of every layer's (padded) bias
+  for (int l = 0; l < L; ++l) {
+    const int cnt_b = (l + 1 < L) ? HP : ((N.dims[l + 1] + 1) & ~1);
+    for (int i = threadIdx.x; i < cnt_b; i += blockDim.x) bias_s[P.bias_s_off[l] + i] = blob[N.b_off[l] + i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < P.nstage && static_cast<uint32_t>(s) < total_chunks; ++s) ws_in.issue(s, s);
 
-  // ------------------------------------------------------------ sample warp
+  // ------------------------------------------------------------ per-warp sample
   const long long b = static_cast<long long>(blockIdx.x) * spc + warp;
   const bool valid = b < P.B;
   double* ws = wbase + static_cast<size_t>(warp) * P.warp_doubles;
   double* stA = ws + P.o_stA;  // n x nzs: [G0 | Q1 .. Qnq | (fresh)]
   double* cc = ws + P.o_c;     // n
-  double* pre = ws + P.o_pre;  // per hidden layer, (lo,hi) per unit
+  double* pre = ws + P.o_pre;  // per hidden layer: (lo,hi) per padded unit
   double* hb = ws + P.o_h;     // IBP layer input (lo,hi) per unit
   double* LT = ws + P.o_LT;    // Lambda^T: [col][NOP]
   double* R = ws + P.o_R;      // relaxation (s, li, ui) per unit
-  double* bf0 = ws + P.o_bf0;  // frozen first-layer bias (per sample: actions differ)
+  double* bf0 = ws + P.o_bf0;  // frozen first-layer bias (actions differ per sample)
   const int nzs = P.nzs;
-  WStream ws_in{stages, full, empty, P.nstage, P.stage_doubles, 0u};
 
   const double* act_base = P.actions;
   if (!P.actions_shared && m > 0) act_base += static_cast<size_t>(valid ? b : 0) * H * m;
@@ -254,7 +264,6 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
     }
   }
   auto emit_box = [&](int k, double lo, double hi, bool fin) {
-    // lane < n holds dim `lane` of box k
     if (!valid || lane >= n) return;
     if (!P.split) {
       const size_t o = (static_cast<size_t>(b) * (H + 1) + k) * n + lane;
@@ -271,10 +280,10 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
     }
   };
   auto init_state = [&](double lo, double hi) {
-    // lane i < n: c_i = mid, G0 = diag(rad); queue emptied
     if (lane < n) {
       cc[lane] = mul(add(lo, hi), 0.5);
-      for (int j = 0; j < n; ++j) stA[lane * nzs + j] = (j == lane) ? mul(sub(hi, lo), 0.5) : 0.0;
+      const double rad = mul(sub(hi, lo), 0.5);
+      for (int j = 0; j < n; ++j) stA[lane * nzs + j] = (j == lane) ? rad : 0.0;
     }
     __syncwarp();
   };
@@ -290,15 +299,13 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
     bool preact_bad = false;
 
     // ---- prepend layer IBP (neural.hpp:360-373 + interval.hpp:284-295):
-    // pre0_i = sum_j iv_scale(A_ij, [-1,1]) (+ [0,0] remainder block) + c_i
+    // pre0_i = sum_j iv_scale(A_ij, [-1,1]) (+ the [0,0] remainder block) + c_i
     if (!done && lane < n) {
       double lo = 0.0, hi = 0.0;
       for (int j = 0; j < nz; ++j) {
         const double a = stA[lane * nzs + j];
-        const double sl = (a >= 0.0) ? -a : a;  // a*-1 : a*1
-        const double sh = (a >= 0.0) ? a : -a;
-        lo = add(lo, sl);
-        hi = add(hi, sh);
+        lo = add(lo, (a >= 0.0) ? -a : a);  // a*-1 : a*1
+        hi = add(hi, (a >= 0.0) ? a : -a);
       }
       const double c = cc[lane];
       hb[2 * lane] = add(lo, c);
@@ -313,71 +320,72 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
       const int rows = N.dims[l];
       const int ld = N.ldt[l];
       const int act = N.acts[l];
-      const double* bias = blob + N.b_off[l];
+      const double* bias = bias_s + P.bias_s_off[l];
       double alo[CPL], ahi[CPL], bfold[CPL];
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         alo[c] = 0.0;
         ahi[c] = 0.0;
-        const int o = c * 32 + lane;
-        bfold[c] = (o < width) ? bias[o] : 0.0;
+        bfold[c] = bias[c * 32 + lane];
       }
       const int rpc = rows_per_chunk(ld, P.stage_doubles);
       for (int r0 = 0; r0 < rows; r0 += rpc) {
         const double* ch = ws_in.acquire();
         const int nr = min(rpc, rows - r0);
         if (!done) {
-          for (int r = 0; r < nr; ++r) {
-            const int j = r0 + r;
-            const double* wrow = ch + r * ld;
-            if (j < nin) {
-              const double xl = hb[2 * j], xh = hb[2 * j + 1];
+          const int nx = max(0, min(nr, nin - r0));  // rows of this chunk that are x columns
+#pragma unroll 2
+          for (int r = 0; r < nx; ++r) {
+            const double* wrow = ch + r * ld + lane;
+            const double2 x = *reinterpret_cast<const double2*>(hb + 2 * (r0 + r));
+            double w[CPL], tl[CPL], th[CPL];
 #pragma unroll
-              for (int c = 0; c < CPL; ++c) {
-                const int o = c * 32 + lane;
-                if (o < width) {
-                  const double w = wrow[o];
-                  const bool pos = w >= 0.0;
-                  alo[c] = add(alo[c], mul(w, pos ? xl : xh));
-                  ahi[c] = add(ahi[c], mul(w, pos ? xh : xl));
-                }
-              }
-            } else {  // freeze_trailing_inputs (neural.hpp:410): b += W[:, n+j] * u_j
-              const double uj = u[j - n];
+            for (int c = 0; c < CPL; ++c) w[c] = wrow[c * 32];
 #pragma unroll
-              for (int c = 0; c < CPL; ++c) {
-                const int o = c * 32 + lane;
-                if (o < width) bfold[c] = add(bfold[c], mul(wrow[o], uj));
-              }
+            for (int c = 0; c < CPL; ++c) {
+              const bool pos = w[c] >= 0.0;
+              tl[c] = mul(w[c], pos ? x.x : x.y);
+              th[c] = mul(w[c], pos ? x.y : x.x);
             }
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+              alo[c] = add(alo[c], tl[c]);
+              ahi[c] = add(ahi[c], th[c]);
+            }
+          }
+          for (int r = nx; r < nr; ++r) {  // freeze_trailing_inputs (neural.hpp:410): b += W[:, n+j] u_j
+            const double uj = u[r0 + r - n];
+            const double* wrow = ch + r * ld + lane;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) bfold[c] = add(bfold[c], mul(wrow[c * 32], uj));
           }
         }
         ws_in.release(lane);
       }
       if (!done) {
-        __syncwarp();  // all lanes finished reading hb
-        double* pl = pre + P.pre_off[l];
+        double* pl = pre + l * 2 * HP;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const int o = c * 32 + lane;
-          if (o < width) {
-            const double plo = add(alo[c], bfold[c]);
-            const double phi = add(ahi[c], bfold[c]);
-            pl[2 * o] = plo;
-            pl[2 * o + 1] = phi;
-            if (l == 0) bf0[o] = bfold[c];
-            if (act != 2 && !(finite(plo) && finite(phi))) preact_bad = true;
-            hb[2 * o] = act_apply(act, plo);
-            hb[2 * o + 1] = act_apply(act, phi);
-          }
+          const double plo = add(alo[c], bfold[c]);
+          const double phi = add(ahi[c], bfold[c]);
+          *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(plo, phi);
+          if (l == 0) bf0[o] = bfold[c];
+          if (o < width && act != 2 && !(finite(plo) && finite(phi))) preact_bad = true;
+          alo[c] = act_apply(act, plo);
+          ahi[c] = act_apply(act, phi);
         }
+        __syncwarp();  // every lane is done reading hb
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          *reinterpret_cast<double2*>(hb + 2 * (c * 32 + lane)) = make_double2(alo[c], ahi[c]);
         __syncwarp();
       }
     }
     if (!done) preact_bad = __any_sync(0xffffffffu, preact_bad);
 
     // ---- CROWN backward (neural.hpp:297-327)
-    // init: Lambda = I * W_{L-1} = W_{L-1}; b = 0 + I * b_{L-1}
+    // init: Lambda = I . W_{L-1} = W_{L-1};  b = 0 + I . b_{L-1}
     double blo = 0.0, bup = 0.0;
     {
       const int l = L - 1;
@@ -397,8 +405,7 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
         ws_in.release(lane);
       }
       if (!done && lane < n) {
-        const double* bias = blob + N.b_off[l];
-        double bi = bias[lane];
+        double bi = bias_s[P.bias_s_off[l] + lane];
         if (l == 0 && m > 0) {  // single-layer net: fold the action into the bias here
           const double* w = blob + N.w_off[0] + static_cast<size_t>(lane) * N.ldw[0];
           for (int j = 0; j < m; ++j) bi = add(bi, mul(w[n + j], u[j]));
@@ -412,32 +419,43 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
     for (int l = L - 2; l >= 0; --l) {
       const int width = N.dims[l + 1];  // Lambda columns on entry
       const int act = N.acts[l];
-      const double* bvec = (l == 0 && m > 0) ? bf0 : blob + N.b_off[l];
-      // relaxation + intercept chains + shift chain (lane i owns Lambda row i)
+      const double* bvec = (l == 0 && m > 0) ? bf0 : bias_s + P.bias_s_off[l];
+      // relaxation (parallel), then the intercept / shift chains (lane i owns row i)
       if (!done) {
         if (act != 2) {
-          const double* pl = pre + P.pre_off[l];
+          const double* pl = pre + l * 2 * HP;
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
             const int o = c * 32 + lane;
-            if (o < width) relax(act, pl[2 * o], pl[2 * o + 1], R[3 * o], R[3 * o + 1], R[3 * o + 2]);
+            const double2 p = *reinterpret_cast<const double2*>(pl + 2 * o);
+            double s, li, ui;
+            relax(act, p.x, p.y, s, li, ui);
+            R[3 * o] = s;
+            R[3 * o + 1] = li;
+            R[3 * o + 2] = ui;
           }
           __syncwarp();
         }
         if (lane < n) {
           double shift = 0.0;
           if (act != 2) {
+#pragma unroll 4
             for (int j = 0; j < width; ++j) {
               const double a = LT[j * NOP + lane];
               const double s = R[3 * j], li = R[3 * j + 1], ui = R[3 * j + 2];
+              const double bj = bvec[j];
               const bool pos = a >= 0.0;
-              blo = add(blo, mul(a, pos ? li : ui));
-              bup = add(bup, mul(a, pos ? ui : li));
+              const double pl = mul(a, pos ? li : ui);
+              const double pu = mul(a, pos ? ui : li);
               const double as = mul(a, s);
+              const double ps = mul(as, bj);
               LT[j * NOP + lane] = as;
-              shift = add(shift, mul(as, bvec[j]));
+              blo = add(blo, pl);
+              bup = add(bup, pu);
+              shift = add(shift, ps);
             }
           } else {
+#pragma unroll 4
             for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
           }
           blo = add(blo, shift);
@@ -446,50 +464,84 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
         __syncwarp();
       }
       // dense contraction Lambda <- Lambda . W_l  (linalg.hpp:53-63, i-k-j order)
-      const int ncols = (l == 0) ? n : N.dims[l];
       const int ld = N.ldw[l];
-      double acc[NO][CPL];
-#pragma unroll
-      for (int i = 0; i < NO; ++i)
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) acc[i][c] = 0.0;
       const int rpc = rows_per_chunk(ld, P.stage_doubles);
-      for (int r0 = 0; r0 < width; r0 += rpc) {
-        const double* ch = ws_in.acquire();
-        const int nr = min(rpc, width - r0);
-        if (!done) {
-          for (int r = 0; r < nr; ++r) {
-            const int kk = r0 + r;
-            const double* wrow = ch + r * ld;
-            double lam[NOP];
+      if (l > 0) {
+        double acc[NO][CPL];
 #pragma unroll
-            for (int i = 0; i < NOP; i += 2) {
-              const double2 v = *reinterpret_cast<const double2*>(LT + kk * NOP + i);
-              lam[i] = v.x;
-              lam[i + 1] = v.y;
-            }
+        for (int i = 0; i < NO; ++i)
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) {
-              const int jj = c * 32 + lane;
-              const double w = (jj < ncols) ? wrow[jj] : 0.0;
+          for (int c = 0; c < CPL; ++c) acc[i][c] = 0.0;
+        for (int r0 = 0; r0 < width; r0 += rpc) {
+          const double* ch = ws_in.acquire();
+          const int nr = min(rpc, width - r0);
+          if (!done) {
+#pragma unroll 2
+            for (int r = 0; r < nr; ++r) {
+              const double* lrow = LT + (r0 + r) * NOP;
+              const double* wrow = ch + r * ld + lane;
+              double lam[NOP], w[CPL];
 #pragma unroll
-              for (int i = 0; i < NO; ++i) acc[i][c] = mac(acc[i][c], lam[i], w);
+              for (int i = 0; i < NOP; i += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(lrow + i);
+                lam[i] = v.x;
+                lam[i + 1] = v.y;
+              }
+#pragma unroll
+              for (int c = 0; c < CPL; ++c) w[c] = wrow[c * 32];
+              double t[NO][CPL];
+#pragma unroll
+              for (int i = 0; i < NO; ++i)
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) t[i][c] = mul(lam[i], w[c]);
+#pragma unroll
+              for (int i = 0; i < NO; ++i)
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) acc[i][c] = add(acc[i][c], t[i][c]);
             }
           }
+          ws_in.release(lane);
         }
-        ws_in.release(lane);
-      }
-      if (!done) {
-        __syncwarp();
+        if (!done) {
+          __syncwarp();
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const int jj = c * 32 + lane;
-          if (jj < ncols)
+          for (int c = 0; c < CPL; ++c) {
+            double* dst = LT + (c * 32 + lane) * NOP;
 #pragma unroll
-            for (int i = 0; i < NO; ++i)
-              if (i < n) LT[jj * NOP + i] = acc[i][c];
+            for (int i = 0; i < NOP; i += 2)
+              *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i][c], (i + 1 < NO) ? acc[i + 1][c] : 0.0);
+          }
+          __syncwarp();
         }
-        __syncwarp();
+      } else {
+        // frozen first layer: only the n state columns survive -- a tiny GEMM
+        // (n_o x width) . (width x n); lane p owns outputs p and p + 32 of the
+        // n_o x n grid, each a sequential k chain as the reference's.
+        const int npair = n * n;
+        const int p0 = lane, p1 = lane + 32;
+        const int i0 = p0 / n, j0 = p0 % n, i1 = p1 / n, j1 = p1 % n;
+        double a0 = 0.0, a1 = 0.0;
+        for (int r0 = 0; r0 < width; r0 += rpc) {
+          const double* ch = ws_in.acquire();
+          const int nr = min(rpc, width - r0);
+          if (!done) {
+            if (p0 < npair) {
+#pragma unroll 4
+              for (int r = 0; r < nr; ++r) a0 = add(a0, mul(LT[(r0 + r) * NOP + i0], ch[r * ld + j0]));
+            }
+            if (p1 < npair) {
+#pragma unroll 4
+              for (int r = 0; r < nr; ++r) a1 = add(a1, mul(LT[(r0 + r) * NOP + i1], ch[r * ld + j1]));
+            }
+          }
+          ws_in.release(lane);
+        }
+        if (!done) {
+          __syncwarp();
+          if (p0 < npair) LT[j0 * NOP + i0] = a0;
+          if (p1 < npair) LT[j1 * NOP + i1] = a1;
+          __syncwarp();
+        }
       }
     }
     if (done) continue;  // keep draining the weight stream in lockstep
@@ -552,7 +604,7 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
 
     // ---- fold_overflow (flowpipe_ct.hpp:317-350), warp-parallel
     while (nq > cap) {
-      double* M = LT;           // [n][2n] augmented [G0 | a]
+      double* M = LT;              // [n][2n] augmented [G0 | a]
       double* X = LT + 2 * n * n;  // [n][n]
       double* E = X + n * n;       // [n][n]
       double* rr = E + n * n;      // [n]
@@ -597,8 +649,7 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
       bool folded = false;
       double* newest = stA + n * nq;  // column offset of the newest block
       if (ok) {
-        // back substitution, lane j owns RHS column j
-        if (lane < n) {
+        if (lane < n) {  // back substitution, lane j owns RHS column j
           for (int i = n - 1; i >= 0; --i) {
             double a = M[i * n2 + n + lane];
             for (int kk = i + 1; kk < n; ++kk) a = sub(a, mul(M[i * n2 + kk], X[kk * n + lane]));
@@ -627,8 +678,6 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
           if (lane < n) {
             const double sc = add(1.0, rr[lane]);
             for (int i = 0; i < n; ++i) stA[i * nzs + lane] = mul(stA[i * nzs + lane], sc);
-          }
-          if (lane < n) {
             double s = 0.0;
             for (int j = 0; j < n; ++j) s = add(s, fabs(E[lane * n + j]));
             newest[lane * nzs + lane] = add(newest[lane * nzs + lane], mul(s, 1.0 + 1e-12));
@@ -698,9 +747,9 @@ __global__ void __launch_bounds__(288, 1) dt_horizon_kernel(const DTParams P) {
   } else if (lane == 0) {
     atomicMin(P.hull_nboxes, nboxes);
     if (status != ST_OK) {
-      const unsigned long long key = (static_cast<unsigned long long>(failed_step >= 0 ? failed_step : nboxes) << 40) |
-                                     (static_cast<unsigned long long>(P.part_begin + b) << 8) |
-                                     static_cast<unsigned long long>(status & 0xff);
+      const unsigned long long key =
+          (static_cast<unsigned long long>(failed_step >= 0 ? failed_step : nboxes) << 40) |
+          (static_cast<unsigned long long>(P.part_begin + b) << 8) | static_cast<unsigned long long>(status & 0xff);
       atomicMin(P.hull_fail_key, key);
     }
   }

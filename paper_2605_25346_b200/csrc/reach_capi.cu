@@ -38,6 +38,8 @@ struct reach_net {
   rb::DevNet dev{};
   double* blob = nullptr;
   int L = 0;
+  int cpl = 0;  // hidden units per lane of the kernel family (0 = unsupported width)
+  int hp = 0;   // padded hidden width 32 * cpl
   std::vector<int> dims, acts;
 };
 
@@ -105,21 +107,17 @@ struct DTLayout {
 constexpr int kStageDoubles = 2048;  // 16 KB bulk-copy stages
 constexpr int kNStage = 3;
 
+int cpl_for(int maxh) { return maxh <= 32 ? 1 : maxh <= 64 ? 2 : maxh <= 96 ? 3 : maxh <= 128 ? 4 : maxh <= 256 ? 8 : 0; }
+
 int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::DTParams& P, DTLayout& lay) {
   const int L = net->L;
   const int cap = window > 0 ? window : 1;
-  int maxh = 0;
-  for (int l = 0; l + 1 < L; ++l) maxh = std::max(maxh, net->dims[l + 1]);
   const int no = n <= 2 ? 2 : n <= 4 ? 4 : n <= 6 ? 6 : n <= 8 ? 8 : 0;
   if (no == 0) return fail(ctx, REACH_E_UNSUPPORTED, "state dim > 8 not in this kernel family");
-  const int cpl = maxh <= 32 ? 1 : maxh <= 64 ? 2 : maxh <= 96 ? 3 : maxh <= 128 ? 4 : maxh <= 256 ? 8 : 0;
-  if (cpl == 0) return fail(ctx, REACH_E_UNSUPPORTED, "hidden width > 256 not in this kernel family");
+  if (net->cpl == 0) return fail(ctx, REACH_E_UNSUPPORTED, "hidden width > 256 not in this kernel family");
+  const int hp = net->hp;
   const int nzs = n * (cap + 2);
   if (nzs > 64) return fail(ctx, REACH_E_UNSUPPORTED, "n * (window + 2) > 64 not in this kernel family");
-  if (2 * n > 32) return fail(ctx, REACH_E_UNSUPPORTED, "state dim too large for warp fold");
-  for (int l = 0; l < L; ++l)
-    if (net->dims[l] + 2 > kStageDoubles || net->dims[l + 1] + 2 > kStageDoubles)
-      return fail(ctx, REACH_E_UNSUPPORTED, "layer too wide for the weight stage");
   const int nop = (no + 1) & ~1;
   auto ev = [](int x) { return (x + 1) & ~1; };
   int off = 0;
@@ -128,33 +126,54 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::
   P.o_c = off;
   off += ev(n);
   P.o_pre = off;
-  int pacc = 0;
-  for (int l = 0; l + 1 < L; ++l) {
-    P.pre_off[l] = pacc;
-    pacc += 2 * net->dims[l + 1];
-  }
-  off += ev(pacc);
-  const int hw = std::max(n, maxh);
+  off += (L - 1) * 2 * hp;
   P.o_h = off;
-  off += ev(2 * hw);
+  off += 2 * hp;
   P.o_LT = off;
-  off += ev(std::max(nop * std::max(hw, n + m), 4 * n * n + n));
+  off += ev(std::max(nop * std::max(hp, n + m), 4 * n * n + n));
   P.o_R = off;
-  off += ev(3 * std::max(maxh, 1));
+  off += 3 * hp;
   P.o_bf0 = off;
-  off += ev(std::max(L > 1 ? net->dims[1] : n, n));
+  off += std::max(hp, ev(n));
   P.warp_doubles = ev(off);
   P.nzs = nzs;
+  P.hp = hp;
+  int boff = 0;
+  for (int l = 0; l < L; ++l) {
+    P.bias_s_off[l] = boff;
+    boff += (l + 1 < L) ? hp : ev(net->dims[l + 1]);
+  }
+  P.bias_doubles = ev(boff);
   P.stage_doubles = kStageDoubles;
   P.nstage = kNStage;
-  const size_t fixed = 128 + static_cast<size_t>(kNStage) * kStageDoubles * 8;
+  // weight-stream chunk table of one DT step (consumption order of the kernel)
+  const rb::DevNet& d = net->dev;
+  int nc = 0;
+  auto add_matrix = [&](long long moff, int rows, int ld) -> bool {
+    if (ld > kStageDoubles) return false;
+    const int rpc = std::max(1, kStageDoubles / ld);
+    for (int r0 = 0; r0 < rows; r0 += rpc) {
+      if (nc >= rb::kMaxChunks) return false;
+      const int nr = std::min(rpc, rows - r0);
+      P.ch_off[nc] = moff + static_cast<long long>(r0) * ld;
+      P.ch_bytes[nc] = static_cast<unsigned>(nr) * ld * 8u;
+      ++nc;
+    }
+    return true;
+  };
+  bool ok = true;
+  for (int l = 0; l + 1 < L; ++l) ok = ok && add_matrix(d.wt_off[l], d.dims[l], d.ldt[l]);
+  for (int l = L - 1; l >= 0; --l) ok = ok && add_matrix(d.w_off[l], d.dims[l + 1], d.ldw[l]);
+  if (!ok) return fail(ctx, REACH_E_UNSUPPORTED, "network too large for the weight stream");
+  P.n_chunks_step = nc;
+  const size_t fixed = 128 + static_cast<size_t>(kNStage) * kStageDoubles * 8 + static_cast<size_t>(P.bias_doubles) * 8;
   const size_t per = static_cast<size_t>(P.warp_doubles) * 8;
   int spc = static_cast<int>((static_cast<size_t>(ctx->max_smem) - fixed) / per);
-  spc = std::min(spc, 8);
+  spc = std::min(spc, rb::kSampleWarps);
   if (spc < 1) return fail(ctx, REACH_E_UNSUPPORTED, "per-sample working set exceeds shared memory");
   lay.spc = spc;
   lay.no = no;
-  lay.cpl = cpl;
+  lay.cpl = net->cpl;
   lay.smem = fixed + per * spc;
   return REACH_OK;
 }
@@ -165,7 +184,7 @@ cudaError_t launch_dt_t(const rb::DTParams& P, const DTLayout& lay, long long B,
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lay.smem));
   if (e != cudaSuccess) return e;
   const long long grid = (B + lay.spc - 1) / lay.spc;
-  k<<<static_cast<unsigned>(grid), 32 * (lay.spc + 1), lay.smem, s>>>(P);
+  k<<<static_cast<unsigned>(grid), 32 * lay.spc, lay.smem, s>>>(P);
   return cudaGetLastError();
 }
 
@@ -334,18 +353,27 @@ int reach_net_upload(reach_ctx* ctx, const reach_net_desc* d, reach_net** out) {
   net->L = d->n_layers;
   net->dims.assign(d->dims, d->dims + d->n_layers + 1);
   net->acts.assign(d->acts, d->acts + d->n_layers);
-  // host blob: per layer W (rows x ldw), W^T (cols x ldt), b -- 16-byte rows
+  // host blob, laid out for the kernels: per layer W (rows x ldw) and W^T
+  // (cols x ldt), zero-padded so that hidden layers span the padded width
+  // hp = 32 * cpl (no per-column guards in the kernels), biases padded to 32.
+  int maxh = 0;
+  for (int l = 0; l + 1 < d->n_layers; ++l) maxh = std::max(maxh, d->dims[l + 1]);
+  net->cpl = cpl_for(maxh);
+  net->hp = 32 * std::max(net->cpl, 1);
+  const int hp = net->hp;
+  const int L = d->n_layers;
   std::vector<double> blob;
   auto ev = [](int x) { return (x + 1) & ~1; };
+  auto r32 = [](int x) { return (x + 31) / 32 * 32; };
   size_t src = 0;
   rb::DevNet& dn = net->dev;
-  dn.L = d->n_layers;
-  for (int l = 0; l <= d->n_layers; ++l) dn.dims[l] = d->dims[l];
-  for (int l = 0; l < d->n_layers; ++l) {
+  dn.L = L;
+  for (int l = 0; l <= L; ++l) dn.dims[l] = d->dims[l];
+  for (int l = 0; l < L; ++l) {
     const int rows = d->dims[l + 1], cols = d->dims[l];
     dn.acts[l] = d->acts[l];
-    dn.ldw[l] = ev(cols);
-    dn.ldt[l] = ev(rows);
+    dn.ldw[l] = (l >= 1) ? std::max(r32(cols), hp) : ev(cols);
+    dn.ldt[l] = (l + 1 < L) ? std::max(r32(rows), hp) : ev(rows);
     const double* w = d->params + src;
     const double* b = w + static_cast<size_t>(rows) * cols;
     src += static_cast<size_t>(rows) * cols + rows;
@@ -358,7 +386,7 @@ int reach_net_upload(reach_ctx* ctx, const reach_net_desc* d, reach_net** out) {
     for (int i = 0; i < rows; ++i)
       for (int j = 0; j < cols; ++j) blob[dn.wt_off[l] + static_cast<size_t>(j) * dn.ldt[l] + i] = w[static_cast<size_t>(i) * cols + j];
     dn.b_off[l] = static_cast<long long>(blob.size());
-    blob.resize(blob.size() + ev(rows), 0.0);
+    blob.resize(blob.size() + std::max(r32(rows), hp), 0.0);
     for (int i = 0; i < rows; ++i) blob[dn.b_off[l] + i] = b[i];
   }
   cudaError_t e = cudaMalloc(&net->blob, blob.size() * sizeof(double));
