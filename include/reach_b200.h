@@ -140,6 +140,12 @@ int reach_ctx_kernel_time(reach_ctx* ctx, double* total_ms, int64_t* launches);
  * DMUL+DADD mix the exact kernels issue (1 flop/instr).  Roofline denominators. */
 int reach_measure_fp64_peak(reach_ctx* ctx, double* tflops_fma, double* tflops_muladd);
 
+/* Profiling builds only (-DRB_PHASE_TIMING, libreach_b200_phase.so): clock64
+ * cycles per DT-kernel phase summed over warps since the last call
+ * (prepend, IBP, backward init, chains, GEMM, first-layer GEMM, tail, fold,
+ * box, drain).  The product build returns REACH_E_UNSUPPORTED. */
+int reach_debug_phase_cycles(reach_ctx* ctx, uint64_t* out, int32_t count);
+
 /* Uploads an immutable network (SPEC: nets are values). */
 int reach_net_upload(reach_ctx* ctx, const reach_net_desc* desc, reach_net** out);
 int reach_net_free(reach_ctx* ctx, reach_net* net);

@@ -12,7 +12,8 @@ import threading
 
 from . import _abi as A
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libreach_b200.so")
+LIB_PATH = os.environ.get("REACH_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                            "libreach_b200.so")
 
 _lib = None
 _lock = threading.Lock()
@@ -46,6 +47,8 @@ def _declare(lib):
     lib.reach_ctx_enable_kernel_timing.argtypes = [vp, C.c_int32]
     lib.reach_ctx_kernel_time.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     lib.reach_measure_fp64_peak.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    lib.reach_debug_phase_cycles.argtypes = [vp, C.POINTER(C.c_uint64), C.c_int32]
+    lib.reach_debug_phase_cycles.restype = C.c_int
     for f in ("reach_ctx_create", "reach_ctx_destroy", "reach_ctx_set_stream", "reach_ctx_synchronize",
               "reach_net_upload", "reach_net_free", "reach_dt_batch", "reach_split_hull",
               "reach_ctx_enable_kernel_timing", "reach_ctx_kernel_time", "reach_measure_fp64_peak"):
@@ -111,6 +114,12 @@ class Context:
         a, b = C.c_double(), C.c_double()
         self.check(self._lib.reach_measure_fp64_peak(self.handle, C.byref(a), C.byref(b)), "fp64_peak")
         return a.value, b.value
+
+    def phase_cycles(self):
+        """Per-phase cycles of the DT kernel (profiling build only), else None."""
+        arr = (C.c_uint64 * 10)()
+        rc = self._lib.reach_debug_phase_cycles(self.handle, arr, 10)
+        return list(arr) if rc == A.REACH_OK else None
 
     def upload(self, net) -> "C.c_void_p":
         """Device handle of `net` (cached by content: nets are values, SPEC.md)."""

@@ -72,7 +72,8 @@ struct DTParams {
   unsigned long long* hull_fail_key;  // [1]
   // shared-memory layout (doubles)
   int stage_doubles, nstage, warp_doubles, bias_doubles;
-  int o_stA, o_c, o_pre, o_h, o_LT, o_R, o_bf0;
+  int o_stA, o_c, o_pre, o_LT, o_R, o_bf0, o_idx;  // hb aliases LT; R only for tanh nets
+  int has_tanh;
   int nzs;                      // stA row stride (n * (cap + 2))
   int hp;                       // padded hidden width (32 * CPL)
   int bias_s_off[kMaxLayers];   // per-layer bias offsets in the CTA bias copy
@@ -192,9 +193,51 @@ __device__ __forceinline__ void split_edges(const DTParams& P, long long p, int 
 
 
 // ---------------------------------------------------------------------------
+// Optional phase timing (build with -DRB_PHASE_TIMING): clock64 cycles per
+// kernel phase, summed over warps, read back with reach_debug_phase_cycles.
+#ifdef RB_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[16];
+#define RB_PH(i)                               \
+  do {                                         \
+    const long long now_ = clock64();          \
+    ph_acc[ph_cur] += now_ - ph_last;          \
+    ph_last = now_;                            \
+    ph_cur = (i);                              \
+  } while (0)
+#else
+#define RB_PH(i) \
+  do {           \
+  } while (0)
+#endif
+enum { PH_PREP = 0, PH_IBP = 1, PH_BINIT = 2, PH_CHAIN = 3, PH_GEMM = 4, PH_GEMM0 = 5, PH_TAIL = 6, PH_FOLD = 7,
+       PH_BOX = 8, PH_DRAIN = 9 };
+
+// Builds, in ascending order, the list of units o < width with flag set.
+template <int CPL>
+__device__ __forceinline__ int compact(const bool (&flag)[CPL], int width, int lane, unsigned char* list) {
+  int base = 0;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const bool f = flag[c] && (c * 32 + lane < width);
+    const unsigned msk = __ballot_sync(0xffffffffu, f);
+    if (f) list[base + __popc(msk & ((1u << lane) - 1u))] = static_cast<unsigned char>(c * 32 + lane);
+    base += __popc(msk);
+  }
+  return base;
+}
+
+// ---------------------------------------------------------------------------
 // The kernel.  NO: max state dim (= network output dim) of this family;
 // CPL: hidden units per lane (padded hidden width HP = 32 * CPL).
-// Block = kSampleWarps warps, one sample per warp.
+// Block = up to kSampleWarps warps, one sample per warp.
+//
+// ReLU sparsity: a stably inactive unit (u <= 0) has post-activation [0,0]
+// and slope 0, so every product it feeds -- its IBP input rows, its
+// Lambda.W rows, its shift and intercept terms -- is exactly +-0, and adding
+// +-0 never changes a non-zero sum.  Those units are skipped through per-layer
+// compacted index lists; results are identical to the dense reference up to
+// the sign of an exactly-zero entry.  Intercept chains run over the unstable
+// units only (li = ui = 0 for stable ReLU units, li = 0 always for ReLU).
 constexpr int kSampleWarps = 8;
 
 template <int NO, int CPL>
@@ -206,6 +249,11 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
   const int spc = blockDim.x / 32;
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+#ifdef RB_PHASE_TIMING
+  long long ph_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_last = clock64();
+  int ph_cur = PH_PREP;
+#endif
 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   int* cnt = reinterpret_cast<int*>(smem_raw + 64);
@@ -228,8 +276,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
     }
     fence_mbar_init();
   }
-  // CTA copy of every layer's (padded) bias
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < L; ++l) {  // CTA copy of every layer's (padded) bias
     const int cnt_b = (l + 1 < L) ? HP : ((N.dims[l + 1] + 1) & ~1);
     for (int i = threadIdx.x; i < cnt_b; i += blockDim.x) bias_s[P.bias_s_off[l] + i] = blob[N.b_off[l] + i];
   }
@@ -243,11 +290,13 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
   double* ws = wbase + static_cast<size_t>(warp) * P.warp_doubles;
   double* stA = ws + P.o_stA;  // n x nzs: [G0 | Q1 .. Qnq | (fresh)]
   double* cc = ws + P.o_c;     // n
-  double* pre = ws + P.o_pre;  // per hidden layer: (lo,hi) per padded unit
-  double* hb = ws + P.o_h;     // IBP layer input (lo,hi) per unit
+  double* pre = ws + P.o_pre;  // per hidden layer, per padded unit: (lo,hi) -> after relax (s, ui) [ReLU]
   double* LT = ws + P.o_LT;    // Lambda^T: [col][NOP]
-  double* R = ws + P.o_R;      // relaxation (s, li, ui) per unit
+  double* hb = LT;             // IBP layer input (lo,hi) per unit -- forward pass only
+  double* R = ws + P.o_R;      // tanh relaxation (s, li, ui) per unit
   double* bf0 = ws + P.o_bf0;  // frozen first-layer bias (actions differ per sample)
+  unsigned char* lists = reinterpret_cast<unsigned char*>(ws + P.o_idx);  // [L-1][2][HP]
+  int* lcnt = reinterpret_cast<int*>(lists + (L - 1) * 2 * HP);           // [L-1][2]
   const int nzs = P.nzs;
 
   const double* act_base = P.actions;
@@ -294,9 +343,11 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
   bool done = !valid;
 
   for (int k = 0; k < H; ++k) {
+    RB_PH(PH_PREP);
     const double* u = act_base + static_cast<size_t>(k) * m;
     const int nz = n * (1 + nq);
     bool preact_bad = false;
+    bool lam_bad = false;  // a non-finite Lambda entry: the dense reference turns it into a NaN shift
 
     // ---- prepend layer IBP (neural.hpp:360-373 + interval.hpp:284-295):
     // pre0_i = sum_j iv_scale(A_ij, [-1,1]) (+ the [0,0] remainder block) + c_i
@@ -314,13 +365,17 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
     __syncwarp();
 
     // ---- IBP through the hidden layers (neural.hpp:243-257); output layer skipped
+    RB_PH(PH_IBP);
     for (int l = 0; l + 1 < L; ++l) {
       const int width = N.dims[l + 1];
-      const int nin = (l == 0) ? n : N.dims[l];  // frozen first layer: x columns only
       const int rows = N.dims[l];
       const int ld = N.ldt[l];
       const int act = N.acts[l];
       const double* bias = bias_s + P.bias_s_off[l];
+      // input rows that carry non-zero intervals: all n state rows for l = 0,
+      // the active list of layer l-1 otherwise
+      const unsigned char* in_list = (l > 0) ? lists + (l - 1) * 2 * HP : nullptr;
+      const int in_cnt = (l > 0) ? lcnt[(l - 1) * 2] : n;
       double alo[CPL], ahi[CPL], bfold[CPL];
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
@@ -329,15 +384,21 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
         bfold[c] = bias[c * 32 + lane];
       }
       const int rpc = rows_per_chunk(ld, P.stage_doubles);
+      int t = 0;
       for (int r0 = 0; r0 < rows; r0 += rpc) {
         const double* ch = ws_in.acquire();
         const int nr = min(rpc, rows - r0);
         if (!done) {
-          const int nx = max(0, min(nr, nin - r0));  // rows of this chunk that are x columns
-#pragma unroll 2
-          for (int r = 0; r < nx; ++r) {
-            const double* wrow = ch + r * ld + lane;
-            const double2 x = *reinterpret_cast<const double2*>(hb + 2 * (r0 + r));
+          int tend = t;
+          if (l > 0) {
+            while (tend < in_cnt && in_list[tend] < r0 + nr) ++tend;
+          } else {
+            tend = min(in_cnt, r0 + nr);
+          }
+          for (; t < tend; ++t) {
+            const int j = (l > 0) ? in_list[t] : t;
+            const double* wrow = ch + (j - r0) * ld + lane;
+            const double2 x = *reinterpret_cast<const double2*>(hb + 2 * j);
             double w[CPL], tl[CPL], th[CPL];
 #pragma unroll
             for (int c = 0; c < CPL; ++c) w[c] = wrow[c * 32];
@@ -353,28 +414,36 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
               ahi[c] = add(ahi[c], th[c]);
             }
           }
-          for (int r = nx; r < nr; ++r) {  // freeze_trailing_inputs (neural.hpp:410): b += W[:, n+j] u_j
-            const double uj = u[r0 + r - n];
-            const double* wrow = ch + r * ld + lane;
+          if (l == 0) {  // freeze_trailing_inputs (neural.hpp:410): b += W[:, n+j] u_j
+            for (int r = max(n - r0, 0); r < nr; ++r) {
+              const double uj = u[r0 + r - n];
+              const double* wrow = ch + r * ld + lane;
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) bfold[c] = add(bfold[c], mul(wrow[c * 32], uj));
+              for (int c = 0; c < CPL; ++c) bfold[c] = add(bfold[c], mul(wrow[c * 32], uj));
+            }
           }
         }
         ws_in.release(lane);
       }
       if (!done) {
         double* pl = pre + l * 2 * HP;
+        bool nz_flag[CPL], unst[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const int o = c * 32 + lane;
           const double plo = add(alo[c], bfold[c]);
           const double phi = add(ahi[c], bfold[c]);
           *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(plo, phi);
-          if (l == 0) bf0[o] = bfold[c];
+          if (l == 0 && m > 0) bf0[o] = bfold[c];
           if (o < width && act != 2 && !(finite(plo) && finite(phi))) preact_bad = true;
+          // ReLU: inactive iff hi <= 0; unstable iff lo < 0 < hi.  Other acts: dense.
+          nz_flag[c] = (act != 0) || !(phi <= 0.0);
+          unst[c] = (act != 0) || (plo < 0.0 && phi > 0.0) || !(finite(plo) && finite(phi));
           alo[c] = act_apply(act, plo);
           ahi[c] = act_apply(act, phi);
         }
+        lcnt[l * 2] = compact<CPL>(nz_flag, width, lane, lists + l * 2 * HP);
+        lcnt[l * 2 + 1] = compact<CPL>(unst, width, lane, lists + l * 2 * HP + HP);
         __syncwarp();  // every lane is done reading hb
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
@@ -386,6 +455,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
 
     // ---- CROWN backward (neural.hpp:297-327)
     // init: Lambda = I . W_{L-1} = W_{L-1};  b = 0 + I . b_{L-1}
+    RB_PH(PH_BINIT);
     double blo = 0.0, bup = 0.0;
     {
       const int l = L - 1;
@@ -417,69 +487,108 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
       __syncwarp();
     }
     for (int l = L - 2; l >= 0; --l) {
-      const int width = N.dims[l + 1];  // Lambda columns on entry
       const int act = N.acts[l];
       const double* bvec = (l == 0 && m > 0) ? bf0 : bias_s + P.bias_s_off[l];
+      const unsigned char* alist = lists + l * 2 * HP;
+      const unsigned char* ulist = alist + HP;
+      const int acnt = lcnt[l * 2], ucnt = lcnt[l * 2 + 1];
+      double* pl = pre + l * 2 * HP;
       // relaxation (parallel), then the intercept / shift chains (lane i owns row i)
+      RB_PH(PH_CHAIN);
       if (!done) {
-        if (act != 2) {
-          const double* pl = pre + l * 2 * HP;
+        if (act == 0) {
+          // ReLU: (s, ui) overwrite the preactivation slots of the listed units; li = 0
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
             const int o = c * 32 + lane;
             const double2 p = *reinterpret_cast<const double2*>(pl + 2 * o);
             double s, li, ui;
-            relax(act, p.x, p.y, s, li, ui);
-            R[3 * o] = s;
-            R[3 * o + 1] = li;
-            R[3 * o + 2] = ui;
+            relax(0, p.x, p.y, s, li, ui);
+            *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(s, ui);
           }
           __syncwarp();
-        }
-        if (lane < n) {
-          double shift = 0.0;
-          if (act != 2) {
-#pragma unroll 4
-            for (int j = 0; j < width; ++j) {
+          if (lane < n) {
+            // intercept chains: only unstable units have a non-zero intercept (ui; li = 0)
+            for (int t = 0; t < ucnt; ++t) {
+              const int j = ulist[t];
               const double a = LT[j * NOP + lane];
-              const double s = R[3 * j], li = R[3 * j + 1], ui = R[3 * j + 2];
-              const double bj = bvec[j];
-              const bool pos = a >= 0.0;
-              const double pl = mul(a, pos ? li : ui);
-              const double pu = mul(a, pos ? ui : li);
-              const double as = mul(a, s);
-              const double ps = mul(as, bj);
-              LT[j * NOP + lane] = as;
-              blo = add(blo, pl);
-              bup = add(bup, pu);
-              shift = add(shift, ps);
+              const double ui = pl[2 * j + 1];
+              if (a >= 0.0) bup = add(bup, mul(a, ui));
+              else blo = add(blo, mul(a, ui));
             }
-          } else {
+            // scaling + shift chain over units with a non-zero slope
+            double shift = 0.0;
 #pragma unroll 4
-            for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
+            for (int t = 0; t < acnt; ++t) {
+              const int j = alist[t];
+              const double as = mul(LT[j * NOP + lane], pl[2 * j]);
+              LT[j * NOP + lane] = as;
+              shift = add(shift, mul(as, bvec[j]));
+            }
+            blo = add(blo, shift);
+            bup = add(bup, shift);
           }
-          blo = add(blo, shift);
-          bup = add(bup, shift);
+        } else {
+          const int width = N.dims[l + 1];
+          if (act == 1) {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+              const int o = c * 32 + lane;
+              const double2 p = *reinterpret_cast<const double2*>(pl + 2 * o);
+              double s, li, ui;
+              relax(1, p.x, p.y, s, li, ui);
+              R[3 * o] = s;
+              R[3 * o + 1] = li;
+              R[3 * o + 2] = ui;
+            }
+            __syncwarp();
+          }
+          if (lane < n) {
+            double shift = 0.0;
+            if (act == 1) {
+              for (int j = 0; j < width; ++j) {
+                const double a = LT[j * NOP + lane];
+                const double s = R[3 * j], li = R[3 * j + 1], ui = R[3 * j + 2];
+                const bool pos = a >= 0.0;
+                blo = add(blo, mul(a, pos ? li : ui));
+                bup = add(bup, mul(a, pos ? ui : li));
+                const double as = mul(a, s);
+                LT[j * NOP + lane] = as;
+                shift = add(shift, mul(as, bvec[j]));
+              }
+            } else {
+              for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
+            }
+            blo = add(blo, shift);
+            bup = add(bup, shift);
+          }
         }
         __syncwarp();
       }
-      // dense contraction Lambda <- Lambda . W_l  (linalg.hpp:53-63, i-k-j order)
+      // dense contraction Lambda <- Lambda . W_l  (linalg.hpp:53-63, i-k-j order), rows k
+      // over the units with a non-zero slope
+      const int width = N.dims[l + 1];
       const int ld = N.ldw[l];
       const int rpc = rows_per_chunk(ld, P.stage_doubles);
       if (l > 0) {
+        RB_PH(PH_GEMM);
         double acc[NO][CPL];
 #pragma unroll
         for (int i = 0; i < NO; ++i)
 #pragma unroll
           for (int c = 0; c < CPL; ++c) acc[i][c] = 0.0;
+        int t = 0;
         for (int r0 = 0; r0 < width; r0 += rpc) {
           const double* ch = ws_in.acquire();
           const int nr = min(rpc, width - r0);
           if (!done) {
+            int tend = t;
+            while (tend < acnt && alist[tend] < r0 + nr) ++tend;
 #pragma unroll 2
-            for (int r = 0; r < nr; ++r) {
-              const double* lrow = LT + (r0 + r) * NOP;
-              const double* wrow = ch + r * ld + lane;
+            for (; t < tend; ++t) {
+              const int kk = alist[t];
+              const double* lrow = LT + kk * NOP;
+              const double* wrow = ch + (kk - r0) * ld + lane;
               double lam[NOP], w[CPL];
 #pragma unroll
               for (int i = 0; i < NOP; i += 2) {
@@ -489,20 +598,26 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
               }
 #pragma unroll
               for (int c = 0; c < CPL; ++c) w[c] = wrow[c * 32];
-              double t[NO][CPL];
+              double tt[NO][CPL];
 #pragma unroll
               for (int i = 0; i < NO; ++i)
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) t[i][c] = mul(lam[i], w[c]);
+                for (int c = 0; c < CPL; ++c) tt[i][c] = mul(lam[i], w[c]);
 #pragma unroll
               for (int i = 0; i < NO; ++i)
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) acc[i][c] = add(acc[i][c], t[i][c]);
+                for (int c = 0; c < CPL; ++c) acc[i][c] = add(acc[i][c], tt[i][c]);
             }
           }
           ws_in.release(lane);
         }
         if (!done) {
+          const int ncols = N.dims[l];
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+              if (i < n && c * 32 + lane < ncols && !finite(acc[i][c])) lam_bad = true;
           __syncwarp();
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
@@ -517,26 +632,37 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
         // frozen first layer: only the n state columns survive -- a tiny GEMM
         // (n_o x width) . (width x n); lane p owns outputs p and p + 32 of the
         // n_o x n grid, each a sequential k chain as the reference's.
+        RB_PH(PH_GEMM0);
         const int npair = n * n;
         const int p0 = lane, p1 = lane + 32;
         const int i0 = p0 / n, j0 = p0 % n, i1 = p1 / n, j1 = p1 % n;
         double a0 = 0.0, a1 = 0.0;
+        int t = 0;
         for (int r0 = 0; r0 < width; r0 += rpc) {
           const double* ch = ws_in.acquire();
           const int nr = min(rpc, width - r0);
           if (!done) {
+            int tend = t;
+            while (tend < acnt && alist[tend] < r0 + nr) ++tend;
             if (p0 < npair) {
 #pragma unroll 4
-              for (int r = 0; r < nr; ++r) a0 = add(a0, mul(LT[(r0 + r) * NOP + i0], ch[r * ld + j0]));
+              for (int q = t; q < tend; ++q) {
+                const int kk = alist[q];
+                a0 = add(a0, mul(LT[kk * NOP + i0], ch[(kk - r0) * ld + j0]));
+              }
             }
             if (p1 < npair) {
-#pragma unroll 4
-              for (int r = 0; r < nr; ++r) a1 = add(a1, mul(LT[(r0 + r) * NOP + i1], ch[r * ld + j1]));
+              for (int q = t; q < tend; ++q) {
+                const int kk = alist[q];
+                a1 = add(a1, mul(LT[kk * NOP + i1], ch[(kk - r0) * ld + j1]));
+              }
             }
+            t = tend;
           }
           ws_in.release(lane);
         }
         if (!done) {
+          if ((p0 < npair && !finite(a0)) || (p1 < npair && !finite(a1))) lam_bad = true;
           __syncwarp();
           if (p0 < npair) LT[j0 * NOP + i0] = a0;
           if (p1 < npair) LT[j1 * NOP + i1] = a1;
@@ -544,6 +670,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
         }
       }
     }
+    RB_PH(PH_TAIL);
     if (done) continue;  // keep draining the weight stream in lockstep
 
     // ---- prepended layer W = [A | I], b = c: shift chain and A_out = Lambda . A
@@ -577,7 +704,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
       rh = sub(bup, mid);
       rem_ok = finite(rl) && finite(rh);
     }
-    rem_ok = __all_sync(0xffffffffu, rem_ok);
+    rem_ok = __all_sync(0xffffffffu, rem_ok && !lam_bad);
     if (preact_bad || !rem_ok) {
       status = preact_bad ? ST_PREACT : ST_CERT;
       failed_step = k;
@@ -603,6 +730,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
     __syncwarp();
 
     // ---- fold_overflow (flowpipe_ct.hpp:317-350), warp-parallel
+    RB_PH(PH_FOLD);
     while (nq > cap) {
       double* M = LT;              // [n][2n] augmented [G0 | a]
       double* X = LT + 2 * n * n;  // [n][n]
@@ -706,6 +834,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
     }
 
     // ---- symbolic_box (flowpipe_ct.hpp:413-424)
+    RB_PH(PH_BOX);
     double lo = 0.0, hi = 0.0;
     bool fin = true;
     if (lane < n) {
@@ -736,6 +865,12 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
       nq = 0;
     }
   }
+  RB_PH(PH_DRAIN);
+#ifdef RB_PHASE_TIMING
+  RB_PH(PH_DRAIN);
+  if (lane == 0)
+    for (int i = 0; i < 10; ++i) atomicAdd(&g_phase_cycles[i], static_cast<unsigned long long>(ph_acc[i]));
+#endif
 
   if (!valid) return;
   if (!P.split) {

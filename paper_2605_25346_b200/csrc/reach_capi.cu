@@ -127,14 +127,17 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::
   off += ev(n);
   P.o_pre = off;
   off += (L - 1) * 2 * hp;
-  P.o_h = off;
-  off += 2 * hp;
-  P.o_LT = off;
-  off += ev(std::max(nop * std::max(hp, n + m), 4 * n * n + n));
+  P.o_LT = off;  // also the IBP input buffer (2 hp) and the fold scratch (4 n^2 + n)
+  off += ev(std::max({nop * std::max(hp, n + m), 2 * hp, 4 * n * n + n}));
+  bool tanh_any = false;
+  for (int l = 0; l + 1 < L; ++l) tanh_any |= net->acts[l] == REACH_ACT_TANH;
+  P.has_tanh = tanh_any ? 1 : 0;
   P.o_R = off;
-  off += 3 * hp;
+  if (tanh_any) off += 3 * hp;
   P.o_bf0 = off;
-  off += std::max(hp, ev(n));
+  if (m > 0) off += std::max(hp, ev(n));
+  P.o_idx = off;  // per hidden layer two unit lists (uint8) + their counts
+  off += ((L - 1) * 2 * hp + (L - 1) * 2 * 4 + 15) / 16 * 2;
   P.warp_doubles = ev(off);
   P.nzs = nzs;
   P.hp = hp;
@@ -331,6 +334,22 @@ int reach_measure_fp64_peak(reach_ctx* ctx, double* tflops_fma, double* tflops_m
   *tflops_fma = best_fma;
   *tflops_muladd = best_ma;
   return REACH_OK;
+}
+
+int reach_debug_phase_cycles(reach_ctx* ctx, uint64_t* out, int32_t count) {
+  if (!ctx || !out || count <= 0) return REACH_E_INVALID_ARGUMENT;
+#ifdef RB_PHASE_TIMING
+  RB_CUDA(cudaSetDevice(ctx->device));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  unsigned long long tmp[16] = {0};
+  RB_CUDA(cudaMemcpyFromSymbol(tmp, rb::g_phase_cycles, sizeof(tmp)));
+  for (int i = 0; i < count && i < 16; ++i) out[i] = tmp[i];
+  unsigned long long zero[16] = {0};
+  RB_CUDA(cudaMemcpyToSymbol(rb::g_phase_cycles, zero, sizeof(zero)));
+  return REACH_OK;
+#else
+  return fail(ctx, REACH_E_UNSUPPORTED, "library built without RB_PHASE_TIMING");
+#endif
 }
 
 const char* reach_ctx_last_error(const reach_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }

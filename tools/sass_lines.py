@@ -29,7 +29,7 @@ def main():
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
     cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-    dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    dis = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
     # find function section by mangled-name match
     lines = dis.splitlines()
     cur_fn, cur_line, in_fn = None, None, False
@@ -41,7 +41,7 @@ def main():
             continue
         if not in_fn:
             continue
-        m = re.search(r"//## File \"(.*?)\", line (\d+)", ln)
+        m = re.search(r"//## File \"(.*?)\", line (\d+)$", ln.strip()) or re.search(r"inlined at \"(.*?)\", line (\d+)", ln)
         if m:
             cur_line = (os.path.basename(m.group(1)), int(m.group(2)))
             continue
