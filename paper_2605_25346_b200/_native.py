@@ -117,8 +117,8 @@ class Context:
 
     def phase_cycles(self):
         """Per-phase cycles of the DT kernel (profiling build only), else None."""
-        arr = (C.c_uint64 * 10)()
-        rc = self._lib.reach_debug_phase_cycles(self.handle, arr, 10)
+        arr = (C.c_uint64 * 11)()
+        rc = self._lib.reach_debug_phase_cycles(self.handle, arr, 11)
         return list(arr) if rc == A.REACH_OK else None
 
     def upload(self, net) -> "C.c_void_p":

@@ -43,6 +43,8 @@ struct DevNet {
 };
 
 constexpr int kMaxChunks = 96;  // weight-stream chunks per DT step
+// shared-memory header: 8 mbarriers, 16 counters, the chunk table
+constexpr int kHeaderBytes = (128 + kMaxChunks * 12 + 127) / 128 * 128;
 
 struct DTParams {
   DevNet net;
@@ -90,37 +92,59 @@ enum : int { ST_OK = 0, ST_PREACT = 1, ST_CERT = 2, ST_BOX = 3 };
 // warp to release a stage refills it with the chunk NSTAGE ahead, so no warp
 // is dedicated to producing and no warp blocks on a slow sibling to refill.
 struct WStream {
-  const DTParams* P;
   double* stages;
   uint64_t* full;
   int* cnt;
-  int spc;
+  const long long* ch_off;      // shared-memory copy of the chunk table
+  const unsigned* ch_bytes;
+  const double* blob;
+  int spc, nstage, stage_doubles, n_chunks_step;
   uint32_t g;
   uint32_t total;
+  int sidx = 0;      // g % nstage, tracked incrementally
+  uint32_t ph = 0u;  // (g / nstage) & 1
+#ifdef RB_PHASE_TIMING
+  long long wait_cycles = 0;
+#endif
   __device__ __forceinline__ void issue(uint32_t gn, int s) const {
-    const int idx = static_cast<int>(gn % static_cast<uint32_t>(P->n_chunks_step));
-    const uint32_t bytes = P->ch_bytes[idx];
+    const int idx = static_cast<int>(gn % static_cast<uint32_t>(n_chunks_step));
+    const uint32_t bytes = ch_bytes[idx];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_expect_tx(&full[s], bytes);
-    bulk_g2s(stages + static_cast<size_t>(s) * P->stage_doubles, P->net.blob + P->ch_off[idx], bytes, &full[s]);
+    bulk_g2s(stages + static_cast<size_t>(s) * stage_doubles, blob + ch_off[idx], bytes, &full[s]);
   }
-  __device__ __forceinline__ const double* acquire() const {
-    const int s = g % P->nstage;
-    mbar_wait(&full[s], (g / P->nstage) & 1u);
-    return stages + static_cast<size_t>(s) * P->stage_doubles;
+  // Waits for the current chunk; returns its stage index (the caller forms the
+  // pointer from its own shared-memory base so the address space stays known).
+  __device__ __forceinline__ int acquire() {
+#ifdef RB_PHASE_TIMING
+    const long long t0 = clock64();
+#endif
+    mbar_wait(&full[sidx], ph);
+#ifdef RB_PHASE_TIMING
+    wait_cycles += clock64() - t0;
+#endif
+    return sidx;
   }
   __device__ __forceinline__ void release(int lane) {
     __syncwarp();
     if (lane == 0) {
-      const int s = g % P->nstage;
-      __threadfence_block();
-      if (atomicAdd(&cnt[s], 1) == spc - 1) {
-        atomicExch(&cnt[s], 0);
-        const uint32_t gn = g + P->nstage;
+      const int s = sidx;
+      int old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(old)
+                   : "r"(smem_u32(&cnt[s]))
+                   : "memory");
+      if (old == spc - 1) {
+        cnt[s] = 0;
+        const uint32_t gn = g + nstage;
         if (gn < total) issue(gn, s);
       }
     }
     ++g;
+    if (++sidx == nstage) {
+      sidx = 0;
+      ph ^= 1u;
+    }
   }
 };
 
@@ -212,36 +236,116 @@ __device__ unsigned long long g_phase_cycles[16];
 enum { PH_PREP = 0, PH_IBP = 1, PH_BINIT = 2, PH_CHAIN = 3, PH_GEMM = 4, PH_GEMM0 = 5, PH_TAIL = 6, PH_FOLD = 7,
        PH_BOX = 8, PH_DRAIN = 9 };
 
-// Builds, in ascending order, the list of units o < width with flag set.
-template <int CPL>
-__device__ __forceinline__ int compact(const bool (&flag)[CPL], int width, int lane, unsigned char* list) {
-  int base = 0;
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    const bool f = flag[c] && (c * 32 + lane < width);
-    const unsigned msk = __ballot_sync(0xffffffffu, f);
-    if (f) list[base + __popc(msk & ((1u << lane) - 1u))] = static_cast<unsigned char>(c * 32 + lane);
-    base += __popc(msk);
+
+// Iterates the set bits of `mask` (CPL words, bit o = unit o) inside rows [r0, r0 + nr),
+// calling f(row) in ascending order.  The mask is per sample, so warp-uniform.
+template <typename F>
+__device__ __forceinline__ void for_each_row(const unsigned* mask, int r0, int nr, F&& f) {
+  const int r1 = r0 + nr;
+  for (int wi = r0 >> 5; wi * 32 < r1; ++wi) {
+    unsigned bits = mask[wi];
+    const int lo = wi * 32;
+    if (r0 > lo) bits &= ~0u << (r0 - lo);
+    if (r1 < lo + 32) bits &= (1u << (r1 - lo)) - 1u;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      f(lo + b);
+    }
   }
-  return base;
+}
+
+// Ascending rows of [r0, r0 + nr) whose mask bit is set (mask == nullptr: every row).
+struct RowIter {
+  const unsigned* mask;
+  int r0, r1, wi, cur;
+  unsigned bits;
+  __device__ __forceinline__ RowIter(const unsigned* m, int r0_, int nr) : mask(m), r0(r0_), r1(r0_ + nr) {
+    cur = r0_;
+    wi = (r0_ >> 5) - 1;
+    bits = 0u;
+  }
+  __device__ __forceinline__ int next() {
+    if (!mask) return cur < r1 ? cur++ : -1;
+    while (bits == 0u) {
+      ++wi;
+      if (wi * 32 >= r1) return -1;
+      unsigned b = mask[wi];
+      const int lo = wi * 32;
+      if (r0 > lo) b &= ~0u << (r0 - lo);
+      if (r1 < lo + 32) b &= (1u << (r1 - lo)) - 1u;
+      bits = b;
+    }
+    const int b = __ffs(bits) - 1;
+    bits &= bits - 1u;
+    return wi * 32 + b;
+  }
+};
+
+// Number of set bits of `mask` below bit x.
+__device__ __forceinline__ int popc_below(const unsigned* mask, int x) {
+  int c = 0;
+  const int w = x >> 5;
+  for (int i = 0; i < w; ++i) c += __popc(mask[i]);
+  if (x & 31) c += __popc(mask[w] & ((1u << (x & 31)) - 1u));
+  return c;
+}
+
+// Two-deep software pipeline over the rows of `it`: the operands of the next
+// row are loaded before the current row's arithmetic is issued, so shared-
+// memory latency hides behind the FP64 work of the previous row.
+template <class Ops, class Load, class Comp>
+__device__ __forceinline__ void pipelined_rows(RowIter& it, Load&& load, Comp&& comp) {
+#if !RB_PIPELINE
+  for (int j = it.next(); j >= 0; j = it.next()) {
+    Ops A;
+    load(j, A);
+    comp(j, A);
+  }
+  return;
+#endif
+  int ja = it.next();
+  if (ja < 0) return;
+  Ops A, B;
+  load(ja, A);
+  for (;;) {
+    const int jb = it.next();
+    if (jb >= 0) load(jb, B);
+    comp(ja, A);
+    if (jb < 0) return;
+    ja = it.next();
+    if (ja >= 0) load(ja, A);
+    comp(jb, B);
+    if (ja < 0) return;
+  }
 }
 
 // ---------------------------------------------------------------------------
 // The kernel.  NO: max state dim (= network output dim) of this family;
 // CPL: hidden units per lane (padded hidden width HP = 32 * CPL).
-// Block = up to kSampleWarps warps, one sample per warp.
+// Block = up to kSampleWarps warps, one sample per warp; two CTAs per SM so
+// the serial phases of one CTA overlap the contractions of the other.
 //
 // ReLU sparsity: a stably inactive unit (u <= 0) has post-activation [0,0]
-// and slope 0, so every product it feeds -- its IBP input rows, its
-// Lambda.W rows, its shift and intercept terms -- is exactly +-0, and adding
-// +-0 never changes a non-zero sum.  Those units are skipped through per-layer
-// compacted index lists; results are identical to the dense reference up to
-// the sign of an exactly-zero entry.  Intercept chains run over the unstable
-// units only (li = ui = 0 for stable ReLU units, li = 0 always for ReLU).
-constexpr int kSampleWarps = 8;
+// and slope 0, so every product it feeds -- its IBP input rows and its
+// Lambda.W rows -- is exactly +-0, and adding +-0 never changes a non-zero
+// sum.  Those rows are skipped through per-layer unit bitmasks; results are
+// identical to the dense reference up to the sign of an exactly-zero entry.
+// Intercept chains run over the unstable units only (ReLU: li = 0 always,
+// ui = 0 for stable units).
+#ifndef RB_SAMPLE_WARPS
+#define RB_SAMPLE_WARPS 4
+#endif
+#ifndef RB_MIN_BLOCKS
+#define RB_MIN_BLOCKS 2
+#endif
+#ifndef RB_PIPELINE
+#define RB_PIPELINE 0
+#endif
+constexpr int kSampleWarps = RB_SAMPLE_WARPS;
 
 template <int NO, int CPL>
-__global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const DTParams P) {
+__global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_kernel(const DTParams P) {
   constexpr int NOP = (NO + 1) & ~1;  // Lambda^T row stride (16-byte rows)
   constexpr int NZG = 2;              // 32-column groups of the generator matrix (nzs <= 64)
   constexpr int HP = 32 * CPL;
@@ -257,8 +361,11 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   int* cnt = reinterpret_cast<int*>(smem_raw + 64);
-  double* stages = reinterpret_cast<double*>(smem_raw + 128);
-  double* bias_s = stages + static_cast<size_t>(P.nstage) * P.stage_doubles;
+  long long* tab_off = reinterpret_cast<long long*>(smem_raw + 128);          // [kMaxChunks]
+  unsigned* tab_bytes = reinterpret_cast<unsigned*>(tab_off + kMaxChunks);   // [kMaxChunks]
+  double* stages = reinterpret_cast<double*>(smem_raw + kHeaderBytes);
+  const int SD = P.stage_doubles;
+  double* bias_s = stages + static_cast<size_t>(P.nstage) * SD;
   double* wbase = bias_s + P.bias_doubles;
 
   const DevNet& N = P.net;
@@ -268,7 +375,12 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
   const double* blob = N.blob;
   const uint32_t total_chunks = static_cast<uint32_t>(P.n_chunks_step) * static_cast<uint32_t>(H);
 
-  WStream ws_in{&P, stages, full, cnt, spc, 0u, total_chunks};
+  for (int i = threadIdx.x; i < P.n_chunks_step; i += blockDim.x) {
+    tab_off[i] = P.ch_off[i];
+    tab_bytes[i] = P.ch_bytes[i];
+  }
+  WStream ws_in{stages, full, cnt, tab_off, tab_bytes, blob, spc, P.nstage, P.stage_doubles, P.n_chunks_step,
+                0u, total_chunks};
   if (threadIdx.x == 0) {
     for (int s = 0; s < P.nstage; ++s) {
       mbar_init(&full[s], 1);
@@ -295,8 +407,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
   double* hb = LT;             // IBP layer input (lo,hi) per unit -- forward pass only
   double* R = ws + P.o_R;      // tanh relaxation (s, li, ui) per unit
   double* bf0 = ws + P.o_bf0;  // frozen first-layer bias (actions differ per sample)
-  unsigned char* lists = reinterpret_cast<unsigned char*>(ws + P.o_idx);  // [L-1][2][HP]
-  int* lcnt = reinterpret_cast<int*>(lists + (L - 1) * 2 * HP);           // [L-1][2]
+  unsigned* masks = reinterpret_cast<unsigned*>(ws + P.o_idx);  // [L-1][2][CPL]: active, unstable
+  unsigned char* alists = reinterpret_cast<unsigned char*>(masks + (L - 1) * 2 * CPL);  // [L-1][HP] active units
   const int nzs = P.nzs;
 
   const double* act_base = P.actions;
@@ -372,10 +484,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
       const int ld = N.ldt[l];
       const int act = N.acts[l];
       const double* bias = bias_s + P.bias_s_off[l];
-      // input rows that carry non-zero intervals: all n state rows for l = 0,
-      // the active list of layer l-1 otherwise
-      const unsigned char* in_list = (l > 0) ? lists + (l - 1) * 2 * HP : nullptr;
-      const int in_cnt = (l > 0) ? lcnt[(l - 1) * 2] : n;
+      const unsigned* in_mask = masks + (l - 1) * 2 * CPL;  // l >= 1: active units of layer l-1
       double alo[CPL], ahi[CPL], bfold[CPL];
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
@@ -383,38 +492,42 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
         ahi[c] = 0.0;
         bfold[c] = bias[c * 32 + lane];
       }
-      const int rpc = rows_per_chunk(ld, P.stage_doubles);
+      const unsigned char* in_list = alists + (l - 1) * HP;
+      auto ibp_row = [&](const double* ch, int r0, int j) {
+        const double* wrow = ch + (j - r0) * ld + lane;
+        const double2 x = *reinterpret_cast<const double2*>(hb + 2 * j);
+        double w[CPL], tl[CPL], th[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) w[c] = wrow[c * 32];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const bool pos = w[c] >= 0.0;
+          tl[c] = mul(w[c], pos ? x.x : x.y);
+          th[c] = mul(w[c], pos ? x.y : x.x);
+        }
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          alo[c] = add(alo[c], tl[c]);
+          ahi[c] = add(ahi[c], th[c]);
+        }
+      };
+      const int rpc = rows_per_chunk(ld, SD);
       int t = 0;
       for (int r0 = 0; r0 < rows; r0 += rpc) {
-        const double* ch = ws_in.acquire();
+        const double* ch = stages + ws_in.acquire() * SD;
         const int nr = min(rpc, rows - r0);
         if (!done) {
-          int tend = t;
           if (l > 0) {
-            while (tend < in_cnt && in_list[tend] < r0 + nr) ++tend;
+            const int t1 = popc_below(in_mask, r0 + nr);
+#pragma unroll 2
+            for (; t < t1; ++t) ibp_row(ch, r0, in_list[t]);
           } else {
-            tend = min(in_cnt, r0 + nr);
+            const int nx = min(n, r0 + nr);
+#pragma unroll 2
+            for (int j = r0; j < nx; ++j) ibp_row(ch, r0, j);
           }
-          for (; t < tend; ++t) {
-            const int j = (l > 0) ? in_list[t] : t;
-            const double* wrow = ch + (j - r0) * ld + lane;
-            const double2 x = *reinterpret_cast<const double2*>(hb + 2 * j);
-            double w[CPL], tl[CPL], th[CPL];
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) w[c] = wrow[c * 32];
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) {
-              const bool pos = w[c] >= 0.0;
-              tl[c] = mul(w[c], pos ? x.x : x.y);
-              th[c] = mul(w[c], pos ? x.y : x.x);
-            }
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) {
-              alo[c] = add(alo[c], tl[c]);
-              ahi[c] = add(ahi[c], th[c]);
-            }
-          }
-          if (l == 0) {  // freeze_trailing_inputs (neural.hpp:410): b += W[:, n+j] u_j
+          if (l == 0) {
+            // freeze_trailing_inputs (neural.hpp:410): b += W[:, n+j] u_j
             for (int r = max(n - r0, 0); r < nr; ++r) {
               const double uj = u[r0 + r - n];
               const double* wrow = ch + r * ld + lane;
@@ -427,7 +540,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
       }
       if (!done) {
         double* pl = pre + l * 2 * HP;
-        bool nz_flag[CPL], unst[CPL];
+        unsigned* am = masks + l * 2 * CPL;
+        int lbase = 0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const int o = c * 32 + lane;
@@ -435,15 +549,22 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
           const double phi = add(ahi[c], bfold[c]);
           *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(plo, phi);
           if (l == 0 && m > 0) bf0[o] = bfold[c];
-          if (o < width && act != 2 && !(finite(plo) && finite(phi))) preact_bad = true;
+          const bool fin = finite(plo) && finite(phi);
+          if (o < width && act != 2 && !fin) preact_bad = true;
           // ReLU: inactive iff hi <= 0; unstable iff lo < 0 < hi.  Other acts: dense.
-          nz_flag[c] = (act != 0) || !(phi <= 0.0);
-          unst[c] = (act != 0) || (plo < 0.0 && phi > 0.0) || !(finite(plo) && finite(phi));
+          const bool actv = (o < width) && ((act != 0) || !(phi <= 0.0));
+          const bool unst = (o < width) && ((act != 0) || (plo < 0.0 && phi > 0.0) || !fin);
+          const unsigned ma = __ballot_sync(0xffffffffu, actv);
+          const unsigned mu = __ballot_sync(0xffffffffu, unst);
+          if (lane == 0) {
+            am[c] = ma;
+            am[CPL + c] = mu;
+          }
+          if (actv) alists[l * HP + lbase + __popc(ma & ((1u << lane) - 1u))] = static_cast<unsigned char>(o);
+          lbase += __popc(ma);
           alo[c] = act_apply(act, plo);
           ahi[c] = act_apply(act, phi);
         }
-        lcnt[l * 2] = compact<CPL>(nz_flag, width, lane, lists + l * 2 * HP);
-        lcnt[l * 2 + 1] = compact<CPL>(unst, width, lane, lists + l * 2 * HP + HP);
         __syncwarp();  // every lane is done reading hb
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
@@ -464,7 +585,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
       const int ld = N.ldw[l];
       const int rpc = rows_per_chunk(ld, P.stage_doubles);
       for (int r0 = 0; r0 < rows; r0 += rpc) {
-        const double* ch = ws_in.acquire();
+        const double* ch = stages + ws_in.acquire() * SD;
         const int nr = min(rpc, rows - r0);
         if (!done) {
           for (int r = 0; r < nr; ++r) {
@@ -488,16 +609,14 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
     }
     for (int l = L - 2; l >= 0; --l) {
       const int act = N.acts[l];
+      const int width = N.dims[l + 1];
       const double* bvec = (l == 0 && m > 0) ? bf0 : bias_s + P.bias_s_off[l];
-      const unsigned char* alist = lists + l * 2 * HP;
-      const unsigned char* ulist = alist + HP;
-      const int acnt = lcnt[l * 2], ucnt = lcnt[l * 2 + 1];
+      const unsigned* am = masks + l * 2 * CPL;
       double* pl = pre + l * 2 * HP;
-      // relaxation (parallel), then the intercept / shift chains (lane i owns row i)
       RB_PH(PH_CHAIN);
       if (!done) {
         if (act == 0) {
-          // ReLU: (s, ui) overwrite the preactivation slots of the listed units; li = 0
+          // ReLU relaxation (parallel): (s, ui) overwrite the preactivation slots; li = 0
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
             const int o = c * 32 + lane;
@@ -507,29 +626,38 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
             *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(s, ui);
           }
           __syncwarp();
+          // intercept chains over the unstable units (unscaled Lambda), lane i = row i
           if (lane < n) {
-            // intercept chains: only unstable units have a non-zero intercept (ui; li = 0)
-            for (int t = 0; t < ucnt; ++t) {
-              const int j = ulist[t];
+            for_each_row(am + CPL, 0, width, [&](int j) {
               const double a = LT[j * NOP + lane];
               const double ui = pl[2 * j + 1];
               if (a >= 0.0) bup = add(bup, mul(a, ui));
               else blo = add(blo, mul(a, ui));
+            });
+          }
+          __syncwarp();
+          // slope scaling (parallel over units): Lambda(:, j) *= s_j
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const int o = c * 32 + lane;
+            const double s = pl[2 * o];
+            double* col = LT + o * NOP;
+#pragma unroll
+            for (int i = 0; i < NOP; i += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(col + i);
+              *reinterpret_cast<double2*>(col + i) = make_double2(mul(v.x, s), mul(v.y, s));
             }
-            // scaling + shift chain over units with a non-zero slope
+          }
+          __syncwarp();
+          // shift chain Lambda_s . b (dense; inactive units add +-0), lane i = row i
+          if (lane < n) {
             double shift = 0.0;
-#pragma unroll 4
-            for (int t = 0; t < acnt; ++t) {
-              const int j = alist[t];
-              const double as = mul(LT[j * NOP + lane], pl[2 * j]);
-              LT[j * NOP + lane] = as;
-              shift = add(shift, mul(as, bvec[j]));
-            }
+#pragma unroll 8
+            for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
             blo = add(blo, shift);
             bup = add(bup, shift);
           }
         } else {
-          const int width = N.dims[l + 1];
           if (act == 1) {
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
@@ -565,9 +693,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
         }
         __syncwarp();
       }
-      // dense contraction Lambda <- Lambda . W_l  (linalg.hpp:53-63, i-k-j order), rows k
-      // over the units with a non-zero slope
-      const int width = N.dims[l + 1];
+      // dense contraction Lambda <- Lambda_s . W_l  (linalg.hpp:53-63, i-k-j order) over the rows
+      // k of units with a non-zero slope
       const int ld = N.ldw[l];
       const int rpc = rows_per_chunk(ld, P.stage_doubles);
       if (l > 0) {
@@ -577,15 +704,15 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
         for (int i = 0; i < NO; ++i)
 #pragma unroll
           for (int c = 0; c < CPL; ++c) acc[i][c] = 0.0;
+        const unsigned char* alist = alists + l * HP;
         int t = 0;
         for (int r0 = 0; r0 < width; r0 += rpc) {
-          const double* ch = ws_in.acquire();
+          const double* ch = stages + ws_in.acquire() * SD;
           const int nr = min(rpc, width - r0);
           if (!done) {
-            int tend = t;
-            while (tend < acnt && alist[tend] < r0 + nr) ++tend;
+            const int t1 = popc_below(am, r0 + nr);
 #pragma unroll 2
-            for (; t < tend; ++t) {
+            for (; t < t1; ++t) {
               const int kk = alist[t];
               const double* lrow = LT + kk * NOP;
               const double* wrow = ch + (kk - r0) * ld + lane;
@@ -635,29 +762,23 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
         RB_PH(PH_GEMM0);
         const int npair = n * n;
         const int p0 = lane, p1 = lane + 32;
-        const int i0 = p0 / n, j0 = p0 % n, i1 = p1 / n, j1 = p1 % n;
+        const int i0 = (p0 < npair ? p0 : 0) / n, j0 = (p0 < npair ? p0 : 0) % n;
+        const int i1 = (p1 < npair ? p1 : 0) / n, j1 = (p1 < npair ? p1 : 0) % n;
         double a0 = 0.0, a1 = 0.0;
+        const unsigned char* alist0 = alists;  // layer 0's active units
         int t = 0;
         for (int r0 = 0; r0 < width; r0 += rpc) {
-          const double* ch = ws_in.acquire();
+          const double* ch = stages + ws_in.acquire() * SD;
           const int nr = min(rpc, width - r0);
           if (!done) {
-            int tend = t;
-            while (tend < acnt && alist[tend] < r0 + nr) ++tend;
-            if (p0 < npair) {
+            const int t1 = popc_below(am, r0 + nr);
 #pragma unroll 4
-              for (int q = t; q < tend; ++q) {
-                const int kk = alist[q];
-                a0 = add(a0, mul(LT[kk * NOP + i0], ch[(kk - r0) * ld + j0]));
-              }
+            for (; t < t1; ++t) {
+              const int kk = alist0[t];
+              const double* wrow = ch + (kk - r0) * ld;
+              a0 = add(a0, mul(LT[kk * NOP + i0], wrow[j0]));
+              a1 = add(a1, mul(LT[kk * NOP + i1], wrow[j1]));
             }
-            if (p1 < npair) {
-              for (int q = t; q < tend; ++q) {
-                const int kk = alist[q];
-                a1 = add(a1, mul(LT[kk * NOP + i1], ch[(kk - r0) * ld + j1]));
-              }
-            }
-            t = tend;
           }
           ws_in.release(lane);
         }
@@ -729,59 +850,94 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
     ++nq;
     __syncwarp();
 
-    // ---- fold_overflow (flowpipe_ct.hpp:317-350), warp-parallel
+    // ---- fold_overflow (flowpipe_ct.hpp:317-350): lane j < 2n holds column j of
+    // [G0 | oldest block] in registers; pivots and row multipliers travel by shuffles
     RB_PH(PH_FOLD);
     while (nq > cap) {
-      double* M = LT;              // [n][2n] augmented [G0 | a]
-      double* X = LT + 2 * n * n;  // [n][n]
-      double* E = X + n * n;       // [n][n]
-      double* rr = E + n * n;      // [n]
       const int n2 = 2 * n;
-      if (lane < n2)
-        for (int i = 0; i < n; ++i) M[i * n2 + lane] = stA[i * nzs + lane];  // G0 | oldest block
-      __syncwarp();
+      double col[NO];
+#pragma unroll
+      for (int i = 0; i < NO; ++i) col[i] = (lane < n2 && i < n) ? stA[i * nzs + lane] : 0.0;
       bool ok = true;
       for (int kk = 0; kk < n; ++kk) {
+        // pivot search on column kk (owner lane kk), first maximum wins (linalg.hpp:104-112)
         int piv = kk;
-        double best = fabs(M[kk * n2 + kk]);
-        for (int i = kk + 1; i < n; ++i) {
-          const double cand = fabs(M[i * n2 + kk]);
-          if (cand > best) {
-            best = cand;
+        double best = 0.0;
+#pragma unroll
+        for (int i = 0; i < NO; ++i) {
+          const double v = fabs(col[i]);
+          if (i == kk) best = v;
+          if (i > kk && i < n && v > best) {
+            best = v;
             piv = i;
           }
         }
+        piv = __shfl_sync(0xffffffffu, piv, kk);
+        best = __shfl_sync(0xffffffffu, best, kk);
         if (!(best > 1e-12)) {
           ok = false;
           break;
         }
-        if (piv != kk && lane < n2) {
-          const double t = M[kk * n2 + lane];
-          M[kk * n2 + lane] = M[piv * n2 + lane];
-          M[piv * n2 + lane] = t;
-        }
-        __syncwarp();
-        double f[NO];
-        const double akk = M[kk * n2 + kk];
+        if (piv != kk) {  // swap rows kk and piv in every column
+          double vk = 0.0, vp = 0.0;
 #pragma unroll
-        for (int i = 0; i < NO; ++i) f[i] = (i > kk && i < n) ? __ddiv_rn(M[i * n2 + kk], akk) : 0.0;
-        __syncwarp();
-        if (lane < n2 && (lane >= kk)) {
-          const double mk = M[kk * n2 + lane];
+          for (int i = 0; i < NO; ++i) {
+            if (i == kk) vk = col[i];
+            if (i == piv) vp = col[i];
+          }
+#pragma unroll
+          for (int i = 0; i < NO; ++i) {
+            if (i == kk) col[i] = vp;
+            if (i == piv) col[i] = vk;
+          }
+        }
+        // multipliers f_i = a(i,kk) / a(kk,kk), computed by the pivot-column lane
+        double f[NO];
+        double akk = 0.0;
+#pragma unroll
+        for (int i = 0; i < NO; ++i)
+          if (i == kk) akk = col[i];
+#pragma unroll
+        for (int i = 0; i < NO; ++i) f[i] = (i > kk && i < n) ? __ddiv_rn(col[i], akk) : 0.0;
+#pragma unroll
+        for (int i = 0; i < NO; ++i) f[i] = __shfl_sync(0xffffffffu, f[i], kk);
+        double mk = 0.0;
+#pragma unroll
+        for (int i = 0; i < NO; ++i)
+          if (i == kk) mk = col[i];
+        if (lane < n2 && lane >= kk) {
 #pragma unroll
           for (int i = 0; i < NO; ++i)
-            if (i > kk && i < n) M[i * n2 + lane] = sub(M[i * n2 + lane], mul(f[i], mk));
+            if (i > kk && i < n) col[i] = sub(col[i], mul(f[i], mk));
         }
-        __syncwarp();
       }
       bool folded = false;
       double* newest = stA + n * nq;  // column offset of the newest block
+      double* M = LT;                  // [n][2n] eliminated [U | B']
+      double* X = LT + 2 * n * n;      // [n][n]
+      double* E = X + n * n;           // [n][n]
+      double* rr = E + n * n;          // [n]
       if (ok) {
-        if (lane < n) {  // back substitution, lane j owns RHS column j
-          for (int i = n - 1; i >= 0; --i) {
-            double a = M[i * n2 + n + lane];
-            for (int kk = i + 1; kk < n; ++kk) a = sub(a, mul(M[i * n2 + kk], X[kk * n + lane]));
-            X[i * n + lane] = __ddiv_rn(a, M[i * n2 + i]);
+        if (lane < n2)
+#pragma unroll
+          for (int i = 0; i < NO; ++i)
+            if (i < n) M[i * n2 + lane] = col[i];
+        __syncwarp();
+        if (lane >= n && lane < n2) {  // back substitution, lane n+j owns RHS column j
+          const int jc = lane - n;
+          double x[NO];
+#pragma unroll
+          for (int i = NO - 1; i >= 0; --i) {
+            if (i < n) {
+              double a = col[i];
+#pragma unroll
+              for (int kk = i + 1; kk < NO; ++kk)
+                if (kk < n) a = sub(a, mul(M[i * n2 + kk], x[kk]));
+              x[i] = __ddiv_rn(a, M[i * n2 + i]);
+              X[i * n + jc] = x[i];
+            } else {
+              x[i] = 0.0;
+            }
           }
         }
         __syncwarp();
@@ -868,8 +1024,10 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 1) dt_horizon_kernel(const 
   RB_PH(PH_DRAIN);
 #ifdef RB_PHASE_TIMING
   RB_PH(PH_DRAIN);
-  if (lane == 0)
+  if (lane == 0) {
     for (int i = 0; i < 10; ++i) atomicAdd(&g_phase_cycles[i], static_cast<unsigned long long>(ph_acc[i]));
+    atomicAdd(&g_phase_cycles[10], static_cast<unsigned long long>(ws_in.wait_cycles));
+  }
 #endif
 
   if (!valid) return;

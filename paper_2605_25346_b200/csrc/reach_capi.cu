@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -104,8 +105,16 @@ struct DTLayout {
   size_t smem = 0;
 };
 
-constexpr int kStageDoubles = 2048;  // 16 KB bulk-copy stages
-constexpr int kNStage = 3;
+constexpr int kStageDoublesDefault = 2048;  // 16 KB bulk-copy stages
+constexpr int kNStageDefault = 3;
+
+// Weight-stream ring geometry; RB_NSTAGE / RB_STAGE_DOUBLES override it for tuning runs.
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* v = std::getenv(name);
+  if (!v) return dflt;
+  int x = std::atoi(v);
+  return (x < lo || x > hi) ? dflt : x;
+}
 
 int cpl_for(int maxh) { return maxh <= 32 ? 1 : maxh <= 64 ? 2 : maxh <= 96 ? 3 : maxh <= 128 ? 4 : maxh <= 256 ? 8 : 0; }
 
@@ -136,8 +145,8 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::
   if (tanh_any) off += 3 * hp;
   P.o_bf0 = off;
   if (m > 0) off += std::max(hp, ev(n));
-  P.o_idx = off;  // per hidden layer two unit lists (uint8) + their counts
-  off += ((L - 1) * 2 * hp + (L - 1) * 2 * 4 + 15) / 16 * 2;
+  P.o_idx = off;  // per hidden layer two unit bitmasks (active, unstable) + the active-unit list
+  off += ev(((L - 1) * 2 * (hp / 32) * 4 + (L - 1) * hp + 7) / 8);
   P.warp_doubles = ev(off);
   P.nzs = nzs;
   P.hp = hp;
@@ -147,6 +156,8 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::
     boff += (l + 1 < L) ? hp : ev(net->dims[l + 1]);
   }
   P.bias_doubles = ev(boff);
+  const int kStageDoubles = env_int("RB_STAGE_DOUBLES", kStageDoublesDefault, 512, 8192) & ~1;
+  const int kNStage = env_int("RB_NSTAGE", kNStageDefault, 2, 8);
   P.stage_doubles = kStageDoubles;
   P.nstage = kNStage;
   // weight-stream chunk table of one DT step (consumption order of the kernel)
@@ -169,7 +180,7 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::
   for (int l = L - 1; l >= 0; --l) ok = ok && add_matrix(d.w_off[l], d.dims[l + 1], d.ldw[l]);
   if (!ok) return fail(ctx, REACH_E_UNSUPPORTED, "network too large for the weight stream");
   P.n_chunks_step = nc;
-  const size_t fixed = 128 + static_cast<size_t>(kNStage) * kStageDoubles * 8 + static_cast<size_t>(P.bias_doubles) * 8;
+  const size_t fixed = rb::kHeaderBytes + static_cast<size_t>(kNStage) * kStageDoubles * 8 + static_cast<size_t>(P.bias_doubles) * 8;
   const size_t per = static_cast<size_t>(P.warp_doubles) * 8;
   int spc = static_cast<int>((static_cast<size_t>(ctx->max_smem) - fixed) / per);
   spc = std::min(spc, rb::kSampleWarps);
@@ -178,6 +189,8 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::
   lay.no = no;
   lay.cpl = net->cpl;
   lay.smem = fixed + per * spc;
+  // tuning knob: pad the allocation to force fewer CTAs per SM (RB_MIN_SMEM_KB)
+  lay.smem = std::max<size_t>(lay.smem, static_cast<size_t>(env_int("RB_MIN_SMEM_KB", 0, 0, 227)) * 1024);
   return REACH_OK;
 }
 

@@ -27,10 +27,16 @@ def main():
     reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), w.plan, w.actions, part_end=parts, ctx=ctx)
     dt = time.perf_counter() - t0
     cyc = ctx.phase_cycles()
+    if cyc is None:
+        print(f"wall {dt*1e3:.1f} ms (product build, no phase counters)")
+        return
+    wait = cyc[10]
+    cyc = cyc[:10]
     tot = sum(cyc)
     print(f"wall {dt*1e3:.1f} ms; warp-cycles {tot:.3e}")
     for nm, c in zip(NAMES, cyc):
         print(f"  {nm:9s} {100*c/tot:5.1f}%  {c/ (w.plan.total_parts() if not parts else parts) / w.horizon:9.0f} cyc/sample-step")
+    print(f"  (of which waiting for weight chunks: {100*wait/tot:5.1f}%)")
 
 
 if __name__ == "__main__":
