@@ -334,10 +334,10 @@ __device__ __forceinline__ void pipelined_rows(RowIter& it, Load&& load, Comp&& 
 // Intercept chains run over the unstable units only (ReLU: li = 0 always,
 // ui = 0 for stable units).
 #ifndef RB_SAMPLE_WARPS
-#define RB_SAMPLE_WARPS 4
+#define RB_SAMPLE_WARPS 8
 #endif
 #ifndef RB_MIN_BLOCKS
-#define RB_MIN_BLOCKS 2
+#define RB_MIN_BLOCKS 1
 #endif
 #ifndef RB_PIPELINE
 #define RB_PIPELINE 0

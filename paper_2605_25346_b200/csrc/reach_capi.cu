@@ -106,7 +106,7 @@ struct DTLayout {
 };
 
 constexpr int kStageDoublesDefault = 2048;  // 16 KB bulk-copy stages
-constexpr int kNStageDefault = 3;
+constexpr int kNStageDefault = 6;
 
 // Weight-stream ring geometry; RB_NSTAGE / RB_STAGE_DOUBLES override it for tuning runs.
 int env_int(const char* name, int dflt, int lo, int hi) {
