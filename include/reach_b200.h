@@ -113,6 +113,53 @@ typedef struct reach_hull_out {
   int64_t* fail_key;     /* [1] (div_step << 40 | part << 8 | status), INT64_MAX if no part failed */
 } reach_hull_out;
 
+/* Reachability-aware MPC (mpc.hpp).  Constraint::Type (mpc.hpp:26-86). */
+enum reach_constraint_type {
+  REACH_CON_HALFSPACE_AVOID = 0, /* unsafe {y : a.y >= b} */
+  REACH_CON_SPHERE_AVOID = 1,    /* unsafe open ball B(center, radius) */
+  REACH_CON_BOX_STAY_IN = 2,     /* safe box [lo, hi] */
+  REACH_CON_MAX_VOLUME = 3       /* width-sum budget vmax */
+};
+
+typedef struct reach_constraint {
+  int32_t type;
+  int32_t n_dims;        /* 0 = all state dims */
+  const int32_t* dims;   /* [n_dims] */
+  const double* a;       /* halfspace normal [k] */
+  double b;              /* halfspace offset */
+  const double* center;  /* sphere center [k] */
+  double radius;
+  const double* lo;      /* stay-in box [k] */
+  const double* hi;
+  double vmax;
+} reach_constraint;
+
+/* PlanProblem (mpc.hpp:115-142); the one-step map is the uploaded network. */
+typedef struct reach_plan_problem {
+  int32_t n, m, horizon, window, rebuild_from_box;
+  const double* x_goal;     /* [n] */
+  const double* q_weights;  /* [n] */
+  const double* r_weights;  /* [m] */
+  int32_t n_constraints;
+  const reach_constraint* constraints;
+  double penalty;           /* C */
+  double diverged_margin;
+  double eps;               /* planning radius around x0 */
+  const double* u_lo;       /* [m] action box */
+  const double* u_hi;
+} reach_plan_problem;
+
+/* SamplerConfig (mpc.hpp:220-234). */
+typedef struct reach_sampler_config {
+  int32_t population;
+  double elite_frac;
+  int32_t iterations;
+  double init_std;
+  double smoothing;
+  int32_t refine_iters; /* gradient refinement is not on the device path: must be 0 */
+  uint64_t seed;
+} reach_sampler_config;
+
 /* ----------------------------------------------------------------------- */
 /* GPU product (libreach_b200.so).                                          */
 typedef struct reach_ctx reach_ctx;
@@ -163,6 +210,37 @@ int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* ar
  * pointers and the call is stream-ordered. */
 int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_args* args,
                      const reach_hull_out* out, int32_t flags);
+
+/* plan_eval (mpc.hpp:158-202) for a batch of action sequences from one x0:
+ * objective[b] and diverged[b] (the tube's diverged flag) per candidate;
+ * tubes (optional, may be NULL) receives the certified tubes.  Host pointers
+ * unless REACH_FLAG_DEVICE_PTRS (then x0, actions, objective, diverged and
+ * the tube arrays are device pointers; the problem struct stays on the host). */
+int reach_plan_eval_batch(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
+                          int32_t batch, const double* actions, double* objective, int32_t* diverged,
+                          const reach_tube_out* tubes, int32_t flags);
+
+/* plan_cem (mpc.hpp:258-368) with refine_iters == 0: the reference's
+ * sequential mt19937_64 / Box-Muller sampling on the host, every population
+ * evaluated by reach_plan_eval_batch, stable-sort elite refit on the host.
+ * best_actions [H][m], best_history [iterations], best_effort flag, and the
+ * final plan's tube (batch 1, optional). */
+int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
+                   const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
+                   double* best_history, int32_t* best_effort, const reach_tube_out* final_tube);
+
+/* The CEM loop in pieces, for multi-GPU drivers that shard each population
+ * and all-gather the scores between sample() and update(). */
+typedef struct reach_cem reach_cem;
+int reach_cem_create(const reach_plan_problem* prob, const reach_sampler_config* cfg, reach_cem** out);
+int reach_cem_destroy(reach_cem* cem);
+/* Draws iteration `it`'s population into candidates [population][H][m]. */
+int reach_cem_sample(reach_cem* cem, double* candidates);
+/* Consumes the scores / ok flags of the population drawn last. */
+int reach_cem_update(reach_cem* cem, const double* scores, const int32_t* ok);
+/* best actions [H][m], best objective, best_effort, history [iterations so far] */
+int reach_cem_result(const reach_cem* cem, double* best_actions, double* best_objective, int32_t* best_effort,
+                     double* best_history);
 
 #ifdef __cplusplus
 }

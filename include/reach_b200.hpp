@@ -1,0 +1,248 @@
+// reach_b200.hpp -- header-only C++17 host API over the C ABI (reach_b200.h).
+//
+// Mirrors the reference's C++ API for the DT reachability path
+// (/root/reference/proj/include/reach/): same names, argument meaning and
+// error behaviour (std::invalid_argument on shape errors, per-sample
+// failures as tube data), with every batch evaluated by the B200 kernels.
+//
+//   reference                                   here
+//   MLPNet<double> / Layer / Act (neural.hpp)   reach_b200::MLPNet / Layer / Act
+//   DTSystem, DTReachParams (dt_reach.hpp)      reach_b200::DTSystem, DTReachParams
+//   IntervalBox<double> (interval.hpp)          reach_b200::Box
+//   ReachTube<double> (tube.hpp)                reach_b200::ReachTube
+//   dt_reach / dt_reach_batch                   reach_b200::dt_reach / dt_reach_batch
+//   SplitPlan / reach_with_splitting(dt_reach)  reach_b200::SplitPlan / reach_with_splitting
+//
+// For code that already holds the reference's own types, see
+// reach_b200_reference.hpp (drop-in overloads taking reach:: types).
+#pragma once
+
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "reach_b200.h"
+
+namespace reach_b200 {
+
+enum class Act { Relu = REACH_ACT_RELU, Tanh = REACH_ACT_TANH, Identity = REACH_ACT_IDENTITY };
+
+struct Layer {
+  int rows = 0, cols = 0;
+  std::vector<double> w;  // row-major rows x cols
+  std::vector<double> b;  // rows
+  Act act = Act::Identity;
+};
+
+struct MLPNet {
+  std::vector<Layer> layers;
+  int input_dim() const { return layers.front().cols; }
+  int output_dim() const { return layers.back().rows; }
+  void validate() const {  // neural.hpp:49-56
+    if (layers.empty()) throw std::invalid_argument("MLPNet: empty");
+    for (size_t l = 0; l + 1 < layers.size(); ++l)
+      if (layers[l + 1].cols != layers[l].rows) throw std::invalid_argument("MLPNet: layer shapes do not chain");
+    if (layers.back().act != Act::Identity)
+      throw std::invalid_argument("MLPNet: final activation must be identity");
+  }
+};
+
+struct DTSystem {  // dt_reach.hpp:17-29
+  MLPNet step;
+  int n = 0, m = 0;
+  void validate() const {
+    step.validate();
+    if (n <= 0 || m < 0) throw std::invalid_argument("DTSystem: invalid dimensions");
+    if (step.input_dim() != n + m || step.output_dim() != n)
+      throw std::invalid_argument("DTSystem: one-step map shape mismatch");
+  }
+};
+
+struct DTReachParams {  // dt_reach.hpp:31-36
+  int window = 4;
+  bool rebuild_from_box = false;
+};
+
+struct Interval {
+  double lo = 0.0, hi = 0.0;
+};
+using Box = std::vector<Interval>;
+
+struct ReachTube {  // tube.hpp:12-35
+  std::vector<Box> boxes;
+  std::vector<double> t_lo, t_hi;
+  bool diverged = false;
+  int failed_step = -1;
+  std::string failure_reason;
+  int steps() const { return static_cast<int>(boxes.size()); }
+};
+
+struct SplitPlan {  // refine.hpp:25-78
+  std::vector<int> counts;
+};
+
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+// One device + stream + uploaded networks (one per host thread).
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    int rc = reach_ctx_create(device, &ctx_);
+    if (rc != REACH_OK) throw Error("reach_ctx_create failed (no usable CUDA device)");
+  }
+  ~Context() {
+    for (auto& kv : nets_) reach_net_free(ctx_, kv.second);
+    reach_ctx_destroy(ctx_);
+  }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  reach_ctx* raw() const { return ctx_; }
+
+  void check(int rc, const char* what) const {
+    if (rc == REACH_OK) return;
+    std::string msg = std::string(what) + ": " + reach_ctx_last_error(ctx_);
+    if (rc == REACH_E_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    throw Error(msg);
+  }
+
+  // Uploads (once per distinct network value) and returns the device network.
+  reach_net* upload(const MLPNet& net) {
+    net.validate();
+    std::vector<int32_t> dims{net.input_dim()}, acts;
+    std::vector<double> params;
+    for (const auto& L : net.layers) {
+      dims.push_back(L.rows);
+      acts.push_back(static_cast<int32_t>(L.act));
+      params.insert(params.end(), L.w.begin(), L.w.end());
+      params.insert(params.end(), L.b.begin(), L.b.end());
+    }
+    uint64_t key = 1469598103934665603ull;  // FNV-1a over the flattened value
+    auto mix = [&key](const void* p, size_t bytes) {
+      const unsigned char* c = static_cast<const unsigned char*>(p);
+      for (size_t i = 0; i < bytes; ++i) key = (key ^ c[i]) * 1099511628211ull;
+    };
+    mix(dims.data(), dims.size() * sizeof(int32_t));
+    mix(acts.data(), acts.size() * sizeof(int32_t));
+    mix(params.data(), params.size() * sizeof(double));
+    auto it = nets_.find(key);
+    if (it != nets_.end()) return it->second;
+    reach_net_desc d{static_cast<int32_t>(net.layers.size()), dims.data(), acts.data(), params.data()};
+    reach_net* h = nullptr;
+    check(reach_net_upload(ctx_, &d, &h), "reach_net_upload");
+    nets_[key] = h;
+    return h;
+  }
+
+ private:
+  reach_ctx* ctx_ = nullptr;
+  std::unordered_map<uint64_t, reach_net*> nets_;
+};
+
+inline const char* failure_reason(int32_t status) { return reach_tube_status_string(status); }
+
+// dt_reach_batch (dt_reach.hpp:108-125).
+inline std::vector<ReachTube> dt_reach_batch(Context& ctx, const DTSystem& sys, const std::vector<Box>& x0s,
+                                             const std::vector<std::vector<std::vector<double>>>& action_seqs,
+                                             const DTReachParams& prm = {}) {
+  sys.validate();
+  if (x0s.size() != action_seqs.size()) throw std::invalid_argument("dt_reach_batch: batch size mismatch");
+  std::vector<ReachTube> out(x0s.size());
+  if (x0s.empty()) return out;
+  const int B = static_cast<int>(x0s.size()), n = sys.n, m = sys.m;
+  const int H = static_cast<int>(action_seqs.front().size());
+  std::vector<double> lo(static_cast<size_t>(B) * n), hi(lo.size()), acts(static_cast<size_t>(B) * H * m);
+  for (int b = 0; b < B; ++b) {
+    if (static_cast<int>(x0s[b].size()) != n) throw std::invalid_argument("dt_reach: X0 dimension mismatch");
+    if (static_cast<int>(action_seqs[b].size()) != H) throw std::invalid_argument("dt_reach_batch: ragged horizon");
+    for (int d = 0; d < n; ++d) {
+      lo[static_cast<size_t>(b) * n + d] = x0s[b][d].lo;
+      hi[static_cast<size_t>(b) * n + d] = x0s[b][d].hi;
+    }
+    for (int k = 0; k < H; ++k) {
+      if (static_cast<int>(action_seqs[b][k].size()) != m)
+        throw std::invalid_argument("dt_reach: action dimension mismatch");
+      for (int j = 0; j < m; ++j) acts[(static_cast<size_t>(b) * H + k) * m + j] = action_seqs[b][k][j];
+    }
+  }
+  std::vector<double> olo(static_cast<size_t>(B) * (H + 1) * n), ohi(olo.size());
+  std::vector<int32_t> nb(B), fs(B), st(B);
+  reach_dt_args a{B, H, n, m, prm.window, prm.rebuild_from_box ? 1 : 0, lo.data(), hi.data(),
+                  acts.empty() ? nullptr : acts.data(), 0};
+  reach_tube_out o{olo.data(), ohi.data(), nb.data(), fs.data(), st.data()};
+  ctx.check(reach_dt_batch(ctx.raw(), ctx.upload(sys.step), &a, &o, 0), "dt_reach_batch");
+  for (int b = 0; b < B; ++b) {
+    ReachTube& t = out[b];
+    for (int k = 0; k < nb[b]; ++k) {
+      Box box(n);
+      for (int d = 0; d < n; ++d) {
+        const size_t i = (static_cast<size_t>(b) * (H + 1) + k) * n + d;
+        box[d] = {olo[i], ohi[i]};
+      }
+      t.boxes.push_back(std::move(box));
+      t.t_lo.push_back(k);
+      t.t_hi.push_back(k);
+    }
+    t.failed_step = fs[b];
+    t.diverged = st[b] != REACH_TUBE_OK;
+    t.failure_reason = st[b] != REACH_TUBE_OK ? failure_reason(st[b]) : "";
+  }
+  return out;
+}
+
+// dt_reach (dt_reach.hpp:40-104).
+inline ReachTube dt_reach(Context& ctx, const DTSystem& sys, const Box& x0,
+                          const std::vector<std::vector<double>>& actions, const DTReachParams& prm = {}) {
+  return dt_reach_batch(ctx, sys, {x0}, {actions}, prm).front();
+}
+
+// reach_with_splitting(dt_reach engine, x0, plan) (refine.hpp:121-160); the
+// sub-box grid, every sub-tube and the per-step hull stay on the device.
+inline ReachTube reach_with_splitting(Context& ctx, const DTSystem& sys, const Box& x0, const SplitPlan& plan,
+                                      const std::vector<std::vector<double>>& actions, const DTReachParams& prm = {}) {
+  sys.validate();
+  const int n = sys.n, m = sys.m, H = static_cast<int>(actions.size());
+  if (static_cast<int>(x0.size()) != n || static_cast<int>(plan.counts.size()) != n)
+    throw std::invalid_argument("SplitPlan: dimension mismatch");
+  std::vector<double> lo(n), hi(n), acts(static_cast<size_t>(H) * m);
+  for (int d = 0; d < n; ++d) {
+    lo[d] = x0[d].lo;
+    hi[d] = x0[d].hi;
+  }
+  for (int k = 0; k < H; ++k)
+    for (int j = 0; j < m; ++j) acts[static_cast<size_t>(k) * m + j] = actions[k][j];
+  std::vector<int32_t> counts(plan.counts.begin(), plan.counts.end());
+  std::vector<double> olo(static_cast<size_t>(H + 1) * n), ohi(olo.size());
+  std::vector<int32_t> div(H + 1);
+  int32_t nb = 0;
+  int64_t key = 0;
+  reach_split_args a{n, m, H, prm.window, prm.rebuild_from_box ? 1 : 0, lo.data(), hi.data(), counts.data(),
+                     acts.empty() ? nullptr : acts.data(), 0, 0};
+  reach_hull_out o{olo.data(), ohi.data(), div.data(), &nb, &key};
+  ctx.check(reach_split_hull(ctx.raw(), ctx.upload(sys.step), &a, &o, 0), "reach_with_splitting");
+  ReachTube t;
+  for (int k = 0; k < nb; ++k) {
+    Box box(n);
+    for (int d = 0; d < n; ++d) box[d] = {olo[static_cast<size_t>(k) * n + d], ohi[static_cast<size_t>(k) * n + d]};
+    t.boxes.push_back(std::move(box));
+    t.t_lo.push_back(k);
+    t.t_hi.push_back(k);
+    if (div[k]) t.diverged = true;
+  }
+  if (key != std::numeric_limits<int64_t>::max()) {
+    t.diverged = true;
+    t.failed_step = static_cast<int>(key >> 40);
+    t.failure_reason = "sub-box " + std::to_string((key >> 8) & 0xffffffffLL) + ": " +
+                       failure_reason(static_cast<int32_t>(key & 0xff));
+  }
+  return t;
+}
+
+}  // namespace reach_b200

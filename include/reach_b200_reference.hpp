@@ -1,0 +1,99 @@
+// reach_b200_reference.hpp -- drop-in overloads for code that holds the
+// reference's own types (include after the reference headers, with the
+// reference's include/ on the include path):
+//
+//   #include "reach/dt_reach.hpp"
+//   #include "reach/refine.hpp"
+//   #include "reach_b200_reference.hpp"
+//   reach_b200::Context gpu;
+//   auto tubes = reach_b200::dt_reach_batch(gpu, sys, x0s, seqs, prm);   // same args as
+//                                                                        // reach::dt_reach_batch
+//
+// Each overload converts the reference value types at the boundary and
+// returns reference ReachTube<double> values (boxes, time stamps, diverged,
+// failed_step, failure_reason exactly as the reference builds them,
+// tube.hpp:23-34), computed by the B200 kernels.
+#pragma once
+
+#include "reach/dt_reach.hpp"
+#include "reach/refine.hpp"
+#include "reach_b200.hpp"
+
+namespace reach_b200 {
+
+inline MLPNet from_reference(const reach::MLPNet<double>& net) {
+  MLPNet out;
+  for (const auto& L : net.layers) {
+    Layer l;
+    l.rows = L.w.rows;
+    l.cols = L.w.cols;
+    l.w = L.w.a;
+    l.b = L.b;
+    l.act = L.act == reach::Act::Relu ? Act::Relu : L.act == reach::Act::Tanh ? Act::Tanh : Act::Identity;
+    out.layers.push_back(std::move(l));
+  }
+  return out;
+}
+
+inline DTSystem from_reference(const reach::DTSystem<double>& sys) {
+  DTSystem s;
+  s.step = from_reference(sys.step);
+  s.n = sys.n;
+  s.m = sys.m;
+  return s;
+}
+
+inline Box from_reference(const reach::IntervalBox<double>& b) {
+  Box out(b.size());
+  for (int d = 0; d < b.size(); ++d) out[d] = {b[d].lo, b[d].hi};
+  return out;
+}
+
+inline reach::ReachTube<double> to_reference(const ReachTube& t) {
+  reach::ReachTube<double> out;
+  for (size_t k = 0; k < t.boxes.size(); ++k) {
+    reach::IntervalBox<double> b(static_cast<int>(t.boxes[k].size()));
+    for (int d = 0; d < b.size(); ++d) b[d] = {t.boxes[k][d].lo, t.boxes[k][d].hi};
+    b.check_divergence();
+    out.push(b, t.t_lo[k], t.t_hi[k]);
+  }
+  if (t.failed_step >= 0 || t.diverged) out.mark_failed(t.failed_step, t.failure_reason);
+  return out;
+}
+
+// reach::dt_reach_batch (dt_reach.hpp:108-125)
+inline std::vector<reach::ReachTube<double>> dt_reach_batch(
+    Context& ctx, const reach::DTSystem<double>& sys, const std::vector<reach::IntervalBox<double>>& x0s,
+    const std::vector<std::vector<reach::Vec<double>>>& action_seqs, const reach::DTReachParams& prm = {}) {
+  std::vector<Box> boxes;
+  boxes.reserve(x0s.size());
+  for (const auto& b : x0s) boxes.push_back(from_reference(b));
+  DTReachParams p{prm.window, prm.rebuild_from_box};
+  auto tubes = dt_reach_batch(ctx, from_reference(sys), boxes, action_seqs, p);
+  std::vector<reach::ReachTube<double>> out;
+  out.reserve(tubes.size());
+  for (const auto& t : tubes) out.push_back(to_reference(t));
+  return out;
+}
+
+// reach::dt_reach (dt_reach.hpp:40-104)
+inline reach::ReachTube<double> dt_reach(Context& ctx, const reach::DTSystem<double>& sys,
+                                         const reach::IntervalBox<double>& x0,
+                                         const std::vector<reach::Vec<double>>& actions,
+                                         const reach::DTReachParams& prm = {}) {
+  return dt_reach_batch(ctx, sys, {x0}, {actions}, prm).front();
+}
+
+// reach::reach_with_splitting with the dt_reach engine (refine.hpp:121-160)
+inline reach::ReachTube<double> reach_with_splitting_dt(Context& ctx, const reach::DTSystem<double>& sys,
+                                                        const reach::IntervalBox<double>& x0,
+                                                        const reach::SplitPlan& plan,
+                                                        const std::vector<reach::Vec<double>>& actions,
+                                                        const reach::DTReachParams& prm = {}) {
+  plan.validate(x0.size());
+  SplitPlan p{plan.counts};
+  DTReachParams q{prm.window, prm.rebuild_from_box};
+  return to_reference(reach_with_splitting(ctx, from_reference(sys), from_reference(x0), p, actions, q));
+}
+
+}  // namespace reach_b200

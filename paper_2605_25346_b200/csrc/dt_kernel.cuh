@@ -59,6 +59,8 @@ struct DTParams {
   double sx_hi[kMaxSplitDims];
   const double* actions;
   int actions_shared;
+  int x0_center;    // 1: every sample's X0 = box_from_center(x0_lo[0..n), x0_eps) (interval.hpp:224-235)
+  double x0_eps;
   // tube outputs
   double* out_lo;
   double* out_hi;
@@ -419,6 +421,10 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
   if (lane < n && valid) {
     if (P.split) {
       split_edges(P, P.part_begin + b, lane, x_lo, x_hi);
+    } else if (P.x0_center) {
+      const double c = P.x0_lo[lane];
+      x_lo = sub(c, P.x0_eps);
+      x_hi = add(c, P.x0_eps);
     } else {
       x_lo = P.x0_lo[b * n + lane];
       x_hi = P.x0_hi[b * n + lane];

@@ -1,0 +1,167 @@
+// Reachability-aware MPC objective on the device (mpc.hpp:40-202).
+//
+// plan_eval = nominal rollout through the one-step network + quadratic stage
+// costs, then constraint penalties over the certified tube (computed by the
+// DT horizon kernel).  One warp per candidate: the rollout's layer outputs
+// are spread over the lanes (each a sequential dot product over the inputs,
+// as MLPNet::forward's matvec, linalg.hpp:40-51), the objective is summed by
+// lane 0 in the reference's order with separate multiply / add roundings.
+#pragma once
+
+#include "dt_common.cuh"
+#include "dt_kernel.cuh"
+
+namespace rb {
+
+constexpr int kMaxConstraints = 16;
+
+struct DevConstraint {
+  int type, k;       // k = number of dims the constraint reads
+  int dims_off;      // offsets into PlanParams::ibuf / dbuf
+  int a_off, c_off, lo_off, hi_off;
+  double b, radius, vmax;
+};
+
+struct PlanParams {
+  DevNet net;
+  int B, H, n, m;
+  const double* x0;       // [n]
+  const double* actions;  // [B][H][m]
+  const double* x_goal;   // [n]   (in dbuf)
+  const double* q_w;
+  const double* r_w;
+  int n_con;
+  DevConstraint con[kMaxConstraints];
+  const int* ibuf;
+  const double* dbuf;
+  double penalty, diverged_margin;
+  // tube produced by the DT kernel
+  const double* tube_lo;  // [B][H+1][n]
+  const double* tube_hi;
+  const int* n_boxes;
+  const int* status;
+  double* objective;      // [B]
+  int* diverged;          // [B]
+};
+
+// Constraint::margin (mpc.hpp:40-86) on box k of candidate b.
+__device__ inline double con_margin(const PlanParams& P, const DevConstraint& c, const double* lo, const double* hi) {
+  const int* dims = P.ibuf + c.dims_off;
+  const double* dv = P.dbuf;
+  switch (c.type) {
+    case 0: {  // halfspace_avoid: b - max_{y in box} a.y
+      double worst = c.b;
+      for (int j = 0; j < c.k; ++j) {
+        const int d = dims[j];
+        const double aj = dv[c.a_off + j];
+        const double term = aj >= 0.0 ? mul(hi[d], aj) : mul(lo[d], aj);
+        worst = sub(worst, term);
+      }
+      return worst;
+    }
+    case 1: {  // sphere_avoid: box-to-center distance minus radius
+      double d2 = 0.0;
+      for (int j = 0; j < c.k; ++j) {
+        const int d = dims[j];
+        const double cj = dv[c.c_off + j];
+        double gap = 0.0;
+        if (lo[d] > cj) gap = sub(lo[d], cj);
+        else if (hi[d] < cj) gap = sub(cj, hi[d]);
+        d2 = add(d2, mul(gap, gap));
+      }
+      return sub(__dsqrt_rn(d2), c.radius);
+    }
+    case 2: {  // box_stay_in: worst slack
+      double worst = __longlong_as_double(0x7ff0000000000000ll);
+      for (int j = 0; j < c.k; ++j) {
+        const int d = dims[j];
+        worst = smin(worst, sub(lo[d], dv[c.lo_off + j]));
+        worst = smin(worst, sub(dv[c.hi_off + j], hi[d]));
+      }
+      return worst;
+    }
+    default: {  // max_volume
+      double v = 0.0;
+      for (int j = 0; j < c.k; ++j) {
+        const int d = dims[j];
+        v = add(v, sub(hi[d], lo[d]));
+      }
+      return sub(c.vmax, v);
+    }
+  }
+}
+
+// One warp per candidate: nominal rollout + stage costs + tube penalties.
+// Shared memory: per warp two vectors of `vec` doubles (layer input / output).
+__global__ void __launch_bounds__(256) plan_objective_kernel(const PlanParams P, int vec) {
+  extern __shared__ __align__(16) double psm[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int b = blockIdx.x * (blockDim.x / 32) + warp;
+  if (b >= P.B) return;
+  double* vin = psm + static_cast<size_t>(warp) * 2 * vec;
+  double* vout = vin + vec;
+  const DevNet& N = P.net;
+  const int n = P.n, m = P.m, H = P.H, L = N.L;
+  const double* acts = P.actions + static_cast<size_t>(b) * H * m;
+  double x_reg = (lane < n) ? P.x0[lane] : 0.0;  // lane d holds x_d between steps
+  double obj = 0.0;                               // lane 0's running objective
+  for (int t = 0; t < H; ++t) {
+    const double* u = acts + static_cast<size_t>(t) * m;
+    // in = [x; u]
+    if (lane < n) vin[lane] = x_reg;
+    for (int j = lane; j < m; j += 32) vin[n + j] = u[j];
+    __syncwarp();
+    for (int l = 0; l < L; ++l) {
+      const int rows = N.dims[l + 1], cols = N.dims[l];
+      const double* wt = N.blob + N.wt_off[l];
+      const int ld = N.ldt[l];
+      const double* bias = N.blob + N.b_off[l];
+      const int act = N.acts[l];
+      for (int o = lane; o < rows; o += 32) {
+        double acc = 0.0;
+        for (int j = 0; j < cols; ++j) acc = add(acc, mul(__ldg(wt + static_cast<size_t>(j) * ld + o), vin[j]));
+        double v = add(acc, __ldg(bias + o));
+        if (act == 0) v = (v < 0.0) ? 0.0 : v;  // MLPNet::h_relu (neural.hpp:85-87)
+        else if (act == 1) v = tanh(v);
+        vout[o] = v;
+      }
+      __syncwarp();
+      double* tmp = vin;
+      vin = vout;
+      vout = tmp;
+    }
+    // vin now holds x_{t+1}
+    if (lane < n) x_reg = vin[lane];
+    if (lane == 0) {
+      for (int j = 0; j < m; ++j) obj = add(obj, mul(mul(P.r_w[j], u[j]), u[j]));
+      for (int j = 0; j < n; ++j) {
+        const double d = sub(vin[j], P.x_goal[j]);
+        obj = add(obj, mul(mul(P.q_w[j], d), d));
+      }
+    }
+    __syncwarp();
+  }
+  if (lane != 0) return;
+  const int nb = P.n_boxes[b];
+  for (int t = 1; t <= H; ++t) {
+    const double* lo = P.tube_lo + (static_cast<size_t>(b) * (H + 1) + t) * n;
+    const double* hi = P.tube_hi + (static_cast<size_t>(b) * (H + 1) + t) * n;
+    bool box_ok = t < nb;
+    if (box_ok)
+      for (int d = 0; d < n; ++d)
+        if (!(finite(lo[d]) && finite(hi[d]))) box_ok = false;
+    if (box_ok) {
+      for (int c = 0; c < P.n_con; ++c) {
+        const double g = con_margin(P, P.con[c], lo, hi);
+        const double ng = -g;
+        obj = add(obj, mul(P.penalty, (0.0 < ng) ? ng : 0.0));
+      }
+    } else if (P.n_con > 0) {
+      obj = add(obj, mul(mul(P.penalty, P.diverged_margin), static_cast<double>(P.n_con)));
+    }
+  }
+  P.objective[b] = obj;
+  P.diverged[b] = P.status[b] != ST_OK ? 1 : 0;
+}
+
+}  // namespace rb

@@ -8,6 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <limits>
+#include <memory>
 #include <climits>
 #include <cstdint>
 #include <cstdlib>
@@ -18,6 +21,9 @@
 #include "../../include/reach_b200.h"
 #include "diag.cuh"
 #include "dt_kernel.cuh"
+#include "plan.cuh"
+
+#include <random>
 
 struct reach_ctx {
   int device = 0;
@@ -649,6 +655,400 @@ int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_arg
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   return REACH_OK;
+}
+
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Reachability-aware MPC (mpc.hpp).
+namespace {
+
+// PlanProblem::validate + Constraint::validate (mpc.hpp:88-142).
+int validate_problem(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* p) {
+  int rc = validate_system(ctx, net, p->n, p->m);
+  if (rc) return rc;
+  if (p->horizon < 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "PlanProblem: horizon < 1");
+  if (!p->x_goal || !p->q_weights || (p->m > 0 && !p->r_weights))
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "PlanProblem: cost dimension mismatch");
+  if (p->m > 0 && (!p->u_lo || !p->u_hi))
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "PlanProblem: action box dimension mismatch");
+  for (int j = 0; j < p->m; ++j)
+    if (!(p->u_lo[j] <= p->u_hi[j]) || !std::isfinite(p->u_lo[j]) || !std::isfinite(p->u_hi[j]))
+      return fail(ctx, REACH_E_INVALID_ARGUMENT, "PlanProblem: action box must be bounded");
+  if (p->eps < 0.0 || p->penalty < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "PlanProblem: negative weight");
+  if (p->n_constraints < 0 || p->n_constraints > rb::kMaxConstraints)
+    return fail(ctx, REACH_E_UNSUPPORTED, "too many constraints");
+  for (int c = 0; c < p->n_constraints; ++c) {
+    const reach_constraint& k = p->constraints[c];
+    for (int j = 0; j < k.n_dims; ++j)
+      if (k.dims[j] < 0 || k.dims[j] >= p->n) return fail(ctx, REACH_E_INVALID_ARGUMENT, "Constraint: dim out of range");
+    switch (k.type) {
+      case REACH_CON_HALFSPACE_AVOID:
+        if (!k.a) return fail(ctx, REACH_E_INVALID_ARGUMENT, "Constraint: halfspace size");
+        break;
+      case REACH_CON_SPHERE_AVOID:
+        if (!k.center || k.radius < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "Constraint: sphere parameters");
+        break;
+      case REACH_CON_BOX_STAY_IN:
+        if (!k.lo || !k.hi) return fail(ctx, REACH_E_INVALID_ARGUMENT, "Constraint: stay-in box size");
+        break;
+      case REACH_CON_MAX_VOLUME:
+        if (k.vmax < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "Constraint: volume budget");
+        break;
+      default:
+        return fail(ctx, REACH_E_INVALID_ARGUMENT, "Constraint: unknown type");
+    }
+  }
+  return REACH_OK;
+}
+
+// Device-side copy of the problem's small arrays (goal, weights, constraints).
+struct PlanBuffers {
+  std::vector<int> ib;
+  std::vector<double> db;
+  rb::PlanParams P{};
+};
+
+void pack_problem(const reach_plan_problem* p, PlanBuffers& pb) {
+  auto put = [&](const double* v, int k) {
+    const int o = static_cast<int>(pb.db.size());
+    for (int j = 0; j < k; ++j) pb.db.push_back(v ? v[j] : 0.0);
+    return o;
+  };
+  const int og = put(p->x_goal, p->n), oq = put(p->q_weights, p->n), orr = put(p->r_weights, p->m);
+  pb.P.n_con = p->n_constraints;
+  for (int c = 0; c < p->n_constraints; ++c) {
+    const reach_constraint& k = p->constraints[c];
+    rb::DevConstraint& d = pb.P.con[c];
+    d.type = k.type;
+    d.k = k.n_dims > 0 ? k.n_dims : p->n;
+    d.dims_off = static_cast<int>(pb.ib.size());
+    for (int j = 0; j < d.k; ++j) pb.ib.push_back(k.n_dims > 0 ? k.dims[j] : j);
+    d.a_off = put(k.a, k.type == REACH_CON_HALFSPACE_AVOID ? d.k : 0);
+    d.c_off = put(k.center, k.type == REACH_CON_SPHERE_AVOID ? d.k : 0);
+    d.lo_off = put(k.lo, k.type == REACH_CON_BOX_STAY_IN ? d.k : 0);
+    d.hi_off = put(k.hi, k.type == REACH_CON_BOX_STAY_IN ? d.k : 0);
+    d.b = k.b;
+    d.radius = k.radius;
+    d.vmax = k.vmax;
+  }
+  if (pb.ib.empty()) pb.ib.push_back(0);
+  pb.P.penalty = p->penalty;
+  pb.P.diverged_margin = p->diverged_margin;
+  pb.P.x_goal = reinterpret_cast<const double*>(static_cast<intptr_t>(og));  // offsets, rebased after upload
+  pb.P.q_w = reinterpret_cast<const double*>(static_cast<intptr_t>(oq));
+  pb.P.r_w = reinterpret_cast<const double*>(static_cast<intptr_t>(orr));
+}
+
+// plan_eval for `batch` candidates with everything already on the device.
+int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* p, const double* d_x0, int batch,
+                     const double* d_actions, double* d_obj, int* d_div, double* d_tlo, double* d_thi, int* d_nb,
+                     int* d_fs, int* d_st) {
+  rb::DTParams P{};
+  DTLayout lay;
+  int rc = plan_dt(ctx, net, p->n, p->m, p->window, P, lay);
+  if (rc) return rc;
+  P.net = net->dev;
+  P.B = batch;
+  P.H = p->horizon;
+  P.n = p->n;
+  P.m = p->m;
+  P.window = p->window;
+  P.rebuild = p->rebuild_from_box;
+  P.x0_lo = d_x0;
+  P.x0_hi = d_x0;
+  P.x0_center = 1;
+  P.x0_eps = p->eps;
+  P.actions = d_actions;
+  P.out_lo = d_tlo;
+  P.out_hi = d_thi;
+  P.n_boxes = d_nb;
+  P.failed_step = d_fs;
+  P.status = d_st;
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  RB_CUDA(launch_dt(P, lay, batch, ctx->stream));
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  // objective kernel: problem arrays staged after the tube in the plan workspace
+  PlanBuffers pb;
+  pack_problem(p, pb);
+  double* d_db = nullptr;
+  int* d_ib = nullptr;
+  RB_CUDA(cudaMallocAsync(&d_db, pb.db.size() * 8 + 8, ctx->stream));
+  RB_CUDA(cudaMallocAsync(&d_ib, pb.ib.size() * 4, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(d_db, pb.db.data(), pb.db.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(d_ib, pb.ib.data(), pb.ib.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  rb::PlanParams Q = pb.P;
+  Q.net = net->dev;
+  Q.B = batch;
+  Q.H = p->horizon;
+  Q.n = p->n;
+  Q.m = p->m;
+  Q.x0 = d_x0;
+  Q.actions = d_actions;
+  Q.x_goal = d_db + reinterpret_cast<intptr_t>(pb.P.x_goal);
+  Q.q_w = d_db + reinterpret_cast<intptr_t>(pb.P.q_w);
+  Q.r_w = d_db + reinterpret_cast<intptr_t>(pb.P.r_w);
+  Q.ibuf = d_ib;
+  Q.dbuf = d_db;
+  Q.tube_lo = d_tlo;
+  Q.tube_hi = d_thi;
+  Q.n_boxes = d_nb;
+  Q.status = d_st;
+  Q.objective = d_obj;
+  Q.diverged = d_div;
+  int vec = 0;
+  for (int l = 0; l <= net->L; ++l) vec = std::max(vec, net->dims[l]);
+  vec = (vec + 1) & ~1;
+  const int wpb = 8;
+  const size_t smem = static_cast<size_t>(wpb) * 2 * vec * 8;
+  RB_CUDA(cudaFuncSetAttribute(rb::plan_objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  rb::plan_objective_kernel<<<(batch + wpb - 1) / wpb, 32 * wpb, smem, ctx->stream>>>(Q, vec);
+  RB_CUDA(cudaGetLastError());
+  RB_CUDA(cudaFreeAsync(d_db, ctx->stream));
+  RB_CUDA(cudaFreeAsync(d_ib, ctx->stream));
+  ctx->launches += 2;
+  return REACH_OK;
+}
+
+// Host-pointer plan_eval: stages inputs / outputs through the ctx workspace.
+int plan_eval_host(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* p, const double* x0, int batch,
+                   const double* actions, double* objective, int32_t* diverged, const reach_tube_out* tubes) {
+  const size_t B = batch, H = p->horizon, n = p->n, m = p->m;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t box = B * (H + 1) * n * 8;
+  const size_t o_x0 = take(n * 8), o_a = take(B * H * m * 8), o_obj = take(B * 8), o_div = take(B * 4),
+               o_lo = take(box), o_hi = take(box), o_nb = take(B * 4), o_fs = take(B * 4), o_st = take(B * 4);
+  int rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto D = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  auto I = [&](size_t o) { return reinterpret_cast<int*>(w + o); };
+  RB_CUDA(cudaMemcpyAsync(D(o_x0), x0, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (m) RB_CUDA(cudaMemcpyAsync(D(o_a), actions, B * H * m * 8, cudaMemcpyHostToDevice, ctx->stream));
+  rc = plan_eval_device(ctx, net, p, D(o_x0), batch, D(o_a), D(o_obj), I(o_div), D(o_lo), D(o_hi), I(o_nb), I(o_fs),
+                        I(o_st));
+  if (rc) return rc;
+  RB_CUDA(cudaMemcpyAsync(objective, D(o_obj), B * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(diverged, I(o_div), B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (tubes) {
+    RB_CUDA(cudaMemcpyAsync(tubes->lo, D(o_lo), box, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(tubes->hi, D(o_hi), box, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(tubes->n_boxes, I(o_nb), B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(tubes->failed_step, I(o_fs), B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(tubes->status, I(o_st), B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return REACH_OK;
+}
+
+}  // namespace
+
+// CEM state (plan_cem, mpc.hpp:258-335): the reference's Rng (rng.hpp:13-52)
+// -- std::mt19937_64, 53-bit uniforms, cached Box-Muller -- drawn sequentially.
+struct reach_cem {
+  int h = 0, m = 0;
+  std::vector<double> u_lo, u_hi;
+  reach_sampler_config cfg{};
+  std::mt19937_64 gen;
+  bool has_spare = false;
+  double spare = 0.0;
+  std::vector<double> mean, stdv, best;
+  double best_obj = std::numeric_limits<double>::infinity();
+  bool any_finite = false;
+  int n_elite = 1, it = 0;
+  std::vector<std::vector<double>> cands;
+  std::vector<double> history;
+
+  double uniform01() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
+  double normal() {
+    if (has_spare) {
+      has_spare = false;
+      return spare;
+    }
+    double u1 = uniform01(), u2 = uniform01();
+    while (u1 <= 0.0) u1 = uniform01();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 6.28318530717958647692 * u2;
+    spare = r * std::sin(a);
+    has_spare = true;
+    return r * std::cos(a);
+  }
+  void clip(std::vector<double>& flat) const {
+    for (size_t k = 0; k < flat.size(); ++k) {
+      const size_t j = k % static_cast<size_t>(m);
+      flat[k] = std::clamp(flat[k], u_lo[j], u_hi[j]);
+    }
+  }
+};
+
+extern "C" {
+
+int reach_plan_eval_batch(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
+                          int32_t batch, const double* actions, double* objective, int32_t* diverged,
+                          const reach_tube_out* tubes, int32_t flags) {
+  if (!ctx || !net || !prob || !x0 || !objective || !diverged || batch < 0) return REACH_E_INVALID_ARGUMENT;
+  int rc = validate_problem(ctx, net, prob);
+  if (rc) return rc;
+  if (batch == 0) return REACH_OK;
+  RB_CUDA(cudaSetDevice(ctx->device));
+  if (flags & REACH_FLAG_DEVICE_PTRS) {
+    const size_t B = batch, H = prob->horizon, n = prob->n;
+    double *tlo = tubes ? tubes->lo : nullptr, *thi = tubes ? tubes->hi : nullptr;
+    int *nb = tubes ? tubes->n_boxes : nullptr, *fs = tubes ? tubes->failed_step : nullptr,
+        *st = tubes ? tubes->status : nullptr;
+    if (!tubes) {  // scratch tube in the workspace
+      size_t off = 0;
+      auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+      };
+      const size_t box = B * (H + 1) * n * 8;
+      const size_t o_lo = take(box), o_hi = take(box), o_nb = take(B * 4), o_fs = take(B * 4), o_st = take(B * 4);
+      rc = ensure_ws(ctx, off);
+      if (rc) return rc;
+      char* w = static_cast<char*>(ctx->ws);
+      tlo = reinterpret_cast<double*>(w + o_lo);
+      thi = reinterpret_cast<double*>(w + o_hi);
+      nb = reinterpret_cast<int*>(w + o_nb);
+      fs = reinterpret_cast<int*>(w + o_fs);
+      st = reinterpret_cast<int*>(w + o_st);
+    }
+    return plan_eval_device(ctx, net, prob, x0, batch, actions, objective, diverged, tlo, thi, nb, fs, st);
+  }
+  return plan_eval_host(ctx, net, prob, x0, batch, actions, objective, diverged, tubes);
+}
+
+int reach_cem_create(const reach_plan_problem* prob, const reach_sampler_config* cfg, reach_cem** out) {
+  if (!prob || !cfg || !out) return REACH_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  // SamplerConfig::validate (mpc.hpp:228-233)
+  if (cfg->population < 2 || cfg->elite_frac <= 0.0 || cfg->elite_frac > 1.0 || cfg->iterations < 1 ||
+      cfg->init_std <= 0.0 || cfg->smoothing < 0.0 || cfg->smoothing >= 1.0 || cfg->refine_iters < 0)
+    return REACH_E_INVALID_ARGUMENT;
+  if (cfg->refine_iters > 0) return REACH_E_UNSUPPORTED;  // gradient refinement is not on the device path
+  if (prob->m < 1 || prob->horizon < 1) return REACH_E_INVALID_ARGUMENT;
+  reach_cem* c = new reach_cem();
+  c->h = prob->horizon;
+  c->m = prob->m;
+  c->u_lo.assign(prob->u_lo, prob->u_lo + prob->m);
+  c->u_hi.assign(prob->u_hi, prob->u_hi + prob->m);
+  c->cfg = *cfg;
+  c->gen.seed(cfg->seed);
+  const size_t dim = static_cast<size_t>(c->h) * c->m;
+  c->mean.assign(dim, 0.0);
+  c->stdv.assign(dim, cfg->init_std);
+  for (int t = 0; t < c->h; ++t)
+    for (int j = 0; j < c->m; ++j) c->mean[static_cast<size_t>(t) * c->m + j] = 0.5 * (c->u_lo[j] + c->u_hi[j]);
+  c->best = c->mean;
+  c->clip(c->best);
+  c->n_elite = std::max(1, static_cast<int>(cfg->population * cfg->elite_frac));
+  c->cands.assign(static_cast<size_t>(cfg->population), std::vector<double>(dim));
+  *out = c;
+  return REACH_OK;
+}
+
+int reach_cem_destroy(reach_cem* cem) {
+  delete cem;
+  return REACH_OK;
+}
+
+int reach_cem_sample(reach_cem* c, double* candidates) {
+  if (!c || !candidates) return REACH_E_INVALID_ARGUMENT;
+  if (c->it >= c->cfg.iterations) return REACH_E_INVALID_ARGUMENT;
+  const size_t dim = c->mean.size();
+  for (int k = 0; k < c->cfg.population; ++k) {  // mpc.hpp:290-299, sequential stream
+    std::vector<double>& u = c->cands[static_cast<size_t>(k)];
+    if (c->it > 0 && k == 0) {
+      u = c->best;
+    } else {
+      for (size_t q = 0; q < dim; ++q) u[q] = c->mean[q] + c->stdv[q] * c->normal();
+      c->clip(u);
+    }
+    std::copy(u.begin(), u.end(), candidates + static_cast<size_t>(k) * dim);
+  }
+  return REACH_OK;
+}
+
+int reach_cem_update(reach_cem* c, const double* scores, const int32_t* ok) {
+  if (!c || !scores || !ok) return REACH_E_INVALID_ARGUMENT;
+  const int pop = c->cfg.population;
+  std::vector<int> order(static_cast<size_t>(pop));
+  for (int k = 0; k < pop; ++k) order[static_cast<size_t>(k)] = k;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return scores[a] < scores[b]; });
+  const int top = order.front();
+  if (scores[top] < c->best_obj) {
+    c->best_obj = scores[top];
+    c->best = c->cands[static_cast<size_t>(top)];
+  }
+  for (int e = 0; e < c->n_elite; ++e)
+    if (ok[order[static_cast<size_t>(e)]]) c->any_finite = true;
+  c->history.push_back(c->best_obj);
+  const double sm = c->cfg.smoothing;
+  for (size_t k = 0; k < c->mean.size(); ++k) {  // mpc.hpp:320-333
+    double em = 0.0, ev = 0.0;
+    for (int e = 0; e < c->n_elite; ++e) em += c->cands[static_cast<size_t>(order[static_cast<size_t>(e)])][k];
+    em /= c->n_elite;
+    for (int e = 0; e < c->n_elite; ++e) {
+      const double d = c->cands[static_cast<size_t>(order[static_cast<size_t>(e)])][k] - em;
+      ev += d * d;
+    }
+    const double es = std::sqrt(ev / c->n_elite);
+    c->mean[k] = sm * c->mean[k] + (1.0 - sm) * em;
+    c->stdv[k] = std::max(1e-6, sm * c->stdv[k] + (1.0 - sm) * es);
+  }
+  ++c->it;
+  return REACH_OK;
+}
+
+int reach_cem_result(const reach_cem* c, double* best_actions, double* best_objective, int32_t* best_effort,
+                     double* best_history) {
+  if (!c) return REACH_E_INVALID_ARGUMENT;
+  if (best_actions) std::copy(c->best.begin(), c->best.end(), best_actions);
+  if (best_objective) *best_objective = c->best_obj;
+  if (best_effort) *best_effort = c->any_finite ? 0 : 1;
+  if (best_history) std::copy(c->history.begin(), c->history.end(), best_history);
+  return REACH_OK;
+}
+
+int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
+                   const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
+                   double* best_history, int32_t* best_effort, const reach_tube_out* final_tube) {
+  if (!ctx || !net || !prob || !cfg || !x0 || !best_actions || !objective) return REACH_E_INVALID_ARGUMENT;
+  int rc = validate_problem(ctx, net, prob);
+  if (rc) return rc;
+  reach_cem* c = nullptr;
+  rc = reach_cem_create(prob, cfg, &c);
+  if (rc) return fail(ctx, rc, "SamplerConfig: invalid configuration");
+  std::unique_ptr<reach_cem> guard(c);
+  const size_t dim = c->mean.size(), pop = cfg->population;
+  std::vector<double> cand(pop * dim), scores(pop);
+  std::vector<int32_t> okv(pop), div(pop);
+  for (int it = 0; it < cfg->iterations; ++it) {
+    reach_cem_sample(c, cand.data());
+    rc = plan_eval_host(ctx, net, prob, x0, static_cast<int>(pop), cand.data(), scores.data(), div.data(), nullptr);
+    if (rc) return rc;
+    for (size_t k = 0; k < pop; ++k) okv[k] = div[k] ? 0 : 1;
+    reach_cem_update(c, scores.data(), okv.data());
+  }
+  double best_obj = 0.0;
+  int32_t be = 0;
+  reach_cem_result(c, best_actions, &best_obj, &be, best_history);
+  if (best_effort) *best_effort = be;
+  // final evaluation of the chosen plan (mpc.hpp:363-367)
+  int32_t dv = 0;
+  rc = plan_eval_host(ctx, net, prob, x0, 1, best_actions, objective, &dv, final_tube);
+  return rc;
 }
 
 }  // extern "C"
