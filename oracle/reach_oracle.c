@@ -509,3 +509,240 @@ int orc_split_hull(const reach_net_desc* desc, const reach_split_args* a, const 
   free(lo); free(hi); free(net.layers);
   return REACH_OK;
 }
+
+/* ======================================================================= */
+/* Reachability-aware MPC (mpc.hpp): plan_eval and plan_cem restated.       */
+
+/* MLPNet::forward (neural.hpp:58-76): matvec then + b, ReLU as h_relu. */
+static void mlp_forward(const net_t* net, const double* in, double* out, double* buf1, double* buf2) {
+  const double* h = in;
+  double* bufs[2] = {buf1, buf2};
+  for (int l = 0; l < net->n_layers; ++l) {
+    const layer_t* Ly = &net->layers[l];
+    double* o = bufs[l & 1];
+    for (int i = 0; i < Ly->rows; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < Ly->cols; ++j) acc += Ly->w[(size_t)i * Ly->cols + j] * h[j];
+      double v = acc + Ly->b[i];
+      if (Ly->act == REACH_ACT_RELU) { if (v < 0.0) v = 0.0; }
+      else if (Ly->act == REACH_ACT_TANH) v = tanh(v);
+      o[i] = v;
+    }
+    h = o;
+  }
+  memcpy(out, h, sizeof(double) * (size_t)net->layers[net->n_layers - 1].rows);
+}
+
+/* Constraint::margin (mpc.hpp:40-86). */
+static double con_margin(const reach_constraint* c, int n, const double* lo, const double* hi) {
+  const int k = c->n_dims > 0 ? c->n_dims : n;
+  switch (c->type) {
+    case REACH_CON_HALFSPACE_AVOID: {
+      double worst = c->b;
+      for (int j = 0; j < k; ++j) {
+        const int d = c->n_dims > 0 ? c->dims[j] : j;
+        const double term = c->a[j] >= 0.0 ? hi[d] * c->a[j] : lo[d] * c->a[j];
+        worst -= term;
+      }
+      return worst;
+    }
+    case REACH_CON_SPHERE_AVOID: {
+      double d2 = 0.0;
+      for (int j = 0; j < k; ++j) {
+        const int d = c->n_dims > 0 ? c->dims[j] : j;
+        double gap = 0.0;
+        if (lo[d] > c->center[j]) gap = lo[d] - c->center[j];
+        else if (hi[d] < c->center[j]) gap = c->center[j] - hi[d];
+        d2 += gap * gap;
+      }
+      return sqrt(d2) - c->radius;
+    }
+    case REACH_CON_BOX_STAY_IN: {
+      double worst = INFINITY;
+      for (int j = 0; j < k; ++j) {
+        const int d = c->n_dims > 0 ? c->dims[j] : j;
+        worst = smin(worst, lo[d] - c->lo[j]);
+        worst = smin(worst, c->hi[j] - hi[d]);
+      }
+      return worst;
+    }
+    default: {
+      double v = 0.0;
+      for (int j = 0; j < k; ++j) {
+        const int d = c->n_dims > 0 ? c->dims[j] : j;
+        v += hi[d] - lo[d];
+      }
+      return c->vmax - v;
+    }
+  }
+}
+
+/* plan_eval (mpc.hpp:158-202) for one candidate. */
+static double plan_eval_one(const net_t* net, const reach_plan_problem* p, const double* x0, const double* acts,
+                            int* diverged) {
+  const int n = p->n, m = p->m, H = p->horizon;
+  int maxw = n + m;
+  for (int l = 0; l < net->n_layers; ++l) if (net->layers[l].rows > maxw) maxw = net->layers[l].rows;
+  double* x = (double*)malloc(sizeof(double) * (size_t)maxw);
+  double* in = (double*)malloc(sizeof(double) * (size_t)maxw);
+  double* b1 = (double*)malloc(sizeof(double) * (size_t)maxw);
+  double* b2 = (double*)malloc(sizeof(double) * (size_t)maxw);
+  double obj = 0.0;
+  memcpy(x, x0, sizeof(double) * (size_t)n);
+  for (int t = 0; t < H; ++t) {
+    const double* u = acts + (size_t)t * m;
+    memcpy(in, x, sizeof(double) * (size_t)n);
+    memcpy(in + n, u, sizeof(double) * (size_t)m);
+    mlp_forward(net, in, x, b1, b2);
+    for (int j = 0; j < m; ++j) obj += p->r_weights[j] * u[j] * u[j];
+    for (int j = 0; j < n; ++j) {
+      const double d = x[j] - p->x_goal[j];
+      obj += p->q_weights[j] * d * d;
+    }
+  }
+  /* tube at radius eps: box_from_center (interval.hpp:224-235) */
+  double* lo0 = (double*)malloc(sizeof(double) * (size_t)n);
+  double* hi0 = (double*)malloc(sizeof(double) * (size_t)n);
+  for (int d = 0; d < n; ++d) { lo0[d] = x0[d] - p->eps; hi0[d] = x0[d] + p->eps; }
+  double* tlo = (double*)malloc(sizeof(double) * (size_t)(H + 1) * n);
+  double* thi = (double*)malloc(sizeof(double) * (size_t)(H + 1) * n);
+  int fs, st;
+  const int nb = dt_reach_one(net, n, m, H, p->window, p->rebuild_from_box, lo0, hi0, acts, tlo, thi, &fs, &st);
+  *diverged = st != REACH_TUBE_OK;
+  for (int t = 1; t <= H; ++t) {
+    int ok = t < nb;
+    for (int d = 0; ok && d < n; ++d)
+      if (!isfinite(tlo[(size_t)t * n + d]) || !isfinite(thi[(size_t)t * n + d])) ok = 0;
+    if (ok) {
+      for (int c = 0; c < p->n_constraints; ++c) {
+        const double g = con_margin(&p->constraints[c], n, tlo + (size_t)t * n, thi + (size_t)t * n);
+        obj += p->penalty * smax(0.0, -g);
+      }
+    } else if (p->n_constraints > 0) {
+      obj += p->penalty * p->diverged_margin * (double)p->n_constraints;
+    }
+  }
+  free(x); free(in); free(b1); free(b2); free(lo0); free(hi0); free(tlo); free(thi);
+  return obj;
+}
+
+int orc_plan_eval_batch(const reach_net_desc* desc, const reach_plan_problem* p, const double* x0, int32_t batch,
+                        const double* actions, double* objective, int32_t* diverged) {
+  net_t net = net_from_desc(desc);
+  for (int b = 0; b < batch; ++b) {
+    int dv;
+    objective[b] = plan_eval_one(&net, p, x0, actions + (size_t)b * p->horizon * p->m, &dv);
+    diverged[b] = dv;
+  }
+  free(net.layers);
+  return REACH_OK;
+}
+
+/* std::mt19937_64 (the reference Rng's engine, rng.hpp:13-52). */
+typedef struct { uint64_t mt[312]; int idx; } mt64;
+static void mt64_seed(mt64* s, uint64_t seed) {
+  s->mt[0] = seed;
+  for (int i = 1; i < 312; ++i) s->mt[i] = 6364136223846793005ULL * (s->mt[i - 1] ^ (s->mt[i - 1] >> 62)) + (uint64_t)i;
+  s->idx = 312;
+}
+static uint64_t mt64_next(mt64* s) {
+  if (s->idx >= 312) {
+    for (int i = 0; i < 312; ++i) {
+      const uint64_t x = (s->mt[i] & 0xFFFFFFFF80000000ULL) | (s->mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+      uint64_t xa = x >> 1;
+      if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+      s->mt[i] = s->mt[(i + 156) % 312] ^ xa;
+    }
+    s->idx = 0;
+  }
+  uint64_t y = s->mt[s->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+typedef struct { mt64 g; int has_spare; double spare; } rng_t;
+static double rng_u01(rng_t* r) { return (double)(mt64_next(&r->g) >> 11) * 0x1.0p-53; }
+static double rng_normal(rng_t* r) { /* Rng::normal, cached Box-Muller */
+  if (r->has_spare) { r->has_spare = 0; return r->spare; }
+  double u1 = rng_u01(r), u2 = rng_u01(r);
+  while (u1 <= 0.0) u1 = rng_u01(r);
+  const double rad = sqrt(-2.0 * log(u1));
+  const double a = 6.28318530717958647692 * u2;
+  r->spare = rad * sin(a);
+  r->has_spare = 1;
+  return rad * cos(a);
+}
+static double clampd(double v, double lo, double hi) { return (v < lo) ? lo : (hi < v) ? hi : v; } /* std::clamp */
+
+static const double* g_sort_scores;
+static int cmp_score_index(const void* a, const void* b) {  /* stable ascending: (score, index) */
+  const int ia = *(const int*)a, ib = *(const int*)b;
+  const double sa = g_sort_scores[ia], sb = g_sort_scores[ib];
+  if (sa < sb) return -1;
+  if (sb < sa) return 1;
+  return (ia > ib) - (ia < ib);
+}
+
+/* plan_cem (mpc.hpp:258-368) with refine_iters == 0 (single-threaded restatement). */
+int orc_plan_cem(const reach_net_desc* desc, const reach_plan_problem* p, const reach_sampler_config* cfg,
+                 const double* x0, double* best_actions, double* objective, double* best_history, int32_t* best_effort) {
+  if (cfg->refine_iters != 0) return REACH_E_UNSUPPORTED;
+  net_t net = net_from_desc(desc);
+  const int h = p->horizon, m = p->m, pop = cfg->population;
+  const size_t dim = (size_t)h * m;
+  rng_t rng; mt64_seed(&rng.g, cfg->seed); rng.has_spare = 0; rng.spare = 0.0;
+  double* mean = (double*)malloc(sizeof(double) * dim);
+  double* stdv = (double*)malloc(sizeof(double) * dim);
+  double* best = (double*)malloc(sizeof(double) * dim);
+  double* cands = (double*)malloc(sizeof(double) * dim * (size_t)pop);
+  double* scores = (double*)malloc(sizeof(double) * (size_t)pop);
+  int* okv = (int*)malloc(sizeof(int) * (size_t)pop);
+  int* order = (int*)malloc(sizeof(int) * (size_t)pop);
+  for (int t = 0; t < h; ++t)
+    for (int j = 0; j < m; ++j) mean[(size_t)t * m + j] = 0.5 * (p->u_lo[j] + p->u_hi[j]);
+  for (size_t k = 0; k < dim; ++k) { stdv[k] = cfg->init_std; best[k] = clampd(mean[k], p->u_lo[k % m], p->u_hi[k % m]); }
+  double best_obj = INFINITY;
+  int any_finite = 0;
+  int n_elite = (int)(pop * cfg->elite_frac);
+  if (n_elite < 1) n_elite = 1;
+  for (int it = 0; it < cfg->iterations; ++it) {
+    for (int c = 0; c < pop; ++c) {
+      double* u = cands + (size_t)c * dim;
+      if (it > 0 && c == 0) {
+        memcpy(u, best, sizeof(double) * dim);
+      } else {
+        for (size_t k = 0; k < dim; ++k) u[k] = mean[k] + stdv[k] * rng_normal(&rng);
+        for (size_t k = 0; k < dim; ++k) u[k] = clampd(u[k], p->u_lo[k % m], p->u_hi[k % m]);
+      }
+    }
+    for (int c = 0; c < pop; ++c) {
+      int dv;
+      scores[c] = plan_eval_one(&net, p, x0, cands + (size_t)c * dim, &dv);
+      okv[c] = !dv;
+    }
+    for (int c = 0; c < pop; ++c) order[c] = c;
+    g_sort_scores = scores;
+    qsort(order, (size_t)pop, sizeof(int), cmp_score_index);
+    const int top = order[0];
+    if (scores[top] < best_obj) { best_obj = scores[top]; memcpy(best, cands + (size_t)top * dim, sizeof(double) * dim); }
+    for (int e = 0; e < n_elite; ++e) if (okv[order[e]]) any_finite = 1;
+    best_history[it] = best_obj;
+    for (size_t k = 0; k < dim; ++k) {
+      double em = 0.0, ev = 0.0;
+      for (int e = 0; e < n_elite; ++e) em += cands[(size_t)order[e] * dim + k];
+      em /= n_elite;
+      for (int e = 0; e < n_elite; ++e) { const double d = cands[(size_t)order[e] * dim + k] - em; ev += d * d; }
+      const double es = sqrt(ev / n_elite);
+      mean[k] = cfg->smoothing * mean[k] + (1.0 - cfg->smoothing) * em;
+      stdv[k] = smax(1e-6, cfg->smoothing * stdv[k] + (1.0 - cfg->smoothing) * es);
+    }
+  }
+  *best_effort = !any_finite;
+  memcpy(best_actions, best, sizeof(double) * dim);
+  int dv;
+  *objective = plan_eval_one(&net, p, x0, best, &dv);
+  free(mean); free(stdv); free(best); free(cands); free(scores); free(okv); free(order); free(net.layers);
+  return REACH_OK;
+}

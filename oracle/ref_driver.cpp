@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "reach/dt_reach.hpp"
+#include "reach/mpc.hpp"
 #include "reach/neural.hpp"
 #include "reach/parallel.hpp"
 #include "reach/refine.hpp"
@@ -209,5 +210,93 @@ int ref_reach_with_splitting(const reach_net_desc* desc, const reach_split_args*
 }
 
 int ref_hardware_threads(void) { return hardware_threads(); }
+
+}  // extern "C"
+
+namespace {
+
+PlanProblem problem_from(const reach_net_desc* desc, const reach_plan_problem* p) {
+  PlanProblem prob;
+  prob.sys = make_sys(desc, p->n, p->m);
+  prob.x_goal.assign(p->x_goal, p->x_goal + p->n);
+  prob.q_weights.assign(p->q_weights, p->q_weights + p->n);
+  prob.r_weights.assign(p->r_weights, p->r_weights + p->m);
+  for (int c = 0; c < p->n_constraints; ++c) {
+    const reach_constraint& k = p->constraints[c];
+    Constraint con;
+    con.type = static_cast<Constraint::Type>(k.type);
+    con.dims.assign(k.dims, k.dims + k.n_dims);
+    const int kk = k.n_dims > 0 ? k.n_dims : p->n;
+    if (k.a) con.a.assign(k.a, k.a + kk);
+    con.b = k.b;
+    if (k.center) con.center.assign(k.center, k.center + kk);
+    con.radius = k.radius;
+    if (k.lo) con.lo.assign(k.lo, k.lo + kk);
+    if (k.hi) con.hi.assign(k.hi, k.hi + kk);
+    con.vmax = k.vmax;
+    prob.constraints.push_back(con);
+  }
+  prob.penalty = p->penalty;
+  prob.diverged_margin = p->diverged_margin;
+  prob.horizon = p->horizon;
+  prob.u_lo.assign(p->u_lo, p->u_lo + p->m);
+  prob.u_hi.assign(p->u_hi, p->u_hi + p->m);
+  prob.eps = p->eps;
+  prob.dt_prm.window = p->window;
+  prob.dt_prm.rebuild_from_box = p->rebuild_from_box != 0;
+  return prob;
+}
+
+}  // namespace
+
+extern "C" {
+
+// plan_eval (mpc.hpp:158-202) per candidate inside the reference parallel_for.
+int ref_plan_eval_batch(const reach_net_desc* desc, const reach_plan_problem* p, const double* x0, int32_t batch,
+                        const double* actions, double* objective, int32_t* diverged, int32_t threads) {
+  try {
+    PlanProblem prob = problem_from(desc, p);
+    prob.validate();
+    Vec<double> x(x0, x0 + p->n);
+    const int H = p->horizon, m = p->m;
+    parallel_for(
+        batch,
+        [&](int b) {
+          auto ev = plan_eval(prob, x, actions_at(actions + static_cast<size_t>(b) * H * m, H, m));
+          objective[b] = ev.objective;
+          diverged[b] = ev.diverged ? 1 : 0;
+        },
+        threads);
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+
+// plan_cem (mpc.hpp:258-368), the reference driver itself (its own parallel_for).
+int ref_plan_cem(const reach_net_desc* desc, const reach_plan_problem* p, const reach_sampler_config* c,
+                 const double* x0, double* best_actions, double* objective, double* best_history,
+                 int32_t* best_effort) {
+  try {
+    PlanProblem prob = problem_from(desc, p);
+    SamplerConfig cfg;
+    cfg.population = c->population;
+    cfg.elite_frac = c->elite_frac;
+    cfg.iterations = c->iterations;
+    cfg.init_std = c->init_std;
+    cfg.smoothing = c->smoothing;
+    cfg.refine_iters = c->refine_iters;
+    cfg.seed = c->seed;
+    auto res = plan_cem(prob, cfg, Vec<double>(x0, x0 + p->n));
+    for (int t = 0; t < p->horizon; ++t)
+      for (int j = 0; j < p->m; ++j) best_actions[t * p->m + j] = res.actions[static_cast<size_t>(t)][static_cast<size_t>(j)];
+    *objective = res.objective;
+    for (size_t i = 0; i < res.best_history.size(); ++i) best_history[i] = res.best_history[i];
+    *best_effort = res.best_effort ? 1 : 0;
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
 
 }  // extern "C"

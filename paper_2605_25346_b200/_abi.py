@@ -103,3 +103,32 @@ def decode_fail_key(key: int):
     if key == FAIL_KEY_NONE:
         return None
     return key >> 40, (key >> 8) & ((1 << 32) - 1), key & 0xFF
+
+
+# --- MPC (mpc.hpp) -----------------------------------------------------------
+CON_HALFSPACE_AVOID, CON_SPHERE_AVOID, CON_BOX_STAY_IN, CON_MAX_VOLUME = 0, 1, 2, 3
+
+
+class ConstraintC(C.Structure):
+    _fields_ = [
+        ("type", C.c_int32), ("n_dims", C.c_int32), ("dims", _ip), ("a", _dp), ("b", C.c_double),
+        ("center", _dp), ("radius", C.c_double), ("lo", _dp), ("hi", _dp), ("vmax", C.c_double),
+    ]
+
+
+class PlanProblemC(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("m", C.c_int32), ("horizon", C.c_int32), ("window", C.c_int32),
+        ("rebuild_from_box", C.c_int32),
+        ("x_goal", _dp), ("q_weights", _dp), ("r_weights", _dp),
+        ("n_constraints", C.c_int32), ("constraints", C.POINTER(ConstraintC)),
+        ("penalty", C.c_double), ("diverged_margin", C.c_double), ("eps", C.c_double),
+        ("u_lo", _dp), ("u_hi", _dp),
+    ]
+
+
+class SamplerConfigC(C.Structure):
+    _fields_ = [
+        ("population", C.c_int32), ("elite_frac", C.c_double), ("iterations", C.c_int32),
+        ("init_std", C.c_double), ("smoothing", C.c_double), ("refine_iters", C.c_int32), ("seed", C.c_uint64),
+    ]

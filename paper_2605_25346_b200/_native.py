@@ -48,6 +48,19 @@ def _declare(lib):
     lib.reach_ctx_kernel_time.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     lib.reach_measure_fp64_peak.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     lib.reach_debug_phase_cycles.argtypes = [vp, C.POINTER(C.c_uint64), C.c_int32]
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    lib.reach_plan_eval_batch.argtypes = [vp, vp, C.POINTER(A.PlanProblemC), dp, C.c_int32, dp, dp, ip,
+                                          C.POINTER(A.TubeOut), C.c_int32]
+    lib.reach_plan_cem.argtypes = [vp, vp, C.POINTER(A.PlanProblemC), C.POINTER(A.SamplerConfigC), dp, dp, dp, dp,
+                                   ip, C.POINTER(A.TubeOut)]
+    lib.reach_cem_create.argtypes = [C.POINTER(A.PlanProblemC), C.POINTER(A.SamplerConfigC), C.POINTER(vp)]
+    lib.reach_cem_destroy.argtypes = [vp]
+    lib.reach_cem_sample.argtypes = [vp, dp]
+    lib.reach_cem_update.argtypes = [vp, dp, ip]
+    lib.reach_cem_result.argtypes = [vp, dp, dp, ip, dp]
+    for f in ("reach_plan_eval_batch", "reach_plan_cem", "reach_cem_create", "reach_cem_destroy",
+              "reach_cem_sample", "reach_cem_update", "reach_cem_result"):
+        getattr(lib, f).restype = C.c_int
     lib.reach_debug_phase_cycles.restype = C.c_int
     for f in ("reach_ctx_create", "reach_ctx_destroy", "reach_ctx_set_stream", "reach_ctx_synchronize",
               "reach_net_upload", "reach_net_free", "reach_dt_batch", "reach_split_hull",

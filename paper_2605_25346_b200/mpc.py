@@ -1,0 +1,204 @@
+"""Reachability-aware MPC host API (mirrors mpc.hpp).
+
+    Constraint (mpc.hpp:26-110), PlanProblem (115-142), SamplerConfig (220-234),
+    plan_eval (158-202), plan_cem (258-368), with every candidate population
+    evaluated on the device (C ABI reach_plan_eval_batch / reach_plan_cem).
+Gradient refinement of the top candidate (refine_iters > 0) is outside the
+device path and raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _abi as A
+from ._native import Context, default_context
+from .api import DTReachParams, DTSystem, TubeBatch
+
+
+@dataclass
+class Constraint:
+    type: int = A.CON_MAX_VOLUME
+    dims: List[int] = field(default_factory=list)
+    a: Optional[np.ndarray] = None
+    b: float = 0.0
+    center: Optional[np.ndarray] = None
+    radius: float = 0.0
+    lo: Optional[np.ndarray] = None
+    hi: Optional[np.ndarray] = None
+    vmax: float = 0.0
+
+    HALFSPACE_AVOID, SPHERE_AVOID, BOX_STAY_IN, MAX_VOLUME = 0, 1, 2, 3
+
+
+@dataclass
+class PlanProblem:
+    sys: DTSystem
+    x_goal: np.ndarray
+    q_weights: np.ndarray
+    r_weights: np.ndarray
+    constraints: List[Constraint] = field(default_factory=list)
+    penalty: float = 100.0
+    diverged_margin: float = 1e3
+    horizon: int = 5
+    u_lo: Optional[np.ndarray] = None
+    u_hi: Optional[np.ndarray] = None
+    eps: float = 0.0
+    dt_prm: DTReachParams = field(default_factory=DTReachParams)
+
+    def c_struct(self):
+        """(reach_plan_problem, keepalive)."""
+        keep = []
+
+        def arr(x, dt=np.float64):
+            if x is None:
+                return None
+            a = np.ascontiguousarray(np.asarray(x, dtype=dt))
+            keep.append(a)
+            return a
+
+        cons = (A.ConstraintC * max(1, len(self.constraints)))()
+        for i, c in enumerate(self.constraints):
+            dims = arr(c.dims, np.int32) if c.dims else None
+            cons[i] = A.ConstraintC(int(c.type), len(c.dims), A.iptr(dims), A.dptr(arr(c.a)), float(c.b),
+                                    A.dptr(arr(c.center)), float(c.radius), A.dptr(arr(c.lo)), A.dptr(arr(c.hi)),
+                                    float(c.vmax))
+        keep.append(cons)
+        p = A.PlanProblemC(self.sys.n, self.sys.m, self.horizon, self.dt_prm.window, int(self.dt_prm.rebuild_from_box),
+                           A.dptr(arr(self.x_goal)), A.dptr(arr(self.q_weights)),
+                           A.dptr(arr(self.r_weights if self.sys.m else np.zeros(1))),
+                           len(self.constraints), cons, float(self.penalty), float(self.diverged_margin),
+                           float(self.eps), A.dptr(arr(self.u_lo if self.sys.m else np.zeros(1))),
+                           A.dptr(arr(self.u_hi if self.sys.m else np.zeros(1))))
+        return p, keep
+
+
+@dataclass
+class SamplerConfig:
+    population: int = 256
+    elite_frac: float = 0.1
+    iterations: int = 5
+    init_std: float = 0.3
+    smoothing: float = 0.5
+    refine_iters: int = 5
+    seed: int = 0
+
+    def c_struct(self):
+        return A.SamplerConfigC(self.population, self.elite_frac, self.iterations, self.init_std, self.smoothing,
+                                self.refine_iters, self.seed)
+
+
+@dataclass
+class PlanBatch:
+    objective: np.ndarray
+    diverged: np.ndarray
+    tubes: Optional[TubeBatch] = None
+
+
+def plan_eval_batch(prob: PlanProblem, x0, actions: np.ndarray, with_tubes: bool = False,
+                    ctx: Optional[Context] = None) -> PlanBatch:
+    """plan_eval (mpc.hpp:158-202) for actions [B][H][m] from one x0."""
+    prob.sys.validate()
+    ctx = ctx or default_context()
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    acts = np.ascontiguousarray(actions, dtype=np.float64)
+    B = acts.shape[0]
+    if acts.shape[1:] != (prob.horizon, prob.sys.m):
+        raise ValueError("plan_eval: action count != horizon")
+    obj = np.zeros(B)
+    div = np.zeros(B, np.int32)
+    tubes = None
+    to_p = None
+    if with_tubes:
+        H, n = prob.horizon, prob.sys.n
+        tubes = TubeBatch(np.full((B, H + 1, n), np.nan), np.full((B, H + 1, n), np.nan), np.zeros(B, np.int32),
+                          np.zeros(B, np.int32), np.zeros(B, np.int32))
+        to = A.TubeOut(A.dptr(tubes.lo), A.dptr(tubes.hi), A.iptr(tubes.n_boxes), A.iptr(tubes.failed_step),
+                       A.iptr(tubes.status))
+        to_p = C.byref(to)
+    p, keep = prob.c_struct()
+    net = ctx.upload(prob.sys.step)
+    ctx.check(ctx._lib.reach_plan_eval_batch(ctx.handle, net, C.byref(p), A.dptr(x0), B, A.dptr(acts), A.dptr(obj),
+                                             A.iptr(div), to_p, 0), "plan_eval")
+    return PlanBatch(obj, div.astype(bool), tubes)
+
+
+def plan_eval(prob: PlanProblem, x0, actions, ctx: Optional[Context] = None):
+    r = plan_eval_batch(prob, x0, np.asarray(actions, np.float64)[None], with_tubes=True, ctx=ctx)
+    return r.objective[0], r.diverged[0], r.tubes.tube(0)
+
+
+@dataclass
+class PlanResult:
+    actions: np.ndarray       # [H][m]
+    objective: float
+    best_history: np.ndarray  # [iterations]
+    best_effort: bool
+    tube: object = None
+
+
+def plan_cem(prob: PlanProblem, cfg: SamplerConfig, x0, ctx: Optional[Context] = None) -> PlanResult:
+    """plan_cem (mpc.hpp:258-368); refine_iters must be 0 on the device path."""
+    if cfg.refine_iters != 0:
+        raise NotImplementedError("plan_cem: gradient refinement (refine_iters > 0) is not on the device path")
+    prob.sys.validate()
+    ctx = ctx or default_context()
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    H, m, n = prob.horizon, prob.sys.m, prob.sys.n
+    best = np.zeros((H, m))
+    obj = np.zeros(1)
+    hist = np.zeros(cfg.iterations)
+    be = np.zeros(1, np.int32)
+    tb = TubeBatch(np.full((1, H + 1, n), np.nan), np.full((1, H + 1, n), np.nan), np.zeros(1, np.int32),
+                   np.zeros(1, np.int32), np.zeros(1, np.int32))
+    to = A.TubeOut(A.dptr(tb.lo), A.dptr(tb.hi), A.iptr(tb.n_boxes), A.iptr(tb.failed_step), A.iptr(tb.status))
+    p, keep = prob.c_struct()
+    c = cfg.c_struct()
+    net = ctx.upload(prob.sys.step)
+    ctx.check(ctx._lib.reach_plan_cem(ctx.handle, net, C.byref(p), C.byref(c), A.dptr(x0), A.dptr(best),
+                                      A.dptr(obj), A.dptr(hist), A.iptr(be), C.byref(to)), "plan_cem")
+    return PlanResult(best, float(obj[0]), hist, bool(be[0]), tb.tube(0))
+
+
+class CEM:
+    """plan_cem's loop in pieces (sample -> evaluate a shard -> gather -> update)
+    for multi-GPU drivers; identical sampling stream on every rank."""
+
+    def __init__(self, prob: PlanProblem, cfg: SamplerConfig):
+        from ._native import lib
+        self._lib = lib()
+        self.prob, self.cfg = prob, cfg
+        self._p, self._keep = prob.c_struct()
+        self._c = cfg.c_struct()
+        h = C.c_void_p()
+        rc = self._lib.reach_cem_create(C.byref(self._p), C.byref(self._c), C.byref(h))
+        if rc != 0:
+            raise ValueError(f"reach_cem_create failed ({rc})")
+        self.h = h
+
+    def sample(self) -> np.ndarray:
+        out = np.zeros((self.cfg.population, self.prob.horizon, self.prob.sys.m))
+        assert self._lib.reach_cem_sample(self.h, A.dptr(out)) == 0
+        return out
+
+    def update(self, scores: np.ndarray, ok: np.ndarray):
+        s = np.ascontiguousarray(scores, np.float64)
+        o = np.ascontiguousarray(ok, np.int32)
+        assert self._lib.reach_cem_update(self.h, A.dptr(s), A.iptr(o)) == 0
+
+    def result(self):
+        best = np.zeros((self.prob.horizon, self.prob.sys.m))
+        obj = np.zeros(1)
+        be = np.zeros(1, np.int32)
+        hist = np.zeros(self.cfg.iterations)
+        assert self._lib.reach_cem_result(self.h, A.dptr(best), A.dptr(obj), A.iptr(be), A.dptr(hist)) == 0
+        return best, float(obj[0]), bool(be[0]), hist
+
+    def __del__(self):
+        try:
+            self._lib.reach_cem_destroy(self.h)
+        except Exception:
+            pass

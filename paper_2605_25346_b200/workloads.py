@@ -125,3 +125,27 @@ def small_batch(seed: int, n: int, m: int, hidden: List[int], batch: int, horizo
     r = rng.uniform(0.2 * eps, eps, size=(batch, n))
     acts = rng.uniform(-0.5, 0.5, size=(batch, horizon, m))
     return BatchWorkload(DTSystem(net, n, m), c - r, c + r, acts)
+
+
+def c3_tpushing(seed: int = MASTER_SEED, population: int = 4096, horizon: int = 20, iterations: int = 5):
+    """BASELINE configs[2]: T-pushing reachability-aware MPC -- 7->96x3->5 ReLU
+    learned dynamics (n=5 object/pusher state, m=2 push action), H=20, planning
+    radius eps=0.005 around x0=0, U=[-1,1]^2, one box-stay-in constraint on the
+    object position, CEM with 4096 candidates x 5 iterations, no gradient refine
+    (SURVEY.md §8 shape sheet C3 / §8d)."""
+    from .mpc import Constraint, PlanProblem, SamplerConfig
+    rng = np.random.default_rng(seed + 3)
+    n, m = 5, 2
+    net = residual_relu_dynamics(rng, n, m, [96, 96, 96], dt=0.1)
+    prob = PlanProblem(
+        sys=DTSystem(net, n, m),
+        x_goal=np.array([0.4, 0.25, 0.0, 0.0, 0.0]),
+        q_weights=np.array([1.0, 1.0, 0.1, 0.1, 0.1]),
+        r_weights=np.array([0.01, 0.01]),
+        constraints=[Constraint(type=Constraint.BOX_STAY_IN, dims=[0, 1], lo=np.array([-0.3, -0.3]),
+                                hi=np.array([0.45, 0.3]))],
+        penalty=100.0, diverged_margin=1e3, horizon=horizon,
+        u_lo=np.array([-1.0, -1.0]), u_hi=np.array([1.0, 1.0]), eps=0.005)
+    cfg = SamplerConfig(population=population, elite_frac=0.1, iterations=iterations, init_std=0.3, smoothing=0.5,
+                        refine_iters=0, seed=seed)
+    return prob, cfg, np.zeros(n)

@@ -135,3 +135,63 @@ def assert_tubes_equal(got: TubeBatch, exp: TubeBatch, exact=True, rtol=1e-12):
                 fin = np.isfinite(e)
                 scale = np.maximum(np.abs(e[fin]), 1e-300)
                 assert np.all(np.abs(g[fin] - e[fin]) <= rtol * np.maximum(scale, 1.0)), b
+
+
+# --- MPC -------------------------------------------------------------------
+def _mpc_fn(lib, name, argtypes):
+    f = getattr(lib, name)
+    f.argtypes = argtypes
+    f.restype = C.c_int
+    return f
+
+
+def _plan_eval(lib, prefix, prob, x0, actions, threads=None):
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    args = [C.POINTER(A.NetDesc), C.POINTER(A.PlanProblemC), dp, C.c_int32, dp, dp, ip]
+    if prefix == "ref_":
+        args.append(C.c_int32)
+    f = _mpc_fn(lib, prefix + "plan_eval_batch", args)
+    x0 = np.ascontiguousarray(x0, np.float64)
+    acts = np.ascontiguousarray(actions, np.float64)
+    B = acts.shape[0]
+    obj = np.zeros(B)
+    div = np.zeros(B, np.int32)
+    desc, keep = prob.sys.step.desc()
+    p, keep2 = prob.c_struct()
+    extra = [threads or 0] if prefix == "ref_" else []
+    rc = f(C.byref(desc), C.byref(p), A.dptr(x0), B, A.dptr(acts), A.dptr(obj), A.iptr(div), *extra)
+    assert rc == 0, rc
+    return obj, div.astype(bool)
+
+
+def oracle_plan_eval_batch(prob, x0, actions):
+    return _plan_eval(oracle_lib(), "orc_", prob, x0, actions)
+
+
+def ref_plan_eval_batch(prob, x0, actions, threads=0):
+    return _plan_eval(ref_lib(), "ref_", prob, x0, actions, threads)
+
+
+def _plan_cem(lib, prefix, prob, cfg, x0):
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    f = _mpc_fn(lib, prefix + "plan_cem", [C.POINTER(A.NetDesc), C.POINTER(A.PlanProblemC),
+                                           C.POINTER(A.SamplerConfigC), dp, dp, dp, dp, ip])
+    x0 = np.ascontiguousarray(x0, np.float64)
+    best = np.zeros((prob.horizon, prob.sys.m))
+    obj = np.zeros(1)
+    hist = np.zeros(cfg.iterations)
+    be = np.zeros(1, np.int32)
+    desc, keep = prob.sys.step.desc()
+    p, keep2 = prob.c_struct()
+    c = cfg.c_struct()
+    rc = f(C.byref(desc), C.byref(p), C.byref(c), A.dptr(x0), A.dptr(best), A.dptr(obj), A.dptr(hist), A.iptr(be))
+    assert rc == 0, rc
+    return best, float(obj[0]), hist, bool(be[0])
+
+
+def oracle_plan_cem(prob, cfg, x0):
+    return _plan_cem(oracle_lib(), "orc_", prob, cfg, x0)
+
+
+def ref_plan_cem(prob, cfg, x0):
+    return _plan_cem(ref_lib(), "ref_", prob, cfg, x0)
