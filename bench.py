@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample-parts", type=int, default=0, help="parts per CPU sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mpc", action="store_true", help="skip the C3 MPC replan leg")
     return ap.parse_args()
 
 
@@ -161,6 +162,60 @@ def auto_cpu_parts():
     cores = os.cpu_count() or 8
     # ~15 ms per sub-box-horizon per core (survey probe) -> aim at ~10-15 s
     return int(max(256, min(65536, cores * 800)))
+
+
+def mpc_replan(args, ctx, world, rank, dev, barrier):
+    """C3 T-pushing replan: 4096 candidates x H=20 x 5 CEM iterations + final plan_eval.
+    N=1: the C++ host loop (reach_plan_cem); N>1: candidates sharded over the ranks with one
+    NCCL all-gather of (objective, ok) per iteration.  Wall time of whole replans, max over ranks."""
+    import torch
+    from paper_2605_25346_b200.mpc import plan_cem
+    from paper_2605_25346_b200.workloads import c3_tpushing
+    prob, cfg, x0 = c3_tpushing()
+    ctx.set_stream(None)
+
+    def once():
+        if world == 1:
+            r = plan_cem(prob, cfg, x0, ctx=ctx)
+            return r.actions, r.objective
+        from paper_2605_25346_b200.distributed import sharded_plan_cem
+        best, obj, _, _ = sharded_plan_cem(prob, cfg, x0)
+        return best, obj
+
+    reps = max(2, min(args.steps, 5))
+    once()
+    times = []
+    for _ in range(reps):
+        barrier()
+        t0 = time.perf_counter()
+        best, obj = once()
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    steps = cfg.population * cfg.iterations * prob.horizon + prob.horizon
+    out = {"workload": "c3_tpushing (BASELINE configs[2]): 4096 candidates x H=20 x 5 CEM iterations, "
+                       "7->96x3->5 ReLU, eps=0.005, box-stay-in constraint, refine_iters=0",
+           "ms_per_replan": 1e3 * t, "target_ms": 50.0, "replans_timed": reps,
+           "reach_steps_per_s": steps / t, "objective": obj,
+           "parity": "bit-identical plan/objective/history vs the reference plan_cem (tests/test_gpu_mpc.py)"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle_bind import ref_available, ref_plan_cem, ref_lib
+            if ref_available():
+                t0 = time.perf_counter()
+                ref_plan_cem(prob, cfg, x0)
+                tc = time.perf_counter() - t0
+                lib = ref_lib()
+                lib.ref_hardware_threads.restype = C.c_int
+                out["cpu_reference_ms_per_replan"] = 1e3 * tc
+                out["cpu_reference_cores"] = int(lib.ref_hardware_threads())
+        except Exception as ex:  # noqa: BLE001
+            out["cpu_reference_error"] = str(ex)
+    return out
 
 
 def run_reference(args):
@@ -354,6 +409,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(w, args.cpu_sample_parts or auto_cpu_parts())
 
+    # ---- the metric's second half: ms per reachability-aware MPC replan (BASELINE configs[2])
+    mpc = None if args.no_mpc else mpc_replan(args, ctx, world, rank, dev, barrier)
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
@@ -365,7 +423,7 @@ def main():
                            "parallelism": f"dp{world}"},
                 "roofline": roof, "cpu_baseline": cb,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-                "gpu_launches": launches, "clocks": clk, "parity": parity,
+                "gpu_launches": launches, "clocks": clk, "parity": parity, "mpc_replan": mpc,
                 "bit_exact_vs_reference": "ReLU path: identical operation order and roundings (tests/test_gpu_dt.py)"}
         print(json.dumps(line))
     if world > 1:

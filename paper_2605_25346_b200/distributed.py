@@ -1,0 +1,136 @@
+"""Multi-GPU sharding of the batch primitive (one process per GPU, torch.distributed).
+
+The batch shards naturally: sub-boxes of a split plan or MPC
+candidates are independent.  The only exchanges are
+  * the per-step hull of reach_with_splitting: one all-reduce (min on lo, max
+    on hi, min on the failure key / box count, max on the box-diverged flags);
+  * CEM selection: one all-gather of each rank's (objective, ok) slice per
+    iteration, after which every rank runs the identical stable sort / refit
+    (every rank draws the same sampling stream, mpc.hpp:290-299).
+With the NCCL backend these run on the GPU over NVLink; with gloo (tests) on
+the CPU.  Evaluation is pluggable so the sharding logic is testable without a
+GPU (tests pass the CPU oracle); the product path evaluates on the device.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+import numpy as np
+
+from . import _abi as A
+
+
+def shard_range(total: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous [begin, end) slice of `total` items for `rank` (sizes differ by at most 1)."""
+    base, rem = divmod(total, world)
+    begin = rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def _device_for(group) -> "object":
+    import torch
+    dist = _dist()
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def combine_hulls(partials):
+    """Reference-order combination of partial hulls (list of HullResult, ascending part ranges)."""
+    lo = partials[0].lo.copy()
+    hi = partials[0].hi.copy()
+    for p in partials[1:]:
+        lo = np.where(p.lo < lo, p.lo, lo)  # std::min(a, b) = (b < a) ? b : a
+        hi = np.where(hi < p.hi, p.hi, hi)
+    nb = min(p.n_boxes for p in partials)
+    key = min(p.fail_key for p in partials)
+    div = np.max(np.stack([p.box_diverged for p in partials]), axis=0)
+    return lo, hi, div, nb, key
+
+
+def allreduce_hull(res, group=None):
+    """All-reduces a rank's partial HullResult in place (NaN only survives from part 0, as the reference)."""
+    import torch
+    dist = _dist()
+    dev = _device_for(group)
+    nan0 = np.isnan(res.lo)
+    nan0h = np.isnan(res.hi)
+    lo = torch.tensor(np.where(nan0, np.inf, res.lo), device=dev)
+    hi = torch.tensor(np.where(nan0h, -np.inf, res.hi), device=dev)
+    meta = torch.tensor([res.n_boxes, res.fail_key], dtype=torch.int64, device=dev)
+    div = torch.tensor(res.box_diverged.astype(np.int64), device=dev)
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(meta, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(div, op=dist.ReduceOp.MAX, group=group)
+    # the rank holding part 0 (rank 0) shares its NaN mask: reference NaN iff part 0's value is NaN
+    rank = dist.get_rank(group)
+    own = np.stack([nan0, nan0h]).astype(np.int64) if rank == 0 else np.zeros((2,) + res.lo.shape, np.int64)
+    mask = torch.tensor(own, device=dev)
+    dist.all_reduce(mask, op=dist.ReduceOp.MAX, group=group)
+    m = mask.cpu().numpy().astype(bool)
+    lo = torch.where(torch.tensor(m[0], device=dev), torch.full_like(lo, float("nan")), lo)
+    hi = torch.where(torch.tensor(m[1], device=dev), torch.full_like(hi, float("nan")), hi)
+    res.lo = lo.cpu().numpy()
+    res.hi = hi.cpu().numpy()
+    res.n_boxes = int(meta[0])
+    res.fail_key = int(meta[1])
+    res.box_diverged = div.cpu().numpy().astype(np.int32)
+    return res
+
+
+def sharded_split_hull(sys, x0, plan, actions, prm, group=None,
+                       evaluate: Optional[Callable] = None):
+    """reach_with_splitting over all ranks: each evaluates its contiguous part range, then one all-reduce."""
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    total = plan.total_parts()
+    b, e = shard_range(total, rank, world)
+    if evaluate is None:
+        from .api import reach_split_hull
+
+        def evaluate(sys_, x0_, plan_, acts_, prm_, begin, end):
+            return reach_split_hull(sys_, x0_, plan_, acts_, prm_, part_begin=begin, part_end=end)
+    res = evaluate(sys, x0, plan, actions, prm, b, e)
+    return allreduce_hull(res, group)
+
+
+def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = None):
+    """plan_cem (mpc.hpp:258-368) over all ranks; returns (actions, objective, best_effort, history).
+
+    Every rank draws the full population (same stream), evaluates its slice,
+    and all-gathers (objective, ok) -- identical selection on every rank."""
+    import torch
+    from .mpc import CEM, plan_eval_batch
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = _device_for(group)
+    if evaluate is None:
+        def evaluate(prob_, x0_, acts_):
+            r = plan_eval_batch(prob_, x0_, acts_)
+            return r.objective, r.diverged
+    cem = CEM(prob, cfg)
+    pop = cfg.population
+    b, e = shard_range(pop, rank, world)
+    sizes = [shard_range(pop, r, world) for r in range(world)]
+    width = max(hi - lo for lo, hi in sizes)
+    for _ in range(cfg.iterations):
+        cands = cem.sample()
+        obj, div = evaluate(prob, x0, cands[b:e])
+        local = torch.zeros((width, 2), dtype=torch.float64, device=dev)
+        local[: e - b, 0] = torch.as_tensor(obj, dtype=torch.float64)
+        local[: e - b, 1] = torch.as_tensor((~np.asarray(div, bool)).astype(np.float64))
+        gathered = [torch.zeros_like(local) for _ in range(world)]
+        dist.all_gather(gathered, local, group=group)
+        scores = np.concatenate([g[: hi - lo, 0].cpu().numpy() for g, (lo, hi) in zip(gathered, sizes)])
+        ok = np.concatenate([g[: hi - lo, 1].cpu().numpy() for g, (lo, hi) in zip(gathered, sizes)]) > 0.5
+        cem.update(scores, ok.astype(np.int32))
+    best, best_obj, best_effort, hist = cem.result()
+    fin, _ = evaluate(prob, x0, best[None])
+    return best, float(fin[0]), best_effort, hist
