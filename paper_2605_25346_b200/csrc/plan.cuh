@@ -2,10 +2,8 @@
 //
 // plan_eval = nominal rollout through the one-step network + quadratic stage
 // costs, then constraint penalties over the certified tube (computed by the
-// DT horizon kernel).  One warp per candidate: the rollout's layer outputs
-// are spread over the lanes (each a sequential dot product over the inputs,
-// as MLPNet::forward's matvec, linalg.hpp:40-51), the objective is summed by
-// lane 0 in the reference's order with separate multiply / add roundings.
+// DT horizon kernel), all in the reference's operation order with separate
+// multiply / add roundings.
 #pragma once
 
 #include "dt_common.cuh"
@@ -91,57 +89,68 @@ __device__ inline double con_margin(const PlanParams& P, const DevConstraint& c,
   }
 }
 
-// One warp per candidate: nominal rollout + stage costs + tube penalties.
-// Shared memory: per warp two vectors of `vec` doubles (layer input / output).
-__global__ void __launch_bounds__(256) plan_objective_kernel(const PlanParams P, int vec) {
+// One warp per candidate, kPlanWarps candidates per block.  Per step and
+// layer the block stages W_l^T once in shared memory (coalesced), then every
+// warp runs the layer with lanes over output units, each output a sequential
+// dot product over the inputs exactly as MLPNet::forward's matvec
+// (linalg.hpp:40-51); lane 0 sums the objective in the reference's order.
+constexpr int kPlanWarps = 16;
+
+__global__ void __launch_bounds__(kPlanWarps * 32) plan_objective_kernel(const PlanParams P, int vec, int wmax) {
   extern __shared__ __align__(16) double psm[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int b = blockIdx.x * (blockDim.x / 32) + warp;
-  if (b >= P.B) return;
-  double* vin = psm + static_cast<size_t>(warp) * 2 * vec;
+  const int b = blockIdx.x * kPlanWarps + warp;
+  const bool live = b < P.B;
+  double* wsm = psm;                                      // staged W_l^T: cols x rows (ld = rows)
+  double* vin = psm + wmax + static_cast<size_t>(warp) * 2 * vec;
   double* vout = vin + vec;
   const DevNet& N = P.net;
   const int n = P.n, m = P.m, H = P.H, L = N.L;
-  const double* acts = P.actions + static_cast<size_t>(b) * H * m;
+  const double* acts = P.actions + static_cast<size_t>(live ? b : 0) * H * m;
   double x_reg = (lane < n) ? P.x0[lane] : 0.0;  // lane d holds x_d between steps
   double obj = 0.0;                               // lane 0's running objective
   for (int t = 0; t < H; ++t) {
     const double* u = acts + static_cast<size_t>(t) * m;
-    // in = [x; u]
     if (lane < n) vin[lane] = x_reg;
     for (int j = lane; j < m; j += 32) vin[n + j] = u[j];
-    __syncwarp();
+    double* a = vin;
+    double* o = vout;
     for (int l = 0; l < L; ++l) {
       const int rows = N.dims[l + 1], cols = N.dims[l];
       const double* wt = N.blob + N.wt_off[l];
       const int ld = N.ldt[l];
+      __syncthreads();  // previous layer done with wsm
+      for (int q = threadIdx.x; q < cols * rows; q += blockDim.x) {
+        const int j = q / rows, oo = q % rows;
+        wsm[q] = __ldg(wt + static_cast<size_t>(j) * ld + oo);
+      }
+      __syncthreads();
       const double* bias = N.blob + N.b_off[l];
       const int act = N.acts[l];
-      for (int o = lane; o < rows; o += 32) {
+      for (int o0 = lane; o0 < rows; o0 += 32) {
         double acc = 0.0;
-        for (int j = 0; j < cols; ++j) acc = add(acc, mul(__ldg(wt + static_cast<size_t>(j) * ld + o), vin[j]));
-        double v = add(acc, __ldg(bias + o));
+        for (int j = 0; j < cols; ++j) acc = add(acc, mul(wsm[j * rows + o0], a[j]));
+        double v = add(acc, __ldg(bias + o0));
         if (act == 0) v = (v < 0.0) ? 0.0 : v;  // MLPNet::h_relu (neural.hpp:85-87)
         else if (act == 1) v = tanh(v);
-        vout[o] = v;
+        o[o0] = v;
       }
       __syncwarp();
-      double* tmp = vin;
-      vin = vout;
-      vout = tmp;
+      double* tmp = a;
+      a = o;
+      o = tmp;
     }
-    // vin now holds x_{t+1}
-    if (lane < n) x_reg = vin[lane];
-    if (lane == 0) {
+    if (lane < n) x_reg = a[lane];
+    if (lane == 0) {  // stage costs (mpc.hpp:171-183)
       for (int j = 0; j < m; ++j) obj = add(obj, mul(mul(P.r_w[j], u[j]), u[j]));
       for (int j = 0; j < n; ++j) {
-        const double d = sub(vin[j], P.x_goal[j]);
+        const double d = sub(a[j], P.x_goal[j]);
         obj = add(obj, mul(mul(P.q_w[j], d), d));
       }
     }
     __syncwarp();
   }
-  if (lane != 0) return;
+  if (lane != 0 || !live) return;
   const int nb = P.n_boxes[b];
   for (int t = 1; t <= H; ++t) {
     const double* lo = P.tube_lo + (static_cast<size_t>(b) * (H + 1) + t) * n;

@@ -23,7 +23,9 @@
 #include "dt_kernel.cuh"
 #include "plan.cuh"
 
+#include <atomic>
 #include <random>
+#include <thread>
 
 struct reach_ctx {
   int device = 0;
@@ -36,6 +38,9 @@ struct reach_ctx {
   // growable device workspace for host-pointer calls
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  // plan-problem staging buffer (goal, weights, constraints) for the MPC kernels
+  void* pbuf = nullptr;
+  size_t pbuf_bytes = 0;
   // kernel timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
@@ -279,6 +284,7 @@ int reach_ctx_destroy(reach_ctx* ctx) {
   if (!ctx) return REACH_OK;
   cudaSetDevice(ctx->device);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->pbuf) cudaFree(ctx->pbuf);
   for (auto& p : ctx->ev_used) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   for (auto& p : ctx->ev_free) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -775,10 +781,16 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
   // objective kernel: problem arrays staged after the tube in the plan workspace
   PlanBuffers pb;
   pack_problem(p, pb);
-  double* d_db = nullptr;
-  int* d_ib = nullptr;
-  RB_CUDA(cudaMallocAsync(&d_db, pb.db.size() * 8 + 8, ctx->stream));
-  RB_CUDA(cudaMallocAsync(&d_ib, pb.ib.size() * 4, ctx->stream));
+  const size_t need = align_up(pb.db.size() * 8 + 8, 256) + pb.ib.size() * 4;
+  if (need > ctx->pbuf_bytes) {
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->pbuf) cudaFree(ctx->pbuf);
+    ctx->pbuf = nullptr;
+    RB_CUDA(cudaMalloc(&ctx->pbuf, need));
+    ctx->pbuf_bytes = need;
+  }
+  double* d_db = static_cast<double*>(ctx->pbuf);
+  int* d_ib = reinterpret_cast<int*>(static_cast<char*>(ctx->pbuf) + align_up(pb.db.size() * 8 + 8, 256));
   RB_CUDA(cudaMemcpyAsync(d_db, pb.db.data(), pb.db.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
   RB_CUDA(cudaMemcpyAsync(d_ib, pb.ib.data(), pb.ib.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
   rb::PlanParams Q = pb.P;
@@ -803,14 +815,17 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
   int vec = 0;
   for (int l = 0; l <= net->L; ++l) vec = std::max(vec, net->dims[l]);
   vec = (vec + 1) & ~1;
-  const int wpb = 8;
-  const size_t smem = static_cast<size_t>(wpb) * 2 * vec * 8;
+  int wmax = 0;
+  for (int l = 0; l < net->L; ++l) wmax = std::max(wmax, net->dims[l] * net->dims[l + 1]);
+  wmax = (wmax + 1) & ~1;
+  const size_t smem = (static_cast<size_t>(wmax) + static_cast<size_t>(rb::kPlanWarps) * 2 * vec) * 8;
+  if (smem > static_cast<size_t>(ctx->max_smem))
+    return fail(ctx, REACH_E_UNSUPPORTED, "plan_eval: layer too large for the staged rollout");
   RB_CUDA(cudaFuncSetAttribute(rb::plan_objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
-  rb::plan_objective_kernel<<<(batch + wpb - 1) / wpb, 32 * wpb, smem, ctx->stream>>>(Q, vec);
+  rb::plan_objective_kernel<<<(batch + rb::kPlanWarps - 1) / rb::kPlanWarps, 32 * rb::kPlanWarps, smem,
+                              ctx->stream>>>(Q, vec, wmax);
   RB_CUDA(cudaGetLastError());
-  RB_CUDA(cudaFreeAsync(d_db, ctx->stream));
-  RB_CUDA(cudaFreeAsync(d_ib, ctx->stream));
   ctx->launches += 2;
   return REACH_OK;
 }
@@ -1032,10 +1047,43 @@ int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_proble
   if (rc) return fail(ctx, rc, "SamplerConfig: invalid configuration");
   std::unique_ptr<reach_cem> guard(c);
   const size_t dim = c->mean.size(), pop = cfg->population;
+  const int iters = cfg->iterations;
+  // The normal stream does not depend on mean/std, so it is drawn ahead on a
+  // worker thread (same sequential order as mpc.hpp:290-299) while the device
+  // evaluates the previous population.
+  const size_t per_it0 = pop * dim, per_it = (pop - 1) * dim;
+  std::vector<double> z(per_it0 + static_cast<size_t>(iters - 1) * per_it);
+  std::atomic<int> ready{0};
+  std::thread gen([&] {
+    size_t o = 0;
+    for (int it = 0; it < iters; ++it) {
+      const size_t cnt = it == 0 ? per_it0 : per_it;
+      for (size_t q = 0; q < cnt; ++q) z[o + q] = c->normal();
+      o += cnt;
+      ready.store(it + 1, std::memory_order_release);
+    }
+  });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{gen};
   std::vector<double> cand(pop * dim), scores(pop);
   std::vector<int32_t> okv(pop), div(pop);
-  for (int it = 0; it < cfg->iterations; ++it) {
-    reach_cem_sample(c, cand.data());
+  size_t zo = 0;
+  for (int it = 0; it < iters; ++it) {
+    while (ready.load(std::memory_order_acquire) <= it) std::this_thread::yield();
+    for (size_t k = 0; k < pop; ++k) {  // reach_cem_sample with the pre-drawn normals
+      std::vector<double>& u = c->cands[k];
+      if (it > 0 && k == 0) {
+        u = c->best;
+      } else {
+        for (size_t q = 0; q < dim; ++q) u[q] = c->mean[q] + c->stdv[q] * z[zo++];
+        c->clip(u);
+      }
+      std::copy(u.begin(), u.end(), cand.begin() + k * dim);
+    }
     rc = plan_eval_host(ctx, net, prob, x0, static_cast<int>(pop), cand.data(), scores.data(), div.data(), nullptr);
     if (rc) return rc;
     for (size_t k = 0; k < pop; ++k) okv[k] = div[k] ? 0 : 1;
