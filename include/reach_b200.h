@@ -51,6 +51,9 @@ enum reach_tube_status {
   REACH_TUBE_NONFINITE_PREACT = 1, /* "relax_activation: non-finite preactivation" (neural.hpp:171) */
   REACH_TUBE_DIVERGED_CERT = 2,    /* "diverged certification" (dt_reach.hpp:65) */
   REACH_TUBE_DIVERGED_BOX = 3,     /* "diverged box" (dt_reach.hpp:98) */
+  REACH_TUBE_CTL_FAILED = 4,       /* "controller certification failed: relax_activation: non-finite preactivation"
+                                      (closed_loop.hpp:106-109) */
+  REACH_TUBE_CTL_DIVERGED = 5,     /* "controller certification diverged" (closed_loop.hpp:111-114) */
   REACH_TUBE_OTHER = 99            /* any other reference exception text */
 };
 
@@ -202,6 +205,15 @@ int reach_net_free(reach_ctx* ctx, reach_net* net);
  * and returns without synchronizing. */
 int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* args,
                    const reach_tube_out* out, int32_t flags);
+
+/* DT closed loop (the cl_reach stacking of closed_loop.hpp:
+ * 118-153 on a discrete-time one-step network): per step u = ctl_crown(x_tm,
+ * ctl) (neural.hpp:418), the symbolic state is stacked to [x; u] over the shared
+ * variables (control remainder as a fresh diagonal block), the dynamics network
+ * (n + l inputs -> n outputs) is certified on it, then re-seed / fold / box as
+ * dt_reach.  args->m must be 0 (the control comes from the controller). */
+int reach_dtcl_batch(reach_ctx* ctx, const reach_net* dyn, const reach_net* ctl, const reach_dt_args* args,
+                     const reach_tube_out* out, int32_t flags);
 
 /* reach_with_splitting(dt_reach) on the device: split, per-part horizon,
  * hull reduction, all without materializing per-part tubes.  The X0 box and

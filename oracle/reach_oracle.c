@@ -746,3 +746,170 @@ int orc_plan_cem(const reach_net_desc* desc, const reach_plan_problem* p, const 
   free(mean); free(stdv); free(best); free(cands); free(scores); free(okv); free(order); free(net.layers);
   return REACH_OK;
 }
+
+/* ======================================================================= */
+/* DT closed loop: the composition of reference        */
+/* functions mirroring cl_reach's stacking (closed_loop.hpp:118-153), with */
+/* generator blocks of varying widths.                                      */
+
+typedef struct {
+  int n, nq, window, ld;
+  double* c;   /* n */
+  double* S;   /* n x ld: [G0 | Q1 .. Qnq] */
+  int* wid;    /* block widths */
+} symv;
+
+static int symv_nz(const symv* s) { int z = s->n; for (int q = 0; q < s->nq; ++q) z += s->wid[q]; return z; }
+
+/* fold_overflow (flowpipe_ct.hpp:317-350) with an n x w oldest block. */
+static void symv_fold(symv* s) {
+  const int n = s->n, cap = s->window > 0 ? s->window : 1;
+  while (s->nq > cap) {
+    const int w = s->wid[0];
+    double* g0 = (double*)malloc(sizeof(double) * (size_t)n * n);
+    double* a = (double*)malloc(sizeof(double) * (size_t)n * w);
+    double* x = (double*)malloc(sizeof(double) * (size_t)n * w);
+    double* e = (double*)malloc(sizeof(double) * (size_t)n * w);
+    double* r = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < n; ++j) g0[(size_t)i * n + j] = s->S[(size_t)i * s->ld + j];
+      for (int j = 0; j < w; ++j) a[(size_t)i * w + j] = s->S[(size_t)i * s->ld + n + j];
+    }
+    int off_new = n;
+    for (int q = 0; q + 1 < s->nq; ++q) off_new += s->wid[q];
+    int folded = 0;
+    if (mat_solve(n, w, g0, a, x)) {
+      double worst = 0.0;
+      for (int j = 0; j < n; ++j) {
+        r[j] = row_abs_sum(x, w, j) * (1.0 + 1e-12);
+        worst = smax(worst, r[j]);
+      }
+      if (worst <= 1.0) {
+        for (int i = 0; i < n; ++i) {
+          for (int j = 0; j < w; ++j) e[(size_t)i * w + j] = 0.0;
+          for (int k = 0; k < n; ++k) {
+            const double gik = g0[(size_t)i * n + k];
+            for (int j = 0; j < w; ++j) e[(size_t)i * w + j] += gik * x[(size_t)k * w + j];
+          }
+        }
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < w; ++j) e[(size_t)i * w + j] -= a[(size_t)i * w + j];
+        for (int j = 0; j < n; ++j)
+          for (int i = 0; i < n; ++i) s->S[(size_t)i * s->ld + j] *= 1.0 + r[j];
+        for (int i = 0; i < n; ++i) s->S[(size_t)i * s->ld + off_new + i] += row_abs_sum(e, w, i) * (1.0 + 1e-12);
+        folded = 1;
+      }
+    }
+    if (!folded)
+      for (int i = 0; i < n; ++i) s->S[(size_t)i * s->ld + off_new + i] += row_abs_sum(a, w, i);
+    const int total = symv_nz(s);
+    for (int i = 0; i < n; ++i)
+      memmove(s->S + (size_t)i * s->ld + n, s->S + (size_t)i * s->ld + n + w, sizeof(double) * (size_t)(total - n - w));
+    memmove(s->wid, s->wid + 1, sizeof(int) * (size_t)(s->nq - 1));
+    s->nq -= 1;
+    free(g0); free(a); free(x); free(e); free(r);
+  }
+}
+
+static int dtcl_one(const net_t* dyn, const net_t* ctl, int n, int H, int window, int rebuild, const double* x0lo,
+                    const double* x0hi, double* lo, double* hi, int* failed_step, int* status) {
+  const int l = ctl->layers[ctl->n_layers - 1].rows;
+  const int cap = window > 0 ? window : 1;
+  const int ld = n + (cap + 3) * (n + l);
+  symv s;
+  s.n = n; s.nq = 0; s.window = window; s.ld = ld;
+  s.c = (double*)malloc(sizeof(double) * (size_t)n);
+  s.S = (double*)calloc((size_t)n * ld, sizeof(double));
+  s.wid = (int*)malloc(sizeof(int) * (size_t)(cap + 4));
+  double* A = (double*)malloc(sizeof(double) * (size_t)(n + l) * ld);
+  double* uc = (double*)malloc(sizeof(double) * (size_t)l);
+  double* uA = (double*)malloc(sizeof(double) * (size_t)l * ld);
+  iv* urem = (iv*)malloc(sizeof(iv) * (size_t)l);
+  double* cag = (double*)malloc(sizeof(double) * (size_t)(n + l));
+  double* oc = (double*)malloc(sizeof(double) * (size_t)n);
+  double* oA = (double*)malloc(sizeof(double) * (size_t)n * ld);
+  iv* rem = (iv*)malloc(sizeof(iv) * (size_t)n);
+  iv* ig = (iv*)calloc((size_t)(n + l), sizeof(iv));
+  *failed_step = -1;
+  *status = REACH_TUBE_OK;
+  for (int d = 0; d < n; ++d) { lo[d] = x0lo[d]; hi[d] = x0hi[d]; }
+  int nb = 1;
+  /* init_symbolic_state */
+  for (int i = 0; i < n; ++i) {
+    s.c[i] = (x0lo[i] + x0hi[i]) * 0.5;
+    for (int j = 0; j < n; ++j) s.S[(size_t)i * ld + j] = (i == j) ? (x0hi[i] - x0lo[i]) * 0.5 : 0.0;
+  }
+  for (int k = 0; k < H; ++k) {
+    const int nz = symv_nz(&s);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < nz; ++j) A[(size_t)i * nz + j] = s.S[(size_t)i * ld + j];
+    /* u_tm = ctl_crown(x_tm, ctl, {}) */
+    if (certify_tm_input(ctl, n, nz, s.c, A, ig, uc, uA, urem)) { *failed_step = k; *status = REACH_TUBE_CTL_FAILED; break; }
+    int fin = 1;
+    for (int i = 0; i < l; ++i) if (!iv_finite(urem[i])) fin = 0;
+    if (!fin) { *failed_step = k; *status = REACH_TUBE_CTL_DIVERGED; break; }
+    /* stacked [x; u] over nz + (n + l) variables */
+    const int w_new = n + l, nza = nz + w_new;
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < nza; ++j) A[(size_t)i * nza + j] = (j < nz) ? s.S[(size_t)i * ld + j] : 0.0;
+      cag[i] = s.c[i] + (0.0 + 0.0) * 0.5;
+    }
+    for (int i = 0; i < l; ++i) {
+      for (int j = 0; j < nza; ++j)
+        A[(size_t)(n + i) * nza + j] = (j < nz) ? uA[(size_t)i * nz + j] : ((j - nz == n + i) ? (urem[i].hi - urem[i].lo) * 0.5 : 0.0);
+      cag[n + i] = uc[i] + (urem[i].lo + urem[i].hi) * 0.5;
+    }
+    if (certify_tm_input(dyn, n + l, nza, cag, A, ig, oc, oA, rem)) { *failed_step = k; *status = REACH_TUBE_NONFINITE_PREACT; break; }
+    for (int i = 0; i < n; ++i) if (!iv_finite(rem[i])) fin = 0;
+    if (!fin) { *failed_step = k; *status = REACH_TUBE_DIVERGED_CERT; break; }
+    for (int i = 0; i < n; ++i) {
+      s.c[i] = oc[i] + (rem[i].lo + rem[i].hi) * 0.5;
+      for (int j = 0; j < nza; ++j) s.S[(size_t)i * ld + j] = oA[(size_t)i * nza + j];
+      for (int j = 0; j < n; ++j) s.S[(size_t)i * ld + nza + j] = (i == j) ? (rem[i].hi - rem[i].lo) * 0.5 : 0.0;
+    }
+    s.wid[s.nq++] = w_new;
+    s.wid[s.nq++] = n;
+    symv_fold(&s);
+    /* symbolic_box */
+    int bfin = 1;
+    double* blo = lo + (size_t)nb * n;
+    double* bhi = hi + (size_t)nb * n;
+    for (int i = 0; i < n; ++i) {
+      double r = row_abs_sum(s.S + (size_t)i * ld, n, 0);
+      int off = n;
+      for (int q = 0; q < s.nq; ++q) { r += row_abs_sum(s.S + (size_t)i * ld + off, s.wid[q], 0); off += s.wid[q]; }
+      blo[i] = s.c[i] - r;
+      bhi[i] = s.c[i] + r;
+      if (!isfinite(blo[i]) || !isfinite(bhi[i])) bfin = 0;
+    }
+    nb += 1;
+    if (!bfin) { *failed_step = k; *status = REACH_TUBE_DIVERGED_BOX; break; }
+    if (rebuild) {
+      s.nq = 0;
+      for (int i = 0; i < n; ++i) {
+        s.c[i] = (blo[i] + bhi[i]) * 0.5;
+        for (int j = 0; j < n; ++j) s.S[(size_t)i * ld + j] = (i == j) ? (bhi[i] - blo[i]) * 0.5 : 0.0;
+      }
+    }
+  }
+  free(s.c); free(s.S); free(s.wid); free(A); free(uc); free(uA); free(urem); free(cag); free(oc); free(oA);
+  free(rem); free(ig);
+  return nb;
+}
+
+int orc_dtcl_batch(const reach_net_desc* dyn_desc, const reach_net_desc* ctl_desc, const reach_dt_args* a,
+                   const reach_tube_out* out) {
+  net_t dyn = net_from_desc(dyn_desc), ctl = net_from_desc(ctl_desc);
+  const int H = a->horizon, n = a->n;
+  for (int b = 0; b < a->batch; ++b) {
+    int fs, st;
+    const int nb = dtcl_one(&dyn, &ctl, n, H, a->window, a->rebuild_from_box, a->x0_lo + (size_t)b * n,
+                            a->x0_hi + (size_t)b * n, out->lo + (size_t)b * (H + 1) * n,
+                            out->hi + (size_t)b * (H + 1) * n, &fs, &st);
+    out->n_boxes[b] = nb;
+    out->failed_step[b] = fs;
+    out->status[b] = st;
+  }
+  free(dyn.layers); free(ctl.layers);
+  return REACH_OK;
+}

@@ -215,6 +215,152 @@ int ref_hardware_threads(void) { return hardware_threads(); }
 
 namespace {
 
+// DT closed loop: the reference has no driver for it; this
+// composes reference functions only, mirroring cl_reach's stacking
+// (closed_loop.hpp:118-153) on a DT one-step network: u = ctl_crown(x_tm, ctl)
+// (neural.hpp:418), [x; u] over the shared variables with the control remainder
+// as a fresh block (no fold on the stacked state), certify_tm_input(dyn, .),
+// then dt_reach's re-seed / fold_overflow / symbolic_box (dt_reach.hpp:69-100).
+ReachTube<double> dt_closed_loop(const MLPNet<double>& dyn, const MLPNet<double>& ctl, int n, const Box& x0, int H,
+                                 int window, bool rebuild) {
+  const int l = ctl.output_dim();
+  ReachTube<double> tube;
+  tube.push(x0, 0.0, 0.0);
+  SymbolicState<double> sym = init_symbolic_state(x0, window);
+  for (int k = 0; k < H; ++k) {
+    LinearTM<double> x_tm = symbolic_seed(sym);
+    LinearTM<double> u_tm;
+    try {
+      u_tm = ctl_crown(x_tm, ctl, Vec<double>{});
+    } catch (const std::exception& e) {
+      tube.mark_failed(k, std::string("controller certification failed: ") + e.what());
+      return tube;
+    }
+    if (!u_tm.remainder.finite() || u_tm.remainder.diverged) {
+      tube.mark_failed(k, "controller certification diverged");
+      return tube;
+    }
+    const int nz = x_tm.nz(), p0 = sym.g0.cols;
+    SymbolicState<double> aug;
+    aug.window = window;
+    aug.c = Vec<double>(static_cast<size_t>(n + l));
+    aug.g0 = Mat<double>(n + l, p0);
+    Mat<double> fresh(n + l, n + l);
+    for (int d = 0; d < n; ++d) {
+      aug.c[static_cast<size_t>(d)] = x_tm.c[static_cast<size_t>(d)] + x_tm.remainder[d].mid();
+      for (int j = 0; j < p0; ++j) aug.g0(d, j) = x_tm.A(d, j);
+      fresh(d, d) = x_tm.remainder[d].rad();
+    }
+    for (int d = 0; d < l; ++d) {
+      aug.c[static_cast<size_t>(n + d)] = u_tm.c[static_cast<size_t>(d)] + u_tm.remainder[d].mid();
+      for (int j = 0; j < p0; ++j) aug.g0(n + d, j) = u_tm.A(d, j);
+      fresh(n + d, n + d) = u_tm.remainder[d].rad();
+    }
+    int off = p0;
+    for (const auto& q : sym.queue) {
+      Mat<double> nq(n + l, q.cols);
+      for (int j = 0; j < q.cols; ++j) {
+        for (int d = 0; d < n; ++d) nq(d, j) = x_tm.A(d, off + j);
+        for (int d = 0; d < l; ++d) nq(n + d, j) = u_tm.A(d, off + j);
+      }
+      aug.queue.push_back(std::move(nq));
+      off += q.cols;
+    }
+    (void)nz;
+    aug.queue.push_back(std::move(fresh));
+    LinearTM<double> xu = symbolic_seed(aug);
+    LinearTM<double> out;
+    try {
+      out = certify_tm_input(dyn, xu);
+    } catch (const std::exception& e) {
+      tube.mark_failed(k, e.what());
+      return tube;
+    }
+    if (!out.remainder.finite() || out.remainder.diverged) {
+      tube.mark_failed(k, "diverged certification");
+      return tube;
+    }
+    SymbolicState<double> next;
+    next.window = window;
+    next.c = Vec<double>(static_cast<size_t>(n));
+    next.g0 = Mat<double>(n, p0);
+    for (int i = 0; i < n; ++i) {
+      next.c[static_cast<size_t>(i)] = out.c[static_cast<size_t>(i)] + out.remainder[i].mid();
+      for (int j = 0; j < p0; ++j) next.g0(i, j) = out.A(i, j);
+    }
+    off = p0;
+    for (const auto& q : aug.queue) {
+      Mat<double> nq(n, q.cols);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < q.cols; ++j) nq(i, j) = out.A(i, off + j);
+      next.queue.push_back(std::move(nq));
+      off += q.cols;
+    }
+    Mat<double> fr(n, n);
+    for (int i = 0; i < n; ++i) fr(i, i) = out.remainder[i].rad();
+    next.queue.push_back(std::move(fr));
+    fold_overflow(next);
+    sym = std::move(next);
+    Box box = symbolic_box(sym);
+    const double t = static_cast<double>(k + 1);
+    tube.push(box, t, t);
+    if (box.diverged) {
+      tube.mark_failed(k, "diverged box");
+      return tube;
+    }
+    if (rebuild) sym = init_symbolic_state(box, window);
+  }
+  return tube;
+}
+
+int32_t cl_status_of(const ReachTube<double>& t) {
+  if (t.failure_reason == "controller certification failed: relax_activation: non-finite preactivation")
+    return REACH_TUBE_CTL_FAILED;
+  if (t.failure_reason == "controller certification diverged") return REACH_TUBE_CTL_DIVERGED;
+  return status_of(t);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_dtcl_batch(const reach_net_desc* dyn_desc, const reach_net_desc* ctl_desc, const reach_dt_args* a,
+                   const reach_tube_out* out, int32_t threads) {
+  try {
+    MLPNet<double> dyn = net_from_desc(dyn_desc), ctl = net_from_desc(ctl_desc);
+    const int H = a->horizon, n = a->n;
+    parallel_for(
+        a->batch,
+        [&](int b) {
+          ReachTube<double> tube;
+          try {
+            tube = dt_closed_loop(dyn, ctl, n,
+                                  box_at(a->x0_lo + static_cast<size_t>(b) * n, a->x0_hi + static_cast<size_t>(b) * n, n),
+                                  H, a->window, a->rebuild_from_box != 0);
+          } catch (const std::exception& e) {
+            tube.mark_failed(0, e.what());
+          }
+          out->n_boxes[b] = tube.steps();
+          out->failed_step[b] = tube.failed_step;
+          out->status[b] = cl_status_of(tube);
+          for (int k = 0; k < tube.steps(); ++k)
+            for (int d = 0; d < n; ++d) {
+              size_t o = (static_cast<size_t>(b) * (H + 1) + k) * n + d;
+              out->lo[o] = tube.boxes[static_cast<size_t>(k)][d].lo;
+              out->hi[o] = tube.boxes[static_cast<size_t>(k)][d].hi;
+            }
+        },
+        threads);
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
 PlanProblem problem_from(const reach_net_desc* desc, const reach_plan_problem* p) {
   PlanProblem prob;
   prob.sys = make_sys(desc, p->n, p->m);

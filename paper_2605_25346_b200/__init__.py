@@ -6,6 +6,6 @@ the in-tree CUDA library libreach_b200.so via the C ABI in include/reach_b200.h.
 from .api import (  # noqa: F401
     Act, Layer, MLPNet, affine_net, DTSystem, DTReachParams, ReachTube, TubeBatch, HullResult,
     SplitPlan, split_box, dt_reach, dt_reach_batch, dt_reach_batch_arrays, reach_split_hull,
-    reach_with_splitting, tube_volume, box_volume_proxy, box_from_center,
+    reach_with_splitting, tube_volume, box_volume_proxy, box_from_center, dt_closed_loop_batch,
 )
 from ._native import Context, default_context, ReachError, NativeMissing, LIB_PATH  # noqa: F401

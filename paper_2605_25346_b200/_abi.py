@@ -25,12 +25,16 @@ TUBE_OK = 0
 TUBE_NONFINITE_PREACT = 1
 TUBE_DIVERGED_CERT = 2
 TUBE_DIVERGED_BOX = 3
+TUBE_CTL_FAILED = 4
+TUBE_CTL_DIVERGED = 5
 TUBE_OTHER = 99
 TUBE_REASON = {
     TUBE_OK: "",
     TUBE_NONFINITE_PREACT: "relax_activation: non-finite preactivation",
     TUBE_DIVERGED_CERT: "diverged certification",
     TUBE_DIVERGED_BOX: "diverged box",
+    TUBE_CTL_FAILED: "controller certification failed: relax_activation: non-finite preactivation",
+    TUBE_CTL_DIVERGED: "controller certification diverged",
     TUBE_OTHER: "error",
 }
 

@@ -44,6 +44,8 @@ def _declare(lib):
     lib.reach_net_free.argtypes = [vp, vp]
     lib.reach_dt_batch.argtypes = [vp, vp, C.POINTER(A.DTArgs), C.POINTER(A.TubeOut), C.c_int32]
     lib.reach_split_hull.argtypes = [vp, vp, C.POINTER(A.SplitArgs), C.POINTER(A.HullOut), C.c_int32]
+    lib.reach_dtcl_batch.argtypes = [vp, vp, vp, C.POINTER(A.DTArgs), C.POINTER(A.TubeOut), C.c_int32]
+    lib.reach_dtcl_batch.restype = C.c_int
     lib.reach_ctx_enable_kernel_timing.argtypes = [vp, C.c_int32]
     lib.reach_ctx_kernel_time.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     lib.reach_measure_fp64_peak.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]

@@ -361,3 +361,31 @@ def reach_with_splitting(sys: DTSystem, x0, plan: SplitPlan, actions, prm: DTRea
                          ctx: Optional[Context] = None) -> ReachTube:
     """reach_with_splitting(dt_reach engine, x0, plan) (refine.hpp:121-160)."""
     return reach_split_hull(sys, x0, plan, actions, prm, ctx=ctx).tube()
+
+
+# ---------------------------------------------------------------------------
+def dt_closed_loop_batch(dyn: MLPNet, ctl: MLPNet, n: int, x0_lo: np.ndarray, x0_hi: np.ndarray, horizon: int,
+                         prm: DTReachParams = DTReachParams(), ctx: Optional[Context] = None) -> TubeBatch:
+    """DT closed loop: per step u = ctl_crown(x_tm, ctl) (neural.hpp:418),
+    [x; u] stacked as cl_reach does (closed_loop.hpp:118-153), certify_tm_input(dyn, .), then
+    dt_reach's re-seed / fold / box.  dyn: (n + l) -> n, ctl: n -> l."""
+    dyn.validate()
+    ctl.validate()
+    l = ctl.output_dim()
+    if ctl.input_dim() != n:
+        raise ValueError("ClosedLoopSpec: controller input dim mismatch")
+    if dyn.input_dim() != n + l or dyn.output_dim() != n:
+        raise ValueError("ClosedLoopSpec: dynamics must act on the augmented (x,u) state")
+    ctx = ctx or default_context()
+    x0_lo = np.ascontiguousarray(x0_lo, np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, np.float64)
+    B = x0_lo.shape[0]
+    out = TubeBatch(np.full((B, horizon + 1, n), np.nan), np.full((B, horizon + 1, n), np.nan),
+                    np.zeros(B, np.int32), np.zeros(B, np.int32), np.zeros(B, np.int32))
+    args = A.DTArgs(B, horizon, n, 0, prm.window, int(prm.rebuild_from_box), A.dptr(x0_lo), A.dptr(x0_hi),
+                    A.dptr(np.zeros(1)), 0)
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step),
+                   A.iptr(out.status))
+    hd, hc = ctx.upload(dyn), ctx.upload(ctl)
+    ctx.check(ctx._lib.reach_dtcl_batch(ctx.handle, hd, hc, C.byref(args), C.byref(to), 0), "dt closed loop")
+    return out

@@ -47,7 +47,9 @@ constexpr int kMaxChunks = 96;  // weight-stream chunks per DT step
 constexpr int kHeaderBytes = (128 + kMaxChunks * 12 + 127) / 128 * 128;
 
 struct DTParams {
-  DevNet net;
+  DevNet net;       // the one-step map (DT) or the dynamics network (closed loop)
+  DevNet ctl;       // closed loop only: the controller network (l outputs)
+  int l;            // control dimension; 0 = open-loop dt_reach
   int B, H, n, m, window, rebuild;
   // per-sample inputs (tube mode) -- or split mode (sub-box from the grid)
   const double* x0_lo;
@@ -77,17 +79,21 @@ struct DTParams {
   // shared-memory layout (doubles)
   int stage_doubles, nstage, warp_doubles, bias_doubles;
   int o_stA, o_c, o_pre, o_LT, o_R, o_bf0, o_idx;  // hb aliases LT; R only for tanh nets
+  int o_aug, ldag, o_cag;       // closed loop: stacked [x; u] TM ((n+l) x ldag) and its centre
+  int o_wid;                    // generator block widths (ints)
   int has_tanh;
   int nzs;                      // stA row stride (n * (cap + 2))
   int hp;                       // padded hidden width (32 * CPL)
   int bias_s_off[kMaxLayers];   // per-layer bias offsets in the CTA bias copy
-  // weight stream: chunk table of one DT step (the sequence repeats every step)
+  int bias_s_off_ctl[kMaxLayers];
+  // weight stream: chunk table of one DT step (the sequence repeats every step);
+  // entries are absolute device addresses (the two networks live in two blobs)
   int n_chunks_step;
   long long ch_off[kMaxChunks];
   unsigned ch_bytes[kMaxChunks];
 };
 
-enum : int { ST_OK = 0, ST_PREACT = 1, ST_CERT = 2, ST_BOX = 3 };
+enum : int { ST_OK = 0, ST_PREACT = 1, ST_CERT = 2, ST_BOX = 3, ST_CTL_PREACT = 4, ST_CTL_CERT = 5 };
 
 // Weight stream: a ring of shared-memory stages filled by the bulk-copy (TMA)
 // engine.  Every sample warp consumes every chunk in the same order; the LAST
@@ -97,9 +103,8 @@ struct WStream {
   double* stages;
   uint64_t* full;
   int* cnt;
-  const long long* ch_off;      // shared-memory copy of the chunk table
+  const long long* ch_off;      // shared-memory copy of the chunk table (device addresses)
   const unsigned* ch_bytes;
-  const double* blob;
   int spc, nstage, stage_doubles, n_chunks_step;
   uint32_t g;
   uint32_t total;
@@ -113,7 +118,8 @@ struct WStream {
     const uint32_t bytes = ch_bytes[idx];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_expect_tx(&full[s], bytes);
-    bulk_g2s(stages + static_cast<size_t>(s) * stage_doubles, blob + ch_off[idx], bytes, &full[s]);
+    bulk_g2s(stages + static_cast<size_t>(s) * stage_doubles, reinterpret_cast<const double*>(ch_off[idx]), bytes,
+             &full[s]);
   }
   // Waits for the current chunk; returns its stage index (the caller forms the
   // pointer from its own shared-memory base so the address space stays known).
@@ -323,43 +329,596 @@ __device__ __forceinline__ void pipelined_rows(RowIter& it, Load&& load, Comp&& 
 }
 
 // ---------------------------------------------------------------------------
-// The kernel.  NO: max state dim (= network output dim) of this family;
-// CPL: hidden units per lane (padded hidden width HP = 32 * CPL).
-// Block = up to kSampleWarps warps, one sample per warp; two CTAs per SM so
-// the serial phases of one CTA overlap the contractions of the other.
-//
-// ReLU sparsity: a stably inactive unit (u <= 0) has post-activation [0,0]
-// and slope 0, so every product it feeds -- its IBP input rows and its
-// Lambda.W rows -- is exactly +-0, and adding +-0 never changes a non-zero
-// sum.  Those rows are skipped through per-layer unit bitmasks; results are
-// identical to the dense reference up to the sign of an exactly-zero entry.
-// Intercept chains run over the unstable units only (ReLU: li = 0 always,
-// ui = 0 for stable units).
+// Kernel configuration.
 #ifndef RB_SAMPLE_WARPS
 #define RB_SAMPLE_WARPS 8
 #endif
 #ifndef RB_MIN_BLOCKS
 #define RB_MIN_BLOCKS 1
 #endif
-#ifndef RB_PIPELINE
-#define RB_PIPELINE 0
-#endif
 constexpr int kSampleWarps = RB_SAMPLE_WARPS;
+constexpr int kNZG = 2;  // 32-column groups of a generator matrix (<= 64 columns)
 
+// Per-warp scratch of one certification (shared memory).
+template <int CPL>
+struct CertScratch {
+  double* pre;            // per hidden layer, per padded unit: (lo,hi) -> after relax (s, ui) [ReLU]
+  double* LT;             // Lambda^T [col][NOP]; also the IBP input buffer and the fold scratch
+  double* R;              // tanh relaxation (s, li, ui) per unit
+  double* bf0;            // frozen first-layer bias
+  unsigned* masks;        // [L-1][2][CPL] active / unstable unit bitmasks
+  unsigned char* alists;  // [L-1][HP] compacted active units
+};
+
+// ---------------------------------------------------------------------------
+// certify_tm_input (neural.hpp:342-394) of one sample, by one warp.
+//
+// Input TM x = c + A z (+ the zero remainder of a symbolic seed), A = n_i x nz
+// in shared memory (row stride lda); rows n_i.. of layer 0 are frozen trailing
+// inputs u (freeze_trailing_inputs, neural.hpp:398-413).  Consumes the net's
+// weight chunks (W^T of the hidden layers, then W of every layer, top down)
+// from the stream even when `done`.  Returns A_out = Lambda . A in registers
+// (lane = column j of group g, rows i < n_o) and, on lanes < n_o, the tail
+// (mid, rem_lo, rem_hi) of neural.hpp:383-391.
+template <int NO, int CPL>
+__device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, const int* bias_off, int n_i, int n_o,
+                                        const double* u, const double* A, int lda, int nz, const double* c,
+                                        const CertScratch<CPL>& S, WStream& ws_in, const double* stages, int SD,
+                                        int lane, bool done, double (&aout)[NO][kNZG], double& mid, double& rl,
+                                        double& rh, bool& preact_bad, bool& lam_bad) {
+  constexpr int NOP = (NO + 1) & ~1;  // Lambda^T row stride (16-byte rows)
+  constexpr int HP = 32 * CPL;
+  const int L = N.L;
+  const int m_frz = N.dims[0] - n_i;  // frozen trailing inputs
+  double* LT = S.LT;
+  double* hb = S.LT;
+  preact_bad = false;
+  lam_bad = false;
+
+  // ---- prepend layer IBP (neural.hpp:360-373 + interval.hpp:284-295):
+  // pre0_i = sum_j iv_scale(A_ij, [-1,1]) (+ the [0,0] remainder block) + c_i
+  if (!done && lane < n_i) {
+    double lo = 0.0, hi = 0.0;
+    for (int j = 0; j < nz; ++j) {
+      const double a = A[lane * lda + j];
+      lo = add(lo, (a >= 0.0) ? -a : a);  // a*-1 : a*1
+      hi = add(hi, (a >= 0.0) ? a : -a);
+    }
+    const double cl = c[lane];
+    hb[2 * lane] = add(lo, cl);
+    hb[2 * lane + 1] = add(hi, cl);
+  }
+  __syncwarp();
+
+  // ---- IBP through the hidden layers (neural.hpp:243-257); output layer skipped
+  for (int l = 0; l + 1 < L; ++l) {
+    const int width = N.dims[l + 1];
+    const int rows = N.dims[l];
+    const int ld = N.ldt[l];
+    const int act = N.acts[l];
+    const double* bias = bias_s + bias_off[l];
+    const unsigned* in_mask = S.masks + (l - 1) * 2 * CPL;  // l >= 1: active units of layer l-1
+    const unsigned char* in_list = S.alists + (l - 1) * HP;
+    double alo[CPL], ahi[CPL], bfold[CPL];
+#pragma unroll
+    for (int cc = 0; cc < CPL; ++cc) {
+      alo[cc] = 0.0;
+      ahi[cc] = 0.0;
+      bfold[cc] = bias[cc * 32 + lane];
+    }
+    auto ibp_row = [&](const double* ch, int r0, int j) {
+      const double* wrow = ch + (j - r0) * ld + lane;
+      const double2 x = *reinterpret_cast<const double2*>(hb + 2 * j);
+      double w[CPL], tl[CPL], th[CPL];
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) w[cc] = wrow[cc * 32];
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        const bool pos = w[cc] >= 0.0;
+        tl[cc] = mul(w[cc], pos ? x.x : x.y);
+        th[cc] = mul(w[cc], pos ? x.y : x.x);
+      }
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        alo[cc] = add(alo[cc], tl[cc]);
+        ahi[cc] = add(ahi[cc], th[cc]);
+      }
+    };
+    const int rpc = rows_per_chunk(ld, SD);
+    int t = 0;
+    for (int r0 = 0; r0 < rows; r0 += rpc) {
+      const double* ch = stages + ws_in.acquire() * SD;
+      const int nr = min(rpc, rows - r0);
+      if (!done) {
+        if (l > 0) {
+          const int t1 = popc_below(in_mask, r0 + nr);
+#pragma unroll 2
+          for (; t < t1; ++t) ibp_row(ch, r0, in_list[t]);
+        } else {
+          const int nx = min(n_i, r0 + nr);
+#pragma unroll 2
+          for (int j = r0; j < nx; ++j) ibp_row(ch, r0, j);
+          // freeze_trailing_inputs (neural.hpp:410): b += W[:, n_i + j] u_j
+          for (int r = max(n_i - r0, 0); r < nr; ++r) {
+            const double uj = u[r0 + r - n_i];
+            const double* wrow = ch + r * ld + lane;
+#pragma unroll
+            for (int cc = 0; cc < CPL; ++cc) bfold[cc] = add(bfold[cc], mul(wrow[cc * 32], uj));
+          }
+        }
+      }
+      ws_in.release(lane);
+    }
+    if (!done) {
+      double* pl = S.pre + l * 2 * HP;
+      unsigned* am = S.masks + l * 2 * CPL;
+      int lbase = 0;
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        const int o = cc * 32 + lane;
+        const double plo = add(alo[cc], bfold[cc]);
+        const double phi = add(ahi[cc], bfold[cc]);
+        *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(plo, phi);
+        if (l == 0 && m_frz > 0) S.bf0[o] = bfold[cc];
+        const bool fin = finite(plo) && finite(phi);
+        if (o < width && act != 2 && !fin) preact_bad = true;
+        // ReLU: inactive iff hi <= 0; unstable iff lo < 0 < hi.  Other acts: dense.
+        const bool actv = (o < width) && ((act != 0) || !(phi <= 0.0));
+        const bool unst = (o < width) && ((act != 0) || (plo < 0.0 && phi > 0.0) || !fin);
+        const unsigned ma = __ballot_sync(0xffffffffu, actv);
+        const unsigned mu = __ballot_sync(0xffffffffu, unst);
+        if (lane == 0) {
+          am[cc] = ma;
+          am[CPL + cc] = mu;
+        }
+        if (actv) S.alists[l * HP + lbase + __popc(ma & ((1u << lane) - 1u))] = static_cast<unsigned char>(o);
+        lbase += __popc(ma);
+        alo[cc] = act_apply(act, plo);
+        ahi[cc] = act_apply(act, phi);
+      }
+      __syncwarp();  // every lane is done reading hb
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc)
+        *reinterpret_cast<double2*>(hb + 2 * (cc * 32 + lane)) = make_double2(alo[cc], ahi[cc]);
+      __syncwarp();
+    }
+  }
+  if (!done) preact_bad = __any_sync(0xffffffffu, preact_bad);
+
+  // ---- CROWN backward (neural.hpp:297-327)
+  // init: Lambda = I . W_{L-1} = W_{L-1};  b = 0 + I . b_{L-1}
+  double blo = 0.0, bup = 0.0;
+  {
+    const int l = L - 1;
+    const int rows = N.dims[l + 1];  // = n_o
+    const int ncols = (l == 0) ? n_i : N.dims[l];
+    const int ld = N.ldw[l];
+    const int rpc = rows_per_chunk(ld, SD);
+    for (int r0 = 0; r0 < rows; r0 += rpc) {
+      const double* ch = stages + ws_in.acquire() * SD;
+      const int nr = min(rpc, rows - r0);
+      if (!done) {
+        for (int r = 0; r < nr; ++r) {
+          const int i = r0 + r;
+          for (int j = lane; j < ncols; j += 32) LT[j * NOP + i] = add(0.0, ch[r * ld + j]);
+        }
+      }
+      ws_in.release(lane);
+    }
+    if (!done && lane < n_o) {
+      double bi = bias_s[bias_off[l] + lane];
+      if (l == 0 && m_frz > 0) {  // single-layer net: fold the frozen inputs into the bias here
+        const double* w = N.blob + N.w_off[0] + static_cast<size_t>(lane) * N.ldw[0];
+        for (int j = 0; j < m_frz; ++j) bi = add(bi, mul(w[n_i + j], u[j]));
+        S.bf0[lane] = bi;
+      }
+      blo = add(0.0, bi);
+      bup = blo;
+    }
+    __syncwarp();
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    const int act = N.acts[l];
+    const int width = N.dims[l + 1];
+    const double* bvec = (l == 0 && m_frz > 0) ? S.bf0 : bias_s + bias_off[l];
+    const unsigned* am = S.masks + l * 2 * CPL;
+    double* pl = S.pre + l * 2 * HP;
+    if (!done) {
+      if (act == 0) {
+        // ReLU relaxation (parallel): (s, ui) overwrite the preactivation slots; li = 0
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) {
+          const int o = cc * 32 + lane;
+          const double2 p = *reinterpret_cast<const double2*>(pl + 2 * o);
+          double s, li, ui;
+          relax(0, p.x, p.y, s, li, ui);
+          *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(s, ui);
+        }
+        __syncwarp();
+        // intercept chains over the unstable units (unscaled Lambda), lane i = row i
+        if (lane < n_o) {
+          for_each_row(am + CPL, 0, width, [&](int j) {
+            const double a = LT[j * NOP + lane];
+            const double ui = pl[2 * j + 1];
+            if (a >= 0.0) bup = add(bup, mul(a, ui));
+            else blo = add(blo, mul(a, ui));
+          });
+        }
+        __syncwarp();
+        // slope scaling (parallel over units): Lambda(:, j) *= s_j
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) {
+          const int o = cc * 32 + lane;
+          const double s = pl[2 * o];
+          double* col = LT + o * NOP;
+#pragma unroll
+          for (int i = 0; i < NOP; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(col + i);
+            *reinterpret_cast<double2*>(col + i) = make_double2(mul(v.x, s), mul(v.y, s));
+          }
+        }
+        __syncwarp();
+        // shift chain Lambda_s . b (dense; inactive units add +-0), lane i = row i
+        if (lane < n_o) {
+          double shift = 0.0;
+#pragma unroll 8
+          for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
+          blo = add(blo, shift);
+          bup = add(bup, shift);
+        }
+      } else {
+        if (act == 1) {
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) {
+            const int o = cc * 32 + lane;
+            const double2 p = *reinterpret_cast<const double2*>(pl + 2 * o);
+            double s, li, ui;
+            relax(1, p.x, p.y, s, li, ui);
+            S.R[3 * o] = s;
+            S.R[3 * o + 1] = li;
+            S.R[3 * o + 2] = ui;
+          }
+          __syncwarp();
+        }
+        if (lane < n_o) {
+          double shift = 0.0;
+          if (act == 1) {
+            for (int j = 0; j < width; ++j) {
+              const double a = LT[j * NOP + lane];
+              const double s = S.R[3 * j], li = S.R[3 * j + 1], ui = S.R[3 * j + 2];
+              const bool pos = a >= 0.0;
+              blo = add(blo, mul(a, pos ? li : ui));
+              bup = add(bup, mul(a, pos ? ui : li));
+              const double as = mul(a, s);
+              LT[j * NOP + lane] = as;
+              shift = add(shift, mul(as, bvec[j]));
+            }
+          } else {
+            for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
+          }
+          blo = add(blo, shift);
+          bup = add(bup, shift);
+        }
+      }
+      __syncwarp();
+    }
+    // dense contraction Lambda <- Lambda_s . W_l  (linalg.hpp:53-63, i-k-j order) over the rows
+    // k of units with a non-zero slope
+    const int ld = N.ldw[l];
+    const int rpc = rows_per_chunk(ld, SD);
+    const unsigned char* alist = S.alists + l * HP;
+    if (l > 0) {
+      double acc[NO][CPL];
+#pragma unroll
+      for (int i = 0; i < NO; ++i)
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) acc[i][cc] = 0.0;
+      int t = 0;
+      for (int r0 = 0; r0 < width; r0 += rpc) {
+        const double* ch = stages + ws_in.acquire() * SD;
+        const int nr = min(rpc, width - r0);
+        if (!done) {
+          const int t1 = popc_below(am, r0 + nr);
+#pragma unroll 2
+          for (; t < t1; ++t) {
+            const int kk = alist[t];
+            const double* lrow = LT + kk * NOP;
+            const double* wrow = ch + (kk - r0) * ld + lane;
+            double lam[NOP], w[CPL];
+#pragma unroll
+            for (int i = 0; i < NOP; i += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(lrow + i);
+              lam[i] = v.x;
+              lam[i + 1] = v.y;
+            }
+#pragma unroll
+            for (int cc = 0; cc < CPL; ++cc) w[cc] = wrow[cc * 32];
+            double tt[NO][CPL];
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+#pragma unroll
+              for (int cc = 0; cc < CPL; ++cc) tt[i][cc] = mul(lam[i], w[cc]);
+#pragma unroll
+            for (int i = 0; i < NO; ++i)
+#pragma unroll
+              for (int cc = 0; cc < CPL; ++cc) acc[i][cc] = add(acc[i][cc], tt[i][cc]);
+          }
+        }
+        ws_in.release(lane);
+      }
+      if (!done) {
+        const int ncols = N.dims[l];
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc)
+#pragma unroll
+          for (int i = 0; i < NO; ++i)
+            if (i < n_o && cc * 32 + lane < ncols && !finite(acc[i][cc])) lam_bad = true;
+        __syncwarp();
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) {
+          double* dst = LT + (cc * 32 + lane) * NOP;
+#pragma unroll
+          for (int i = 0; i < NOP; i += 2)
+            *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i][cc], (i + 1 < NO) ? acc[i + 1][cc] : 0.0);
+        }
+        __syncwarp();
+      }
+    } else {
+      // frozen first layer: only the n_i TM columns survive -- a tiny GEMM
+      // (n_o x width) . (width x n_i); lane p owns outputs p and p + 32 of the
+      // n_o x n_i grid, each a sequential k chain as the reference's.
+      const int npair = n_o * n_i;
+      const int p0 = lane, p1 = lane + 32;
+      const int i0 = (p0 < npair ? p0 : 0) / n_i, j0 = (p0 < npair ? p0 : 0) % n_i;
+      const int i1 = (p1 < npair ? p1 : 0) / n_i, j1 = (p1 < npair ? p1 : 0) % n_i;
+      double a0 = 0.0, a1 = 0.0;
+      int t = 0;
+      for (int r0 = 0; r0 < width; r0 += rpc) {
+        const double* ch = stages + ws_in.acquire() * SD;
+        const int nr = min(rpc, width - r0);
+        if (!done) {
+          const int t1 = popc_below(am, r0 + nr);
+#pragma unroll 4
+          for (; t < t1; ++t) {
+            const int kk = alist[t];
+            const double* wrow = ch + (kk - r0) * ld;
+            a0 = add(a0, mul(LT[kk * NOP + i0], wrow[j0]));
+            a1 = add(a1, mul(LT[kk * NOP + i1], wrow[j1]));
+          }
+        }
+        ws_in.release(lane);
+      }
+      if (!done) {
+        if ((p0 < npair && !finite(a0)) || (p1 < npair && !finite(a1))) lam_bad = true;
+        __syncwarp();
+        if (p0 < npair) LT[j0 * NOP + i0] = a0;
+        if (p1 < npair) LT[j1 * NOP + i1] = a1;
+        __syncwarp();
+      }
+    }
+  }
+  if (done) return;
+
+  // ---- prepended layer W = [A | I], b = c: shift chain and A_out = Lambda . A
+  if (lane < n_o) {
+    double shift = 0.0;
+    for (int kk = 0; kk < n_i; ++kk) shift = add(shift, mul(LT[kk * NOP + lane], c[kk]));
+    blo = add(blo, shift);
+    bup = add(bup, shift);
+  }
+#pragma unroll
+  for (int g = 0; g < kNZG; ++g) {
+    const int j = g * 32 + lane;
+#pragma unroll
+    for (int i = 0; i < NO; ++i) aout[i][g] = 0.0;
+    if (j < nz) {
+      for (int kk = 0; kk < n_i; ++kk) {
+        const double akj = A[kk * lda + j];
+#pragma unroll
+        for (int i = 0; i < NO; ++i) aout[i][g] = mac(aout[i][g], LT[kk * NOP + i], akj);
+      }
+    }
+  }
+  // ---- tail (neural.hpp:383-391)
+  mid = 0.0;
+  rl = 0.0;
+  rh = 0.0;
+  bool rem_ok = true;
+  if (lane < n_o) {
+    mid = mul(add(blo, bup), 0.5);
+    rl = sub(blo, mid);
+    rh = sub(bup, mid);
+    rem_ok = finite(rl) && finite(rh);
+  }
+  lam_bad = !__all_sync(0xffffffffu, rem_ok && !lam_bad);  // reused as "remainder not finite"
+}
+
+// ---------------------------------------------------------------------------
+// fold_overflow (flowpipe_ct.hpp:317-350) on a symbolic state whose generator
+// blocks have widths wid[0..nq) (G0 = stA[:, 0:n], square).  Lane j < n + w
+// holds column j of [G0 | oldest block] in registers; pivots and multipliers
+// travel by shuffles (partial pivoting, first maximum wins, linalg.hpp:96-132).
+template <int NO>
+__device__ __forceinline__ void fold_overflow_warp(double* stA, int nzs, int n, int* wid, int& nq, int cap,
+                                                   double* scratch, int lane) {
+  while (nq > cap) {
+    const int w = wid[0];
+    const int nc = n + w;
+    constexpr int MR = NO;  // rows
+    double col[MR];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) col[i] = (lane < nc && i < n) ? stA[i * nzs + lane] : 0.0;
+    bool ok = true;
+    for (int kk = 0; kk < n; ++kk) {
+      int piv = kk;
+      double best = 0.0;
+#pragma unroll
+      for (int i = 0; i < MR; ++i) {
+        const double v = fabs(col[i]);
+        if (i == kk) best = v;
+        if (i > kk && i < n && v > best) {
+          best = v;
+          piv = i;
+        }
+      }
+      piv = __shfl_sync(0xffffffffu, piv, kk);
+      best = __shfl_sync(0xffffffffu, best, kk);
+      if (!(best > 1e-12)) {
+        ok = false;
+        break;
+      }
+      if (piv != kk) {
+        double vk = 0.0, vp = 0.0;
+#pragma unroll
+        for (int i = 0; i < MR; ++i) {
+          if (i == kk) vk = col[i];
+          if (i == piv) vp = col[i];
+        }
+#pragma unroll
+        for (int i = 0; i < MR; ++i) {
+          if (i == kk) col[i] = vp;
+          if (i == piv) col[i] = vk;
+        }
+      }
+      double f[MR];
+      double akk = 0.0;
+#pragma unroll
+      for (int i = 0; i < MR; ++i)
+        if (i == kk) akk = col[i];
+#pragma unroll
+      for (int i = 0; i < MR; ++i) f[i] = (i > kk && i < n) ? __ddiv_rn(col[i], akk) : 0.0;
+#pragma unroll
+      for (int i = 0; i < MR; ++i) f[i] = __shfl_sync(0xffffffffu, f[i], kk);
+      double mk = 0.0;
+#pragma unroll
+      for (int i = 0; i < MR; ++i)
+        if (i == kk) mk = col[i];
+      if (lane < nc && lane >= kk) {
+#pragma unroll
+        for (int i = 0; i < MR; ++i)
+          if (i > kk && i < n) col[i] = sub(col[i], mul(f[i], mk));
+      }
+    }
+    bool folded = false;
+    int off_new = n;  // column offset of the newest block
+    for (int q = 0; q + 1 < nq; ++q) off_new += wid[q];
+    double* newest = stA + off_new;
+    double* M = scratch;        // [n][nc] eliminated [U | B']
+    double* X = M + n * nc;     // [n][w]
+    double* E = X + n * w;      // [n][w]
+    double* rr = E + n * w;     // [n]
+    if (ok) {
+      if (lane < nc)
+#pragma unroll
+        for (int i = 0; i < MR; ++i)
+          if (i < n) M[i * nc + lane] = col[i];
+      __syncwarp();
+      if (lane >= n && lane < nc) {  // back substitution, lane n+j owns RHS column j
+        const int jc = lane - n;
+        double x[MR];
+#pragma unroll
+        for (int i = MR - 1; i >= 0; --i) {
+          if (i < n) {
+            double a = col[i];
+#pragma unroll
+            for (int kk = i + 1; kk < MR; ++kk)
+              if (kk < n) a = sub(a, mul(M[i * nc + kk], x[kk]));
+            x[i] = __ddiv_rn(a, M[i * nc + i]);
+            X[i * w + jc] = x[i];
+          } else {
+            x[i] = 0.0;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < n) {
+        double s = 0.0;
+        for (int j = 0; j < w; ++j) s = add(s, fabs(X[lane * w + j]));
+        rr[lane] = mul(s, 1.0 + 1e-12);
+      }
+      __syncwarp();
+      double worst = 0.0;
+      for (int j = 0; j < n; ++j) worst = smax(worst, rr[j]);
+      if (worst <= 1.0) {
+        // residual e = G0 X - a, then scale G0 columns, box e into the newest block
+        if (lane < w) {
+          for (int i = 0; i < n; ++i) {
+            double e = 0.0;
+            for (int kk = 0; kk < n; ++kk) e = add(e, mul(stA[i * nzs + kk], X[kk * w + lane]));
+            E[i * w + lane] = sub(e, stA[i * nzs + n + lane]);
+          }
+        }
+        __syncwarp();
+        if (lane < n) {
+          const double sc = add(1.0, rr[lane]);
+          for (int i = 0; i < n; ++i) stA[i * nzs + lane] = mul(stA[i * nzs + lane], sc);
+          double s = 0.0;
+          for (int j = 0; j < w; ++j) s = add(s, fabs(E[lane * w + j]));
+          newest[lane * nzs + lane] = add(newest[lane * nzs + lane], mul(s, 1.0 + 1e-12));
+        }
+        folded = true;
+      }
+    }
+    if (!folded && lane < n) {
+      double s = 0.0;
+      for (int j = 0; j < w; ++j) s = add(s, fabs(stA[lane * nzs + n + j]));
+      newest[lane * nzs + lane] = add(newest[lane * nzs + lane], s);
+    }
+    __syncwarp();
+    // pop the oldest block: columns [n + w, off_end) -> [n, off_end - w)
+    const int span = off_new + n - (n + w);  // remaining queue columns (newest block is n wide)
+    for (int i = 0; i < n; ++i) {
+      for (int j0 = 0; j0 < span; j0 += 32) {
+        const int j = j0 + lane;
+        const double v = (j < span) ? stA[i * nzs + n + w + j] : 0.0;
+        __syncwarp();
+        if (j < span) stA[i * nzs + n + j] = v;
+        __syncwarp();
+      }
+    }
+    if (lane == 0)
+      for (int q = 0; q + 1 < nq; ++q) wid[q] = wid[q + 1];
+    __syncwarp();
+    --nq;
+  }
+}
+
+// symbolic_box (flowpipe_ct.hpp:413-424): lane i < n returns box dim i.
+__device__ __forceinline__ bool symbolic_box_warp(const double* stA, int nzs, int n, const int* wid, int nq,
+                                                  const double* cc, int lane, double& lo, double& hi) {
+  lo = 0.0;
+  hi = 0.0;
+  bool fin = true;
+  if (lane < n) {
+    double r = 0.0;
+    for (int j = 0; j < n; ++j) r = add(r, fabs(stA[lane * nzs + j]));
+    int off = n;
+    for (int q = 0; q < nq; ++q) {
+      double s = 0.0;
+      for (int j = 0; j < wid[q]; ++j) s = add(s, fabs(stA[lane * nzs + off + j]));
+      r = add(r, s);
+      off += wid[q];
+    }
+    const double c = cc[lane];
+    lo = sub(c, r);
+    hi = add(c, r);
+    fin = finite(lo) && finite(hi);
+  }
+  return __all_sync(0xffffffffu, fin);
+}
+
+// ---------------------------------------------------------------------------
+// The horizon kernel: dt_reach (l == 0, dt_reach.hpp:41-104) or the DT closed
+// loop (l > 0: controller certification + [x; u] stacking as cl_reach,
+// closed_loop.hpp:118-153, then the dynamics certification), one warp per
+// sample for the whole horizon, weights streamed through the TMA ring.
 template <int NO, int CPL>
 __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_kernel(const DTParams P) {
-  constexpr int NOP = (NO + 1) & ~1;  // Lambda^T row stride (16-byte rows)
-  constexpr int NZG = 2;              // 32-column groups of the generator matrix (nzs <= 64)
   constexpr int HP = 32 * CPL;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int spc = blockDim.x / 32;
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-#ifdef RB_PHASE_TIMING
-  long long ph_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  long long ph_last = clock64();
-  int ph_cur = PH_PREP;
-#endif
 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   int* cnt = reinterpret_cast<int*>(smem_raw + 64);
@@ -371,18 +930,15 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
   double* wbase = bias_s + P.bias_doubles;
 
   const DevNet& N = P.net;
-  const int L = N.L;
-  const int n = P.n, m = P.m, H = P.H;
+  const int n = P.n, m = P.m, H = P.H, l_ctl = P.l;
   const int cap = P.window > 0 ? P.window : 1;
-  const double* blob = N.blob;
   const uint32_t total_chunks = static_cast<uint32_t>(P.n_chunks_step) * static_cast<uint32_t>(H);
 
   for (int i = threadIdx.x; i < P.n_chunks_step; i += blockDim.x) {
     tab_off[i] = P.ch_off[i];
     tab_bytes[i] = P.ch_bytes[i];
   }
-  WStream ws_in{stages, full, cnt, tab_off, tab_bytes, blob, spc, P.nstage, P.stage_doubles, P.n_chunks_step,
-                0u, total_chunks};
+  WStream ws_in{stages, full, cnt, tab_off, tab_bytes, spc, P.nstage, SD, P.n_chunks_step, 0u, total_chunks};
   if (threadIdx.x == 0) {
     for (int s = 0; s < P.nstage; ++s) {
       mbar_init(&full[s], 1);
@@ -390,10 +946,16 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
     }
     fence_mbar_init();
   }
-  for (int l = 0; l < L; ++l) {  // CTA copy of every layer's (padded) bias
-    const int cnt_b = (l + 1 < L) ? HP : ((N.dims[l + 1] + 1) & ~1);
-    for (int i = threadIdx.x; i < cnt_b; i += blockDim.x) bias_s[P.bias_s_off[l] + i] = blob[N.b_off[l] + i];
+  for (int l = 0; l < N.L; ++l) {  // CTA copy of every layer's (padded) bias
+    const int cnt_b = (l + 1 < N.L) ? HP : ((N.dims[l + 1] + 1) & ~1);
+    for (int i = threadIdx.x; i < cnt_b; i += blockDim.x) bias_s[P.bias_s_off[l] + i] = N.blob[N.b_off[l] + i];
   }
+  if (l_ctl > 0)
+    for (int l = 0; l < P.ctl.L; ++l) {
+      const int cnt_b = (l + 1 < P.ctl.L) ? HP : ((P.ctl.dims[l + 1] + 1) & ~1);
+      for (int i = threadIdx.x; i < cnt_b; i += blockDim.x)
+        bias_s[P.bias_s_off_ctl[l] + i] = P.ctl.blob[P.ctl.b_off[l] + i];
+    }
   __syncthreads();
   if (threadIdx.x == 0)
     for (int s = 0; s < P.nstage && static_cast<uint32_t>(s) < total_chunks; ++s) ws_in.issue(s, s);
@@ -404,14 +966,13 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
   double* ws = wbase + static_cast<size_t>(warp) * P.warp_doubles;
   double* stA = ws + P.o_stA;  // n x nzs: [G0 | Q1 .. Qnq | (fresh)]
   double* cc = ws + P.o_c;     // n
-  double* pre = ws + P.o_pre;  // per hidden layer, per padded unit: (lo,hi) -> after relax (s, ui) [ReLU]
-  double* LT = ws + P.o_LT;    // Lambda^T: [col][NOP]
-  double* hb = LT;             // IBP layer input (lo,hi) per unit -- forward pass only
-  double* R = ws + P.o_R;      // tanh relaxation (s, li, ui) per unit
-  double* bf0 = ws + P.o_bf0;  // frozen first-layer bias (actions differ per sample)
-  unsigned* masks = reinterpret_cast<unsigned*>(ws + P.o_idx);  // [L-1][2][CPL]: active, unstable
-  unsigned char* alists = reinterpret_cast<unsigned char*>(masks + (L - 1) * 2 * CPL);  // [L-1][HP] active units
-  const int nzs = P.nzs;
+  int* wid = reinterpret_cast<int*>(ws + P.o_wid);
+  CertScratch<CPL> S{ws + P.o_pre, ws + P.o_LT, ws + P.o_R, ws + P.o_bf0, reinterpret_cast<unsigned*>(ws + P.o_idx),
+                     nullptr};
+  S.alists = reinterpret_cast<unsigned char*>(S.masks + (max(N.L, P.ctl.L) - 1) * 2 * CPL);
+  double* AG = ws + P.o_aug;   // closed loop: stacked (n+l) x ldag
+  double* cag = ws + P.o_cag;  // its centre
+  const int nzs = P.nzs, ldag = P.ldag;
 
   const double* act_base = P.actions;
   if (!P.actions_shared && m > 0) act_base += static_cast<size_t>(valid ? b : 0) * H * m;
@@ -461,378 +1022,64 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
   bool done = !valid;
 
   for (int k = 0; k < H; ++k) {
-    RB_PH(PH_PREP);
     const double* u = act_base + static_cast<size_t>(k) * m;
-    const int nz = n * (1 + nq);
-    bool preact_bad = false;
-    bool lam_bad = false;  // a non-finite Lambda entry: the dense reference turns it into a NaN shift
+    int nz = n;
+    for (int q = 0; q < nq; ++q) nz += wid[q];
+    double aout[NO][kNZG];
+    double mid, rl, rh;
+    bool preact_bad, rem_bad;
+    const double* Ain = stA;
+    int lda = nzs, nz_in = nz, n_i = n;
+    const double* cin = cc;
 
-    // ---- prepend layer IBP (neural.hpp:360-373 + interval.hpp:284-295):
-    // pre0_i = sum_j iv_scale(A_ij, [-1,1]) (+ the [0,0] remainder block) + c_i
-    if (!done && lane < n) {
-      double lo = 0.0, hi = 0.0;
-      for (int j = 0; j < nz; ++j) {
-        const double a = stA[lane * nzs + j];
-        lo = add(lo, (a >= 0.0) ? -a : a);  // a*-1 : a*1
-        hi = add(hi, (a >= 0.0) ? a : -a);
-      }
-      const double c = cc[lane];
-      hb[2 * lane] = add(lo, c);
-      hb[2 * lane + 1] = add(hi, c);
-    }
-    __syncwarp();
-
-    // ---- IBP through the hidden layers (neural.hpp:243-257); output layer skipped
-    RB_PH(PH_IBP);
-    for (int l = 0; l + 1 < L; ++l) {
-      const int width = N.dims[l + 1];
-      const int rows = N.dims[l];
-      const int ld = N.ldt[l];
-      const int act = N.acts[l];
-      const double* bias = bias_s + P.bias_s_off[l];
-      const unsigned* in_mask = masks + (l - 1) * 2 * CPL;  // l >= 1: active units of layer l-1
-      double alo[CPL], ahi[CPL], bfold[CPL];
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        alo[c] = 0.0;
-        ahi[c] = 0.0;
-        bfold[c] = bias[c * 32 + lane];
-      }
-      const unsigned char* in_list = alists + (l - 1) * HP;
-      auto ibp_row = [&](const double* ch, int r0, int j) {
-        const double* wrow = ch + (j - r0) * ld + lane;
-        const double2 x = *reinterpret_cast<const double2*>(hb + 2 * j);
-        double w[CPL], tl[CPL], th[CPL];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) w[c] = wrow[c * 32];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const bool pos = w[c] >= 0.0;
-          tl[c] = mul(w[c], pos ? x.x : x.y);
-          th[c] = mul(w[c], pos ? x.y : x.x);
-        }
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          alo[c] = add(alo[c], tl[c]);
-          ahi[c] = add(ahi[c], th[c]);
-        }
-      };
-      const int rpc = rows_per_chunk(ld, SD);
-      int t = 0;
-      for (int r0 = 0; r0 < rows; r0 += rpc) {
-        const double* ch = stages + ws_in.acquire() * SD;
-        const int nr = min(rpc, rows - r0);
-        if (!done) {
-          if (l > 0) {
-            const int t1 = popc_below(in_mask, r0 + nr);
-#pragma unroll 2
-            for (; t < t1; ++t) ibp_row(ch, r0, in_list[t]);
-          } else {
-            const int nx = min(n, r0 + nr);
-#pragma unroll 2
-            for (int j = r0; j < nx; ++j) ibp_row(ch, r0, j);
-          }
-          if (l == 0) {
-            // freeze_trailing_inputs (neural.hpp:410): b += W[:, n+j] u_j
-            for (int r = max(n - r0, 0); r < nr; ++r) {
-              const double uj = u[r0 + r - n];
-              const double* wrow = ch + r * ld + lane;
-#pragma unroll
-              for (int c = 0; c < CPL; ++c) bfold[c] = add(bfold[c], mul(wrow[c * 32], uj));
-            }
-          }
-        }
-        ws_in.release(lane);
+    if (l_ctl > 0) {
+      // ---- controller: u_tm = ctl_crown(x_tm, ctl, {}) (neural.hpp:418-424)
+      certify<NO, CPL>(P.ctl, bias_s, P.bias_s_off_ctl, n, l_ctl, nullptr, stA, nzs, nz, cc, S, ws_in, stages, SD,
+                       lane, done, aout, mid, rl, rh, preact_bad, rem_bad);
+      if (!done && (preact_bad || rem_bad)) {  // cl_reach's controller failures (closed_loop.hpp:106-115)
+        status = preact_bad ? ST_CTL_PREACT : ST_CTL_CERT;
+        failed_step = k;
+        done = true;
       }
       if (!done) {
-        double* pl = pre + l * 2 * HP;
-        unsigned* am = masks + l * 2 * CPL;
-        int lbase = 0;
+        // stack [x; u] over the shared variables (closed_loop.hpp:118-153): x rows keep their
+        // columns, u rows take the certified control map; fresh block diag(0.., rad(u.rem))
+        const int w_new = n + l_ctl;
+        for (int i = 0; i < n; ++i)
+          for (int j = lane; j < nz + w_new; j += 32) AG[i * ldag + j] = (j < nz) ? stA[i * nzs + j] : 0.0;
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const int o = c * 32 + lane;
-          const double plo = add(alo[c], bfold[c]);
-          const double phi = add(ahi[c], bfold[c]);
-          *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(plo, phi);
-          if (l == 0 && m > 0) bf0[o] = bfold[c];
-          const bool fin = finite(plo) && finite(phi);
-          if (o < width && act != 2 && !fin) preact_bad = true;
-          // ReLU: inactive iff hi <= 0; unstable iff lo < 0 < hi.  Other acts: dense.
-          const bool actv = (o < width) && ((act != 0) || !(phi <= 0.0));
-          const bool unst = (o < width) && ((act != 0) || (plo < 0.0 && phi > 0.0) || !fin);
-          const unsigned ma = __ballot_sync(0xffffffffu, actv);
-          const unsigned mu = __ballot_sync(0xffffffffu, unst);
-          if (lane == 0) {
-            am[c] = ma;
-            am[CPL + c] = mu;
-          }
-          if (actv) alists[l * HP + lbase + __popc(ma & ((1u << lane) - 1u))] = static_cast<unsigned char>(o);
-          lbase += __popc(ma);
-          alo[c] = act_apply(act, plo);
-          ahi[c] = act_apply(act, phi);
-        }
-        __syncwarp();  // every lane is done reading hb
-#pragma unroll
-        for (int c = 0; c < CPL; ++c)
-          *reinterpret_cast<double2*>(hb + 2 * (c * 32 + lane)) = make_double2(alo[c], ahi[c]);
-        __syncwarp();
-      }
-    }
-    if (!done) preact_bad = __any_sync(0xffffffffu, preact_bad);
-
-    // ---- CROWN backward (neural.hpp:297-327)
-    // init: Lambda = I . W_{L-1} = W_{L-1};  b = 0 + I . b_{L-1}
-    RB_PH(PH_BINIT);
-    double blo = 0.0, bup = 0.0;
-    {
-      const int l = L - 1;
-      const int rows = N.dims[l + 1];  // = n
-      const int ncols = (l == 0) ? n : N.dims[l];
-      const int ld = N.ldw[l];
-      const int rpc = rows_per_chunk(ld, P.stage_doubles);
-      for (int r0 = 0; r0 < rows; r0 += rpc) {
-        const double* ch = stages + ws_in.acquire() * SD;
-        const int nr = min(rpc, rows - r0);
-        if (!done) {
-          for (int r = 0; r < nr; ++r) {
-            const int i = r0 + r;
-            for (int j = lane; j < ncols; j += 32) LT[j * NOP + i] = add(0.0, ch[r * ld + j]);
-          }
-        }
-        ws_in.release(lane);
-      }
-      if (!done && lane < n) {
-        double bi = bias_s[P.bias_s_off[l] + lane];
-        if (l == 0 && m > 0) {  // single-layer net: fold the action into the bias here
-          const double* w = blob + N.w_off[0] + static_cast<size_t>(lane) * N.ldw[0];
-          for (int j = 0; j < m; ++j) bi = add(bi, mul(w[n + j], u[j]));
-          bf0[lane] = bi;
-        }
-        blo = add(0.0, bi);
-        bup = blo;
-      }
-      __syncwarp();
-    }
-    for (int l = L - 2; l >= 0; --l) {
-      const int act = N.acts[l];
-      const int width = N.dims[l + 1];
-      const double* bvec = (l == 0 && m > 0) ? bf0 : bias_s + P.bias_s_off[l];
-      const unsigned* am = masks + l * 2 * CPL;
-      double* pl = pre + l * 2 * HP;
-      RB_PH(PH_CHAIN);
-      if (!done) {
-        if (act == 0) {
-          // ReLU relaxation (parallel): (s, ui) overwrite the preactivation slots; li = 0
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const int o = c * 32 + lane;
-            const double2 p = *reinterpret_cast<const double2*>(pl + 2 * o);
-            double s, li, ui;
-            relax(0, p.x, p.y, s, li, ui);
-            *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(s, ui);
-          }
-          __syncwarp();
-          // intercept chains over the unstable units (unscaled Lambda), lane i = row i
-          if (lane < n) {
-            for_each_row(am + CPL, 0, width, [&](int j) {
-              const double a = LT[j * NOP + lane];
-              const double ui = pl[2 * j + 1];
-              if (a >= 0.0) bup = add(bup, mul(a, ui));
-              else blo = add(blo, mul(a, ui));
-            });
-          }
-          __syncwarp();
-          // slope scaling (parallel over units): Lambda(:, j) *= s_j
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const int o = c * 32 + lane;
-            const double s = pl[2 * o];
-            double* col = LT + o * NOP;
-#pragma unroll
-            for (int i = 0; i < NOP; i += 2) {
-              const double2 v = *reinterpret_cast<const double2*>(col + i);
-              *reinterpret_cast<double2*>(col + i) = make_double2(mul(v.x, s), mul(v.y, s));
-            }
-          }
-          __syncwarp();
-          // shift chain Lambda_s . b (dense; inactive units add +-0), lane i = row i
-          if (lane < n) {
-            double shift = 0.0;
-#pragma unroll 8
-            for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
-            blo = add(blo, shift);
-            bup = add(bup, shift);
-          }
-        } else {
-          if (act == 1) {
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) {
-              const int o = c * 32 + lane;
-              const double2 p = *reinterpret_cast<const double2*>(pl + 2 * o);
-              double s, li, ui;
-              relax(1, p.x, p.y, s, li, ui);
-              R[3 * o] = s;
-              R[3 * o + 1] = li;
-              R[3 * o + 2] = ui;
-            }
-            __syncwarp();
-          }
-          if (lane < n) {
-            double shift = 0.0;
-            if (act == 1) {
-              for (int j = 0; j < width; ++j) {
-                const double a = LT[j * NOP + lane];
-                const double s = R[3 * j], li = R[3 * j + 1], ui = R[3 * j + 2];
-                const bool pos = a >= 0.0;
-                blo = add(blo, mul(a, pos ? li : ui));
-                bup = add(bup, mul(a, pos ? ui : li));
-                const double as = mul(a, s);
-                LT[j * NOP + lane] = as;
-                shift = add(shift, mul(as, bvec[j]));
-              }
-            } else {
-              for (int j = 0; j < width; ++j) shift = add(shift, mul(LT[j * NOP + lane], bvec[j]));
-            }
-            blo = add(blo, shift);
-            bup = add(bup, shift);
-          }
-        }
-        __syncwarp();
-      }
-      // dense contraction Lambda <- Lambda_s . W_l  (linalg.hpp:53-63, i-k-j order) over the rows
-      // k of units with a non-zero slope
-      const int ld = N.ldw[l];
-      const int rpc = rows_per_chunk(ld, P.stage_doubles);
-      if (l > 0) {
-        RB_PH(PH_GEMM);
-        double acc[NO][CPL];
-#pragma unroll
-        for (int i = 0; i < NO; ++i)
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) acc[i][c] = 0.0;
-        const unsigned char* alist = alists + l * HP;
-        int t = 0;
-        for (int r0 = 0; r0 < width; r0 += rpc) {
-          const double* ch = stages + ws_in.acquire() * SD;
-          const int nr = min(rpc, width - r0);
-          if (!done) {
-            const int t1 = popc_below(am, r0 + nr);
-#pragma unroll 2
-            for (; t < t1; ++t) {
-              const int kk = alist[t];
-              const double* lrow = LT + kk * NOP;
-              const double* wrow = ch + (kk - r0) * ld + lane;
-              double lam[NOP], w[CPL];
-#pragma unroll
-              for (int i = 0; i < NOP; i += 2) {
-                const double2 v = *reinterpret_cast<const double2*>(lrow + i);
-                lam[i] = v.x;
-                lam[i + 1] = v.y;
-              }
-#pragma unroll
-              for (int c = 0; c < CPL; ++c) w[c] = wrow[c * 32];
-              double tt[NO][CPL];
-#pragma unroll
-              for (int i = 0; i < NO; ++i)
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) tt[i][c] = mul(lam[i], w[c]);
-#pragma unroll
-              for (int i = 0; i < NO; ++i)
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) acc[i][c] = add(acc[i][c], tt[i][c]);
-            }
-          }
-          ws_in.release(lane);
-        }
-        if (!done) {
-          const int ncols = N.dims[l];
-#pragma unroll
-          for (int c = 0; c < CPL; ++c)
+        for (int g = 0; g < kNZG; ++g) {
+          const int j = g * 32 + lane;
+          if (j < nz)
 #pragma unroll
             for (int i = 0; i < NO; ++i)
-              if (i < n && c * 32 + lane < ncols && !finite(acc[i][c])) lam_bad = true;
-          __syncwarp();
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            double* dst = LT + (c * 32 + lane) * NOP;
-#pragma unroll
-            for (int i = 0; i < NOP; i += 2)
-              *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i][c], (i + 1 < NO) ? acc[i + 1][c] : 0.0);
-          }
-          __syncwarp();
+              if (i < l_ctl) AG[(n + i) * ldag + j] = aout[i][g];
         }
+        const double urad = mul(sub(rh, rl), 0.5);
+        const double umid = add(mid, mul(add(rl, rh), 0.5));
+        for (int i = 0; i < l_ctl; ++i) {
+          const double ri = __shfl_sync(0xffffffffu, urad, i);
+          const double mi = __shfl_sync(0xffffffffu, umid, i);
+          for (int j = lane; j < w_new; j += 32) AG[(n + i) * ldag + nz + j] = (j == n + i) ? ri : 0.0;
+          if (lane == 0) cag[n + i] = mi;
+        }
+        if (lane < n) cag[lane] = add(cc[lane], 0.0);  // x_tm.c + mid([0,0])
+        __syncwarp();
+        Ain = AG;
+        lda = ldag;
+        nz_in = nz + w_new;
+        n_i = n + l_ctl;
+        cin = cag;
       } else {
-        // frozen first layer: only the n state columns survive -- a tiny GEMM
-        // (n_o x width) . (width x n); lane p owns outputs p and p + 32 of the
-        // n_o x n grid, each a sequential k chain as the reference's.
-        RB_PH(PH_GEMM0);
-        const int npair = n * n;
-        const int p0 = lane, p1 = lane + 32;
-        const int i0 = (p0 < npair ? p0 : 0) / n, j0 = (p0 < npair ? p0 : 0) % n;
-        const int i1 = (p1 < npair ? p1 : 0) / n, j1 = (p1 < npair ? p1 : 0) % n;
-        double a0 = 0.0, a1 = 0.0;
-        const unsigned char* alist0 = alists;  // layer 0's active units
-        int t = 0;
-        for (int r0 = 0; r0 < width; r0 += rpc) {
-          const double* ch = stages + ws_in.acquire() * SD;
-          const int nr = min(rpc, width - r0);
-          if (!done) {
-            const int t1 = popc_below(am, r0 + nr);
-#pragma unroll 4
-            for (; t < t1; ++t) {
-              const int kk = alist0[t];
-              const double* wrow = ch + (kk - r0) * ld;
-              a0 = add(a0, mul(LT[kk * NOP + i0], wrow[j0]));
-              a1 = add(a1, mul(LT[kk * NOP + i1], wrow[j1]));
-            }
-          }
-          ws_in.release(lane);
-        }
-        if (!done) {
-          if ((p0 < npair && !finite(a0)) || (p1 < npair && !finite(a1))) lam_bad = true;
-          __syncwarp();
-          if (p0 < npair) LT[j0 * NOP + i0] = a0;
-          if (p1 < npair) LT[j1 * NOP + i1] = a1;
-          __syncwarp();
-        }
+        nz_in = nz + n + l_ctl;
       }
     }
-    RB_PH(PH_TAIL);
+
+    // ---- dynamics / one-step map: certify_tm_input (neural.hpp:342-394)
+    certify<NO, CPL>(N, bias_s, P.bias_s_off, n_i, n, u, Ain, lda, nz_in, cin, S, ws_in, stages, SD, lane, done, aout,
+                     mid, rl, rh, preact_bad, rem_bad);
     if (done) continue;  // keep draining the weight stream in lockstep
-
-    // ---- prepended layer W = [A | I], b = c: shift chain and A_out = Lambda . A
-    if (lane < n) {
-      double shift = 0.0;
-      for (int kk = 0; kk < n; ++kk) shift = add(shift, mul(LT[kk * NOP + lane], cc[kk]));
-      blo = add(blo, shift);
-      bup = add(bup, shift);
-    }
-    double aout[NO][NZG];
-#pragma unroll
-    for (int g = 0; g < NZG; ++g) {
-      const int j = g * 32 + lane;
-#pragma unroll
-      for (int i = 0; i < NO; ++i) aout[i][g] = 0.0;
-      if (j < nz) {
-        for (int kk = 0; kk < n; ++kk) {
-          const double akj = stA[kk * nzs + j];
-#pragma unroll
-          for (int i = 0; i < NO; ++i) aout[i][g] = mac(aout[i][g], LT[kk * NOP + i], akj);
-        }
-      }
-    }
-
-    // ---- tail (neural.hpp:383-391), failure checks (dt_reach.hpp:58-67)
-    double mid = 0.0, rl = 0.0, rh = 0.0;
-    bool rem_ok = true;
-    if (lane < n) {
-      mid = mul(add(blo, bup), 0.5);
-      rl = sub(blo, mid);
-      rh = sub(bup, mid);
-      rem_ok = finite(rl) && finite(rh);
-    }
-    rem_ok = __all_sync(0xffffffffu, rem_ok && !lam_bad);
-    if (preact_bad || !rem_ok) {
+    if (preact_bad || rem_bad) {  // dt_reach.hpp:58-67
       status = preact_bad ? ST_PREACT : ST_CERT;
       failed_step = k;
       done = true;
@@ -841,9 +1088,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
     __syncwarp();
     // ---- re-seed (dt_reach.hpp:69-92): c' = c + mid(rem), blocks <- A_out, fresh = diag(rad(rem))
 #pragma unroll
-    for (int g = 0; g < NZG; ++g) {
+    for (int g = 0; g < kNZG; ++g) {
       const int j = g * 32 + lane;
-      if (j < nz)
+      if (j < nz_in)
 #pragma unroll
         for (int i = 0; i < NO; ++i)
           if (i < n) stA[i * nzs + j] = aout[i][g];
@@ -851,168 +1098,21 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
     if (lane < n) {
       cc[lane] = add(mid, mul(add(rl, rh), 0.5));
       const double rad = mul(sub(rh, rl), 0.5);
-      for (int j = 0; j < n; ++j) stA[lane * nzs + nz + j] = (j == lane) ? rad : 0.0;
+      for (int j = 0; j < n; ++j) stA[lane * nzs + nz_in + j] = (j == lane) ? rad : 0.0;
     }
-    ++nq;
+    if (lane == 0) {
+      if (l_ctl > 0) wid[nq++] = n + l_ctl;
+      wid[nq++] = n;
+    }
+    nq = __shfl_sync(0xffffffffu, nq, 0);
     __syncwarp();
 
-    // ---- fold_overflow (flowpipe_ct.hpp:317-350): lane j < 2n holds column j of
-    // [G0 | oldest block] in registers; pivots and row multipliers travel by shuffles
-    RB_PH(PH_FOLD);
-    while (nq > cap) {
-      const int n2 = 2 * n;
-      double col[NO];
-#pragma unroll
-      for (int i = 0; i < NO; ++i) col[i] = (lane < n2 && i < n) ? stA[i * nzs + lane] : 0.0;
-      bool ok = true;
-      for (int kk = 0; kk < n; ++kk) {
-        // pivot search on column kk (owner lane kk), first maximum wins (linalg.hpp:104-112)
-        int piv = kk;
-        double best = 0.0;
-#pragma unroll
-        for (int i = 0; i < NO; ++i) {
-          const double v = fabs(col[i]);
-          if (i == kk) best = v;
-          if (i > kk && i < n && v > best) {
-            best = v;
-            piv = i;
-          }
-        }
-        piv = __shfl_sync(0xffffffffu, piv, kk);
-        best = __shfl_sync(0xffffffffu, best, kk);
-        if (!(best > 1e-12)) {
-          ok = false;
-          break;
-        }
-        if (piv != kk) {  // swap rows kk and piv in every column
-          double vk = 0.0, vp = 0.0;
-#pragma unroll
-          for (int i = 0; i < NO; ++i) {
-            if (i == kk) vk = col[i];
-            if (i == piv) vp = col[i];
-          }
-#pragma unroll
-          for (int i = 0; i < NO; ++i) {
-            if (i == kk) col[i] = vp;
-            if (i == piv) col[i] = vk;
-          }
-        }
-        // multipliers f_i = a(i,kk) / a(kk,kk), computed by the pivot-column lane
-        double f[NO];
-        double akk = 0.0;
-#pragma unroll
-        for (int i = 0; i < NO; ++i)
-          if (i == kk) akk = col[i];
-#pragma unroll
-        for (int i = 0; i < NO; ++i) f[i] = (i > kk && i < n) ? __ddiv_rn(col[i], akk) : 0.0;
-#pragma unroll
-        for (int i = 0; i < NO; ++i) f[i] = __shfl_sync(0xffffffffu, f[i], kk);
-        double mk = 0.0;
-#pragma unroll
-        for (int i = 0; i < NO; ++i)
-          if (i == kk) mk = col[i];
-        if (lane < n2 && lane >= kk) {
-#pragma unroll
-          for (int i = 0; i < NO; ++i)
-            if (i > kk && i < n) col[i] = sub(col[i], mul(f[i], mk));
-        }
-      }
-      bool folded = false;
-      double* newest = stA + n * nq;  // column offset of the newest block
-      double* M = LT;                  // [n][2n] eliminated [U | B']
-      double* X = LT + 2 * n * n;      // [n][n]
-      double* E = X + n * n;           // [n][n]
-      double* rr = E + n * n;          // [n]
-      if (ok) {
-        if (lane < n2)
-#pragma unroll
-          for (int i = 0; i < NO; ++i)
-            if (i < n) M[i * n2 + lane] = col[i];
-        __syncwarp();
-        if (lane >= n && lane < n2) {  // back substitution, lane n+j owns RHS column j
-          const int jc = lane - n;
-          double x[NO];
-#pragma unroll
-          for (int i = NO - 1; i >= 0; --i) {
-            if (i < n) {
-              double a = col[i];
-#pragma unroll
-              for (int kk = i + 1; kk < NO; ++kk)
-                if (kk < n) a = sub(a, mul(M[i * n2 + kk], x[kk]));
-              x[i] = __ddiv_rn(a, M[i * n2 + i]);
-              X[i * n + jc] = x[i];
-            } else {
-              x[i] = 0.0;
-            }
-          }
-        }
-        __syncwarp();
-        if (lane < n) {
-          double s = 0.0;
-          for (int j = 0; j < n; ++j) s = add(s, fabs(X[lane * n + j]));
-          rr[lane] = mul(s, 1.0 + 1e-12);
-        }
-        __syncwarp();
-        double worst = 0.0;
-        for (int j = 0; j < n; ++j) worst = smax(worst, rr[j]);
-        if (worst <= 1.0) {
-          // residual e = G0 X - a, then scale G0 columns, box e into the newest block
-          if (lane < n) {
-            for (int i = 0; i < n; ++i) {
-              double e = 0.0;
-              for (int kk = 0; kk < n; ++kk) e = add(e, mul(stA[i * nzs + kk], X[kk * n + lane]));
-              E[i * n + lane] = sub(e, stA[i * nzs + n + lane]);
-            }
-          }
-          __syncwarp();
-          if (lane < n) {
-            const double sc = add(1.0, rr[lane]);
-            for (int i = 0; i < n; ++i) stA[i * nzs + lane] = mul(stA[i * nzs + lane], sc);
-            double s = 0.0;
-            for (int j = 0; j < n; ++j) s = add(s, fabs(E[lane * n + j]));
-            newest[lane * nzs + lane] = add(newest[lane * nzs + lane], mul(s, 1.0 + 1e-12));
-          }
-          folded = true;
-        }
-      }
-      if (!folded && lane < n) {
-        double s = 0.0;
-        for (int j = 0; j < n; ++j) s = add(s, fabs(stA[lane * nzs + n + j]));
-        newest[lane * nzs + lane] = add(newest[lane * nzs + lane], s);
-      }
-      __syncwarp();
-      // pop the oldest block: columns [2n, n(nq+1)) -> [n, n nq)
-      const int span = n * (nq - 1);
-      for (int i = 0; i < n; ++i) {
-        for (int j0 = 0; j0 < span; j0 += 32) {
-          const int j = j0 + lane;
-          const double v = (j < span) ? stA[i * nzs + 2 * n + j] : 0.0;
-          __syncwarp();
-          if (j < span) stA[i * nzs + n + j] = v;
-          __syncwarp();
-        }
-      }
-      --nq;
-    }
+    // ---- fold_overflow (flowpipe_ct.hpp:317-350)
+    fold_overflow_warp<NO>(stA, nzs, n, wid, nq, cap, S.LT, lane);
 
     // ---- symbolic_box (flowpipe_ct.hpp:413-424)
-    RB_PH(PH_BOX);
-    double lo = 0.0, hi = 0.0;
-    bool fin = true;
-    if (lane < n) {
-      double r = 0.0;
-      for (int j = 0; j < n; ++j) r = add(r, fabs(stA[lane * nzs + j]));
-      for (int q = 1; q <= nq; ++q) {
-        double s = 0.0;
-        for (int j = 0; j < n; ++j) s = add(s, fabs(stA[lane * nzs + q * n + j]));
-        r = add(r, s);
-      }
-      const double c = cc[lane];
-      lo = sub(c, r);
-      hi = add(c, r);
-      fin = finite(lo) && finite(hi);
-    }
-    fin = __all_sync(0xffffffffu, fin);
+    double lo, hi;
+    const bool fin = symbolic_box_warp(stA, nzs, n, wid, nq, cc, lane, lo, hi);
     emit_box(k + 1, lo, hi, fin);
     nboxes = k + 2;
     if (!fin) {
@@ -1027,14 +1127,6 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
       nq = 0;
     }
   }
-  RB_PH(PH_DRAIN);
-#ifdef RB_PHASE_TIMING
-  RB_PH(PH_DRAIN);
-  if (lane == 0) {
-    for (int i = 0; i < 10; ++i) atomicAdd(&g_phase_cycles[i], static_cast<unsigned long long>(ph_acc[i]));
-    atomicAdd(&g_phase_cycles[10], static_cast<unsigned long long>(ws_in.wait_cycles));
-  }
-#endif
 
   if (!valid) return;
   if (!P.split) {

@@ -129,16 +129,28 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 
 int cpl_for(int maxh) { return maxh <= 32 ? 1 : maxh <= 64 ? 2 : maxh <= 96 ? 3 : maxh <= 128 ? 4 : maxh <= 256 ? 8 : 0; }
 
-int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::DTParams& P, DTLayout& lay) {
+// Layout of the horizon kernel for the one-step network `net` (open loop) or
+// the dynamics `net` + controller `ctl` (closed loop, l = ctl output dim).
+int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::DTParams& P, DTLayout& lay,
+            const reach_net* ctl = nullptr) {
   const int L = net->L;
+  const int l = ctl ? ctl->dims[ctl->L] : 0;
   const int cap = window > 0 ? window : 1;
-  const int no = n <= 2 ? 2 : n <= 4 ? 4 : n <= 6 ? 6 : n <= 8 ? 8 : 0;
+  const int rows_max = std::max(n, l);
+  const int no = rows_max <= 2 ? 2 : rows_max <= 4 ? 4 : rows_max <= 6 ? 6 : rows_max <= 8 ? 8 : 0;
   if (no == 0) return fail(ctx, REACH_E_UNSUPPORTED, "state dim > 8 not in this kernel family");
-  if (net->cpl == 0) return fail(ctx, REACH_E_UNSUPPORTED, "hidden width > 256 not in this kernel family");
+  if (net->cpl == 0 || (ctl && ctl->cpl == 0))
+    return fail(ctx, REACH_E_UNSUPPORTED, "hidden width > 256 not in this kernel family");
+  if (ctl && ctl->cpl != net->cpl)
+    return fail(ctx, REACH_E_UNSUPPORTED, "controller and dynamics hidden widths in different kernel families");
   const int hp = net->hp;
-  const int nzs = n * (cap + 2);
-  if (nzs > 64) return fail(ctx, REACH_E_UNSUPPORTED, "n * (window + 2) > 64 not in this kernel family");
+  const int n_i = n + l;  // rows of the certified input TM
+  const int wmax = n + l;  // widest generator block
+  const int nzs = n + (cap + 2) * wmax;  // G0 + queue (<= cap + 2 blocks before a fold)
+  if (n + (cap + 1) * wmax > 64) return fail(ctx, REACH_E_UNSUPPORTED, "generator matrix wider than 64 columns");
+  if (n * n_i > 64 || n + wmax > 32) return fail(ctx, REACH_E_UNSUPPORTED, "state/control dims too large");
   const int nop = (no + 1) & ~1;
+  const int Lmax = std::max(L, ctl ? ctl->L : 0);
   auto ev = [](int x) { return (x + 1) & ~1; };
   int off = 0;
   P.o_stA = off;
@@ -146,52 +158,76 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::
   P.o_c = off;
   off += ev(n);
   P.o_pre = off;
-  off += (L - 1) * 2 * hp;
-  P.o_LT = off;  // also the IBP input buffer (2 hp) and the fold scratch (4 n^2 + n)
-  off += ev(std::max({nop * std::max(hp, n + m), 2 * hp, 4 * n * n + n}));
+  off += (Lmax - 1) * 2 * hp;
+  P.o_LT = off;  // also the IBP input buffer (2 hp) and the fold scratch
+  const int fold_scr = n * (n + wmax) + 2 * n * wmax + n;
+  off += ev(std::max({nop * std::max(hp, n_i + m), 2 * std::max(hp, n_i), fold_scr}));
   bool tanh_any = false;
-  for (int l = 0; l + 1 < L; ++l) tanh_any |= net->acts[l] == REACH_ACT_TANH;
+  for (int i = 0; i + 1 < L; ++i) tanh_any |= net->acts[i] == REACH_ACT_TANH;
+  if (ctl)
+    for (int i = 0; i + 1 < ctl->L; ++i) tanh_any |= ctl->acts[i] == REACH_ACT_TANH;
   P.has_tanh = tanh_any ? 1 : 0;
   P.o_R = off;
   if (tanh_any) off += 3 * hp;
   P.o_bf0 = off;
   if (m > 0) off += std::max(hp, ev(n));
   P.o_idx = off;  // per hidden layer two unit bitmasks (active, unstable) + the active-unit list
-  off += ev(((L - 1) * 2 * (hp / 32) * 4 + (L - 1) * hp + 7) / 8);
+  off += ev(((Lmax - 1) * 2 * (hp / 32) * 4 + (Lmax - 1) * hp + 7) / 8);
+  P.o_wid = off;  // generator block widths
+  off += ev((cap + 4 + 1) / 2);
+  P.o_aug = off;
+  P.ldag = nzs;
+  if (ctl) off += ev(n_i * nzs);
+  P.o_cag = off;
+  if (ctl) off += ev(n_i);
   P.warp_doubles = ev(off);
   P.nzs = nzs;
   P.hp = hp;
   int boff = 0;
-  for (int l = 0; l < L; ++l) {
-    P.bias_s_off[l] = boff;
-    boff += (l + 1 < L) ? hp : ev(net->dims[l + 1]);
+  for (int i = 0; i < L; ++i) {
+    P.bias_s_off[i] = boff;
+    boff += (i + 1 < L) ? hp : ev(net->dims[i + 1]);
   }
+  if (ctl)
+    for (int i = 0; i < ctl->L; ++i) {
+      P.bias_s_off_ctl[i] = boff;
+      boff += (i + 1 < ctl->L) ? hp : ev(ctl->dims[i + 1]);
+    }
   P.bias_doubles = ev(boff);
   const int kStageDoubles = env_int("RB_STAGE_DOUBLES", kStageDoublesDefault, 512, 8192) & ~1;
   const int kNStage = env_int("RB_NSTAGE", kNStageDefault, 2, 8);
   P.stage_doubles = kStageDoubles;
   P.nstage = kNStage;
-  // weight-stream chunk table of one DT step (consumption order of the kernel)
-  const rb::DevNet& d = net->dev;
+  // weight-stream chunk table of one DT step (consumption order of the kernel), absolute addresses
   int nc = 0;
-  auto add_matrix = [&](long long moff, int rows, int ld) -> bool {
+  auto add_matrix = [&](const double* base, long long moff, int rows, int ld) -> bool {
     if (ld > kStageDoubles) return false;
     const int rpc = std::max(1, kStageDoubles / ld);
     for (int r0 = 0; r0 < rows; r0 += rpc) {
       if (nc >= rb::kMaxChunks) return false;
       const int nr = std::min(rpc, rows - r0);
-      P.ch_off[nc] = moff + static_cast<long long>(r0) * ld;
+      P.ch_off[nc] = reinterpret_cast<long long>(base + moff + static_cast<long long>(r0) * ld);
       P.ch_bytes[nc] = static_cast<unsigned>(nr) * ld * 8u;
       ++nc;
     }
     return true;
   };
+  auto add_net = [&](const reach_net* nt) -> bool {
+    const rb::DevNet& d = nt->dev;
+    bool ok = true;
+    for (int i = 0; i + 1 < d.L; ++i) ok = ok && add_matrix(nt->blob, d.wt_off[i], d.dims[i], d.ldt[i]);
+    for (int i = d.L - 1; i >= 0; --i) ok = ok && add_matrix(nt->blob, d.w_off[i], d.dims[i + 1], d.ldw[i]);
+    return ok;
+  };
   bool ok = true;
-  for (int l = 0; l + 1 < L; ++l) ok = ok && add_matrix(d.wt_off[l], d.dims[l], d.ldt[l]);
-  for (int l = L - 1; l >= 0; --l) ok = ok && add_matrix(d.w_off[l], d.dims[l + 1], d.ldw[l]);
+  if (ctl) ok = add_net(ctl);
+  ok = ok && add_net(net);
   if (!ok) return fail(ctx, REACH_E_UNSUPPORTED, "network too large for the weight stream");
   P.n_chunks_step = nc;
-  const size_t fixed = rb::kHeaderBytes + static_cast<size_t>(kNStage) * kStageDoubles * 8 + static_cast<size_t>(P.bias_doubles) * 8;
+  P.l = l;
+  if (ctl) P.ctl = ctl->dev;
+  const size_t fixed =
+      rb::kHeaderBytes + static_cast<size_t>(kNStage) * kStageDoubles * 8 + static_cast<size_t>(P.bias_doubles) * 8;
   const size_t per = static_cast<size_t>(P.warp_doubles) * 8;
   int spc = static_cast<int>((static_cast<size_t>(ctx->max_smem) - fixed) / per);
   spc = std::min(spc, rb::kSampleWarps);
@@ -255,6 +291,8 @@ const char* reach_tube_status_string(int32_t status) {
     case REACH_TUBE_NONFINITE_PREACT: return "relax_activation: non-finite preactivation";
     case REACH_TUBE_DIVERGED_CERT: return "diverged certification";
     case REACH_TUBE_DIVERGED_BOX: return "diverged box";
+    case REACH_TUBE_CTL_FAILED: return "controller certification failed: relax_activation: non-finite preactivation";
+    case REACH_TUBE_CTL_DIVERGED: return "controller certification diverged";
     default: return "error";
   }
 }
@@ -453,17 +491,17 @@ int reach_net_free(reach_ctx* ctx, reach_net* net) {
   return REACH_OK;
 }
 
-int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, const reach_tube_out* out,
-                   int32_t flags) {
-  if (!ctx || !net || !a || !out) return REACH_E_INVALID_ARGUMENT;
-  if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach_batch: negative size");
-  int rc = validate_system(ctx, net, a->n, a->m);
-  if (rc) return rc;
+}  // extern "C"
+
+namespace {
+int run_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_net* ctl, const reach_dt_args* a,
+                 const reach_tube_out* out, int32_t flags) {
+  int rc = 0;
   if (a->batch == 0) return REACH_OK;
   RB_CUDA(cudaSetDevice(ctx->device));
   rb::DTParams P{};
   DTLayout lay;
-  rc = plan_dt(ctx, net, a->n, a->m, a->window, P, lay);
+  rc = plan_dt(ctx, net, a->n, a->m, a->window, P, lay, ctl);
   if (rc) return rc;
   P.net = net->dev;
   P.B = a->batch;
@@ -546,6 +584,34 @@ int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a,
   return REACH_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, const reach_tube_out* out,
+                   int32_t flags) {
+  if (!ctx || !net || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach_batch: negative size");
+  int rc = validate_system(ctx, net, a->n, a->m);
+  if (rc) return rc;
+  return run_dt_batch(ctx, net, nullptr, a, out, flags);
+}
+
+int reach_dtcl_batch(reach_ctx* ctx, const reach_net* dyn, const reach_net* ctl, const reach_dt_args* a,
+                     const reach_tube_out* out, int32_t flags) {
+  if (!ctx || !dyn || !ctl || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt closed loop: negative size");
+  if (a->m != 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt closed loop: actions come from the controller (m = 0)");
+  const int l = ctl->dims[ctl->L];
+  if (a->n <= 0 || ctl->dims[0] != a->n)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "ClosedLoopSpec: controller input dim mismatch");
+  if (dyn->dims[0] != a->n + l || dyn->dims[dyn->L] != a->n)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "ClosedLoopSpec: dynamics must act on the augmented (x,u) state");
+  return run_dt_batch(ctx, dyn, ctl, a, out, flags);
+}
+
+}  // extern "C"
+
 namespace {
 __global__ void hull_init_kernel(unsigned long long* klo, unsigned long long* khi, int* nan0, int* div, int count,
                                  int hp1, int* nboxes, unsigned long long* key) {
@@ -563,6 +629,8 @@ __global__ void hull_init_kernel(unsigned long long* klo, unsigned long long* kh
   }
 }
 }  // namespace
+
+extern "C" {
 
 int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_args* a, const reach_hull_out* out,
                      int32_t flags) {

@@ -149,3 +149,25 @@ def c3_tpushing(seed: int = MASTER_SEED, population: int = 4096, horizon: int = 
     cfg = SamplerConfig(population=population, elite_frac=0.1, iterations=iterations, init_std=0.3, smoothing=0.5,
                         refine_iters=0, seed=seed)
     return prob, cfg, np.zeros(n)
+
+
+@dataclass
+class ClosedLoopWorkload:
+    dyn: MLPNet
+    ctl: MLPNet
+    n: int
+    x0_lo: np.ndarray  # [B][n]
+    x0_hi: np.ndarray
+    horizon: int
+
+
+def c1_closed_loop(seed: int = MASTER_SEED, batch: int = 1, horizon: int = 20) -> ClosedLoopWorkload:
+    """BASELINE configs[0]: DT closed loop, 4-D NN dynamics (6->64->64->4 ReLU) + 2x64 ReLU
+    controller (4->64->64->2), one initial box, H=20 (SURVEY §8 shape sheet C1 / §8d)."""
+    rng = np.random.default_rng(seed + 1)
+    n, l = 4, 2
+    dyn = residual_relu_dynamics(rng, n, l, [64, 64], dt=0.1)
+    ctl = random_mlp(rng, n, [64, 64], l, Act.Relu, 0.6)
+    ctl.layers[-1].w *= 0.3
+    c = rng.uniform(-0.5, 0.5, size=(batch, n))
+    return ClosedLoopWorkload(dyn, ctl, n, c - 0.05, c + 0.05, horizon)

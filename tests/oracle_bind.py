@@ -195,3 +195,32 @@ def oracle_plan_cem(prob, cfg, x0):
 
 def ref_plan_cem(prob, cfg, x0):
     return _plan_cem(ref_lib(), "ref_", prob, cfg, x0)
+
+
+# --- DT closed loop (A11) ---------------------------------------------------
+def _dtcl(lib, prefix, dyn, ctl, n, x0_lo, x0_hi, horizon, prm, threads=None):
+    args_t = [C.POINTER(A.NetDesc), C.POINTER(A.NetDesc), C.POINTER(A.DTArgs), C.POINTER(A.TubeOut)]
+    if prefix == "ref_":
+        args_t.append(C.c_int32)
+    f = _mpc_fn(lib, prefix + "dtcl_batch", args_t)
+    x0_lo = np.ascontiguousarray(x0_lo, np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, np.float64)
+    B = x0_lo.shape[0]
+    out = TubeBatch(np.full((B, horizon + 1, n), np.nan), np.full((B, horizon + 1, n), np.nan),
+                    np.zeros(B, np.int32), np.zeros(B, np.int32), np.zeros(B, np.int32))
+    dd, k1 = dyn.desc()
+    cd, k2 = ctl.desc()
+    args = A.DTArgs(B, horizon, n, 0, prm.window, int(prm.rebuild_from_box), A.dptr(x0_lo), A.dptr(x0_hi),
+                    A.dptr(np.zeros(1)), 0)
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step), A.iptr(out.status))
+    extra = [threads or 0] if prefix == "ref_" else []
+    assert f(C.byref(dd), C.byref(cd), C.byref(args), C.byref(to), *extra) == 0
+    return out
+
+
+def oracle_dtcl_batch(dyn, ctl, n, x0_lo, x0_hi, horizon, prm=DTReachParams()):
+    return _dtcl(oracle_lib(), "orc_", dyn, ctl, n, x0_lo, x0_hi, horizon, prm)
+
+
+def ref_dtcl_batch(dyn, ctl, n, x0_lo, x0_hi, horizon, prm=DTReachParams(), threads=0):
+    return _dtcl(ref_lib(), "ref_", dyn, ctl, n, x0_lo, x0_hi, horizon, prm, threads)
