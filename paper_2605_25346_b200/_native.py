@@ -132,8 +132,8 @@ class Context:
 
     def phase_cycles(self):
         """Per-phase cycles of the DT kernel (profiling build only), else None."""
-        arr = (C.c_uint64 * 11)()
-        rc = self._lib.reach_debug_phase_cycles(self.handle, arr, 11)
+        arr = (C.c_uint64 * 16)()
+        rc = self._lib.reach_debug_phase_cycles(self.handle, arr, 16)
         return list(arr) if rc == A.REACH_OK else None
 
     def upload(self, net) -> "C.c_void_p":

@@ -91,6 +91,13 @@ struct DTParams {
   int n_chunks_step;
   long long ch_off[kMaxChunks];
   unsigned ch_bytes[kMaxChunks];
+  // wide family (wide_kernel.cuh): one CTA per sample, symbolic state in global memory
+  double* wws;              // per-CTA workspace: two state buffers of w_rows x w_lds
+  long long wws_stride;     // doubles per CTA
+  int w_lds, w_rows;        // state row stride / rows (n + l)
+  int w_nop, w_hw;          // Lambda^T row stride (odd), widest streamed row / unit count
+  int w_o_stage, w_o_relax, w_o_bf0, w_o_misc, w_o_int;  // shared-memory offsets (doubles)
+  unsigned long long* w_phase;  // optional per-phase cycle counters (RB_WIDE_PHASE=1), else null
 };
 
 enum : int { ST_OK = 0, ST_PREACT = 1, ST_CERT = 2, ST_BOX = 3, ST_CTL_PREACT = 4, ST_CTL_CERT = 5 };
@@ -462,8 +469,9 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
         if (l == 0 && m_frz > 0) S.bf0[o] = bfold[cc];
         const bool fin = finite(plo) && finite(phi);
         if (o < width && act != 2 && !fin) preact_bad = true;
-        // ReLU: inactive iff hi <= 0; unstable iff lo < 0 < hi.  Other acts: dense.
-        const bool actv = (o < width) && ((act != 0) || !(phi <= 0.0));
+        // ReLU slope (neural.hpp:166-227): 1 if lo >= 0 (a [0,0] preactivation is
+        // stably active), else 0 if hi <= 0 (inactive), else unstable.  Other acts: dense.
+        const bool actv = (o < width) && ((act != 0) || plo >= 0.0 || !(phi <= 0.0));
         const bool unst = (o < width) && ((act != 0) || (plo < 0.0 && phi > 0.0) || !fin);
         const unsigned ma = __ballot_sync(0xffffffffu, actv);
         const unsigned mu = __ballot_sync(0xffffffffu, unst);
@@ -1147,7 +1155,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, RB_MIN_BLOCKS) dt_horizon_k
 }
 
 // Converts the hull order keys back to doubles, applying the part-0 NaN rule.
-__global__ void hull_finalize_kernel(const unsigned long long* klo, const unsigned long long* khi, const int* nan0,
+static __global__ void hull_finalize_kernel(const unsigned long long* klo, const unsigned long long* khi, const int* nan0,
                                      int count, double* lo, double* hi) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;

@@ -22,6 +22,14 @@
 #include "diag.cuh"
 #include "dt_kernel.cuh"
 #include "plan.cuh"
+#include "wide_kernel.cuh"
+
+namespace rb {  // wide_inst.cu, one object per rows-per-thread value
+cudaError_t wide_call_rd1(int rc, const DTParams* P, size_t smem, int grid, int* occ, cudaStream_t s);
+cudaError_t wide_call_rd2(int rc, const DTParams* P, size_t smem, int grid, int* occ, cudaStream_t s);
+cudaError_t wide_call_rd4(int rc, const DTParams* P, size_t smem, int grid, int* occ, cudaStream_t s);
+cudaError_t wide_call_rd9(int rc, const DTParams* P, size_t smem, int grid, int* occ, cudaStream_t s);
+}  // namespace rb
 
 #include <atomic>
 #include <random>
@@ -41,6 +49,10 @@ struct reach_ctx {
   // plan-problem staging buffer (goal, weights, constraints) for the MPC kernels
   void* pbuf = nullptr;
   size_t pbuf_bytes = 0;
+  // per-CTA symbolic-state buffers of the wide kernel family
+  void* wws = nullptr;
+  size_t wws_bytes = 0;
+  unsigned long long* wphase = nullptr;  // wide-kernel phase counters (RB_WIDE_PHASE=1)
   // kernel timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
@@ -114,6 +126,8 @@ int timed_end(reach_ctx* ctx, cudaEvent_t stop) {
 struct DTLayout {
   int spc = 0, no = 0, cpl = 0;
   size_t smem = 0;
+  bool wide = false;  // dt_wide_kernel<rd, rc>, grid CTAs persistent over the batch
+  int rd = 0, rc = 0, grid = 0;
 };
 
 constexpr int kStageDoublesDefault = 2048;  // 16 KB bulk-copy stages
@@ -131,8 +145,8 @@ int cpl_for(int maxh) { return maxh <= 32 ? 1 : maxh <= 64 ? 2 : maxh <= 96 ? 3 
 
 // Layout of the horizon kernel for the one-step network `net` (open loop) or
 // the dynamics `net` + controller `ctl` (closed loop, l = ctl output dim).
-int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::DTParams& P, DTLayout& lay,
-            const reach_net* ctl = nullptr) {
+int plan_warp(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::DTParams& P, DTLayout& lay,
+              const reach_net* ctl) {
   const int L = net->L;
   const int l = ctl ? ctl->dims[ctl->L] : 0;
   const int cap = window > 0 ? window : 1;
@@ -241,6 +255,112 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb::
   return REACH_OK;
 }
 
+int wide_rows_pick(int rows) { return rows <= 8 ? 1 : rows <= 16 ? 2 : rows <= 32 ? 4 : rows <= 72 ? 9 : 0; }
+
+cudaError_t wide_dispatch(const rb::DTParams* P, const DTLayout& lay, int* occ, cudaStream_t s) {
+  switch (lay.rd) {
+    case 1: return rb::wide_call_rd1(lay.rc, P, lay.smem, lay.grid, occ, s);
+    case 2: return rb::wide_call_rd2(lay.rc, P, lay.smem, lay.grid, occ, s);
+    case 4: return rb::wide_call_rd4(lay.rc, P, lay.smem, lay.grid, occ, s);
+    case 9: return rb::wide_call_rd9(lay.rc, P, lay.smem, lay.grid, occ, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Layout of the wide (CTA-per-sample) family: Lambda^T, the cp.async ring, the
+// relaxations and small per-sample vectors in shared memory; two symbolic-state
+// buffers per CTA in global memory.
+int plan_wide(reach_ctx* ctx, const reach_net* net, int n, int m, int window, long long B, rb::DTParams& P,
+              DTLayout& lay, const reach_net* ctl) {
+  const int l = ctl ? ctl->dims[ctl->L] : 0;
+  const int cap = window > 0 ? window : 1;
+  const int n_i = n + l;
+  const int rd = wide_rows_pick(n), rc = l == 0 ? 0 : l <= 8 ? 1 : l <= 24 ? 3 : -1;
+  if (rd == 0 || rc < 0 || n > 128)
+    return fail(ctx, REACH_E_UNSUPPORTED, "state/control dims outside the wide kernel family (n <= 72, l <= 24)");
+  int hw = n_i;
+  auto widths = [&](const reach_net* nt) {
+    for (int i = 0; i + 1 < nt->L; ++i) hw = std::max(hw, nt->dims[i + 1]);
+  };
+  widths(net);
+  if (ctl) widths(ctl);
+  if (hw > rb::kWideSW) return fail(ctx, REACH_E_UNSUPPORTED, "layer width > 256 not in the wide kernel family");
+  const int lmax = std::max(net->L, ctl ? ctl->L : 0);
+  auto ev = [](long long x) { return (x + 1) & ~1ll; };
+  const int nop = std::max(8 * rd, 8 * rc) | 1;
+  long long off = static_cast<long long>(nop) * hw;
+  P.w_o_stage = static_cast<int>(ev(off));
+  off = P.w_o_stage + rb::kWideNS * rb::kWideRS * rb::kWideSW;
+  P.w_o_relax = static_cast<int>(off);
+  off += static_cast<long long>(std::max(lmax - 1, 1)) * hw * 4;
+  P.w_o_bf0 = static_cast<int>(off);
+  const int wmax = n + l;
+  const long long fold_need = static_cast<long long>(n) * (n + 2 * wmax) + 4 * n;
+  if (fold_need > P.w_o_bf0) return fail(ctx, REACH_E_UNSUPPORTED, "fold scratch exceeds shared memory");
+  off += hw;
+  P.w_o_misc = static_cast<int>(off);
+  const int nomax = std::max(n, l);
+  off += n + n_i + 2 * n + 3 * nomax + std::max(l, 1) + n + 32;
+  P.w_o_int = static_cast<int>(ev(off));
+  const size_t bytes = static_cast<size_t>(P.w_o_int) * 8 + 48 * 4 + static_cast<size_t>(std::max(lmax - 1, 1)) * 256;
+  if (bytes > static_cast<size_t>(ctx->max_smem))
+    return fail(ctx, REACH_E_UNSUPPORTED, "wide kernel working set exceeds shared memory");
+  P.w_nop = nop;
+  P.w_hw = hw;
+  P.w_rows = n + l;
+  P.w_lds = static_cast<int>(ev(n + static_cast<long long>(cap + 2) * wmax));
+  P.wws_stride = ev(2ll * P.w_rows * P.w_lds);
+  P.l = l;
+  if (ctl) P.ctl = ctl->dev;
+  lay.wide = true;
+  lay.rd = rd;
+  lay.rc = rc;
+  lay.smem = bytes;
+  int occ = 0;
+  cudaError_t e = wide_dispatch(nullptr, lay, &occ, nullptr);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "wide kernel setup");
+  if (occ < 1) return fail(ctx, REACH_E_UNSUPPORTED, "wide kernel does not fit on an SM");
+  lay.grid = static_cast<int>(std::min<long long>(B, static_cast<long long>(occ) * ctx->num_sms));
+  const size_t need = static_cast<size_t>(lay.grid) * P.wws_stride * 8;
+  if (need > ctx->wws_bytes) {
+    if (ctx->wws) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->wws);
+      ctx->wws = nullptr;
+      ctx->wws_bytes = 0;
+    }
+    RB_CUDA(cudaMalloc(&ctx->wws, need));
+    ctx->wws_bytes = need;
+  }
+  P.wws = static_cast<double*>(ctx->wws);
+  if (env_int("RB_WIDE_PHASE", 0, 0, 1)) {
+    if (!ctx->wphase) {
+      RB_CUDA(cudaMalloc(&ctx->wphase, 16 * sizeof(unsigned long long)));
+      RB_CUDA(cudaMemset(ctx->wphase, 0, 16 * sizeof(unsigned long long)));
+    }
+    P.w_phase = ctx->wphase;
+  }
+  return REACH_OK;
+}
+
+// Kernel family choice: the warp-per-sample kernel when the sample fits a
+// warp's shared-memory slice, else the wide CTA-per-sample kernel
+// (RB_FORCE_WIDE=1 forces the wide family, for parity runs of both).
+int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, long long B, rb::DTParams& P,
+            DTLayout& lay, const reach_net* ctl = nullptr) {
+  if (!env_int("RB_FORCE_WIDE", 0, 0, 1)) {
+    const int rc = plan_warp(ctx, net, n, m, window, P, lay, ctl);
+    if (rc != REACH_E_UNSUPPORTED) return rc;
+    const std::string why = ctx->err;
+    P = rb::DTParams{};
+    lay = DTLayout{};
+    const int rw = plan_wide(ctx, net, n, m, window, B, P, lay, ctl);
+    if (rw == REACH_E_UNSUPPORTED) ctx->err = why + "; " + ctx->err;
+    return rw;
+  }
+  return plan_wide(ctx, net, n, m, window, B, P, lay, ctl);
+}
+
 template <int NO, int CPL>
 cudaError_t launch_dt_t(const rb::DTParams& P, const DTLayout& lay, long long B, cudaStream_t s) {
   auto k = rb::dt_horizon_kernel<NO, CPL>;
@@ -263,6 +383,7 @@ cudaError_t launch_dt_no(const rb::DTParams& P, const DTLayout& lay, long long B
 }
 
 cudaError_t launch_dt(const rb::DTParams& P, const DTLayout& lay, long long B, cudaStream_t s) {
+  if (lay.wide) return wide_dispatch(&P, lay, nullptr, s);
   switch (lay.no) {
     case 2: return launch_dt_no<2>(P, lay, B, s);
     case 4: return launch_dt_no<4>(P, lay, B, s);
@@ -323,6 +444,8 @@ int reach_ctx_destroy(reach_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->pbuf) cudaFree(ctx->pbuf);
+  if (ctx->wws) cudaFree(ctx->wws);
+  if (ctx->wphase) cudaFree(ctx->wphase);
   for (auto& p : ctx->ev_used) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   for (auto& p : ctx->ev_free) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -401,6 +524,15 @@ int reach_measure_fp64_peak(reach_ctx* ctx, double* tflops_fma, double* tflops_m
 
 int reach_debug_phase_cycles(reach_ctx* ctx, uint64_t* out, int32_t count) {
   if (!ctx || !out || count <= 0) return REACH_E_INVALID_ARGUMENT;
+  if (ctx->wphase) {  // wide family, runtime-enabled counters
+    RB_CUDA(cudaSetDevice(ctx->device));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    unsigned long long tmp[16] = {0};
+    RB_CUDA(cudaMemcpy(tmp, ctx->wphase, sizeof(tmp), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < count && i < 16; ++i) out[i] = tmp[i];
+    RB_CUDA(cudaMemset(ctx->wphase, 0, sizeof(tmp)));
+    return REACH_OK;
+  }
 #ifdef RB_PHASE_TIMING
   RB_CUDA(cudaSetDevice(ctx->device));
   RB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -501,7 +633,7 @@ int run_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_net* ctl, con
   RB_CUDA(cudaSetDevice(ctx->device));
   rb::DTParams P{};
   DTLayout lay;
-  rc = plan_dt(ctx, net, a->n, a->m, a->window, P, lay, ctl);
+  rc = plan_dt(ctx, net, a->n, a->m, a->window, a->batch, P, lay, ctl);
   if (rc) return rc;
   P.net = net->dev;
   P.B = a->batch;
@@ -650,7 +782,7 @@ int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_arg
   RB_CUDA(cudaSetDevice(ctx->device));
   rb::DTParams P{};
   DTLayout lay;
-  rc = plan_dt(ctx, net, a->n, a->m, a->window, P, lay);
+  rc = plan_dt(ctx, net, a->n, a->m, a->window, end - begin, P, lay);
   if (rc) return rc;
   const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
   const int n = a->n, H = a->horizon, m = a->m;
@@ -821,7 +953,7 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
                      int* d_fs, int* d_st) {
   rb::DTParams P{};
   DTLayout lay;
-  int rc = plan_dt(ctx, net, p->n, p->m, p->window, P, lay);
+  int rc = plan_dt(ctx, net, p->n, p->m, p->window, batch, P, lay);
   if (rc) return rc;
   P.net = net->dev;
   P.B = batch;
@@ -853,6 +985,8 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
   if (need > ctx->pbuf_bytes) {
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
     if (ctx->pbuf) cudaFree(ctx->pbuf);
+  if (ctx->wws) cudaFree(ctx->wws);
+  if (ctx->wphase) cudaFree(ctx->wphase);
     ctx->pbuf = nullptr;
     RB_CUDA(cudaMalloc(&ctx->pbuf, need));
     ctx->pbuf_bytes = need;

@@ -171,3 +171,19 @@ def c1_closed_loop(seed: int = MASTER_SEED, batch: int = 1, horizon: int = 20) -
     ctl.layers[-1].w *= 0.3
     c = rng.uniform(-0.5, 0.5, size=(batch, n))
     return ClosedLoopWorkload(dyn, ctl, n, c - 0.05, c + 0.05, horizon)
+
+
+def c5_closed_loop(seed: int = MASTER_SEED, batch: int = 1024, horizon: int = 20) -> ClosedLoopWorkload:
+    """BASELINE configs[4]: 72-D closed loop (SURVEY §8 shape sheet C5): residual 3x256 ReLU
+    dynamics 90->256->256->256->72 (dt 0.02) and a 3x256 ReLU controller 72->...->18
+    (random_mlp scale 0.2, output x0.1); X0 = c0 +- 1e-3 with c0 ~ U(-0.2, 0.2)^72, H = 20.
+
+    The survey's C1 controller recipe (scale 0.6, output x0.3) makes the 3x256 loop's certified
+    width grow 1.7e26x over 20 steps (vacuous bounds); scale 0.2 / x0.1 grows 21x."""
+    rng = np.random.default_rng(seed + 5)
+    n, l = 72, 18
+    dyn = residual_relu_dynamics(rng, n, l, [256, 256, 256], dt=0.02)
+    ctl = random_mlp(rng, n, [256, 256, 256], l, Act.Relu, 0.2)
+    ctl.layers[-1].w *= 0.1
+    c = rng.uniform(-0.2, 0.2, size=(batch, n))
+    return ClosedLoopWorkload(dyn, ctl, n, c - 1e-3, c + 1e-3, horizon)

@@ -104,6 +104,18 @@ def cases():
     net = residual_relu_dynamics(rng, 8, 0, [256, 200], dt=0.05)
     lo, hi = _rand_boxes(rng, 10, 8, 0.3, 1e-3, 5e-3)
     out.append(("wide_n8", DTSystem(net, 8, 0), lo, hi, np.zeros((10, 12, 0)), DTReachParams(window=2), False))
+    # a hidden unit whose preactivation is exactly [0, 0] on a point box (W x + b = 1 - 0.5 - 0.5):
+    # relax_activation makes it stably ACTIVE (lo >= 0 branch first), so its Lambda column survives
+    rng = np.random.default_rng(19)
+    W0 = np.concatenate([np.array([[1.0, -1.0]]), rng.normal(0, 0.5, size=(4, 2))])
+    b0 = np.concatenate([[-0.5], rng.normal(0, 0.3, size=4)])
+    W1 = rng.normal(0, 0.5, size=(5, 5))
+    b1 = rng.normal(0, 0.3, size=5)
+    W2 = rng.normal(0, 0.3, size=(2, 5))
+    b2 = rng.normal(0, 0.1, size=2)
+    net = MLPNet([Layer(W0, b0, Act.Relu), Layer(W1, b1, Act.Relu), Layer(W2, b2, Act.Identity)])
+    out.append(("zero_preact_point", DTSystem(net, 2, 0), np.array([[1.0, 0.5]]), np.array([[1.0, 0.5]]),
+                np.zeros((1, 3, 0)), DTReachParams(), False))
     # n = 1, one hidden layer of 20
     rng = np.random.default_rng(17)
     net = random_mlp(rng, 2, [20], 1, Act.Relu, 0.8)
