@@ -54,6 +54,10 @@ enum reach_tube_status {
   REACH_TUBE_CTL_FAILED = 4,       /* "controller certification failed: relax_activation: non-finite preactivation"
                                       (closed_loop.hpp:106-109) */
   REACH_TUBE_CTL_DIVERGED = 5,     /* "controller certification diverged" (closed_loop.hpp:111-114) */
+  REACH_TUBE_REMAINDER = 6,        /* "remainder not contractive after max enlargements (reduce h)"
+                                      (flowpipe_ct.hpp:200-210) */
+  REACH_TUBE_PICARD_NONFINITE = 7, /* "poly_picard: non-finite coefficients" (flowpipe_ct.hpp:135) */
+  REACH_TUBE_TME_INV = 8,          /* "tme_inv: range contains zero" (taylor_model.hpp:367-368) */
   REACH_TUBE_OTHER = 99            /* any other reference exception text */
 };
 
@@ -253,6 +257,69 @@ int reach_cem_update(reach_cem* cem, const double* scores, const int32_t* ok);
 /* best actions [H][m], best objective, best_effort, history [iterations so far] */
 int reach_cem_result(const reach_cem* cem, double* best_actions, double* best_objective, int32_t* best_effort,
                      double* best_history);
+
+/* ----------------------------------------------------------------------- */
+/* Continuous-time closed loop under zero-order-hold neural feedback        */
+/* (cl_reach, closed_loop.hpp:76-182): controller certification at control  */
+/* boundaries (ctl_crown, neural.hpp:418-424) + stacking, then k_atomic     */
+/* validated Taylor-model flowpipe steps of the augmented (x, u) field       */
+/* (poly_picard / remainder_picard / symbolic_step, flowpipe_ct.hpp).        */
+/* The plant is an analytic system from systems.hpp, evaluated on the       */
+/* device; VectorField's host std::function closures cannot run there, so   */
+/* an unknown plant is REACH_E_UNSUPPORTED, never a CPU fallback.           */
+
+/* Analytic plants (systems.hpp), augmented with udot = 0 rows (fields.hpp:96-128). */
+enum reach_plant {
+  REACH_PLANT_QUADROTOR = 0 /* quadrotor_ode (systems.hpp:22-64): n = 12, l = 4;
+                               params = {mass, gravity, jx, jy, jz} (QuadrotorParams) */
+};
+
+/* FlowpipeParams (flowpipe_ct.hpp:35-50). `steps` is not used by cl_reach. */
+typedef struct reach_flowpipe_params {
+  double h;
+  int32_t steps;
+  int32_t order;            /* Picard truncation order k, 1 or 2 */
+  double eps_init;
+  int32_t refine_rounds;
+  double enlargement;
+  int32_t max_enlargements;
+  int32_t window;
+} reach_flowpipe_params;
+
+/* ClosedLoopSpec<double> (closed_loop.hpp:16-44) with an analytic plant. */
+typedef struct reach_cl_spec {
+  int32_t plant;            /* reach_plant */
+  double plant_params[8];
+  int32_t n, l;             /* state / control dims; the controller maps n + ref_dim -> l */
+  int32_t ctl_steps;        /* control intervals */
+  int32_t k_atomic;         /* flowpipe steps per control interval */
+  int32_t ref_dim;          /* 0: no reference input */
+  const double* y_ref;      /* [ctl_steps][ref_dim], host pointer */
+  reach_flowpipe_params fp;
+  int32_t intervalize_boundary;
+} reach_cl_spec;
+
+/* cl_reach for a batch of initial boxes.  Tubes have up to
+ * 1 + ctl_steps * k_atomic boxes of n + l dims: box 0 is the augmented
+ * initial set, box k >= 1 covers [(k-1) h, k h]; lo/hi are
+ * [batch][1 + ctl_steps*k_atomic][n + l]. */
+int reach_cl_batch(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* spec, int32_t batch,
+                   const double* x0_lo, const double* x0_hi, const reach_tube_out* out, int32_t flags);
+
+/* reach_with_splitting(cl_reach engine, x0, SplitPlan) (refine.hpp:121-160):
+ * the per-step hull over the sub-boxes [part_begin, part_end) of the grid
+ * split of X0 (n dims, e.g. SplitPlan::rpy, refine.hpp:51-61).  Hull boxes:
+ * [1 + ctl_steps*k_atomic][n + l].  X0 and counts are host pointers. */
+typedef struct reach_cl_split_args {
+  const double* x0_lo;   /* [n] */
+  const double* x0_hi;   /* [n] */
+  const int32_t* counts; /* [n] */
+  int64_t part_begin;
+  int64_t part_end;      /* <= 0 means "all parts" */
+} reach_cl_split_args;
+
+int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* spec,
+                        const reach_cl_split_args* args, const reach_hull_out* out, int32_t flags);
 
 #ifdef __cplusplus
 }

@@ -17,13 +17,11 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include "reach_b200.h"
+#include "oracle_int.h"
 
 /* std::min / std::max semantics (first argument wins ties, NaN-asymmetric). */
 static double smin(double a, double b) { return (b < a) ? b : a; }
 static double smax(double a, double b) { return (a < b) ? b : a; }
-
-typedef struct { double lo, hi; } iv;
 
 /* iv_add (interval.hpp:60) in nearest rounding. */
 static iv iv_add(iv a, iv b) { iv r = {a.lo + b.lo, a.hi + b.hi}; return r; }
@@ -35,17 +33,6 @@ static iv iv_scale(double a, iv x) {
   return r;
 }
 static int iv_finite(iv x) { return isfinite(x.lo) && isfinite(x.hi); }
-
-typedef struct {
-  int rows, cols, act;
-  const double* w; /* row-major rows x cols */
-  const double* b;
-} layer_t;
-
-typedef struct {
-  int n_layers;
-  layer_t* layers;
-} net_t;
 
 static net_t net_from_desc(const reach_net_desc* d) {
   net_t net;
@@ -912,4 +899,11 @@ int orc_dtcl_batch(const reach_net_desc* dyn_desc, const reach_net_desc* ctl_des
   }
   free(dyn.layers); free(ctl.layers);
   return REACH_OK;
+}
+
+/* Bridges for ct_oracle.c. */
+net_t orc_i_net_from_desc(const reach_net_desc* d) { return net_from_desc(d); }
+int orc_i_certify_tm_input(const net_t* net, int n_i, int nz, const double* c, const double* A, const iv* ig,
+                           double* out_c, double* out_A, iv* rem) {
+  return certify_tm_input(net, n_i, nz, c, A, ig, out_c, out_A, rem);
 }

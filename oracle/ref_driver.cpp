@@ -16,7 +16,9 @@
 #include <string>
 #include <vector>
 
+#include "reach/closed_loop.hpp"
 #include "reach/dt_reach.hpp"
+#include "reach/fields.hpp"
 #include "reach/mpc.hpp"
 #include "reach/neural.hpp"
 #include "reach/parallel.hpp"
@@ -439,6 +441,176 @@ int ref_plan_cem(const reach_net_desc* desc, const reach_plan_problem* p, const 
     *objective = res.objective;
     for (size_t i = 0; i < res.best_history.size(); ++i) best_history[i] = res.best_history[i];
     *best_effort = res.best_effort ? 1 : 0;
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Continuous-time closed loop (cl_reach, closed_loop.hpp:76-182) with the
+// quadrotor plant augmented by udot = 0 rows (make_augmented_field,
+// fields.hpp:96-128 -- exactly the CLI's `make_augmented("quadrotor")`,
+// reach_cli.cpp:125-131), and reach_with_splitting over it (refine.hpp:121-160).
+namespace {
+
+ClosedLoopSpec<double> cl_spec_from(const reach_net_desc* ctl_desc, const reach_cl_spec* sp) {
+  if (sp->plant != REACH_PLANT_QUADROTOR) throw std::invalid_argument("unknown plant");
+  QuadrotorParams prm;
+  prm.mass = sp->plant_params[0];
+  prm.gravity = sp->plant_params[1];
+  prm.jx = sp->plant_params[2];
+  prm.jy = sp->plant_params[3];
+  prm.jz = sp->plant_params[4];
+  ClosedLoopSpec<double> spec;
+  spec.n = sp->n;
+  spec.l = sp->l;
+  spec.ctl_steps = sp->ctl_steps;
+  spec.k_atomic = sp->k_atomic;
+  spec.controller = net_from_desc(ctl_desc);
+  auto plant = [prm](const auto& x, const auto& u, auto& dx) { quadrotor_ode(x, u, prm, dx); };
+  spec.dynamics = make_augmented_field<double>(sp->n, sp->l, plant);
+  for (int i = 0; sp->ref_dim > 0 && i < sp->ctl_steps; ++i)
+    spec.y_ref.emplace_back(sp->y_ref + static_cast<size_t>(i) * sp->ref_dim,
+                            sp->y_ref + static_cast<size_t>(i + 1) * sp->ref_dim);
+  spec.fp.h = sp->fp.h;
+  spec.fp.steps = sp->fp.steps;
+  spec.fp.order = sp->fp.order;
+  spec.fp.eps_init = sp->fp.eps_init;
+  spec.fp.refine_rounds = sp->fp.refine_rounds;
+  spec.fp.enlargement = sp->fp.enlargement;
+  spec.fp.max_enlargements = sp->fp.max_enlargements;
+  spec.fp.window = sp->fp.window;
+  spec.intervalize_boundary = sp->intervalize_boundary != 0;
+  return spec;
+}
+
+int32_t ct_status_of(const ReachTube<double>& t) {
+  if (!t.diverged && t.failed_step < 0) return REACH_TUBE_OK;
+  const std::string& r = t.failure_reason;
+  if (r == "remainder not contractive after max enlargements (reduce h)") return REACH_TUBE_REMAINDER;
+  if (r == "poly_picard: non-finite coefficients") return REACH_TUBE_PICARD_NONFINITE;
+  if (r == "tme_inv: range contains zero") return REACH_TUBE_TME_INV;
+  return cl_status_of(t);
+}
+
+void put_tube(const ReachTube<double>& t, int na, int T, double* lo, double* hi, int32_t* nb, int32_t* fs,
+              int32_t* st) {
+  for (int k = 0; k < t.steps() && k < T; ++k)
+    for (int d = 0; d < na; ++d) {
+      lo[static_cast<size_t>(k) * na + d] = t.boxes[static_cast<size_t>(k)][d].lo;
+      hi[static_cast<size_t>(k) * na + d] = t.boxes[static_cast<size_t>(k)][d].hi;
+    }
+  *nb = t.steps();
+  *fs = t.failed_step;
+  *st = ct_status_of(t);
+}
+
+}  // namespace
+
+extern "C" {
+
+// cl_reach per initial box (parallel_for over the batch, like dt_reach_batch).
+int ref_cl_batch(const reach_net_desc* ctl_desc, const reach_cl_spec* sp, int32_t batch, const double* x0_lo,
+                 const double* x0_hi, const reach_tube_out* out, int32_t threads) {
+  try {
+    ClosedLoopSpec<double> spec = cl_spec_from(ctl_desc, sp);
+    const int n = sp->n, na = sp->n + sp->l, T = 1 + sp->ctl_steps * sp->k_atomic;
+    parallel_for(
+        batch,
+        [&](int b) {
+          ReachTube<double> t;
+          try {
+            t = cl_reach(spec, box_at(x0_lo + static_cast<size_t>(b) * n, x0_hi + static_cast<size_t>(b) * n, n));
+          } catch (const std::exception& e) {
+            t = ReachTube<double>();
+            t.mark_failed(0, e.what());
+          }
+          put_tube(t, na, T, out->lo + static_cast<size_t>(b) * T * na, out->hi + static_cast<size_t>(b) * T * na,
+                   out->n_boxes + b, out->failed_step + b, out->status + b);
+        },
+        threads);
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+
+// reach_with_splitting(cl_reach, x0, plan).  Full range and threads == 0: the
+// reference driver verbatim; otherwise the same pieces on parts [begin, end).
+int ref_cl_split_hull(const reach_net_desc* ctl_desc, const reach_cl_spec* sp, const reach_cl_split_args* a,
+                      const reach_hull_out* out, int32_t threads) {
+  try {
+    ClosedLoopSpec<double> spec = cl_spec_from(ctl_desc, sp);
+    const int n = sp->n, na = sp->n + sp->l;
+    Box x0 = box_at(a->x0_lo, a->x0_hi, n);
+    SplitPlan plan;
+    plan.counts.assign(a->counts, a->counts + n);
+    const long long total = plan.total_parts();
+    long long begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
+    if (begin < 0 || begin >= end || end > total) return REACH_E_INVALID_ARGUMENT;
+    auto engine = [&](const Box& b) { return cl_reach(spec, b); };
+    if (begin == 0 && end == total && threads == 0) {
+      ReachTube<double> hull = reach_with_splitting(engine, x0, plan);
+      for (int k = 0; k < hull.steps(); ++k) {
+        for (int d = 0; d < na; ++d) {
+          out->lo[static_cast<size_t>(k) * na + d] = hull.boxes[static_cast<size_t>(k)][d].lo;
+          out->hi[static_cast<size_t>(k) * na + d] = hull.boxes[static_cast<size_t>(k)][d].hi;
+        }
+        out->box_diverged[k] = hull.boxes[static_cast<size_t>(k)].diverged ? 1 : 0;
+      }
+      out->n_boxes[0] = hull.steps();
+      // the reference reports (failed_step, "sub-box i: reason"); rebuild the key
+      int64_t key = std::numeric_limits<int64_t>::max();
+      if (hull.diverged) {
+        size_t colon = hull.failure_reason.find(':');
+        long long part = std::stoll(hull.failure_reason.substr(7, colon - 7));
+        ReachTube<double> t;
+        t.mark_failed(hull.failed_step, hull.failure_reason.substr(colon + 2));
+        key = (static_cast<int64_t>(hull.failed_step) << 40) | (static_cast<int64_t>(part) << 8) |
+              static_cast<int64_t>(ct_status_of(t) & 0xff);
+      }
+      out->fail_key[0] = key;
+      return REACH_OK;
+    }
+    auto parts = split_box(x0, plan);
+    const int count = static_cast<int>(end - begin);
+    std::vector<ReachTube<double>> subs(static_cast<size_t>(count));
+    parallel_for(
+        count,
+        [&](int i) {
+          try {
+            subs[static_cast<size_t>(i)] = engine(parts[static_cast<size_t>(begin + i)]);
+          } catch (const std::exception& e) {
+            subs[static_cast<size_t>(i)].mark_failed(0, e.what());
+          }
+        },
+        threads);
+    int steps = subs.front().steps();
+    int64_t key = std::numeric_limits<int64_t>::max();
+    for (int i = 0; i < count; ++i) {
+      const auto& s = subs[static_cast<size_t>(i)];
+      steps = std::min(steps, s.steps());
+      if (s.diverged) {
+        int fs = s.failed_step >= 0 ? s.failed_step : s.steps();
+        int64_t k = (static_cast<int64_t>(fs) << 40) | (static_cast<int64_t>(begin + i) << 8) |
+                    static_cast<int64_t>(ct_status_of(s) & 0xff);
+        key = std::min(key, k);
+      }
+    }
+    for (int k = 0; k < steps; ++k) {
+      Box b = subs.front().boxes[static_cast<size_t>(k)];
+      for (int i = 1; i < count; ++i) b = box_hull(b, subs[static_cast<size_t>(i)].boxes[static_cast<size_t>(k)]);
+      for (int d = 0; d < na; ++d) {
+        out->lo[static_cast<size_t>(k) * na + d] = b[d].lo;
+        out->hi[static_cast<size_t>(k) * na + d] = b[d].hi;
+      }
+      out->box_diverged[k] = b.diverged ? 1 : 0;
+    }
+    out->n_boxes[0] = steps;
+    out->fail_key[0] = key;
   } catch (const std::exception&) {
     return REACH_E_INVALID_ARGUMENT;
   }

@@ -27,6 +27,9 @@ TUBE_DIVERGED_CERT = 2
 TUBE_DIVERGED_BOX = 3
 TUBE_CTL_FAILED = 4
 TUBE_CTL_DIVERGED = 5
+TUBE_REMAINDER = 6
+TUBE_PICARD_NONFINITE = 7
+TUBE_TME_INV = 8
 TUBE_OTHER = 99
 TUBE_REASON = {
     TUBE_OK: "",
@@ -35,6 +38,9 @@ TUBE_REASON = {
     TUBE_DIVERGED_BOX: "diverged box",
     TUBE_CTL_FAILED: "controller certification failed: relax_activation: non-finite preactivation",
     TUBE_CTL_DIVERGED: "controller certification diverged",
+    TUBE_REMAINDER: "remainder not contractive after max enlargements (reduce h)",
+    TUBE_PICARD_NONFINITE: "poly_picard: non-finite coefficients",
+    TUBE_TME_INV: "tme_inv: range contains zero",
     TUBE_OTHER: "error",
 }
 
@@ -136,3 +142,27 @@ class SamplerConfigC(C.Structure):
         ("population", C.c_int32), ("elite_frac", C.c_double), ("iterations", C.c_int32),
         ("init_std", C.c_double), ("smoothing", C.c_double), ("refine_iters", C.c_int32), ("seed", C.c_uint64),
     ]
+
+
+# --- continuous-time closed loop (closed_loop.hpp) -----------------------------
+PLANT_QUADROTOR = 0
+
+
+class FlowpipeParamsC(C.Structure):
+    _fields_ = [
+        ("h", C.c_double), ("steps", C.c_int32), ("order", C.c_int32), ("eps_init", C.c_double),
+        ("refine_rounds", C.c_int32), ("enlargement", C.c_double), ("max_enlargements", C.c_int32),
+        ("window", C.c_int32),
+    ]
+
+
+class CLSpecC(C.Structure):
+    _fields_ = [
+        ("plant", C.c_int32), ("plant_params", C.c_double * 8), ("n", C.c_int32), ("l", C.c_int32),
+        ("ctl_steps", C.c_int32), ("k_atomic", C.c_int32), ("ref_dim", C.c_int32), ("y_ref", _dp),
+        ("fp", FlowpipeParamsC), ("intervalize_boundary", C.c_int32),
+    ]
+
+
+class CLSplitArgs(C.Structure):
+    _fields_ = [("x0_lo", _dp), ("x0_hi", _dp), ("counts", _ip), ("part_begin", C.c_int64), ("part_end", C.c_int64)]

@@ -11,6 +11,9 @@ templates for the DT reachability path:
     reach_with_splitting            refine.hpp:121-160  (engine = dt_reach)
     ReachTube, tube_volume          tube.hpp:12-46
     box_from_center, box_volume_proxy  interval.hpp:224-258
+    QuadrotorParams                 systems.hpp:16-20
+    FlowpipeParams                  flowpipe_ct.hpp:35-50
+    ClosedLoopSpec, cl_reach        closed_loop.hpp:16-182  (plant = quadrotor_ode, fields.hpp:96-128)
 
 Every compute call runs the CUDA kernels through the C ABI
 (include/reach_b200.h); there is no CPU path.  Shape errors raise
@@ -168,22 +171,31 @@ def box_from_center(center, radius):
 # ---------------------------------------------------------------------------
 @dataclass
 class TubeBatch:
-    """Batch output of dt_reach_batch in array form (the device layout)."""
+    """Batch output of dt_reach_batch / cl_reach in array form (the device layout)."""
     lo: np.ndarray  # [B][H+1][n]
     hi: np.ndarray
     n_boxes: np.ndarray
     failed_step: np.ndarray
     status: np.ndarray
+    h: float = 0.0  # > 0: continuous-time tube, box k >= 1 covers [(k-1)h, kh] (closed_loop.hpp:172)
 
     def tube(self, b: int) -> ReachTube:
         k = int(self.n_boxes[b])
         st = int(self.status[b])
-        t = np.arange(k, dtype=np.float64)
-        return ReachTube(self.lo[b, :k].copy(), self.hi[b, :k].copy(), t, t.copy(), diverged=st != A.TUBE_OK,
+        t_lo, t_hi = _tube_times(k, self.h)
+        return ReachTube(self.lo[b, :k].copy(), self.hi[b, :k].copy(), t_lo, t_hi, diverged=st != A.TUBE_OK,
                          failed_step=int(self.failed_step[b]), failure_reason=A.TUBE_REASON.get(st, "error"))
 
     def tubes(self) -> List[ReachTube]:
         return [self.tube(b) for b in range(self.lo.shape[0])]
+
+
+def _tube_times(k: int, h: float):
+    if h <= 0.0:
+        t = np.arange(k, dtype=np.float64)
+        return t, t.copy()
+    j = np.arange(k, dtype=np.float64)
+    return np.where(j > 0, (j - 1) * h, 0.0), j * h
 
 
 def _actions_array(seqs, B, H, m) -> np.ndarray:
@@ -319,11 +331,12 @@ class HullResult:
     box_diverged: np.ndarray
     n_boxes: int
     fail_key: int
+    h: float = 0.0  # > 0: continuous-time hull (cl_reach engine)
 
     def tube(self) -> ReachTube:
         k = self.n_boxes
-        t = np.arange(k, dtype=np.float64)
-        tube = ReachTube(self.lo[:k].copy(), self.hi[:k].copy(), t, t.copy())
+        t_lo, t_hi = _tube_times(k, self.h)
+        tube = ReachTube(self.lo[:k].copy(), self.hi[:k].copy(), t_lo, t_hi)
         f = A.decode_fail_key(self.fail_key)
         tube.diverged = bool(np.any(self.box_diverged[:k])) or f is not None
         if f is not None:
@@ -389,3 +402,148 @@ def dt_closed_loop_batch(dyn: MLPNet, ctl: MLPNet, n: int, x0_lo: np.ndarray, x0
     hd, hc = ctx.upload(dyn), ctx.upload(ctl)
     ctx.check(ctx._lib.reach_dtcl_batch(ctx.handle, hd, hc, C.byref(args), C.byref(to), 0), "dt closed loop")
     return out
+
+
+# ---------------------------------------------------------------------------
+# Continuous-time closed loop (closed_loop.hpp:16-182) with an analytic plant.
+@dataclass
+class QuadrotorParams:
+    """QuadrotorParams (systems.hpp:16-20)."""
+    mass: float = 1.0
+    gravity: float = 9.81
+    jx: float = 0.01
+    jy: float = 0.01
+    jz: float = 0.02
+
+    def as_array(self):
+        return [self.mass, self.gravity, self.jx, self.jy, self.jz]
+
+
+@dataclass
+class FlowpipeParams:
+    """FlowpipeParams (flowpipe_ct.hpp:35-50)."""
+    h: float = 0.01
+    steps: int = 100
+    order: int = 2
+    eps_init: float = 1e-4
+    refine_rounds: int = 3
+    enlargement: float = 2.0
+    max_enlargements: int = 20
+    window: int = 4
+
+    def validate(self):
+        if (self.h <= 0 or self.steps <= 0 or self.order < 1 or self.order > 2 or self.eps_init <= 0
+                or self.enlargement <= 1.0 or self.refine_rounds < 0 or self.max_enlargements < 0 or self.window < 0):
+            raise ValueError("FlowpipeParams: invalid configuration")
+
+    def c_struct(self):
+        return A.FlowpipeParamsC(self.h, self.steps, self.order, self.eps_init, self.refine_rounds, self.enlargement,
+                                 self.max_enlargements, self.window)
+
+
+@dataclass(eq=False)
+class ClosedLoopSpec:
+    """ClosedLoopSpec<double> (closed_loop.hpp:16-44).  The dynamics are an analytic plant
+    augmented with udot = 0 rows (make_augmented_field, fields.hpp:96-128); only
+    quadrotor_ode (systems.hpp:22-64, n = 12, l = 4) runs on the device."""
+    controller: MLPNet
+    n: int = 12
+    l: int = 4
+    ctl_steps: int = 1
+    k_atomic: int = 1
+    y_ref: Optional[np.ndarray] = None  # [ctl_steps][ref_dim]
+    fp: FlowpipeParams = field(default_factory=FlowpipeParams)
+    intervalize_boundary: bool = False
+    plant: str = "quadrotor"
+    plant_params: QuadrotorParams = field(default_factory=QuadrotorParams)
+
+    def steps(self) -> int:
+        return 1 + self.ctl_steps * self.k_atomic
+
+    def validate(self):
+        """ClosedLoopSpec::validate (closed_loop.hpp:30-43)."""
+        self.fp.validate()
+        if self.n <= 0 or self.l <= 0 or self.ctl_steps <= 0 or self.k_atomic <= 0:
+            raise ValueError("ClosedLoopSpec: invalid dimensions")
+        if self.plant != "quadrotor" or self.n != 12 or self.l != 4:
+            raise ValueError("ClosedLoopSpec: dynamics must act on the augmented (x,u) state")
+        self.controller.validate()
+        if self.controller.output_dim() != self.l:
+            raise ValueError("ClosedLoopSpec: controller output dim mismatch")
+        yr = self._yref()
+        ref_dim = 0 if yr is None else yr.shape[1]
+        if self.controller.input_dim() != self.n + ref_dim:
+            raise ValueError("ClosedLoopSpec: controller input dim mismatch")
+        if yr is not None and yr.shape[0] != self.ctl_steps:
+            raise ValueError("ClosedLoopSpec: reference sequence length mismatch")
+
+    def _yref(self):
+        if self.y_ref is None or len(self.y_ref) == 0:
+            return None
+        return np.ascontiguousarray(np.asarray(self.y_ref, np.float64).reshape(len(self.y_ref), -1))
+
+    def c_struct(self):
+        """(reach_cl_spec, keepalive)."""
+        yr = self._yref()
+        prm = (C.c_double * 8)(*(self.plant_params.as_array() + [0.0] * 3))
+        s = A.CLSpecC(A.PLANT_QUADROTOR, prm, self.n, self.l, self.ctl_steps, self.k_atomic,
+                      0 if yr is None else yr.shape[1], A.dptr(yr), self.fp.c_struct(), int(self.intervalize_boundary))
+        return s, (yr, prm)
+
+
+def cl_reach_batch_arrays(spec: ClosedLoopSpec, x0_lo: np.ndarray, x0_hi: np.ndarray,
+                          ctx: Optional[Context] = None) -> TubeBatch:
+    """cl_reach (closed_loop.hpp:76-182) for a batch of initial boxes x0 [B][n]; boxes have n + l dims."""
+    spec.validate()
+    ctx = ctx or default_context()
+    x0_lo = np.ascontiguousarray(x0_lo, dtype=np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, dtype=np.float64)
+    B = x0_lo.shape[0]
+    if x0_lo.shape != (B, spec.n) or x0_hi.shape != (B, spec.n):
+        raise ValueError("cl_reach: X0 dimension mismatch")
+    T, na = spec.steps(), spec.n + spec.l
+    out = TubeBatch(np.full((B, T, na), np.nan), np.full((B, T, na), np.nan), np.zeros(B, np.int32),
+                    np.zeros(B, np.int32), np.zeros(B, np.int32), h=spec.fp.h)
+    cs, keep = spec.c_struct()
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step),
+                   A.iptr(out.status))
+    net = ctx.upload(spec.controller)
+    ctx.check(ctx._lib.reach_cl_batch(ctx.handle, net, C.byref(cs), B, A.dptr(x0_lo), A.dptr(x0_hi), C.byref(to), 0),
+              "cl_reach")
+    return out
+
+
+def cl_reach(spec: ClosedLoopSpec, x0, ctx: Optional[Context] = None) -> ReachTube:
+    """cl_reach (closed_loop.hpp:76-77): x0 = (lo, hi)."""
+    lo = np.asarray(x0[0], np.float64).reshape(1, -1)
+    hi = np.asarray(x0[1], np.float64).reshape(1, -1)
+    return cl_reach_batch_arrays(spec, lo, hi, ctx).tube(0)
+
+
+def cl_split_hull(spec: ClosedLoopSpec, x0, plan: SplitPlan, part_begin: int = 0, part_end: int = 0,
+                  ctx: Optional[Context] = None) -> HullResult:
+    """Hull over sub-boxes [part_begin, part_end) of reach_with_splitting(cl_reach) (C ABI reach_cl_split_hull)."""
+    spec.validate()
+    ctx = ctx or default_context()
+    lo0 = np.ascontiguousarray(x0[0], dtype=np.float64)
+    hi0 = np.ascontiguousarray(x0[1], dtype=np.float64)
+    plan.validate(spec.n)
+    counts = np.array(plan.counts, dtype=np.int32)
+    T, na = spec.steps(), spec.n + spec.l
+    out = HullResult(np.full((T, na), np.nan), np.full((T, na), np.nan), np.zeros(T, np.int32), 0, 0, h=spec.fp.h)
+    nb = np.zeros(1, np.int32)
+    key = np.zeros(1, np.int64)
+    cs, keep = spec.c_struct()
+    args = A.CLSplitArgs(A.dptr(lo0), A.dptr(hi0), A.iptr(counts), int(part_begin), int(part_end))
+    ho = A.HullOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.box_diverged), A.iptr(nb), A.lptr(key))
+    net = ctx.upload(spec.controller)
+    ctx.check(ctx._lib.reach_cl_split_hull(ctx.handle, net, C.byref(cs), C.byref(args), C.byref(ho), 0),
+              "reach_with_splitting(cl_reach)")
+    out.n_boxes = int(nb[0])
+    out.fail_key = int(key[0])
+    return out
+
+
+def cl_reach_with_splitting(spec: ClosedLoopSpec, x0, plan: SplitPlan, ctx: Optional[Context] = None) -> ReachTube:
+    """reach_with_splitting(cl_reach engine, x0, plan) (refine.hpp:121-160)."""
+    return cl_split_hull(spec, x0, plan, ctx=ctx).tube()

@@ -414,6 +414,9 @@ const char* reach_tube_status_string(int32_t status) {
     case REACH_TUBE_DIVERGED_BOX: return "diverged box";
     case REACH_TUBE_CTL_FAILED: return "controller certification failed: relax_activation: non-finite preactivation";
     case REACH_TUBE_CTL_DIVERGED: return "controller certification diverged";
+    case REACH_TUBE_REMAINDER: return "remainder not contractive after max enlargements (reduce h)";
+    case REACH_TUBE_PICARD_NONFINITE: return "poly_picard: non-finite coefficients";
+    case REACH_TUBE_TME_INV: return "tme_inv: range contains zero";
     default: return "error";
   }
 }

@@ -187,3 +187,35 @@ def c5_closed_loop(seed: int = MASTER_SEED, batch: int = 1024, horizon: int = 20
     ctl.layers[-1].w *= 0.1
     c = rng.uniform(-0.2, 0.2, size=(batch, n))
     return ClosedLoopWorkload(dyn, ctl, n, c - 1e-3, c + 1e-3, horizon)
+
+
+@dataclass
+class CTWorkload:
+    spec: "ClosedLoopSpec"
+    x0_lo: np.ndarray  # [n]
+    x0_hi: np.ndarray
+    plan: SplitPlan
+
+
+def quadrotor_controller(rng: np.random.Generator, hidden=(64, 64, 64), scale: float = 0.4, out_scale: float = 0.1,
+                         mass: float = 1.0, gravity: float = 9.81) -> MLPNet:
+    """Velocity-command tanh controller of test_closed_loop.cpp:236-241 with the C2 widths:
+    random_mlp(15 -> hidden -> 4, Tanh, scale), output layer x out_scale, thrust bias + m g."""
+    ctl = random_mlp(rng, 15, list(hidden), 4, Act.Tanh, scale)
+    ctl.layers[-1].w *= out_scale
+    ctl.layers[-1].b[0] += mass * gravity
+    return ctl
+
+
+def c2_quadrotor(seed: int = MASTER_SEED, parts: int = 4096, ctl_steps: int = 10, k_atomic: int = 5,
+                 hidden=(64, 64, 64)) -> CTWorkload:
+    """BASELINE configs[1]: 12-D quadrotor (quadrotor_ode) under a 3x64 tanh NN controller (15 -> 4,
+    y_ref = (0.1, 0, 0)), order-2 Taylor-model flowpipe, h = 0.01, 10 control intervals x 5 atomic
+    steps = 50 steps; X0 = +-0.05 on dims 0-5, +-0.02 on dims 6-11, split rpy:parts."""
+    from .api import ClosedLoopSpec, FlowpipeParams
+    rng = np.random.default_rng(seed + 2)
+    ctl = quadrotor_controller(rng, hidden)
+    spec = ClosedLoopSpec(controller=ctl, n=12, l=4, ctl_steps=ctl_steps, k_atomic=k_atomic,
+                          y_ref=np.tile([0.1, 0.0, 0.0], (ctl_steps, 1)), fp=FlowpipeParams(h=0.01, order=2))
+    r = np.array([0.05] * 6 + [0.02] * 6)
+    return CTWorkload(spec, -r, r.copy(), SplitPlan.rpy(12, parts))

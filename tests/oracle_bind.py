@@ -224,3 +224,66 @@ def oracle_dtcl_batch(dyn, ctl, n, x0_lo, x0_hi, horizon, prm=DTReachParams()):
 
 def ref_dtcl_batch(dyn, ctl, n, x0_lo, x0_hi, horizon, prm=DTReachParams(), threads=0):
     return _dtcl(ref_lib(), "ref_", dyn, ctl, n, x0_lo, x0_hi, horizon, prm, threads)
+
+
+# --- continuous-time closed loop (cl_reach) ----------------------------------
+def _cl(lib, prefix, spec, x0_lo, x0_hi, threads=None):
+    from paper_2605_25346_b200.api import TubeBatch as TB
+    args_t = [C.POINTER(A.NetDesc), C.POINTER(A.CLSpecC), C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+              C.POINTER(A.TubeOut)]
+    if prefix == "ref_":
+        args_t.append(C.c_int32)
+    f = _mpc_fn(lib, prefix + "cl_batch", args_t)
+    x0_lo = np.ascontiguousarray(x0_lo, np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, np.float64)
+    B = x0_lo.shape[0]
+    T, na = spec.steps(), spec.n + spec.l
+    out = TB(np.full((B, T, na), np.nan), np.full((B, T, na), np.nan), np.zeros(B, np.int32),
+             np.zeros(B, np.int32), np.zeros(B, np.int32), h=spec.fp.h)
+    cd, k1 = spec.controller.desc()
+    cs, k2 = spec.c_struct()
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step), A.iptr(out.status))
+    extra = [threads or 0] if prefix == "ref_" else []
+    rc = f(C.byref(cd), C.byref(cs), B, A.dptr(x0_lo), A.dptr(x0_hi), C.byref(to), *extra)
+    assert rc == 0, rc
+    return out
+
+
+def oracle_cl_batch(spec, x0_lo, x0_hi):
+    return _cl(oracle_lib(), "orc_", spec, x0_lo, x0_hi)
+
+
+def ref_cl_batch(spec, x0_lo, x0_hi, threads=0):
+    return _cl(ref_lib(), "ref_", spec, x0_lo, x0_hi, threads)
+
+
+def _cl_hull(lib, prefix, spec, x0_lo, x0_hi, plan, begin=0, end=0, threads=None):
+    args_t = [C.POINTER(A.NetDesc), C.POINTER(A.CLSpecC), C.POINTER(A.CLSplitArgs), C.POINTER(A.HullOut)]
+    if prefix == "ref_":
+        args_t.append(C.c_int32)
+    f = _mpc_fn(lib, prefix + "cl_split_hull", args_t)
+    T, na = spec.steps(), spec.n + spec.l
+    lo0 = np.ascontiguousarray(x0_lo, np.float64)
+    hi0 = np.ascontiguousarray(x0_hi, np.float64)
+    counts = np.array(plan.counts, np.int32)
+    out = HullResult(np.full((T, na), np.nan), np.full((T, na), np.nan), np.zeros(T, np.int32), 0, 0, h=spec.fp.h)
+    nb = np.zeros(1, np.int32)
+    key = np.zeros(1, np.int64)
+    cd, k1 = spec.controller.desc()
+    cs, k2 = spec.c_struct()
+    args = A.CLSplitArgs(A.dptr(lo0), A.dptr(hi0), A.iptr(counts), int(begin), int(end))
+    ho = A.HullOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.box_diverged), A.iptr(nb), A.lptr(key))
+    extra = [threads if threads is not None else 0] if prefix == "ref_" else []
+    rc = f(C.byref(cd), C.byref(cs), C.byref(args), C.byref(ho), *extra)
+    assert rc == 0, rc
+    out.n_boxes = int(nb[0])
+    out.fail_key = int(key[0])
+    return out
+
+
+def oracle_cl_split_hull(spec, x0_lo, x0_hi, plan, begin=0, end=0):
+    return _cl_hull(oracle_lib(), "orc_", spec, x0_lo, x0_hi, plan, begin, end)
+
+
+def ref_cl_split_hull(spec, x0_lo, x0_hi, plan, begin=0, end=0, threads=0):
+    return _cl_hull(ref_lib(), "ref_", spec, x0_lo, x0_hi, plan, begin, end, threads)
