@@ -1,0 +1,103 @@
+// Host-side internals shared by the library's translation units (reach_capi.cu:
+// DT / MPC entry points, ct_capi.cu: continuous-time closed loop).  Not part of
+// the ABI: include/reach_b200.h exposes these types as opaque handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/reach_b200.h"
+#include "dt_kernel.cuh"
+
+struct reach_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int num_sms = 0;
+  int max_smem = 0;
+  // growable device workspace for host-pointer calls
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // plan-problem staging buffer (goal, weights, constraints) for the MPC kernels
+  void* pbuf = nullptr;
+  size_t pbuf_bytes = 0;
+  // per-CTA symbolic-state buffers of the wide kernel family
+  void* wws = nullptr;
+  size_t wws_bytes = 0;
+  unsigned long long* wphase = nullptr;  // wide-kernel phase counters (RB_WIDE_PHASE=1)
+  // kernel timing
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
+};
+
+struct reach_net {
+  rb::DevNet dev{};
+  double* blob = nullptr;
+  int L = 0;
+  int cpl = 0;  // hidden units per lane of the kernel family (0 = unsupported width)
+  int hp = 0;   // padded hidden width 32 * cpl
+  std::vector<int> dims, acts;
+};
+
+namespace rbh {
+
+inline int fail(reach_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+inline int cuda_fail(reach_ctx* ctx, cudaError_t e, const char* where) {
+  return fail(ctx, e == cudaErrorMemoryAllocation ? REACH_E_OOM : REACH_E_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define RB_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline int ensure_ws(reach_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->ws_bytes) return REACH_OK;
+  if (ctx->ws) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+  }
+  RB_CUDA(cudaMalloc(&ctx->ws, bytes));
+  ctx->ws_bytes = bytes;
+  return REACH_OK;
+}
+
+inline int timed_begin(reach_ctx* ctx, cudaEvent_t* stop) {
+  *stop = nullptr;
+  if (!ctx->timing) return REACH_OK;
+  std::pair<cudaEvent_t, cudaEvent_t> p;
+  if (!ctx->ev_free.empty()) {
+    p = ctx->ev_free.back();
+    ctx->ev_free.pop_back();
+  } else {
+    RB_CUDA(cudaEventCreate(&p.first));
+    RB_CUDA(cudaEventCreate(&p.second));
+  }
+  RB_CUDA(cudaEventRecord(p.first, ctx->stream));
+  ctx->ev_used.push_back(p);
+  *stop = p.second;
+  return REACH_OK;
+}
+
+inline int timed_end(reach_ctx* ctx, cudaEvent_t stop) {
+  if (stop) RB_CUDA(cudaEventRecord(stop, ctx->stream));
+  return REACH_OK;
+}
+
+}  // namespace rbh
