@@ -192,7 +192,11 @@ static void tme_integrate(tme* r, const tme* u) {
 /* systems.hpp:24-64).  x: 16 rows; dx: 16 rows.  prm: mass, g, jx, jy, jz. */
 typedef struct { tme t[12]; } qscratch;
 
+/* Field evaluations so far (work accounting for the roofline, not part of the algorithm). */
+long long orc_ct_field_evals = 0;
+
 static void quad_field(const tme* x, tme* dx, const double* prm, qscratch* s, int* thrown) {
+  ++orc_ct_field_evals;
   const double mass = prm[0], grav = prm[1], jx = prm[2], jy = prm[3], jz = prm[4];
   const int nz = x[0].nz;
   const double h = x[0].h;

@@ -87,6 +87,17 @@ int setup_params(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s, l
   P.eps = s->fp.eps_init;
   P.enl = s->fp.enlargement;
   for (int i = 0; i < 8; ++i) P.prm[i] = s->plant_params[i];
+  // quadrotor_ode's constants, computed as the reference does (systems.hpp:48-63)
+  const double mass = s->plant_params[0], grav = s->plant_params[1], jx = s->plant_params[2],
+               jy = s->plant_params[3], jz = s->plant_params[4];
+  P.kc[0] = 1.0 / mass;
+  P.kc[1] = grav;
+  P.kc[2] = (jy - jz) / jx;
+  P.kc[3] = 1.0 / jx;
+  P.kc[4] = (jz - jx) / jy;
+  P.kc[5] = 1.0 / jy;
+  P.kc[6] = (jx - jy) / jz;
+  P.kc[7] = 1.0 / jz;
   P.ctl = ctl->dev;
   P.T = 1 + s->ctl_steps * s->k_atomic;
   (void)ctx;

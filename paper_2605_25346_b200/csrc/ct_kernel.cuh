@@ -17,13 +17,17 @@
 // between the two launches; inside a launch it lives in shared memory.
 //
 // TMExpr rows (taylor_model.hpp:197-238) are lane-strided in shared memory:
-// lane L owns generator columns L, L+32, L+64 of az and bz, so every TMExpr
-// operation (products with excess folding, reciprocal, sin / cos,
-// integration) is a per-lane FP64 update of three coefficient slots plus
-// warp-uniform scalar interval arithmetic; the abs-sums the remainder bounds
-// need (abs_z / abs_b) are butterfly shuffle reductions, computed once when a
-// row is produced and cached next to it.  Lanes only ever touch their own
-// coefficient slots, so the algebra needs no warp barriers.
+// lane L owns generator columns L, L+32 (, L+64) of az and bz, so every
+// TMExpr operation (products with excess folding, integration) is a per-lane
+// FP64 update of <= 3 coefficient slots plus warp-uniform scalar interval
+// arithmetic; the abs-sums the remainder bounds need (abs_z / abs_b) are
+// butterfly shuffle reductions, computed once when a row is produced and
+// cached next to it.  Lanes only ever touch their own coefficient slots, so
+// the algebra needs no warp barriers.  sin / cos / reciprocal / scalar
+// products are scalar multiples of their operand's coefficients and stay
+// "views" (no storage, no coefficient pass).  The field itself is a short
+// program (kQuadTape) run by one interpreter loop, which keeps the kernel's
+// code inside the instruction cache.
 //
 // Numerics: the reference's operation order inside every TMExpr operation;
 // the abs-sums are tree reductions (the reference sums sequentially) and libm
@@ -43,10 +47,8 @@ namespace ct {
 
 constexpr int NX = 12;      // quadrotor state
 constexpr int NA = 16;      // augmented (x, u)
-constexpr int NZC = 3;      // generator slots per lane
-constexpr int NZP = 32 * NZC;  // generator columns per row (nz <= 96)
-constexpr int NT = 10;      // temporary rows of one field evaluation
-constexpr int LDS = NZP + 1;   // state row stride in shared memory (odd: conflict-free row sweeps)
+constexpr int NZC = 3;      // generator slots per lane (lanes >= 16 use two)
+constexpr int NZP = 80;     // generator columns per row: n + window (n + l) <= 76 (window <= 4)
 constexpr int kMaxCtlW = 128;  // widest controller layer (and input dim)
 constexpr int LDX = NZP + 1;
 
@@ -58,6 +60,7 @@ struct CTParams {
   int B, n, l, K, window, order, refine, maxe, intervalize, ref_dim, ci, ctl_steps;
   double h, eps, enl;
   double prm[8];
+  double kc[8];  // plant constants of the field program (kQuadTape)
   DevNet ctl;
   const double* y_ref;  // device [ctl_steps][ref_dim]
   // initial boxes: batch (x0_lo/hi [B][n]) or split of one box
@@ -118,15 +121,42 @@ __device__ __forceinline__ double wsum(double a) {
 }
 
 // ---------------------------------------------------------------------------
-// One TMExpr row in shared memory.  Scalars are warp-uniform: every lane
-// writes the same value, so a lane always reads back its own store.
-struct Row {
-  double az[NZP];
-  double bz[NZP];
+// TMExpr rows as slots.  A slot is a row of the field evaluation: its
+// warp-uniform scalars (centre, time coefficient, remainder, the cached
+// abs-sums) plus the shared-memory rows of its az / bz coefficients.
+//   P0..15  the Picard iterate p_k: az aliases the seed rows S (poly_picard
+//           never changes the z columns: g = seed + Int f adds only tau terms),
+//           bz in Pbz;
+//   T0..3   full temporaries;
+//   V0..9   views: rows whose coefficients are a scalar multiple of another
+//           row's (sin / cos linearizations, scalar products, reciprocals,
+//           taylor_model.hpp:284-295, 364-425), az = (base.az * s1) * s2, so
+//           they cost no coefficient storage and no coefficient pass.
+constexpr int NTF = 4;
+constexpr int NV = 10;
+constexpr int SLOT_T = NA;
+constexpr int SLOT_V = NA + NTF;
+constexpr int NSLOT = NA + NTF + NV;
+
+struct Slot {
   double c, at, rlo, rhi;
-  double sz, sb;  // cached abs_z / abs_b (taylor_model.hpp:213-224)
-  double pad[2];
+  double sz, sb;  // abs_z / abs_b (taylor_model.hpp:213-224) of the row's coefficients
+  double s1, s2;  // view scales (1, 1 for a stored row)
+  int az, bz;     // coefficient rows: offsets (doubles) into FlowSmem::coef
+  int view, pad;
 };
+
+// Shared memory of one flow warp (~29 KB: 7 warps per SM).
+struct FlowSmem {
+  double coef[NA * NZP + NA * NZP + 2 * NTF * NZP];  // S (= P.az) | Pbz | Taz | Tbz
+  Slot D[NSLOT];
+  double sc[NA];   // seed centre
+  double ssz[NA];  // abs_z of the seed rows
+  double ec[NA];   // endpoint centre
+  double kc[8];    // plant constants (CTParams::kc)
+  Iv erem[NA], i0[NA], i1[NA], nx[NA];
+};
+constexpr int OFF_S = 0, OFF_PBZ = NA * NZP, OFF_TAZ = 2 * NA * NZP, OFF_TBZ = 2 * NA * NZP + NTF * NZP;
 
 struct Lane {
   int lane;
@@ -141,11 +171,18 @@ __device__ __forceinline__ Iv poly_range(double c, double sz, double at, double 
   const double br = sb * h;
   return iadd(r, Iv{-br, br});
 }
-__device__ __forceinline__ Iv total_range(const Row& u, double h) {
-  return iadd(poly_range(u.c, u.sz, u.at, u.sb, h), Iv{u.rlo, u.rhi});
+
+// Coefficients of slot d at lane slot j (views scaled in the reference's order).
+__device__ __forceinline__ void fetch(const double* coef, const Slot& d, int j, double& a, double& b) {
+  a = coef[d.az + j];
+  b = coef[d.bz + j];
+  if (d.view) {
+    a = (a * d.s1) * d.s2;
+    b = (b * d.s1) * d.s2;
+  }
 }
 
-__device__ __forceinline__ void put_scalars(Row& r, double c, double at, Iv rem, double sz, double sb) {
+__device__ __forceinline__ void set_scalars(Slot& r, double c, double at, Iv rem, double sz, double sb) {
   r.c = c;
   r.at = at;
   r.rlo = rem.lo;
@@ -154,8 +191,66 @@ __device__ __forceinline__ void put_scalars(Row& r, double c, double at, Iv rem,
   r.sb = sb;
 }
 
+// ---- the field program ------------------------------------------------------
+enum : unsigned char { OP_MUL, OP_ADD, OP_SUB, OP_SUBK, OP_SCALE, OP_SIN, OP_COS, OP_INV, OP_CONS, OP_CONS0, OP_END };
+struct TOp {
+  unsigned char code, dst, a, b;  // b: second operand, or the constant index (SCALE / SUBK)
+};
+#define P_(i) static_cast<unsigned char>(i)
+#define T_(i) static_cast<unsigned char>(SLOT_T + (i))
+#define V_(i) static_cast<unsigned char>(SLOT_V + (i))
+
+// make_augmented_field(12, 4, quadrotor_ode) (fields.hpp:96-107,
+// systems.hpp:24-64) as a program over the slots.  Constants (CTParams::kc):
+// 0 = 1/mass, 1 = gravity, 2 = (jy-jz)/jx, 3 = 1/jx, 4 = (jz-jx)/jy,
+// 5 = 1/jy, 6 = (jx-jy)/jz, 7 = 1/jz.  Each derivative row dx_i is consumed
+// (CONS i) once neither P_i nor a view of it is read again, so a consumer may
+// overwrite P_i (poly_picard's in-place update).  Expression trees and
+// operand order are the reference's.
+__constant__ TOp kQuadTape[] = {
+    {OP_CONS, 0, P_(3), 0}, {OP_CONS, 1, P_(4), 0}, {OP_CONS, 2, P_(5), 0},  // dx0..2 = v
+    {OP_SIN, V_(0), P_(6), 0}, {OP_COS, V_(1), P_(6), 0},                     // sphi, cphi
+    {OP_SIN, V_(2), P_(7), 0}, {OP_COS, V_(3), P_(7), 0},                     // sth, cth
+    {OP_SIN, V_(4), P_(8), 0}, {OP_COS, V_(5), P_(8), 0},                     // spsi, cpsi
+    {OP_SCALE, V_(6), P_(12), 0},                                             // a = u0 * (1/mass)
+    {OP_MUL, T_(0), V_(1), V_(2)},                                            // cphi*sth
+    {OP_MUL, T_(1), T_(0), V_(5)}, {OP_MUL, T_(2), V_(0), V_(4)},             // *cpsi, sphi*spsi
+    {OP_ADD, T_(1), T_(1), T_(2)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3x, a*b3x
+    {OP_CONS, 3, T_(2), 0},
+    {OP_MUL, T_(1), T_(0), V_(4)}, {OP_MUL, T_(2), V_(0), V_(5)},             // *spsi, sphi*cpsi
+    {OP_SUB, T_(1), T_(1), T_(2)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3y, a*b3y
+    {OP_CONS, 4, T_(2), 0},
+    {OP_MUL, T_(1), V_(1), V_(3)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3z, a*b3z
+    {OP_SUBK, T_(2), 0, 1},                                                   // - gravity
+    {OP_CONS, 5, T_(2), 0},
+    {OP_INV, V_(7), V_(3), 0},                                                // tme_inv(cth)
+    {OP_MUL, T_(0), V_(2), V_(7)},                                            // tth = sth / cth
+    {OP_MUL, T_(1), V_(0), T_(0)}, {OP_MUL, T_(1), T_(1), P_(10)},            // sphi*tth*q
+    {OP_ADD, T_(1), P_(9), T_(1)},                                            // p + ...
+    {OP_MUL, T_(2), V_(1), T_(0)}, {OP_MUL, T_(2), T_(2), P_(11)},            // cphi*tth*r
+    {OP_ADD, T_(1), T_(1), T_(2)},                                            // dx6 (held)
+    {OP_MUL, T_(0), V_(1), P_(10)}, {OP_MUL, T_(2), V_(0), P_(11)},           // cphi*q, sphi*r
+    {OP_SUB, T_(0), T_(0), T_(2)},                                            // dx7 (held)
+    {OP_MUL, T_(2), V_(0), V_(7)}, {OP_MUL, T_(2), T_(2), P_(10)},            // (sphi/cth)*q
+    {OP_MUL, T_(3), V_(1), V_(7)}, {OP_MUL, T_(3), T_(3), P_(11)},            // (cphi/cth)*r
+    {OP_ADD, T_(2), T_(2), T_(3)},                                            // dx8
+    // the views of P6 / P7 (sphi, cphi, 1/cth) are dead only now: consume rows 6..8
+    {OP_CONS, 6, T_(1), 0}, {OP_CONS, 7, T_(0), 0}, {OP_CONS, 8, T_(2), 0},
+    {OP_MUL, T_(0), P_(10), P_(11)}, {OP_SCALE, V_(8), T_(0), 2},             // q*r*c1
+    {OP_SCALE, V_(9), P_(13), 3}, {OP_ADD, T_(0), V_(8), V_(9)},              // + u1/jx
+    {OP_MUL, T_(1), P_(9), P_(11)}, {OP_SCALE, V_(8), T_(1), 4},              // p*r*c3
+    {OP_SCALE, V_(9), P_(14), 5}, {OP_ADD, T_(1), V_(8), V_(9)},              // + u2/jy
+    {OP_MUL, T_(2), P_(9), P_(10)}, {OP_SCALE, V_(8), T_(2), 6},              // p*q*c5
+    {OP_SCALE, V_(9), P_(15), 7}, {OP_ADD, T_(2), V_(8), V_(9)},              // + u3/jz
+    {OP_CONS, 9, T_(0), 0}, {OP_CONS, 10, T_(1), 0}, {OP_CONS, 11, T_(2), 0},
+    {OP_CONS0, 12, 0, 0}, {OP_CONS0, 13, 0, 0}, {OP_CONS0, 14, 0, 0}, {OP_CONS0, 15, 0, 0},
+    {OP_END, 0, 0, 0},
+};
+
+enum : int { MODE_PICARD = 0, MODE_REPLAY = 1, MODE_ENDPOINT = 2 };
+
 // operator* (taylor_model.hpp:325-360).  r may alias u or v.
-__device__ __forceinline__ void tm_mul(Row& r, const Row& u, const Row& v, const Lane& L) {
+__device__ __forceinline__ void op_mul(FlowSmem& W, Slot& r, const Slot& u, const Slot& v, const Lane& L) {
   const double h = L.h;
   const double uc = u.c, vc = v.c, uat = u.at, vat = v.at;
   const double au = u.sz, av = v.sz, bu = u.sb, bv = v.sb;
@@ -165,11 +260,13 @@ __device__ __forceinline__ void tm_mul(Row& r, const Row& u, const Row& v, const
   for (int k = 0; k < NZC; ++k) {
     if (!L.act[k]) continue;
     const int j = L.lane + 32 * k;
-    const double ua = u.az[j], ub = u.bz[j], va = v.az[j], vb = v.bz[j];
+    double ua, ub, va, vb;
+    fetch(W.coef, u, j, ua, ub);
+    fetch(W.coef, v, j, va, vb);
     const double ra = uc * va + vc * ua;
     const double rb = uc * vb + vc * ub + uat * va + vat * ua;
-    r.az[j] = ra;
-    r.bz[j] = rb;
+    W.coef[r.az + j] = ra;
+    W.coef[r.bz + j] = rb;
     s1 += fabs(ra);
     s2 += fabs(rb);
   }
@@ -185,195 +282,176 @@ __device__ __forceinline__ void tm_mul(Row& r, const Row& u, const Row& v, const
   rem = iadd(rem, imul(pu, vr));
   rem = iadd(rem, imul(pv, ur));
   rem = iadd(rem, imul(ur, vr));
-  put_scalars(r, uc * vc, uc * vat + vc * uat, rem, s1, s2);
+  set_scalars(r, uc * vc, uc * vat + vc * uat, rem, s1, s2);
 }
 
 // a + b / a - b (taylor_model.hpp:245-269); r may alias a or b.
-template <bool SUB>
-__device__ __forceinline__ void tm_addsub(Row& r, const Row& a, const Row& b, const Lane& L) {
-  const double c = SUB ? a.c - b.c : a.c + b.c;
-  const double at = SUB ? a.at - b.at : a.at + b.at;
-  const Iv rem = SUB ? isub(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi}) : iadd(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi});
+__device__ __forceinline__ void op_addsub(FlowSmem& W, Slot& r, const Slot& a, const Slot& b, bool sub, const Lane& L) {
+  const double c = sub ? a.c - b.c : a.c + b.c;
+  const double at = sub ? a.at - b.at : a.at + b.at;
+  const Iv rem = sub ? isub(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi}) : iadd(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi});
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll
   for (int k = 0; k < NZC; ++k) {
     if (!L.act[k]) continue;
     const int j = L.lane + 32 * k;
-    const double ra = SUB ? a.az[j] - b.az[j] : a.az[j] + b.az[j];
-    const double rb = SUB ? a.bz[j] - b.bz[j] : a.bz[j] + b.bz[j];
-    r.az[j] = ra;
-    r.bz[j] = rb;
+    double aa, ab, ba, bb;
+    fetch(W.coef, a, j, aa, ab);
+    fetch(W.coef, b, j, ba, bb);
+    const double ra = sub ? aa - ba : aa + ba;
+    const double rb = sub ? ab - bb : ab + bb;
+    W.coef[r.az + j] = ra;
+    W.coef[r.bz + j] = rb;
     s1 += fabs(ra);
     s2 += fabs(rb);
   }
   wsum2(s1, s2);
-  put_scalars(r, c, at, rem, s1, s2);
+  set_scalars(r, c, at, rem, s1, s2);
 }
 
-// s * a (+ d): scalar product (taylor_model.hpp:284-295) then + d (:302-306).
-__device__ __forceinline__ void tm_affine(Row& r, double s, const Row& a, double d, const Lane& L) {
-  const double c = a.c * s + d;
-  const double at = a.at * s;
-  const Iv rem = iscale(s, Iv{a.rlo, a.rhi});
-  double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-  for (int k = 0; k < NZC; ++k) {
-    if (!L.act[k]) continue;
-    const int j = L.lane + 32 * k;
-    const double ra = a.az[j] * s, rb = a.bz[j] * s;
-    r.az[j] = ra;
-    r.bz[j] = rb;
-    s1 += fabs(ra);
-    s2 += fabs(rb);
+// r = view of u scaled by s: r.az = (u.az * s) (taylor_model.hpp:284-295).
+// A view of a view adds the second scale (the reference's two roundings).
+__device__ __forceinline__ void make_view(Slot& r, const Slot& u, double s) {
+  r.az = u.az;
+  r.bz = u.bz;
+  r.view = 1;
+  if (u.view) {
+    r.s1 = u.s1;
+    r.s2 = s;
+  } else {
+    r.s1 = s;
+    r.s2 = 1.0;
   }
-  wsum2(s1, s2);
-  put_scalars(r, c, at, rem, s1, s2);
 }
 
-// sin / cos by linearization about the centre (taylor_model.hpp:397-425):
-// r = f'(m) (u - m) + f(m) (+) [-rad^2/2, rad^2/2].  r may alias u.
-template <bool COS>
-__device__ __forceinline__ void tm_trig(Row& r, const Row& u, const Lane& L) {
-  const double m = u.c;
-  const Iv range = total_range(u, L.h);
-  const double rad = smax(fabs(range.lo - m), fabs(range.hi - m));
-  const double err = rad * rad * 0.5;
-  double sm, cm;
-  sincos(m, &sm, &cm);
-  const double s = COS ? -sm : cm;
-  const double c = (m - m) * s + (COS ? cm : sm);  // (u - m) has centre u.c - m
-  const double at = u.at * s;
-  Iv rem = iscale(s, Iv{u.rlo, u.rhi});
-  rem = iadd(rem, Iv{-err, err});
-  double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-  for (int k = 0; k < NZC; ++k) {
-    if (!L.act[k]) continue;
-    const int j = L.lane + 32 * k;
-    const double ra = u.az[j] * s, rb = u.bz[j] * s;
-    r.az[j] = ra;
-    r.bz[j] = rb;
-    s1 += fabs(ra);
-    s2 += fabs(rb);
-  }
-  wsum2(s1, s2);
-  put_scalars(r, c, at, rem, s1, s2);
-}
-
-// tme_inv (taylor_model.hpp:364-380); `thrown` replaces the domain_error.
-__device__ __forceinline__ void tm_inv(Row& r, const Row& v, bool& thrown, const Lane& L) {
-  const Iv range = total_range(v, L.h);
-  if (range.lo <= 0.0 && range.hi >= 0.0) thrown = true;
-  const double m = v.c;
-  const double mm = m * m;
-  const double e_lo = 1.0 / range.lo - (2.0 / m - range.lo / mm);
-  const double e_hi = 1.0 / range.hi - (2.0 / m - range.hi / mm);
-  const Iv e{smin(smin(e_lo, e_hi), 0.0), smax(smax(e_lo, e_hi), 0.0)};
-  const double s = -1.0 / mm;
-  tm_affine(r, s, v, 2.0 / m, L);
-  r.rlo = r.rlo + e.lo;
-  r.rhi = r.rhi + e.hi;
-}
-
-// ---------------------------------------------------------------------------
-// make_augmented_field(12, 4, quadrotor_ode) (fields.hpp:96-107,
-// systems.hpp:24-64) on the rows P[0..16) with temporaries T[0..NT).  Each
-// derivative row dx_i is handed to consume(i, row) as soon as it exists
-// (consume(i, nullptr) for the udot = 0 rows), in an order that lets a
-// consumer overwrite P[i] (poly_picard's in-place update): P[i] is never
-// read after dx_i is consumed.  The expression trees are the reference's,
-// operand order included (TMExpr products are not commutative in rounding).
-template <class Consume>
-__device__ __forceinline__ bool quad_field(Row* P, Row* T, const double* prm, const Lane& L, Consume&& consume) {
+// The field program on the slots; `mode` selects what CONS does with dx_i:
+//   PICARD    g_i = seed_i + Int dx_i written over P_i (flowpipe_ct.hpp:130-133)
+//   REPLAY    I1_i = range(seed_i + Int dx_i - p_k,i) (:154-165)
+//   ENDPOINT  x(h)_i = seed_i + h (dx_i(0) + h/2 dx_i') to the state's HBM rows (:241-257)
+// Returns the tme_inv "throw" (taylor_model.hpp:367-368).
+__device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, const Lane L, double* gM) {
   bool thrown = false;
-  const double mass = prm[0], grav = prm[1], jx = prm[2], jy = prm[3], jz = prm[4];
-  Row &sphi = T[0], &cphi = T[1], &sth = T[2], &cth = T[3], &spsi = T[4], &cpsi = T[5];
-  Row &a = T[6], &t1 = T[7], &t2 = T[8], &t3 = T[9];
-  const Row &p = P[9], &q = P[10], &r = P[11];
-  consume(0, &P[3]);
-  consume(1, &P[4]);
-  consume(2, &P[5]);
-  tm_trig<false>(sphi, P[6], L);
-  tm_trig<true>(cphi, P[6], L);
-  tm_trig<false>(sth, P[7], L);
-  tm_trig<true>(cth, P[7], L);
-  tm_trig<false>(spsi, P[8], L);
-  tm_trig<true>(cpsi, P[8], L);
-  tm_affine(a, 1.0 / mass, P[12], 0.0, L);
-  // b3x = cphi*sth*cpsi + sphi*spsi ; dx3 = a*b3x
-  tm_mul(t1, cphi, sth, L);
-  tm_mul(t2, t1, cpsi, L);
-  tm_mul(t3, sphi, spsi, L);
-  tm_addsub<false>(t2, t2, t3, L);
-  tm_mul(t3, a, t2, L);
-  consume(3, &t3);
-  // b3y = cphi*sth*spsi - sphi*cpsi ; dx4 = a*b3y
-  tm_mul(t2, t1, spsi, L);
-  tm_mul(t3, sphi, cpsi, L);
-  tm_addsub<true>(t2, t2, t3, L);
-  tm_mul(t3, a, t2, L);
-  consume(4, &t3);
-  // dx5 = a*(cphi*cth) - g
-  tm_mul(t2, cphi, cth, L);
-  tm_mul(t3, a, t2, L);
-  t3.c = t3.c - grav;
-  consume(5, &t3);
-  // tth = sth / cth = sth * tme_inv(cth); `a` now holds tme_inv(cth)
-  tm_inv(a, cth, thrown, L);
-  tm_mul(t1, sth, a, L);
-  // dx6 = p + sphi*tth*q + cphi*tth*r
-  tm_mul(t2, sphi, t1, L);
-  tm_mul(t2, t2, q, L);
-  tm_addsub<false>(t2, p, t2, L);
-  tm_mul(t3, cphi, t1, L);
-  tm_mul(t3, t3, r, L);
-  tm_addsub<false>(t3, t2, t3, L);
-  consume(6, &t3);
-  // dx7 = cphi*q - sphi*r
-  tm_mul(t2, cphi, q, L);
-  tm_mul(t3, sphi, r, L);
-  tm_addsub<true>(t2, t2, t3, L);
-  consume(7, &t2);
-  // dx8 = (sphi/cth)*q + (cphi/cth)*r (each division re-evaluates tme_inv(cth): same value)
-  tm_mul(t2, sphi, a, L);
-  tm_mul(t2, t2, q, L);
-  tm_mul(t3, cphi, a, L);
-  tm_mul(t3, t3, r, L);
-  tm_addsub<false>(t2, t2, t3, L);
-  consume(8, &t2);
-  // dx9..11 = (rate products) * inertia ratio + torque / inertia
-  tm_mul(T[0], q, r, L);
-  tm_affine(T[0], (jy - jz) / jx, T[0], 0.0, L);
-  tm_affine(T[1], 1.0 / jx, P[13], 0.0, L);
-  tm_addsub<false>(T[0], T[0], T[1], L);
-  tm_mul(T[1], p, r, L);
-  tm_affine(T[1], (jz - jx) / jy, T[1], 0.0, L);
-  tm_affine(T[2], 1.0 / jy, P[14], 0.0, L);
-  tm_addsub<false>(T[1], T[1], T[2], L);
-  tm_mul(T[2], p, q, L);
-  tm_affine(T[2], (jx - jy) / jz, T[2], 0.0, L);
-  tm_affine(T[3], 1.0 / jz, P[15], 0.0, L);
-  tm_addsub<false>(T[2], T[2], T[3], L);
-  consume(9, &T[0]);
-  consume(10, &T[1]);
-  consume(11, &T[2]);
+  const double h = L.h;
+  const int lane = L.lane;
+  for (int pc = 0;; ++pc) {
+    const TOp op = kQuadTape[pc];
+    if (op.code == OP_END) break;
+    switch (op.code) {
+      case OP_MUL:
+        op_mul(W, W.D[op.dst], W.D[op.a], W.D[op.b], L);
+        break;
+      case OP_ADD:
+      case OP_SUB:
+        op_addsub(W, W.D[op.dst], W.D[op.a], W.D[op.b], op.code == OP_SUB, L);
+        break;
+      case OP_SUBK:
+        W.D[op.dst].c = W.D[op.dst].c - kc[op.b];
+        break;
+      case OP_SCALE: {  // TM * s (taylor_model.hpp:297-300)
+        const Slot& u = W.D[op.a];
+        Slot& r = W.D[op.dst];
+        const double s = kc[op.b];
+        const Iv rem = iscale(s, Iv{u.rlo, u.rhi});
+        set_scalars(r, u.c * s, u.at * s, rem, fabs(s) * u.sz, fabs(s) * u.sb);
+        make_view(r, u, s);
+        break;
+      }
+      case OP_SIN:
+      case OP_COS: {  // linearization about the centre (taylor_model.hpp:397-425)
+        const Slot& u = W.D[op.a];
+        Slot& r = W.D[op.dst];
+        const double m = u.c;
+        const Iv range = iadd(poly_range(u.c, u.sz, u.at, u.sb, h), Iv{u.rlo, u.rhi});
+        const double rad = smax(fabs(range.lo - m), fabs(range.hi - m));
+        const double err = rad * rad * 0.5;
+        double sm, cm;
+        sincos(m, &sm, &cm);
+        const bool isc = op.code == OP_COS;
+        const double s = isc ? -sm : cm;
+        Iv rem = iscale(s, Iv{u.rlo, u.rhi});
+        rem = iadd(rem, Iv{-err, err});
+        set_scalars(r, (m - m) * s + (isc ? cm : sm), u.at * s, rem, fabs(s) * u.sz, fabs(s) * u.sb);
+        make_view(r, u, s);
+        break;
+      }
+      case OP_INV: {  // tme_inv (taylor_model.hpp:364-380)
+        const Slot& v = W.D[op.a];
+        Slot& r = W.D[op.dst];
+        const Iv range = iadd(poly_range(v.c, v.sz, v.at, v.sb, h), Iv{v.rlo, v.rhi});
+        if (range.lo <= 0.0 && range.hi >= 0.0) thrown = true;
+        const double m = v.c, mm = m * m;
+        const double e_lo = 1.0 / range.lo - (2.0 / m - range.lo / mm);
+        const double e_hi = 1.0 / range.hi - (2.0 / m - range.hi / mm);
+        const Iv e{smin(smin(e_lo, e_hi), 0.0), smax(smax(e_lo, e_hi), 0.0)};
+        const double s = -1.0 / mm;
+        Iv rem = iscale(s, Iv{v.rlo, v.rhi});
+        rem = iadd(rem, e);
+        set_scalars(r, v.c * s + 2.0 / m, v.at * s, rem, fabs(s) * v.sz, fabs(s) * v.sb);
+        make_view(r, v, s);
+        break;
+      }
+      case OP_CONS:
+      case OP_CONS0: {
+        const int i = op.dst;
+        const bool zero = op.code == OP_CONS0;
+        const Slot& f = W.D[zero ? 0 : op.a];
+        const double fc = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at;
+        const double fsz = zero ? 0.0 : f.sz, fsb = zero ? 0.0 : f.sb;
+        const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
+        double* S = W.coef + OFF_S + i * NZP;
+        double* Pb = W.coef + OFF_PBZ + i * NZP;
+        if (mode == MODE_ENDPOINT) {
 #pragma unroll
-  for (int i = 12; i < NA; ++i) consume(i, static_cast<const Row*>(nullptr));
+          for (int k = 0; k < NZC; ++k) {
+            if (!L.act[k]) continue;
+            const int j = lane + 32 * k;
+            double fa = 0.0, fb = 0.0;
+            if (!zero) fetch(W.coef, f, j, fa, fb);
+            gM[i * NZP + j] = S[j] + h * (fa + fb * h * 0.5);
+          }
+          W.ec[i] = W.sc[i] + h * (fc + fat * h * 0.5);
+          W.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
+          break;
+        }
+        // tme_integrate(dx_i) remainder (taylor_model.hpp:436-443)
+        const double half_at = fat * 0.5;
+        Iv rem = imul(Iv{0.0, h * h}, Iv{half_at, half_at});
+        const double bb = fsb * h * h * 0.5;
+        rem = iadd(rem, Iv{-bb, bb});
+        rem = iadd(rem, imul(fr, Iv{0.0, h}));
+        if (mode == MODE_PICARD) {
+#pragma unroll
+          for (int k = 0; k < NZC; ++k) {
+            if (!L.act[k]) continue;
+            const int j = lane + 32 * k;
+            double fa = 0.0, fb;
+            if (!zero) fetch(W.coef, f, j, fa, fb);
+            Pb[j] = fa;
+          }
+          set_scalars(W.D[i], W.sc[i], fc, rem, W.ssz[i], fsz);
+        } else {  // REPLAY: (seed + Int f) - p_k; its z part seed - p_k.az is exactly 0
+          double s2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < NZC; ++k) {
+            if (!L.act[k]) continue;
+            const int j = lane + 32 * k;
+            double fa = 0.0, fb;
+            if (!zero) fetch(W.coef, f, j, fa, fb);
+            s2 += fabs(fa - Pb[j]);
+          }
+          s2 = wsum(s2);
+          const Slot& pk = W.D[i];
+          const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
+          W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc - pk.at, s2, h), rem);
+        }
+        break;
+      }
+      default:
+        break;
+    }
+  }
   return thrown;
 }
-
-// ---------------------------------------------------------------------------
-// Shared memory of one flow warp.
-struct FlowSmem {
-  Row P[NA];          // the Picard iterate p_k (candidate remainders in rem)
-  Row T[NT];          // field temporaries
-  double S[NA * LDS];  // seed / endpoint generator rows [G0 | Q1..Qnq], stride LDS
-  double sc[NA];      // seed centre
-  double ssz[NA];     // abs_z of the seed rows
-  double ec[NA];      // endpoint centre
-  Iv erem[NA];        // endpoint remainder
-  Iv i0[NA], i1[NA], nx[NA];
-};
 
 __device__ __forceinline__ void emit_box(const CTParams& P, long long b, int k, int d, double lo, double hi) {
   if (!P.split) {
@@ -409,37 +487,53 @@ __device__ __forceinline__ void finalize(const CTParams& P, long long b, int nb,
   }
 }
 
-// hull fold of fold_overflow (flowpipe_ct.hpp:347-348) on the shared state:
-// the oldest block (columns [p0, p0 + NA)) is boxed into the newest block's
-// diagonal (columns [nz - NA, nz)), then dropped.  Lane i < NA sweeps row i
-// sequentially (the reference's row_abs_sum order).
-__device__ __forceinline__ void fold_hull(double* S, int p0, int& nz, int& nq, int cap, int lane) {
-  while (nq > cap) {
-    __syncwarp();
-    if (lane < NA) {
-      double r = 0.0;
-      for (int j = 0; j < NA; ++j) r += fabs(S[lane * LDS + p0 + j]);
-      S[lane * LDS + (nz - NA) + lane] += r;
-    }
-    __syncwarp();
+// symbolic_step's queue push + fold_overflow (flowpipe_ct.hpp:378-409,
+// 347-348) on rows of stride `ld`: the fresh block diag(rad) joins the queue;
+// if the queue overflows, the oldest block (columns [p0, p0 + NA)) is boxed
+// into the fresh block's diagonal and dropped.  The oldest block's row sums
+// are taken first and the fresh block is written after the shift, so rows
+// never exceed nz + NA - NA columns: newest(i,i) = rad_i + row_abs_sum(oldest, i),
+// the reference's one addition.  Lane i < NA sweeps row i sequentially.
+template <class RowPtr>
+__device__ __forceinline__ void push_fresh_fold(RowPtr row, const Iv* erem, int p0, int& nz, int& nq, int cap,
+                                                int lane) {
+  __syncwarp();
+  const bool fold = nq + 1 > cap;
+  double add = 0.0;
+  if (fold && lane < NA)
+    for (int j = 0; j < NA; ++j) add += fabs(row(lane)[p0 + j]);
+  __syncwarp();
+  if (fold) {
     for (int i = 0; i < NA; ++i) {
       double v[NZC];
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
         const int j = lane + 32 * k;
-        v[k] = (j >= p0 && j + NA < nz) ? S[i * LDS + j + NA] : 0.0;
+        v[k] = (j >= p0 && j + NA < nz) ? row(i)[j + NA] : 0.0;
       }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
         const int j = lane + 32 * k;
-        if (j >= p0 && j < nz) S[i * LDS + j] = v[k];
+        if (j >= p0 && j < nz) row(i)[j] = v[k];
       }
     }
-    __syncwarp();
     nz -= NA;
     nq -= 1;
   }
+  __syncwarp();
+  for (int i = 0; i < NA; ++i) {
+    const double ai = fold ? __shfl_sync(0xffffffffu, add, i) : 0.0;
+#pragma unroll
+    for (int k = 0; k < NZC; ++k) {
+      const int j = lane + 32 * k;
+      const double rad = (erem[i].hi - erem[i].lo) * 0.5;
+      if (j >= nz && j < nz + NA) row(i)[j] = (j - nz == i) ? (fold ? rad + ai : rad) : 0.0;
+    }
+  }
+  nz += NA;
+  nq += 1;
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -461,25 +555,31 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
   const int p0 = Pm.n;
   const int cap = Pm.window > 0 ? Pm.window : 1;
   int nz = p0 + nq * NA;
-  // load the state; zero every row's padding once (ops never write it)
-  {
-    const double* gM = Pm.st_M + static_cast<size_t>(b) * NA * NZP;
-    for (int i = 0; i < NA; ++i) {
-#pragma unroll
-      for (int k = 0; k < NZC; ++k) {
-        const int j = lane + 32 * k;
-        W.S[i * LDS + j] = gM[i * NZP + j];
-        W.P[i].az[j] = 0.0;
-        W.P[i].bz[j] = 0.0;
-      }
+  double* gM = Pm.st_M + static_cast<size_t>(b) * NA * NZP;
+  // state in, every coefficient row zeroed beyond nz (ops never write there)
+  for (int t = lane; t < NA * NZP; t += 32) {
+    const int j = t % NZP;
+    W.coef[OFF_S + t] = (j < nz) ? gM[t] : 0.0;
+    W.coef[OFF_PBZ + t] = 0.0;
+  }
+  for (int t = lane; t < 2 * NTF * NZP; t += 32) W.coef[OFF_TAZ + t] = 0.0;
+  if (lane < NA) W.sc[lane] = Pm.st_c[b * NA + lane];
+  if (lane < 8) W.kc[lane] = Pm.kc[lane];
+  for (int s = 0; s < NSLOT; ++s) {  // stored rows: P_i = (S_i, Pbz_i), T_t
+    Slot& d = W.D[s];
+    d.s1 = 1.0;
+    d.s2 = 1.0;
+    d.view = 0;
+    if (s < NA) {
+      d.az = OFF_S + s * NZP;
+      d.bz = OFF_PBZ + s * NZP;
+    } else if (s < SLOT_V) {
+      d.az = OFF_TAZ + (s - SLOT_T) * NZP;
+      d.bz = OFF_TBZ + (s - SLOT_T) * NZP;
+    } else {
+      d.az = OFF_TAZ;
+      d.bz = OFF_TBZ;
     }
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int k = 0; k < NZC; ++k) {
-        W.T[t].az[lane + 32 * k] = 0.0;
-        W.T[t].bz[lane + 32 * k] = 0.0;
-      }
-    if (lane < NA) W.sc[lane] = Pm.st_c[b * NA + lane];
   }
   __syncwarp();
 
@@ -490,91 +590,40 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     const int gstep = Pm.ci * Pm.K + step;
 #pragma unroll
     for (int k = 0; k < NZC; ++k) L.act[k] = (lane + 32 * k) < nz;
-    // seed rows: abs_z of each (cached for the Picard rows)
+    // seed rows: abs_z (cached: the Picard rows share their z columns)
     for (int i = 0; i < NA; i += 2) {
       double s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
         if (!L.act[k]) continue;
         const int j = lane + 32 * k;
-        s1 += fabs(W.S[i * LDS + j]);
-        s2 += fabs(W.S[(i + 1) * LDS + j]);
+        s1 += fabs(W.coef[OFF_S + i * NZP + j]);
+        s2 += fabs(W.coef[OFF_S + (i + 1) * NZP + j]);
       }
       wsum2(s1, s2);
       W.ssz[i] = s1;
       W.ssz[i + 1] = s2;
     }
-    // poly_picard (flowpipe_ct.hpp:126-139): g_0 = seed
+    // poly_picard (flowpipe_ct.hpp:126-139): g_0 = seed (bz = 0, at = 0, rem = 0)
     for (int i = 0; i < NA; ++i) {
 #pragma unroll
-      for (int k = 0; k < NZC; ++k) {
-        if (!L.act[k]) continue;
-        const int j = lane + 32 * k;
-        W.P[i].az[j] = W.S[i * LDS + j];
-        W.P[i].bz[j] = 0.0;
-      }
-      put_scalars(W.P[i], W.sc[i], 0.0, Iv{0.0, 0.0}, W.ssz[i], 0.0);
+      for (int k = 0; k < NZC; ++k)
+        if (L.act[k]) W.coef[OFF_PBZ + i * NZP + lane + 32 * k] = 0.0;
+      set_scalars(W.D[i], W.sc[i], 0.0, Iv{0.0, 0.0}, W.ssz[i], 0.0);
     }
-    // g_{j+1} = seed + Int f(g_j), rows overwritten in place as dx_i appears
-    auto picard = [&](int i, const Row* f) {
-      Row& g = W.P[i];
-      const double fc = f ? f->c : 0.0, fat = f ? f->at : 0.0, fsz = f ? f->sz : 0.0, fsb = f ? f->sb : 0.0;
-      const Iv fr = f ? Iv{f->rlo, f->rhi} : Iv{0.0, 0.0};
-#pragma unroll
-      for (int k = 0; k < NZC; ++k) {
-        if (!L.act[k]) continue;
-        const int j = lane + 32 * k;
-        const double fa = f ? f->az[j] : 0.0;
-        g.az[j] = W.S[i * LDS + j];
-        g.bz[j] = fa;
-      }
-      // tme_integrate (taylor_model.hpp:429-445) rem, added to the seed's [0, 0]
-      const double half_at = fat * 0.5;
-      Iv rem = imul(Iv{0.0, h * h}, Iv{half_at, half_at});
-      const double bb = fsb * h * h * 0.5;
-      rem = iadd(rem, Iv{-bb, bb});
-      rem = iadd(rem, imul(fr, Iv{0.0, h}));
-      put_scalars(g, W.sc[i], fc, rem, W.ssz[i], fsz);
-    };
     bool thrown = false;
-    for (int it = 0; it < Pm.order && !thrown; ++it) thrown = quad_field(W.P, W.T, Pm.prm, L, picard);
-    int fail = CT_OK;
-    if (thrown) fail = CT_TME_INV;
-    if (fail == CT_OK) {
+    for (int it = 0; it < Pm.order && !thrown; ++it) thrown = run_field(W, W.kc, MODE_PICARD, L, gM);
+    int fail = thrown ? CT_TME_INV : CT_OK;
+    if (fail == CT_OK)
       for (int i = 0; i < NA; ++i)
-        if (!isfinite(W.P[i].c)) fail = CT_PICARD;
-    }
+        if (!isfinite(W.D[i].c)) fail = CT_PICARD;
     // remainder_picard (flowpipe_ct.hpp:144-276)
-    auto replay = [&](const Iv* cand) {  // I1 induced by candidate remainder `cand` (:154-165)
+    auto replay = [&](const Iv* cand) {
       for (int i = 0; i < NA; ++i) {
-        W.P[i].rlo = cand[i].lo;
-        W.P[i].rhi = cand[i].hi;
+        W.D[i].rlo = cand[i].lo;
+        W.D[i].rhi = cand[i].hi;
       }
-      auto induced = [&](int i, const Row* f) {
-        const Row& pk = W.P[i];
-        const double fc = f ? f->c : 0.0, fat = f ? f->at : 0.0, fsb = f ? f->sb : 0.0;
-        const Iv fr = f ? Iv{f->rlo, f->rhi} : Iv{0.0, 0.0};
-        double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < NZC; ++k) {
-          if (!L.act[k]) continue;
-          const int j = lane + 32 * k;
-          const double fa = f ? f->az[j] : 0.0;
-          s1 += fabs(W.S[i * LDS + j] - pk.az[j]);
-          s2 += fabs(fa - pk.bz[j]);
-        }
-        wsum2(s1, s2);
-        // (seed + Int f) - p_k with p_k's own remainder [0, 0]
-        const double half_at = fat * 0.5;
-        Iv rem = imul(Iv{0.0, h * h}, Iv{half_at, half_at});
-        const double bb = fsb * h * h * 0.5;
-        rem = iadd(rem, Iv{-bb, bb});
-        rem = iadd(rem, imul(fr, Iv{0.0, h}));
-        const double dc = W.sc[i] - pk.c, dat = fc - pk.at;
-        const Iv r = iadd(poly_range(dc, s1, dat, s2, h), rem);
-        W.nx[i] = r;
-      };
-      return quad_field(W.P, W.T, Pm.prm, L, induced);
+      return run_field(W, W.kc, MODE_REPLAY, L, gM);
     };
     auto finite_box = [&](const Iv* x) {
       bool ok = true;
@@ -588,8 +637,6 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     };
     if (fail == CT_OK) {
       for (int i = 0; i < NA; ++i) {
-        W.P[i].rlo = 0.0;
-        W.P[i].rhi = 0.0;
         W.i0[i] = Iv{-Pm.eps, Pm.eps};
         W.i1[i] = Iv{0.0, 0.0};
       }
@@ -618,45 +665,20 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
         if (!(finite_box(W.nx) && subset(W.nx, W.i1))) break;
         for (int i = 0; i < NA; ++i) W.i1[i] = W.nx[i];
       }
-      // endpoint by exact integration at tau = h (:236-263), written over the seed rows
+      // endpoint by exact integration at tau = h (:236-263) into the HBM state rows
       for (int i = 0; i < NA; ++i) {
-        W.P[i].rlo = W.i1[i].lo;
-        W.P[i].rhi = W.i1[i].hi;
+        W.D[i].rlo = W.i1[i].lo;
+        W.D[i].rhi = W.i1[i].hi;
       }
-      auto endpoint = [&](int i, const Row* f) {
-        const double fc = f ? f->c : 0.0, fat = f ? f->at : 0.0;
-        const Iv fr = f ? Iv{f->rlo, f->rhi} : Iv{0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < NZC; ++k) {
-          if (!L.act[k]) continue;
-          const int j = lane + 32 * k;
-          const double fa = f ? f->az[j] : 0.0, fb = f ? f->bz[j] : 0.0;
-          W.S[i * LDS + j] = W.S[i * LDS + j] + h * (fa + fb * h * 0.5);
-        }
-        W.ec[i] = W.sc[i] + h * (fc + fat * h * 0.5);
-        W.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
-      };
-      const bool threw = quad_field(W.P, W.T, Pm.prm, L, endpoint);
+      const bool threw = run_field(W, W.kc, MODE_ENDPOINT, L, gM);
       bool exact_ok = !threw && finite_box(W.erem);
       for (int i = 0; i < NA; ++i) exact_ok = exact_ok && isfinite(W.ec[i]);
-      if (!exact_ok) {  // fallback: the certified segment at tau = h (:264-274)
-        for (int i = 0; i < NA; ++i) {
-#pragma unroll
-          for (int k = 0; k < NZC; ++k) {
-            if (!L.act[k]) continue;
-            const int j = lane + 32 * k;
-            W.S[i * LDS + j] = W.P[i].az[j] + W.P[i].bz[j] * h;
-          }
-          W.ec[i] = W.P[i].c + W.P[i].at * h;
-          W.erem[i] = W.i1[i];
-        }
-      }
-      // tm_eval_interval(segment, [0, h]) (taylor_model.hpp:73-97)
+      // tm_eval_interval(segment, [0, h]) (taylor_model.hpp:73-97), before S changes
       bool fin = true;
       const int kbox = 1 + gstep;
       double blo = 0.0, bhi = 0.0;
       for (int i = 0; i < NA; ++i) {
-        const Row& p = W.P[i];
+        const Slot& p = W.D[i];
         Iv acc{p.c - p.sz, p.c + p.sz};
         acc = iadd(acc, iscale(p.at, Iv{0.0, h}));
         const double tau_mag = smax(0.0, h);
@@ -670,24 +692,30 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
       }
       if (lane < NA) emit_box(Pm, b, kbox, lane, blo, bhi);
       nboxes = kbox + 1;
+      // new generator rows: the exact endpoint (HBM, L2-resident) or the fallback
+      // p_k(h) = seed + B h (:264-274), computed in place
+      for (int i = 0; i < NA; ++i) {
+#pragma unroll
+        for (int k = 0; k < NZC; ++k) {
+          if (!L.act[k]) continue;
+          const int j = lane + 32 * k;
+          double& s = W.coef[OFF_S + i * NZP + j];
+          s = exact_ok ? gM[i * NZP + j] : s + W.coef[OFF_PBZ + i * NZP + j] * h;
+        }
+        if (!exact_ok) {
+          W.ec[i] = W.D[i].c + W.D[i].at * h;
+          W.erem[i] = W.i1[i];
+        }
+      }
       if (!fin) {
         fail = CT_BOX;
       } else {
-        // symbolic_step (flowpipe_ct.hpp:378-409): centre the remainder, push
-        // its radius as a fresh diagonal block, fold the overflow
+        // symbolic_step (flowpipe_ct.hpp:378-409)
+        double c_new = 0.0;
+        if (lane < NA) c_new = W.ec[lane] + (W.erem[lane].lo + W.erem[lane].hi) * 0.5;
+        push_fresh_fold([&](int i) { return W.coef + OFF_S + i * NZP; }, W.erem, p0, nz, nq, cap, lane);
+        if (lane < NA) W.sc[lane] = c_new;
         __syncwarp();
-        for (int i = 0; i < NA; ++i) {
-#pragma unroll
-          for (int k = 0; k < NZC; ++k) {
-            const int j = lane + 32 * k;
-            if (j >= nz && j < nz + NA)
-              W.S[i * LDS + j] = (j - nz == i) ? (W.erem[i].hi - W.erem[i].lo) * 0.5 : 0.0;
-          }
-        }
-        if (lane < NA) W.sc[lane] = W.ec[lane] + (W.erem[lane].lo + W.erem[lane].hi) * 0.5;
-        nz += NA;
-        nq += 1;
-        fold_hull(W.S, p0, nz, nq, cap, lane);
       }
     }
     if (fail != CT_OK) {
@@ -695,18 +723,10 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
       fstep = gstep;
     }
   }
-  // write the state back
+  // state out
   __syncwarp();
-  {
-    double* gM = Pm.st_M + static_cast<size_t>(b) * NA * NZP;
-    for (int i = 0; i < NA; ++i)
-#pragma unroll
-      for (int k = 0; k < NZC; ++k) {
-        const int j = lane + 32 * k;
-        gM[i * NZP + j] = (j < nz) ? W.S[i * LDS + j] : 0.0;
-      }
-    if (lane < NA) Pm.st_c[b * NA + lane] = W.sc[lane];
-  }
+  for (int t = lane; t < NA * NZP; t += 32) gM[t] = W.coef[OFF_S + t];
+  if (lane < NA) Pm.st_c[b * NA + lane] = W.sc[lane];
   if (lane == 0) {
     meta[0] = nq;
     meta[1] = status;
@@ -725,7 +745,7 @@ struct CtlSmem {
   double xc[NX];
   double pre[kMaxLayers][kMaxCtlW][2];  // preactivation boxes of the hidden layers
   double hb[2][kMaxCtlW][2];     // IBP boxes
-  double lam[2][4][NZP + 32];    // Lambda (n_o x width), double buffered
+  double lam[2][4][kMaxCtlW];    // Lambda (n_o x width), double buffered
   double bf0[kMaxCtlW];          // frozen first-layer bias
   double blo[4], bup[4];
   double uc[4];
@@ -974,7 +994,7 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (i < no) S[i * (NZP + 32) + jc] = acc[i];
+      if (i < no) S[i * kMaxCtlW + jc] = acc[i];
   }
   __syncwarp();
   bool ufin = true;
@@ -988,16 +1008,29 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     }
     return;
   }
-  // ---- stacking (closed_loop.hpp:122-153) into global memory
-  int nz = nzx + NA;
-  int nqn = nbw + 1;
+  // ---- stacking (closed_loop.hpp:122-153) into global memory: rows [x; u]
+  // over columns [0, nzx), then the fresh diagonal block of the remainder
+  // radii.  If the queue overflows, fold_overflow's hull branch
+  // (flowpipe_ct.hpp:347-348; G0 = (n + l) x n is never square) boxes the
+  // oldest block (columns [n, n + NA)) into the fresh block's diagonal and
+  // drops it, so the rows are written in their folded layout directly.
+  auto stacked = [&](int d, int j) { return (d < n) ? W.xA[d * LDX + j] : S[(d - n) * kMaxCtlW + j]; };
+  const bool fold = nbw + 1 > cap;
+  const int nz_keep = fold ? nzx - NA : nzx;
+  const int nqn = fold ? nbw : nbw + 1;
+  const int nz = nz_keep + NA;
+  double add = 0.0;
+  if (fold && lane < NA)
+    for (int j = 0; j < NA; ++j) add += fabs(stacked(lane, n + j));
   for (int d = 0; d < NA; ++d) {
+    const double ad = fold ? __shfl_sync(0xffffffffu, add, d) : 0.0;
+    const double rad = (d < n) ? (0.0 - 0.0) * 0.5 : (W.urem[d - n].hi - W.urem[d - n].lo) * 0.5;
     for (int j = lane; j < NZP; j += 32) {
       double v = 0.0;
-      if (j < nzx) {
-        v = (d < n) ? W.xA[d * LDX + j] : S[(d - n) * (NZP + 32) + j];
-      } else if (j - nzx == d) {
-        v = (d < n) ? (0.0 - 0.0) * 0.5 : (W.urem[d - n].hi - W.urem[d - n].lo) * 0.5;
+      if (j < nz_keep) {
+        v = stacked(d, (fold && j >= n) ? j + NA : j);
+      } else if (j - nz_keep == d) {
+        v = fold ? rad + ad : rad;
       }
       gM[d * NZP + j] = v;
     }
@@ -1005,35 +1038,7 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
   if (lane < NA) gc[lane] = (lane < n) ? W.xc[lane] + (0.0 + 0.0) * 0.5
                                        : W.uc[lane - n] + (W.urem[lane - n].lo + W.urem[lane - n].hi) * 0.5;
   __syncwarp();
-  __threadfence_block();
-  // fold_overflow hull branch (flowpipe_ct.hpp:347-348), G0 = (n + l) x n is never square
-  while (nqn > cap) {
-    if (lane < NA) {
-      double r = 0.0;
-      for (int j = 0; j < NA; ++j) r += fabs(gM[lane * NZP + n + j]);
-      gM[lane * NZP + (nz - NA) + lane] += r;
-    }
-    __syncwarp();
-    __threadfence_block();
-    for (int d = 0; d < NA; ++d) {
-      double v[NZC];
-#pragma unroll
-      for (int k = 0; k < NZC; ++k) {
-        const int j = lane + 32 * k;
-        v[k] = (j >= n && j + NA < nz) ? gM[d * NZP + j + NA] : 0.0;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < NZC; ++k) {
-        const int j = lane + 32 * k;
-        if (j >= n && j < nz) gM[d * NZP + j] = v[k];
-      }
-      __syncwarp();
-    }
-    __threadfence_block();
-    nz -= NA;
-    nqn -= 1;
-  }
+  (void)nz;
   // box 0 = symbolic_box of the first augmented state (closed_loop.hpp:155)
   if (Pm.ci == 0) {
     __syncwarp();
