@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-sample-parts", type=int, default=0, help="parts per CPU sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mpc", action="store_true", help="skip the C3 MPC replan leg")
+    ap.add_argument("--no-ct", action="store_true", help="skip the C2 continuous-time closed-loop leg")
     return ap.parse_args()
 
 
@@ -216,6 +217,131 @@ def mpc_replan(args, ctx, world, rank, dev, barrier):
         except Exception as ex:  # noqa: BLE001
             out["cpu_reference_error"] = str(ex)
     return out
+
+
+def ct_flops_per_step(nz: int = 76, evals: float = 8.06) -> float:
+    """Algorithmic FP64 work of one C2 flowpipe step, counted on the reference's own TMExpr
+    operation sequence (taylor_model.hpp:245-445) for quadrotor_ode (systems.hpp:24-64):
+    per field evaluation 23 products (10 flops per generator column + the 4 abs-sums of the
+    operands' poly_range), 9 additions, 7 scalar products, 6 sin/cos and 3 reciprocals
+    (total_range + scaling), 16 integrations and the Picard/replay/endpoint combinations;
+    `evals` = measured field evaluations per step (2 Picard + remainder attempts + shrink
+    replays + endpoint, oracle/ct_oracle.c counter on the C2 workload)."""
+    mul = 14 * nz + 50
+    add = 2 * nz + 4
+    trig = 4 * nz + 20
+    integ = nz + 10
+    cons = 350 * nz / 76
+    per_eval = 23 * mul + 9 * add + 7 * add + 6 * trig + 3 * trig + 16 * (integ + cons)
+    return evals * per_eval + 3 * 16 * nz
+
+
+def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
+    """C2 (BASELINE configs[1]): reach_with_splitting(cl_reach) of the quadrotor + 3x64 tanh
+    controller, rpy:4096 sub-boxes x 50 flowpipe steps per GPU (weak scaling: x split N ways),
+    one hull all-reduce for N > 1.  Device-resident hull output, CUDA events on the library's stream."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_25346_b200 import _abi as A
+    from paper_2605_25346_b200.api import SplitPlan, cl_split_hull
+    from paper_2605_25346_b200.workloads import c2_quadrotor
+    w = c2_quadrotor()
+    spec = w.spec
+    per_rank = w.plan.total_parts()
+    counts = list(w.plan.counts)
+    counts[0] *= world
+    plan = SplitPlan(counts)
+    begin, end = rank * per_rank, (rank + 1) * per_rank
+    T, na = spec.steps(), spec.n + spec.l
+    ctx.set_stream(stream.cuda_stream)
+    d_lo = torch.empty(T * na, dtype=torch.float64, device=dev)
+    d_hi = torch.empty(T * na, dtype=torch.float64, device=dev)
+    d_div = torch.empty(T, dtype=torch.int32, device=dev)
+    d_nb = torch.empty(1, dtype=torch.int32, device=dev)
+    d_key = torch.empty(1, dtype=torch.int64, device=dev)
+    cs, keep = spec.c_struct()
+    cts = np.array(counts, dtype=np.int32)
+    x0lo, x0hi = np.ascontiguousarray(w.x0_lo), np.ascontiguousarray(w.x0_hi)
+    args_c = A.CLSplitArgs(A.dptr(x0lo), A.dptr(x0hi), A.iptr(cts), begin, end)
+    out_c = A.HullOut(A.dptr(d_lo.data_ptr()), A.dptr(d_hi.data_ptr()), A.iptr(d_div.data_ptr()),
+                      A.iptr(d_nb.data_ptr()), A.lptr(d_key.data_ptr()))
+    net = ctx.upload(spec.controller)
+
+    def step():
+        ctx.check(ctx._lib.reach_cl_split_hull(ctx.handle, net, C.byref(cs), C.byref(args_c), C.byref(out_c),
+                                               A.REACH_FLAG_DEVICE_PTRS), "reach_cl_split_hull")
+        if world > 1:
+            lo_ = torch.where(torch.isnan(d_lo), torch.full_like(d_lo, float("inf")), d_lo)
+            dist.all_reduce(lo_, op=dist.ReduceOp.MIN)
+            dist.all_reduce(d_hi, op=dist.ReduceOp.MAX)
+            dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
+            dist.all_reduce(d_nb, op=dist.ReduceOp.MIN)
+            d_lo.copy_(lo_)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    reps = max(3, min(args.steps, 5))
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ctx.kernel_time()
+    ms = []
+    for _ in range(reps):
+        ev0.record(stream)
+        step()
+        ev1.record(stream)
+        ev1.synchronize()
+        ms.append(ev0.elapsed_time(ev1))
+    kern_ms, kern_n = ctx.kernel_time()
+    t = float(np.mean(ms))
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    steps_total = per_rank * world * (T - 1)
+    fl = ct_flops_per_step()
+    tf_fma, _ = ctx.fp64_peak()
+    ach = fl * per_rank * (T - 1) / (t / 1e3) / 1e12
+    out = {"workload": "c2_quadrotor (BASELINE configs[1]): reach_with_splitting(cl_reach), 12-D quadrotor_ode + "
+                       "15->64x3->4 tanh controller, rpy:4096 sub-boxes per GPU, 10 control x 5 flowpipe steps, "
+                       "h=0.01, order 2, window 4",
+           "sub_boxes_per_gpu": per_rank, "ms_per_sweep": t, "reach_steps_per_s": steps_total / (t / 1e3),
+           "launches_per_sweep": 2 * spec.ctl_steps + 2,
+           "roofline": {"bound": "fp64", "achieved": ach, "peak": tf_fma, "unit": "TFLOP/s", "frac": ach / tf_fma,
+                        "flops_per_reach_step": fl,
+                        "note": "algorithmic flops of the reference's TMExpr op sequence (bench.ct_flops_per_step); "
+                                "the kernel is issue/latency-bound (profiles/r01_c2_summary.md)"}}
+    if rank == 0 and world == 1:
+        try:
+            from oracle_bind import oracle_cl_split_hull, ref_available, ref_cl_split_hull, ref_lib
+            g = cl_split_hull(spec, (w.x0_lo, w.x0_hi), plan, 2040, 2056, ctx=_host_ctx(ctx))
+            e = oracle_cl_split_hull(spec, w.x0_lo, w.x0_hi, plan, 2040, 2056)
+            scale = np.maximum(np.maximum(np.abs(e.lo), np.abs(e.hi - e.lo)), 1e-300)
+            rel = float(max(np.max(np.abs(g.lo - e.lo) / scale), np.max(np.abs(g.hi - e.hi) / scale)))
+            out["parity"] = {"parts": 16, "max_rel_diff_vs_oracle": rel, "tolerance": 1e-9,
+                             "ok": bool(rel <= 1e-9 and g.n_boxes == e.n_boxes)}
+            if ref_available() and not args.no_cpu_baseline:
+                lib = ref_lib()
+                lib.ref_hardware_threads.restype = C.c_int
+                cores = int(lib.ref_hardware_threads())
+                parts = int(min(per_rank, max(64, cores * 24)))
+                t0 = time.perf_counter()
+                ref_cl_split_hull(spec, w.x0_lo, w.x0_hi, plan, 0, parts, threads=0)
+                dt = time.perf_counter() - t0
+                out["cpu_baseline"] = {"value": parts * (T - 1) / dt, "unit": UNIT, "cores": cores,
+                                       "kind": "reference",
+                                       "sample": f"{parts} of {per_rank} sub-boxes x {T - 1} steps through the "
+                                                 f"reference cl_reach / reach_with_splitting pieces (oracle/_ref), "
+                                                 f"{dt:.2f} s"}
+        except Exception as ex:  # noqa: BLE001
+            out["check_error"] = str(ex)
+    ctx.set_stream(stream.cuda_stream)
+    return out
+
+
+def _host_ctx(ctx):
+    ctx.set_stream(None)
+    return ctx
 
 
 def run_reference(args):
@@ -409,6 +535,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(w, args.cpu_sample_parts or auto_cpu_parts())
 
+    # ---- C2: the continuous-time quadrotor closed loop (BASELINE configs[1])
+    ct = None if args.no_ct else ct_sweep(args, ctx, world, rank, dev, barrier, stream)
+
     # ---- the metric's second half: ms per reachability-aware MPC replan (BASELINE configs[2])
     mpc = None if args.no_mpc else mpc_replan(args, ctx, world, rank, dev, barrier)
 
@@ -423,7 +552,7 @@ def main():
                            "parallelism": f"dp{world}"},
                 "roofline": roof, "cpu_baseline": cb,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-                "gpu_launches": launches, "clocks": clk, "parity": parity, "mpc_replan": mpc,
+                "gpu_launches": launches, "clocks": clk, "parity": parity, "ct_quadrotor": ct, "mpc_replan": mpc,
                 "bit_exact_vs_reference": "ReLU path: identical operation order and roundings (tests/test_gpu_dt.py)"}
         print(json.dumps(line))
     if world > 1:

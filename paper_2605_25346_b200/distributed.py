@@ -2,8 +2,9 @@
 
 The batch shards naturally: sub-boxes of a split plan or MPC
 candidates are independent.  The only exchanges are
-  * the per-step hull of reach_with_splitting: one all-reduce (min on lo, max
-    on hi, min on the failure key / box count, max on the box-diverged flags);
+  * the per-step hull of reach_with_splitting (dt_reach or cl_reach engine):
+    one all-reduce (min on lo, max on hi, min on the failure key / box count,
+    max on the box-diverged flags);
   * CEM selection: one all-gather of each rank's (objective, ok) slice per
     iteration, after which every rank runs the identical stable sort / refit
     (every rank draws the same sampling stream, mpc.hpp:290-299).
@@ -99,6 +100,19 @@ def sharded_split_hull(sys, x0, plan, actions, prm, group=None,
             return reach_split_hull(sys_, x0_, plan_, acts_, prm_, part_begin=begin, part_end=end)
     res = evaluate(sys, x0, plan, actions, prm, b, e)
     return allreduce_hull(res, group)
+
+
+def sharded_cl_split_hull(spec, x0, plan, group=None, evaluate: Optional[Callable] = None):
+    """reach_with_splitting(cl_reach) over all ranks (C2): contiguous part ranges, one all-reduce."""
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    b, e = shard_range(plan.total_parts(), rank, world)
+    if evaluate is None:
+        from .api import cl_split_hull
+
+        def evaluate(spec_, x0_, plan_, begin, end):
+            return cl_split_hull(spec_, x0_, plan_, part_begin=begin, part_end=end)
+    return allreduce_hull(evaluate(spec, x0, plan, b, e), group)
 
 
 def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = None):

@@ -36,7 +36,7 @@ def _worker(rank, world, port, q):
     from mpc_cases import small_cem
     from oracle_bind import oracle_plan_eval_batch, oracle_split_hull
     from paper_2605_25346_b200.api import DTReachParams, DTSystem, SplitPlan
-    from paper_2605_25346_b200.distributed import sharded_plan_cem, sharded_split_hull
+    from paper_2605_25346_b200.distributed import sharded_cl_split_hull, sharded_plan_cem, sharded_split_hull
     from paper_2605_25346_b200.workloads import residual_relu_dynamics
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -58,7 +58,13 @@ def _worker(rank, world, port, q):
         def ev_plan(p, x, a):
             return oracle_plan_eval_batch(p, x, a)
         best, obj, be, hist = sharded_plan_cem(prob, cfg, x0, evaluate=ev_plan)
-        q.put((rank, h.lo, h.hi, h.n_boxes, h.fail_key, best, obj, be, hist))
+
+        from ct_cases import ct_split_case
+        from oracle_bind import oracle_cl_split_hull
+        spec, clo, chi, cplan = ct_split_case()
+        ch = sharded_cl_split_hull(spec, (clo, chi), cplan,
+                                   evaluate=lambda s_, x_, p_, b_, e_: oracle_cl_split_hull(s_, x_[0], x_[1], p_, b_, e_))
+        q.put((rank, h.lo, h.hi, h.n_boxes, h.fail_key, best, obj, be, hist, ch.lo, ch.hi, ch.n_boxes, ch.fail_key))
     finally:
         dist.destroy_process_group()
 
@@ -89,11 +95,18 @@ def test_two_rank_gloo_sharding_matches_single_process():
     full = oracle_split_hull(sys_, c - 0.01, c + 0.01, plan, acts, DTReachParams())
     prob, cfg, x0 = small_cem()
     eb, eo, eh, ebe = oracle_plan_cem(prob, cfg, x0)
-    for rank, lo, hi, nb, key, best, obj, be, hist in outs:
+    from ct_cases import ct_split_case
+    from oracle_bind import oracle_cl_split_hull
+    spec, clo, chi, cplan = ct_split_case()
+    cfull = oracle_cl_split_hull(spec, clo, chi, cplan)
+    for rank, lo, hi, nb, key, best, obj, be, hist, clo_r, chi_r, cnb, ckey in outs:
         k = full.n_boxes
         assert nb == full.n_boxes and key == full.fail_key
         assert same_bits(lo[:k], full.lo[:k]) and same_bits(hi[:k], full.hi[:k])
         assert same_bits(best, eb) and obj == eo and same_bits(hist, eh) and be == ebe
+        # C2's continuous-time hull sharded over two ranks: identical to the single-process hull
+        assert cnb == cfull.n_boxes and ckey == cfull.fail_key
+        assert same_bits(clo_r, cfull.lo) and same_bits(chi_r, cfull.hi)
 
 
 def test_combine_hulls_matches_full_oracle():
