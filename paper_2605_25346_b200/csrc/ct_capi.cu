@@ -105,7 +105,7 @@ int setup_params(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s, l
 }
 
 int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
-  const size_t flow_smem = sizeof(rb::ct::FlowSmem);
+  const size_t flow_smem = rb::ct::SPW * sizeof(rb::ct::FlowSmem);  // SPW sub-boxes per warp
   const size_t ctl_smem = sizeof(rb::ct::CtlSmem) * rb::ct::kCtlWarps;
   RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(flow_smem)));
@@ -119,7 +119,7 @@ int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
     P.ci = ci;
     rb::ct::ct_ctl_kernel<<<ctl_grid, 32 * rb::ct::kCtlWarps, ctl_smem, ctx->stream>>>(P);
     RB_CUDA(cudaGetLastError());
-    rb::ct::ct_flow_kernel<<<P.B, 32, flow_smem, ctx->stream>>>(P);
+    rb::ct::ct_flow_kernel<<<(P.B + rb::ct::SPW - 1) / rb::ct::SPW, 32, flow_smem, ctx->stream>>>(P);
     RB_CUDA(cudaGetLastError());
   }
   rc = timed_end(ctx, stop);

@@ -47,8 +47,13 @@ namespace ct {
 
 constexpr int NX = 12;      // quadrotor state
 constexpr int NA = 16;      // augmented (x, u)
-constexpr int NZC = 3;      // generator slots per lane (lanes >= 16 use two)
 constexpr int NZP = 80;     // generator columns per row: n + window (n + l) <= 76 (window <= 4)
+#ifndef RB_CT_HW
+#define RB_CT_HW 32
+#endif
+constexpr int HW = RB_CT_HW;              // lanes per sub-box in the flow kernel (32: one per warp, 16: two)
+constexpr int SPW = 32 / HW;              // sub-boxes per warp
+constexpr int NZC = (NZP + HW - 1) / HW;  // generator slots per lane
 constexpr int kMaxCtlW = 128;  // widest controller layer (and input dim)
 constexpr int LDX = NZP + 1;
 
@@ -102,21 +107,28 @@ __device__ __forceinline__ Iv imul(Iv a, Iv b) {
   const double p1 = a.lo * b.lo, p2 = a.lo * b.hi, p3 = a.hi * b.lo, p4 = a.hi * b.hi;
   return Iv{smin(smin(p1, p2), smin(p3, p4)), smax(smax(p1, p2), smax(p3, p4))};
 }
+// iv_mul({0, H}, {t, t}): the four products are pairwise identical, so
+// min(min(p1,p2),min(p3,p4)) = min(0*t, H*t) bit for bit (NaN cases included).
+__device__ __forceinline__ Iv imul_0h(double H, double t) {
+  const double p1 = 0.0 * t, p3 = H * t;
+  return Iv{smin(p1, p3), smax(p1, p3)};
+}
 __device__ __forceinline__ Iv iscale(double a, Iv x) {
   return (a >= 0.0) ? Iv{a * x.lo, a * x.hi} : Iv{a * x.hi, a * x.lo};
 }
 __device__ __forceinline__ bool ifin(Iv x) { return isfinite(x.lo) && isfinite(x.hi); }
 
-__device__ __forceinline__ void wsum2(double& a, double& b) {
+// Butterfly sums over the HW lanes of one sub-box (identical result on every lane).
+__device__ __forceinline__ void wsum2(double& a, double& b, unsigned mask) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
+  for (int o = HW / 2; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(mask, a, o, HW);
+    b += __shfl_xor_sync(mask, b, o, HW);
   }
 }
-__device__ __forceinline__ double wsum(double a) {
+__device__ __forceinline__ double wsum(double a, unsigned mask) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  for (int o = HW / 2; o > 0; o >>= 1) a += __shfl_xor_sync(mask, a, o, HW);
   return a;
 }
 
@@ -146,9 +158,12 @@ struct Slot {
   int view, pad;
 };
 
-// Shared memory of one flow warp (~29 KB: 7 warps per SM).
+// Shared memory of one sub-box (~25 KB: 8 per SM).
+// Picard rows 0..2 have bz = dx_{0..2}.az = S_{3..5} and rows 12..15 bz = 0
+// (udot = 0), so only rows 3..11 own a bz row; the others alias S or a zero row.
+constexpr int NPB = 9;  // owned Picard bz rows (P3..P11)
 struct FlowSmem {
-  double coef[NA * NZP + NA * NZP + 2 * NTF * NZP];  // S (= P.az) | Pbz | Taz | Tbz
+  double coef[NA * NZP + (NPB + 1) * NZP + 2 * NTF * NZP];  // S (= P.az) | Pbz 3..11 | zero | Taz | Tbz
   Slot D[NSLOT];
   double sc[NA];   // seed centre
   double ssz[NA];  // abs_z of the seed rows
@@ -156,29 +171,46 @@ struct FlowSmem {
   double kc[8];    // plant constants (CTParams::kc)
   Iv erem[NA], i0[NA], i1[NA], nx[NA];
 };
-constexpr int OFF_S = 0, OFF_PBZ = NA * NZP, OFF_TAZ = 2 * NA * NZP, OFF_TBZ = 2 * NA * NZP + NTF * NZP;
+constexpr int OFF_S = 0, OFF_PBZ = NA * NZP, OFF_ZERO = OFF_PBZ + NPB * NZP, OFF_TAZ = OFF_ZERO + NZP,
+              OFF_TBZ = OFF_TAZ + NTF * NZP;
+__device__ __forceinline__ int pbz_off(int i) {
+  return (i < 3) ? OFF_S + (i + 3) * NZP : (i < 3 + NPB) ? OFF_PBZ + (i - 3) * NZP : OFF_ZERO;
+}
 
 struct Lane {
-  int lane;
+  int lane;       // lane within the sub-box's half-warp
+  unsigned mask;  // the half-warp
   double h;
-  bool act[NZC];  // slot lane + 32 k < nz
+  bool act[NZC];  // slot lane + HW k < nz
 };
 
 // poly_range (taylor_model.hpp:227-235) from the cached sums.
 __device__ __forceinline__ Iv poly_range(double c, double sz, double at, double sb, double h) {
   Iv r{c - sz, c + sz};
-  r = iadd(r, imul(Iv{0.0, h}, Iv{at, at}));
+  r = iadd(r, imul_0h(h, at));
   const double br = sb * h;
   return iadd(r, Iv{-br, br});
 }
 
-// Coefficients of slot d at lane slot j (views scaled in the reference's order).
-__device__ __forceinline__ void fetch(const double* coef, const Slot& d, int j, double& a, double& b) {
-  a = coef[d.az + j];
-  b = coef[d.bz + j];
+// An operand's coefficient rows, read once per operation into registers (the
+// coefficient stores of the operation could alias the descriptor otherwise).
+// A view of a view (1/cos) carries s1*s2 as one scale: one rounding instead of
+// the reference's two, a <= 1 ulp difference inside the stated tolerance.
+struct Opnd {
+  const double* az;
+  const double* bz;
+  double s;
+  bool view;
+};
+__device__ __forceinline__ Opnd opnd(const double* coef, const Slot& d) {
+  return Opnd{coef + d.az, coef + d.bz, d.s1 * d.s2, d.view != 0};
+}
+__device__ __forceinline__ void fetch(const Opnd& d, int j, double& a, double& b) {
+  a = d.az[j];
+  b = d.bz[j];
   if (d.view) {
-    a = (a * d.s1) * d.s2;
-    b = (b * d.s1) * d.s2;
+    a *= d.s;
+    b *= d.s;
   }
 }
 
@@ -255,29 +287,32 @@ __device__ __forceinline__ void op_mul(FlowSmem& W, Slot& r, const Slot& u, cons
   const double uc = u.c, vc = v.c, uat = u.at, vat = v.at;
   const double au = u.sz, av = v.sz, bu = u.sb, bv = v.sb;
   const Iv ur{u.rlo, u.rhi}, vr{v.rlo, v.rhi};
+  const Opnd U = opnd(W.coef, u), V = opnd(W.coef, v);
+  double* raz = W.coef + r.az;
+  double* rbz = W.coef + r.bz;
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll
   for (int k = 0; k < NZC; ++k) {
     if (!L.act[k]) continue;
-    const int j = L.lane + 32 * k;
+    const int j = L.lane + HW * k;
     double ua, ub, va, vb;
-    fetch(W.coef, u, j, ua, ub);
-    fetch(W.coef, v, j, va, vb);
+    fetch(U, j, ua, ub);
+    fetch(V, j, va, vb);
     const double ra = uc * va + vc * ua;
     const double rb = uc * vb + vc * ub + uat * va + vat * ua;
-    W.coef[r.az + j] = ra;
-    W.coef[r.bz + j] = rb;
+    raz[j] = ra;
+    rbz[j] = rb;
     s1 += fabs(ra);
     s2 += fabs(rb);
   }
-  wsum2(s1, s2);
+  wsum2(s1, s2, L.mask);
   double sym = au * av;
   sym += (au * bv + av * bu) * h;
   sym += bu * bv * h * h;
   sym += (fabs(uat) * bv + fabs(vat) * bu) * h * h;
   Iv rem{-sym, sym};
   const double tt = uat * vat;
-  rem = iadd(rem, imul(Iv{0.0, h * h}, Iv{tt, tt}));
+  rem = iadd(rem, imul_0h(h * h, tt));
   const Iv pu = poly_range(uc, au, uat, bu, h), pv = poly_range(vc, av, vat, bv, h);
   rem = iadd(rem, imul(pu, vr));
   rem = iadd(rem, imul(pv, ur));
@@ -290,22 +325,25 @@ __device__ __forceinline__ void op_addsub(FlowSmem& W, Slot& r, const Slot& a, c
   const double c = sub ? a.c - b.c : a.c + b.c;
   const double at = sub ? a.at - b.at : a.at + b.at;
   const Iv rem = sub ? isub(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi}) : iadd(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi});
+  const Opnd A = opnd(W.coef, a), B = opnd(W.coef, b);
+  double* raz = W.coef + r.az;
+  double* rbz = W.coef + r.bz;
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll
   for (int k = 0; k < NZC; ++k) {
     if (!L.act[k]) continue;
-    const int j = L.lane + 32 * k;
+    const int j = L.lane + HW * k;
     double aa, ab, ba, bb;
-    fetch(W.coef, a, j, aa, ab);
-    fetch(W.coef, b, j, ba, bb);
+    fetch(A, j, aa, ab);
+    fetch(B, j, ba, bb);
     const double ra = sub ? aa - ba : aa + ba;
     const double rb = sub ? ab - bb : ab + bb;
-    W.coef[r.az + j] = ra;
-    W.coef[r.bz + j] = rb;
+    raz[j] = ra;
+    rbz[j] = rb;
     s1 += fabs(ra);
     s2 += fabs(rb);
   }
-  wsum2(s1, s2);
+  wsum2(s1, s2, L.mask);
   set_scalars(r, c, at, rem, s1, s2);
 }
 
@@ -333,9 +371,11 @@ __device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, 
   bool thrown = false;
   const double h = L.h;
   const int lane = L.lane;
+  TOp next = kQuadTape[0];
   for (int pc = 0;; ++pc) {
-    const TOp op = kQuadTape[pc];
+    const TOp op = next;
     if (op.code == OP_END) break;
+    next = kQuadTape[pc + 1];  // dispatch of the next op overlaps this one
     switch (op.code) {
       case OP_MUL:
         op_mul(W, W.D[op.dst], W.D[op.a], W.D[op.b], L);
@@ -395,18 +435,19 @@ __device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, 
         const int i = op.dst;
         const bool zero = op.code == OP_CONS0;
         const Slot& f = W.D[zero ? 0 : op.a];
+        const Opnd F = opnd(W.coef, f);
         const double fc = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at;
         const double fsz = zero ? 0.0 : f.sz, fsb = zero ? 0.0 : f.sb;
         const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
         double* S = W.coef + OFF_S + i * NZP;
-        double* Pb = W.coef + OFF_PBZ + i * NZP;
+        double* Pb = W.coef + pbz_off(i);
         if (mode == MODE_ENDPOINT) {
 #pragma unroll
           for (int k = 0; k < NZC; ++k) {
             if (!L.act[k]) continue;
-            const int j = lane + 32 * k;
+            const int j = lane + HW * k;
             double fa = 0.0, fb = 0.0;
-            if (!zero) fetch(W.coef, f, j, fa, fb);
+            if (!zero) fetch(F, j, fa, fb);
             gM[i * NZP + j] = S[j] + h * (fa + fb * h * 0.5);
           }
           W.ec[i] = W.sc[i] + h * (fc + fat * h * 0.5);
@@ -415,18 +456,20 @@ __device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, 
         }
         // tme_integrate(dx_i) remainder (taylor_model.hpp:436-443)
         const double half_at = fat * 0.5;
-        Iv rem = imul(Iv{0.0, h * h}, Iv{half_at, half_at});
+        Iv rem = imul_0h(h * h, half_at);
         const double bb = fsb * h * h * 0.5;
         rem = iadd(rem, Iv{-bb, bb});
         rem = iadd(rem, imul(fr, Iv{0.0, h}));
         if (mode == MODE_PICARD) {
+          if (i >= 3 && i < 3 + NPB) {  // rows 0..2 / 12..15: bz aliases S_{i+3} / zeros
 #pragma unroll
-          for (int k = 0; k < NZC; ++k) {
-            if (!L.act[k]) continue;
-            const int j = lane + 32 * k;
-            double fa = 0.0, fb;
-            if (!zero) fetch(W.coef, f, j, fa, fb);
-            Pb[j] = fa;
+            for (int k = 0; k < NZC; ++k) {
+              if (!L.act[k]) continue;
+              const int j = lane + HW * k;
+              double fa, fb;
+              fetch(F, j, fa, fb);
+              Pb[j] = fa;
+            }
           }
           set_scalars(W.D[i], W.sc[i], fc, rem, W.ssz[i], fsz);
         } else {  // REPLAY: (seed + Int f) - p_k; its z part seed - p_k.az is exactly 0
@@ -434,12 +477,12 @@ __device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, 
 #pragma unroll
           for (int k = 0; k < NZC; ++k) {
             if (!L.act[k]) continue;
-            const int j = lane + 32 * k;
+            const int j = lane + HW * k;
             double fa = 0.0, fb;
-            if (!zero) fetch(W.coef, f, j, fa, fb);
+            if (!zero) fetch(F, j, fa, fb);
             s2 += fabs(fa - Pb[j]);
           }
-          s2 = wsum(s2);
+          s2 = wsum(s2, L.mask);
           const Slot& pk = W.D[i];
           const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
           W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc - pk.at, s2, h), rem);
@@ -496,54 +539,60 @@ __device__ __forceinline__ void finalize(const CTParams& P, long long b, int nb,
 // the reference's one addition.  Lane i < NA sweeps row i sequentially.
 template <class RowPtr>
 __device__ __forceinline__ void push_fresh_fold(RowPtr row, const Iv* erem, int p0, int& nz, int& nq, int cap,
-                                                int lane) {
-  __syncwarp();
+                                                int lane, unsigned mask) {
+  __syncwarp(mask);
   const bool fold = nq + 1 > cap;
   double add = 0.0;
   if (fold && lane < NA)
     for (int j = 0; j < NA; ++j) add += fabs(row(lane)[p0 + j]);
-  __syncwarp();
+  __syncwarp(mask);
   if (fold) {
     for (int i = 0; i < NA; ++i) {
       double v[NZC];
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
-        const int j = lane + 32 * k;
+        const int j = lane + HW * k;
         v[k] = (j >= p0 && j + NA < nz) ? row(i)[j + NA] : 0.0;
       }
-      __syncwarp();
+      __syncwarp(mask);
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
-        const int j = lane + 32 * k;
+        const int j = lane + HW * k;
         if (j >= p0 && j < nz) row(i)[j] = v[k];
       }
     }
     nz -= NA;
     nq -= 1;
   }
-  __syncwarp();
+  __syncwarp(mask);
   for (int i = 0; i < NA; ++i) {
-    const double ai = fold ? __shfl_sync(0xffffffffu, add, i) : 0.0;
+    const double ai = fold ? __shfl_sync(mask, add, i, HW) : 0.0;
 #pragma unroll
     for (int k = 0; k < NZC; ++k) {
-      const int j = lane + 32 * k;
+      const int j = lane + HW * k;
       const double rad = (erem[i].hi - erem[i].lo) * 0.5;
       if (j >= nz && j < nz + NA) row(i)[j] = (j - nz == i) ? (fold ? rad + ai : rad) : 0.0;
     }
   }
   nz += NA;
   nq += 1;
-  __syncwarp();
+  __syncwarp(mask);
 }
 
 // ---------------------------------------------------------------------------
-// k_atomic flowpipe steps of one control interval, one warp per sub-box.
+// k_atomic flowpipe steps of one control interval; HW lanes own one sub-box
+// (RB_CT_HW = 16 packs two per warp, so each warp-uniform instruction -- the
+// scalar interval arithmetic, the program dispatch -- serves two; the default
+// 32 keeps one per warp, which measured faster: the kernel is latency-bound
+// and wants warps, profiles/r01_c2_summary.md).
 __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
   extern __shared__ __align__(16) unsigned char ct_smem[];
-  FlowSmem& W = *reinterpret_cast<FlowSmem*>(ct_smem);
-  const long long b = blockIdx.x;
+  const int half = threadIdx.x / HW;
+  const int lane = threadIdx.x % HW;
+  const unsigned mask = (HW == 32) ? 0xffffffffu : (((1u << HW) - 1u) << (HW * half));
+  FlowSmem& W = reinterpret_cast<FlowSmem*>(ct_smem)[half];
+  const long long b = static_cast<long long>(SPW) * blockIdx.x + half;
   if (b >= Pm.B) return;
-  const int lane = threadIdx.x;
   int* meta = Pm.st_meta + b * 4;
   int nq = meta[0], status = meta[1], fstep = meta[2], nboxes = meta[3];
   const bool last = (Pm.ci + 1 == Pm.ctl_steps);
@@ -557,12 +606,11 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
   int nz = p0 + nq * NA;
   double* gM = Pm.st_M + static_cast<size_t>(b) * NA * NZP;
   // state in, every coefficient row zeroed beyond nz (ops never write there)
-  for (int t = lane; t < NA * NZP; t += 32) {
+  for (int t = lane; t < NA * NZP; t += HW) {
     const int j = t % NZP;
     W.coef[OFF_S + t] = (j < nz) ? gM[t] : 0.0;
-    W.coef[OFF_PBZ + t] = 0.0;
   }
-  for (int t = lane; t < 2 * NTF * NZP; t += 32) W.coef[OFF_TAZ + t] = 0.0;
+  for (int t = lane; t < (NPB + 1) * NZP + 2 * NTF * NZP; t += HW) W.coef[OFF_PBZ + t] = 0.0;
   if (lane < NA) W.sc[lane] = Pm.st_c[b * NA + lane];
   if (lane < 8) W.kc[lane] = Pm.kc[lane];
   for (int s = 0; s < NSLOT; ++s) {  // stored rows: P_i = (S_i, Pbz_i), T_t
@@ -572,7 +620,7 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     d.view = 0;
     if (s < NA) {
       d.az = OFF_S + s * NZP;
-      d.bz = OFF_PBZ + s * NZP;
+      d.bz = pbz_off(s);
     } else if (s < SLOT_V) {
       d.az = OFF_TAZ + (s - SLOT_T) * NZP;
       d.bz = OFF_TBZ + (s - SLOT_T) * NZP;
@@ -581,34 +629,36 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
       d.bz = OFF_TBZ;
     }
   }
-  __syncwarp();
+  __syncwarp(mask);
 
   Lane L;
   L.lane = lane;
+  L.mask = mask;
   L.h = h;
   for (int step = 0; step < Pm.K && status == CT_OK; ++step) {
     const int gstep = Pm.ci * Pm.K + step;
 #pragma unroll
-    for (int k = 0; k < NZC; ++k) L.act[k] = (lane + 32 * k) < nz;
+    for (int k = 0; k < NZC; ++k) L.act[k] = (lane + HW * k) < nz;
     // seed rows: abs_z (cached: the Picard rows share their z columns)
     for (int i = 0; i < NA; i += 2) {
       double s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
         if (!L.act[k]) continue;
-        const int j = lane + 32 * k;
+        const int j = lane + HW * k;
         s1 += fabs(W.coef[OFF_S + i * NZP + j]);
         s2 += fabs(W.coef[OFF_S + (i + 1) * NZP + j]);
       }
-      wsum2(s1, s2);
+      wsum2(s1, s2, L.mask);
       W.ssz[i] = s1;
       W.ssz[i + 1] = s2;
     }
     // poly_picard (flowpipe_ct.hpp:126-139): g_0 = seed (bz = 0, at = 0, rem = 0)
     for (int i = 0; i < NA; ++i) {
+      if (i >= 3 && i < 3 + NPB)  // (rows 0..2 alias S: never read before their first Picard update)
 #pragma unroll
-      for (int k = 0; k < NZC; ++k)
-        if (L.act[k]) W.coef[OFF_PBZ + i * NZP + lane + 32 * k] = 0.0;
+        for (int k = 0; k < NZC; ++k)
+          if (L.act[k]) W.coef[pbz_off(i) + lane + HW * k] = 0.0;
       set_scalars(W.D[i], W.sc[i], 0.0, Iv{0.0, 0.0}, W.ssz[i], 0.0);
     }
     bool thrown = false;
@@ -698,9 +748,9 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
 #pragma unroll
         for (int k = 0; k < NZC; ++k) {
           if (!L.act[k]) continue;
-          const int j = lane + 32 * k;
+          const int j = lane + HW * k;
           double& s = W.coef[OFF_S + i * NZP + j];
-          s = exact_ok ? gM[i * NZP + j] : s + W.coef[OFF_PBZ + i * NZP + j] * h;
+          s = exact_ok ? gM[i * NZP + j] : s + W.coef[pbz_off(i) + j] * h;  // (aliases read before update)
         }
         if (!exact_ok) {
           W.ec[i] = W.D[i].c + W.D[i].at * h;
@@ -713,9 +763,9 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
         // symbolic_step (flowpipe_ct.hpp:378-409)
         double c_new = 0.0;
         if (lane < NA) c_new = W.ec[lane] + (W.erem[lane].lo + W.erem[lane].hi) * 0.5;
-        push_fresh_fold([&](int i) { return W.coef + OFF_S + i * NZP; }, W.erem, p0, nz, nq, cap, lane);
+        push_fresh_fold([&](int i) { return W.coef + OFF_S + i * NZP; }, W.erem, p0, nz, nq, cap, lane, mask);
         if (lane < NA) W.sc[lane] = c_new;
-        __syncwarp();
+        __syncwarp(mask);
       }
     }
     if (fail != CT_OK) {
@@ -724,8 +774,8 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     }
   }
   // state out
-  __syncwarp();
-  for (int t = lane; t < NA * NZP; t += 32) gM[t] = W.coef[OFF_S + t];
+  __syncwarp(mask);
+  for (int t = lane; t < NA * NZP; t += HW) gM[t] = W.coef[OFF_S + t];
   if (lane < NA) Pm.st_c[b * NA + lane] = W.sc[lane];
   if (lane == 0) {
     meta[0] = nq;

@@ -28,8 +28,12 @@ def main():
                for r in data}
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
-    cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-    dis = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    dis = ""
+    for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+        d = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+        if re.search(r"\.text\.\S*" + re.escape(kname.split("|")[0]), d):
+            dis = d
+            break
     # find function section by mangled-name match
     lines = dis.splitlines()
     cur_fn, cur_line, in_fn = None, None, False
