@@ -14,6 +14,11 @@ N x 65,536 parts (first split count x N), each rank sweeps its own contiguous
 65,536 parts, and the per-step hull is combined with one NCCL all-reduce
 (min on lo / max on hi / min on the failure key), the path's only exchange.
 
+Extra legs in the same JSON line (one per remaining BASELINE config):
+ct_quadrotor (C2, continuous-time cl_reach sweep), c5_closed_loop (C5, 72-D DT
+closed loop), c1_closed_loop (C1 latency at batch 1), mpc_replan (C3, ms per
+replan) -- each with its CPU reference sample and parity note.
+
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 unmodified reference headers compiled -O2) on the host cores, each step a
 bounded sample of the same sweep.
@@ -49,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mpc", action="store_true", help="skip the C3 MPC replan leg")
     ap.add_argument("--no-ct", action="store_true", help="skip the C2 continuous-time closed-loop leg")
+    ap.add_argument("--no-cl", action="store_true", help="skip the C5 / C1 DT closed-loop legs")
     return ap.parse_args()
 
 
@@ -339,6 +345,98 @@ def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
     return out
 
 
+def c5_flops_per_step():
+    """SURVEY §8d formula for C5 (72-D, 3x256 ReLU dynamics + controller): controller
+    certification over nz = 5n + 2l = 396 generators, dynamics certification over the stacked
+    486, fold solve 6 n^3."""
+    def cert(n_i, n_o, hidden, nz):
+        w = [hidden[0] * n_i] + [hidden[i] * hidden[i - 1] for i in range(1, len(hidden))]
+        return 2 * n_o * sum(w) + 2 * n_o * n_i * nz + 4 * (n_i * (nz + n_i) + sum(w)) + 6 * n_o * sum(hidden)
+    return cert(72, 18, [256] * 3, 396) + cert(90, 72, [256] * 3, 486) + 6 * 72 ** 3
+
+
+def closed_loop_legs(args, ctx, world, rank, dev, barrier, stream):
+    """C5 (BASELINE configs[4]): 72-D DT closed loop, 1024 initial boxes x 20 steps per GPU (weak
+    scaling, no collective: independent samples).  C1 (configs[0]): the 4-D DT closed loop at
+    batch 1 -- a latency figure, timed on rank 0 only."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_25346_b200.api import dt_closed_loop_batch
+    from paper_2605_25346_b200.workloads import c1_closed_loop, c5_closed_loop
+    ctx.set_stream(None)
+    out = {}
+    w = c5_closed_loop()
+    B = w.x0_lo.shape[0]
+    for _ in range(2):
+        r = dt_closed_loop_batch(w.dyn, w.ctl, w.n, w.x0_lo, w.x0_hi, w.horizon, ctx=ctx)
+    barrier()
+    ctx.kernel_time()
+    reps = 2
+    for _ in range(reps):
+        r = dt_closed_loop_batch(w.dyn, w.ctl, w.n, w.x0_lo, w.x0_hi, w.horizon, ctx=ctx)
+    kern_ms, kern_n = ctx.kernel_time()
+    t = kern_ms / reps
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    tf_fma, tf_ma = ctx.fp64_peak()
+    fl = c5_flops_per_step()
+    ach = fl * B * w.horizon / (t / 1e3) / 1e12
+    c5 = {"workload": "c5_closed_loop (BASELINE configs[4]): 72-D DT closed loop, 90->256x3->72 ReLU dynamics + "
+                      "72->256x3->18 ReLU controller, 1024 boxes x H=20 per GPU, window 4",
+          "ms_per_batch": t, "reach_steps_per_s": B * world * w.horizon / (t / 1e3),
+          "ok": int((r.status == 0).sum()), "kernel": "rb::dt_wide_kernel<9,3>",
+          "roofline": {"bound": "fp64", "achieved": ach, "peak": tf_fma, "unit": "TFLOP/s", "frac": ach / tf_fma,
+                       "flops_per_reach_step": fl, "exact_mode_ceiling_tflops": tf_ma},
+          "parity": "bit-identical to the oracle / reference composition (tests/test_gpu_wide.py)"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle_bind import ref_available, ref_dtcl_batch, ref_lib
+            if ref_available():
+                lib = ref_lib()
+                lib.ref_hardware_threads.restype = C.c_int
+                cores = int(lib.ref_hardware_threads())
+                k = int(min(B, max(16, cores * 2)))
+                t0 = time.perf_counter()
+                ref_dtcl_batch(w.dyn, w.ctl, w.n, w.x0_lo[:k], w.x0_hi[:k], w.horizon, threads=0)
+                dt = time.perf_counter() - t0
+                c5["cpu_baseline"] = {"value": k * w.horizon / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+                                      "sample": f"{k} of {B} boxes x {w.horizon} steps through the reference "
+                                                f"composition (oracle/_ref), {dt:.2f} s"}
+        except Exception as ex:  # noqa: BLE001
+            c5["check_error"] = str(ex)
+    out["c5_closed_loop"] = c5
+    if rank == 0:
+        w1 = c1_closed_loop(batch=1)
+        for _ in range(3):
+            dt_closed_loop_batch(w1.dyn, w1.ctl, w1.n, w1.x0_lo, w1.x0_hi, w1.horizon, ctx=ctx)
+        lat = []
+        for _ in range(10):
+            t0 = time.perf_counter()
+            dt_closed_loop_batch(w1.dyn, w1.ctl, w1.n, w1.x0_lo, w1.x0_hi, w1.horizon, ctx=ctx)
+            lat.append(time.perf_counter() - t0)
+        c1 = {"workload": "c1_closed_loop (BASELINE configs[0]): 4-D DT closed loop, 6->64x2->4 ReLU dynamics + "
+                          "4->64x2->2 ReLU controller, one box, H=20",
+              "latency_ms_end_to_end": 1e3 * float(np.median(lat)),
+              "note": "batch 1 is latency-bound (SURVEY §8d): host call incl. copies, median of 10"}
+        if not args.no_cpu_baseline:
+            try:
+                from oracle_bind import ref_available, ref_dtcl_batch
+                if ref_available():
+                    ts = []
+                    for _ in range(5):
+                        t0 = time.perf_counter()
+                        ref_dtcl_batch(w1.dyn, w1.ctl, w1.n, w1.x0_lo, w1.x0_hi, w1.horizon, threads=1)
+                        ts.append(time.perf_counter() - t0)
+                    c1["cpu_reference_latency_ms"] = 1e3 * float(np.median(ts))
+            except Exception as ex:  # noqa: BLE001
+                c1["check_error"] = str(ex)
+        out["c1_closed_loop"] = c1
+    ctx.set_stream(stream.cuda_stream)
+    return out
+
+
 def _host_ctx(ctx):
     ctx.set_stream(None)
     return ctx
@@ -537,6 +635,8 @@ def main():
 
     # ---- C2: the continuous-time quadrotor closed loop (BASELINE configs[1])
     ct = None if args.no_ct else ct_sweep(args, ctx, world, rank, dev, barrier, stream)
+    # ---- C5 / C1: the DT closed loop at 72-D (throughput) and 4-D batch 1 (latency)
+    cl = {} if args.no_cl else closed_loop_legs(args, ctx, world, rank, dev, barrier, stream)
 
     # ---- the metric's second half: ms per reachability-aware MPC replan (BASELINE configs[2])
     mpc = None if args.no_mpc else mpc_replan(args, ctx, world, rank, dev, barrier)
@@ -552,7 +652,7 @@ def main():
                            "parallelism": f"dp{world}"},
                 "roofline": roof, "cpu_baseline": cb,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-                "gpu_launches": launches, "clocks": clk, "parity": parity, "ct_quadrotor": ct, "mpc_replan": mpc,
+                "gpu_launches": launches, "clocks": clk, "parity": parity, "ct_quadrotor": ct, **cl, "mpc_replan": mpc,
                 "bit_exact_vs_reference": "ReLU path: identical operation order and roundings (tests/test_gpu_dt.py)"}
         print(json.dumps(line))
     if world > 1:

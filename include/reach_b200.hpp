@@ -12,6 +12,10 @@
 //   ReachTube<double> (tube.hpp)                reach_b200::ReachTube
 //   dt_reach / dt_reach_batch                   reach_b200::dt_reach / dt_reach_batch
 //   SplitPlan / reach_with_splitting(dt_reach)  reach_b200::SplitPlan / reach_with_splitting
+//   QuadrotorParams (systems.hpp:16-20)         reach_b200::QuadrotorParams
+//   FlowpipeParams (flowpipe_ct.hpp:35-50)      reach_b200::FlowpipeParams
+//   ClosedLoopSpec / cl_reach (closed_loop.hpp) reach_b200::ClosedLoopSpec / cl_reach / cl_reach_batch
+//   reach_with_splitting(cl_reach)              reach_b200::reach_with_splitting_cl
 //
 // For code that already holds the reference's own types, see
 // reach_b200_reference.hpp (drop-in overloads taking reach:: types).
@@ -234,6 +238,148 @@ inline ReachTube reach_with_splitting(Context& ctx, const DTSystem& sys, const B
     t.boxes.push_back(std::move(box));
     t.t_lo.push_back(k);
     t.t_hi.push_back(k);
+    if (div[k]) t.diverged = true;
+  }
+  if (key != std::numeric_limits<int64_t>::max()) {
+    t.diverged = true;
+    t.failed_step = static_cast<int>(key >> 40);
+    t.failure_reason = "sub-box " + std::to_string((key >> 8) & 0xffffffffLL) + ": " +
+                       failure_reason(static_cast<int32_t>(key & 0xff));
+  }
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// Continuous-time closed loop (closed_loop.hpp:16-182).  The dynamics are an
+// analytic plant from systems.hpp evaluated on the device (VectorField's host
+// closures cannot run there): quadrotor_ode augmented by udot = 0 rows.
+struct QuadrotorParams {  // systems.hpp:16-20
+  double mass = 1.0, gravity = 9.81, jx = 0.01, jy = 0.01, jz = 0.02;
+};
+
+struct FlowpipeParams {  // flowpipe_ct.hpp:35-50
+  double h = 0.01;
+  int steps = 100;
+  int order = 2;
+  double eps_init = 1e-4;
+  int refine_rounds = 3;
+  double enlargement = 2.0;
+  int max_enlargements = 20;
+  int window = 4;
+};
+
+struct ClosedLoopSpec {  // closed_loop.hpp:16-44 (dynamics = the quadrotor plant)
+  QuadrotorParams plant;
+  MLPNet controller;
+  int n = 12, l = 4, ctl_steps = 1, k_atomic = 1;
+  std::vector<std::vector<double>> y_ref;
+  FlowpipeParams fp;
+  bool intervalize_boundary = false;
+};
+
+namespace detail {
+inline reach_cl_spec cl_c_spec(const ClosedLoopSpec& s, std::vector<double>& yr) {
+  reach_cl_spec c{};
+  c.plant = REACH_PLANT_QUADROTOR;
+  c.plant_params[0] = s.plant.mass;
+  c.plant_params[1] = s.plant.gravity;
+  c.plant_params[2] = s.plant.jx;
+  c.plant_params[3] = s.plant.jy;
+  c.plant_params[4] = s.plant.jz;
+  c.n = s.n;
+  c.l = s.l;
+  c.ctl_steps = s.ctl_steps;
+  c.k_atomic = s.k_atomic;
+  c.ref_dim = s.y_ref.empty() ? 0 : static_cast<int32_t>(s.y_ref.front().size());
+  if (!s.y_ref.empty() && static_cast<int>(s.y_ref.size()) != s.ctl_steps)
+    throw std::invalid_argument("ClosedLoopSpec: reference sequence length mismatch");
+  yr.clear();
+  for (const auto& v : s.y_ref) {
+    if (static_cast<int>(v.size()) != c.ref_dim) throw std::invalid_argument("ClosedLoopSpec: ragged reference");
+    yr.insert(yr.end(), v.begin(), v.end());
+  }
+  c.y_ref = yr.empty() ? nullptr : yr.data();
+  c.fp = reach_flowpipe_params{s.fp.h, s.fp.steps, s.fp.order, s.fp.eps_init, s.fp.refine_rounds,
+                               s.fp.enlargement, s.fp.max_enlargements, s.fp.window};
+  c.intervalize_boundary = s.intervalize_boundary ? 1 : 0;
+  return c;
+}
+inline void ct_times(ReachTube& t, int k, double h) {  // closed_loop.hpp:155, 172
+  t.t_lo.push_back(k == 0 ? 0.0 : (k - 1) * h);
+  t.t_hi.push_back(k == 0 ? 0.0 : k * h);
+}
+}  // namespace detail
+
+// cl_reach (closed_loop.hpp:76-182) for a batch of initial boxes (n dims);
+// tubes have up to 1 + ctl_steps * k_atomic boxes of n + l dims.
+inline std::vector<ReachTube> cl_reach_batch(Context& ctx, const ClosedLoopSpec& spec, const std::vector<Box>& x0s) {
+  std::vector<ReachTube> out(x0s.size());
+  if (x0s.empty()) return out;
+  std::vector<double> yr;
+  reach_cl_spec c = detail::cl_c_spec(spec, yr);
+  const int B = static_cast<int>(x0s.size()), n = spec.n, na = spec.n + spec.l;
+  const int T = 1 + spec.ctl_steps * spec.k_atomic;
+  std::vector<double> lo(static_cast<size_t>(B) * n), hi(lo.size());
+  for (int b = 0; b < B; ++b) {
+    if (static_cast<int>(x0s[b].size()) != n) throw std::invalid_argument("cl_reach: X0 dimension mismatch");
+    for (int d = 0; d < n; ++d) {
+      lo[static_cast<size_t>(b) * n + d] = x0s[b][d].lo;
+      hi[static_cast<size_t>(b) * n + d] = x0s[b][d].hi;
+    }
+  }
+  std::vector<double> olo(static_cast<size_t>(B) * T * na), ohi(olo.size());
+  std::vector<int32_t> nb(B), fs(B), st(B);
+  reach_tube_out o{olo.data(), ohi.data(), nb.data(), fs.data(), st.data()};
+  ctx.check(reach_cl_batch(ctx.raw(), ctx.upload(spec.controller), &c, B, lo.data(), hi.data(), &o, 0), "cl_reach");
+  for (int b = 0; b < B; ++b) {
+    ReachTube& t = out[b];
+    for (int k = 0; k < nb[b]; ++k) {
+      Box box(na);
+      for (int d = 0; d < na; ++d) {
+        const size_t i = (static_cast<size_t>(b) * T + k) * na + d;
+        box[d] = {olo[i], ohi[i]};
+      }
+      t.boxes.push_back(std::move(box));
+      detail::ct_times(t, k, spec.fp.h);
+    }
+    t.failed_step = fs[b];
+    t.diverged = st[b] != REACH_TUBE_OK;
+    t.failure_reason = st[b] != REACH_TUBE_OK ? failure_reason(st[b]) : "";
+  }
+  return out;
+}
+
+inline ReachTube cl_reach(Context& ctx, const ClosedLoopSpec& spec, const Box& x0) {
+  return cl_reach_batch(ctx, spec, {x0}).front();
+}
+
+// reach_with_splitting(cl_reach engine, x0, plan) (refine.hpp:121-160) on the device.
+inline ReachTube reach_with_splitting_cl(Context& ctx, const ClosedLoopSpec& spec, const Box& x0,
+                                         const SplitPlan& plan) {
+  const int n = spec.n, na = spec.n + spec.l, T = 1 + spec.ctl_steps * spec.k_atomic;
+  if (static_cast<int>(x0.size()) != n || static_cast<int>(plan.counts.size()) != n)
+    throw std::invalid_argument("SplitPlan: dimension mismatch");
+  std::vector<double> yr, lo(n), hi(n);
+  reach_cl_spec c = detail::cl_c_spec(spec, yr);
+  for (int d = 0; d < n; ++d) {
+    lo[d] = x0[d].lo;
+    hi[d] = x0[d].hi;
+  }
+  std::vector<int32_t> counts(plan.counts.begin(), plan.counts.end());
+  std::vector<double> olo(static_cast<size_t>(T) * na), ohi(olo.size());
+  std::vector<int32_t> div(T);
+  int32_t nb = 0;
+  int64_t key = 0;
+  reach_cl_split_args a{lo.data(), hi.data(), counts.data(), 0, 0};
+  reach_hull_out o{olo.data(), ohi.data(), div.data(), &nb, &key};
+  ctx.check(reach_cl_split_hull(ctx.raw(), ctx.upload(spec.controller), &c, &a, &o, 0),
+            "reach_with_splitting(cl_reach)");
+  ReachTube t;
+  for (int k = 0; k < nb; ++k) {
+    Box box(na);
+    for (int d = 0; d < na; ++d) box[d] = {olo[static_cast<size_t>(k) * na + d], ohi[static_cast<size_t>(k) * na + d]};
+    t.boxes.push_back(std::move(box));
+    detail::ct_times(t, k, spec.fp.h);
     if (div[k]) t.diverged = true;
   }
   if (key != std::numeric_limits<int64_t>::max()) {

@@ -15,8 +15,10 @@
 // tube.hpp:23-34), computed by the B200 kernels.
 #pragma once
 
+#include "reach/closed_loop.hpp"
 #include "reach/dt_reach.hpp"
 #include "reach/refine.hpp"
+#include "reach/systems.hpp"
 #include "reach_b200.hpp"
 
 namespace reach_b200 {
@@ -94,6 +96,42 @@ inline reach::ReachTube<double> reach_with_splitting_dt(Context& ctx, const reac
   SplitPlan p{plan.counts};
   DTReachParams q{prm.window, prm.rebuild_from_box};
   return to_reference(reach_with_splitting(ctx, from_reference(sys), from_reference(x0), p, actions, q));
+}
+
+// reach::cl_reach (closed_loop.hpp:76-182).  A ClosedLoopSpec's dynamics is a
+// host closure the device cannot run, so the caller names the plant it was
+// built from: spec.dynamics must be make_augmented_field(12, 4, quadrotor_ode
+// with `plant`) (fields.hpp:96-128), which the shape check below enforces.
+inline ClosedLoopSpec from_reference(const reach::ClosedLoopSpec<double>& spec, const reach::QuadrotorParams& plant) {
+  spec.validate();
+  if (spec.n != 12 || spec.l != 4 || spec.dynamics.n != 16)
+    throw std::invalid_argument("cl_reach: the device plant is quadrotor_ode (n = 12, l = 4)");
+  ClosedLoopSpec s;
+  s.plant = {plant.mass, plant.gravity, plant.jx, plant.jy, plant.jz};
+  s.controller = from_reference(spec.controller);
+  s.n = spec.n;
+  s.l = spec.l;
+  s.ctl_steps = spec.ctl_steps;
+  s.k_atomic = spec.k_atomic;
+  s.y_ref = spec.y_ref;
+  s.fp = {spec.fp.h, spec.fp.steps, spec.fp.order, spec.fp.eps_init, spec.fp.refine_rounds,
+          spec.fp.enlargement, spec.fp.max_enlargements, spec.fp.window};
+  s.intervalize_boundary = spec.intervalize_boundary;
+  return s;
+}
+
+inline reach::ReachTube<double> cl_reach(Context& ctx, const reach::ClosedLoopSpec<double>& spec,
+                                         const reach::QuadrotorParams& plant, const reach::IntervalBox<double>& x0) {
+  return to_reference(cl_reach(ctx, from_reference(spec, plant), from_reference(x0)));
+}
+
+// reach::reach_with_splitting with the cl_reach engine (refine.hpp:121-160)
+inline reach::ReachTube<double> reach_with_splitting_cl(Context& ctx, const reach::ClosedLoopSpec<double>& spec,
+                                                        const reach::QuadrotorParams& plant,
+                                                        const reach::IntervalBox<double>& x0,
+                                                        const reach::SplitPlan& plan) {
+  plan.validate(x0.size());
+  return to_reference(reach_with_splitting_cl(ctx, from_reference(spec, plant), from_reference(x0), SplitPlan{plan.counts}));
 }
 
 }  // namespace reach_b200

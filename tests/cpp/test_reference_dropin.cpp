@@ -6,7 +6,9 @@
 #include <cstdio>
 #include <vector>
 
+#include "reach/closed_loop.hpp"
 #include "reach/dt_reach.hpp"
+#include "reach/fields.hpp"
 #include "reach/refine.hpp"
 #include "reach/rng.hpp"
 #include "reach_b200_reference.hpp"
@@ -87,6 +89,60 @@ int main() {
     auto ref = reach_with_splitting([&](const Box& b) { return reach::dt_reach(sys, b, acts); }, x0, plan);
     auto got = reach_b200::reach_with_splitting_dt(gpu, sys, x0, plan, acts);
     failures += compare(ref, got, "reach_with_splitting");
+  }
+  // cl_reach with the quadrotor plant and a tanh controller (test_closed_loop.cpp:236-254 shape):
+  // CUDA libm + tree-reduced abs-sums, so bounds agree to rounding (rel. 1e-9), statuses exactly
+  {
+    QuadrotorParams prm;
+    Rng crng(7788);
+    ClosedLoopSpec<double> spec;
+    spec.n = 12;
+    spec.l = 4;
+    spec.ctl_steps = 4;
+    spec.k_atomic = 5;
+    spec.fp.h = 0.01;
+    spec.controller = random_mlp(crng, 15, {16}, 4, Act::Tanh, 0.4);
+    for (auto& w : spec.controller.layers.back().w.a) w *= 0.1;
+    spec.controller.layers.back().b[0] += prm.mass * prm.gravity;
+    auto plant = [prm](const auto& x, const auto& u, auto& dx) { quadrotor_ode(x, u, prm, dx); };
+    spec.dynamics = make_augmented_field<double>(12, 4, plant);
+    spec.y_ref.assign(4, Vec<double>{0.1, 0.0, 0.0});
+    Box x0(12);
+    for (int d = 0; d < 12; ++d) x0[d] = {d < 3 ? -0.3 : d < 6 ? -0.05 : -0.02, d < 3 ? 0.3 : d < 6 ? 0.05 : 0.02};
+    auto ref = reach::cl_reach(spec, x0);
+    auto got = reach_b200::cl_reach(gpu, spec, prm, x0);
+    int bad = (ref.steps() != got.steps() || ref.diverged != got.diverged || ref.failed_step != got.failed_step) ? 1 : 0;
+    double worst = 0.0;
+    for (int k = 0; !bad && k < ref.steps(); ++k)
+      for (int d = 0; d < 16; ++d) {
+        const auto& x = ref.boxes[k][d];
+        const auto& y = got.boxes[k][d];
+        const double scale = std::fmax(std::fmax(std::fabs(x.lo), std::fabs(x.hi)), x.hi - x.lo);
+        worst = std::fmax(worst, std::fmax(std::fabs(x.lo - y.lo), std::fabs(x.hi - y.hi)) / scale);
+        if (ref.t_lo[k] != got.t_lo[k] || ref.t_hi[k] != got.t_hi[k]) bad = 1;
+      }
+    if (bad || worst > 1e-9) {
+      std::printf("cl_reach: mismatch (bad=%d, max rel diff %.3e)\n", bad, worst);
+      ++failures;
+    }
+    SplitPlan plan;
+    plan.counts = std::vector<int>(12, 1);
+    plan.counts[6] = plan.counts[7] = 2;
+    auto href = reach_with_splitting([&](const Box& b) { return reach::cl_reach(spec, b); }, x0, plan);
+    auto hgot = reach_b200::reach_with_splitting_cl(gpu, spec, prm, x0, plan);
+    double hw = 0.0;
+    for (int k = 0; k < href.steps() && k < hgot.steps(); ++k)
+      for (int d = 0; d < 16; ++d) {
+        const auto& x = href.boxes[k][d];
+        const auto& y = hgot.boxes[k][d];
+        const double scale = std::fmax(std::fmax(std::fabs(x.lo), std::fabs(x.hi)), x.hi - x.lo);
+        hw = std::fmax(hw, std::fmax(std::fabs(x.lo - y.lo), std::fabs(x.hi - y.hi)) / scale);
+      }
+    if (href.steps() != hgot.steps() || hw > 1e-9) {
+      std::printf("reach_with_splitting(cl_reach): mismatch (%d/%d steps, max rel diff %.3e)\n", href.steps(),
+                  hgot.steps(), hw);
+      ++failures;
+    }
   }
   std::printf(failures ? "FAIL (%d)\n" : "OK: reference drop-in parity\n", failures);
   return failures ? 1 : 0;

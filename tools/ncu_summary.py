@@ -10,9 +10,11 @@ det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_o
 keys = ["Duration", "Registers Per Thread", "Achieved Occupancy", "Theoretical Occupancy", "Issue Slots Busy",
         "Executed Ipc Active", "Warp Cycles Per Issued Instruction", "No Eligible", "Active Warps Per Scheduler",
         "Eligible Warps Per Scheduler", "DRAM Throughput", "Dynamic Shared Memory Per Block", "L1/TEX Hit Rate"]
-for r in csv.reader(io.StringIO(det)):
-    if len(r) > 3 and r[-3] in keys:
-        print(f"{r[-3]:40s} {r[-1]} {r[-2]}")
+rows_d = list(csv.reader(io.StringIO(det)))
+hd = {h: i for i, h in enumerate(rows_d[0])}
+for r in rows_d[1:]:
+    if len(r) > hd["Metric Value"] and r[hd["Metric Name"]] in keys:
+        print(f"{r[hd['Metric Name']]:40s} {r[hd['Metric Value']]} {r[hd['Metric Unit']]}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
