@@ -370,11 +370,13 @@ def closed_loop_legs(args, ctx, world, rank, dev, barrier, stream):
     for _ in range(2):
         r = dt_closed_loop_batch(w.dyn, w.ctl, w.n, w.x0_lo, w.x0_hi, w.horizon, ctx=ctx)
     barrier()
+    ctx.enable_kernel_timing(True)
     ctx.kernel_time()
     reps = 2
     for _ in range(reps):
         r = dt_closed_loop_batch(w.dyn, w.ctl, w.n, w.x0_lo, w.x0_hi, w.horizon, ctx=ctx)
     kern_ms, kern_n = ctx.kernel_time()
+    ctx.enable_kernel_timing(False)
     t = kern_ms / reps
     if world > 1:
         tt = torch.tensor([t], dtype=torch.float64, device=dev)
