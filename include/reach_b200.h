@@ -321,6 +321,31 @@ typedef struct reach_cl_split_args {
 int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* spec,
                         const reach_cl_split_args* args, const reach_hull_out* out, int32_t flags);
 
+/* ----------------------------------------------------------------------- */
+/* Open-loop continuous-time flowpipe (ct_reach, flowpipe_ct.hpp:428-458) of */
+/* an analytic VectorField from fields.hpp: box 0 is X0, box k >= 1 covers  */
+/* [(k-1) h, k h]; the symbolic state's G0 is square, so fold_overflow uses  */
+/* the G0^-1 Q solve (flowpipe_ct.hpp:326-346, linalg.hpp:96-132).          */
+enum reach_ct_field {
+  REACH_FIELD_ZERO = 0,        /* zero_field(n) (fields.hpp:87-92): params unused */
+  REACH_FIELD_DIAG_LINEAR = 1, /* diag_linear_field(lambda) (fields.hpp:72-78): params = lambda[n] */
+  REACH_FIELD_ROTATION = 2,    /* rotation_field(w) (fields.hpp:80-85), n = 2: params = {w} */
+  REACH_FIELD_QUADROTOR = 3    /* quadrotor_field(prm, u) (fields.hpp:51-56), n = 12:
+                                  params = {mass, gravity, jx, jy, jz, u0, u1, u2, u3} */
+};
+
+typedef struct reach_field_desc {
+  int32_t kind; /* reach_ct_field */
+  int32_t n;
+  double params[16];
+} reach_field_desc;
+
+/* ct_reach for a batch of initial boxes [batch][n]; tubes of up to
+ * 1 + fp.steps boxes of n dims (lo/hi [batch][1 + steps][n]).
+ * Limits of the device family: n * (fp.window + 2) <= 80, n <= 16. */
+int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* field, const reach_flowpipe_params* fp, int32_t batch,
+                   const double* x0_lo, const double* x0_hi, const reach_tube_out* out, int32_t flags);
+
 #ifdef __cplusplus
 }
 #endif

@@ -188,14 +188,15 @@ static void tme_integrate(tme* r, const tme* u) {
 }
 
 /* ----------------------------------------------------------------------- */
-/* make_augmented_field(12, 4, quadrotor_ode) (fields.hpp:96-107,           */
-/* systems.hpp:24-64).  x: 16 rows; dx: 16 rows.  prm: mass, g, jx, jy, jz. */
-typedef struct { tme t[12]; } qscratch;
+/* quadrotor_ode (systems.hpp:24-64) on TM rows: x 12 state rows, u 4 input  */
+/* rows (the augmented (x, u) rows, fields.hpp:96-107, or held constants,    */
+/* fields.hpp:20-32), dx 12 rows.  prm: mass, g, jx, jy, jz.                 */
+typedef struct { tme t[12]; tme u[4]; } qscratch;
 
 /* Field evaluations so far (work accounting for the roofline, not part of the algorithm). */
 long long orc_ct_field_evals = 0;
 
-static void quad_field(const tme* x, tme* dx, const double* prm, qscratch* s, int* thrown) {
+static void quad_body(const tme* x, const tme* u, tme* dx, const double* prm, qscratch* s, int* thrown) {
   ++orc_ct_field_evals;
   const double mass = prm[0], grav = prm[1], jx = prm[2], jy = prm[3], jz = prm[4];
   const int nz = x[0].nz;
@@ -203,7 +204,6 @@ static void quad_field(const tme* x, tme* dx, const double* prm, qscratch* s, in
   tme *sphi = &s->t[0], *cphi = &s->t[1], *sth = &s->t[2], *cth = &s->t[3], *spsi = &s->t[4], *cpsi = &s->t[5];
   tme *a = &s->t[6], *t1 = &s->t[7], *t2 = &s->t[8], *t3 = &s->t[9], *ic = &s->t[10], *tth = &s->t[11];
   const tme *phi = &x[6], *theta = &x[7], *psi = &x[8], *p = &x[9], *q = &x[10], *r = &x[11];
-  const tme* u = &x[12];
   tme_sin(sphi, phi); tme_cos(cphi, phi);
   tme_sin(sth, theta); tme_cos(cth, theta);
   tme_sin(spsi, psi); tme_cos(cpsi, psi);
@@ -232,8 +232,41 @@ static void quad_field(const tme* x, tme* dx, const double* prm, qscratch* s, in
   tme_mul(t1, q, r); tme_smul(t1, (jy - jz) / jx, t1); tme_smul(t2, 1.0 / jx, &u[1]); tme_add(&dx[9], t1, t2);
   tme_mul(t1, p, r); tme_smul(t1, (jz - jx) / jy, t1); tme_smul(t2, 1.0 / jy, &u[2]); tme_add(&dx[10], t1, t2);
   tme_mul(t1, p, q); tme_smul(t1, (jx - jy) / jz, t1); tme_smul(t2, 1.0 / jz, &u[3]); tme_add(&dx[11], t1, t2);
-  for (int i = 12; i < 16; ++i) tme_const(&dx[i], 0.0, nz, h);
+  (void)nz; (void)h;
 }
+
+/* The fields of fields.hpp that run on the device. */
+#define CTF_QUAD_AUG 100 /* make_augmented_field(12, 4, quadrotor_ode): 16 rows */
+typedef struct { int kind; int n; const double* params; } ctfield;
+
+static void field_eval(const ctfield* F, const tme* x, tme* dx, qscratch* s, int* thrown) {
+  const int nz = x[0].nz;
+  const double h = x[0].h;
+  switch (F->kind) {
+    case CTF_QUAD_AUG: /* fields.hpp:96-107: (x, u) rows, udot = 0 */
+      quad_body(x, &x[12], dx, F->params, s, thrown);
+      for (int i = 12; i < 16; ++i) tme_const(&dx[i], 0.0, nz, h);
+      break;
+    case REACH_FIELD_QUADROTOR: /* quadrotor_field (fields.hpp:51-56): held input rows tme_const(u) */
+      for (int k = 0; k < 4; ++k) tme_const(&s->u[k], F->params[5 + k], nz, h);
+      quad_body(x, s->u, dx, F->params, s, thrown);
+      break;
+    case REACH_FIELD_ZERO: /* dx.assign(n, x[0] * 0.0) (fields.hpp:90) */
+      ++orc_ct_field_evals;
+      for (int i = 0; i < F->n; ++i) tme_smul(&dx[i], 0.0, &x[0]);
+      break;
+    case REACH_FIELD_DIAG_LINEAR: /* diag_linear_ode (systems.hpp:154-159) */
+      ++orc_ct_field_evals;
+      for (int i = 0; i < F->n; ++i) tme_smul(&dx[i], F->params[i], &x[i]);
+      break;
+    case REACH_FIELD_ROTATION: /* rotation_ode (systems.hpp:162-167) */
+      ++orc_ct_field_evals;
+      tme_smul(&dx[0], -F->params[0], &x[1]);
+      tme_smul(&dx[1], F->params[0], &x[0]);
+      break;
+  }
+}
+
 
 /* ----------------------------------------------------------------------- */
 /* Symbolic state (flowpipe_ct.hpp:286-300): x = c + [G0 | Q1 .. Qnq] y.    */
@@ -246,22 +279,59 @@ typedef struct {
 
 static int ct_nz(const ctsym* s) { int z = s->p0; for (int q = 0; q < s->nq; ++q) z += s->wid[q]; return z; }
 
-/* fold_overflow (flowpipe_ct.hpp:317-350).  In cl_reach G0 is (n+l) x n,
- * never square, so the fold is always the box-hull fallback (:347-348). */
+/* fold_overflow (flowpipe_ct.hpp:317-350).  Square G0 (ct_reach): absorb the
+ * oldest block into G0's frame when G0^-1 Q is bounded (:326-346); else (and
+ * always in cl_reach, where G0 is (n+l) x n) the box-hull fallback (:347-348). */
 static void ct_fold(ctsym* s) {
   const int cap = s->window > 0 ? s->window : 1;
+  const int n = s->na;
   while (s->nq > cap) {
     const int w = s->wid[0];
     int off_new = s->p0;
     for (int q = 0; q + 1 < s->nq; ++q) off_new += s->wid[q];
-    for (int i = 0; i < s->na; ++i) {
+    int folded = 0;
+    if (s->p0 == n) {
+      double g0[CT_MAXR * CT_MAXR], a[CT_MAXR * CT_MAXR], x[CT_MAXR * CT_MAXR], e[CT_MAXR * CT_MAXR], r[CT_MAXR];
+      for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) g0[i * n + j] = s->M[i][j];
+        for (int j = 0; j < w; ++j) a[i * w + j] = s->M[i][n + j];
+      }
+      if (orc_i_mat_solve(n, w, g0, a, x)) {
+        double worst = 0.0;
+        for (int j = 0; j < n; ++j) {
+          double rs = 0.0;
+          for (int k = 0; k < w; ++k) rs += fabs(x[j * w + k]);
+          r[j] = rs * (1.0 + 1e-12);
+          worst = smax(worst, r[j]);
+        }
+        if (worst <= 1.0) {
+          for (int i = 0; i < n; ++i) {
+            for (int j = 0; j < w; ++j) e[i * w + j] = 0.0;
+            for (int k = 0; k < n; ++k)
+              for (int j = 0; j < w; ++j) e[i * w + j] += g0[i * n + k] * x[k * w + j];
+          }
+          for (int i = 0; i < n; ++i)
+            for (int j = 0; j < w; ++j) e[i * w + j] -= a[i * w + j];
+          for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) s->M[i][j] *= 1.0 + r[j];
+          for (int i = 0; i < n; ++i) {
+            double rs = 0.0;
+            for (int j = 0; j < w; ++j) rs += fabs(e[i * w + j]);
+            s->M[i][off_new + i] += rs * (1.0 + 1e-12);
+          }
+          folded = 1;
+        }
+      }
+    }
+    for (int i = 0; !folded && i < s->na; ++i) {
       double r = 0.0;
       for (int j = 0; j < w; ++j) r += fabs(s->M[i][s->p0 + j]);
       s->M[i][off_new + i] += r;
     }
     const int total = ct_nz(s);
-    for (int i = 0; i < s->na; ++i)
-      memmove(&s->M[i][s->p0], &s->M[i][s->p0 + w], sizeof(double) * (size_t)(total - s->p0 - w));
+    const int keep = total - s->p0 - w;
+    for (int i = 0; keep > 0 && i < s->na; ++i)
+      memmove(&s->M[i][s->p0], &s->M[i][s->p0 + w], sizeof(double) * (size_t)keep);
     memmove(s->wid, s->wid + 1, sizeof(int) * (size_t)(s->nq - 1));
     s->nq -= 1;
   }
@@ -304,10 +374,10 @@ typedef struct {
 } ctstep;
 
 /* replay (flowpipe_ct.hpp:154-165): I1 induced by candidate remainder i0. */
-static int ct_replay(ctwork* w, const double* prm, int na, const iv* i0, iv* i1) {
+static int ct_replay(ctwork* w, const ctfield* F, int na, const iv* i0, iv* i1) {
   int thrown = 0;
   for (int i = 0; i < na; ++i) { w->cand[i] = w->pk[i]; w->cand[i].rem = i0[i]; }
-  quad_field(w->cand, w->fg, prm, &w->q, &thrown);
+  field_eval(F, w->cand, w->fg, &w->q, &thrown);
   if (thrown) return 1;
   for (int i = 0; i < na; ++i) {
     tme_integrate(&w->d1, &w->fg[i]);
@@ -326,11 +396,10 @@ static int box_subset(const iv* in, const iv* out, int n) {
 
 /* Returns REACH_TUBE_OK, or the failure status.  Fills st (segment remainder
  * i1, endpoint) and the step box lo/hi (tm_eval_interval, taylor_model.hpp:73-97). */
-static int ct_flow_step(const ctsym* s, const reach_cl_spec* sp, ctwork* w, ctstep* st, double* blo, double* bhi,
-                        int* box_fin) {
+static int ct_flow_step(const ctsym* s, const reach_flowpipe_params* fp, const ctfield* F, ctwork* w, ctstep* st,
+                        double* blo, double* bhi, int* box_fin) {
   const int na = s->na, nz = ct_nz(s);
-  const double h = sp->fp.h;
-  const double* prm = sp->plant_params;
+  const double h = fp->h;
   /* seed rows (rows_from_linear_tm, flowpipe_ct.hpp:89-100) */
   for (int i = 0; i < na; ++i) {
     tme_const(&w->seed[i], s->c[i], nz, h);
@@ -338,9 +407,9 @@ static int ct_flow_step(const ctsym* s, const reach_cl_spec* sp, ctwork* w, ctst
   }
   /* poly_picard (flowpipe_ct.hpp:126-139) */
   for (int i = 0; i < na; ++i) w->g[i] = w->seed[i];
-  for (int it = 0; it < sp->fp.order; ++it) {
+  for (int it = 0; it < fp->order; ++it) {
     int thrown = 0;
-    quad_field(w->g, w->fg, prm, &w->q, &thrown);
+    field_eval(F, w->g, w->fg, &w->q, &thrown);
     if (thrown) return REACH_TUBE_TME_INV;
     for (int i = 0; i < na; ++i) {
       tme_integrate(&w->d1, &w->fg[i]);
@@ -354,22 +423,22 @@ static int ct_flow_step(const ctsym* s, const reach_cl_spec* sp, ctwork* w, ctst
   for (int i = 0; i < na; ++i) w->pk[i] = w->g[i];
   /* remainder_picard (flowpipe_ct.hpp:144-276) */
   iv i0[CT_MAXR], i1[CT_MAXR], nx[CT_MAXR];
-  for (int i = 0; i < na; ++i) { i0[i] = ivp(-sp->fp.eps_init, sp->fp.eps_init); i1[i] = ivp(0.0, 0.0); }
+  for (int i = 0; i < na; ++i) { i0[i] = ivp(-fp->eps_init, fp->eps_init); i1[i] = ivp(0.0, 0.0); }
   int accepted = 0;
-  for (int attempt = 0; attempt <= sp->fp.max_enlargements; ++attempt) {
-    int threw = ct_replay(w, prm, na, i0, nx);
+  for (int attempt = 0; attempt <= fp->max_enlargements; ++attempt) {
+    int threw = ct_replay(w, F, na, i0, nx);
     if (!threw) memcpy(i1, nx, sizeof(iv) * (size_t)na);
     if (!threw && box_finite(i1, na) && box_subset(i1, i0, na)) { accepted = 1; break; }
     for (int i = 0; i < na; ++i) {
       iv induced = threw ? ivp(0.0, 0.0) : i1[i];
       iv hull = iv_valid(induced) ? iv_hull(i0[i], induced) : i0[i];
-      double mid = iv_mid(hull), rad = iv_rad(hull) * sp->fp.enlargement;
+      double mid = iv_mid(hull), rad = iv_rad(hull) * fp->enlargement;
       i0[i] = ivp(mid - rad, mid + rad);
     }
   }
   if (!accepted) return REACH_TUBE_REMAINDER;
-  for (int round = 0; round < sp->fp.refine_rounds; ++round) {
-    if (ct_replay(w, prm, na, i1, nx)) break;
+  for (int round = 0; round < fp->refine_rounds; ++round) {
+    if (ct_replay(w, F, na, i1, nx)) break;
     if (!(box_finite(nx, na) && box_subset(nx, i1, na))) break;
     memcpy(i1, nx, sizeof(iv) * (size_t)na);
   }
@@ -379,7 +448,7 @@ static int ct_flow_step(const ctsym* s, const reach_cl_spec* sp, ctwork* w, ctst
   {
     int thrown = 0;
     for (int i = 0; i < na; ++i) { w->cand[i] = w->pk[i]; w->cand[i].rem = i1[i]; }
-    quad_field(w->cand, w->fg, prm, &w->q, &thrown);
+    field_eval(F, w->cand, w->fg, &w->q, &thrown);
     if (thrown) exact_ok = 0;
     const double hh = h;
     for (int i = 0; exact_ok && i < na; ++i) {
@@ -532,9 +601,10 @@ static int cl_one(const net_t* ctl, const reach_cl_spec* sp, const double* x0lo,
       ct_box(s, lo, hi);
       nb = 1;
     }
+    const ctfield F = {CTF_QUAD_AUG, na, sp->plant_params};
     for (int j = 0; j < K; ++j) {
       int fin;
-      int rc = ct_flow_step(s, sp, w, st, lo + (size_t)nb * na, hi + (size_t)nb * na, &fin);
+      int rc = ct_flow_step(s, &sp->fp, &F, w, st, lo + (size_t)nb * na, hi + (size_t)nb * na, &fin);
       if (rc != REACH_TUBE_OK) { *failed_step = gstep; *status = rc; goto done; }
       nb += 1;
       gstep += 1;
@@ -619,5 +689,50 @@ int orc_cl_split_hull(const reach_net_desc* ctl_desc, const reach_cl_spec* sp, c
   out->n_boxes[0] = steps;
   out->fail_key[0] = key;
   free(lo); free(hi); free(ctl.layers);
+  return REACH_OK;
+}
+
+/* ----------------------------------------------------------------------- */
+/* ct_reach (flowpipe_ct.hpp:428-458) of an analytic field: box 0 is X0.    */
+static int ct_reach_one(const ctfield* F, const reach_flowpipe_params* fp, const double* x0lo, const double* x0hi,
+                        double* lo, double* hi, int* failed_step, int* status) {
+  const int n = F->n;
+  ctsym* s = (ctsym*)calloc(1, sizeof(ctsym));
+  ctwork* w = (ctwork*)malloc(sizeof(ctwork));
+  ctstep* st = (ctstep*)malloc(sizeof(ctstep));
+  *failed_step = -1;
+  *status = REACH_TUBE_OK;
+  for (int d = 0; d < n; ++d) { lo[d] = x0lo[d]; hi[d] = x0hi[d]; }
+  int nb = 1;
+  /* init_symbolic_state (flowpipe_ct.hpp:302-309) */
+  s->na = n; s->p0 = n; s->nq = 0; s->window = fp->window;
+  for (int i = 0; i < n; ++i) {
+    s->c[i] = (x0lo[i] + x0hi[i]) * 0.5;
+    s->M[i][i] = (x0hi[i] - x0lo[i]) * 0.5;
+  }
+  for (int step = 0; step < fp->steps; ++step) {
+    int fin;
+    int rc = ct_flow_step(s, fp, F, w, st, lo + (size_t)nb * n, hi + (size_t)nb * n, &fin);
+    if (rc != REACH_TUBE_OK) { *failed_step = step; *status = rc; break; }
+    nb += 1;
+    if (!fin) { *failed_step = step; *status = REACH_TUBE_DIVERGED_BOX; break; }
+    ct_symbolic_step(s, st);
+  }
+  free(s); free(w); free(st);
+  return nb;
+}
+
+int orc_ct_batch(const reach_field_desc* fd, const reach_flowpipe_params* fp, int32_t batch, const double* x0_lo,
+                 const double* x0_hi, const reach_tube_out* out) {
+  const int n = fd->n, T = 1 + fp->steps;
+  if (n < 1 || n > 16) return REACH_E_UNSUPPORTED;
+  const ctfield F = {fd->kind, n, fd->params};
+  for (int b = 0; b < batch; ++b) {
+    int fs, st;
+    out->n_boxes[b] = ct_reach_one(&F, fp, x0_lo + (size_t)b * n, x0_hi + (size_t)b * n, out->lo + (size_t)b * T * n,
+                                   out->hi + (size_t)b * T * n, &fs, &st);
+    out->failed_step[b] = fs;
+    out->status[b] = st;
+  }
   return REACH_OK;
 }

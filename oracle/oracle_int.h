@@ -23,6 +23,7 @@ typedef struct {
 
 /* Bridges into reach_oracle.c (see the static functions they wrap). */
 net_t orc_i_net_from_desc(const reach_net_desc* d);
+int orc_i_mat_solve(int n, int m, const double* A, const double* B, double* X);
 int orc_i_certify_tm_input(const net_t* net, int n_i, int nz, const double* c, const double* A, const iv* ig,
                            double* out_c, double* out_A, iv* rem);
 

@@ -902,6 +902,7 @@ int orc_dtcl_batch(const reach_net_desc* dyn_desc, const reach_net_desc* ctl_des
 }
 
 /* Bridges for ct_oracle.c. */
+int orc_i_mat_solve(int n, int m, const double* A, const double* B, double* X) { return mat_solve(n, m, A, B, X); }
 net_t orc_i_net_from_desc(const reach_net_desc* d) { return net_from_desc(d); }
 int orc_i_certify_tm_input(const net_t* net, int n_i, int nz, const double* c, const double* A, const iv* ig,
                            double* out_c, double* out_A, iv* rem) {

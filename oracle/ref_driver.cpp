@@ -618,3 +618,61 @@ int ref_cl_split_hull(const reach_net_desc* ctl_desc, const reach_cl_spec* sp, c
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// ct_reach (flowpipe_ct.hpp:428-458) with the analytic fields of fields.hpp.
+namespace {
+VectorField<double> field_from(const reach_field_desc* f) {
+  switch (f->kind) {
+    case REACH_FIELD_ZERO: return zero_field<double>(f->n);
+    case REACH_FIELD_DIAG_LINEAR: return diag_linear_field<double>(std::vector<double>(f->params, f->params + f->n));
+    case REACH_FIELD_ROTATION: return rotation_field<double>(f->params[0]);
+    case REACH_FIELD_QUADROTOR: {
+      QuadrotorParams prm;
+      prm.mass = f->params[0];
+      prm.gravity = f->params[1];
+      prm.jx = f->params[2];
+      prm.jy = f->params[3];
+      prm.jz = f->params[4];
+      return quadrotor_field<double>(prm, Vec<double>(f->params + 5, f->params + 9));
+    }
+  }
+  throw std::invalid_argument("unknown field");
+}
+}  // namespace
+
+extern "C" {
+int ref_ct_batch(const reach_field_desc* fd, const reach_flowpipe_params* fp, int32_t batch, const double* x0_lo,
+                 const double* x0_hi, const reach_tube_out* out, int32_t threads) {
+  try {
+    VectorField<double> f = field_from(fd);
+    FlowpipeParams prm;
+    prm.h = fp->h;
+    prm.steps = fp->steps;
+    prm.order = fp->order;
+    prm.eps_init = fp->eps_init;
+    prm.refine_rounds = fp->refine_rounds;
+    prm.enlargement = fp->enlargement;
+    prm.max_enlargements = fp->max_enlargements;
+    prm.window = fp->window;
+    const int n = fd->n, T = 1 + fp->steps;
+    parallel_for(
+        batch,
+        [&](int b) {
+          ReachTube<double> t;
+          try {
+            t = ct_reach(f, box_at(x0_lo + static_cast<size_t>(b) * n, x0_hi + static_cast<size_t>(b) * n, n), prm);
+          } catch (const std::exception& e) {
+            t = ReachTube<double>();
+            t.mark_failed(0, e.what());
+          }
+          put_tube(t, n, T, out->lo + static_cast<size_t>(b) * T * n, out->hi + static_cast<size_t>(b) * T * n,
+                   out->n_boxes + b, out->failed_step + b, out->status + b);
+        },
+        threads);
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+}  // extern "C"

@@ -8,6 +8,7 @@ from .api import (  # noqa: F401
     SplitPlan, split_box, dt_reach, dt_reach_batch, dt_reach_batch_arrays, reach_split_hull,
     reach_with_splitting, tube_volume, box_volume_proxy, box_from_center, dt_closed_loop_batch,
     QuadrotorParams, FlowpipeParams, ClosedLoopSpec, cl_reach, cl_reach_batch_arrays, cl_split_hull,
-    cl_reach_with_splitting,
+    cl_reach_with_splitting, AnalyticField, zero_field, diag_linear_field, rotation_field, quadrotor_field,
+    quadrotor_hover_input, ct_reach, ct_reach_batch_arrays,
 )
 from ._native import Context, default_context, ReachError, NativeMissing, LIB_PATH  # noqa: F401

@@ -166,3 +166,10 @@ class CLSpecC(C.Structure):
 
 class CLSplitArgs(C.Structure):
     _fields_ = [("x0_lo", _dp), ("x0_hi", _dp), ("counts", _ip), ("part_begin", C.c_int64), ("part_end", C.c_int64)]
+
+
+FIELD_ZERO, FIELD_DIAG_LINEAR, FIELD_ROTATION, FIELD_QUADROTOR = 0, 1, 2, 3
+
+
+class FieldDescC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("params", C.c_double * 16)]

@@ -14,6 +14,9 @@ templates for the DT reachability path:
     QuadrotorParams                 systems.hpp:16-20
     FlowpipeParams                  flowpipe_ct.hpp:35-50
     ClosedLoopSpec, cl_reach        closed_loop.hpp:16-182  (plant = quadrotor_ode, fields.hpp:96-128)
+    zero_field, diag_linear_field,  fields.hpp:51-92 (the analytic VectorFields the device runs)
+    rotation_field, quadrotor_field
+    ct_reach                        flowpipe_ct.hpp:428-458
 
 Every compute call runs the CUDA kernels through the C ABI
 (include/reach_b200.h); there is no CPU path.  Shape errors raise
@@ -547,3 +550,77 @@ def cl_split_hull(spec: ClosedLoopSpec, x0, plan: SplitPlan, part_begin: int = 0
 def cl_reach_with_splitting(spec: ClosedLoopSpec, x0, plan: SplitPlan, ctx: Optional[Context] = None) -> ReachTube:
     """reach_with_splitting(cl_reach engine, x0, plan) (refine.hpp:121-160)."""
     return cl_split_hull(spec, x0, plan, ctx=ctx).tube()
+
+
+# ---------------------------------------------------------------------------
+# Open-loop continuous-time flowpipes (ct_reach, flowpipe_ct.hpp:428-458) of the
+# analytic VectorFields of fields.hpp.  A field here is a descriptor, not a
+# closure: the device evaluates it as a Taylor-model field program.
+@dataclass
+class AnalyticField:
+    kind: int
+    n: int
+    params: List[float] = field(default_factory=list)
+
+    def c_struct(self):
+        p = (C.c_double * 16)(*(list(self.params) + [0.0] * (16 - len(self.params))))
+        return A.FieldDescC(self.kind, self.n, p)
+
+
+def zero_field(n: int) -> AnalyticField:
+    """zero_field (fields.hpp:87-92)."""
+    return AnalyticField(A.FIELD_ZERO, n)
+
+
+def diag_linear_field(lam) -> AnalyticField:
+    """diag_linear_field (fields.hpp:72-78): xdot_i = lambda_i x_i."""
+    lam = [float(v) for v in lam]
+    return AnalyticField(A.FIELD_DIAG_LINEAR, len(lam), lam)
+
+
+def rotation_field(w: float) -> AnalyticField:
+    """rotation_field (fields.hpp:80-85): x' = -w y, y' = w x."""
+    return AnalyticField(A.FIELD_ROTATION, 2, [float(w)])
+
+
+def quadrotor_hover_input(prm: QuadrotorParams = None):
+    """quadrotor_hover_input (systems.hpp:66-68)."""
+    prm = prm or QuadrotorParams()
+    return [prm.mass * prm.gravity, 0.0, 0.0, 0.0]
+
+
+def quadrotor_field(prm: QuadrotorParams = None, u=None) -> AnalyticField:
+    """quadrotor_field (fields.hpp:51-56) with the held input u (4)."""
+    prm = prm or QuadrotorParams()
+    u = list(u) if u is not None else quadrotor_hover_input(prm)
+    return AnalyticField(A.FIELD_QUADROTOR, 12, prm.as_array() + [float(v) for v in u])
+
+
+def ct_reach_batch_arrays(f: AnalyticField, x0_lo: np.ndarray, x0_hi: np.ndarray, prm: FlowpipeParams = None,
+                          ctx: Optional[Context] = None) -> TubeBatch:
+    """ct_reach (flowpipe_ct.hpp:428-458) for a batch of initial boxes x0 [B][n]."""
+    prm = prm or FlowpipeParams()
+    prm.validate()
+    ctx = ctx or default_context()
+    x0_lo = np.ascontiguousarray(x0_lo, dtype=np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, dtype=np.float64)
+    B = x0_lo.shape[0]
+    if x0_lo.shape != (B, f.n) or x0_hi.shape != (B, f.n):
+        raise ValueError("ct_reach: X0 dimension mismatch")
+    T = 1 + prm.steps
+    out = TubeBatch(np.full((B, T, f.n), np.nan), np.full((B, T, f.n), np.nan), np.zeros(B, np.int32),
+                    np.zeros(B, np.int32), np.zeros(B, np.int32), h=prm.h)
+    fd = f.c_struct()
+    fp = prm.c_struct()
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step),
+                   A.iptr(out.status))
+    ctx.check(ctx._lib.reach_ct_batch(ctx.handle, C.byref(fd), C.byref(fp), B, A.dptr(x0_lo), A.dptr(x0_hi),
+                                      C.byref(to), 0), "ct_reach")
+    return out
+
+
+def ct_reach(f: AnalyticField, x0, prm: FlowpipeParams = None, ctx: Optional[Context] = None) -> ReachTube:
+    """ct_reach (flowpipe_ct.hpp:428-430): x0 = (lo, hi)."""
+    lo = np.asarray(x0[0], np.float64).reshape(1, -1)
+    hi = np.asarray(x0[1], np.float64).reshape(1, -1)
+    return ct_reach_batch_arrays(f, lo, hi, prm, ctx).tube(0)

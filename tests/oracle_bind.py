@@ -287,3 +287,34 @@ def oracle_cl_split_hull(spec, x0_lo, x0_hi, plan, begin=0, end=0):
 
 def ref_cl_split_hull(spec, x0_lo, x0_hi, plan, begin=0, end=0, threads=0):
     return _cl_hull(ref_lib(), "ref_", spec, x0_lo, x0_hi, plan, begin, end, threads)
+
+
+# --- open-loop continuous-time flowpipe (ct_reach) ---------------------------
+def _ct(lib, prefix, f, x0_lo, x0_hi, prm, threads=None):
+    from paper_2605_25346_b200.api import TubeBatch as TB
+    args_t = [C.POINTER(A.FieldDescC), C.POINTER(A.FlowpipeParamsC), C.c_int32, C.POINTER(C.c_double),
+              C.POINTER(C.c_double), C.POINTER(A.TubeOut)]
+    if prefix == "ref_":
+        args_t.append(C.c_int32)
+    fn = _mpc_fn(lib, prefix + "ct_batch", args_t)
+    x0_lo = np.ascontiguousarray(x0_lo, np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, np.float64)
+    B = x0_lo.shape[0]
+    T = 1 + prm.steps
+    out = TB(np.full((B, T, f.n), np.nan), np.full((B, T, f.n), np.nan), np.zeros(B, np.int32),
+             np.zeros(B, np.int32), np.zeros(B, np.int32), h=prm.h)
+    fd = f.c_struct()
+    fp = prm.c_struct()
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step), A.iptr(out.status))
+    extra = [threads or 0] if prefix == "ref_" else []
+    rc = fn(C.byref(fd), C.byref(fp), B, A.dptr(x0_lo), A.dptr(x0_hi), C.byref(to), *extra)
+    assert rc == 0, rc
+    return out
+
+
+def oracle_ct_batch(f, x0_lo, x0_hi, prm):
+    return _ct(oracle_lib(), "orc_", f, x0_lo, x0_hi, prm)
+
+
+def ref_ct_batch(f, x0_lo, x0_hi, prm, threads=0):
+    return _ct(ref_lib(), "ref_", f, x0_lo, x0_hi, prm, threads)
