@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -45,6 +47,186 @@ __global__ void ct_hull_finalize_kernel(const unsigned long long* klo, const uns
   if (t >= count) return;
   lo[t] = nan0[2 * t] ? __longlong_as_double(0x7ff8000000000000ll) : rb::from_order_key(klo[t]);
   hi[t] = nan0[2 * t + 1] ? __longlong_as_double(0x7ff8000000000000ll) : rb::from_order_key(khi[t]);
+}
+
+// ---------------------------------------------------------------------------
+// Field programs (ct_kernel.cuh: slots P0.., T0..3, V0..9, C0..3).  Each is the
+// reference's expression tree for the field body, operand order included.
+using rb::ct::TOp;
+struct Program {
+  std::vector<TOp> ops;
+  double kc[rb::ct::kMaxKc] = {};
+};
+constexpr unsigned char P_(int i) { return static_cast<unsigned char>(i); }
+constexpr unsigned char T_(int i) { return static_cast<unsigned char>(rb::ct::SLOT_T + i); }
+constexpr unsigned char V_(int i) { return static_cast<unsigned char>(rb::ct::SLOT_V + i); }
+constexpr unsigned char C_(int i) { return static_cast<unsigned char>(rb::ct::SLOT_C + i); }
+
+// quadrotor_ode (systems.hpp:24-64) with the input rows u: the augmented rows
+// P12..15 (make_augmented_field, fields.hpp:96-107: cl_reach) or held
+// constants (quadrotor_field, fields.hpp:20-32,51-56: ct_reach).  Each dx_i is
+// consumed once neither P_i nor a view of it is read again, so the consumer
+// may overwrite P_i (poly_picard's in-place update).
+Program quad_program(const double* prm, const double* u_held) {
+  using namespace rb::ct;
+  Program p;
+  const double mass = prm[0], grav = prm[1], jx = prm[2], jy = prm[3], jz = prm[4];
+  p.kc[0] = 1.0 / mass;  // the reference's constants (systems.hpp:48-63)
+  p.kc[1] = grav;
+  p.kc[2] = (jy - jz) / jx;
+  p.kc[3] = 1.0 / jx;
+  p.kc[4] = (jz - jx) / jy;
+  p.kc[5] = 1.0 / jy;
+  p.kc[6] = (jx - jy) / jz;
+  p.kc[7] = 1.0 / jz;
+  auto U = [&](int k) { return u_held ? C_(k) : P_(12 + k); };
+  auto& o = p.ops;
+  if (u_held)
+    for (int k = 0; k < 4; ++k) {
+      p.kc[8 + k] = u_held[k];
+      o.push_back({OP_CONST, C_(k), 0, static_cast<unsigned char>(8 + k)});
+    }
+  o.insert(o.end(), {
+      {OP_CONS, 0, P_(3), 0}, {OP_CONS, 1, P_(4), 0}, {OP_CONS, 2, P_(5), 0},  // dx0..2 = v
+      {OP_SIN, V_(0), P_(6), 0}, {OP_COS, V_(1), P_(6), 0},                     // sphi, cphi
+      {OP_SIN, V_(2), P_(7), 0}, {OP_COS, V_(3), P_(7), 0},                     // sth, cth
+      {OP_SIN, V_(4), P_(8), 0}, {OP_COS, V_(5), P_(8), 0},                     // spsi, cpsi
+      {OP_SCALE, V_(6), U(0), 0},                                               // a = u0 * (1/mass)
+      {OP_MUL, T_(0), V_(1), V_(2)},                                            // cphi*sth
+      {OP_MUL, T_(1), T_(0), V_(5)}, {OP_MUL, T_(2), V_(0), V_(4)},             // *cpsi, sphi*spsi
+      {OP_ADD, T_(1), T_(1), T_(2)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3x, a*b3x
+      {OP_CONS, 3, T_(2), 0},
+      {OP_MUL, T_(1), T_(0), V_(4)}, {OP_MUL, T_(2), V_(0), V_(5)},             // *spsi, sphi*cpsi
+      {OP_SUB, T_(1), T_(1), T_(2)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3y, a*b3y
+      {OP_CONS, 4, T_(2), 0},
+      {OP_MUL, T_(1), V_(1), V_(3)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3z, a*b3z
+      {OP_SUBK, T_(2), 0, 1},                                                   // - gravity
+      {OP_CONS, 5, T_(2), 0},
+      {OP_INV, V_(7), V_(3), 0},                                                // tme_inv(cth)
+      {OP_MUL, T_(0), V_(2), V_(7)},                                            // tth = sth / cth
+      {OP_MUL, T_(1), V_(0), T_(0)}, {OP_MUL, T_(1), T_(1), P_(10)},            // sphi*tth*q
+      {OP_ADD, T_(1), P_(9), T_(1)},                                            // p + ...
+      {OP_MUL, T_(2), V_(1), T_(0)}, {OP_MUL, T_(2), T_(2), P_(11)},            // cphi*tth*r
+      {OP_ADD, T_(1), T_(1), T_(2)},                                            // dx6 (held)
+      {OP_MUL, T_(0), V_(1), P_(10)}, {OP_MUL, T_(2), V_(0), P_(11)},           // cphi*q, sphi*r
+      {OP_SUB, T_(0), T_(0), T_(2)},                                            // dx7 (held)
+      {OP_MUL, T_(2), V_(0), V_(7)}, {OP_MUL, T_(2), T_(2), P_(10)},            // (sphi/cth)*q
+      {OP_MUL, T_(3), V_(1), V_(7)}, {OP_MUL, T_(3), T_(3), P_(11)},            // (cphi/cth)*r
+      {OP_ADD, T_(2), T_(2), T_(3)},                                            // dx8
+      // the views of P6 / P7 (sphi, cphi, 1/cth) are dead only now: consume rows 6..8
+      {OP_CONS, 6, T_(1), 0}, {OP_CONS, 7, T_(0), 0}, {OP_CONS, 8, T_(2), 0},
+      {OP_MUL, T_(0), P_(10), P_(11)}, {OP_SCALE, V_(8), T_(0), 2},             // q*r*c1
+      {OP_SCALE, V_(9), U(1), 3}, {OP_ADD, T_(0), V_(8), V_(9)},                // + u1/jx
+      {OP_MUL, T_(1), P_(9), P_(11)}, {OP_SCALE, V_(8), T_(1), 4},              // p*r*c3
+      {OP_SCALE, V_(9), U(2), 5}, {OP_ADD, T_(1), V_(8), V_(9)},                // + u2/jy
+      {OP_MUL, T_(2), P_(9), P_(10)}, {OP_SCALE, V_(8), T_(2), 6},              // p*q*c5
+      {OP_SCALE, V_(9), U(3), 7}, {OP_ADD, T_(2), V_(8), V_(9)},                // + u3/jz
+      {OP_CONS, 9, T_(0), 0}, {OP_CONS, 10, T_(1), 0}, {OP_CONS, 11, T_(2), 0},
+  });
+  if (!u_held)
+    for (int i = 12; i < 16; ++i) o.push_back({OP_CONS0, static_cast<unsigned char>(i), 0, 0});  // udot = 0
+  o.push_back({OP_END, 0, 0, 0});
+  return p;
+}
+
+// rotation_ode (systems.hpp:162-167): dx0 = x1 * (-w), dx1 = x0 * w.  Both
+// rows read each other, so the scaled rows are materialized before consuming.
+Program rotation_program(double w) {
+  using namespace rb::ct;
+  Program p;
+  p.kc[0] = -w;
+  p.kc[1] = w;
+  p.ops = {{OP_SCALE, V_(0), P_(1), 0}, {OP_SCALE, V_(1), P_(0), 1}, {OP_COPY, T_(0), V_(0), 0},
+           {OP_COPY, T_(1), V_(1), 0},  {OP_CONS, 0, T_(0), 0},      {OP_CONS, 1, T_(1), 0},
+           {OP_END, 0, 0, 0}};
+  return p;
+}
+
+// diag_linear_ode (systems.hpp:154-159): dx_i = x_i * lambda_i.
+Program diag_program(const double* lam, int n) {
+  using namespace rb::ct;
+  Program p;
+  for (int i = 0; i < n; ++i) {
+    p.kc[i] = lam[i];
+    p.ops.push_back({OP_SCALE, V_(0), P_(i), static_cast<unsigned char>(i)});
+    p.ops.push_back({OP_CONS, static_cast<unsigned char>(i), V_(0), 0});
+  }
+  p.ops.push_back({OP_END, 0, 0, 0});
+  return p;
+}
+
+// zero_field (fields.hpp:87-92): dx.assign(n, x[0] * 0.0).
+Program zero_program(int n) {
+  using namespace rb::ct;
+  Program p;
+  p.kc[0] = 0.0;
+  p.ops = {{OP_SCALE, V_(0), P_(0), 0}, {OP_COPY, T_(0), V_(0), 0}};
+  for (int i = 0; i < n; ++i) p.ops.push_back({OP_CONS, static_cast<unsigned char>(i), T_(0), 0});
+  p.ops.push_back({OP_END, 0, 0, 0});
+  return p;
+}
+
+// The program store: every field program's op sequence (they depend on the
+// field kind and n only; per-call constants travel in CTParams::kc), uploaded
+// to the constant bank of each device once.
+struct ProgramStore {
+  std::vector<TOp> ops;
+  std::map<std::pair<int, int>, int> offset;  // (kind, n) -> first op
+  std::mutex mu;
+  std::vector<char> uploaded = std::vector<char>(256, 0);
+};
+constexpr int kKindQuadAug = 100;
+ProgramStore& program_store() {
+  static ProgramStore* s = [] {
+    auto* st = new ProgramStore();
+    const double prm[5] = {1.0, 1.0, 1.0, 1.0, 1.0}, u[4] = {0.0, 0.0, 0.0, 0.0}, lam[16] = {};
+    auto add = [&](int kind, int n, const Program& p) {
+      st->offset[{kind, n}] = static_cast<int>(st->ops.size());
+      st->ops.insert(st->ops.end(), p.ops.begin(), p.ops.end());
+    };
+    add(kKindQuadAug, 16, quad_program(prm, nullptr));
+    add(REACH_FIELD_QUADROTOR, 12, quad_program(prm, u));
+    add(REACH_FIELD_ROTATION, 2, rotation_program(1.0));
+    for (int n = 1; n <= 16; ++n) {
+      add(REACH_FIELD_DIAG_LINEAR, n, diag_program(lam, n));
+      add(REACH_FIELD_ZERO, n, zero_program(n));
+    }
+    return st;
+  }();
+  return *s;
+}
+
+int ensure_programs(reach_ctx* ctx) {
+  ProgramStore& st = program_store();
+  std::lock_guard<std::mutex> g(st.mu);
+  if (ctx->device < 0 || ctx->device >= static_cast<int>(st.uploaded.size())) return REACH_E_INVALID_ARGUMENT;
+  if (st.uploaded[ctx->device]) return REACH_OK;
+  if (st.ops.size() > static_cast<size_t>(rb::ct::kProgCap)) return fail(ctx, REACH_E_UNSUPPORTED, "program store full");
+  RB_CUDA(cudaMemcpyToSymbol(rb::ct::kProgs, st.ops.data(), st.ops.size() * sizeof(TOp)));
+  st.uploaded[ctx->device] = 1;
+  return REACH_OK;
+}
+
+// Selects a stored program and loads the call's constants; derives the Picard
+// bz row of every state row: a row whose derivative is a copy of P_j (and which
+// the program never reads) has bz = S_j, one whose derivative is 0 the zero row.
+void load_program(const Program& p, int kind, int na, rb::ct::CTParams& P) {
+  using namespace rb::ct;
+  P.prog = program_store().offset.at({kind, na});
+  for (int i = 0; i < kMaxKc; ++i) P.kc[i] = p.kc[i];
+  bool read[16] = {};
+  for (const TOp& op : p.ops) {
+    if (op.code == OP_CONS0 || op.code == OP_END || op.code == OP_CONST || op.code == OP_SUBK) continue;
+    if (op.code != OP_CONS) {
+      if (op.a < NA) read[op.a] = true;
+      if ((op.code == OP_MUL || op.code == OP_ADD || op.code == OP_SUB) && op.b < NA) read[op.b] = true;
+    }
+  }
+  for (int i = 0; i < 16; ++i) P.bzsrc[i] = -1;
+  for (const TOp& op : p.ops) {
+    if (op.code == OP_CONS0) P.bzsrc[op.dst] = -2;
+    if (op.code == OP_CONS && op.a < NA && !read[op.dst]) P.bzsrc[op.dst] = static_cast<signed char>(op.a);
+  }
 }
 
 // ClosedLoopSpec::validate (closed_loop.hpp:30-43) + the device family's limits.
@@ -87,27 +269,31 @@ int setup_params(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s, l
   P.eps = s->fp.eps_init;
   P.enl = s->fp.enlargement;
   for (int i = 0; i < 8; ++i) P.prm[i] = s->plant_params[i];
-  // quadrotor_ode's constants, computed as the reference does (systems.hpp:48-63)
-  const double mass = s->plant_params[0], grav = s->plant_params[1], jx = s->plant_params[2],
-               jy = s->plant_params[3], jz = s->plant_params[4];
-  P.kc[0] = 1.0 / mass;
-  P.kc[1] = grav;
-  P.kc[2] = (jy - jz) / jx;
-  P.kc[3] = 1.0 / jx;
-  P.kc[4] = (jz - jx) / jy;
-  P.kc[5] = 1.0 / jy;
-  P.kc[6] = (jx - jy) / jz;
-  P.kc[7] = 1.0 / jz;
+  P.na = rb::ct::NA;
+  P.bw = rb::ct::NA;
+  P.square = 0;
+  P.ct = 0;
+  load_program(quad_program(s->plant_params, nullptr), kKindQuadAug, P.na, P);
   P.ctl = ctl->dev;
   P.T = 1 + s->ctl_steps * s->k_atomic;
   (void)ctx;
   return REACH_OK;
 }
 
+// Dynamic shared memory of the flow kernel: the fixed part + S, the zero row,
+// the own Picard bz rows and the temporaries.
+size_t flow_smem_bytes(const rb::ct::CTParams& P) {
+  int npb = 0;
+  for (int i = 0; i < P.na; ++i) npb += (P.bzsrc[i] == -1);
+  return sizeof(rb::ct::FlowSmem) + static_cast<size_t>(P.na + 1 + npb + 2 * rb::ct::NTF) * rb::ct::NZP * 8;
+}
+
 int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
-  const size_t flow_smem = rb::ct::SPW * sizeof(rb::ct::FlowSmem);  // SPW sub-boxes per warp
+  int prc = ensure_programs(ctx);
+  if (prc) return prc;
+  const size_t flow_smem = flow_smem_bytes(P);
   const size_t ctl_smem = sizeof(rb::ct::CtlSmem) * rb::ct::kCtlWarps;
-  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(flow_smem)));
   RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_ctl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(ctl_smem)));
@@ -119,7 +305,7 @@ int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
     P.ci = ci;
     rb::ct::ct_ctl_kernel<<<ctl_grid, 32 * rb::ct::kCtlWarps, ctl_smem, ctx->stream>>>(P);
     RB_CUDA(cudaGetLastError());
-    rb::ct::ct_flow_kernel<<<(P.B + rb::ct::SPW - 1) / rb::ct::SPW, 32, flow_smem, ctx->stream>>>(P);
+    rb::ct::ct_flow_kernel<false><<<P.B, 32, flow_smem, ctx->stream>>>(P);
     RB_CUDA(cudaGetLastError());
   }
   rc = timed_end(ctx, stop);
@@ -301,6 +487,127 @@ int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spe
     RB_CUDA(cudaMemcpyAsync(out->box_diverged, P.hull_div, T * 4, cudaMemcpyDeviceToHost, ctx->stream));
     RB_CUDA(cudaMemcpyAsync(out->n_boxes, P.hull_nboxes, 4, cudaMemcpyDeviceToHost, ctx->stream));
     RB_CUDA(cudaMemcpyAsync(out->fail_key, P.hull_fail_key, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return REACH_OK;
+}
+
+int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowpipe_params* fp, int32_t batch,
+                   const double* x0_lo, const double* x0_hi, const reach_tube_out* out, int32_t flags) {
+  if (!ctx || !fd || !fp || !out) return REACH_E_INVALID_ARGUMENT;
+  if (batch < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: negative batch");
+  if (!(fp->h > 0) || fp->steps <= 0 || fp->order < 1 || fp->order > 2 || !(fp->eps_init > 0) ||
+      !(fp->enlargement > 1.0) || fp->refine_rounds < 0 || fp->max_enlargements < 0 || fp->window < 0)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "FlowpipeParams: invalid configuration");
+  const int n = fd->n;
+  Program prog;
+  switch (fd->kind) {
+    case REACH_FIELD_ZERO: prog = zero_program(n); break;
+    case REACH_FIELD_DIAG_LINEAR: prog = diag_program(fd->params, n); break;
+    case REACH_FIELD_ROTATION:
+      if (n != 2) return fail(ctx, REACH_E_INVALID_ARGUMENT, "rotation_field: n must be 2");
+      prog = rotation_program(fd->params[0]);
+      break;
+    case REACH_FIELD_QUADROTOR:
+      if (n != 12) return fail(ctx, REACH_E_INVALID_ARGUMENT, "quadrotor_field: n must be 12");
+      prog = quad_program(fd->params, fd->params + 5);
+      break;
+    default: return fail(ctx, REACH_E_UNSUPPORTED, "ct_reach: unknown field");
+  }
+  if (n < 1 || n > 16 || n * (fp->window + 2) > rb::ct::NZP)
+    return fail(ctx, REACH_E_UNSUPPORTED, "ct_reach: n <= 16 and n (window + 2) <= 80 on the device");
+  if (batch == 0) return REACH_OK;
+  const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
+  if (!dev)  // build_linear_tm / init_symbolic_state on a diverged X0
+    for (size_t i = 0; i < static_cast<size_t>(batch) * n; ++i)
+      if (!std::isfinite(x0_lo[i]) || !std::isfinite(x0_hi[i]))
+        return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: non-finite X0");
+  RB_CUDA(cudaSetDevice(ctx->device));
+  rb::ct::CTParams P{};
+  int rc = REACH_OK;
+  P.B = batch;
+  P.n = n;
+  P.na = n;
+  P.bw = n;
+  P.square = 1;
+  P.ct = 1;
+  P.ci = 0;
+  P.ctl_steps = 1;
+  P.K = fp->steps;
+  P.T = 1 + fp->steps;
+  P.window = fp->window;
+  P.order = fp->order;
+  P.refine = fp->refine_rounds;
+  P.maxe = fp->max_enlargements;
+  P.h = fp->h;
+  P.eps = fp->eps_init;
+  P.enl = fp->enlargement;
+  load_program(prog, fd->kind, n, P);
+  rc = ensure_programs(ctx);
+  if (rc) return rc;
+  const size_t B = batch, NA = rb::ct::NA, T = P.T;
+  const size_t box_bytes = B * T * n * 8, i_bytes = B * 4, x_bytes = B * n * 8;
+  Carve cv;
+  const size_t o_c = cv.take(B * NA * 8), o_M = cv.take(B * NA * rb::ct::NZP * 8), o_meta = cv.take(B * 16);
+  size_t o_xl = 0, o_xh = 0, o_ol = 0, o_oh = 0, o_nb = 0, o_fs = 0, o_st = 0;
+  if (!dev) {
+    o_xl = cv.take(x_bytes);
+    o_xh = cv.take(x_bytes);
+    o_ol = cv.take(box_bytes);
+    o_oh = cv.take(box_bytes);
+    o_nb = cv.take(i_bytes);
+    o_fs = cv.take(i_bytes);
+    o_st = cv.take(i_bytes);
+  }
+  rc = ensure_ws(ctx, cv.off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  P.st_c = reinterpret_cast<double*>(w + o_c);
+  P.st_M = reinterpret_cast<double*>(w + o_M);
+  P.st_meta = reinterpret_cast<int*>(w + o_meta);
+  if (dev) {
+    P.x0_lo = x0_lo;
+    P.x0_hi = x0_hi;
+    P.out_lo = out->lo;
+    P.out_hi = out->hi;
+    P.n_boxes = out->n_boxes;
+    P.failed_step = out->failed_step;
+    P.status = out->status;
+  } else {
+    P.x0_lo = reinterpret_cast<double*>(w + o_xl);
+    P.x0_hi = reinterpret_cast<double*>(w + o_xh);
+    P.out_lo = reinterpret_cast<double*>(w + o_ol);
+    P.out_hi = reinterpret_cast<double*>(w + o_oh);
+    P.n_boxes = reinterpret_cast<int*>(w + o_nb);
+    P.failed_step = reinterpret_cast<int*>(w + o_fs);
+    P.status = reinterpret_cast<int*>(w + o_st);
+    RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.x0_lo), x0_lo, x_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.x0_hi), x0_hi, x_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  const size_t smem = flow_smem_bytes(P);
+  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  rb::ct::ct_flow_kernel<true><<<batch, 32, smem, ctx->stream>>>(P);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  if (!dev) {
+    std::vector<int32_t> nb(B);
+    RB_CUDA(cudaMemcpyAsync(nb.data(), P.n_boxes, i_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(out->failed_step, P.failed_step, i_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(out->status, P.status, i_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(out->n_boxes, nb.data(), i_bytes);
+    for (size_t i = 0; i < B; ++i) {
+      const size_t o = i * T * n, cnt = static_cast<size_t>(nb[i]) * n * 8;
+      if (!cnt) continue;
+      RB_CUDA(cudaMemcpyAsync(out->lo + o, P.out_lo + o, cnt, cudaMemcpyDeviceToHost, ctx->stream));
+      RB_CUDA(cudaMemcpyAsync(out->hi + o, P.out_hi + o, cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    }
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   return REACH_OK;

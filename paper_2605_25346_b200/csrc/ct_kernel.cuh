@@ -3,6 +3,10 @@
 // udot = 0 rows (make_augmented_field, fields.hpp:96-128; quadrotor_ode,
 // systems.hpp:22-64) under a neural (tanh / ReLU) controller.
 //
+// ct_reach (flowpipe_ct.hpp:428-458) of the analytic fields of fields.hpp
+// (zero, diagonal-linear, rotation, quadrotor with a held input) runs the same
+// flow kernel alone, with a square G0 and the G0^-1 Q fold.
+//
 // One warp owns one sub-box.  Per control interval the host launches
 //   ct_ctl_kernel   controller certification ctl_crown (neural.hpp:418-424,
 //                   certify_tm_input :342-394) on the boundary state TM, the
@@ -47,13 +51,8 @@ namespace ct {
 
 constexpr int NX = 12;      // quadrotor state
 constexpr int NA = 16;      // augmented (x, u)
-constexpr int NZP = 80;     // generator columns per row: n + window (n + l) <= 76 (window <= 4)
-#ifndef RB_CT_HW
-#define RB_CT_HW 32
-#endif
-constexpr int HW = RB_CT_HW;              // lanes per sub-box in the flow kernel (32: one per warp, 16: two)
-constexpr int SPW = 32 / HW;              // sub-boxes per warp
-constexpr int NZC = (NZP + HW - 1) / HW;  // generator slots per lane
+constexpr int NZP = 80;     // generator columns per row (cl_reach: n + window (n + l) <= 76; ct_reach: n (window + 2) <= 80)
+constexpr int NZC = (NZP + 31) / 32;  // generator slots per lane (lane + 32 k)
 constexpr int kMaxCtlW = 128;  // widest controller layer (and input dim)
 constexpr int LDX = NZP + 1;
 
@@ -61,11 +60,30 @@ constexpr int LDX = NZP + 1;
 enum : int { CT_OK = 0, CT_CTL_FAILED = 4, CT_CTL_DIVERGED = 5, CT_REMAINDER = 6, CT_PICARD = 7, CT_TME_INV = 8,
              CT_BOX = 3, CT_OTHER = 99 };
 
+// One operation of a field program (see quad / rotation / ... programs built by
+// the host, ct_capi.cu): dst / a / b are slot indices, b a constant index for
+// SCALE / SUBK / CONST.
+struct TOp {
+  unsigned char code, dst, a, b;
+};
+constexpr int kMaxKc = 24;
+// Every field program lives in constant memory (uploaded once per device by
+// the host, ct_capi.cu): the dispatch reads a provably warp-uniform opcode, so
+// the shuffles inside the operations need no divergence handling.
+constexpr int kProgCap = 1024;
+__constant__ TOp kProgs[kProgCap];
+
 struct CTParams {
   int B, n, l, K, window, order, refine, maxe, intervalize, ref_dim, ci, ctl_steps;
+  int na;      // rows of the flowed state: n + l (cl_reach) or n (ct_reach)
+  int bw;      // width of a queue block: na in both drivers
+  int square;  // 1: G0 is na x na (ct_reach) -> the G0^-1 Q fold; 0: the hull fold
+  int ct;      // 1: ct_reach -- no controller; the first launch builds the state from X0
   double h, eps, enl;
   double prm[8];
-  double kc[8];  // plant constants of the field program (kQuadTape)
+  double kc[kMaxKc];         // constants of the field program
+  int prog;                  // offset of the field program in kProgs
+  signed char bzsrc[16];     // Picard bz row of row i: -1 own storage, -2 the zero row, j >= 0 the seed row j
   DevNet ctl;
   const double* y_ref;  // device [ctl_steps][ref_dim]
   // initial boxes: batch (x0_lo/hi [B][n]) or split of one box
@@ -100,7 +118,6 @@ struct CTParams {
 struct Iv {
   double lo, hi;
 };
-__device__ __forceinline__ Iv iv(double lo, double hi) { return Iv{lo, hi}; }
 __device__ __forceinline__ Iv iadd(Iv a, Iv b) { return Iv{a.lo + b.lo, a.hi + b.hi}; }
 __device__ __forceinline__ Iv isub(Iv a, Iv b) { return Iv{a.lo - b.hi, a.hi - b.lo}; }
 __device__ __forceinline__ Iv imul(Iv a, Iv b) {
@@ -118,17 +135,17 @@ __device__ __forceinline__ Iv iscale(double a, Iv x) {
 }
 __device__ __forceinline__ bool ifin(Iv x) { return isfinite(x.lo) && isfinite(x.hi); }
 
-// Butterfly sums over the HW lanes of one sub-box (identical result on every lane).
-__device__ __forceinline__ void wsum2(double& a, double& b, unsigned mask) {
+// Butterfly sums over the warp (identical result on every lane).
+__device__ __forceinline__ void wsum2(double& a, double& b) {
 #pragma unroll
-  for (int o = HW / 2; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(mask, a, o, HW);
-    b += __shfl_xor_sync(mask, b, o, HW);
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
   }
 }
-__device__ __forceinline__ double wsum(double a, unsigned mask) {
+__device__ __forceinline__ double wsum(double a) {
 #pragma unroll
-  for (int o = HW / 2; o > 0; o >>= 1) a += __shfl_xor_sync(mask, a, o, HW);
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   return a;
 }
 
@@ -136,52 +153,56 @@ __device__ __forceinline__ double wsum(double a, unsigned mask) {
 // TMExpr rows as slots.  A slot is a row of the field evaluation: its
 // warp-uniform scalars (centre, time coefficient, remainder, the cached
 // abs-sums) plus the shared-memory rows of its az / bz coefficients.
-//   P0..15  the Picard iterate p_k: az aliases the seed rows S (poly_picard
-//           never changes the z columns: g = seed + Int f adds only tau terms),
-//           bz in Pbz;
-//   T0..3   full temporaries;
-//   V0..9   views: rows whose coefficients are a scalar multiple of another
-//           row's (sin / cos linearizations, scalar products, reciprocals,
-//           taylor_model.hpp:284-295, 364-425), az = (base.az * s1) * s2, so
-//           they cost no coefficient storage and no coefficient pass.
+//   P0..      the Picard iterate p_k: az aliases the seed rows S (poly_picard
+//             never changes the z columns: g = seed + Int f adds only tau
+//             terms); bz in an own row, or aliased (CTParams::bzsrc): a row
+//             whose derivative is a copy of P_j has bz = S_j, one whose
+//             derivative is 0 has bz = 0;
+//   T0..3     full temporaries;
+//   V0..9     views: rows whose coefficients are a scalar multiple of another
+//             row's (sin / cos linearizations, scalar products, reciprocals,
+//             taylor_model.hpp:284-295, 364-425), az = base.az * s, so they
+//             cost no coefficient storage and no coefficient pass;
+//   C0..3     constant rows (tme_const of a held input, fields.hpp:28).
 constexpr int NTF = 4;
 constexpr int NV = 10;
+constexpr int NCST = 4;
 constexpr int SLOT_T = NA;
 constexpr int SLOT_V = NA + NTF;
-constexpr int NSLOT = NA + NTF + NV;
+constexpr int SLOT_C = SLOT_V + NV;
+constexpr int NSLOT = SLOT_C + NCST;
 
 struct Slot {
   double c, at, rlo, rhi;
   double sz, sb;  // abs_z / abs_b (taylor_model.hpp:213-224) of the row's coefficients
   double s1, s2;  // view scales (1, 1 for a stored row)
-  int az, bz;     // coefficient rows: offsets (doubles) into FlowSmem::coef
+  int az, bz;     // coefficient rows: offsets (doubles) into FlowSmem::coef()
   int view, pad;
 };
 
-// Shared memory of one sub-box (~25 KB: 8 per SM).
-// Picard rows 0..2 have bz = dx_{0..2}.az = S_{3..5} and rows 12..15 bz = 0
-// (udot = 0), so only rows 3..11 own a bz row; the others alias S or a zero row.
-constexpr int NPB = 9;  // owned Picard bz rows (P3..P11)
-struct FlowSmem {
-  double coef[NA * NZP + (NPB + 1) * NZP + 2 * NTF * NZP];  // S (= P.az) | Pbz 3..11 | zero | Taz | Tbz
+// Shared memory of one sub-box: this fixed part, then the coefficient rows
+//   S [na][NZP] | zero row | own Picard bz rows | Taz [NTF][NZP] | Tbz [NTF][NZP]
+// (cl_reach: 25.6 KB -> 8 sub-boxes per SM).  The Picard bz / temporary rows
+// double as the scratch of the square fold.
+struct __align__(128) FlowSmem {
   Slot D[NSLOT];
   double sc[NA];   // seed centre
   double ssz[NA];  // abs_z of the seed rows
   double ec[NA];   // endpoint centre
-  double kc[8];    // plant constants (CTParams::kc)
+  double kc[kMaxKc];
   Iv erem[NA], i0[NA], i1[NA], nx[NA];
+  int pbz[NA];     // Picard bz row offset of row i
+  int own[NA];     // row i owns its bz row
+  int wid[8];      // queue block widths (square fold)
+  int na, off_zero, off_pbz, off_taz, off_tbz, pad;
+  __device__ __forceinline__ double* coef() { return reinterpret_cast<double*>(this + 1); }
 };
-constexpr int OFF_S = 0, OFF_PBZ = NA * NZP, OFF_ZERO = OFF_PBZ + NPB * NZP, OFF_TAZ = OFF_ZERO + NZP,
-              OFF_TBZ = OFF_TAZ + NTF * NZP;
-__device__ __forceinline__ int pbz_off(int i) {
-  return (i < 3) ? OFF_S + (i + 3) * NZP : (i < 3 + NPB) ? OFF_PBZ + (i - 3) * NZP : OFF_ZERO;
-}
+static_assert(sizeof(FlowSmem) % 128 == 0, "coefficient rows start on a 128-byte line: a warp's 256-byte row segment is two smem wavefronts, not three");
 
 struct Lane {
-  int lane;       // lane within the sub-box's half-warp
-  unsigned mask;  // the half-warp
+  int lane;
   double h;
-  bool act[NZC];  // slot lane + HW k < nz
+  bool act[NZC];  // slot lane + 32 k < nz
 };
 
 // poly_range (taylor_model.hpp:227-235) from the cached sums.
@@ -223,78 +244,30 @@ __device__ __forceinline__ void set_scalars(Slot& r, double c, double at, Iv rem
   r.sb = sb;
 }
 
-// ---- the field program ------------------------------------------------------
-enum : unsigned char { OP_MUL, OP_ADD, OP_SUB, OP_SUBK, OP_SCALE, OP_SIN, OP_COS, OP_INV, OP_CONS, OP_CONS0, OP_END };
-struct TOp {
-  unsigned char code, dst, a, b;  // b: second operand, or the constant index (SCALE / SUBK)
+// ---- field programs ------------------------------------------------------------
+// MUL / ADD / SUB: TMExpr products and sums (taylor_model.hpp:245-360);
+// SUBK: TM - s; SCALE: TM * s (a view); SIN / COS / INV: linearizations
+// (views); COPY: materialize a view into a temporary; CONST: tme_const(kc);
+// CONS i: hand dx_i to the consumer (CONS0: dx_i = 0).
+enum : unsigned char {
+  OP_MUL, OP_ADD, OP_SUB, OP_SUBK, OP_SCALE, OP_SIN, OP_COS, OP_INV, OP_CONS, OP_CONS0, OP_COPY, OP_CONST, OP_END
 };
-#define P_(i) static_cast<unsigned char>(i)
-#define T_(i) static_cast<unsigned char>(SLOT_T + (i))
-#define V_(i) static_cast<unsigned char>(SLOT_V + (i))
-
-// make_augmented_field(12, 4, quadrotor_ode) (fields.hpp:96-107,
-// systems.hpp:24-64) as a program over the slots.  Constants (CTParams::kc):
-// 0 = 1/mass, 1 = gravity, 2 = (jy-jz)/jx, 3 = 1/jx, 4 = (jz-jx)/jy,
-// 5 = 1/jy, 6 = (jx-jy)/jz, 7 = 1/jz.  Each derivative row dx_i is consumed
-// (CONS i) once neither P_i nor a view of it is read again, so a consumer may
-// overwrite P_i (poly_picard's in-place update).  Expression trees and
-// operand order are the reference's.
-__constant__ TOp kQuadTape[] = {
-    {OP_CONS, 0, P_(3), 0}, {OP_CONS, 1, P_(4), 0}, {OP_CONS, 2, P_(5), 0},  // dx0..2 = v
-    {OP_SIN, V_(0), P_(6), 0}, {OP_COS, V_(1), P_(6), 0},                     // sphi, cphi
-    {OP_SIN, V_(2), P_(7), 0}, {OP_COS, V_(3), P_(7), 0},                     // sth, cth
-    {OP_SIN, V_(4), P_(8), 0}, {OP_COS, V_(5), P_(8), 0},                     // spsi, cpsi
-    {OP_SCALE, V_(6), P_(12), 0},                                             // a = u0 * (1/mass)
-    {OP_MUL, T_(0), V_(1), V_(2)},                                            // cphi*sth
-    {OP_MUL, T_(1), T_(0), V_(5)}, {OP_MUL, T_(2), V_(0), V_(4)},             // *cpsi, sphi*spsi
-    {OP_ADD, T_(1), T_(1), T_(2)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3x, a*b3x
-    {OP_CONS, 3, T_(2), 0},
-    {OP_MUL, T_(1), T_(0), V_(4)}, {OP_MUL, T_(2), V_(0), V_(5)},             // *spsi, sphi*cpsi
-    {OP_SUB, T_(1), T_(1), T_(2)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3y, a*b3y
-    {OP_CONS, 4, T_(2), 0},
-    {OP_MUL, T_(1), V_(1), V_(3)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3z, a*b3z
-    {OP_SUBK, T_(2), 0, 1},                                                   // - gravity
-    {OP_CONS, 5, T_(2), 0},
-    {OP_INV, V_(7), V_(3), 0},                                                // tme_inv(cth)
-    {OP_MUL, T_(0), V_(2), V_(7)},                                            // tth = sth / cth
-    {OP_MUL, T_(1), V_(0), T_(0)}, {OP_MUL, T_(1), T_(1), P_(10)},            // sphi*tth*q
-    {OP_ADD, T_(1), P_(9), T_(1)},                                            // p + ...
-    {OP_MUL, T_(2), V_(1), T_(0)}, {OP_MUL, T_(2), T_(2), P_(11)},            // cphi*tth*r
-    {OP_ADD, T_(1), T_(1), T_(2)},                                            // dx6 (held)
-    {OP_MUL, T_(0), V_(1), P_(10)}, {OP_MUL, T_(2), V_(0), P_(11)},           // cphi*q, sphi*r
-    {OP_SUB, T_(0), T_(0), T_(2)},                                            // dx7 (held)
-    {OP_MUL, T_(2), V_(0), V_(7)}, {OP_MUL, T_(2), T_(2), P_(10)},            // (sphi/cth)*q
-    {OP_MUL, T_(3), V_(1), V_(7)}, {OP_MUL, T_(3), T_(3), P_(11)},            // (cphi/cth)*r
-    {OP_ADD, T_(2), T_(2), T_(3)},                                            // dx8
-    // the views of P6 / P7 (sphi, cphi, 1/cth) are dead only now: consume rows 6..8
-    {OP_CONS, 6, T_(1), 0}, {OP_CONS, 7, T_(0), 0}, {OP_CONS, 8, T_(2), 0},
-    {OP_MUL, T_(0), P_(10), P_(11)}, {OP_SCALE, V_(8), T_(0), 2},             // q*r*c1
-    {OP_SCALE, V_(9), P_(13), 3}, {OP_ADD, T_(0), V_(8), V_(9)},              // + u1/jx
-    {OP_MUL, T_(1), P_(9), P_(11)}, {OP_SCALE, V_(8), T_(1), 4},              // p*r*c3
-    {OP_SCALE, V_(9), P_(14), 5}, {OP_ADD, T_(1), V_(8), V_(9)},              // + u2/jy
-    {OP_MUL, T_(2), P_(9), P_(10)}, {OP_SCALE, V_(8), T_(2), 6},              // p*q*c5
-    {OP_SCALE, V_(9), P_(15), 7}, {OP_ADD, T_(2), V_(8), V_(9)},              // + u3/jz
-    {OP_CONS, 9, T_(0), 0}, {OP_CONS, 10, T_(1), 0}, {OP_CONS, 11, T_(2), 0},
-    {OP_CONS0, 12, 0, 0}, {OP_CONS0, 13, 0, 0}, {OP_CONS0, 14, 0, 0}, {OP_CONS0, 15, 0, 0},
-    {OP_END, 0, 0, 0},
-};
-
 enum : int { MODE_PICARD = 0, MODE_REPLAY = 1, MODE_ENDPOINT = 2 };
 
 // operator* (taylor_model.hpp:325-360).  r may alias u or v.
-__device__ __forceinline__ void op_mul(FlowSmem& W, Slot& r, const Slot& u, const Slot& v, const Lane& L) {
+__device__ __forceinline__ void op_mul(double* coef, Slot& r, const Slot& u, const Slot& v, const Lane& L) {
   const double h = L.h;
   const double uc = u.c, vc = v.c, uat = u.at, vat = v.at;
   const double au = u.sz, av = v.sz, bu = u.sb, bv = v.sb;
   const Iv ur{u.rlo, u.rhi}, vr{v.rlo, v.rhi};
-  const Opnd U = opnd(W.coef, u), V = opnd(W.coef, v);
-  double* raz = W.coef + r.az;
-  double* rbz = W.coef + r.bz;
+  const Opnd U = opnd(coef, u), V = opnd(coef, v);
+  double* raz = coef + r.az;
+  double* rbz = coef + r.bz;
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll
   for (int k = 0; k < NZC; ++k) {
     if (!L.act[k]) continue;
-    const int j = L.lane + HW * k;
+    const int j = L.lane + 32 * k;
     double ua, ub, va, vb;
     fetch(U, j, ua, ub);
     fetch(V, j, va, vb);
@@ -305,7 +278,7 @@ __device__ __forceinline__ void op_mul(FlowSmem& W, Slot& r, const Slot& u, cons
     s1 += fabs(ra);
     s2 += fabs(rb);
   }
-  wsum2(s1, s2, L.mask);
+  wsum2(s1, s2);
   double sym = au * av;
   sym += (au * bv + av * bu) * h;
   sym += bu * bv * h * h;
@@ -321,18 +294,19 @@ __device__ __forceinline__ void op_mul(FlowSmem& W, Slot& r, const Slot& u, cons
 }
 
 // a + b / a - b (taylor_model.hpp:245-269); r may alias a or b.
-__device__ __forceinline__ void op_addsub(FlowSmem& W, Slot& r, const Slot& a, const Slot& b, bool sub, const Lane& L) {
+__device__ __forceinline__ void op_addsub(double* coef, Slot& r, const Slot& a, const Slot& b, bool sub,
+                                          const Lane& L) {
   const double c = sub ? a.c - b.c : a.c + b.c;
   const double at = sub ? a.at - b.at : a.at + b.at;
   const Iv rem = sub ? isub(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi}) : iadd(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi});
-  const Opnd A = opnd(W.coef, a), B = opnd(W.coef, b);
-  double* raz = W.coef + r.az;
-  double* rbz = W.coef + r.bz;
+  const Opnd A = opnd(coef, a), B = opnd(coef, b);
+  double* raz = coef + r.az;
+  double* rbz = coef + r.bz;
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll
   for (int k = 0; k < NZC; ++k) {
     if (!L.act[k]) continue;
-    const int j = L.lane + HW * k;
+    const int j = L.lane + 32 * k;
     double aa, ab, ba, bb;
     fetch(A, j, aa, ab);
     fetch(B, j, ba, bb);
@@ -343,12 +317,33 @@ __device__ __forceinline__ void op_addsub(FlowSmem& W, Slot& r, const Slot& a, c
     s1 += fabs(ra);
     s2 += fabs(rb);
   }
-  wsum2(s1, s2, L.mask);
+  wsum2(s1, s2);
   set_scalars(r, c, at, rem, s1, s2);
 }
 
+// r = a, a view materialized into a stored row (no reference counterpart: the
+// reference's views are ordinary TMExpr values).
+__device__ __noinline__ void op_copy(double* coef, Slot& r, const Slot& a, const Lane L) {
+  const Opnd A = opnd(coef, a);
+  double* raz = coef + r.az;
+  double* rbz = coef + r.bz;
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NZC; ++k) {
+    if (!L.act[k]) continue;
+    const int j = L.lane + 32 * k;
+    double aa, ab;
+    fetch(A, j, aa, ab);
+    raz[j] = aa;
+    rbz[j] = ab;
+    s1 += fabs(aa);
+    s2 += fabs(ab);
+  }
+  wsum2(s1, s2);
+  set_scalars(r, a.c, a.at, Iv{a.rlo, a.rhi}, s1, s2);
+}
+
 // r = view of u scaled by s: r.az = (u.az * s) (taylor_model.hpp:284-295).
-// A view of a view adds the second scale (the reference's two roundings).
 __device__ __forceinline__ void make_view(Slot& r, const Slot& u, double s) {
   r.az = u.az;
   r.bz = u.bz;
@@ -367,30 +362,43 @@ __device__ __forceinline__ void make_view(Slot& r, const Slot& u, double s) {
 //   REPLAY    I1_i = range(seed_i + Int dx_i - p_k,i) (:154-165)
 //   ENDPOINT  x(h)_i = seed_i + h (dx_i(0) + h/2 dx_i') to the state's HBM rows (:241-257)
 // Returns the tme_inv "throw" (taylor_model.hpp:367-368).
-__device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, const Lane L, double* gM) {
+__device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const Lane L, double* gM) {
   bool thrown = false;
   const double h = L.h;
   const int lane = L.lane;
-  TOp next = kQuadTape[0];
-  for (int pc = 0;; ++pc) {
+  double* coef = W.coef();
+  TOp next = kProgs[prog];
+  for (int pc = prog;; ++pc) {
     const TOp op = next;
     if (op.code == OP_END) break;
-    next = kQuadTape[pc + 1];  // dispatch of the next op overlaps this one
+    next = kProgs[pc + 1];  // dispatch of the next op overlaps this one
     switch (op.code) {
       case OP_MUL:
-        op_mul(W, W.D[op.dst], W.D[op.a], W.D[op.b], L);
+        op_mul(coef, W.D[op.dst], W.D[op.a], W.D[op.b], L);
         break;
       case OP_ADD:
       case OP_SUB:
-        op_addsub(W, W.D[op.dst], W.D[op.a], W.D[op.b], op.code == OP_SUB, L);
+        op_addsub(coef, W.D[op.dst], W.D[op.a], W.D[op.b], op.code == OP_SUB, L);
+        break;
+      case OP_COPY:
+        op_copy(coef, W.D[op.dst], W.D[op.a], L);
         break;
       case OP_SUBK:
-        W.D[op.dst].c = W.D[op.dst].c - kc[op.b];
+        W.D[op.dst].c = W.D[op.dst].c - W.kc[op.b];
         break;
+      case OP_CONST: {  // tme_const (taylor_model.hpp:240-243)
+        Slot& r = W.D[op.dst];
+        set_scalars(r, W.kc[op.b], 0.0, Iv{0.0, 0.0}, 0.0, 0.0);
+        r.az = W.off_zero;
+        r.bz = W.off_zero;
+        r.view = 0;
+        r.s1 = r.s2 = 1.0;
+        break;
+      }
       case OP_SCALE: {  // TM * s (taylor_model.hpp:297-300)
         const Slot& u = W.D[op.a];
         Slot& r = W.D[op.dst];
-        const double s = kc[op.b];
+        const double s = W.kc[op.b];
         const Iv rem = iscale(s, Iv{u.rlo, u.rhi});
         set_scalars(r, u.c * s, u.at * s, rem, fabs(s) * u.sz, fabs(s) * u.sb);
         make_view(r, u, s);
@@ -435,17 +443,17 @@ __device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, 
         const int i = op.dst;
         const bool zero = op.code == OP_CONS0;
         const Slot& f = W.D[zero ? 0 : op.a];
-        const Opnd F = opnd(W.coef, f);
+        const Opnd F = opnd(coef, f);
         const double fc = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at;
         const double fsz = zero ? 0.0 : f.sz, fsb = zero ? 0.0 : f.sb;
         const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
-        double* S = W.coef + OFF_S + i * NZP;
-        double* Pb = W.coef + pbz_off(i);
+        const double* S = coef + i * NZP;
+        double* Pb = coef + W.pbz[i];
         if (mode == MODE_ENDPOINT) {
 #pragma unroll
           for (int k = 0; k < NZC; ++k) {
             if (!L.act[k]) continue;
-            const int j = lane + HW * k;
+            const int j = lane + 32 * k;
             double fa = 0.0, fb = 0.0;
             if (!zero) fetch(F, j, fa, fb);
             gM[i * NZP + j] = S[j] + h * (fa + fb * h * 0.5);
@@ -461,13 +469,13 @@ __device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, 
         rem = iadd(rem, Iv{-bb, bb});
         rem = iadd(rem, imul(fr, Iv{0.0, h}));
         if (mode == MODE_PICARD) {
-          if (i >= 3 && i < 3 + NPB) {  // rows 0..2 / 12..15: bz aliases S_{i+3} / zeros
+          if (W.own[i]) {  // aliased rows: bz is S_j or 0 by construction
 #pragma unroll
             for (int k = 0; k < NZC; ++k) {
               if (!L.act[k]) continue;
-              const int j = lane + HW * k;
-              double fa, fb;
-              fetch(F, j, fa, fb);
+              const int j = lane + 32 * k;
+              double fa = 0.0, fb;
+              if (!zero) fetch(F, j, fa, fb);
               Pb[j] = fa;
             }
           }
@@ -477,12 +485,12 @@ __device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, 
 #pragma unroll
           for (int k = 0; k < NZC; ++k) {
             if (!L.act[k]) continue;
-            const int j = lane + HW * k;
+            const int j = lane + 32 * k;
             double fa = 0.0, fb;
             if (!zero) fetch(F, j, fa, fb);
             s2 += fabs(fa - Pb[j]);
           }
-          s2 = wsum(s2, L.mask);
+          s2 = wsum(s2);
           const Slot& pk = W.D[i];
           const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
           W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc - pk.at, s2, h), rem);
@@ -496,17 +504,17 @@ __device__ __noinline__ bool run_field(FlowSmem& W, const double* kc, int mode, 
   return thrown;
 }
 
-__device__ __forceinline__ void emit_box(const CTParams& P, long long b, int k, int d, double lo, double hi) {
+__device__ __forceinline__ void emit_box(const CTParams& P, long long b, int k, int na, int d, double lo, double hi) {
   if (!P.split) {
-    const size_t o = (static_cast<size_t>(b) * P.T + k) * NA + d;
+    const size_t o = (static_cast<size_t>(b) * P.T + k) * na + d;
     P.out_lo[o] = lo;
     P.out_hi[o] = hi;
   } else {
-    if (lo == lo) atomicMin(&P.hull_lo[k * NA + d], order_key(lo));
-    if (hi == hi) atomicMax(&P.hull_hi[k * NA + d], order_key(hi));
+    if (lo == lo) atomicMin(&P.hull_lo[k * na + d], order_key(lo));
+    if (hi == hi) atomicMax(&P.hull_hi[k * na + d], order_key(hi));
     if (P.part_begin + b == 0) {
-      if (lo != lo) P.hull_nan0[(k * NA + d) * 2 + 0] = 1;
-      if (hi != hi) P.hull_nan0[(k * NA + d) * 2 + 1] = 1;
+      if (lo != lo) P.hull_nan0[(k * na + d) * 2 + 0] = 1;
+      if (hi != hi) P.hull_nan0[(k * na + d) * 2 + 1] = 1;
     }
     if (!(isfinite(lo) && isfinite(hi))) atomicOr(&P.hull_div[k], 1);
   }
@@ -530,163 +538,374 @@ __device__ __forceinline__ void finalize(const CTParams& P, long long b, int nb,
   }
 }
 
-// symbolic_step's queue push + fold_overflow (flowpipe_ct.hpp:378-409,
-// 347-348) on rows of stride `ld`: the fresh block diag(rad) joins the queue;
-// if the queue overflows, the oldest block (columns [p0, p0 + NA)) is boxed
-// into the fresh block's diagonal and dropped.  The oldest block's row sums
-// are taken first and the fresh block is written after the shift, so rows
-// never exceed nz + NA - NA columns: newest(i,i) = rad_i + row_abs_sum(oldest, i),
-// the reference's one addition.  Lane i < NA sweeps row i sequentially.
-template <class RowPtr>
-__device__ __forceinline__ void push_fresh_fold(RowPtr row, const Iv* erem, int p0, int& nz, int& nq, int cap,
-                                                int lane, unsigned mask) {
-  __syncwarp(mask);
+// Initial box of sample b, dimension d: a batch row, or part b of split_box
+// (refine.hpp:83-115, last dimension fastest).
+__device__ __forceinline__ void x0_box(const CTParams& P, long long b, int d, double& lo, double& hi) {
+  if (P.split) {
+    long long p = P.part_begin + b;
+    for (int e = P.n - 1; e >= 0; --e) {
+      const int k = P.counts[e];
+      const int i = static_cast<int>(p % k);
+      p /= k;
+      if (e == d) {
+        const double xl = P.sx_lo[e], xh = P.sx_hi[e];
+        lo = (i == 0) ? xl : xl + (xh - xl) * (static_cast<double>(i) / k);
+        hi = (i + 1 == k) ? xh : xl + (xh - xl) * (static_cast<double>(i + 1) / k);
+      }
+    }
+  } else {
+    lo = P.x0_lo[b * P.n + d];
+    hi = P.x0_hi[b * P.n + d];
+  }
+}
+
+// symbolic_step's queue push + fold_overflow, hull branch (flowpipe_ct.hpp:
+// 378-409, 347-348), for a non-square G0 (cl_reach): the fresh block
+// diag(rad) joins the queue; if the queue overflows, the oldest block
+// (columns [p0, p0 + na)) is boxed into the fresh block's diagonal and dropped.
+// The oldest block's row sums are taken first and the fresh block is written
+// after the shift, so rows never exceed nz columns: newest(i,i) = rad_i +
+// row_abs_sum(oldest, i), the reference's one addition.  Lane i sweeps row i.
+__device__ __forceinline__ void push_fresh_fold(double* S, const Iv* erem, int na, int p0, int& nz, int& nq, int cap,
+                                                int lane) {
+  __syncwarp();
   const bool fold = nq + 1 > cap;
   double add = 0.0;
-  if (fold && lane < NA)
-    for (int j = 0; j < NA; ++j) add += fabs(row(lane)[p0 + j]);
-  __syncwarp(mask);
+  if (fold && lane < na)
+    for (int j = 0; j < na; ++j) add += fabs(S[lane * NZP + p0 + j]);
+  __syncwarp();
   if (fold) {
-    for (int i = 0; i < NA; ++i) {
+    for (int i = 0; i < na; ++i) {
       double v[NZC];
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
-        const int j = lane + HW * k;
-        v[k] = (j >= p0 && j + NA < nz) ? row(i)[j + NA] : 0.0;
+        const int j = lane + 32 * k;
+        v[k] = (j >= p0 && j + na < nz) ? S[i * NZP + j + na] : 0.0;
       }
-      __syncwarp(mask);
+      __syncwarp();
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
-        const int j = lane + HW * k;
-        if (j >= p0 && j < nz) row(i)[j] = v[k];
+        const int j = lane + 32 * k;
+        if (j >= p0 && j < nz) S[i * NZP + j] = v[k];
       }
     }
-    nz -= NA;
+    nz -= na;
     nq -= 1;
   }
-  __syncwarp(mask);
-  for (int i = 0; i < NA; ++i) {
-    const double ai = fold ? __shfl_sync(mask, add, i, HW) : 0.0;
+  __syncwarp();
+  for (int i = 0; i < na; ++i) {
+    const double ai = fold ? __shfl_sync(0xffffffffu, add, i) : 0.0;
+    const double rad = (erem[i].hi - erem[i].lo) * 0.5;
 #pragma unroll
     for (int k = 0; k < NZC; ++k) {
-      const int j = lane + HW * k;
-      const double rad = (erem[i].hi - erem[i].lo) * 0.5;
-      if (j >= nz && j < nz + NA) row(i)[j] = (j - nz == i) ? (fold ? rad + ai : rad) : 0.0;
+      const int j = lane + 32 * k;
+      if (j >= nz && j < nz + na) S[i * NZP + j] = (j - nz == i) ? (fold ? rad + ai : rad) : 0.0;
     }
   }
-  nz += NA;
+  nz += na;
   nq += 1;
-  __syncwarp(mask);
+  __syncwarp();
+}
+
+// symbolic_step + fold_overflow for a square G0 (ct_reach, flowpipe_ct.hpp:
+// 317-346, 378-409): push the fresh block diag(rad); if the queue overflows
+// (at most once per step: the queue held <= cap blocks), solve G0 X = Q_old
+// by partial-pivot elimination (linalg.hpp:96-132: first maximum wins, pivot
+// tolerance 1e-12, separate roundings), and if max_j rowabs(X)_j (1+1e-12) <= 1
+// scale G0's columns by 1 + r_j and box the residual G0 X - Q_old into the
+// fresh block's diagonal, else box Q_old itself (:347-348); then drop Q_old.
+// Lane j < n + n holds column j of [G0 | Q_old] in registers; pivots and
+// multipliers travel by shuffles.  Straight-line control flow throughout (no
+// data-dependent loop exits), so the compiler keeps the warp provably
+// converged for the shuffles of the surrounding flowpipe code.
+__device__ __noinline__ void push_fresh_fold_square(double* S, const Iv* erem, int n, int& nz, int& nq, int cap,
+                                                    double* scratch, int lane) {
+  __syncwarp();
+  for (int i = 0; i < n; ++i) {
+    const double rad = (erem[i].hi - erem[i].lo) * 0.5;
+#pragma unroll
+    for (int k = 0; k < NZC; ++k) {
+      const int j = lane + 32 * k;
+      if (j >= nz && j < nz + n) S[i * NZP + j] = (j - nz == i) ? rad : 0.0;
+    }
+  }
+  nz += n;
+  nq += 1;
+  __syncwarp();
+  const bool fold = nq > cap;
+  const int w = n, nc = 2 * n;
+  const int off_new = nz - n;  // the fresh (newest) block
+  double col[NA];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) col[i] = (fold && lane < nc && i < n) ? S[i * NZP + lane] : 0.0;
+  bool ok = fold;
+  for (int kk = 0; kk < NA; ++kk) {
+    const bool live = ok && kk < n;
+    int piv = kk;
+    double best = 0.0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const double v = fabs(col[i]);
+      if (i == kk) best = v;
+      if (i > kk && i < n && v > best) {
+        best = v;
+        piv = i;
+      }
+    }
+    piv = __shfl_sync(0xffffffffu, piv, kk & 31);
+    best = __shfl_sync(0xffffffffu, best, kk & 31);
+    ok = ok && (!live || best > 1e-12);
+    const bool go = live && ok;
+    double vk = 0.0, vp = 0.0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (i == kk) vk = col[i];
+      if (i == piv) vp = col[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      if (go && piv != kk && i == kk) col[i] = vp;
+      if (go && piv != kk && i == piv) col[i] = vk;
+    }
+    double akk = 0.0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i)
+      if (i == kk) akk = col[i];
+    double f[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) f[i] = (go && i > kk && i < n) ? __ddiv_rn(col[i], akk) : 0.0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) f[i] = __shfl_sync(0xffffffffu, f[i], kk & 31);
+    double mk = 0.0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i)
+      if (i == kk) mk = col[i];
+    if (go && lane < nc && lane >= kk) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i)
+        if (i > kk && i < n) col[i] = sub(col[i], mul(f[i], mk));
+    }
+  }
+  double* M = scratch;       // [n][nc] eliminated [U | B']
+  double* X = M + n * nc;    // [n][w]
+  double* E = X + n * w;     // [n][w]
+  double* rr = E + n * w;    // [n]
+  if (ok && lane < nc)
+#pragma unroll
+    for (int i = 0; i < NA; ++i)
+      if (i < n) M[i * nc + lane] = col[i];
+  __syncwarp();
+  if (ok && lane >= n && lane < nc) {  // back substitution, lane n+j owns right-hand side j
+    const int jc = lane - n;
+    double x[NA];
+#pragma unroll
+    for (int i = NA - 1; i >= 0; --i) {
+      if (i < n) {
+        double a = col[i];
+#pragma unroll
+        for (int kk = i + 1; kk < NA; ++kk)
+          if (kk < n) a = sub(a, mul(M[i * nc + kk], x[kk]));
+        x[i] = __ddiv_rn(a, M[i * nc + i]);
+        X[i * w + jc] = x[i];
+      } else {
+        x[i] = 0.0;
+      }
+    }
+  }
+  __syncwarp();
+  if (ok && lane < n) {
+    double s = 0.0;
+    for (int j = 0; j < w; ++j) s = add(s, fabs(X[lane * w + j]));
+    rr[lane] = mul(s, 1.0 + 1e-12);
+  }
+  __syncwarp();
+  double worst = 0.0;
+  for (int j = 0; ok && j < n; ++j) worst = smax(worst, rr[j]);
+  const bool absorb = ok && worst <= 1.0;
+  if (absorb && lane < w)  // residual e = G0 X - Q_old
+    for (int i = 0; i < n; ++i) {
+      double e = 0.0;
+      for (int kk = 0; kk < n; ++kk) e = add(e, mul(S[i * NZP + kk], X[kk * w + lane]));
+      E[i * w + lane] = sub(e, S[i * NZP + n + lane]);
+    }
+  __syncwarp();
+  if (fold && lane < n) {
+    double s = 0.0;
+    if (absorb) {
+      const double sc = add(1.0, rr[lane]);
+      for (int i = 0; i < n; ++i) S[i * NZP + lane] = mul(S[i * NZP + lane], sc);
+      for (int j = 0; j < w; ++j) s = add(s, fabs(E[lane * w + j]));
+      s = mul(s, 1.0 + 1e-12);
+    } else {
+      for (int j = 0; j < w; ++j) s = add(s, fabs(S[lane * NZP + n + j]));
+    }
+    S[lane * NZP + off_new + lane] = add(S[lane * NZP + off_new + lane], s);
+  }
+  __syncwarp();
+  // drop Q_old: columns [2n, nz) -> [n, nz - n)
+  if (fold) {
+    for (int i = 0; i < n; ++i) {
+      double v[NZC];
+#pragma unroll
+      for (int k = 0; k < NZC; ++k) {
+        const int j = lane + 32 * k;
+        v[k] = (j >= n && j + n < nz) ? S[i * NZP + j + n] : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < NZC; ++k) {
+        const int j = lane + 32 * k;
+        if (j >= n && j < nz) S[i * NZP + j] = v[k];
+      }
+    }
+    nz -= n;
+    nq -= 1;
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
-// k_atomic flowpipe steps of one control interval; HW lanes own one sub-box
-// (RB_CT_HW = 16 packs two per warp, so each warp-uniform instruction -- the
-// scalar interval arithmetic, the program dispatch -- serves two; the default
-// 32 keeps one per warp, which measured faster: the kernel is latency-bound
-// and wants warps, profiles/r01_c2_summary.md).
+// Flowpipe steps, one warp per sub-box: k_atomic steps of one control
+// interval (cl_reach, SQUARE = false) or the whole horizon (ct_reach, SQUARE =
+// true).  Two instantiations: the square fold's shuffles otherwise cost the
+// cl_reach kernel the compiler's proof of warp convergence (collective
+// shuffle fallbacks everywhere, +35 % time).
+template <bool SQUARE>
 __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
   extern __shared__ __align__(16) unsigned char ct_smem[];
-  const int half = threadIdx.x / HW;
-  const int lane = threadIdx.x % HW;
-  const unsigned mask = (HW == 32) ? 0xffffffffu : (((1u << HW) - 1u) << (HW * half));
-  FlowSmem& W = reinterpret_cast<FlowSmem*>(ct_smem)[half];
-  const long long b = static_cast<long long>(SPW) * blockIdx.x + half;
+  FlowSmem& W = *reinterpret_cast<FlowSmem*>(ct_smem);
+  double* coef = W.coef();
+  const long long b = blockIdx.x;
   if (b >= Pm.B) return;
+  const int lane = threadIdx.x;
+  const int na = SQUARE ? Pm.na : NA, p0 = Pm.n;  // cl_reach: the augmented quadrotor, 16 rows
+  const bool init = Pm.ct && Pm.ci == 0;
   int* meta = Pm.st_meta + b * 4;
-  int nq = meta[0], status = meta[1], fstep = meta[2], nboxes = meta[3];
+  int nq = 0, status = CT_OK, fstep = -1, nboxes = 0;
+  if (!init) {
+    nq = meta[0];
+    status = meta[1];
+    fstep = meta[2];
+    nboxes = meta[3];
+  }
   const bool last = (Pm.ci + 1 == Pm.ctl_steps);
   if (status != CT_OK) {
     if (last && lane == 0) finalize(Pm, b, nboxes, status, fstep);
     return;
   }
   const double h = Pm.h;
-  const int p0 = Pm.n;
   const int cap = Pm.window > 0 ? Pm.window : 1;
-  int nz = p0 + nq * NA;
+  int nz = p0 + nq * Pm.bw;
   double* gM = Pm.st_M + static_cast<size_t>(b) * NA * NZP;
-  // state in, every coefficient row zeroed beyond nz (ops never write there)
-  for (int t = lane; t < NA * NZP; t += HW) {
-    const int j = t % NZP;
-    W.coef[OFF_S + t] = (j < nz) ? gM[t] : 0.0;
+  // ---- the field program, its constants and the row layout
+  int npb = 0;
+  for (int i = 0; i < na; ++i) npb += (Pm.bzsrc[i] == -1);
+  const int off_zero = na * NZP, off_pbz = off_zero + NZP, off_taz = off_pbz + npb * NZP,
+            off_tbz = off_taz + NTF * NZP, coef_end = off_tbz + NTF * NZP;
+  if (lane < kMaxKc) W.kc[lane] = Pm.kc[lane];
+  if (lane == 0) {
+    W.na = na;
+    W.off_zero = off_zero;
+    W.off_pbz = off_pbz;
+    W.off_taz = off_taz;
+    W.off_tbz = off_tbz;
+    int q = 0;
+    for (int i = 0; i < na; ++i) {
+      const int src = Pm.bzsrc[i];
+      W.own[i] = (src == -1);
+      W.pbz[i] = (src == -1) ? off_pbz + (q++) * NZP : (src == -2) ? off_zero : src * NZP;
+    }
+    for (int i = 0; i < 8; ++i) W.wid[i] = Pm.bw;
   }
-  for (int t = lane; t < (NPB + 1) * NZP + 2 * NTF * NZP; t += HW) W.coef[OFF_PBZ + t] = 0.0;
-  if (lane < NA) W.sc[lane] = Pm.st_c[b * NA + lane];
-  if (lane < 8) W.kc[lane] = Pm.kc[lane];
-  for (int s = 0; s < NSLOT; ++s) {  // stored rows: P_i = (S_i, Pbz_i), T_t
+  for (int s = lane; s < NSLOT; s += 32) {
     Slot& d = W.D[s];
     d.s1 = 1.0;
     d.s2 = 1.0;
     d.view = 0;
-    if (s < NA) {
-      d.az = OFF_S + s * NZP;
-      d.bz = pbz_off(s);
-    } else if (s < SLOT_V) {
-      d.az = OFF_TAZ + (s - SLOT_T) * NZP;
-      d.bz = OFF_TBZ + (s - SLOT_T) * NZP;
-    } else {
-      d.az = OFF_TAZ;
-      d.bz = OFF_TBZ;
-    }
+    d.az = (s < SLOT_T) ? s * NZP : (s < SLOT_V) ? off_taz + (s - SLOT_T) * NZP : off_zero;
+    d.bz = (s < SLOT_V && s >= SLOT_T) ? off_tbz + (s - SLOT_T) * NZP : off_zero;
   }
-  __syncwarp(mask);
+  // ---- the state: from X0 (ct_reach, init_symbolic_state, flowpipe_ct.hpp:302-309) or HBM
+  for (int t = lane; t < coef_end; t += 32) coef[t] = 0.0;
+  __syncwarp();
+  for (int s = lane; s < NA; s += 32)
+    if (s < na) W.D[s].bz = W.pbz[s];
+  if (init) {
+    double lo = 0.0, hi = 0.0;
+    if (lane < na) {
+      x0_box(Pm, b, lane, lo, hi);
+      W.sc[lane] = (lo + hi) * 0.5;
+      coef[lane * NZP + lane] = (hi - lo) * 0.5;
+      emit_box(Pm, b, 0, na, lane, lo, hi);  // box 0 is X0 itself (flowpipe_ct.hpp:433)
+    }
+    nboxes = 1;
+  } else {
+    for (int i = 0; i < na; ++i)
+#pragma unroll
+      for (int k = 0; k < NZC; ++k) {
+        const int j = lane + 32 * k;
+        if (j < nz) coef[i * NZP + j] = gM[i * NZP + j];
+      }
+    if (lane < na) W.sc[lane] = Pm.st_c[b * NA + lane];
+  }
+  __syncwarp();
 
   Lane L;
   L.lane = lane;
-  L.mask = mask;
   L.h = h;
   for (int step = 0; step < Pm.K && status == CT_OK; ++step) {
     const int gstep = Pm.ci * Pm.K + step;
 #pragma unroll
-    for (int k = 0; k < NZC; ++k) L.act[k] = (lane + HW * k) < nz;
+    for (int k = 0; k < NZC; ++k) L.act[k] = (lane + 32 * k) < nz;
     // seed rows: abs_z (cached: the Picard rows share their z columns)
-    for (int i = 0; i < NA; i += 2) {
+    for (int i = 0; i < na; i += 2) {
       double s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
         if (!L.act[k]) continue;
-        const int j = lane + HW * k;
-        s1 += fabs(W.coef[OFF_S + i * NZP + j]);
-        s2 += fabs(W.coef[OFF_S + (i + 1) * NZP + j]);
+        const int j = lane + 32 * k;
+        s1 += fabs(coef[i * NZP + j]);
+        if (i + 1 < na) s2 += fabs(coef[(i + 1) * NZP + j]);
       }
-      wsum2(s1, s2, L.mask);
+      wsum2(s1, s2);
       W.ssz[i] = s1;
-      W.ssz[i + 1] = s2;
+      if (i + 1 < na) W.ssz[i + 1] = s2;
     }
-    // poly_picard (flowpipe_ct.hpp:126-139): g_0 = seed (bz = 0, at = 0, rem = 0)
-    for (int i = 0; i < NA; ++i) {
-      if (i >= 3 && i < 3 + NPB)  // (rows 0..2 alias S: never read before their first Picard update)
+    // poly_picard (flowpipe_ct.hpp:126-139): g_0 = seed (bz = 0, at = 0, rem = 0);
+    // aliased rows are never read before their first update
+    for (int i = 0; i < na; ++i) {
+      if (W.own[i])
 #pragma unroll
         for (int k = 0; k < NZC; ++k)
-          if (L.act[k]) W.coef[pbz_off(i) + lane + HW * k] = 0.0;
+          if (L.act[k]) coef[W.pbz[i] + lane + 32 * k] = 0.0;
       set_scalars(W.D[i], W.sc[i], 0.0, Iv{0.0, 0.0}, W.ssz[i], 0.0);
     }
     bool thrown = false;
-    for (int it = 0; it < Pm.order && !thrown; ++it) thrown = run_field(W, W.kc, MODE_PICARD, L, gM);
+    for (int it = 0; it < Pm.order && !thrown; ++it) thrown = run_field(W, Pm.prog, MODE_PICARD, L, gM);
     int fail = thrown ? CT_TME_INV : CT_OK;
     if (fail == CT_OK)
-      for (int i = 0; i < NA; ++i)
+      for (int i = 0; i < na; ++i)
         if (!isfinite(W.D[i].c)) fail = CT_PICARD;
     // remainder_picard (flowpipe_ct.hpp:144-276)
     auto replay = [&](const Iv* cand) {
-      for (int i = 0; i < NA; ++i) {
+      for (int i = 0; i < na; ++i) {
         W.D[i].rlo = cand[i].lo;
         W.D[i].rhi = cand[i].hi;
       }
-      return run_field(W, W.kc, MODE_REPLAY, L, gM);
+      return run_field(W, Pm.prog, MODE_REPLAY, L, gM);
     };
     auto finite_box = [&](const Iv* x) {
       bool ok = true;
-      for (int i = 0; i < NA; ++i) ok = ok && ifin(x[i]);
+      for (int i = 0; i < na; ++i) ok = ok && ifin(x[i]);
       return ok;
     };
     auto subset = [&](const Iv* in, const Iv* out) {
       bool ok = true;
-      for (int i = 0; i < NA; ++i) ok = ok && (out[i].lo <= in[i].lo && in[i].hi <= out[i].hi);
+      for (int i = 0; i < na; ++i) ok = ok && (out[i].lo <= in[i].lo && in[i].hi <= out[i].hi);
       return ok;
     };
     if (fail == CT_OK) {
-      for (int i = 0; i < NA; ++i) {
+      for (int i = 0; i < na; ++i) {
         W.i0[i] = Iv{-Pm.eps, Pm.eps};
         W.i1[i] = Iv{0.0, 0.0};
       }
@@ -694,12 +913,12 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
       for (int attempt = 0; attempt <= Pm.maxe; ++attempt) {
         const bool threw = replay(W.i0);
         if (!threw)
-          for (int i = 0; i < NA; ++i) W.i1[i] = W.nx[i];
+          for (int i = 0; i < na; ++i) W.i1[i] = W.nx[i];
         if (!threw && finite_box(W.i1) && subset(W.i1, W.i0)) {
           accepted = true;
           break;
         }
-        for (int i = 0; i < NA; ++i) {  // per-dimension adaptive enlargement (:178-182)
+        for (int i = 0; i < na; ++i) {  // per-dimension adaptive enlargement (:178-182)
           const Iv ind = threw ? Iv{0.0, 0.0} : W.i1[i];
           const Iv cur = W.i0[i];
           const Iv hull = (ind.lo <= ind.hi) ? Iv{smin(cur.lo, ind.lo), smax(cur.hi, ind.hi)} : cur;
@@ -713,21 +932,21 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
       for (int round = 0; round < Pm.refine; ++round) {  // shrink (:214-223)
         if (replay(W.i1)) break;
         if (!(finite_box(W.nx) && subset(W.nx, W.i1))) break;
-        for (int i = 0; i < NA; ++i) W.i1[i] = W.nx[i];
+        for (int i = 0; i < na; ++i) W.i1[i] = W.nx[i];
       }
       // endpoint by exact integration at tau = h (:236-263) into the HBM state rows
-      for (int i = 0; i < NA; ++i) {
+      for (int i = 0; i < na; ++i) {
         W.D[i].rlo = W.i1[i].lo;
         W.D[i].rhi = W.i1[i].hi;
       }
-      const bool threw = run_field(W, W.kc, MODE_ENDPOINT, L, gM);
+      const bool threw = run_field(W, Pm.prog, MODE_ENDPOINT, L, gM);
       bool exact_ok = !threw && finite_box(W.erem);
-      for (int i = 0; i < NA; ++i) exact_ok = exact_ok && isfinite(W.ec[i]);
+      for (int i = 0; i < na; ++i) exact_ok = exact_ok && isfinite(W.ec[i]);
       // tm_eval_interval(segment, [0, h]) (taylor_model.hpp:73-97), before S changes
       bool fin = true;
       const int kbox = 1 + gstep;
       double blo = 0.0, bhi = 0.0;
-      for (int i = 0; i < NA; ++i) {
+      for (int i = 0; i < na; ++i) {
         const Slot& p = W.D[i];
         Iv acc{p.c - p.sz, p.c + p.sz};
         acc = iadd(acc, iscale(p.at, Iv{0.0, h}));
@@ -740,32 +959,42 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
           bhi = acc.hi;
         }
       }
-      if (lane < NA) emit_box(Pm, b, kbox, lane, blo, bhi);
+      if (lane < na) emit_box(Pm, b, kbox, na, lane, blo, bhi);
       nboxes = kbox + 1;
-      // new generator rows: the exact endpoint (HBM, L2-resident) or the fallback
-      // p_k(h) = seed + B h (:264-274), computed in place
-      for (int i = 0; i < NA; ++i) {
+      // new generator rows: the exact endpoint (HBM, L2-resident) or the
+      // fallback p_k(h) = seed + B h (:264-274), via HBM so aliased bz rows
+      // are read before any seed row changes
+      if (!exact_ok) {
+        for (int i = 0; i < na; ++i) {
 #pragma unroll
-        for (int k = 0; k < NZC; ++k) {
-          if (!L.act[k]) continue;
-          const int j = lane + HW * k;
-          double& s = W.coef[OFF_S + i * NZP + j];
-          s = exact_ok ? gM[i * NZP + j] : s + W.coef[pbz_off(i) + j] * h;  // (aliases read before update)
-        }
-        if (!exact_ok) {
+          for (int k = 0; k < NZC; ++k) {
+            if (!L.act[k]) continue;
+            const int j = lane + 32 * k;
+            gM[i * NZP + j] = coef[i * NZP + j] + coef[W.pbz[i] + j] * h;
+          }
           W.ec[i] = W.D[i].c + W.D[i].at * h;
           W.erem[i] = W.i1[i];
         }
       }
+      for (int i = 0; i < na; ++i)
+#pragma unroll
+        for (int k = 0; k < NZC; ++k) {
+          if (!L.act[k]) continue;
+          const int j = lane + 32 * k;
+          coef[i * NZP + j] = gM[i * NZP + j];
+        }
       if (!fin) {
         fail = CT_BOX;
       } else {
         // symbolic_step (flowpipe_ct.hpp:378-409)
         double c_new = 0.0;
-        if (lane < NA) c_new = W.ec[lane] + (W.erem[lane].lo + W.erem[lane].hi) * 0.5;
-        push_fresh_fold([&](int i) { return W.coef + OFF_S + i * NZP; }, W.erem, p0, nz, nq, cap, lane, mask);
-        if (lane < NA) W.sc[lane] = c_new;
-        __syncwarp(mask);
+        if (lane < na) c_new = W.ec[lane] + (W.erem[lane].lo + W.erem[lane].hi) * 0.5;
+        if constexpr (SQUARE)
+          push_fresh_fold_square(coef, W.erem, na, nz, nq, cap, coef + off_pbz, lane);
+        else
+          push_fresh_fold(coef, W.erem, na, p0, nz, nq, cap, lane);
+        if (lane < na) W.sc[lane] = c_new;
+        __syncwarp();
       }
     }
     if (fail != CT_OK) {
@@ -774,9 +1003,14 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     }
   }
   // state out
-  __syncwarp(mask);
-  for (int t = lane; t < NA * NZP; t += HW) gM[t] = W.coef[OFF_S + t];
-  if (lane < NA) Pm.st_c[b * NA + lane] = W.sc[lane];
+  __syncwarp();
+  for (int i = 0; i < na; ++i)
+#pragma unroll
+    for (int k = 0; k < NZC; ++k) {
+      const int j = lane + 32 * k;
+      if (j < NZP) gM[i * NZP + j] = (j < nz) ? coef[i * NZP + j] : 0.0;
+    }
+  if (lane < na) Pm.st_c[b * NA + lane] = W.sc[lane];
   if (lane == 0) {
     meta[0] = nq;
     meta[1] = status;
@@ -1101,7 +1335,7 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
         r += rq;
       }
       const double c = gc[lane];
-      emit_box(Pm, b, 0, lane, c - r, c + r);
+      emit_box(Pm, b, 0, NA, lane, c - r, c + r);
     }
     nboxes = 1;
   }

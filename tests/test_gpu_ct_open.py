@@ -1,0 +1,87 @@
+"""GPU parity for the open-loop continuous-time flowpipe (ct_reach, flowpipe_ct.hpp:428-458) through
+the C ABI vs the CPU oracle (oracle/ct_oracle.c, pinned bit for bit to the reference in
+tests/test_oracle_ct_open.py), plus the reference's own flowpipe test properties
+(tests/test_flowpipe_ct.cpp:146-316).  Tolerance as tests/test_gpu_ct.py: CT_RTOL = 1e-9."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from ct_open_cases import ct_open_cases
+from oracle_bind import oracle_ct_batch
+from paper_2605_25346_b200.api import (FlowpipeParams, ct_reach, ct_reach_batch_arrays, diag_linear_field,
+                                       quadrotor_field, rotation_field, zero_field)
+from test_gpu_ct import CT_RTOL, _quad_rhs, assert_ct_close
+
+
+@pytest.mark.parametrize("case", ct_open_cases(), ids=lambda c: c[0])
+def test_ct_matches_oracle(case):
+    name, f, lo, hi, prm, expect_fail = case
+    exp = oracle_ct_batch(f, lo, hi, prm)
+    got = ct_reach_batch_arrays(f, lo, hi, prm)
+    worst = assert_ct_close(got, exp)
+    print(f"{name}: max rel diff {worst:.3e}")
+    assert bool((got.status != 0).any()) == expect_fail
+
+
+def test_zero_field_keeps_x0():  # test_flowpipe_ct.cpp:146-160
+    lo, hi = np.array([0.4, -0.45]), np.array([0.6, -0.05])
+    t = ct_reach(zero_field(2), (lo, hi), FlowpipeParams(h=0.05, steps=10))
+    assert t.steps() == 11 and not t.diverged
+    assert np.allclose(t.lo, lo, rtol=1e-12) and np.allclose(t.hi, hi, rtol=1e-12)
+
+
+def test_exp_decay_closed_form():  # :162-177
+    t = ct_reach(diag_linear_field([-1.0]), (np.array([0.9]), np.array([1.1])), FlowpipeParams(h=0.01, steps=100))
+    assert not t.diverged
+    lo, hi = t.lo[-1, 0], t.hi[-1, 0]
+    assert lo <= 0.9 * math.exp(-1.0) and hi >= 1.1 * math.exp(-1.0)
+    assert hi - lo <= 1.2 * (1.1 * math.exp(-0.99) - 0.9 * math.exp(-1.0))
+
+
+def test_rotation_soundness_and_wrapping():  # :179-234
+    x0 = (np.array([0.9, -0.1]), np.array([1.1, 0.1]))
+    t = ct_reach(rotation_field(1.0), x0, FlowpipeParams(h=0.05, steps=60))
+    assert not t.diverged
+    rng = np.random.default_rng(1029384756)
+    x = rng.uniform(x0[0], x0[1], size=(200, 2))
+    for k in range(1, t.steps()):
+        tt = t.t_hi[k]
+        xt = np.stack([x[:, 0] * np.cos(tt) - x[:, 1] * np.sin(tt), x[:, 0] * np.sin(tt) + x[:, 1] * np.cos(tt)], 1)
+        assert (xt >= t.lo[k]).all() and (xt <= t.hi[k]).all()
+    w = ct_reach(rotation_field(1.0), x0, FlowpipeParams(h=2 * math.pi / 100, steps=100))
+    assert not w.diverged and (w.hi[-1, 0] - w.lo[-1, 0]) <= 1.5 * 0.2
+
+
+def test_quadrotor_hover_monte_carlo():  # :252-282
+    prm = FlowpipeParams(h=0.01, steps=100)
+    r = np.array([0.05] * 6 + [0.0] * 6)
+    t = ct_reach(quadrotor_field(), (-r, r), prm)
+    assert not t.diverged and t.steps() == 101
+    rng = np.random.default_rng(8675309)
+    x = rng.uniform(-r, r, size=(50, 12)).T
+    u = np.array([9.81, 0.0, 0.0, 0.0])[:, None] * np.ones((1, 50))
+    prmq = [1.0, 9.81, 0.01, 0.01, 0.02]
+    sub = 40
+    dt = prm.h / sub
+    for k in range(1, t.steps()):
+        for _ in range(sub):
+            k1 = _quad_rhs(x, u, prmq)
+            k2 = _quad_rhs(x + 0.5 * dt * k1, u, prmq)
+            k3 = _quad_rhs(x + 0.5 * dt * k2, u, prmq)
+            k4 = _quad_rhs(x + dt * k3, u, prmq)
+            x = x + dt / 6.0 * (k1 + 2 * k2 + 2 * k3 + k4)
+        assert (x.T >= t.lo[k] - 1e-10).all() and (x.T <= t.hi[k] + 1e-10).all(), k
+
+
+def test_batch_rows_independent():
+    rng = np.random.default_rng(3)
+    c = rng.uniform(-0.1, 0.1, size=(37, 12))
+    r = np.array([0.02] * 6 + [0.01] * 6)
+    f = quadrotor_field()
+    prm = FlowpipeParams(h=0.01, steps=20)
+    full = ct_reach_batch_arrays(f, c - r, c + r, prm)
+    one = ct_reach_batch_arrays(f, (c - r)[17:18], (c + r)[17:18], prm)
+    assert np.array_equal(full.lo[17], one.lo[0]) and np.array_equal(full.hi[17], one.hi[0])

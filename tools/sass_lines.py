@@ -15,6 +15,7 @@ import tempfile
 def main():
     rep, kname, so = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+    fname = sys.argv[5] if len(sys.argv) > 5 else kname  # function-name pattern in the disassembly
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass", "-k", f"regex:{kname}"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -31,7 +32,7 @@ def main():
     dis = ""
     for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
         d = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
-        if re.search(r"\.text\.\S*" + re.escape(kname.split("|")[0]), d):
+        if re.search(r"\.text\.\S*" + re.escape(fname.split("|")[0]), d):
             dis = d
             break
     # find function section by mangled-name match
@@ -41,7 +42,7 @@ def main():
     for ln in lines:
         m = re.match(r"\s*\.text\.(\S+):", ln)
         if m:
-            in_fn = kname.replace("<", "").split("(")[0] in m.group(1) or all(p in m.group(1) for p in kname.split("|"))
+            in_fn = fname.replace("<", "").split("(")[0] in m.group(1) or all(p in m.group(1) for p in fname.split("|"))
             continue
         if not in_fn:
             continue
