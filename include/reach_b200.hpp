@@ -16,6 +16,8 @@
 //   FlowpipeParams (flowpipe_ct.hpp:35-50)      reach_b200::FlowpipeParams
 //   ClosedLoopSpec / cl_reach (closed_loop.hpp) reach_b200::ClosedLoopSpec / cl_reach / cl_reach_batch
 //   reach_with_splitting(cl_reach)              reach_b200::reach_with_splitting_cl
+//   ct_reach + zero/diag_linear/rotation/       reach_b200::ct_reach / ct_reach_batch +
+//   quadrotor_field (flowpipe_ct.hpp, fields.hpp)  AnalyticField::{zero, diag_linear, rotation, quadrotor}
 //
 // For code that already holds the reference's own types, see
 // reach_b200_reference.hpp (drop-in overloads taking reach:: types).
@@ -389,6 +391,75 @@ inline ReachTube reach_with_splitting_cl(Context& ctx, const ClosedLoopSpec& spe
                        failure_reason(static_cast<int32_t>(key & 0xff));
   }
   return t;
+}
+
+// ---------------------------------------------------------------------------
+// Open-loop continuous-time flowpipes (ct_reach, flowpipe_ct.hpp:428-458) of the
+// analytic fields of fields.hpp: a descriptor, since a VectorField's closures
+// cannot run on the device.
+struct AnalyticField {
+  reach_field_desc d{};
+  static AnalyticField zero(int n) { return make(REACH_FIELD_ZERO, n, {}); }
+  static AnalyticField diag_linear(const std::vector<double>& lambda) {
+    return make(REACH_FIELD_DIAG_LINEAR, static_cast<int>(lambda.size()), lambda);
+  }
+  static AnalyticField rotation(double w) { return make(REACH_FIELD_ROTATION, 2, {w}); }
+  static AnalyticField quadrotor(const QuadrotorParams& p, const std::vector<double>& u) {
+    if (u.size() != 4) throw std::invalid_argument("quadrotor_field: 4 inputs");
+    return make(REACH_FIELD_QUADROTOR, 12, {p.mass, p.gravity, p.jx, p.jy, p.jz, u[0], u[1], u[2], u[3]});
+  }
+  int n() const { return d.n; }
+
+ private:
+  static AnalyticField make(int kind, int n, const std::vector<double>& prm) {
+    if (prm.size() > 16) throw std::invalid_argument("AnalyticField: too many parameters");
+    AnalyticField f;
+    f.d.kind = kind;
+    f.d.n = n;
+    for (size_t i = 0; i < prm.size(); ++i) f.d.params[i] = prm[i];
+    return f;
+  }
+};
+
+inline std::vector<ReachTube> ct_reach_batch(Context& ctx, const AnalyticField& f, const std::vector<Box>& x0s,
+                                             const FlowpipeParams& prm) {
+  std::vector<ReachTube> out(x0s.size());
+  if (x0s.empty()) return out;
+  const int B = static_cast<int>(x0s.size()), n = f.n(), T = 1 + prm.steps;
+  std::vector<double> lo(static_cast<size_t>(B) * n), hi(lo.size());
+  for (int b = 0; b < B; ++b) {
+    if (static_cast<int>(x0s[b].size()) != n) throw std::invalid_argument("ct_reach: X0 dimension mismatch");
+    for (int d = 0; d < n; ++d) {
+      lo[static_cast<size_t>(b) * n + d] = x0s[b][d].lo;
+      hi[static_cast<size_t>(b) * n + d] = x0s[b][d].hi;
+    }
+  }
+  reach_flowpipe_params fp{prm.h, prm.steps, prm.order, prm.eps_init, prm.refine_rounds,
+                           prm.enlargement, prm.max_enlargements, prm.window};
+  std::vector<double> olo(static_cast<size_t>(B) * T * n), ohi(olo.size());
+  std::vector<int32_t> nb(B), fs(B), st(B);
+  reach_tube_out o{olo.data(), ohi.data(), nb.data(), fs.data(), st.data()};
+  ctx.check(reach_ct_batch(ctx.raw(), &f.d, &fp, B, lo.data(), hi.data(), &o, 0), "ct_reach");
+  for (int b = 0; b < B; ++b) {
+    ReachTube& t = out[b];
+    for (int k = 0; k < nb[b]; ++k) {
+      Box box(n);
+      for (int d = 0; d < n; ++d) {
+        const size_t i = (static_cast<size_t>(b) * T + k) * n + d;
+        box[d] = {olo[i], ohi[i]};
+      }
+      t.boxes.push_back(std::move(box));
+      detail::ct_times(t, k, prm.h);
+    }
+    t.failed_step = fs[b];
+    t.diverged = st[b] != REACH_TUBE_OK;
+    t.failure_reason = st[b] != REACH_TUBE_OK ? failure_reason(st[b]) : "";
+  }
+  return out;
+}
+
+inline ReachTube ct_reach(Context& ctx, const AnalyticField& f, const Box& x0, const FlowpipeParams& prm) {
+  return ct_reach_batch(ctx, f, {x0}, prm).front();
 }
 
 }  // namespace reach_b200

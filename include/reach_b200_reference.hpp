@@ -134,4 +134,16 @@ inline reach::ReachTube<double> reach_with_splitting_cl(Context& ctx, const reac
   return to_reference(reach_with_splitting_cl(ctx, from_reference(spec, plant), from_reference(x0), SplitPlan{plan.counts}));
 }
 
+// reach::ct_reach(field, x0, prm) (flowpipe_ct.hpp:428-458) for the analytic
+// fields of fields.hpp, named by a descriptor (a VectorField's closures cannot
+// run on the device): e.g. reach::rotation_field<double>(w) ->
+// AnalyticField::rotation(w).
+inline reach::ReachTube<double> ct_reach(Context& ctx, const AnalyticField& f, const reach::IntervalBox<double>& x0,
+                                         const reach::FlowpipeParams& prm) {
+  prm.validate();
+  FlowpipeParams p{prm.h, prm.steps, prm.order, prm.eps_init, prm.refine_rounds, prm.enlargement,
+                   prm.max_enlargements, prm.window};
+  return to_reference(ct_reach(ctx, f, from_reference(x0), p));
+}
+
 }  // namespace reach_b200

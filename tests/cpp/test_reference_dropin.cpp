@@ -144,6 +144,42 @@ int main() {
       ++failures;
     }
   }
+  // ct_reach of the reference's own rotation / quadrotor-hover flowpipe tests (test_flowpipe_ct.cpp:179-282)
+  {
+    auto rel = [](const ReachTube<double>& a, const ReachTube<double>& b) {
+      if (a.steps() != b.steps() || a.diverged != b.diverged) return 1.0;
+      double worst = 0.0;
+      for (int k = 0; k < a.steps(); ++k)
+        for (int d = 0; d < a.boxes[k].size(); ++d) {
+          const auto& x = a.boxes[k][d];
+          const auto& y = b.boxes[k][d];
+          const double scale = std::fmax(std::fmax(std::fmax(std::fabs(x.lo), std::fabs(x.hi)), x.hi - x.lo), 1e-300);
+          worst = std::fmax(worst, std::fmax(std::fabs(x.lo - y.lo), std::fabs(x.hi - y.hi)) / scale);
+        }
+      return worst;
+    };
+    FlowpipeParams prm;
+    prm.h = 0.05;
+    prm.steps = 60;
+    auto x0 = box_from_center<double>({1.0, 0.0}, 0.1);
+    double r1 = rel(reach::ct_reach(rotation_field<double>(1.0), x0, prm),
+                    reach_b200::ct_reach(gpu, reach_b200::AnalyticField::rotation(1.0), x0, prm));
+    QuadrotorParams qp;
+    Vec<double> u = quadrotor_hover_input(qp);
+    Vec<double> rad(12, 0.0);
+    for (int j = 0; j < 6; ++j) rad[j] = 0.05;
+    auto qx0 = box_from_center(Vec<double>(12, 0.0), rad);
+    FlowpipeParams qprm;
+    qprm.h = 0.01;
+    qprm.steps = 100;
+    double r2 = rel(reach::ct_reach(quadrotor_field<double>(qp, u), qx0, qprm),
+                    reach_b200::ct_reach(gpu, reach_b200::AnalyticField::quadrotor({qp.mass, qp.gravity, qp.jx, qp.jy, qp.jz}, u),
+                                         qx0, qprm));
+    if (r1 > 1e-9 || r2 > 1e-9) {
+      std::printf("ct_reach: max rel diff rotation %.3e quadrotor %.3e\n", r1, r2);
+      ++failures;
+    }
+  }
   std::printf(failures ? "FAIL (%d)\n" : "OK: reference drop-in parity\n", failures);
   return failures ? 1 : 0;
 }
