@@ -92,35 +92,35 @@ Program quad_program(const double* prm, const double* u_held) {
       {OP_SIN, V_(2), P_(7), 0}, {OP_COS, V_(3), P_(7), 0},                     // sth, cth
       {OP_SIN, V_(4), P_(8), 0}, {OP_COS, V_(5), P_(8), 0},                     // spsi, cpsi
       {OP_SCALE, V_(6), U(0), 0},                                               // a = u0 * (1/mass)
-      {OP_MUL, T_(0), V_(1), V_(2)},                                            // cphi*sth
-      {OP_MUL, T_(1), T_(0), V_(5)}, {OP_MUL, T_(2), V_(0), V_(4)},             // *cpsi, sphi*spsi
-      {OP_ADD, T_(1), T_(1), T_(2)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3x, a*b3x
-      {OP_CONS, 3, T_(2), 0},
-      {OP_MUL, T_(1), T_(0), V_(4)}, {OP_MUL, T_(2), V_(0), V_(5)},             // *spsi, sphi*cpsi
-      {OP_SUB, T_(1), T_(1), T_(2)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3y, a*b3y
-      {OP_CONS, 4, T_(2), 0},
-      {OP_MUL, T_(1), V_(1), V_(3)}, {OP_MUL, T_(2), V_(6), T_(1)},             // b3z, a*b3z
-      {OP_SUBK, T_(2), 0, 1},                                                   // - gravity
-      {OP_CONS, 5, T_(2), 0},
+      // independent products run in pairs (OP_MUL2 + the OP_MUL after it); the
+      // expression trees are unchanged, only their schedule
+      {OP_MUL2, T_(0), V_(1), V_(2)}, {OP_MUL, T_(1), V_(0), V_(4)},            // cs = cphi*sth, sphi*spsi
+      {OP_MUL2, T_(2), T_(0), V_(5)}, {OP_MUL, T_(3), T_(0), V_(4)},            // cs*cpsi, cs*spsi
+      {OP_ADD, T_(2), T_(2), T_(1)},                                            // b3x
+      {OP_MUL2, T_(1), V_(0), V_(5)}, {OP_MUL, T_(0), V_(1), V_(3)},            // sphi*cpsi, b3z = cphi*cth
+      {OP_SUB, T_(3), T_(3), T_(1)},                                            // b3y
+      {OP_MUL2, T_(1), V_(6), T_(2)}, {OP_MUL, T_(2), V_(6), T_(3)},            // dx3 = a*b3x, dx4 = a*b3y
+      {OP_CONS, 3, T_(1), 0}, {OP_CONS, 4, T_(2), 0},
       {OP_INV, V_(7), V_(3), 0},                                                // tme_inv(cth)
-      {OP_MUL, T_(0), V_(2), V_(7)},                                            // tth = sth / cth
-      {OP_MUL, T_(1), V_(0), T_(0)}, {OP_MUL, T_(1), T_(1), P_(10)},            // sphi*tth*q
-      {OP_ADD, T_(1), P_(9), T_(1)},                                            // p + ...
-      {OP_MUL, T_(2), V_(1), T_(0)}, {OP_MUL, T_(2), T_(2), P_(11)},            // cphi*tth*r
-      {OP_ADD, T_(1), T_(1), T_(2)},                                            // dx6 (held)
-      {OP_MUL, T_(0), V_(1), P_(10)}, {OP_MUL, T_(2), V_(0), P_(11)},           // cphi*q, sphi*r
-      {OP_SUB, T_(0), T_(0), T_(2)},                                            // dx7 (held)
-      {OP_MUL, T_(2), V_(0), V_(7)}, {OP_MUL, T_(2), T_(2), P_(10)},            // (sphi/cth)*q
-      {OP_MUL, T_(3), V_(1), V_(7)}, {OP_MUL, T_(3), T_(3), P_(11)},            // (cphi/cth)*r
-      {OP_ADD, T_(2), T_(2), T_(3)},                                            // dx8
+      {OP_MUL2, T_(3), V_(6), T_(0)}, {OP_MUL, T_(1), V_(2), V_(7)},            // a*b3z, tth = sth / cth
+      {OP_SUBK, T_(3), 0, 1},                                                   // - gravity
+      {OP_CONS, 5, T_(3), 0},
+      {OP_MUL2, T_(2), V_(0), T_(1)}, {OP_MUL, T_(3), V_(1), T_(1)},            // sphi*tth, cphi*tth
+      {OP_MUL2, T_(2), T_(2), P_(10)}, {OP_MUL, T_(3), T_(3), P_(11)},          // *q, *r
+      {OP_ADD, T_(2), P_(9), T_(2)},                                            // p + ...
+      {OP_ADD, T_(2), T_(2), T_(3)},                                            // dx6 (held)
+      {OP_MUL2, T_(0), V_(1), P_(10)}, {OP_MUL, T_(1), V_(0), P_(11)},          // cphi*q, sphi*r
+      {OP_SUB, T_(0), T_(0), T_(1)},                                            // dx7 (held)
+      {OP_MUL2, T_(1), V_(0), V_(7)}, {OP_MUL, T_(3), V_(1), V_(7)},            // sphi/cth, cphi/cth
+      {OP_MUL2, T_(1), T_(1), P_(10)}, {OP_MUL, T_(3), T_(3), P_(11)},          // *q, *r
+      {OP_ADD, T_(1), T_(1), T_(3)},                                            // dx8
       // the views of P6 / P7 (sphi, cphi, 1/cth) are dead only now: consume rows 6..8
-      {OP_CONS, 6, T_(1), 0}, {OP_CONS, 7, T_(0), 0}, {OP_CONS, 8, T_(2), 0},
-      {OP_MUL, T_(0), P_(10), P_(11)}, {OP_SCALE, V_(8), T_(0), 2},             // q*r*c1
-      {OP_SCALE, V_(9), U(1), 3}, {OP_ADD, T_(0), V_(8), V_(9)},                // + u1/jx
-      {OP_MUL, T_(1), P_(9), P_(11)}, {OP_SCALE, V_(8), T_(1), 4},              // p*r*c3
-      {OP_SCALE, V_(9), U(2), 5}, {OP_ADD, T_(1), V_(8), V_(9)},                // + u2/jy
-      {OP_MUL, T_(2), P_(9), P_(10)}, {OP_SCALE, V_(8), T_(2), 6},              // p*q*c5
-      {OP_SCALE, V_(9), U(3), 7}, {OP_ADD, T_(2), V_(8), V_(9)},                // + u3/jz
+      {OP_CONS, 6, T_(2), 0}, {OP_CONS, 7, T_(0), 0}, {OP_CONS, 8, T_(1), 0},
+      {OP_MUL2, T_(0), P_(10), P_(11)}, {OP_MUL, T_(1), P_(9), P_(11)},         // q*r, p*r
+      {OP_MUL, T_(2), P_(9), P_(10)},                                           // p*q
+      {OP_SCALE, V_(8), T_(0), 2}, {OP_SCALE, V_(9), U(1), 3}, {OP_ADD, T_(0), V_(8), V_(9)},  // dx9
+      {OP_SCALE, V_(8), T_(1), 4}, {OP_SCALE, V_(9), U(2), 5}, {OP_ADD, T_(1), V_(8), V_(9)},  // dx10
+      {OP_SCALE, V_(8), T_(2), 6}, {OP_SCALE, V_(9), U(3), 7}, {OP_ADD, T_(2), V_(8), V_(9)},  // dx11
       {OP_CONS, 9, T_(0), 0}, {OP_CONS, 10, T_(1), 0}, {OP_CONS, 11, T_(2), 0},
   });
   if (!u_held)
@@ -219,7 +219,8 @@ void load_program(const Program& p, int kind, int na, rb::ct::CTParams& P) {
     if (op.code == OP_CONS0 || op.code == OP_END || op.code == OP_CONST || op.code == OP_SUBK) continue;
     if (op.code != OP_CONS) {
       if (op.a < NA) read[op.a] = true;
-      if ((op.code == OP_MUL || op.code == OP_ADD || op.code == OP_SUB) && op.b < NA) read[op.b] = true;
+      if ((op.code == OP_MUL || op.code == OP_MUL2 || op.code == OP_ADD || op.code == OP_SUB) && op.b < NA)
+        read[op.b] = true;
     }
   }
   for (int i = 0; i < 16; ++i) P.bzsrc[i] = -1;

@@ -143,6 +143,15 @@ __device__ __forceinline__ void wsum2(double& a, double& b) {
     b += __shfl_xor_sync(0xffffffffu, b, o);
   }
 }
+__device__ __forceinline__ void wsum4(double& a, double& b, double& c, double& d) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+  }
+}
 __device__ __forceinline__ double wsum(double a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -250,13 +259,30 @@ __device__ __forceinline__ void set_scalars(Slot& r, double c, double at, Iv rem
 // (views); COPY: materialize a view into a temporary; CONST: tme_const(kc);
 // CONS i: hand dx_i to the consumer (CONS0: dx_i = 0).
 enum : unsigned char {
-  OP_MUL, OP_ADD, OP_SUB, OP_SUBK, OP_SCALE, OP_SIN, OP_COS, OP_INV, OP_CONS, OP_CONS0, OP_COPY, OP_CONST, OP_END
+  OP_MUL, OP_ADD, OP_SUB, OP_SUBK, OP_SCALE, OP_SIN, OP_COS, OP_INV, OP_CONS, OP_CONS0, OP_COPY, OP_CONST, OP_END,
+  OP_MUL2  // two independent products: this op (dst = a * b) and the next program entry, one interleaved pass
 };
 enum : int { MODE_PICARD = 0, MODE_REPLAY = 1, MODE_ENDPOINT = 2 };
 
+// Remainder of operator* (taylor_model.hpp:337-359): the excess terms bounded
+// over the domain and the remainder interactions, from the operands' scalars.
+__device__ __forceinline__ Iv mul_rem(double uc, double vc, double uat, double vat, double au, double av, double bu,
+                                      double bv, Iv ur, Iv vr, double h) {
+  double sym = au * av;
+  sym += (au * bv + av * bu) * h;
+  sym += bu * bv * h * h;
+  sym += (fabs(uat) * bv + fabs(vat) * bu) * h * h;
+  Iv rem{-sym, sym};
+  const double tt = uat * vat;
+  rem = iadd(rem, imul_0h(h * h, tt));
+  const Iv pu = poly_range(uc, au, uat, bu, h), pv = poly_range(vc, av, vat, bv, h);
+  rem = iadd(rem, imul(pu, vr));
+  rem = iadd(rem, imul(pv, ur));
+  return iadd(rem, imul(ur, vr));
+}
+
 // operator* (taylor_model.hpp:325-360).  r may alias u or v.
 __device__ __forceinline__ void op_mul(double* coef, Slot& r, const Slot& u, const Slot& v, const Lane& L) {
-  const double h = L.h;
   const double uc = u.c, vc = v.c, uat = u.at, vat = v.at;
   const double au = u.sz, av = v.sz, bu = u.sb, bv = v.sb;
   const Iv ur{u.rlo, u.rhi}, vr{v.rlo, v.rhi};
@@ -279,18 +305,52 @@ __device__ __forceinline__ void op_mul(double* coef, Slot& r, const Slot& u, con
     s2 += fabs(rb);
   }
   wsum2(s1, s2);
-  double sym = au * av;
-  sym += (au * bv + av * bu) * h;
-  sym += bu * bv * h * h;
-  sym += (fabs(uat) * bv + fabs(vat) * bu) * h * h;
-  Iv rem{-sym, sym};
-  const double tt = uat * vat;
-  rem = iadd(rem, imul_0h(h * h, tt));
-  const Iv pu = poly_range(uc, au, uat, bu, h), pv = poly_range(vc, av, vat, bv, h);
-  rem = iadd(rem, imul(pu, vr));
-  rem = iadd(rem, imul(pv, ur));
-  rem = iadd(rem, imul(ur, vr));
+  const Iv rem = mul_rem(uc, vc, uat, vat, au, av, bu, bv, ur, vr, L.h);
   set_scalars(r, uc * vc, uc * vat + vc * uat, rem, s1, s2);
+}
+
+// Two independent products r = u * v, q = x * y in one interleaved pass (ILP
+// for the latency-bound warp; each product's arithmetic is op_mul's).  Every
+// operand slot is loaded before either result is stored, so q may alias u / v
+// and r may alias x / y; r != q, and x, y must not be r.
+__device__ __forceinline__ void op_mul2(double* coef, Slot& r, const Slot& u, const Slot& v, Slot& q, const Slot& x,
+                                        const Slot& y, const Lane& L) {
+  const double uc = u.c, vc = v.c, uat = u.at, vat = v.at, au = u.sz, av = v.sz, bu = u.sb, bv = v.sb;
+  const double xc = x.c, yc = y.c, xat = x.at, yat = y.at, ax = x.sz, ay = y.sz, bx = x.sb, by = y.sb;
+  const Iv ur{u.rlo, u.rhi}, vr{v.rlo, v.rhi}, xr{x.rlo, x.rhi}, yr{y.rlo, y.rhi};
+  const Opnd U = opnd(coef, u), V = opnd(coef, v), X = opnd(coef, x), Y = opnd(coef, y);
+  double* raz = coef + r.az;
+  double* rbz = coef + r.bz;
+  double* qaz = coef + q.az;
+  double* qbz = coef + q.bz;
+  double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NZC; ++k) {
+    if (!L.act[k]) continue;
+    const int j = L.lane + 32 * k;
+    double ua, ub, va, vb, xa, xb, ya, yb;
+    fetch(U, j, ua, ub);
+    fetch(V, j, va, vb);
+    fetch(X, j, xa, xb);
+    fetch(Y, j, ya, yb);
+    const double ra = uc * va + vc * ua;
+    const double rb = uc * vb + vc * ub + uat * va + vat * ua;
+    const double qa = xc * ya + yc * xa;
+    const double qb = xc * yb + yc * xb + xat * ya + yat * xa;
+    raz[j] = ra;
+    rbz[j] = rb;
+    qaz[j] = qa;
+    qbz[j] = qb;
+    s1 += fabs(ra);
+    s2 += fabs(rb);
+    s3 += fabs(qa);
+    s4 += fabs(qb);
+  }
+  wsum4(s1, s2, s3, s4);
+  const Iv rr = mul_rem(uc, vc, uat, vat, au, av, bu, bv, ur, vr, L.h);
+  const Iv qr = mul_rem(xc, yc, xat, yat, ax, ay, bx, by, xr, yr, L.h);
+  set_scalars(r, uc * vc, uc * vat + vc * uat, rr, s1, s2);
+  set_scalars(q, xc * yc, xc * yat + yc * xat, qr, s3, s4);
 }
 
 // a + b / a - b (taylor_model.hpp:245-269); r may alias a or b.
@@ -376,6 +436,13 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
       case OP_MUL:
         op_mul(coef, W.D[op.dst], W.D[op.a], W.D[op.b], L);
         break;
+      case OP_MUL2: {  // this entry and the next one (an OP_MUL) as one pass
+        const TOp o2 = next;
+        ++pc;
+        next = kProgs[pc + 1];
+        op_mul2(coef, W.D[op.dst], W.D[op.a], W.D[op.b], W.D[o2.dst], W.D[o2.a], W.D[o2.b], L);
+        break;
+      }
       case OP_ADD:
       case OP_SUB:
         op_addsub(coef, W.D[op.dst], W.D[op.a], W.D[op.b], op.code == OP_SUB, L);
