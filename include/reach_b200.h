@@ -346,6 +346,12 @@ typedef struct reach_field_desc {
 int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* field, const reach_flowpipe_params* fp, int32_t batch,
                    const double* x0_lo, const double* x0_hi, const reach_tube_out* out, int32_t flags);
 
+/* reach_with_splitting(ct_reach engine, x0, plan) (refine.hpp:121-160; the
+ * CLI's `reach-ct --split` / `split`, reach_cli.cpp:200-211): hull boxes
+ * [1 + fp.steps][n] over the sub-boxes [part_begin, part_end). */
+int reach_ct_split_hull(reach_ctx* ctx, const reach_field_desc* field, const reach_flowpipe_params* fp,
+                        const reach_cl_split_args* args, const reach_hull_out* out, int32_t flags);
+
 #ifdef __cplusplus
 }
 #endif

@@ -736,3 +736,50 @@ int orc_ct_batch(const reach_field_desc* fd, const reach_flowpipe_params* fp, in
   }
   return REACH_OK;
 }
+
+/* reach_with_splitting(ct_reach) hull (refine.hpp:121-160) over parts [begin, end). */
+int orc_ct_split_hull(const reach_field_desc* fd, const reach_flowpipe_params* fp, const reach_cl_split_args* a,
+                      const reach_hull_out* out) {
+  const int n = fd->n, T = 1 + fp->steps;
+  if (n < 1 || n > 16) return REACH_E_UNSUPPORTED;
+  int64_t total = 1;
+  for (int d = 0; d < n; ++d) { if (a->counts[d] < 1) return REACH_E_INVALID_ARGUMENT; total *= a->counts[d]; }
+  int64_t begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
+  if (begin < 0 || begin >= end || end > total) return REACH_E_INVALID_ARGUMENT;
+  const ctfield F = {fd->kind, n, fd->params};
+  double* lo = (double*)malloc(sizeof(double) * (size_t)T * n);
+  double* hi = (double*)malloc(sizeof(double) * (size_t)T * n);
+  double plo[CT_MAXR], phi[CT_MAXR];
+  int steps = 0;
+  int64_t key = INT64_MAX;
+  for (int k = 0; k < T; ++k) out->box_diverged[k] = 0;
+  for (int64_t p = begin; p < end; ++p) {
+    ct_split_part(n, a->x0_lo, a->x0_hi, a->counts, p, plo, phi);
+    int fs, st;
+    int nb = ct_reach_one(&F, fp, plo, phi, lo, hi, &fs, &st);
+    if (p == begin) {
+      steps = nb;
+      for (int k = 0; k < nb * n; ++k) { out->lo[k] = lo[k]; out->hi[k] = hi[k]; }
+    } else {
+      int upto = nb < steps ? nb : steps;
+      for (int k = 0; k < upto * n; ++k) {
+        out->lo[k] = smin(out->lo[k], lo[k]);
+        out->hi[k] = smax(out->hi[k], hi[k]);
+      }
+      if (nb < steps) steps = nb;
+    }
+    for (int k = 0; k < nb; ++k) {
+      int fin = 1;
+      for (int d = 0; d < n; ++d) if (!isfinite(lo[k * n + d]) || !isfinite(hi[k * n + d])) fin = 0;
+      if (!fin) out->box_diverged[k] = 1;
+    }
+    if (st != REACH_TUBE_OK) {
+      int64_t kk = ((int64_t)(fs >= 0 ? fs : nb) << 40) | ((int64_t)p << 8) | (int64_t)(st & 0xff);
+      if (kk < key) key = kk;
+    }
+  }
+  out->n_boxes[0] = steps;
+  out->fail_key[0] = key;
+  free(lo); free(hi);
+  return REACH_OK;
+}

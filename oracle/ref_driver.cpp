@@ -676,3 +676,69 @@ int ref_ct_batch(const reach_field_desc* fd, const reach_flowpipe_params* fp, in
   return REACH_OK;
 }
 }  // extern "C"
+
+extern "C" {
+// reach_with_splitting(ct_reach, x0, plan) -- the CLI's `split` path (reach_cli.cpp:200-211).
+int ref_ct_split_hull(const reach_field_desc* fd, const reach_flowpipe_params* fp, const reach_cl_split_args* a,
+                      const reach_hull_out* out, int32_t threads) {
+  try {
+    VectorField<double> f = field_from(fd);
+    FlowpipeParams prm;
+    prm.h = fp->h;
+    prm.steps = fp->steps;
+    prm.order = fp->order;
+    prm.eps_init = fp->eps_init;
+    prm.refine_rounds = fp->refine_rounds;
+    prm.enlargement = fp->enlargement;
+    prm.max_enlargements = fp->max_enlargements;
+    prm.window = fp->window;
+    const int n = fd->n;
+    Box x0 = box_at(a->x0_lo, a->x0_hi, n);
+    SplitPlan plan;
+    plan.counts.assign(a->counts, a->counts + n);
+    const long long total = plan.total_parts();
+    long long begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
+    if (begin < 0 || begin >= end || end > total) return REACH_E_INVALID_ARGUMENT;
+    auto engine = [&](const Box& b) { return ct_reach(f, b, prm); };
+    auto parts = split_box(x0, plan);
+    const int count = static_cast<int>(end - begin);
+    std::vector<ReachTube<double>> subs(static_cast<size_t>(count));
+    parallel_for(
+        count,
+        [&](int i) {
+          try {
+            subs[static_cast<size_t>(i)] = engine(parts[static_cast<size_t>(begin + i)]);
+          } catch (const std::exception& e) {
+            subs[static_cast<size_t>(i)].mark_failed(0, e.what());
+          }
+        },
+        threads);
+    int steps = subs.front().steps();
+    int64_t key = std::numeric_limits<int64_t>::max();
+    for (int i = 0; i < count; ++i) {
+      const auto& s = subs[static_cast<size_t>(i)];
+      steps = std::min(steps, s.steps());
+      if (s.diverged) {
+        int fs = s.failed_step >= 0 ? s.failed_step : s.steps();
+        int64_t k = (static_cast<int64_t>(fs) << 40) | (static_cast<int64_t>(begin + i) << 8) |
+                    static_cast<int64_t>(ct_status_of(s) & 0xff);
+        key = std::min(key, k);
+      }
+    }
+    for (int k = 0; k < steps; ++k) {
+      Box b = subs.front().boxes[static_cast<size_t>(k)];
+      for (int i = 1; i < count; ++i) b = box_hull(b, subs[static_cast<size_t>(i)].boxes[static_cast<size_t>(k)]);
+      for (int d = 0; d < n; ++d) {
+        out->lo[static_cast<size_t>(k) * n + d] = b[d].lo;
+        out->hi[static_cast<size_t>(k) * n + d] = b[d].hi;
+      }
+      out->box_diverged[k] = b.diverged ? 1 : 0;
+    }
+    out->n_boxes[0] = steps;
+    out->fail_key[0] = key;
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+}  // extern "C"

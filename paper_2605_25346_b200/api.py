@@ -624,3 +624,35 @@ def ct_reach(f: AnalyticField, x0, prm: FlowpipeParams = None, ctx: Optional[Con
     lo = np.asarray(x0[0], np.float64).reshape(1, -1)
     hi = np.asarray(x0[1], np.float64).reshape(1, -1)
     return ct_reach_batch_arrays(f, lo, hi, prm, ctx).tube(0)
+
+
+def ct_split_hull(f: AnalyticField, x0, plan: SplitPlan, prm: FlowpipeParams = None, part_begin: int = 0,
+                  part_end: int = 0, ctx: Optional[Context] = None) -> HullResult:
+    """Hull over sub-boxes [part_begin, part_end) of reach_with_splitting(ct_reach) (C ABI reach_ct_split_hull;
+    the CLI's `split` / `reach-ct --split`, reach_cli.cpp:200-211)."""
+    prm = prm or FlowpipeParams()
+    prm.validate()
+    ctx = ctx or default_context()
+    lo0 = np.ascontiguousarray(x0[0], dtype=np.float64)
+    hi0 = np.ascontiguousarray(x0[1], dtype=np.float64)
+    plan.validate(f.n)
+    counts = np.array(plan.counts, dtype=np.int32)
+    T = 1 + prm.steps
+    out = HullResult(np.full((T, f.n), np.nan), np.full((T, f.n), np.nan), np.zeros(T, np.int32), 0, 0, h=prm.h)
+    nb = np.zeros(1, np.int32)
+    key = np.zeros(1, np.int64)
+    fd = f.c_struct()
+    fp = prm.c_struct()
+    args = A.CLSplitArgs(A.dptr(lo0), A.dptr(hi0), A.iptr(counts), int(part_begin), int(part_end))
+    ho = A.HullOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.box_diverged), A.iptr(nb), A.lptr(key))
+    ctx.check(ctx._lib.reach_ct_split_hull(ctx.handle, C.byref(fd), C.byref(fp), C.byref(args), C.byref(ho), 0),
+              "reach_with_splitting(ct_reach)")
+    out.n_boxes = int(nb[0])
+    out.fail_key = int(key[0])
+    return out
+
+
+def ct_reach_with_splitting(f: AnalyticField, x0, plan: SplitPlan, prm: FlowpipeParams = None,
+                            ctx: Optional[Context] = None) -> ReachTube:
+    """reach_with_splitting(ct_reach engine, x0, plan) (refine.hpp:121-160)."""
+    return ct_split_hull(f, x0, plan, prm, ctx=ctx).tube()

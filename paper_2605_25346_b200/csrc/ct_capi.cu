@@ -493,10 +493,13 @@ int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spe
   return REACH_OK;
 }
 
-int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowpipe_params* fp, int32_t batch,
-                   const double* x0_lo, const double* x0_hi, const reach_tube_out* out, int32_t flags) {
-  if (!ctx || !fd || !fp || !out) return REACH_E_INVALID_ARGUMENT;
-  if (batch < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: negative batch");
+}  // extern "C"
+
+namespace {
+
+// ct_reach's kernel parameters for a field (validation as FlowpipeParams::validate,
+// flowpipe_ct.hpp:45-49, plus the device family's limits).
+int ct_params(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowpipe_params* fp, rb::ct::CTParams& P) {
   if (!(fp->h > 0) || fp->steps <= 0 || fp->order < 1 || fp->order > 2 || !(fp->eps_init > 0) ||
       !(fp->enlargement > 1.0) || fp->refine_rounds < 0 || fp->max_enlargements < 0 || fp->window < 0)
     return fail(ctx, REACH_E_INVALID_ARGUMENT, "FlowpipeParams: invalid configuration");
@@ -517,16 +520,6 @@ int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowp
   }
   if (n < 1 || n > 16 || n * (fp->window + 2) > rb::ct::NZP)
     return fail(ctx, REACH_E_UNSUPPORTED, "ct_reach: n <= 16 and n (window + 2) <= 80 on the device");
-  if (batch == 0) return REACH_OK;
-  const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
-  if (!dev)  // build_linear_tm / init_symbolic_state on a diverged X0
-    for (size_t i = 0; i < static_cast<size_t>(batch) * n; ++i)
-      if (!std::isfinite(x0_lo[i]) || !std::isfinite(x0_hi[i]))
-        return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: non-finite X0");
-  RB_CUDA(cudaSetDevice(ctx->device));
-  rb::ct::CTParams P{};
-  int rc = REACH_OK;
-  P.B = batch;
   P.n = n;
   P.na = n;
   P.bw = n;
@@ -544,8 +537,44 @@ int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowp
   P.eps = fp->eps_init;
   P.enl = fp->enlargement;
   load_program(prog, fd->kind, n, P);
-  rc = ensure_programs(ctx);
+  return ensure_programs(ctx);
+}
+
+int launch_ct(reach_ctx* ctx, const rb::ct::CTParams& P) {
+  const size_t smem = flow_smem_bytes(P);
+  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  cudaEvent_t stop;
+  int rc = timed_begin(ctx, &stop);
   if (rc) return rc;
+  rb::ct::ct_flow_kernel<true><<<P.B, 32, smem, ctx->stream>>>(P);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  return REACH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowpipe_params* fp, int32_t batch,
+                   const double* x0_lo, const double* x0_hi, const reach_tube_out* out, int32_t flags) {
+  if (!ctx || !fd || !fp || !out) return REACH_E_INVALID_ARGUMENT;
+  if (batch < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: negative batch");
+  rb::ct::CTParams P{};
+  int rc = ct_params(ctx, fd, fp, P);
+  if (rc) return rc;
+  const int n = fd->n;
+  if (batch == 0) return REACH_OK;
+  const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
+  if (!dev)  // build_linear_tm / init_symbolic_state on a diverged X0
+    for (size_t i = 0; i < static_cast<size_t>(batch) * n; ++i)
+      if (!std::isfinite(x0_lo[i]) || !std::isfinite(x0_hi[i]))
+        return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: non-finite X0");
+  RB_CUDA(cudaSetDevice(ctx->device));
+  P.B = batch;
   const size_t B = batch, NA = rb::ct::NA, T = P.T;
   const size_t box_bytes = B * T * n * 8, i_bytes = B * 4, x_bytes = B * n * 8;
   Carve cv;
@@ -585,17 +614,8 @@ int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowp
     RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.x0_lo), x0_lo, x_bytes, cudaMemcpyHostToDevice, ctx->stream));
     RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.x0_hi), x0_hi, x_bytes, cudaMemcpyHostToDevice, ctx->stream));
   }
-  const size_t smem = flow_smem_bytes(P);
-  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
-  cudaEvent_t stop;
-  rc = timed_begin(ctx, &stop);
+  rc = launch_ct(ctx, P);
   if (rc) return rc;
-  rb::ct::ct_flow_kernel<true><<<batch, 32, smem, ctx->stream>>>(P);
-  RB_CUDA(cudaGetLastError());
-  rc = timed_end(ctx, stop);
-  if (rc) return rc;
-  ctx->launches += 1;
   if (!dev) {
     std::vector<int32_t> nb(B);
     RB_CUDA(cudaMemcpyAsync(nb.data(), P.n_boxes, i_bytes, cudaMemcpyDeviceToHost, ctx->stream));
@@ -609,6 +629,77 @@ int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowp
       RB_CUDA(cudaMemcpyAsync(out->lo + o, P.out_lo + o, cnt, cudaMemcpyDeviceToHost, ctx->stream));
       RB_CUDA(cudaMemcpyAsync(out->hi + o, P.out_hi + o, cnt, cudaMemcpyDeviceToHost, ctx->stream));
     }
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return REACH_OK;
+}
+
+int reach_ct_split_hull(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowpipe_params* fp,
+                        const reach_cl_split_args* a, const reach_hull_out* out, int32_t flags) {
+  if (!ctx || !fd || !fp || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  rb::ct::CTParams P{};
+  int rc = ct_params(ctx, fd, fp, P);
+  if (rc) return rc;
+  const int n = fd->n;
+  long long total = 1;
+  for (int d = 0; d < n; ++d) {
+    if (a->counts[d] < 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "SplitPlan: counts must be >= 1");
+    total *= a->counts[d];
+    if (total > (1ll << 20)) return fail(ctx, REACH_E_INVALID_ARGUMENT, "SplitPlan: total part count overflow");
+    if (!std::isfinite(a->x0_lo[d]) || !std::isfinite(a->x0_hi[d]))
+      return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: non-finite X0");
+  }
+  const long long begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
+  if (begin < 0 || begin >= end || end > total) return fail(ctx, REACH_E_INVALID_ARGUMENT, "bad part range");
+  RB_CUDA(cudaSetDevice(ctx->device));
+  const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
+  P.B = static_cast<int>(end - begin);
+  P.split = 1;
+  P.part_begin = begin;
+  for (int d = 0; d < n; ++d) {
+    P.sx_lo[d] = a->x0_lo[d];
+    P.sx_hi[d] = a->x0_hi[d];
+    P.counts[d] = a->counts[d];
+  }
+  const size_t B = end - begin, NA = rb::ct::NA, T = P.T, cnt = T * n;
+  Carve cv;
+  const size_t o_c = cv.take(B * NA * 8), o_M = cv.take(B * NA * rb::ct::NZP * 8), o_meta = cv.take(B * 16),
+               o_kl = cv.take(cnt * 8), o_kh = cv.take(cnt * 8), o_nan = cv.take(cnt * 8), o_div = cv.take(T * 4),
+               o_nb = cv.take(4), o_key = cv.take(8), o_lo = cv.take(cnt * 8), o_hi = cv.take(cnt * 8);
+  rc = ensure_ws(ctx, cv.off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  P.st_c = reinterpret_cast<double*>(w + o_c);
+  P.st_M = reinterpret_cast<double*>(w + o_M);
+  P.st_meta = reinterpret_cast<int*>(w + o_meta);
+  P.hull_lo = reinterpret_cast<unsigned long long*>(w + o_kl);
+  P.hull_hi = reinterpret_cast<unsigned long long*>(w + o_kh);
+  P.hull_nan0 = reinterpret_cast<int*>(w + o_nan);
+  P.hull_div = reinterpret_cast<int*>(w + o_div);
+  P.hull_nboxes = reinterpret_cast<int*>(w + o_nb);
+  P.hull_fail_key = reinterpret_cast<unsigned long long*>(w + o_key);
+  const int icount = static_cast<int>(cnt), tpb = 256;
+  ct_hull_init_kernel<<<std::max((std::max(icount, static_cast<int>(T)) + tpb - 1) / tpb, 1), tpb, 0, ctx->stream>>>(
+      P.hull_lo, P.hull_hi, P.hull_nan0, P.hull_div, icount, static_cast<int>(T), P.hull_nboxes, P.hull_fail_key);
+  RB_CUDA(cudaGetLastError());
+  rc = launch_ct(ctx, P);
+  if (rc) return rc;
+  double* dlo = dev ? out->lo : reinterpret_cast<double*>(w + o_lo);
+  double* dhi = dev ? out->hi : reinterpret_cast<double*>(w + o_hi);
+  ct_hull_finalize_kernel<<<(icount + tpb - 1) / tpb, tpb, 0, ctx->stream>>>(P.hull_lo, P.hull_hi, P.hull_nan0, icount,
+                                                                             dlo, dhi);
+  RB_CUDA(cudaGetLastError());
+  ctx->launches += 2;
+  if (dev) {
+    RB_CUDA(cudaMemcpyAsync(out->box_diverged, P.hull_div, T * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(out->n_boxes, P.hull_nboxes, 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(out->fail_key, P.hull_fail_key, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    RB_CUDA(cudaMemcpyAsync(out->lo, dlo, cnt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(out->hi, dhi, cnt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(out->box_diverged, P.hull_div, T * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(out->n_boxes, P.hull_nboxes, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(out->fail_key, P.hull_fail_key, 8, cudaMemcpyDeviceToHost, ctx->stream));
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   return REACH_OK;

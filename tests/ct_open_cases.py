@@ -47,3 +47,10 @@ def ct_open_cases():
     tl[0, 7], th[0, 7] = 1.50, 1.66
     out.append(("quad_tme_inv", quadrotor_field(), tl, th, FlowpipeParams(h=0.01, steps=5), True))
     return out
+
+
+def ct_open_split_case():
+    """The CLI's `split --system quadrotor --split rpy:8` shape (reach_cli.cpp:200-211, 80-82)."""
+    from paper_2605_25346_b200.api import SplitPlan
+    r = np.array([0.05] * 6 + [0.02] * 6)
+    return quadrotor_field(), -r, r.copy(), SplitPlan.rpy(12, 8), FlowpipeParams(h=0.01, steps=20)

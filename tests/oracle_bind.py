@@ -318,3 +318,35 @@ def oracle_ct_batch(f, x0_lo, x0_hi, prm):
 
 def ref_ct_batch(f, x0_lo, x0_hi, prm, threads=0):
     return _ct(ref_lib(), "ref_", f, x0_lo, x0_hi, prm, threads)
+
+
+def _ct_hull(lib, prefix, f, x0_lo, x0_hi, plan, prm, begin=0, end=0, threads=None):
+    args_t = [C.POINTER(A.FieldDescC), C.POINTER(A.FlowpipeParamsC), C.POINTER(A.CLSplitArgs), C.POINTER(A.HullOut)]
+    if prefix == "ref_":
+        args_t.append(C.c_int32)
+    fn = _mpc_fn(lib, prefix + "ct_split_hull", args_t)
+    T = 1 + prm.steps
+    lo0 = np.ascontiguousarray(x0_lo, np.float64)
+    hi0 = np.ascontiguousarray(x0_hi, np.float64)
+    counts = np.array(plan.counts, np.int32)
+    out = HullResult(np.full((T, f.n), np.nan), np.full((T, f.n), np.nan), np.zeros(T, np.int32), 0, 0, h=prm.h)
+    nb = np.zeros(1, np.int32)
+    key = np.zeros(1, np.int64)
+    fd = f.c_struct()
+    fp = prm.c_struct()
+    args = A.CLSplitArgs(A.dptr(lo0), A.dptr(hi0), A.iptr(counts), int(begin), int(end))
+    ho = A.HullOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.box_diverged), A.iptr(nb), A.lptr(key))
+    extra = [threads if threads is not None else 0] if prefix == "ref_" else []
+    rc = fn(C.byref(fd), C.byref(fp), C.byref(args), C.byref(ho), *extra)
+    assert rc == 0, rc
+    out.n_boxes = int(nb[0])
+    out.fail_key = int(key[0])
+    return out
+
+
+def oracle_ct_split_hull(f, x0_lo, x0_hi, plan, prm, begin=0, end=0):
+    return _ct_hull(oracle_lib(), "orc_", f, x0_lo, x0_hi, plan, prm, begin, end)
+
+
+def ref_ct_split_hull(f, x0_lo, x0_hi, plan, prm, begin=0, end=0, threads=0):
+    return _ct_hull(ref_lib(), "ref_", f, x0_lo, x0_hi, plan, prm, begin, end, threads)

@@ -9,11 +9,11 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-from ct_open_cases import ct_open_cases
-from oracle_bind import oracle_ct_batch
-from paper_2605_25346_b200.api import (FlowpipeParams, ct_reach, ct_reach_batch_arrays, diag_linear_field,
+from ct_open_cases import ct_open_cases, ct_open_split_case
+from oracle_bind import oracle_ct_batch, oracle_ct_split_hull
+from paper_2605_25346_b200.api import (FlowpipeParams, ct_reach, ct_reach_batch_arrays, ct_split_hull, diag_linear_field,
                                        quadrotor_field, rotation_field, zero_field)
-from test_gpu_ct import CT_RTOL, _quad_rhs, assert_ct_close
+from test_gpu_ct import CT_RTOL, _close, _quad_rhs, assert_ct_close
 
 
 @pytest.mark.parametrize("case", ct_open_cases(), ids=lambda c: c[0])
@@ -85,3 +85,11 @@ def test_batch_rows_independent():
     full = ct_reach_batch_arrays(f, c - r, c + r, prm)
     one = ct_reach_batch_arrays(f, (c - r)[17:18], (c + r)[17:18], prm)
     assert np.array_equal(full.lo[17], one.lo[0]) and np.array_equal(full.hi[17], one.hi[0])
+
+
+def test_ct_split_hull_matches_oracle():
+    f, lo, hi, plan, prm = ct_open_split_case()
+    exp = oracle_ct_split_hull(f, lo, hi, plan, prm)
+    got = ct_split_hull(f, (lo, hi), plan, prm)
+    assert got.n_boxes == exp.n_boxes and got.fail_key == exp.fail_key
+    assert _close(got.lo, exp.lo, exp.lo, exp.hi) <= CT_RTOL and _close(got.hi, exp.hi, exp.lo, exp.hi) <= CT_RTOL
