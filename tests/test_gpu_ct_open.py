@@ -93,3 +93,65 @@ def test_ct_split_hull_matches_oracle():
     got = ct_split_hull(f, (lo, hi), plan, prm)
     assert got.n_boxes == exp.n_boxes and got.fail_key == exp.fail_key
     assert _close(got.lo, exp.lo, exp.lo, exp.hi) <= CT_RTOL and _close(got.hi, exp.hi, exp.lo, exp.hi) <= CT_RTOL
+
+
+def test_ct_error_behaviour():
+    """FlowpipeParams::validate / shape errors raise ValueError (the reference's std::invalid_argument);
+    shapes outside the device family raise ReachError (REACH_E_UNSUPPORTED), never a CPU fallback."""
+    from paper_2605_25346_b200 import ReachError
+    lo, hi = np.array([[0.9, -0.1]]), np.array([[1.1, 0.1]])
+    with pytest.raises(ValueError):
+        ct_reach_batch_arrays(rotation_field(1.0), lo, hi, FlowpipeParams(h=-0.1))
+    with pytest.raises(ValueError):
+        ct_reach_batch_arrays(rotation_field(1.0), lo[:, :1], hi[:, :1], FlowpipeParams())
+    with pytest.raises(ValueError):
+        ct_reach_batch_arrays(rotation_field(1.0), np.array([[np.inf, 0.0]]), hi, FlowpipeParams())
+    with pytest.raises(ReachError):  # 12 x (window + 2) = 96 > 80 generator columns
+        ct_reach_batch_arrays(quadrotor_field(), np.zeros((1, 12)), np.full((1, 12), 0.01), FlowpipeParams(window=6))
+
+
+def test_cl_error_behaviour():
+    from paper_2605_25346_b200 import ReachError
+    from paper_2605_25346_b200.api import ClosedLoopSpec, cl_reach_batch_arrays
+    from paper_2605_25346_b200.workloads import c2_quadrotor
+    w = c2_quadrotor()
+    lo, hi = w.x0_lo[None], w.x0_hi[None]
+    bad = ClosedLoopSpec(controller=w.spec.controller, ctl_steps=2, k_atomic=2)  # 15-input controller, no y_ref
+    with pytest.raises(ValueError):
+        cl_reach_batch_arrays(bad, lo, hi)
+    spec = ClosedLoopSpec(controller=w.spec.controller, ctl_steps=2, k_atomic=2, y_ref=w.spec.y_ref[:2],
+                          fp=FlowpipeParams(window=5))
+    with pytest.raises(ReachError):  # window 5: 12 + 5 x 16 generator columns exceed the device rows
+        cl_reach_batch_arrays(spec, lo, hi)
+    with pytest.raises(ValueError):
+        cl_reach_batch_arrays(w.spec, lo[:, :6], hi[:, :6])
+
+
+def test_ct_device_pointer_path_matches_host_path():
+    """REACH_FLAG_DEVICE_PTRS: stream-ordered call on device buffers (no host copies inside)."""
+    import ctypes as C
+
+    import torch
+    from paper_2605_25346_b200 import _abi as A
+    from paper_2605_25346_b200.api import default_context
+    f = quadrotor_field()
+    prm = FlowpipeParams(h=0.01, steps=15)
+    rng = np.random.default_rng(9)
+    c = rng.uniform(-0.1, 0.1, size=(8, 12))
+    lo, hi = c - 0.01, c + 0.01
+    exp = ct_reach_batch_arrays(f, lo, hi, prm)
+    ctx = default_context()
+    dev = torch.device("cuda", 0)
+    dlo, dhi = torch.tensor(lo, device=dev), torch.tensor(hi, device=dev)
+    T = prm.steps + 1
+    olo = torch.full((8, T, 12), float("nan"), dtype=torch.float64, device=dev)
+    ohi = torch.full_like(olo, float("nan"))
+    nb, fs, st = (torch.zeros(8, dtype=torch.int32, device=dev) for _ in range(3))
+    to = A.TubeOut(A.dptr(olo.data_ptr()), A.dptr(ohi.data_ptr()), A.iptr(nb.data_ptr()), A.iptr(fs.data_ptr()),
+                   A.iptr(st.data_ptr()))
+    fd, fp = f.c_struct(), prm.c_struct()
+    ctx.check(ctx._lib.reach_ct_batch(ctx.handle, C.byref(fd), C.byref(fp), 8, A.dptr(dlo.data_ptr()),
+                                      A.dptr(dhi.data_ptr()), C.byref(to), A.REACH_FLAG_DEVICE_PTRS), "ct_reach")
+    ctx.synchronize()
+    assert np.array_equal(olo.cpu().numpy(), exp.lo) and np.array_equal(ohi.cpu().numpy(), exp.hi)
+    assert np.array_equal(nb.cpu().numpy(), exp.n_boxes)
