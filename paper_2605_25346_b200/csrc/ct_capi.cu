@@ -293,7 +293,8 @@ int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
   int prc = ensure_programs(ctx);
   if (prc) return prc;
   const size_t flow_smem = flow_smem_bytes(P);
-  const size_t ctl_smem = sizeof(rb::ct::CtlSmem) * rb::ct::kCtlWarps;
+  const size_t ctl_smem = rb::ct::kCtlWarps * (sizeof(rb::ct::CtlSmem) + static_cast<size_t>(P.ctl.L - 1) *
+                                                                           rb::ct::kMaxCtlW * 2 * sizeof(double));
   RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(flow_smem)));
   RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_ctl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

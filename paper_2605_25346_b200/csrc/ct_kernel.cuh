@@ -1091,10 +1091,11 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
 // Controller certification + stacking (closed_loop.hpp:89-155), one warp per
 // sub-box.  Weights are read from the uploaded blob (W row-major, W^T) through
 // L1/L2: the controller is small and certified once per control interval.
-struct CtlSmem {
+// Per warp: this struct, then the preactivation boxes of the controller's
+// hidden layers, [L - 1][kMaxCtlW][2] (sized by the host: ctl_warp_bytes).
+struct __align__(16) CtlSmem {
   double xA[NX * LDX];           // state TM rows (n x nzx), stride LDX
   double xc[NX];
-  double pre[kMaxLayers][kMaxCtlW][2];  // preactivation boxes of the hidden layers
   double hb[2][kMaxCtlW][2];     // IBP boxes
   double lam[2][4][kMaxCtlW];    // Lambda (n_o x width), double buffered
   double bf0[kMaxCtlW];          // frozen first-layer bias
@@ -1112,7 +1113,9 @@ __device__ __forceinline__ void relax_tanh_or_relu(int act, double l, double u, 
 __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams Pm) {
   extern __shared__ __align__(16) unsigned char ct_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  CtlSmem& W = reinterpret_cast<CtlSmem*>(ct_smem)[warp];
+  const size_t warp_bytes = sizeof(CtlSmem) + static_cast<size_t>(Pm.ctl.L - 1) * kMaxCtlW * 2 * sizeof(double);
+  CtlSmem& W = *reinterpret_cast<CtlSmem*>(ct_smem + warp * warp_bytes);
+  double* pre = reinterpret_cast<double*>(&W + 1);  // [L - 1][kMaxCtlW][2]
   const long long b = static_cast<long long>(blockIdx.x) * kCtlWarps + warp;
   if (b >= Pm.B) return;
   const int n = Pm.n, l = Pm.l;
@@ -1234,8 +1237,8 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
       const double bias = (t == 0) ? W.bf0[u] : blob[N.b_off[t] + u];
       lo = lo + bias;
       hi = hi + bias;
-      W.pre[t][u][0] = lo;
-      W.pre[t][u][1] = hi;
+      pre[(t * kMaxCtlW + u) * 2] = lo;
+      pre[(t * kMaxCtlW + u) * 2 + 1] = hi;
       W.hb[cur ^ 1][u][0] = act_apply(N.acts[t], lo);
       W.hb[cur ^ 1][u][1] = act_apply(N.acts[t], hi);
     }
@@ -1261,14 +1264,14 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     // relax_activation (neural.hpp:166-227) per unit; non-finite -> throw
     for (int u = lane; u < width; u += 32) {
       double s, li, ui;
-      const double pl = W.pre[t][u][0], ph = W.pre[t][u][1];
+      const double pl = pre[(t * kMaxCtlW + u) * 2], ph = pre[(t * kMaxCtlW + u) * 2 + 1];
       if (!(isfinite(pl) && isfinite(ph))) {
         bad = true;
         s = li = ui = 0.0;
       } else {
         relax(N.acts[t], pl, ph, s, li, ui);
       }
-      W.pre[t][u][0] = s;
+      pre[(t * kMaxCtlW + u) * 2] = s;
       W.hb[0][u][0] = li;
       W.hb[0][u][1] = ui;
     }
@@ -1288,7 +1291,7 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
           bl = bl + aij * ui;
           bu = bu + aij * li;
         }
-        W.lam[lb][lane][j] = aij * W.pre[t][j][0];
+        W.lam[lb][lane][j] = aij * pre[(t * kMaxCtlW + j) * 2];
       }
       // shift = Lambda . b (linalg.hpp:40-51), b += shift
       const double* bias = (t == 0) ? W.bf0 : blob + N.b_off[t];
