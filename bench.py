@@ -305,6 +305,24 @@ def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt[0])
     steps_total = per_rank * world * (T - 1)
+    # end to end through the public API: host X0 / plan in, host hull out
+    e2e = []
+    for i in range(5):
+        barrier()
+        t0 = time.perf_counter()
+        hres = cl_split_hull(spec, (w.x0_lo, w.x0_hi), plan, begin, end, ctx=_host_ctx(ctx))
+        if world > 1:
+            hl = torch.tensor(np.where(np.isnan(hres.lo), np.inf, hres.lo), device=dev)
+            dist.all_reduce(hl, op=dist.ReduceOp.MIN)
+            hl.cpu()
+        if i >= 2:
+            e2e.append(time.perf_counter() - t0)
+    ctx.set_stream(stream.cuda_stream)
+    te = float(np.mean(e2e))
+    if world > 1:
+        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt[0])
     fl = ct_flops_per_step()
     tf_fma, _ = ctx.fp64_peak()
     ach = fl * per_rank * (T - 1) / (t / 1e3) / 1e12
@@ -313,6 +331,8 @@ def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
                        "h=0.01, order 2, window 4",
            "sub_boxes_per_gpu": per_rank, "ms_per_sweep": t, "reach_steps_per_s": steps_total / (t / 1e3),
            "launches_per_sweep": 2 * spec.ctl_steps + 2,
+           "e2e": {"value": steps_total / te, "unit": UNIT, "h2d_bytes_per_step": 2 * 12 * 8 + 12 * 4 + 3 * 8 * spec.ctl_steps,
+                   "d2h_bytes_per_step": 2 * T * 16 * 8 + T * 4 + 12},
            "roofline": {"bound": "fp64", "achieved": ach, "peak": tf_fma, "unit": "TFLOP/s", "frac": ach / tf_fma,
                         "flops_per_reach_step": fl,
                         "note": "algorithmic flops of the reference's TMExpr op sequence (bench.ct_flops_per_step); "
