@@ -507,10 +507,18 @@ def main():
     from paper_2605_25346_b200.workloads import c4_partition_sweep
 
     rank, world, local = dist_env()
+    # RB_BENCH_SHARE_GPU=1 (logic check of the N > 1 path on a 1-GPU box, never a measurement):
+    # ranks share the visible GPUs and reduce over gloo
+    share = os.environ.get("RB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     w = c4_partition_sweep()
     per_rank = w.plan.total_parts()
     counts = list(w.plan.counts)
