@@ -163,7 +163,7 @@ typedef struct reach_sampler_config {
   int32_t iterations;
   double init_std;
   double smoothing;
-  int32_t refine_iters; /* gradient refinement is not on the device path: must be 0 */
+  int32_t refine_iters; /* reach_plan_cem: forward-dual gradient refinement; the reach_cem_* pieces: must be 0 */
   uint64_t seed;
 } reach_sampler_config;
 
@@ -236,14 +236,28 @@ int reach_plan_eval_batch(reach_ctx* ctx, const reach_net* net, const reach_plan
                           int32_t batch, const double* actions, double* objective, int32_t* diverged,
                           const reach_tube_out* tubes, int32_t flags);
 
-/* plan_cem (mpc.hpp:258-368) with refine_iters == 0: the reference's
- * sequential mt19937_64 / Box-Muller sampling on the host, every population
- * evaluated by reach_plan_eval_batch, stable-sort elite refit on the host.
- * best_actions [H][m], best_history [iterations], best_effort flag, and the
- * final plan's tube (batch 1, optional). */
+/* plan_cem (mpc.hpp:258-368): the reference's sequential mt19937_64 /
+ * Box-Muller sampling on the host, every population evaluated by
+ * reach_plan_eval_batch, stable-sort elite refit on the host, then (for
+ * refine_iters > 0, the reference default 5) gradient_refine of the best
+ * candidate (refine.hpp:347-398) with forward-dual gradients computed on the
+ * device (reach_plan_objective_grad).  best_actions [H][m], best_history
+ * [iterations], best_effort flag, and the final plan's tube (batch 1,
+ * optional).  A non-finite dual derivative is REACH_E_INVALID_ARGUMENT, where
+ * the reference's grad_forward throws. */
 int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
                    const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
                    double* best_history, int32_t* best_effort, const reach_tube_out* final_tube);
+/* As reach_plan_cem, plus PlanResult::refined (mpc.hpp:241): the refinement made progress. */
+int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
+                      const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
+                      double* best_history, int32_t* best_effort, int32_t* refined, const reach_tube_out* final_tube);
+
+/* grad_forward (refine.hpp:186-207) of plan_objective (mpc.hpp:204-208) over
+ * the flat action sequence [H][m]: one reach::Dual pass per direction, all
+ * directions in one launch.  grad [H*m]; objective (optional) = the primal. */
+int reach_plan_objective_grad(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
+                              const double* actions, double* grad, double* objective);
 
 /* The CEM loop in pieces, for multi-GPU drivers that shard each population
  * and all-gather the scores between sample() and update(). */

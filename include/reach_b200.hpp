@@ -18,6 +18,9 @@
 //   reach_with_splitting(cl_reach)              reach_b200::reach_with_splitting_cl
 //   ct_reach + zero/diag_linear/rotation/       reach_b200::ct_reach / ct_reach_batch +
 //   quadrotor_field (flowpipe_ct.hpp, fields.hpp)  AnalyticField::{zero, diag_linear, rotation, quadrotor}
+//   Constraint / PlanProblem / SamplerConfig /  reach_b200::Constraint / PlanProblem / SamplerConfig /
+//   PlanResult / plan_objective / plan_cem      PlanResult / plan_objective(_batch) / plan_cem
+//   grad_forward(plan_objective) (refine.hpp)   reach_b200::plan_objective_grad
 //
 // For code that already holds the reference's own types, see
 // reach_b200_reference.hpp (drop-in overloads taking reach:: types).
@@ -460,6 +463,204 @@ inline std::vector<ReachTube> ct_reach_batch(Context& ctx, const AnalyticField& 
 
 inline ReachTube ct_reach(Context& ctx, const AnalyticField& f, const Box& x0, const FlowpipeParams& prm) {
   return ct_reach_batch(ctx, f, {x0}, prm).front();
+}
+
+// ---------------------------------------------------------------------------
+// Reachability-aware MPC (mpc.hpp).
+
+struct Constraint {  // mpc.hpp:25-112
+  enum class Type { halfspace_avoid = REACH_CON_HALFSPACE_AVOID, sphere_avoid = REACH_CON_SPHERE_AVOID,
+                    box_stay_in = REACH_CON_BOX_STAY_IN, max_volume = REACH_CON_MAX_VOLUME };
+  Type type = Type::max_volume;
+  std::vector<int> dims;  // empty = all state dims
+  std::vector<double> a;
+  double b = 0.0;
+  std::vector<double> center;
+  double radius = 0.0;
+  std::vector<double> lo, hi;
+  double vmax = 0.0;
+};
+
+struct PlanProblem {  // mpc.hpp:115-142
+  DTSystem sys;
+  std::vector<double> x_goal, q_weights, r_weights;
+  std::vector<Constraint> constraints;
+  double penalty = 100.0;
+  double diverged_margin = 1e3;
+  int horizon = 5;
+  std::vector<double> u_lo, u_hi;
+  double eps = 0.0;
+  DTReachParams dt_prm;
+};
+
+struct SamplerConfig {  // mpc.hpp:220-234
+  int population = 256;
+  double elite_frac = 0.1;
+  int iterations = 5;
+  double init_std = 0.3;
+  double smoothing = 0.5;
+  int refine_iters = 5;
+  uint64_t seed = 0;
+};
+
+struct PlanResult {  // mpc.hpp:236-243
+  std::vector<std::vector<double>> actions;
+  double objective = 0.0;
+  ReachTube tube;
+  std::vector<double> best_history;
+  bool best_effort = false;
+  bool refined = false;
+};
+
+namespace detail {
+
+// The C ABI view of a PlanProblem; owns the flattened constraint arrays.
+struct PlanC {
+  reach_plan_problem p{};
+  std::vector<reach_constraint> cons;
+  std::vector<std::vector<int32_t>> dims;
+  explicit PlanC(const PlanProblem& pr) {
+    pr.sys.validate();
+    for (const auto& c : pr.constraints) {
+      dims.emplace_back(c.dims.begin(), c.dims.end());
+      reach_constraint r{};
+      r.type = static_cast<int32_t>(c.type);
+      r.n_dims = static_cast<int32_t>(c.dims.size());
+      r.dims = dims.back().empty() ? nullptr : dims.back().data();
+      r.a = c.a.empty() ? nullptr : c.a.data();
+      r.b = c.b;
+      r.center = c.center.empty() ? nullptr : c.center.data();
+      r.radius = c.radius;
+      r.lo = c.lo.empty() ? nullptr : c.lo.data();
+      r.hi = c.hi.empty() ? nullptr : c.hi.data();
+      r.vmax = c.vmax;
+      cons.push_back(r);
+    }
+    // sizes the ABI cannot see are checked here (PlanProblem::validate, mpc.hpp:129-141)
+    const size_t n = static_cast<size_t>(pr.sys.n), m = static_cast<size_t>(pr.sys.m);
+    if (pr.x_goal.size() != n || pr.q_weights.size() != n || pr.r_weights.size() != m)
+      throw std::invalid_argument("PlanProblem: cost dimension mismatch");
+    if (pr.u_lo.size() != m || pr.u_hi.size() != m)
+      throw std::invalid_argument("PlanProblem: action box dimension mismatch");
+    for (const auto& c : pr.constraints) {
+      const size_t k = c.dims.empty() ? n : c.dims.size();
+      const bool ok = c.type == Constraint::Type::halfspace_avoid ? c.a.size() == k
+                      : c.type == Constraint::Type::sphere_avoid  ? c.center.size() == k
+                      : c.type == Constraint::Type::box_stay_in   ? c.lo.size() == k && c.hi.size() == k
+                                                                  : true;
+      if (!ok) throw std::invalid_argument("Constraint: parameter size");
+    }
+    p.n = pr.sys.n;
+    p.m = pr.sys.m;
+    p.horizon = pr.horizon;
+    p.window = pr.dt_prm.window;
+    p.rebuild_from_box = pr.dt_prm.rebuild_from_box ? 1 : 0;
+    p.x_goal = pr.x_goal.data();
+    p.q_weights = pr.q_weights.data();
+    p.r_weights = pr.r_weights.data();
+    p.n_constraints = static_cast<int32_t>(cons.size());
+    p.constraints = cons.empty() ? nullptr : cons.data();
+    p.penalty = pr.penalty;
+    p.diverged_margin = pr.diverged_margin;
+    p.eps = pr.eps;
+    p.u_lo = pr.u_lo.data();
+    p.u_hi = pr.u_hi.data();
+  }
+};
+
+inline std::vector<double> flatten_plan(const PlanProblem& pr, const std::vector<std::vector<double>>& acts) {
+  if (static_cast<int>(acts.size()) != pr.horizon) throw std::invalid_argument("plan: horizon mismatch");
+  std::vector<double> flat;
+  flat.reserve(static_cast<size_t>(pr.horizon) * pr.sys.m);
+  for (const auto& u : acts) {
+    if (static_cast<int>(u.size()) != pr.sys.m) throw std::invalid_argument("plan: action dimension mismatch");
+    flat.insert(flat.end(), u.begin(), u.end());
+  }
+  return flat;
+}
+
+}  // namespace detail
+
+// plan_objective (mpc.hpp:204-208) of a batch of action sequences, evaluated
+// together (plan_eval's objective and diverged flag per candidate).
+inline std::vector<double> plan_objective_batch(Context& ctx, const PlanProblem& pr, const std::vector<double>& x0,
+                                                const std::vector<std::vector<std::vector<double>>>& cands,
+                                                std::vector<bool>* diverged = nullptr) {
+  detail::PlanC pc(pr);
+  if (static_cast<int>(x0.size()) != pr.sys.n) throw std::invalid_argument("plan_eval: x0 dimension mismatch");
+  std::vector<double> flat;
+  for (const auto& c : cands) {
+    auto f = detail::flatten_plan(pr, c);
+    flat.insert(flat.end(), f.begin(), f.end());
+  }
+  const int B = static_cast<int>(cands.size());
+  std::vector<double> obj(B);
+  std::vector<int32_t> div(B);
+  if (B > 0)
+    ctx.check(reach_plan_eval_batch(ctx.raw(), ctx.upload(pr.sys.step), &pc.p, x0.data(), B, flat.data(),
+                                    obj.data(), div.data(), nullptr, 0),
+              "plan_eval");
+  if (diverged) diverged->assign(div.begin(), div.end());
+  return obj;
+}
+
+inline double plan_objective(Context& ctx, const PlanProblem& pr, const std::vector<double>& x0,
+                             const std::vector<std::vector<double>>& actions) {
+  return plan_objective_batch(ctx, pr, x0, {actions}).front();
+}
+
+// grad_forward (refine.hpp:186-207) of plan_objective over the flat action
+// sequence ([H][m], row-major): forward-dual directions evaluated on the device.
+inline std::vector<double> plan_objective_grad(Context& ctx, const PlanProblem& pr, const std::vector<double>& x0,
+                                               const std::vector<std::vector<double>>& actions,
+                                               double* objective = nullptr) {
+  detail::PlanC pc(pr);
+  if (static_cast<int>(x0.size()) != pr.sys.n) throw std::invalid_argument("plan_eval: x0 dimension mismatch");
+  auto flat = detail::flatten_plan(pr, actions);
+  std::vector<double> g(flat.size());
+  double obj = 0.0;
+  ctx.check(reach_plan_objective_grad(ctx.raw(), ctx.upload(pr.sys.step), &pc.p, x0.data(), flat.data(), g.data(),
+                                      &obj),
+            "grad_forward");
+  if (objective) *objective = obj;
+  return g;
+}
+
+// plan_cem (mpc.hpp:258-368): CEM over device-evaluated populations, then the
+// top candidate's gradient refinement (refine_iters > 0).
+inline PlanResult plan_cem(Context& ctx, const PlanProblem& pr, const SamplerConfig& cfg,
+                           const std::vector<double>& x0) {
+  detail::PlanC pc(pr);
+  if (static_cast<int>(x0.size()) != pr.sys.n) throw std::invalid_argument("plan_eval: x0 dimension mismatch");
+  reach_sampler_config c{cfg.population, cfg.elite_frac, cfg.iterations, cfg.init_std, cfg.smoothing,
+                         cfg.refine_iters, cfg.seed};
+  const int H = pr.horizon, m = pr.sys.m, n = pr.sys.n;
+  std::vector<double> best(static_cast<size_t>(H) * m), hist(cfg.iterations > 0 ? cfg.iterations : 1);
+  double obj = 0.0;
+  int32_t be = 0, rf = 0;
+  std::vector<double> olo(static_cast<size_t>(H + 1) * n), ohi(olo.size());
+  int32_t nb = 0, fs = -1, st = 0;
+  reach_tube_out o{olo.data(), ohi.data(), &nb, &fs, &st};
+  ctx.check(reach_plan_cem_ex(ctx.raw(), ctx.upload(pr.sys.step), &pc.p, &c, x0.data(), best.data(), &obj,
+                              hist.data(), &be, &rf, &o),
+            "plan_cem");
+  PlanResult r;
+  for (int t = 0; t < H; ++t) r.actions.emplace_back(best.begin() + t * m, best.begin() + (t + 1) * m);
+  r.objective = obj;
+  r.best_history.assign(hist.begin(), hist.begin() + cfg.iterations);
+  r.best_effort = be != 0;
+  r.refined = rf != 0;
+  for (int k = 0; k < nb; ++k) {
+    Box box(n);
+    for (int d = 0; d < n; ++d) box[d] = {olo[static_cast<size_t>(k) * n + d], ohi[static_cast<size_t>(k) * n + d]};
+    r.tube.boxes.push_back(std::move(box));
+    r.tube.t_lo.push_back(k);
+    r.tube.t_hi.push_back(k);
+  }
+  r.tube.failed_step = fs;
+  r.tube.diverged = st != REACH_TUBE_OK;
+  r.tube.failure_reason = st != REACH_TUBE_OK ? failure_reason(st) : "";
+  return r;
 }
 
 }  // namespace reach_b200

@@ -17,6 +17,7 @@
 
 #include "reach/closed_loop.hpp"
 #include "reach/dt_reach.hpp"
+#include "reach/mpc.hpp"
 #include "reach/refine.hpp"
 #include "reach/systems.hpp"
 #include "reach_b200.hpp"
@@ -144,6 +145,62 @@ inline reach::ReachTube<double> ct_reach(Context& ctx, const AnalyticField& f, c
   FlowpipeParams p{prm.h, prm.steps, prm.order, prm.eps_init, prm.refine_rounds, prm.enlargement,
                    prm.max_enlargements, prm.window};
   return to_reference(ct_reach(ctx, f, from_reference(x0), p));
+}
+
+// reach::plan_cem (mpc.hpp:258-368) on reference PlanProblem / SamplerConfig
+// values; returns the reference PlanResult (plan, objective, final tube,
+// history, best_effort, refined) computed on the device.
+inline PlanProblem from_reference(const reach::PlanProblem& p) {
+  PlanProblem q;
+  q.sys = from_reference(p.sys);
+  q.x_goal = p.x_goal;
+  q.q_weights = p.q_weights;
+  q.r_weights = p.r_weights;
+  for (const auto& c : p.constraints) {
+    Constraint k;
+    k.type = static_cast<Constraint::Type>(static_cast<int>(c.type));
+    k.dims = c.dims;
+    k.a = c.a;
+    k.b = c.b;
+    k.center = c.center;
+    k.radius = c.radius;
+    k.lo = c.lo;
+    k.hi = c.hi;
+    k.vmax = c.vmax;
+    q.constraints.push_back(std::move(k));
+  }
+  q.penalty = p.penalty;
+  q.diverged_margin = p.diverged_margin;
+  q.horizon = p.horizon;
+  q.u_lo = p.u_lo;
+  q.u_hi = p.u_hi;
+  q.eps = p.eps;
+  q.dt_prm = {p.dt_prm.window, p.dt_prm.rebuild_from_box};
+  return q;
+}
+
+inline reach::PlanResult plan_cem(Context& ctx, const reach::PlanProblem& prob, const reach::SamplerConfig& cfg,
+                                  const reach::Vec<double>& x0) {
+  prob.validate();
+  cfg.validate();
+  SamplerConfig c{cfg.population, cfg.elite_frac, cfg.iterations, cfg.init_std, cfg.smoothing, cfg.refine_iters,
+                  cfg.seed};
+  PlanResult r = plan_cem(ctx, from_reference(prob), c, x0);
+  reach::PlanResult out;
+  out.actions = r.actions;
+  out.objective = r.objective;
+  out.tube = to_reference(r.tube);
+  out.best_history = r.best_history;
+  out.best_effort = r.best_effort;
+  out.refined = r.refined;
+  return out;
+}
+
+// reach::plan_objective (mpc.hpp:204-208) with S = double.
+inline double plan_objective(Context& ctx, const reach::PlanProblem& prob, const reach::Vec<double>& x0,
+                             const std::vector<reach::Vec<double>>& actions) {
+  prob.validate();
+  return plan_objective(ctx, from_reference(prob), x0, actions);
 }
 
 }  // namespace reach_b200

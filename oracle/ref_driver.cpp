@@ -421,10 +421,46 @@ int ref_plan_eval_batch(const reach_net_desc* desc, const reach_plan_problem* p,
   return REACH_OK;
 }
 
+// grad_forward (refine.hpp:186-207) of plan_objective (mpc.hpp:204-208) -- the
+// gradient plan_cem's refinement takes (mpc.hpp:339-346).  Returns 1 where the
+// reference throws (non-finite objective or derivative).
+int ref_plan_objective_grad(const reach_net_desc* desc, const reach_plan_problem* p, const double* x0,
+                            const double* actions, double* grad) {
+  try {
+    PlanProblem prob = problem_from(desc, p);
+    const int h = p->horizon, m = p->m;
+    Vec<double> x(x0, x0 + p->n);
+    auto objective = [&](const auto& q) {
+      using S = typename std::decay_t<decltype(q)>::value_type;
+      std::vector<Vec<S>> acts(static_cast<size_t>(h));
+      for (int t = 0; t < h; ++t)
+        acts[static_cast<size_t>(t)] =
+            Vec<S>(q.begin() + static_cast<long>(t) * m, q.begin() + static_cast<long>(t + 1) * m);
+      return plan_objective(prob, x, acts);
+    };
+    Vec<double> flat(actions, actions + static_cast<size_t>(h) * m);
+    Gradient g = grad_forward(objective, flat);
+    for (size_t j = 0; j < g.g.size(); ++j) grad[j] = g.g[j];
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return REACH_OK;
+}
+
 // plan_cem (mpc.hpp:258-368), the reference driver itself (its own parallel_for).
+int ref_plan_cem_ex(const reach_net_desc* desc, const reach_plan_problem* p, const reach_sampler_config* c,
+                    const double* x0, double* best_actions, double* objective, double* best_history,
+                    int32_t* best_effort, int32_t* refined);
 int ref_plan_cem(const reach_net_desc* desc, const reach_plan_problem* p, const reach_sampler_config* c,
                  const double* x0, double* best_actions, double* objective, double* best_history,
                  int32_t* best_effort) {
+  int32_t refined = 0;
+  return ref_plan_cem_ex(desc, p, c, x0, best_actions, objective, best_history, best_effort, &refined);
+}
+
+int ref_plan_cem_ex(const reach_net_desc* desc, const reach_plan_problem* p, const reach_sampler_config* c,
+                    const double* x0, double* best_actions, double* objective, double* best_history,
+                    int32_t* best_effort, int32_t* refined) {
   try {
     PlanProblem prob = problem_from(desc, p);
     SamplerConfig cfg;
@@ -441,6 +477,7 @@ int ref_plan_cem(const reach_net_desc* desc, const reach_plan_problem* p, const 
     *objective = res.objective;
     for (size_t i = 0; i < res.best_history.size(); ++i) best_history[i] = res.best_history[i];
     *best_effort = res.best_effort ? 1 : 0;
+    *refined = res.refined ? 1 : 0;
   } catch (const std::exception&) {
     return REACH_E_INVALID_ARGUMENT;
   }

@@ -55,12 +55,16 @@ def _declare(lib):
                                           C.POINTER(A.TubeOut), C.c_int32]
     lib.reach_plan_cem.argtypes = [vp, vp, C.POINTER(A.PlanProblemC), C.POINTER(A.SamplerConfigC), dp, dp, dp, dp,
                                    ip, C.POINTER(A.TubeOut)]
+    lib.reach_plan_cem_ex.argtypes = [vp, vp, C.POINTER(A.PlanProblemC), C.POINTER(A.SamplerConfigC), dp, dp, dp, dp,
+                                      ip, ip, C.POINTER(A.TubeOut)]
+    lib.reach_plan_objective_grad.argtypes = [vp, vp, C.POINTER(A.PlanProblemC), dp, dp, dp, dp]
     lib.reach_cem_create.argtypes = [C.POINTER(A.PlanProblemC), C.POINTER(A.SamplerConfigC), C.POINTER(vp)]
     lib.reach_cem_destroy.argtypes = [vp]
     lib.reach_cem_sample.argtypes = [vp, dp]
     lib.reach_cem_update.argtypes = [vp, dp, ip]
     lib.reach_cem_result.argtypes = [vp, dp, dp, ip, dp]
-    for f in ("reach_plan_eval_batch", "reach_plan_cem", "reach_cem_create", "reach_cem_destroy",
+    for f in ("reach_plan_eval_batch", "reach_plan_cem", "reach_plan_cem_ex", "reach_plan_objective_grad",
+              "reach_cem_create", "reach_cem_destroy",
               "reach_cem_sample", "reach_cem_update", "reach_cem_result"):
         getattr(lib, f).restype = C.c_int
     lib.reach_debug_phase_cycles.restype = C.c_int

@@ -1,0 +1,569 @@
+// Forward-mode dual gradients of the MPC planning objective on the device:
+// grad_forward (refine.hpp:186-207) of plan_objective (mpc.hpp:158-208) over
+// the flat action sequence, the gradient plan_cem's top-candidate refinement
+// consumes (mpc.hpp:337-361, gradient_refine refine.hpp:347-398).
+//
+// One CTA per tangent direction j (action t = j / m, component j % m), all
+// directions in one launch: each CTA evaluates the whole objective -- nominal
+// rollout, dt_reach with certify_tm_input / crown_backward / fold_overflow /
+// symbolic_box, constraint penalties -- in reach::Dual arithmetic
+// (scalar.hpp:13-55) seeded with d(action_j) = 1, its working set (~120 KB)
+// in shared memory.  Inside a CTA every output element of a layer (IBP row,
+// Lambda.W entry, intercept row) is owned by one thread and accumulated in the
+// reference's order with separate roundings, so ReLU networks give the
+// reference's gradient bit for bit; reach::min / max / abs keep their Dual tie
+// and NaN rules (a.v <= b.v ? a : b, ...).  Every branch of the reference's
+// Dual pass depends on primal values only, so the CTAs follow one control path.
+#pragma once
+
+#include "dt_common.cuh"
+#include "dt_kernel.cuh"
+#include "plan.cuh"
+
+namespace rb {
+namespace dual {
+
+constexpr int kN = 8;     // state dim
+constexpr int kM = 4;     // action dim
+constexpr int kW = 128;   // widest layer (and nz + n of the prepended layer)
+constexpr int kL = 6;     // layers
+constexpr int kZ = 80;    // generator columns incl. the fresh block
+constexpr int kH = 64;    // horizon
+constexpr int kQ = 12;    // queue blocks
+
+// ---- reach::Dual (scalar.hpp:13-55) ------------------------------------------
+struct D {
+  double v, d;
+};
+__device__ __forceinline__ D dc(double v) { return D{v, 0.0}; }
+__device__ __forceinline__ D dadd(D a, D b) { return D{add(a.v, b.v), add(a.d, b.d)}; }
+__device__ __forceinline__ D dsub(D a, D b) { return D{sub(a.v, b.v), sub(a.d, b.d)}; }
+__device__ __forceinline__ D dneg(D a) { return D{-a.v, -a.d}; }
+__device__ __forceinline__ D dmul(D a, D b) { return D{mul(a.v, b.v), add(mul(a.d, b.v), mul(a.v, b.d))}; }
+__device__ __forceinline__ D ddiv(D a, D b) {
+  return D{__ddiv_rn(a.v, b.v), __ddiv_rn(sub(mul(a.d, b.v), mul(a.v, b.d)), mul(b.v, b.v))};
+}
+__device__ __forceinline__ D dmin(D a, D b) { return a.v <= b.v ? a : b; }
+__device__ __forceinline__ D dmax(D a, D b) { return a.v >= b.v ? a : b; }
+__device__ __forceinline__ D dabs(D a) { return a.v < 0.0 ? D{-a.v, -a.d} : a; }
+__device__ __forceinline__ D dtanh(D a) {
+  const double t = tanh(a.v);
+  return D{t, mul(sub(1.0, mul(t, t)), a.d)};
+}
+__device__ __forceinline__ D dsqrt(D a) {
+  const double s = __dsqrt_rn(a.v);
+  return D{s, a.v > 0.0 ? __ddiv_rn(a.d, mul(2.0, s)) : 0.0};
+}
+__device__ __forceinline__ bool dfin(D a) { return isfinite(a.v); }
+
+// ---- Interval<Dual> (interval.hpp:60-94) ----------------------------------------
+struct DI {
+  D lo, hi;
+};
+__device__ __forceinline__ DI iadd(DI a, DI b) { return DI{dadd(a.lo, b.lo), dadd(a.hi, b.hi)}; }
+__device__ __forceinline__ DI iscale(D a, DI x) {
+  return a.v >= 0.0 ? DI{dmul(a, x.lo), dmul(a, x.hi)} : DI{dmul(a, x.hi), dmul(a, x.lo)};
+}
+__device__ __forceinline__ D imid(DI x) { return dmul(dadd(x.lo, x.hi), dc(0.5)); }
+__device__ __forceinline__ D irad(DI x) { return dmul(dsub(x.hi, x.lo), dc(0.5)); }
+
+struct GradArgs {
+  PlanParams P;         // net, n, m, H, goal / weights / constraints staged on the device
+  int window, rebuild;
+  double eps;
+  const double* base;   // [H*m] the action sequence the gradient is taken at
+  double* grad;         // [H*m] d objective / d action_j
+  double* value;        // [H*m] primal objective seen by direction j
+};
+
+// Per-direction working set, in shared memory (one CTA per direction).
+struct Work {
+  D acts[kH][kM];
+  D c[kN];
+  D S[kN][kZ];          // [G0 | Q1 .. Qnq]
+  int wid[kQ];
+  int nq, stop, bad;
+  DI pre[kL - 1][kW];   // preactivations of the hidden layers
+  DI hb[2][kW];         // IBP boxes / nominal activations (.lo)
+  D lam[2][kN][kW];     // Lambda, double buffered
+  D rs[kW], rli[kW], rui[kW];  // relaxation of the current layer
+  D blo[kN], bup[kN], bf0[kW];
+  D oc[kN];
+  D oA[kN][kZ];
+  DI orem[kN];
+  D tlo[kH + 1][kN], thi[kH + 1][kN];
+  D g0[kN][kN], qa[kN][kN], qx[kN][kN], qe[kN][kN], rr[kN];
+  D obj;
+};
+
+constexpr int kThreads = 256;
+
+struct NetView {
+  const DevNet& N;
+  __device__ __forceinline__ double w(int l, int i, int j) const {
+    return N.blob[N.w_off[l] + static_cast<long long>(i) * N.ldw[l] + j];
+  }
+  // W_l^T copy of the hidden layers: consecutive rows i are consecutive addresses
+  __device__ __forceinline__ double wt(int l, int i, int j) const {
+    return N.blob[N.wt_off[l] + static_cast<long long>(j) * N.ldt[l] + i];
+  }
+  __device__ __forceinline__ double b(int l, int i) const { return N.blob[N.b_off[l] + i]; }
+};
+// relax_activation (neural.hpp:166-227) on a Dual preactivation; false = throw.
+__device__ inline bool relax_d(int act, DI pre, D& s, D& li, D& ui) {
+  if (!(dfin(pre.lo) && dfin(pre.hi))) return false;
+  const D l = pre.lo, u = pre.hi;
+  s = dc(0.0);
+  li = dc(0.0);
+  ui = dc(0.0);
+  if (act == REACH_ACT_IDENTITY) {
+    s = dc(1.0);
+  } else if (act == REACH_ACT_RELU) {
+    if (l.v >= 0.0) {
+      s = dc(1.0);
+    } else if (u.v <= 0.0) {
+      s = dc(0.0);
+    } else {
+      const D sl = ddiv(u, dsub(u, l));
+      s = sl;
+      ui = dmul(dneg(sl), l);
+      li = dmin(dc(0.0), dmin(dmul(dneg(sl), l), dsub(u, dmul(sl, u))));
+    }
+  } else {  // tanh
+    const D tl = dtanh(l), tu = dtanh(u);
+    const D sl = dmin(dsub(dc(1.0), dmul(tl, tl)), dsub(dc(1.0), dmul(tu, tu)));
+    s = sl;
+    D lo_int = dsub(dtanh(l), dmul(sl, l));
+    D hi_int = lo_int;
+    auto consider = [&](D x) {
+      const D g = dsub(dtanh(x), dmul(sl, x));
+      lo_int = dmin(lo_int, g);
+      hi_int = dmax(hi_int, g);
+    };
+    consider(u);
+    if (sl.v < 1.0 && sl.v > 0.0) {
+      const double xs = atanh(sqrt(1.0 - sl.v));
+      if (l.v <= xs && xs <= u.v) consider(dc(xs));
+      if (l.v <= -xs && -xs <= u.v) consider(dc(-xs));
+    }
+    const D margin = dadd(dmul(dsub(hi_int, lo_int), dc(1e-12)), dc(1e-15));
+    li = dsub(lo_int, margin);
+    ui = dadd(hi_int, margin);
+  }
+  return true;
+}
+
+__device__ __forceinline__ DI act_d(int act, DI p) {
+  if (act == REACH_ACT_RELU) return DI{dmax(p.lo, dc(0.0)), dmax(p.hi, dc(0.0))};
+  if (act == REACH_ACT_TANH) return DI{dtanh(p.lo), dtanh(p.hi)};
+  return p;
+}
+
+// certify_tm_input (neural.hpp:342-394) of the frozen network on x = c + A z
+// (A = W.S[:, :nz], zero remainder), by the whole CTA: every output element is
+// owned by one thread and accumulated in the reference's order.  Returns 1 on a
+// non-finite preactivation (relax_activation throws).  Ends synchronized.
+__device__ inline int certify_d(const NetView& net, int n, int nz, Work& W, int tid) {
+  const DevNet& N = net.N;
+  const int L = N.L, n_o = N.dims[L];
+  // prepended layer [A | I], b = c, domain [-1,1]^nz x [0,0]^n (box_affine_image)
+  for (int i = tid; i < n; i += kThreads) {
+    DI acc{dc(0.0), dc(0.0)};
+    for (int j = 0; j < nz; ++j) acc = iadd(acc, iscale(W.S[i][j], DI{dc(-1.0), dc(1.0)}));
+    for (int j = 0; j < n; ++j) acc = iadd(acc, iscale(dc(i == j ? 1.0 : 0.0), DI{dc(0.0), dc(0.0)}));
+    acc = iadd(acc, DI{W.c[i], W.c[i]});
+    W.hb[0][i] = acc;
+  }
+  if (tid == 0) W.bad = 0;
+  __syncthreads();
+  int cur = 0;
+  for (int t = 0; t + 1 < L; ++t) {  // IBP through the hidden layers (W^T rows: coalesced)
+    const int rows = N.dims[t + 1], cols = (t == 0) ? n : N.dims[t];
+    for (int u = tid; u < rows; u += kThreads) {
+      DI acc{dc(0.0), dc(0.0)};
+      for (int j = 0; j < cols; ++j) acc = iadd(acc, iscale(dc(net.wt(t, u, j)), W.hb[cur][j]));
+      const D bias = (t == 0) ? W.bf0[u] : dc(net.b(t, u));
+      acc = iadd(acc, DI{bias, bias});
+      W.pre[t][u] = acc;
+      W.hb[cur ^ 1][u] = act_d(N.acts[t], acc);
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  // crown_backward (neural.hpp:290-335): Lambda = I
+  int lb = 0, acols = n_o;
+  for (int e = tid; e < n_o * n_o; e += kThreads) {
+    const int i = e / n_o, j = e % n_o;
+    W.lam[lb][i][j] = dc(i == j ? 1.0 : 0.0);
+    if (j == 0) {
+      W.blo[i] = dc(0.0);
+      W.bup[i] = dc(0.0);
+    }
+  }
+  __syncthreads();
+  for (int l = L; l >= 0; --l) {  // wide layer l: 0 = prepend, else net layer l - 1
+    const int t = l - 1;
+    const int act = (l == 0) ? REACH_ACT_IDENTITY : N.acts[t];
+    const int cols = (l == 0) ? nz + n : (t == 0 ? n : N.dims[t]);
+    if (act != REACH_ACT_IDENTITY) {
+      for (int j = tid; j < acols; j += kThreads) {
+        D s, li, ui;
+        if (!relax_d(act, W.pre[t][j], s, li, ui)) W.bad = 1;
+        W.rs[j] = s;
+        W.rli[j] = li;
+        W.rui[j] = ui;
+      }
+      __syncthreads();
+      if (W.bad) return 1;
+    }
+    // per output row i: the relaxation intercepts (ascending j), Lambda *= s,
+    // then shift = matvec(Lambda, b) (linalg.hpp:40-51, 65-71)
+    for (int i = tid; i < n_o; i += kThreads) {
+      if (act != REACH_ACT_IDENTITY) {
+        D lo = W.blo[i], up = W.bup[i];
+        for (int j = 0; j < acols; ++j) {
+          const D aij = W.lam[lb][i][j];
+          if (aij.v >= 0.0) {
+            lo = dadd(lo, dmul(aij, W.rli[j]));
+            up = dadd(up, dmul(aij, W.rui[j]));
+          } else {
+            lo = dadd(lo, dmul(aij, W.rui[j]));
+            up = dadd(up, dmul(aij, W.rli[j]));
+          }
+          W.lam[lb][i][j] = dmul(aij, W.rs[j]);
+        }
+        W.blo[i] = lo;
+        W.bup[i] = up;
+      }
+      D acc = dc(0.0);
+      for (int j = 0; j < acols; ++j) {
+        const D bj = (l == 0) ? W.c[j] : (t == 0 ? W.bf0[j] : dc(net.b(t, j)));
+        acc = dadd(acc, dmul(W.lam[lb][i][j], bj));
+      }
+      W.blo[i] = dadd(W.blo[i], acc);
+      W.bup[i] = dadd(W.bup[i], acc);
+    }
+    __syncthreads();
+    // Lambda = matmul(Lambda, W_l) (linalg.hpp:53-63): element (i, j) sums k ascending
+    for (int e = tid; e < n_o * cols; e += kThreads) {
+      const int i = e / cols, j = e % cols;
+      D acc = dc(0.0);
+      for (int k = 0; k < acols; ++k) {
+        D wkj;
+        if (l == 0) wkj = (j < nz) ? W.S[k][j] : dc(j - nz == k ? 1.0 : 0.0);
+        else wkj = dc(net.w(t, k, j));
+        acc = dadd(acc, dmul(W.lam[lb][i][k], wkj));
+      }
+      W.lam[lb ^ 1][i][j] = acc;
+    }
+    __syncthreads();
+    lb ^= 1;
+    acols = cols;
+  }
+  // tail (neural.hpp:383-391)
+  for (int e = tid; e < n_o * nz; e += kThreads) W.oA[e / nz][e % nz] = W.lam[lb][e / nz][e % nz];
+  for (int i = tid; i < n_o; i += kThreads) {
+    const D mid = dmul(dadd(W.blo[i], W.bup[i]), dc(0.5));
+    W.oc[i] = mid;
+    DI rem{dsub(W.blo[i], mid), dsub(W.bup[i], mid)};
+    for (int j = 0; j < n; ++j) rem = iadd(rem, iscale(W.lam[lb][i][nz + j], DI{dc(0.0), dc(0.0)}));
+    W.orem[i] = rem;
+  }
+  __syncthreads();
+  return 0;
+}
+
+// row_abs_sum (linalg.hpp:134-141) in Dual (reach::abs).
+__device__ __forceinline__ D row_abs(const D* row, int cols) {
+  D acc = dc(0.0);
+  for (int j = 0; j < cols; ++j) acc = dadd(acc, dabs(row[j]));
+  return acc;
+}
+
+// mat_solve (linalg.hpp:96-132) on W.g0 (n x n) and W.qa (n x w) into W.qx.
+__device__ inline bool mat_solve_d(int n, int w, Work& W) {
+  D a[kN][kN], b[kN][kN];
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < n; ++j) a[i][j] = W.g0[i][j];
+    for (int j = 0; j < w; ++j) b[i][j] = W.qa[i][j];
+  }
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    double best = fabs(a[k][k].v);
+    for (int i = k + 1; i < n; ++i) {
+      const double cand = fabs(a[i][k].v);
+      if (cand > best) {
+        best = cand;
+        piv = i;
+      }
+    }
+    if (!(best > 1e-12)) return false;
+    if (piv != k) {
+      for (int j = 0; j < n; ++j) {
+        const D t = a[k][j];
+        a[k][j] = a[piv][j];
+        a[piv][j] = t;
+      }
+      for (int j = 0; j < w; ++j) {
+        const D t = b[k][j];
+        b[k][j] = b[piv][j];
+        b[piv][j] = t;
+      }
+    }
+    for (int i = k + 1; i < n; ++i) {
+      const D f = ddiv(a[i][k], a[k][k]);
+      for (int j = k; j < n; ++j) a[i][j] = dsub(a[i][j], dmul(f, a[k][j]));
+      for (int j = 0; j < w; ++j) b[i][j] = dsub(b[i][j], dmul(f, b[k][j]));
+    }
+  }
+  for (int i = n - 1; i >= 0; --i)
+    for (int j = 0; j < w; ++j) {
+      D acc = b[i][j];
+      for (int k = i + 1; k < n; ++k) acc = dsub(acc, dmul(a[i][k], W.qx[k][j]));
+      W.qx[i][j] = ddiv(acc, a[i][i]);
+    }
+  return true;
+}
+
+// fold_overflow (flowpipe_ct.hpp:317-350) with a square G0 (dt_reach).
+__device__ inline void fold_d(int n, int& nq, int cap, Work& W) {
+  while (nq > cap) {
+    const int w = W.wid[0];
+    int off_new = n;
+    for (int q = 0; q + 1 < nq; ++q) off_new += W.wid[q];
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < n; ++j) W.g0[i][j] = W.S[i][j];
+      for (int j = 0; j < w; ++j) W.qa[i][j] = W.S[i][n + j];
+    }
+    bool folded = false;
+    if (mat_solve_d(n, w, W)) {
+      double worst = 0.0;
+      for (int j = 0; j < n; ++j) {
+        W.rr[j] = dmul(row_abs(W.qx[j], w), dc(1.0 + 1e-12));
+        worst = (worst < W.rr[j].v) ? W.rr[j].v : worst;  // std::max on values
+      }
+      if (worst <= 1.0) {
+        for (int i = 0; i < n; ++i) {
+          for (int j = 0; j < w; ++j) W.qe[i][j] = dc(0.0);
+          for (int k = 0; k < n; ++k) {
+            const D gik = W.g0[i][k];
+            for (int j = 0; j < w; ++j) W.qe[i][j] = dadd(W.qe[i][j], dmul(gik, W.qx[k][j]));
+          }
+        }
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < w; ++j) W.qe[i][j] = dsub(W.qe[i][j], W.qa[i][j]);
+        for (int j = 0; j < n; ++j)
+          for (int i = 0; i < n; ++i) W.S[i][j] = dmul(W.S[i][j], dadd(dc(1.0), W.rr[j]));
+        for (int i = 0; i < n; ++i)
+          W.S[i][off_new + i] = dadd(W.S[i][off_new + i], dmul(row_abs(W.qe[i], w), dc(1.0 + 1e-12)));
+        folded = true;
+      }
+    }
+    if (!folded)
+      for (int i = 0; i < n; ++i) W.S[i][off_new + i] = dadd(W.S[i][off_new + i], row_abs(&W.S[i][n], w));
+    int total = n;
+    for (int q = 0; q < nq; ++q) total += W.wid[q];
+    for (int i = 0; i < n; ++i)
+      for (int j = n; j + w < total; ++j) W.S[i][j] = W.S[i][j + w];
+    for (int q = 0; q + 1 < nq; ++q) W.wid[q] = W.wid[q + 1];
+    --nq;
+  }
+}
+
+// Constraint::margin (mpc.hpp:40-86) in Dual on tube box t.
+__device__ inline D margin_d(const PlanParams& P, const DevConstraint& c, const D* lo, const D* hi) {
+  const int* dims = P.ibuf + c.dims_off;
+  const double* dv = P.dbuf;
+  switch (c.type) {
+    case 0: {
+      D worst = dc(c.b);
+      for (int j = 0; j < c.k; ++j) {
+        const int d = dims[j];
+        const double aj = dv[c.a_off + j];
+        const D term = aj >= 0.0 ? dmul(hi[d], dc(aj)) : dmul(lo[d], dc(aj));
+        worst = dsub(worst, term);
+      }
+      return worst;
+    }
+    case 1: {
+      D d2 = dc(0.0);
+      for (int j = 0; j < c.k; ++j) {
+        const int d = dims[j];
+        const double cj = dv[c.c_off + j];
+        D gap = dc(0.0);
+        if (lo[d].v > cj) gap = dsub(lo[d], dc(cj));
+        else if (hi[d].v < cj) gap = dsub(dc(cj), hi[d]);
+        d2 = dadd(d2, dmul(gap, gap));
+      }
+      return dsub(dsqrt(d2), dc(c.radius));
+    }
+    case 2: {
+      D worst = dc(__longlong_as_double(0x7ff0000000000000ll));
+      for (int j = 0; j < c.k; ++j) {
+        const int d = dims[j];
+        worst = dmin(worst, dsub(lo[d], dc(dv[c.lo_off + j])));
+        worst = dmin(worst, dsub(dc(dv[c.hi_off + j]), hi[d]));
+      }
+      return worst;
+    }
+    default: {
+      D v = dc(0.0);
+      for (int j = 0; j < c.k; ++j) v = dadd(v, dsub(hi[dims[j]], lo[dims[j]]));
+      return dsub(dc(c.vmax), v);
+    }
+  }
+}
+
+// plan_objective (mpc.hpp:158-208) in Dual, seeded on action component
+// j = blockIdx.x; one CTA per direction, the working set in shared memory.
+__global__ void __launch_bounds__(kThreads) plan_grad_kernel(const GradArgs G) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Work& W = *reinterpret_cast<Work*>(smem_raw);
+  const int j = blockIdx.x, tid = threadIdx.x;
+  const PlanParams& P = G.P;
+  const int H = P.H, n = P.n, m = P.m;
+  const NetView net{P.net};
+  const DevNet& N = P.net;
+  const int L = N.L;
+  for (int e = tid; e < H * m; e += kThreads) W.acts[e / m][e % m] = D{G.base[e], e == j ? 1.0 : 0.0};
+  if (tid == 0) W.obj = dc(0.0);
+  for (int i = tid; i < n; i += kThreads) W.hb[0][i].lo = dc(P.x0[i]);
+  __syncthreads();
+  // nominal rollout + stage costs (mpc.hpp:170-184), MLPNet::forward (neural.hpp:58-76)
+  int cur = 0;
+  for (int t = 0; t < H; ++t) {
+    for (int i = tid; i < m; i += kThreads) W.hb[cur][n + i].lo = W.acts[t][i];
+    __syncthreads();
+    for (int l = 0; l < L; ++l) {
+      const int rows = N.dims[l + 1], cols = N.dims[l];
+      for (int u = tid; u < rows; u += kThreads) {
+        D acc = dc(0.0);
+        if (l + 1 < L)
+          for (int q = 0; q < cols; ++q) acc = dadd(acc, dmul(dc(net.wt(l, u, q)), W.hb[cur][q].lo));
+        else
+          for (int q = 0; q < cols; ++q) acc = dadd(acc, dmul(dc(net.w(l, u, q)), W.hb[cur][q].lo));
+        D h = dadd(acc, dc(net.b(l, u)));
+        if (N.acts[l] == REACH_ACT_RELU) {
+          if (h.v < 0.0) h = dc(0.0);
+        } else if (N.acts[l] == REACH_ACT_TANH) {
+          h = dtanh(h);
+        }
+        W.hb[cur ^ 1][u].lo = h;
+      }
+      cur ^= 1;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      D obj = W.obj;
+      for (int i = 0; i < m; ++i) obj = dadd(obj, dmul(dmul(dc(P.r_w[i]), W.acts[t][i]), W.acts[t][i]));
+      for (int i = 0; i < n; ++i) {
+        const D dd = dsub(W.hb[cur][i].lo, dc(P.x_goal[i]));
+        obj = dadd(obj, dmul(dmul(dc(P.q_w[i]), dd), dd));
+      }
+      W.obj = obj;
+    }
+    // x_{t+1} stays in hb[cur][0..n); the next step appends its action behind it
+  }
+  __syncthreads();
+  // dt_reach (dt_reach.hpp:41-104) at radius eps around x0
+  const int cap = G.window > 0 ? G.window : 1;
+  auto init_state = [&](const D* lo, const D* hi) {
+    for (int e = tid; e < n * n; e += kThreads) {
+      const int i = e / n, q = e % n;
+      if (q == 0) W.c[i] = dmul(dadd(lo[i], hi[i]), dc(0.5));
+      W.S[i][q] = (i == q) ? dmul(dsub(hi[i], lo[i]), dc(0.5)) : dc(0.0);
+    }
+  };
+  if (tid == 0) {
+    for (int i = 0; i < n; ++i) {
+      const D c0 = dc(P.x0[i]), r0 = dc(G.eps);
+      W.tlo[0][i] = dsub(c0, r0);
+      W.thi[0][i] = dadd(c0, r0);
+    }
+    W.nq = 0;
+    W.stop = 0;
+  }
+  __syncthreads();
+  init_state(W.tlo[0], W.thi[0]);
+  int nb = 1;
+  for (int k = 0; k < H; ++k) {
+    // freeze_trailing_inputs (neural.hpp:398-413)
+    for (int u = tid; u < N.dims[1]; u += kThreads) {
+      D bb = dc(net.b(0, u));
+      for (int q = 0; q < m; ++q) bb = dadd(bb, dmul(dc(net.w(0, u, n + q)), W.acts[k][q]));
+      W.bf0[u] = bb;
+    }
+    __syncthreads();
+    const int nq = W.nq;
+    int nz = n;
+    for (int q = 0; q < nq; ++q) nz += W.wid[q];
+    if (certify_d(net, n, nz, W, tid)) break;  // relax_activation throws: tube failed at k
+    if (tid == 0) {
+      bool rfin = true;
+      for (int i = 0; i < n; ++i) rfin = rfin && dfin(W.orem[i].lo) && dfin(W.orem[i].hi);
+      W.stop = rfin ? 0 : 1;
+    }
+    __syncthreads();
+    if (W.stop) break;  // diverged certification
+    // re-seed (dt_reach.hpp:69-92)
+    for (int e = tid; e < n * (nz + n); e += kThreads) {
+      const int i = e / (nz + n), q = e % (nz + n);
+      if (q == 0) W.c[i] = dadd(W.oc[i], imid(W.orem[i]));
+      W.S[i][q] = q < nz ? W.oA[i][q] : (q - nz == i ? irad(W.orem[i]) : dc(0.0));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int nq2 = nq;
+      W.wid[nq2++] = n;
+      fold_d(n, nq2, cap, W);
+      W.nq = nq2;
+    }
+    __syncthreads();
+    // symbolic_box (flowpipe_ct.hpp:413-424)
+    for (int i = tid; i < n; i += kThreads) {
+      D r = row_abs(W.S[i], n);
+      int off = n;
+      for (int q = 0; q < W.nq; ++q) {
+        r = dadd(r, row_abs(&W.S[i][off], W.wid[q]));
+        off += W.wid[q];
+      }
+      W.tlo[k + 1][i] = dsub(W.c[i], r);
+      W.thi[k + 1][i] = dadd(W.c[i], r);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      bool fin = true;
+      for (int i = 0; i < n; ++i) fin = fin && dfin(W.tlo[k + 1][i]) && dfin(W.thi[k + 1][i]);
+      W.stop = fin ? 0 : 1;
+      if (fin && G.rebuild) W.nq = 0;
+    }
+    __syncthreads();
+    nb = k + 2;
+    if (W.stop) break;  // diverged box (pushed)
+    if (G.rebuild) {
+      init_state(W.tlo[k + 1], W.thi[k + 1]);
+      __syncthreads();
+    }
+  }
+  // constraint penalties over the tube (mpc.hpp:187-200)
+  if (tid == 0) {
+    D obj = W.obj;
+    for (int t = 1; t <= H; ++t) {
+      bool ok = t < nb;
+      for (int i = 0; ok && i < n; ++i) ok = dfin(W.tlo[t][i]) && dfin(W.thi[t][i]);
+      if (ok) {
+        for (int q = 0; q < P.n_con; ++q) {
+          const D g = margin_d(P, P.con[q], W.tlo[t], W.thi[t]);
+          obj = dadd(obj, dmul(dc(P.penalty), dmax(dc(0.0), dneg(g))));
+        }
+      } else if (P.n_con > 0) {
+        obj = dadd(obj, dc(P.penalty * P.diverged_margin * static_cast<double>(P.n_con)));
+      }
+    }
+    G.grad[j] = obj.d;
+    G.value[j] = obj.v;
+  }
+}
+
+}  // namespace dual
+}  // namespace rb

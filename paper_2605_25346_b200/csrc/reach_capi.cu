@@ -20,6 +20,7 @@
 
 #include "../../include/reach_b200.h"
 #include "diag.cuh"
+#include "dual_kernel.cuh"
 #include "dt_kernel.cuh"
 #include "plan.cuh"
 #include "wide_kernel.cuh"
@@ -990,6 +991,79 @@ int plan_eval_host(reach_ctx* ctx, const reach_net* net, const reach_plan_proble
   return REACH_OK;
 }
 
+// grad_forward (refine.hpp:186-207) of plan_objective over the flat action
+// sequence: one Dual pass per direction, all directions in one launch
+// (dual_kernel.cuh).  `value` receives the primal objective (equal in every
+// pass); returns REACH_OK, or REACH_E_CUDA family errors; non-finite
+// derivatives are reported through `finite`.
+int plan_grad_device(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* p, const double* x0,
+                     const double* actions, double* grad, double* value, bool* finite) {
+  namespace rd = rb::dual;
+  const int H = p->horizon, n = p->n, m = p->m, dim = H * m;
+  int maxw = 0;
+  for (int l = 0; l <= net->L; ++l) maxw = std::max(maxw, net->dims[l]);
+  const int cap = p->window > 0 ? p->window : 1;
+  if (n > rd::kN || m > rd::kM || maxw > rd::kW || net->L > rd::kL || H > rd::kH || n * (cap + 2) > rd::kZ ||
+      n * (cap + 2) + n > rd::kW || cap + 2 > rd::kQ)
+    return fail(ctx, REACH_E_UNSUPPORTED, "plan gradient: shape outside the Dual kernel family");
+  PlanBuffers pb;
+  pack_problem(p, pb);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t o_db = take(pb.db.size() * 8), o_ib = take(pb.ib.size() * 4), o_x0 = take(n * 8),
+               o_a = take(static_cast<size_t>(dim) * 8), o_g = take(static_cast<size_t>(dim) * 8),
+               o_v = take(static_cast<size_t>(dim) * 8);
+  int rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  RB_CUDA(cudaMemcpyAsync(Dp(o_db), pb.db.data(), pb.db.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(w + o_ib, pb.ib.data(), pb.ib.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_x0), x0, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_a), actions, static_cast<size_t>(dim) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  rd::GradArgs G{};
+  G.P = pb.P;
+  G.P.net = net->dev;
+  G.P.H = H;
+  G.P.n = n;
+  G.P.m = m;
+  G.P.x0 = Dp(o_x0);
+  G.P.dbuf = Dp(o_db);
+  G.P.ibuf = reinterpret_cast<const int*>(w + o_ib);
+  G.P.x_goal = Dp(o_db) + reinterpret_cast<intptr_t>(pb.P.x_goal);
+  G.P.q_w = Dp(o_db) + reinterpret_cast<intptr_t>(pb.P.q_w);
+  G.P.r_w = Dp(o_db) + reinterpret_cast<intptr_t>(pb.P.r_w);
+  G.window = p->window;
+  G.rebuild = p->rebuild_from_box;
+  G.eps = p->eps;
+  G.base = Dp(o_a);
+  G.grad = Dp(o_g);
+  G.value = Dp(o_v);
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  RB_CUDA(cudaFuncSetAttribute(rd::plan_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sizeof(rd::Work))));
+  rd::plan_grad_kernel<<<dim, rd::kThreads, sizeof(rd::Work), ctx->stream>>>(G);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  std::vector<double> vals(dim);
+  RB_CUDA(cudaMemcpyAsync(grad, Dp(o_g), static_cast<size_t>(dim) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(vals.data(), Dp(o_v), static_cast<size_t>(dim) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  *value = vals[0];
+  *finite = true;
+  for (int j = 0; j < dim; ++j)
+    if (!std::isfinite(vals[j]) || !std::isfinite(grad[j])) *finite = false;
+  return REACH_OK;
+}
+
 }  // namespace
 
 // CEM state (plan_cem, mpc.hpp:258-335): the reference's Rng (rng.hpp:13-52)
@@ -1068,14 +1142,28 @@ int reach_plan_eval_batch(reach_ctx* ctx, const reach_net* net, const reach_plan
   return plan_eval_host(ctx, net, prob, x0, batch, actions, objective, diverged, tubes);
 }
 
+namespace {
+int reach_cem_create_impl(const reach_plan_problem* prob, const reach_sampler_config* cfg, reach_cem** out,
+                          bool allow_refine);
+}
+
 int reach_cem_create(const reach_plan_problem* prob, const reach_sampler_config* cfg, reach_cem** out) {
+  return reach_cem_create_impl(prob, cfg, out, false);
+}
+
+}  // extern "C"
+
+namespace {
+int reach_cem_create_impl(const reach_plan_problem* prob, const reach_sampler_config* cfg, reach_cem** out,
+                          bool allow_refine) {
   if (!prob || !cfg || !out) return REACH_E_INVALID_ARGUMENT;
   *out = nullptr;
   // SamplerConfig::validate (mpc.hpp:228-233)
   if (cfg->population < 2 || cfg->elite_frac <= 0.0 || cfg->elite_frac > 1.0 || cfg->iterations < 1 ||
       cfg->init_std <= 0.0 || cfg->smoothing < 0.0 || cfg->smoothing >= 1.0 || cfg->refine_iters < 0)
     return REACH_E_INVALID_ARGUMENT;
-  if (cfg->refine_iters > 0) return REACH_E_UNSUPPORTED;  // gradient refinement is not on the device path
+  // the piecewise CEM API leaves the refinement to its driver (reach_plan_objective_grad)
+  if (cfg->refine_iters > 0 && !allow_refine) return REACH_E_UNSUPPORTED;
   if (prob->m < 1 || prob->horizon < 1) return REACH_E_INVALID_ARGUMENT;
   reach_cem* c = new reach_cem();
   c->h = prob->horizon;
@@ -1096,6 +1184,9 @@ int reach_cem_create(const reach_plan_problem* prob, const reach_sampler_config*
   *out = c;
   return REACH_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int reach_cem_destroy(reach_cem* cem) {
   delete cem;
@@ -1160,14 +1251,14 @@ int reach_cem_result(const reach_cem* c, double* best_actions, double* best_obje
   return REACH_OK;
 }
 
-int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
-                   const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
-                   double* best_history, int32_t* best_effort, const reach_tube_out* final_tube) {
+int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
+                      const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
+                      double* best_history, int32_t* best_effort, int32_t* refined, const reach_tube_out* final_tube) {
   if (!ctx || !net || !prob || !cfg || !x0 || !best_actions || !objective) return REACH_E_INVALID_ARGUMENT;
   int rc = validate_problem(ctx, net, prob);
   if (rc) return rc;
   reach_cem* c = nullptr;
-  rc = reach_cem_create(prob, cfg, &c);
+  rc = reach_cem_create_impl(prob, cfg, &c, /*allow_refine=*/true);
   if (rc) return fail(ctx, rc, "SamplerConfig: invalid configuration");
   std::unique_ptr<reach_cem> guard(c);
   const size_t dim = c->mean.size(), pop = cfg->population;
@@ -1217,10 +1308,109 @@ int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_proble
   int32_t be = 0;
   reach_cem_result(c, best_actions, &best_obj, &be, best_history);
   if (best_effort) *best_effort = be;
+  if (refined) *refined = 0;
+  // gradient refinement of the top candidate (mpc.hpp:337-361):
+  // gradient_refine (refine.hpp:347-398) with forward-dual gradients on the device
+  if (cfg->refine_iters > 0 && std::isfinite(best_obj)) {
+    const size_t d = dim;
+    std::vector<double> lo(d), hi(d), x(best_actions, best_actions + d), g(d), xn(d);
+    for (size_t k = 0; k < d; ++k) {
+      lo[k] = prob->u_lo[k % prob->m];
+      hi[k] = prob->u_hi[k % prob->m];
+    }
+    auto project = [&](std::vector<double>& v) {
+      for (size_t k = 0; k < d; ++k) v[k] = std::clamp(v[k], lo[k], hi[k]);
+    };
+    auto f = [&](const std::vector<double>& v, double& out) {
+      int32_t dv2 = 0;
+      return plan_eval_host(ctx, net, prob, x0, 1, v.data(), &out, &dv2, nullptr);
+    };
+    project(x);
+    double fx = 0.0;
+    rc = f(x, fx);
+    if (rc) return rc;
+    if (!std::isfinite(fx)) return fail(ctx, REACH_E_INVALID_ARGUMENT, "gradient_refine: initial objective non-finite");
+    int accepted_steps = 0;
+    std::vector<double> cands, fvals;
+    std::vector<int32_t> cdiv;
+    for (int it = 0; it < cfg->refine_iters; ++it) {
+      // grad_forward's primal pass (refine.hpp:190-193) re-evaluates f(x) = fx, finite by construction
+      // (checked above or accepted below): evaluation is deterministic, so it is not repeated here
+      double v = 0.0;
+      bool fin = true;
+      rc = plan_grad_device(ctx, net, prob, x0, x.data(), g.data(), &v, &fin);
+      if (rc) return rc;
+      if (!fin) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_forward: non-finite derivative");
+      double gnorm2 = 0.0;
+      for (size_t k = 0; k < d; ++k) gnorm2 += g[k] * g[k];
+      if (gnorm2 == 0.0) break;
+      // Armijo backtracking (RefineParams: step0 1, shrink 0.5, armijo 1e-4, 30 backtracks).  The trial
+      // points do not depend on earlier trials' objectives, so every trial up to the first one that does not
+      // move is evaluated in ONE batch on the device and the first accepted trial is taken in order --
+      // the same point the reference's sequential loop accepts.
+      cands.clear();
+      std::vector<double> moved_v;
+      double t = 1.0;
+      for (int bt = 0; bt < 30; ++bt, t *= 0.5) {
+        for (size_t k = 0; k < d; ++k) xn[k] = x[k] - t * g[k];
+        project(xn);
+        double moved = 0.0;
+        for (size_t k = 0; k < d; ++k) moved += g[k] * (x[k] - xn[k]);
+        if (moved <= 0.0) break;
+        cands.insert(cands.end(), xn.begin(), xn.end());
+        moved_v.push_back(moved);
+      }
+      const int nt = static_cast<int>(moved_v.size());
+      bool accepted = false;
+      if (nt > 0) {
+        fvals.assign(nt, 0.0);
+        cdiv.assign(nt, 0);
+        rc = plan_eval_host(ctx, net, prob, x0, nt, cands.data(), fvals.data(), cdiv.data(), nullptr);
+        if (rc) return rc;
+        for (int q = 0; q < nt; ++q) {
+          const double fn = fvals[q];
+          if (std::isfinite(fn) && fn <= fx - 1e-4 * moved_v[q]) {
+            std::copy(cands.begin() + static_cast<size_t>(q) * d, cands.begin() + static_cast<size_t>(q + 1) * d,
+                      x.begin());
+            fx = fn;
+            accepted = true;
+            ++accepted_steps;
+            break;
+          }
+        }
+      }
+      if (!accepted) break;
+    }
+    if (fx < best_obj) {
+      std::copy(x.begin(), x.end(), best_actions);
+      if (refined) *refined = accepted_steps > 0 ? 1 : 0;
+    }
+  }
   // final evaluation of the chosen plan (mpc.hpp:363-367)
   int32_t dv = 0;
   rc = plan_eval_host(ctx, net, prob, x0, 1, best_actions, objective, &dv, final_tube);
   return rc;
+}
+
+int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
+                   const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
+                   double* best_history, int32_t* best_effort, const reach_tube_out* final_tube) {
+  return reach_plan_cem_ex(ctx, net, prob, cfg, x0, best_actions, objective, best_history, best_effort, nullptr,
+                           final_tube);
+}
+
+int reach_plan_objective_grad(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
+                              const double* actions, double* grad, double* objective) {
+  if (!ctx || !net || !prob || !x0 || !actions || !grad) return REACH_E_INVALID_ARGUMENT;
+  int rc = validate_problem(ctx, net, prob);
+  if (rc) return rc;
+  double v = 0.0;
+  bool fin = true;
+  rc = plan_grad_device(ctx, net, prob, x0, actions, grad, &v, &fin);
+  if (rc) return rc;
+  if (objective) *objective = v;
+  if (!fin) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_forward: non-finite derivative");
+  return REACH_OK;
 }
 
 }  // extern "C"

@@ -2,9 +2,11 @@
 
     Constraint (mpc.hpp:26-110), PlanProblem (115-142), SamplerConfig (220-234),
     plan_eval (158-202), plan_cem (258-368), with every candidate population
-    evaluated on the device (C ABI reach_plan_eval_batch / reach_plan_cem).
-Gradient refinement of the top candidate (refine_iters > 0) is outside the
-device path and raises.
+    evaluated on the device (C ABI reach_plan_eval_batch / reach_plan_cem_ex),
+    and the top candidate's gradient refinement (refine_iters > 0, the
+    reference default; gradient_refine, refine.hpp:347-398) driven by
+    forward-dual gradients computed on the device (plan_objective_grad,
+    grad_forward refine.hpp:186-207).
 """
 from __future__ import annotations
 
@@ -138,12 +140,27 @@ class PlanResult:
     best_history: np.ndarray  # [iterations]
     best_effort: bool
     tube: object = None
+    refined: bool = False  # gradient refinement made progress (mpc.hpp:241)
+
+
+def plan_objective_grad(prob: PlanProblem, x0, actions, ctx: Optional[Context] = None):
+    """grad_forward (refine.hpp:186-207) of plan_objective over the flat action sequence
+    [H][m] -> (gradient [H][m], objective); one reach::Dual pass per direction on the device."""
+    prob.sys.validate()
+    ctx = ctx or default_context()
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    acts = np.ascontiguousarray(np.asarray(actions, np.float64).reshape(prob.horizon, prob.sys.m))
+    g = np.zeros_like(acts)
+    obj = np.zeros(1)
+    p, keep = prob.c_struct()
+    net = ctx.upload(prob.sys.step)
+    ctx.check(ctx._lib.reach_plan_objective_grad(ctx.handle, net, C.byref(p), A.dptr(x0), A.dptr(acts), A.dptr(g),
+                                                 A.dptr(obj)), "grad_forward")
+    return g, float(obj[0])
 
 
 def plan_cem(prob: PlanProblem, cfg: SamplerConfig, x0, ctx: Optional[Context] = None) -> PlanResult:
-    """plan_cem (mpc.hpp:258-368); refine_iters must be 0 on the device path."""
-    if cfg.refine_iters != 0:
-        raise NotImplementedError("plan_cem: gradient refinement (refine_iters > 0) is not on the device path")
+    """plan_cem (mpc.hpp:258-368), including the top-candidate gradient refinement."""
     prob.sys.validate()
     ctx = ctx or default_context()
     x0 = np.ascontiguousarray(x0, dtype=np.float64)
@@ -158,9 +175,11 @@ def plan_cem(prob: PlanProblem, cfg: SamplerConfig, x0, ctx: Optional[Context] =
     p, keep = prob.c_struct()
     c = cfg.c_struct()
     net = ctx.upload(prob.sys.step)
-    ctx.check(ctx._lib.reach_plan_cem(ctx.handle, net, C.byref(p), C.byref(c), A.dptr(x0), A.dptr(best),
-                                      A.dptr(obj), A.dptr(hist), A.iptr(be), C.byref(to)), "plan_cem")
-    return PlanResult(best, float(obj[0]), hist, bool(be[0]), tb.tube(0))
+    refined = np.zeros(1, np.int32)
+    ctx.check(ctx._lib.reach_plan_cem_ex(ctx.handle, net, C.byref(p), C.byref(c), A.dptr(x0), A.dptr(best),
+                                         A.dptr(obj), A.dptr(hist), A.iptr(be), A.iptr(refined), C.byref(to)),
+              "plan_cem")
+    return PlanResult(best, float(obj[0]), hist, bool(be[0]), tb.tube(0), bool(refined[0]))
 
 
 class CEM:

@@ -9,6 +9,7 @@
 #include "reach/closed_loop.hpp"
 #include "reach/dt_reach.hpp"
 #include "reach/fields.hpp"
+#include "reach/mpc.hpp"
 #include "reach/refine.hpp"
 #include "reach/rng.hpp"
 #include "reach_b200_reference.hpp"
@@ -177,6 +178,63 @@ int main() {
                                          qx0, qprm));
     if (r1 > 1e-9 || r2 > 1e-9) {
       std::printf("ct_reach: max rel diff rotation %.3e quadrotor %.3e\n", r1, r2);
+      ++failures;
+    }
+  }
+  // plan_cem with the reference-default gradient refinement (refine_iters = 5) on a ReLU model with
+  // every constraint type (test_mpc.cpp shape): plan, objective, history, flags and final tube bit-identical
+  {
+    Rng r2(77);
+    PlanProblem prob;
+    prob.sys.n = 3;
+    prob.sys.m = 2;
+    prob.sys.step = random_mlp(r2, 5, {24, 24}, 3, Act::Relu, 0.7);
+    for (auto& w : prob.sys.step.layers.back().w.a) w *= 0.4;
+    prob.x_goal = {0.3, -0.2, 0.1};
+    prob.q_weights = {1.0, 1.0, 1.0};
+    prob.r_weights = {0.05, 0.05};
+    Constraint a;
+    a.type = Constraint::Type::sphere_avoid;
+    a.dims = {0, 2};
+    a.center = {0.2, 0.1};
+    a.radius = 0.1;
+    Constraint b;
+    b.type = Constraint::Type::box_stay_in;
+    b.lo = {-1.0, -1.0, -1.0};
+    b.hi = {1.0, 1.0, 1.0};
+    Constraint c;
+    c.type = Constraint::Type::halfspace_avoid;
+    c.dims = {1};
+    c.a = {1.0};
+    c.b = 0.9;
+    Constraint d;
+    d.type = Constraint::Type::max_volume;
+    d.vmax = 0.5;
+    prob.constraints = {a, b, c, d};
+    prob.horizon = 6;
+    prob.u_lo = {-1.0, -1.0};
+    prob.u_hi = {1.0, 1.0};
+    prob.eps = 0.01;
+    SamplerConfig cfg;
+    cfg.population = 48;
+    cfg.iterations = 4;
+    cfg.seed = 3;
+    Vec<double> x0{0.05, -0.05, 0.0};
+    auto ref = reach::plan_cem(prob, cfg, x0);
+    auto got = reach_b200::plan_cem(gpu, prob, cfg, x0);
+    bool same = ref.actions == got.actions && ref.objective == got.objective &&
+                ref.best_history == got.best_history && ref.best_effort == got.best_effort &&
+                ref.refined == got.refined;
+    if (!same) {
+      std::printf("plan_cem: mismatch (objective %.17g / %.17g, refined %d / %d)\n", ref.objective, got.objective,
+                  int(ref.refined), int(got.refined));
+      ++failures;
+    }
+    failures += compare(ref.tube, got.tube, "plan_cem tube") ? 1 : 0;
+    const double o1 = reach::plan_objective(prob, x0, ref.actions);
+    const double o2 = reach_b200::plan_objective(gpu, prob, x0, ref.actions);
+    if (o1 != o2) {
+      std::printf("plan_objective: %.17g / %.17g\n", o1, o2);
       ++failures;
     }
   }

@@ -350,3 +350,37 @@ def oracle_ct_split_hull(f, x0_lo, x0_hi, plan, prm, begin=0, end=0):
 
 def ref_ct_split_hull(f, x0_lo, x0_hi, plan, prm, begin=0, end=0, threads=0):
     return _ct_hull(ref_lib(), "ref_", f, x0_lo, x0_hi, plan, prm, begin, end, threads)
+
+
+
+# --- forward-dual gradients of the MPC objective (grad_forward) ---------------
+def ref_plan_objective_grad(prob, x0, actions):
+    """The reference's grad_forward of plan_objective; None where it throws."""
+    dp = C.POINTER(C.c_double)
+    f = _mpc_fn(ref_lib(), "ref_plan_objective_grad", [C.POINTER(A.NetDesc), C.POINTER(A.PlanProblemC), dp, dp, dp])
+    x0 = np.ascontiguousarray(x0, np.float64)
+    acts = np.ascontiguousarray(np.asarray(actions, np.float64).reshape(prob.horizon, prob.sys.m))
+    g = np.zeros_like(acts)
+    desc, keep = prob.sys.step.desc()
+    p, keep2 = prob.c_struct()
+    rc = f(C.byref(desc), C.byref(p), A.dptr(x0), A.dptr(acts), A.dptr(g))
+    return None if rc else g
+
+
+def ref_plan_cem_ex(prob, cfg, x0):
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    f = _mpc_fn(ref_lib(), "ref_plan_cem_ex", [C.POINTER(A.NetDesc), C.POINTER(A.PlanProblemC),
+                                               C.POINTER(A.SamplerConfigC), dp, dp, dp, dp, ip, ip])
+    x0 = np.ascontiguousarray(x0, np.float64)
+    best = np.zeros((prob.horizon, prob.sys.m))
+    obj = np.zeros(1)
+    hist = np.zeros(cfg.iterations)
+    be = np.zeros(1, np.int32)
+    rf = np.zeros(1, np.int32)
+    desc, keep = prob.sys.step.desc()
+    p, keep2 = prob.c_struct()
+    c = cfg.c_struct()
+    rc = f(C.byref(desc), C.byref(p), C.byref(c), A.dptr(x0), A.dptr(best), A.dptr(obj), A.dptr(hist), A.iptr(be),
+           A.iptr(rf))
+    assert rc == 0, rc
+    return best, float(obj[0]), hist, bool(be[0]), bool(rf[0])
