@@ -259,6 +259,20 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
 int reach_plan_objective_grad(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
                               const double* actions, double* grad, double* objective);
 
+/* grad_tube_volume (refine.hpp:263-311): the gradient of tube_volume(dt_reach(sys, box_from_center(c, r),
+ * actions, prm)) (tube.hpp:40-46) with respect to GradTarget (refine.hpp:240) -- the X0 centre (radii held
+ * fixed; c, r = box_center / box_radius of [x0_lo, x0_hi]), the flat action sequence [H][m], or the one-step
+ * map's parameters in net_params order (neural.hpp:133-140) -- by GradMethod (refine.hpp:165):
+ * forward_dual (grad_forward: one reach::Dual pass per parameter, one CTA each) or finite_difference
+ * (grad_fd: central differences, h = 1e-5 * max(1, |p_j|), 2 passes per parameter), all passes in one
+ * launch.  `a` describes one tube (batch 1).  grad [dim]; subgradient = Gradient::subgradient (a ReLU
+ * preactivation bound sat exactly at zero, neural.hpp:180); volume = the primal tube volume.  A
+ * non-finite objective or derivative is REACH_E_INVALID_ARGUMENT (the reference throws). */
+enum reach_grad_target { REACH_GRAD_X0_CENTER = 0, REACH_GRAD_ACTIONS = 1, REACH_GRAD_WEIGHTS = 2 };
+enum reach_grad_method { REACH_GRAD_FORWARD_DUAL = 0, REACH_GRAD_FINITE_DIFFERENCE = 1 };
+int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
+                           int32_t method, double* grad, int32_t* subgradient, double* volume);
+
 /* The CEM loop in pieces, for multi-GPU drivers that shard each population
  * and all-gather the scores between sample() and update(). */
 typedef struct reach_cem reach_cem;

@@ -21,6 +21,8 @@
 //   Constraint / PlanProblem / SamplerConfig /  reach_b200::Constraint / PlanProblem / SamplerConfig /
 //   PlanResult / plan_objective / plan_cem      PlanResult / plan_objective(_batch) / plan_cem
 //   grad_forward(plan_objective) (refine.hpp)   reach_b200::plan_objective_grad
+//   GradTarget / GradMethod / Gradient /        reach_b200::GradTarget / GradMethod / Gradient /
+//   grad_tube_volume (refine.hpp:165-311)       grad_tube_volume
 //
 // For code that already holds the reference's own types, see
 // reach_b200_reference.hpp (drop-in overloads taking reach:: types).
@@ -661,6 +663,53 @@ inline PlanResult plan_cem(Context& ctx, const PlanProblem& pr, const SamplerCon
   r.tube.diverged = st != REACH_TUBE_OK;
   r.tube.failure_reason = st != REACH_TUBE_OK ? failure_reason(st) : "";
   return r;
+}
+
+// ---------------------------------------------------------------------------
+// Tube-volume gradients (refine.hpp:165-311).
+
+enum class GradTarget { x0_center = REACH_GRAD_X0_CENTER, actions = REACH_GRAD_ACTIONS, weights = REACH_GRAD_WEIGHTS };
+enum class GradMethod { forward_dual = REACH_GRAD_FORWARD_DUAL, finite_difference = REACH_GRAD_FINITE_DIFFERENCE };
+
+struct Gradient {  // refine.hpp:171-178
+  std::vector<double> g;
+  GradMethod method = GradMethod::forward_dual;
+  bool subgradient = false;
+};
+
+// grad_tube_volume (refine.hpp:263-311): every pass on the device, one launch.
+inline Gradient grad_tube_volume(Context& ctx, const DTSystem& sys, const Box& x0,
+                                 const std::vector<std::vector<double>>& actions, GradTarget target,
+                                 GradMethod method = GradMethod::forward_dual, const DTReachParams& prm = {}) {
+  sys.validate();
+  const int n = sys.n, m = sys.m, H = static_cast<int>(actions.size());
+  if (static_cast<int>(x0.size()) != n) throw std::invalid_argument("dt_reach: X0 dimension mismatch");
+  std::vector<double> lo(n), hi(n), acts;
+  for (int d = 0; d < n; ++d) {
+    lo[d] = x0[d].lo;
+    hi[d] = x0[d].hi;
+  }
+  for (const auto& u : actions) {
+    if (static_cast<int>(u.size()) != m) throw std::invalid_argument("dt_reach: action dimension mismatch");
+    acts.insert(acts.end(), u.begin(), u.end());
+  }
+  size_t dim = 0;
+  if (target == GradTarget::x0_center) dim = n;
+  else if (target == GradTarget::actions) dim = acts.size();
+  else
+    for (const auto& L : sys.step.layers) dim += L.w.size() + L.b.size();
+  Gradient out;
+  out.method = method;
+  out.g.assign(std::max<size_t>(dim, 1), 0.0);
+  int32_t sub = 0;
+  reach_dt_args a{1, H, n, m, prm.window, prm.rebuild_from_box ? 1 : 0, lo.data(), hi.data(),
+                  acts.empty() ? nullptr : acts.data(), 0};
+  ctx.check(reach_grad_tube_volume(ctx.raw(), ctx.upload(sys.step), &a, static_cast<int32_t>(target),
+                                   static_cast<int32_t>(method), out.g.data(), &sub, nullptr),
+            "grad_tube_volume");
+  out.g.resize(dim);
+  out.subgradient = sub != 0;
+  return out;
 }
 
 }  // namespace reach_b200

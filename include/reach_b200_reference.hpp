@@ -203,4 +203,25 @@ inline double plan_objective(Context& ctx, const reach::PlanProblem& prob, const
   return plan_objective(ctx, from_reference(prob), x0, actions);
 }
 
+// reach::grad_tube_volume (refine.hpp:263-311) -> reach::Gradient, computed on the device.
+inline reach::Gradient grad_tube_volume(Context& ctx, const reach::DTSystem<double>& sys,
+                                        const reach::IntervalBox<double>& x0,
+                                        const std::vector<reach::Vec<double>>& actions, reach::GradTarget target,
+                                        reach::GradMethod method = reach::GradMethod::forward_dual,
+                                        const reach::DTReachParams& prm = {}) {
+  sys.validate();
+  const GradTarget t = target == reach::GradTarget::x0_center ? GradTarget::x0_center
+                       : target == reach::GradTarget::actions ? GradTarget::actions
+                                                              : GradTarget::weights;
+  const GradMethod me =
+      method == reach::GradMethod::forward_dual ? GradMethod::forward_dual : GradMethod::finite_difference;
+  Gradient g = grad_tube_volume(ctx, from_reference(sys), from_reference(x0), actions, t, me,
+                                DTReachParams{prm.window, prm.rebuild_from_box});
+  reach::Gradient out;
+  out.g = g.g;
+  out.method = method;
+  out.subgradient = g.subgradient;
+  return out;
+}
+
 }  // namespace reach_b200

@@ -211,6 +211,26 @@ int ref_reach_with_splitting(const reach_net_desc* desc, const reach_split_args*
   return REACH_OK;
 }
 
+// reach::grad_tube_volume (refine.hpp:263-311); REACH_E_INVALID_ARGUMENT where it throws.
+int ref_grad_tube_volume(const reach_net_desc* desc, const reach_dt_args* a, int32_t target, int32_t method,
+                         double* grad, int32_t* subgradient) {
+  try {
+    DTSystem<double> sys = make_sys(desc, a->n, a->m);
+    DTReachParams prm;
+    prm.window = a->window;
+    prm.rebuild_from_box = a->rebuild_from_box != 0;
+    const GradTarget t = target == 0 ? GradTarget::x0_center : target == 1 ? GradTarget::actions : GradTarget::weights;
+    const GradMethod me = method == 0 ? GradMethod::forward_dual : GradMethod::finite_difference;
+    Gradient g = grad_tube_volume(sys, box_at(a->x0_lo, a->x0_hi, a->n), actions_at(a->actions, a->horizon, a->m), t,
+                                  me, prm);
+    std::copy(g.g.begin(), g.g.end(), grad);
+    if (subgradient) *subgradient = g.subgradient ? 1 : 0;
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}
+
 int ref_hardware_threads(void) { return hardware_threads(); }
 
 }  // extern "C"

@@ -17,6 +17,8 @@ templates for the DT reachability path:
     zero_field, diag_linear_field,  fields.hpp:51-92 (the analytic VectorFields the device runs)
     rotation_field, quadrotor_field
     ct_reach                        flowpipe_ct.hpp:428-458
+    GradTarget, GradMethod,         refine.hpp:165-311 (forward-dual passes on the device)
+    Gradient, grad_tube_volume
 
 Every compute call runs the CUDA kernels through the C ABI
 (include/reach_b200.h); there is no CPU path.  Shape errors raise
@@ -259,6 +261,55 @@ def dt_reach(sys: DTSystem, x0, actions: Sequence, prm: DTReachParams = DTReachP
              ctx: Optional[Context] = None) -> ReachTube:
     """dt_reach (dt_reach.hpp:40-104): x0 = (lo, hi)."""
     return dt_reach_batch(sys, [x0], [actions], prm, ctx)[0]
+
+
+# ---------------------------------------------------------------------------
+class GradTarget(enum.IntEnum):  # refine.hpp:240
+    x0_center = 0
+    actions = 1
+    weights = 2
+
+
+class GradMethod(enum.IntEnum):  # refine.hpp:165
+    forward_dual = 0
+    finite_difference = 1
+
+
+@dataclass
+class Gradient:  # refine.hpp:171-178
+    g: np.ndarray
+    method: GradMethod = GradMethod.forward_dual
+    subgradient: bool = False
+    volume: float = 0.0  # the primal tube volume the gradient was taken at
+
+
+def grad_tube_volume(sys: DTSystem, x0, actions: Sequence, target: GradTarget,
+                     method: GradMethod = GradMethod.forward_dual, prm: DTReachParams = DTReachParams(),
+                     ctx: Optional[Context] = None) -> Gradient:
+    """grad_tube_volume (refine.hpp:263-311): d tube_volume(dt_reach(...)) / d target, x0 = (lo, hi).
+    Parameter layouts: x0_center [n]; actions [H*m] step-major; weights in net_params order
+    (neural.hpp:133-140).  Every pass (one per parameter, two per parameter for finite differences)
+    runs on the device in one launch.  Raises ValueError where the reference throws."""
+    sys.validate()
+    ctx = ctx or default_context()
+    lo = np.ascontiguousarray(x0[0], dtype=np.float64).reshape(-1)
+    hi = np.ascontiguousarray(x0[1], dtype=np.float64).reshape(-1)
+    if lo.size != sys.n or hi.size != sys.n:
+        raise ValueError("dt_reach: X0 dimension mismatch")
+    H = len(actions)
+    acts = _actions_array([actions], 1, H, sys.m).reshape(-1)
+    target, method = GradTarget(target), GradMethod(method)
+    dim = {GradTarget.x0_center: sys.n, GradTarget.actions: H * sys.m,
+           GradTarget.weights: int(sys.step.params().size)}[target]
+    g = np.zeros(max(dim, 1))
+    sub = np.zeros(1, np.int32)
+    vol = np.zeros(1)
+    args = A.DTArgs(1, H, sys.n, sys.m, prm.window, int(prm.rebuild_from_box), A.dptr(lo), A.dptr(hi),
+                    A.dptr(acts if acts.size else np.zeros(1)), 0)
+    net = ctx.upload(sys.step)
+    ctx.check(ctx._lib.reach_grad_tube_volume(ctx.handle, net, C.byref(args), int(target), int(method), A.dptr(g),
+                                              A.iptr(sub), A.dptr(vol)), "grad_tube_volume")
+    return Gradient(g[:dim].copy(), method, bool(sub[0]), float(vol[0]))
 
 
 # ---------------------------------------------------------------------------

@@ -43,6 +43,7 @@ struct reach_net {
   int cpl = 0;  // hidden units per lane of the kernel family (0 = unsupported width)
   int hp = 0;   // padded hidden width 32 * cpl
   std::vector<int> dims, acts;
+  std::vector<double> params;  // host copy in net_params order (neural.hpp:133-140)
 };
 
 namespace rbh {

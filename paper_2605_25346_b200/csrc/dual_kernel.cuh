@@ -82,11 +82,13 @@ struct Work {
   D c[kN];
   D S[kN][kZ];          // [G0 | Q1 .. Qnq]
   int wid[kQ];
-  int nq, stop, bad;
+  int nq, stop, bad, sub;
   DI pre[kL - 1][kW];   // preactivations of the hidden layers
-  DI hb[2][kW];         // IBP boxes / nominal activations (.lo)
+  union {
+    DI hb[2][kW];       // IBP boxes / nominal activations (.lo)
+    D rel[3][kW];       // crown: relaxation (slope, lower, upper intercept) of the current layer
+  };
   D lam[2][kN][kW];     // Lambda, double buffered
-  D rs[kW], rli[kW], rui[kW];  // relaxation of the current layer
   D blo[kN], bup[kN], bf0[kW];
   D oc[kN];
   D oA[kN][kZ];
@@ -97,22 +99,37 @@ struct Work {
 };
 
 constexpr int kThreads = 256;
+// two CTAs (directions) per SM: 2 x (Work + 1 KB static + 1 KB reserved) <= 228 KB
+static_assert(sizeof(Work) <= 112 * 1024, "dual working set must fit two CTAs per SM");
 
+// The network as Dual values: every parameter is a constant except, for a
+// weights-target pass (grad_tube_volume, refine.hpp:234-236), the seeded one
+// (layer sl, row si, column sj; sj = -1: the bias), whose value is shifted by
+// `delta` (finite differences) and whose tangent is `seed`.
 struct NetView {
   const DevNet& N;
-  __device__ __forceinline__ double w(int l, int i, int j) const {
-    return N.blob[N.w_off[l] + static_cast<long long>(i) * N.ldw[l] + j];
+  int sl = -1, si = -1, sj = -2;
+  double delta = 0.0, seed = 0.0;
+  __device__ __forceinline__ D pick(double v, int l, int i, int j) const {
+    if (l != sl || i != si || j != sj) return dc(v);
+    return D{delta != 0.0 ? add(v, delta) : v, seed};
+  }
+  __device__ __forceinline__ D w(int l, int i, int j) const {
+    return pick(N.blob[N.w_off[l] + static_cast<long long>(i) * N.ldw[l] + j], l, i, j);
   }
   // W_l^T copy of the hidden layers: consecutive rows i are consecutive addresses
-  __device__ __forceinline__ double wt(int l, int i, int j) const {
-    return N.blob[N.wt_off[l] + static_cast<long long>(j) * N.ldt[l] + i];
+  __device__ __forceinline__ D wt(int l, int i, int j) const {
+    return pick(N.blob[N.wt_off[l] + static_cast<long long>(j) * N.ldt[l] + i], l, i, j);
   }
-  __device__ __forceinline__ double b(int l, int i) const { return N.blob[N.b_off[l] + i]; }
+  __device__ __forceinline__ D b(int l, int i) const { return pick(N.blob[N.b_off[l] + i], l, i, -1); }
 };
+
 // relax_activation (neural.hpp:166-227) on a Dual preactivation; false = throw.
-__device__ inline bool relax_d(int act, DI pre, D& s, D& li, D& ui) {
+__device__ inline bool relax_d(int act, DI pre, D& s, D& li, D& ui, bool& boundary) {
   if (!(dfin(pre.lo) && dfin(pre.hi))) return false;
   const D l = pre.lo, u = pre.hi;
+  // note_branch_boundary (neural.hpp:180): the gradient is only a subgradient
+  if (act == REACH_ACT_RELU && (l.v == 0.0 || u.v == 0.0)) boundary = true;
   s = dc(0.0);
   li = dc(0.0);
   ui = dc(0.0);
@@ -163,7 +180,7 @@ __device__ __forceinline__ DI act_d(int act, DI p) {
 // (A = W.S[:, :nz], zero remainder), by the whole CTA: every output element is
 // owned by one thread and accumulated in the reference's order.  Returns 1 on a
 // non-finite preactivation (relax_activation throws).  Ends synchronized.
-__device__ inline int certify_d(const NetView& net, int n, int nz, Work& W, int tid) {
+__device__ __forceinline__ int certify_d(const NetView& net, int n, int nz, Work& W, int tid) {
   const DevNet& N = net.N;
   const int L = N.L, n_o = N.dims[L];
   // prepended layer [A | I], b = c, domain [-1,1]^nz x [0,0]^n (box_affine_image)
@@ -181,8 +198,8 @@ __device__ inline int certify_d(const NetView& net, int n, int nz, Work& W, int 
     const int rows = N.dims[t + 1], cols = (t == 0) ? n : N.dims[t];
     for (int u = tid; u < rows; u += kThreads) {
       DI acc{dc(0.0), dc(0.0)};
-      for (int j = 0; j < cols; ++j) acc = iadd(acc, iscale(dc(net.wt(t, u, j)), W.hb[cur][j]));
-      const D bias = (t == 0) ? W.bf0[u] : dc(net.b(t, u));
+      for (int j = 0; j < cols; ++j) acc = iadd(acc, iscale(net.wt(t, u, j), W.hb[cur][j]));
+      const D bias = (t == 0) ? W.bf0[u] : net.b(t, u);
       acc = iadd(acc, DI{bias, bias});
       W.pre[t][u] = acc;
       W.hb[cur ^ 1][u] = act_d(N.acts[t], acc);
@@ -208,10 +225,12 @@ __device__ inline int certify_d(const NetView& net, int n, int nz, Work& W, int 
     if (act != REACH_ACT_IDENTITY) {
       for (int j = tid; j < acols; j += kThreads) {
         D s, li, ui;
-        if (!relax_d(act, W.pre[t][j], s, li, ui)) W.bad = 1;
-        W.rs[j] = s;
-        W.rli[j] = li;
-        W.rui[j] = ui;
+        bool boundary = false;
+        if (!relax_d(act, W.pre[t][j], s, li, ui, boundary)) W.bad = 1;
+        if (boundary) W.sub = 1;
+        W.rel[0][j] = s;
+        W.rel[1][j] = li;
+        W.rel[2][j] = ui;
       }
       __syncthreads();
       if (W.bad) return 1;
@@ -224,20 +243,20 @@ __device__ inline int certify_d(const NetView& net, int n, int nz, Work& W, int 
         for (int j = 0; j < acols; ++j) {
           const D aij = W.lam[lb][i][j];
           if (aij.v >= 0.0) {
-            lo = dadd(lo, dmul(aij, W.rli[j]));
-            up = dadd(up, dmul(aij, W.rui[j]));
+            lo = dadd(lo, dmul(aij, W.rel[1][j]));
+            up = dadd(up, dmul(aij, W.rel[2][j]));
           } else {
-            lo = dadd(lo, dmul(aij, W.rui[j]));
-            up = dadd(up, dmul(aij, W.rli[j]));
+            lo = dadd(lo, dmul(aij, W.rel[2][j]));
+            up = dadd(up, dmul(aij, W.rel[1][j]));
           }
-          W.lam[lb][i][j] = dmul(aij, W.rs[j]);
+          W.lam[lb][i][j] = dmul(aij, W.rel[0][j]);
         }
         W.blo[i] = lo;
         W.bup[i] = up;
       }
       D acc = dc(0.0);
       for (int j = 0; j < acols; ++j) {
-        const D bj = (l == 0) ? W.c[j] : (t == 0 ? W.bf0[j] : dc(net.b(t, j)));
+        const D bj = (l == 0) ? W.c[j] : (t == 0 ? W.bf0[j] : net.b(t, j));
         acc = dadd(acc, dmul(W.lam[lb][i][j], bj));
       }
       W.blo[i] = dadd(W.blo[i], acc);
@@ -251,7 +270,7 @@ __device__ inline int certify_d(const NetView& net, int n, int nz, Work& W, int 
       for (int k = 0; k < acols; ++k) {
         D wkj;
         if (l == 0) wkj = (j < nz) ? W.S[k][j] : dc(j - nz == k ? 1.0 : 0.0);
-        else wkj = dc(net.w(t, k, j));
+        else wkj = net.w(t, k, j);
         acc = dadd(acc, dmul(W.lam[lb][i][k], wkj));
       }
       W.lam[lb ^ 1][i][j] = acc;
@@ -414,59 +433,16 @@ __device__ inline D margin_d(const PlanParams& P, const DevConstraint& c, const 
   }
 }
 
-// plan_objective (mpc.hpp:158-208) in Dual, seeded on action component
-// j = blockIdx.x; one CTA per direction, the working set in shared memory.
-__global__ void __launch_bounds__(kThreads) plan_grad_kernel(const GradArgs G) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Work& W = *reinterpret_cast<Work*>(smem_raw);
-  const int j = blockIdx.x, tid = threadIdx.x;
-  const PlanParams& P = G.P;
-  const int H = P.H, n = P.n, m = P.m;
-  const NetView net{P.net};
-  const DevNet& N = P.net;
-  const int L = N.L;
-  for (int e = tid; e < H * m; e += kThreads) W.acts[e / m][e % m] = D{G.base[e], e == j ? 1.0 : 0.0};
-  if (tid == 0) W.obj = dc(0.0);
-  for (int i = tid; i < n; i += kThreads) W.hb[0][i].lo = dc(P.x0[i]);
-  __syncthreads();
-  // nominal rollout + stage costs (mpc.hpp:170-184), MLPNet::forward (neural.hpp:58-76)
-  int cur = 0;
-  for (int t = 0; t < H; ++t) {
-    for (int i = tid; i < m; i += kThreads) W.hb[cur][n + i].lo = W.acts[t][i];
-    __syncthreads();
-    for (int l = 0; l < L; ++l) {
-      const int rows = N.dims[l + 1], cols = N.dims[l];
-      for (int u = tid; u < rows; u += kThreads) {
-        D acc = dc(0.0);
-        if (l + 1 < L)
-          for (int q = 0; q < cols; ++q) acc = dadd(acc, dmul(dc(net.wt(l, u, q)), W.hb[cur][q].lo));
-        else
-          for (int q = 0; q < cols; ++q) acc = dadd(acc, dmul(dc(net.w(l, u, q)), W.hb[cur][q].lo));
-        D h = dadd(acc, dc(net.b(l, u)));
-        if (N.acts[l] == REACH_ACT_RELU) {
-          if (h.v < 0.0) h = dc(0.0);
-        } else if (N.acts[l] == REACH_ACT_TANH) {
-          h = dtanh(h);
-        }
-        W.hb[cur ^ 1][u].lo = h;
-      }
-      cur ^= 1;
-      __syncthreads();
-    }
-    if (tid == 0) {
-      D obj = W.obj;
-      for (int i = 0; i < m; ++i) obj = dadd(obj, dmul(dmul(dc(P.r_w[i]), W.acts[t][i]), W.acts[t][i]));
-      for (int i = 0; i < n; ++i) {
-        const D dd = dsub(W.hb[cur][i].lo, dc(P.x_goal[i]));
-        obj = dadd(obj, dmul(dmul(dc(P.q_w[i]), dd), dd));
-      }
-      W.obj = obj;
-    }
-    // x_{t+1} stays in hb[cur][0..n); the next step appends its action behind it
-  }
-  __syncthreads();
-  // dt_reach (dt_reach.hpp:41-104) at radius eps around x0
-  const int cap = G.window > 0 ? G.window : 1;
+// dt_reach (dt_reach.hpp:41-104) in Dual from the box W.tlo[0] / W.thi[0]
+// (written and synchronized by the caller) under the actions W.acts, by the
+// whole CTA.  Returns the number of boxes pushed; `failed` = the tube was
+// marked failed (a relax_activation throw, a diverged certification or a
+// diverged box).
+__device__ __forceinline__ int dt_tube_d(const NetView& net, int n, int m, int H, int window, int rebuild, Work& W, int tid,
+                                bool& failed) {
+  const DevNet& N = net.N;
+  failed = false;
+  const int cap = window > 0 ? window : 1;
   auto init_state = [&](const D* lo, const D* hi) {
     for (int e = tid; e < n * n; e += kThreads) {
       const int i = e / n, q = e % n;
@@ -475,11 +451,6 @@ __global__ void __launch_bounds__(kThreads) plan_grad_kernel(const GradArgs G) {
     }
   };
   if (tid == 0) {
-    for (int i = 0; i < n; ++i) {
-      const D c0 = dc(P.x0[i]), r0 = dc(G.eps);
-      W.tlo[0][i] = dsub(c0, r0);
-      W.thi[0][i] = dadd(c0, r0);
-    }
     W.nq = 0;
     W.stop = 0;
   }
@@ -489,22 +460,28 @@ __global__ void __launch_bounds__(kThreads) plan_grad_kernel(const GradArgs G) {
   for (int k = 0; k < H; ++k) {
     // freeze_trailing_inputs (neural.hpp:398-413)
     for (int u = tid; u < N.dims[1]; u += kThreads) {
-      D bb = dc(net.b(0, u));
-      for (int q = 0; q < m; ++q) bb = dadd(bb, dmul(dc(net.w(0, u, n + q)), W.acts[k][q]));
+      D bb = net.b(0, u);
+      for (int q = 0; q < m; ++q) bb = dadd(bb, dmul(net.w(0, u, n + q), W.acts[k][q]));
       W.bf0[u] = bb;
     }
     __syncthreads();
     const int nq = W.nq;
     int nz = n;
     for (int q = 0; q < nq; ++q) nz += W.wid[q];
-    if (certify_d(net, n, nz, W, tid)) break;  // relax_activation throws: tube failed at k
+    if (certify_d(net, n, nz, W, tid)) {  // relax_activation throws: tube failed at k
+      failed = true;
+      break;
+    }
     if (tid == 0) {
       bool rfin = true;
       for (int i = 0; i < n; ++i) rfin = rfin && dfin(W.orem[i].lo) && dfin(W.orem[i].hi);
       W.stop = rfin ? 0 : 1;
     }
     __syncthreads();
-    if (W.stop) break;  // diverged certification
+    if (W.stop) {  // diverged certification
+      failed = true;
+      break;
+    }
     // re-seed (dt_reach.hpp:69-92)
     for (int e = tid; e < n * (nz + n); e += kThreads) {
       const int i = e / (nz + n), q = e % (nz + n);
@@ -535,16 +512,86 @@ __global__ void __launch_bounds__(kThreads) plan_grad_kernel(const GradArgs G) {
       bool fin = true;
       for (int i = 0; i < n; ++i) fin = fin && dfin(W.tlo[k + 1][i]) && dfin(W.thi[k + 1][i]);
       W.stop = fin ? 0 : 1;
-      if (fin && G.rebuild) W.nq = 0;
+      if (fin && rebuild) W.nq = 0;
     }
     __syncthreads();
     nb = k + 2;
-    if (W.stop) break;  // diverged box (pushed)
-    if (G.rebuild) {
+    if (W.stop) {  // diverged box (pushed)
+      failed = true;
+      break;
+    }
+    if (rebuild) {
       init_state(W.tlo[k + 1], W.thi[k + 1]);
       __syncthreads();
     }
   }
+  return nb;
+}
+
+// plan_objective (mpc.hpp:158-208) in Dual, seeded on action component
+// j = blockIdx.x; one CTA per direction, the working set in shared memory.
+__global__ void __launch_bounds__(kThreads, 2) plan_grad_kernel(const GradArgs G) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Work& W = *reinterpret_cast<Work*>(smem_raw);
+  const int j = blockIdx.x, tid = threadIdx.x;
+  const PlanParams& P = G.P;
+  const int H = P.H, n = P.n, m = P.m;
+  const NetView net{P.net};
+  const DevNet& N = P.net;
+  const int L = N.L;
+  for (int e = tid; e < H * m; e += kThreads) W.acts[e / m][e % m] = D{G.base[e], e == j ? 1.0 : 0.0};
+  if (tid == 0) {
+    W.obj = dc(0.0);
+    W.sub = 0;
+  }
+  for (int i = tid; i < n; i += kThreads) W.hb[0][i].lo = dc(P.x0[i]);
+  __syncthreads();
+  // nominal rollout + stage costs (mpc.hpp:170-184), MLPNet::forward (neural.hpp:58-76)
+  int cur = 0;
+  for (int t = 0; t < H; ++t) {
+    for (int i = tid; i < m; i += kThreads) W.hb[cur][n + i].lo = W.acts[t][i];
+    __syncthreads();
+    for (int l = 0; l < L; ++l) {
+      const int rows = N.dims[l + 1], cols = N.dims[l];
+      for (int u = tid; u < rows; u += kThreads) {
+        D acc = dc(0.0);
+        if (l + 1 < L)
+          for (int q = 0; q < cols; ++q) acc = dadd(acc, dmul(net.wt(l, u, q), W.hb[cur][q].lo));
+        else
+          for (int q = 0; q < cols; ++q) acc = dadd(acc, dmul(net.w(l, u, q), W.hb[cur][q].lo));
+        D h = dadd(acc, net.b(l, u));
+        if (N.acts[l] == REACH_ACT_RELU) {
+          if (h.v < 0.0) h = dc(0.0);
+        } else if (N.acts[l] == REACH_ACT_TANH) {
+          h = dtanh(h);
+        }
+        W.hb[cur ^ 1][u].lo = h;
+      }
+      cur ^= 1;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      D obj = W.obj;
+      for (int i = 0; i < m; ++i) obj = dadd(obj, dmul(dmul(dc(P.r_w[i]), W.acts[t][i]), W.acts[t][i]));
+      for (int i = 0; i < n; ++i) {
+        const D dd = dsub(W.hb[cur][i].lo, dc(P.x_goal[i]));
+        obj = dadd(obj, dmul(dmul(dc(P.q_w[i]), dd), dd));
+      }
+      W.obj = obj;
+    }
+    // x_{t+1} stays in hb[cur][0..n); the next step appends its action behind it
+  }
+  __syncthreads();
+  // dt_reach (dt_reach.hpp:41-104) at radius eps around x0 (box_from_center, interval.hpp:224-235)
+  if (tid == 0)
+    for (int i = 0; i < n; ++i) {
+      const D c0 = dc(P.x0[i]), r0 = dc(G.eps);
+      W.tlo[0][i] = dsub(c0, r0);
+      W.thi[0][i] = dadd(c0, r0);
+    }
+  __syncthreads();
+  bool failed = false;
+  const int nb = dt_tube_d(net, n, m, H, G.window, G.rebuild, W, tid, failed);
   // constraint penalties over the tube (mpc.hpp:187-200)
   if (tid == 0) {
     D obj = W.obj;
@@ -562,6 +609,110 @@ __global__ void __launch_bounds__(kThreads) plan_grad_kernel(const GradArgs G) {
     }
     G.grad[j] = obj.d;
     G.value[j] = obj.v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// grad_tube_volume (refine.hpp:263-311): d tube_volume(dt_reach(...)) / d p for
+// p = the X0 centre (radii fixed), the flat action sequence, or the network
+// parameters in net_params order (neural.hpp:133-140).  One CTA per pass:
+//   forward_dual (grad_forward, refine.hpp:186-207): CTA j seeds p_j;
+//   finite_difference (grad_fd, refine.hpp:209-231): CTAs 2j / 2j+1 evaluate
+//   p_j +/- h, h = rel_step * max(1, |p_j|); the last CTA is the unperturbed pass
+//   (f0 and the branch-boundary flag, as in the reference).
+enum : int { TARGET_X0_CENTER = 0, TARGET_ACTIONS = 1, TARGET_WEIGHTS = 2 };
+
+struct VolArgs {
+  DevNet net;
+  int n, m, H, window, rebuild;
+  const double* center;   // [n]  box_center(x0)
+  const double* radius;   // [n]  box_radius(x0)
+  const double* actions;  // [H*m]
+  int target, dim, fd;
+  double rel_step;
+  long long poff[kMaxLayers + 1];  // net_params offset of each layer's W (then its b)
+  double* value;          // [passes] tube volume (primal) seen by each pass
+  double* tangent;        // [passes]
+  int* sub;               // [1] any pass noted a branch boundary (forward) / the f0 pass did (fd)
+};
+
+__global__ void __launch_bounds__(kThreads, 2) tube_volume_grad_kernel(const VolArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Work& W = *reinterpret_cast<Work*>(smem_raw);
+  const int tid = threadIdx.x, pass = blockIdx.x;
+  const int n = A.n, m = A.m, H = A.H;
+  // which parameter this pass moves, by how much, with which tangent
+  int p = -1;
+  double delta = 0.0, seed = 0.0;
+  if (!A.fd) {
+    p = pass;
+    seed = 1.0;
+  } else if (pass < 2 * A.dim) {
+    p = pass >> 1;
+  }
+  NetView net{A.net};
+  double x = 0.0;
+  if (p >= 0) {
+    if (A.target == TARGET_X0_CENTER) {
+      x = A.center[p];
+    } else if (A.target == TARGET_ACTIONS) {
+      x = A.actions[p];
+    } else {
+      int l = 0;
+      while (l + 1 <= A.net.L && A.poff[l + 1] <= p) ++l;
+      const long long q = p - A.poff[l];
+      const int rows = A.net.dims[l + 1], cols = A.net.dims[l];
+      net.sl = l;
+      if (q < static_cast<long long>(rows) * cols) {
+        net.si = static_cast<int>(q / cols);
+        net.sj = static_cast<int>(q % cols);
+        x = A.net.blob[A.net.w_off[l] + static_cast<long long>(net.si) * A.net.ldw[l] + net.sj];
+      } else {
+        net.si = static_cast<int>(q - static_cast<long long>(rows) * cols);
+        net.sj = -1;
+        x = A.net.blob[A.net.b_off[l] + net.si];
+      }
+    }
+    if (A.fd) {
+      const double h = mul(A.rel_step, fmax(1.0, fabs(x)));
+      delta = (pass & 1) ? -h : h;
+    }
+    net.delta = delta;
+    net.seed = seed;
+  }
+  auto param = [&](double v, int target, int idx) -> D {
+    if (A.target != target || idx != p) return dc(v);
+    return D{delta != 0.0 ? add(v, delta) : v, seed};
+  };
+  for (int e = tid; e < H * m; e += kThreads) W.acts[e / m][e % m] = param(A.actions[e], TARGET_ACTIONS, e);
+  if (tid == 0) {
+    W.sub = 0;
+    for (int i = 0; i < n; ++i) {  // box_from_center(c, radius) (interval.hpp:224-235)
+      const D c = param(A.center[i], TARGET_X0_CENTER, i), r = dc(A.radius[i]);
+      W.tlo[0][i] = dsub(c, r);
+      W.thi[0][i] = dadd(c, r);
+    }
+  }
+  __syncthreads();
+  bool failed = false;
+  const int nb = dt_tube_d(net, n, m, H, A.window, A.rebuild, W, tid, failed);
+  if (tid == 0) {
+    // tube_volume (tube.hpp:40-46): +inf once diverged; else the sum of box width sums
+    D acc = dc(0.0);
+    bool fin = !failed;
+    for (int k = 0; fin && k < nb; ++k) {
+      D v = dc(0.0);
+      for (int i = 0; i < n; ++i) {
+        fin = fin && dfin(W.tlo[k][i]) && dfin(W.thi[k][i]);
+        v = dadd(v, dsub(W.thi[k][i], W.tlo[k][i]));
+      }
+      acc = dadd(acc, v);
+    }
+    if (!fin) acc = dc(__longlong_as_double(0x7ff0000000000000ll));
+    A.value[pass] = acc.v;
+    A.tangent[pass] = acc.d;
+    const bool counts = !A.fd || pass == 2 * A.dim;
+    if (counts && W.sub) atomicOr(A.sub, 1);
   }
 }
 

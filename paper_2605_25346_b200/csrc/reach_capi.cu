@@ -490,6 +490,11 @@ int reach_net_upload(reach_ctx* ctx, const reach_net_desc* d, reach_net** out) {
   net->L = d->n_layers;
   net->dims.assign(d->dims, d->dims + d->n_layers + 1);
   net->acts.assign(d->acts, d->acts + d->n_layers);
+  {
+    size_t np = 0;
+    for (int l = 0; l < d->n_layers; ++l) np += static_cast<size_t>(d->dims[l + 1]) * (d->dims[l] + 1);
+    net->params.assign(d->params, d->params + np);
+  }
   // host blob, laid out for the kernels: per layer W (rows x ldw) and W^T
   // (cols x ldt), zero-padded so that hidden layers span the padded width
   // hp = 32 * cpl (no per-column guards in the kernels), biases padded to 32.
@@ -1410,6 +1415,130 @@ int reach_plan_objective_grad(reach_ctx* ctx, const reach_net* net, const reach_
   if (rc) return rc;
   if (objective) *objective = v;
   if (!fin) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_forward: non-finite derivative");
+  return REACH_OK;
+}
+
+int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
+                           int32_t method, double* grad, int32_t* subgradient, double* volume) {
+  namespace rd = rb::dual;
+  if (!ctx || !net || !a || !grad) return REACH_E_INVALID_ARGUMENT;
+  if (a->batch != 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: batch must be 1");
+  if (a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach: negative horizon");
+  if (target < REACH_GRAD_X0_CENTER || target > REACH_GRAD_WEIGHTS || method < REACH_GRAD_FORWARD_DUAL ||
+      method > REACH_GRAD_FINITE_DIFFERENCE)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: unknown target / method");
+  int rc = validate_system(ctx, net, a->n, a->m);
+  if (rc) return rc;
+  const int n = a->n, m = a->m, H = a->horizon;
+  if (!a->x0_lo || !a->x0_hi || (H * m > 0 && !a->actions))
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: missing input");
+  int maxw = 0;
+  for (int l = 0; l <= net->L; ++l) maxw = std::max(maxw, net->dims[l]);
+  const int cap = a->window > 0 ? a->window : 1;
+  if (n > rd::kN || m > rd::kM || maxw > rd::kW || net->L > rd::kL || H > rd::kH || n * (cap + 2) > rd::kZ ||
+      n * (cap + 2) + n > rd::kW || cap + 2 > rd::kQ)
+    return fail(ctx, REACH_E_UNSUPPORTED, "grad_tube_volume: shape outside the Dual kernel family");
+  // box_center / box_radius (interval.hpp:270-281), box_from_center's radius check (interval.hpp:229)
+  std::vector<double> center(n), radius(n);
+  for (int i = 0; i < n; ++i) {
+    center[i] = (a->x0_lo[i] + a->x0_hi[i]) * 0.5;
+    radius[i] = (a->x0_hi[i] - a->x0_lo[i]) * 0.5;
+    if (radius[i] < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "box_from_center: negative radius");
+  }
+  rd::VolArgs V{};
+  V.poff[0] = 0;
+  for (int l = 0; l < net->L; ++l)
+    V.poff[l + 1] = V.poff[l] + static_cast<long long>(net->dims[l + 1]) * net->dims[l] + net->dims[l + 1];
+  const long long dim = target == REACH_GRAD_X0_CENTER ? n
+                        : target == REACH_GRAD_ACTIONS ? static_cast<long long>(H) * m
+                                                       : V.poff[net->L];
+  const bool fd = method == REACH_GRAD_FINITE_DIFFERENCE;
+  const long long passes = fd ? 2 * dim + 1 : dim;
+  if (passes > (1ll << 30)) return fail(ctx, REACH_E_UNSUPPORTED, "grad_tube_volume: too many parameters");
+  if (subgradient) *subgradient = 0;
+  if (passes == 0) {  // nothing to differentiate: grad_forward still evaluates f0
+    if (volume) *volume = 0.0;
+  }
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const long long np = std::max<long long>(passes, 1);
+  const size_t o_c = take(n * 8), o_r = take(n * 8), o_a = take(static_cast<size_t>(H) * m * 8),
+               o_v = take(static_cast<size_t>(np) * 8), o_t = take(static_cast<size_t>(np) * 8), o_s = take(4);
+  rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  RB_CUDA(cudaMemcpyAsync(Dp(o_c), center.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_r), radius.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (H * m > 0)
+    RB_CUDA(cudaMemcpyAsync(Dp(o_a), a->actions, static_cast<size_t>(H) * m * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemsetAsync(w + o_s, 0, 4, ctx->stream));
+  V.net = net->dev;
+  V.n = n;
+  V.m = m;
+  V.H = H;
+  V.window = a->window;
+  V.rebuild = a->rebuild_from_box;
+  V.center = Dp(o_c);
+  V.radius = Dp(o_r);
+  V.actions = Dp(o_a);
+  V.target = target;
+  V.dim = static_cast<int>(dim);
+  V.fd = fd ? 1 : 0;
+  V.rel_step = 1e-5;
+  V.value = Dp(o_v);
+  V.tangent = Dp(o_t);
+  V.sub = reinterpret_cast<int*>(w + o_s);
+  // grad_forward with no parameters still runs its primal pass: launch one unseeded pass
+  const long long launch = passes > 0 ? passes : 1;
+  if (passes == 0) V.fd = 1;  // dim 0: pass 0 == 2 * dim is the unperturbed pass
+  RB_CUDA(cudaFuncSetAttribute(rd::tube_volume_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sizeof(rd::Work))));
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  rd::tube_volume_grad_kernel<<<static_cast<unsigned>(launch), rd::kThreads, sizeof(rd::Work), ctx->stream>>>(V);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  std::vector<double> val(launch), tan(launch);
+  int32_t sub = 0;
+  RB_CUDA(cudaMemcpyAsync(val.data(), Dp(o_v), launch * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(tan.data(), Dp(o_t), launch * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(&sub, w + o_s, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double f0 = (fd || passes == 0) ? val[launch - 1] : val[0];  // primal values are identical across passes
+  if (volume) *volume = f0;
+  if (!std::isfinite(f0))
+    return fail(ctx, REACH_E_INVALID_ARGUMENT,
+                fd ? "grad_fd: objective non-finite" : "grad_forward: objective non-finite");
+  for (long long j = 0; j < dim; ++j) {
+    if (!fd) {
+      if (!std::isfinite(val[j]) || !std::isfinite(tan[j]))
+        return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_forward: non-finite derivative");
+      grad[j] = tan[j];
+    } else {
+      const double fp = val[2 * j], fm = val[2 * j + 1];
+      if (!std::isfinite(fp) || !std::isfinite(fm))
+        return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_fd: objective non-finite near x");
+      double xj;  // the parameter value, for h (refine.hpp:222)
+      if (target == REACH_GRAD_X0_CENTER) {
+        xj = center[j];
+      } else if (target == REACH_GRAD_ACTIONS) {
+        xj = a->actions[j];
+      } else {
+        xj = net->params[static_cast<size_t>(j)];  // net_params order == the upload's flat order
+      }
+      const double h = 1e-5 * std::max(1.0, std::abs(xj));
+      grad[j] = (fp - fm) / (2.0 * h);
+    }
+  }
+  if (subgradient) *subgradient = sub ? 1 : 0;
   return REACH_OK;
 }
 

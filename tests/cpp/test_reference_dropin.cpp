@@ -238,6 +238,27 @@ int main() {
       ++failures;
     }
   }
+  // grad_tube_volume on the reference's own gradient-test shapes (test_refine.cpp:253-284): all three
+  // targets, both methods, ReLU map -> bit-identical gradients and subgradient flags
+  {
+    Rng r3(9090);
+    DTSystem<double> sys;
+    sys.n = 3;
+    sys.m = 2;
+    sys.step = random_mlp(r3, 5, {16, 16}, 3, Act::Relu, 0.6);
+    Box x0 = box_from_center<double>({0.1, 0.0, -0.2}, 0.05);
+    std::vector<Vec<double>> actions;
+    for (int k = 0; k < 5; ++k) actions.push_back({r3.uniform(-0.3, 0.3), r3.uniform(-0.3, 0.3)});
+    for (auto t : {GradTarget::x0_center, GradTarget::actions, GradTarget::weights})
+      for (auto me : {GradMethod::forward_dual, GradMethod::finite_difference}) {
+        auto ref = reach::grad_tube_volume(sys, x0, actions, t, me);
+        auto got = reach_b200::grad_tube_volume(gpu, sys, x0, actions, t, me);
+        if (ref.g != got.g || ref.subgradient != got.subgradient) {
+          std::printf("grad_tube_volume(target %d, method %d): mismatch\n", int(t), int(me));
+          ++failures;
+        }
+      }
+  }
   std::printf(failures ? "FAIL (%d)\n" : "OK: reference drop-in parity\n", failures);
   return failures ? 1 : 0;
 }

@@ -384,3 +384,21 @@ def ref_plan_cem_ex(prob, cfg, x0):
            A.iptr(rf))
     assert rc == 0, rc
     return best, float(obj[0]), hist, bool(be[0]), bool(rf[0])
+
+
+def ref_grad_tube_volume(sys, x0, actions, target, method=0, prm=DTReachParams()):
+    """The reference's grad_tube_volume -> (g, subgradient), or None where it throws."""
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    f = _mpc_fn(ref_lib(), "ref_grad_tube_volume", [C.POINTER(A.NetDesc), C.POINTER(A.DTArgs), C.c_int32, C.c_int32,
+                                                   dp, ip])
+    lo = np.ascontiguousarray(x0[0], np.float64)
+    hi = np.ascontiguousarray(x0[1], np.float64)
+    H = len(actions)
+    acts = np.ascontiguousarray(np.asarray(actions, np.float64).reshape(H * sys.m)) if H * sys.m else np.zeros(1)
+    dim = {0: sys.n, 1: H * sys.m, 2: sys.step.params().size}[int(target)]
+    g = np.zeros(max(dim, 1))
+    sub = np.zeros(1, np.int32)
+    desc, keep = sys.step.desc()
+    args = A.DTArgs(1, H, sys.n, sys.m, prm.window, int(prm.rebuild_from_box), A.dptr(lo), A.dptr(hi), A.dptr(acts), 0)
+    rc = f(C.byref(desc), C.byref(args), int(target), int(method), A.dptr(g), A.iptr(sub))
+    return None if rc else (g[:dim], bool(sub[0]))

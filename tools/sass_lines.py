@@ -37,7 +37,7 @@ def main():
             break
     # find function section by mangled-name match
     lines = dis.splitlines()
-    cur_fn, cur_line, in_fn = None, None, False
+    cur_fn, cur_line, in_fn, prev_marker = None, None, False, False
     addr_line = {}
     for ln in lines:
         m = re.match(r"\s*\.text\.(\S+):", ln)
@@ -46,10 +46,14 @@ def main():
             continue
         if not in_fn:
             continue
-        m = re.search(r"//## File \"(.*?)\", line (\d+)$", ln.strip()) or re.search(r"inlined at \"(.*?)\", line (\d+)", ln)
+        # an inline chain is a run of markers, innermost first: keep the first of each run
+        m = re.search(r"//## File \"(.*?)\", line (\d+)", ln)
         if m:
-            cur_line = (os.path.basename(m.group(1)), int(m.group(2)))
+            if not prev_marker:
+                cur_line = (os.path.basename(m.group(1)), int(m.group(2)))
+            prev_marker = True
             continue
+        prev_marker = False
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if m and cur_line:
             addr_line[int(m.group(1), 16)] = cur_line
