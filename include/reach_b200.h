@@ -273,6 +273,37 @@ enum reach_grad_method { REACH_GRAD_FORWARD_DUAL = 0, REACH_GRAD_FINITE_DIFFEREN
 int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
                            int32_t method, double* grad, int32_t* subgradient, double* volume);
 
+/* mpc_run (mpc.hpp:373-495): receding-horizon execution.  MPCConfig (mpc.hpp:373-387). */
+typedef struct reach_mpc_config {
+  int32_t replan_period;  /* actions executed per plan */
+  int32_t total_steps;
+  double dist_action;     /* uniform noise bound on executed actions */
+  double dist_state;      /* uniform noise bound on the next state */
+  int32_t n_goal_dims;    /* 0 = all */
+  const int32_t* goal_dims;
+  double goal_radius;
+  uint64_t seed;
+} reach_mpc_config;
+/* The true simulator x_next = sim(x, u); return 0 on success. */
+typedef int (*reach_sim_fn)(void* user, const double* x, const double* u, double* x_next);
+/* MPCResult::log (mpc.hpp:389-396), row-major, capacity total_steps rows; any pointer may be NULL. */
+typedef struct reach_mpc_log {
+  int32_t* step;
+  double* state;        /* [rows][n] */
+  double* action;       /* [rows][m] */
+  double* objective;
+  double* tube_volume;
+  double* g_margin;
+} reach_mpc_log;
+/* Plans with reach_plan_cem_ex (seed = sampler.seed ^ (0x9e3779b97f4a7c15 * (step + 1))), executes
+ * replan_period actions through `sim` (NULL: the uploaded one-step model's forward on the device, as the
+ * reference CLI does) with the reference's disturbance stream, replans.  Outputs MPCResult's success,
+ * violated, steps_used, final_state [n] and the log (log_rows rows). */
+int reach_mpc_run(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
+                  const reach_sampler_config* sampler, const reach_mpc_config* cfg, reach_sim_fn sim, void* sim_user,
+                  const double* x0, int32_t* success, int32_t* violated, int32_t* steps_used, double* final_state,
+                  const reach_mpc_log* log, int32_t* log_rows);
+
 /* The CEM loop in pieces, for multi-GPU drivers that shard each population
  * and all-gather the scores between sample() and update(). */
 typedef struct reach_cem reach_cem;

@@ -21,6 +21,7 @@
 //   Constraint / PlanProblem / SamplerConfig /  reach_b200::Constraint / PlanProblem / SamplerConfig /
 //   PlanResult / plan_objective / plan_cem      PlanResult / plan_objective(_batch) / plan_cem
 //   grad_forward(plan_objective) (refine.hpp)   reach_b200::plan_objective_grad
+//   MPCConfig / MPCResult / mpc_run (mpc.hpp)   reach_b200::MPCConfig / MPCResult / mpc_run
 //   GradTarget / GradMethod / Gradient /        reach_b200::GradTarget / GradMethod / Gradient /
 //   grad_tube_volume (refine.hpp:165-311)       grad_tube_volume
 //
@@ -29,6 +30,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <limits>
 #include <memory>
 #include <stdexcept>
@@ -662,6 +664,87 @@ inline PlanResult plan_cem(Context& ctx, const PlanProblem& pr, const SamplerCon
   r.tube.failed_step = fs;
   r.tube.diverged = st != REACH_TUBE_OK;
   r.tube.failure_reason = st != REACH_TUBE_OK ? failure_reason(st) : "";
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Receding-horizon MPC (mpc.hpp:373-495).
+
+struct MPCConfig {  // mpc.hpp:373-387
+  int replan_period = 3;
+  int total_steps = 30;
+  double dist_action = 0.0;
+  double dist_state = 0.0;
+  std::vector<int> goal_dims;
+  double goal_radius = 0.1;
+  uint64_t seed = 0;
+};
+
+struct MPCLogRow {  // mpc.hpp:389-396
+  int step = 0;
+  std::vector<double> state, action;
+  double objective = 0.0, tube_volume = 0.0, g_margin = 0.0;
+};
+
+struct MPCResult {  // mpc.hpp:398-419
+  bool success = false, violated = false;
+  int steps_used = 0;
+  std::vector<double> final_state;
+  std::vector<MPCLogRow> log;
+};
+
+using SimStep = std::function<std::vector<double>(const std::vector<double>&, const std::vector<double>&)>;
+
+// mpc_run: planning, margins and (sim empty) the model simulator on the device;
+// a non-empty `sim` is the caller's true system, called on the host.
+inline MPCResult mpc_run(Context& ctx, const PlanProblem& pr, const SamplerConfig& sampler, const MPCConfig& cfg,
+                         const SimStep& sim, const std::vector<double>& x0) {
+  detail::PlanC pc(pr);
+  const int n = pr.sys.n, m = pr.sys.m, T = cfg.total_steps > 0 ? cfg.total_steps : 1;
+  if (static_cast<int>(x0.size()) != n) throw std::invalid_argument("mpc_run: x0 dimension mismatch");
+  reach_sampler_config sc{sampler.population, sampler.elite_frac, sampler.iterations, sampler.init_std,
+                          sampler.smoothing, sampler.refine_iters, sampler.seed};
+  std::vector<int32_t> gd(cfg.goal_dims.begin(), cfg.goal_dims.end());
+  reach_mpc_config mc{cfg.replan_period, cfg.total_steps, cfg.dist_action, cfg.dist_state,
+                      static_cast<int32_t>(gd.size()), gd.empty() ? nullptr : gd.data(), cfg.goal_radius, cfg.seed};
+  std::vector<int32_t> st(T);
+  std::vector<double> xs(static_cast<size_t>(T) * n), us(static_cast<size_t>(T) * (m > 0 ? m : 1)), ob(T), tv(T),
+      gm(T);
+  reach_mpc_log lg{st.data(), xs.data(), us.data(), ob.data(), tv.data(), gm.data()};
+  struct Tramp {
+    const SimStep* f;
+    int n, m;
+    static int call(void* user, const double* x, const double* u, double* xn) {
+      auto* t = static_cast<Tramp*>(user);
+      try {
+        std::vector<double> out = (*t->f)(std::vector<double>(x, x + t->n), std::vector<double>(u, u + t->m));
+        if (static_cast<int>(out.size()) != t->n) return 1;
+        std::copy(out.begin(), out.end(), xn);
+        return 0;
+      } catch (...) {
+        return 1;
+      }
+    }
+  } tr{&sim, n, m};
+  MPCResult r;
+  r.final_state.assign(n, 0.0);
+  int32_t succ = 0, viol = 0, used = 0, rows = 0;
+  ctx.check(reach_mpc_run(ctx.raw(), ctx.upload(pr.sys.step), &pc.p, &sc, &mc, sim ? &Tramp::call : nullptr, &tr,
+                          x0.data(), &succ, &viol, &used, r.final_state.data(), &lg, &rows),
+            "mpc_run");
+  r.success = succ != 0;
+  r.violated = viol != 0;
+  r.steps_used = used;
+  for (int i = 0; i < rows; ++i) {
+    MPCLogRow row;
+    row.step = st[i];
+    row.state.assign(xs.begin() + static_cast<size_t>(i) * n, xs.begin() + static_cast<size_t>(i + 1) * n);
+    if (m > 0) row.action.assign(us.begin() + static_cast<size_t>(i) * m, us.begin() + static_cast<size_t>(i + 1) * m);
+    row.objective = ob[i];
+    row.tube_volume = tv[i];
+    row.g_margin = gm[i];
+    r.log.push_back(std::move(row));
+  }
   return r;
 }
 

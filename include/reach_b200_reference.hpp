@@ -224,4 +224,37 @@ inline reach::Gradient grad_tube_volume(Context& ctx, const reach::DTSystem<doub
   return out;
 }
 
+// reach::mpc_run (mpc.hpp:425-495) -> reach::MPCResult.  sim_step is the
+// reference's Sim argument (called on the host); planning runs on the device.
+template <class Sim>
+inline reach::MPCResult mpc_run(Context& ctx, const reach::PlanProblem& prob, const reach::SamplerConfig& sampler,
+                                const reach::MPCConfig& cfg, Sim&& sim_step, const reach::Vec<double>& x0) {
+  prob.validate();
+  cfg.validate(prob.horizon);
+  SamplerConfig s{sampler.population, sampler.elite_frac, sampler.iterations, sampler.init_std, sampler.smoothing,
+                  sampler.refine_iters, sampler.seed};
+  MPCConfig c{cfg.replan_period, cfg.total_steps, cfg.dist_action, cfg.dist_state, cfg.goal_dims, cfg.goal_radius,
+              cfg.seed};
+  SimStep f = [&](const std::vector<double>& x, const std::vector<double>& u) {
+    return std::vector<double>(sim_step(reach::Vec<double>(x), reach::Vec<double>(u)));
+  };
+  MPCResult r = mpc_run(ctx, from_reference(prob), s, c, f, x0);
+  reach::MPCResult out;
+  out.success = r.success;
+  out.violated = r.violated;
+  out.steps_used = r.steps_used;
+  out.final_state = r.final_state;
+  for (const auto& row : r.log) {
+    reach::MPCLogRow q;
+    q.step = row.step;
+    q.state = row.state;
+    q.action = row.action;
+    q.objective = row.objective;
+    q.tube_volume = row.tube_volume;
+    q.g_margin = row.g_margin;
+    out.log.push_back(std::move(q));
+  }
+  return out;
+}
+
 }  // namespace reach_b200

@@ -799,3 +799,45 @@ int ref_ct_split_hull(const reach_field_desc* fd, const reach_flowpipe_params* f
   return REACH_OK;
 }
 }  // extern "C"
+
+// reach::mpc_run (mpc.hpp:425-495) with the CLI's simulator (the model's own forward,
+// reach_cli.cpp:445-449) and the CSV log (MPCResult::log_to_csv) written to csv[csv_cap].
+extern "C" int ref_mpc_run(const reach_net_desc* desc, const reach_plan_problem* p, const reach_sampler_config* c,
+                           const reach_mpc_config* mc, const double* x0, int32_t* success, int32_t* violated,
+                           int32_t* steps_used, double* final_state, char* csv, int32_t csv_cap) {
+  try {
+    PlanProblem prob = problem_from(desc, p);
+    SamplerConfig cfg;
+    cfg.population = c->population;
+    cfg.elite_frac = c->elite_frac;
+    cfg.iterations = c->iterations;
+    cfg.init_std = c->init_std;
+    cfg.smoothing = c->smoothing;
+    cfg.refine_iters = c->refine_iters;
+    cfg.seed = c->seed;
+    MPCConfig m;
+    m.replan_period = mc->replan_period;
+    m.total_steps = mc->total_steps;
+    m.dist_action = mc->dist_action;
+    m.dist_state = mc->dist_state;
+    m.goal_dims.assign(mc->goal_dims, mc->goal_dims + mc->n_goal_dims);
+    m.goal_radius = mc->goal_radius;
+    m.seed = mc->seed;
+    auto sim = [&](const Vec<double>& x, const Vec<double>& u) {
+      Vec<double> in = x;
+      in.insert(in.end(), u.begin(), u.end());
+      return prob.sys.step.forward(in);
+    };
+    auto res = mpc_run(prob, cfg, m, sim, Vec<double>(x0, x0 + p->n));
+    *success = res.success ? 1 : 0;
+    *violated = res.violated ? 1 : 0;
+    *steps_used = res.steps_used;
+    std::copy(res.final_state.begin(), res.final_state.end(), final_state);
+    const std::string s = res.log_to_csv();
+    if (static_cast<int32_t>(s.size()) + 1 > csv_cap) return REACH_E_INVALID_ARGUMENT;
+    std::memcpy(csv, s.c_str(), s.size() + 1);
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}

@@ -144,6 +144,22 @@ class SamplerConfigC(C.Structure):
     ]
 
 
+class MPCConfigC(C.Structure):
+    _fields_ = [
+        ("replan_period", C.c_int32), ("total_steps", C.c_int32), ("dist_action", C.c_double),
+        ("dist_state", C.c_double), ("n_goal_dims", C.c_int32), ("goal_dims", _ip), ("goal_radius", C.c_double),
+        ("seed", C.c_uint64),
+    ]
+
+
+class MPCLogC(C.Structure):
+    _fields_ = [("step", _ip), ("state", _dp), ("action", _dp), ("objective", _dp), ("tube_volume", _dp),
+                ("g_margin", _dp)]
+
+
+SIM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, _dp, _dp, _dp)
+
+
 # --- continuous-time closed loop (closed_loop.hpp) -----------------------------
 PLANT_QUADROTOR = 0
 

@@ -173,4 +173,45 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_objective_kernel(const P
   P.diverged[b] = P.status[b] != ST_OK ? 1 : 0;
 }
 
+// plan_step_margin (mpc.hpp:211-215) of K boxes: min over the constraints of
+// Constraint::margin, folded with std::min's (b < a ? b : a) from +inf.
+__global__ void box_margin_kernel(const PlanParams P, const double* lo, const double* hi, int K, double* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double worst = __longlong_as_double(0x7ff0000000000000ll);
+  for (int c = 0; c < P.n_con; ++c) {
+    const double g = con_margin(P, P.con[c], lo + static_cast<size_t>(k) * P.n, hi + static_cast<size_t>(k) * P.n);
+    worst = (g < worst) ? g : worst;
+  }
+  out[k] = worst;
+}
+
+// MLPNet::forward (neural.hpp:58-76) of one input [x; u] -> x_next: the model
+// as the simulator of mpc_run (the CLI's sim, reach_cli.cpp:445-449).  One
+// CTA; thread o owns output o of each layer, dot product in matvec's order.
+__global__ void model_step_kernel(const DevNet N, const double* xu, double* out, int maxw) {
+  extern __shared__ __align__(16) double fwd[];
+  double* a = fwd;
+  double* o = fwd + maxw;
+  for (int j = threadIdx.x; j < N.dims[0]; j += blockDim.x) a[j] = xu[j];
+  __syncthreads();
+  for (int l = 0; l < N.L; ++l) {
+    const int rows = N.dims[l + 1], cols = N.dims[l];
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      const double* w = N.blob + N.w_off[l] + static_cast<size_t>(r) * N.ldw[l];
+      double acc = 0.0;
+      for (int j = 0; j < cols; ++j) acc = add(acc, mul(w[j], a[j]));
+      double v = add(acc, N.blob[N.b_off[l] + r]);
+      if (N.acts[l] == 0) v = (v < 0.0) ? 0.0 : v;
+      else if (N.acts[l] == 1) v = tanh(v);
+      o[r] = v;
+    }
+    __syncthreads();
+    double* t = a;
+    a = o;
+    o = t;
+  }
+  for (int j = threadIdx.x; j < N.dims[N.L]; j += blockDim.x) out[j] = a[j];
+}
+
 }  // namespace rb

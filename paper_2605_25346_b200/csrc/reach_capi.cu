@@ -1542,4 +1542,173 @@ int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_
   return REACH_OK;
 }
 
+// mpc_run (mpc.hpp:425-495): receding-horizon execution around plan_cem.
+// Planning, the simulator (the uploaded model's forward when sim == NULL, the
+// CLI's choice, reach_cli.cpp:445-449) and the constraint margins run on the
+// device; the loop, the disturbance stream (std::mt19937_64(cfg.seed), 53-bit
+// uniforms) and the log bookkeeping are the reference's host logic.
+int reach_mpc_run(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
+                  const reach_sampler_config* sampler, const reach_mpc_config* cfg, reach_sim_fn sim, void* sim_user,
+                  const double* x0, int32_t* success, int32_t* violated, int32_t* steps_used, double* final_state,
+                  const reach_mpc_log* log, int32_t* log_rows) {
+  if (!ctx || !net || !prob || !sampler || !cfg || !x0) return REACH_E_INVALID_ARGUMENT;
+  int rc = validate_problem(ctx, net, prob);
+  if (rc) return rc;
+  if (cfg->replan_period < 1 || cfg->replan_period > prob->horizon || cfg->total_steps < 1 ||
+      cfg->dist_action < 0.0 || cfg->dist_state < 0.0 || cfg->goal_radius <= 0.0)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "MPCConfig: invalid configuration");
+  const int n = prob->n, m = prob->m, H = prob->horizon;
+  for (int j = 0; j < cfg->n_goal_dims; ++j)
+    if (!cfg->goal_dims || cfg->goal_dims[j] < 0 || cfg->goal_dims[j] >= n)
+      return fail(ctx, REACH_E_INVALID_ARGUMENT, "MPCConfig: goal dim out of range");
+  if (!sim && (net->dims[0] != n + m || net->dims[net->L] != n))
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "mpc_run: the model simulator needs the one-step map");
+  // device buffers of this run (own allocation: plan_cem may grow the context workspace)
+  PlanBuffers pb;
+  pack_problem(prob, pb);
+  int maxw = 0;
+  for (int l = 0; l <= net->L; ++l) maxw = std::max(maxw, net->dims[l]);
+  const size_t nb_boxes = static_cast<size_t>(H) + 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t o_db = take(pb.db.size() * 8), o_ib = take(pb.ib.size() * 4), o_xu = take((n + m) * 8),
+               o_x = take(n * 8), o_lo = take(nb_boxes * n * 8), o_hi = take(nb_boxes * n * 8),
+               o_mg = take(nb_boxes * 8);
+  char* dev = nullptr;
+  RB_CUDA(cudaMalloc(&dev, off));
+  struct Free {
+    char* p;
+    ~Free() { cudaFree(p); }
+  } free_guard{dev};
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(dev + o); };
+  RB_CUDA(cudaMemcpyAsync(Dp(o_db), pb.db.data(), pb.db.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(dev + o_ib, pb.ib.data(), pb.ib.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  rb::PlanParams MP = pb.P;
+  MP.n = n;
+  MP.dbuf = Dp(o_db);
+  MP.ibuf = reinterpret_cast<const int*>(dev + o_ib);
+  // margins of K boxes on the device (plan_step_margin, mpc.hpp:211-215)
+  auto margins = [&](const double* lo, const double* hi, int K, double* out) -> int {
+    RB_CUDA(cudaMemcpyAsync(Dp(o_lo), lo, static_cast<size_t>(K) * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    RB_CUDA(cudaMemcpyAsync(Dp(o_hi), hi, static_cast<size_t>(K) * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    rb::box_margin_kernel<<<(K + 127) / 128, 128, 0, ctx->stream>>>(MP, Dp(o_lo), Dp(o_hi), K, Dp(o_mg));
+    RB_CUDA(cudaGetLastError());
+    ctx->launches += 1;
+    RB_CUDA(cudaMemcpyAsync(out, Dp(o_mg), static_cast<size_t>(K) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return REACH_OK;
+  };
+  auto state_ok = [&](const std::vector<double>& s, bool& ok) -> int {  // box_from_center(s, 0.0)
+    std::vector<double> lo(s), hi(s);
+    for (int d = 0; d < n; ++d) {
+      lo[d] = s[d] - 0.0;
+      hi[d] = s[d] + 0.0;
+    }
+    double g = 0.0;
+    int e = margins(lo.data(), hi.data(), 1, &g);
+    ok = g >= 0.0;
+    return e;
+  };
+  auto goal_reached = [&](const std::vector<double>& s) {
+    double d2 = 0.0;
+    const int k = cfg->n_goal_dims > 0 ? cfg->n_goal_dims : n;
+    for (int j = 0; j < k; ++j) {
+      const int d = cfg->n_goal_dims > 0 ? cfg->goal_dims[j] : j;
+      const double diff = s[d] - prob->x_goal[d];
+      d2 += diff * diff;
+    }
+    return std::sqrt(d2) <= cfg->goal_radius;
+  };
+  auto sim_step = [&](const std::vector<double>& x, const std::vector<double>& u, std::vector<double>& xn) -> int {
+    if (sim) {
+      if (sim(sim_user, x.data(), u.data(), xn.data()) != 0)
+        return fail(ctx, REACH_E_INVALID_ARGUMENT, "mpc_run: sim_step failed");
+      return REACH_OK;
+    }
+    std::vector<double> xu(x);
+    xu.insert(xu.end(), u.begin(), u.end());
+    RB_CUDA(cudaMemcpyAsync(Dp(o_xu), xu.data(), xu.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    rb::model_step_kernel<<<1, 256, 2 * maxw * sizeof(double), ctx->stream>>>(net->dev, Dp(o_xu), Dp(o_x), maxw);
+    RB_CUDA(cudaGetLastError());
+    ctx->launches += 1;
+    RB_CUDA(cudaMemcpyAsync(xn.data(), Dp(o_x), n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return REACH_OK;
+  };
+  std::mt19937_64 rng(cfg->seed);
+  auto uniform = [&](double lo, double hi) {  // Rng::uniform (rng.hpp:22)
+    return lo + (hi - lo) * (static_cast<double>(rng() >> 11) * 0x1.0p-53);
+  };
+  std::vector<double> x(x0, x0 + n), xn(n), u(m), best(static_cast<size_t>(H) * m), hist(sampler->iterations);
+  std::vector<double> tlo(nb_boxes * n), thi(nb_boxes * n);
+  int32_t tnb = 0, tfs = -1, tst = 0;
+  reach_tube_out tube{tlo.data(), thi.data(), &tnb, &tfs, &tst};
+  bool viol = false, ok = true;
+  int rows = 0;
+  auto finish = [&](int used, bool succ) {
+    if (success) *success = succ ? 1 : 0;
+    if (violated) *violated = viol ? 1 : 0;
+    if (steps_used) *steps_used = used;
+    if (final_state) std::copy(x.begin(), x.end(), final_state);
+    if (log_rows) *log_rows = rows;
+    return REACH_OK;
+  };
+  if ((rc = state_ok(x, ok))) return rc;
+  if (!ok) viol = true;
+  int step = 0;
+  reach_sampler_config plan_cfg = *sampler;
+  while (step < cfg->total_steps && !goal_reached(x)) {
+    plan_cfg.seed = sampler->seed ^ (0x9e3779b97f4a7c15ull * static_cast<uint64_t>(step + 1));
+    double pobj = 0.0;
+    int32_t be = 0, rf = 0;
+    rc = reach_plan_cem_ex(ctx, net, prob, &plan_cfg, x.data(), best.data(), &pobj, hist.data(), &be, &rf, &tube);
+    if (rc) return rc;
+    // tube_volume of the plan's tube (tube.hpp:40-46) and the per-step planned margins
+    double tvol = std::numeric_limits<double>::infinity();
+    if (tst == REACH_TUBE_OK) {
+      tvol = 0.0;
+      for (int k = 0; k < tnb; ++k) {
+        double v = 0.0;
+        for (int d = 0; d < n; ++d) v += thi[static_cast<size_t>(k) * n + d] - tlo[static_cast<size_t>(k) * n + d];
+        tvol += v;
+      }
+    }
+    std::vector<double> gm(std::max(tnb, 1));
+    if (tnb > 0 && (rc = margins(tlo.data(), thi.data(), tnb, gm.data()))) return rc;
+    for (int k = 0; k < cfg->replan_period && step < cfg->total_steps; ++k, ++step) {
+      for (int j = 0; j < m; ++j) {
+        double v = best[static_cast<size_t>(k) * m + j];
+        v += uniform(-cfg->dist_action, cfg->dist_action);
+        u[j] = std::clamp(v, prob->u_lo[j], prob->u_hi[j]);
+      }
+      if (log && rows < cfg->total_steps) {
+        if (log->step) log->step[rows] = step;
+        if (log->state) std::copy(x.begin(), x.end(), log->state + static_cast<size_t>(rows) * n);
+        if (log->action) std::copy(u.begin(), u.end(), log->action + static_cast<size_t>(rows) * m);
+        if (log->objective) log->objective[rows] = pobj;
+        if (log->tube_volume) log->tube_volume[rows] = tvol;
+        if (log->g_margin) log->g_margin[rows] = (k + 1 < tnb) ? gm[k + 1] : -std::numeric_limits<double>::infinity();
+      }
+      ++rows;
+      if ((rc = sim_step(x, u, xn))) return rc;
+      x = xn;
+      for (auto& v : x) {
+        if (!std::isfinite(v)) return finish(step + 1, false);  // simulator divergence: failure with log
+        v += uniform(-cfg->dist_state, cfg->dist_state);
+      }
+      if ((rc = state_ok(x, ok))) return rc;
+      if (!ok) viol = true;
+      if (goal_reached(x)) {
+        ++step;
+        break;
+      }
+    }
+  }
+  return finish(step, goal_reached(x) && !viol);
+}
+
 }  // extern "C"

@@ -6,7 +6,8 @@
     and the top candidate's gradient refinement (refine_iters > 0, the
     reference default; gradient_refine, refine.hpp:347-398) driven by
     forward-dual gradients computed on the device (plan_objective_grad,
-    grad_forward refine.hpp:186-207).
+    grad_forward refine.hpp:186-207); MPCConfig / mpc_run (373-495), the
+    receding-horizon loop around the device planner.
 """
 from __future__ import annotations
 
@@ -221,3 +222,98 @@ class CEM:
             self._lib.reach_cem_destroy(self.h)
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class MPCConfig:  # mpc.hpp:373-387
+    replan_period: int = 3
+    total_steps: int = 30
+    dist_action: float = 0.0
+    dist_state: float = 0.0
+    goal_dims: List[int] = field(default_factory=list)
+    goal_radius: float = 0.1
+    seed: int = 0
+
+
+@dataclass
+class MPCLogRow:  # mpc.hpp:389-396
+    step: int
+    state: np.ndarray
+    action: np.ndarray
+    objective: float
+    tube_volume: float
+    g_margin: float
+
+
+def _g17(v: float) -> str:
+    """fmt_g17 (io.hpp:23-27): printf("%.17g")."""
+    return "%.17g" % v
+
+
+@dataclass
+class MPCResult:  # mpc.hpp:398-419
+    success: bool
+    violated: bool
+    steps_used: int
+    final_state: np.ndarray
+    log: List[MPCLogRow]
+
+    def log_to_csv(self) -> str:
+        out = "step,objective,tube_volume,g_margin,state,action\n"
+        for r in self.log:
+            out += (f"{r.step},{_g17(r.objective)},{_g17(r.tube_volume)},{_g17(r.g_margin)},"
+                    + ";".join(_g17(v) for v in r.state) + "," + ";".join(_g17(v) for v in r.action) + "\n")
+        return out
+
+
+def mpc_run(prob: PlanProblem, sampler: SamplerConfig, cfg: MPCConfig, x0, sim=None,
+            ctx: Optional[Context] = None) -> MPCResult:
+    """mpc_run (mpc.hpp:425-495).  sim(x, u) -> x_next is the true simulator; None = the planning model's
+    forward on the device (the reference CLI's simulator, reach_cli.cpp:445-449)."""
+    prob.sys.validate()
+    ctx = ctx or default_context()
+    n, m = prob.sys.n, prob.sys.m
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    if x0.shape != (n,):
+        raise ValueError("mpc_run: x0 dimension mismatch")
+    T = int(cfg.total_steps)
+    rows = max(T, 1)
+    lg_step = np.zeros(rows, np.int32)
+    lg_state = np.zeros((rows, n))
+    lg_action = np.zeros((rows, max(m, 1)))
+    lg_obj, lg_vol, lg_mar = np.zeros(rows), np.zeros(rows), np.zeros(rows)
+    log = A.MPCLogC(A.iptr(lg_step), A.dptr(lg_state), A.dptr(lg_action), A.dptr(lg_obj), A.dptr(lg_vol),
+                    A.dptr(lg_mar))
+    gd = np.ascontiguousarray(cfg.goal_dims, dtype=np.int32) if cfg.goal_dims else np.zeros(1, np.int32)
+    mc = A.MPCConfigC(cfg.replan_period, cfg.total_steps, cfg.dist_action, cfg.dist_state, len(cfg.goal_dims),
+                      A.iptr(gd), cfg.goal_radius, cfg.seed)
+    err = []
+    if sim is None:
+        cb = A.SIM_FN()
+    else:
+        def _cb(user, xp, up, outp):
+            try:
+                xs = np.ctypeslib.as_array(xp, shape=(n,)).copy()
+                us = np.ctypeslib.as_array(up, shape=(m,)).copy() if m else np.zeros(0)
+                out = np.asarray(sim(xs, us), dtype=np.float64).reshape(n)
+                np.ctypeslib.as_array(outp, shape=(n,))[:] = out
+                return 0
+            except Exception as e:  # surfaced after the call
+                err.append(e)
+                return 1
+        cb = A.SIM_FN(_cb)
+    succ, viol, used, nrows = (np.zeros(1, np.int32) for _ in range(4))
+    fin = np.zeros(n)
+    p, keep = prob.c_struct()
+    sc = sampler.c_struct()
+    net = ctx.upload(prob.sys.step)
+    rc = ctx._lib.reach_mpc_run(ctx.handle, net, C.byref(p), C.byref(sc), C.byref(mc), cb, None, A.dptr(x0),
+                                A.iptr(succ), A.iptr(viol), A.iptr(used), A.dptr(fin), C.byref(log), A.iptr(nrows))
+    if err:
+        raise err[0]
+    ctx.check(rc, "mpc_run")
+    k = int(nrows[0])
+    rows_out = [MPCLogRow(int(lg_step[i]), lg_state[i].copy(), lg_action[i, :m].copy(), float(lg_obj[i]),
+                          float(lg_vol[i]), float(lg_mar[i])) for i in range(k)]
+    return MPCResult(bool(succ[0]), bool(viol[0]), int(used[0]), fin, rows_out)

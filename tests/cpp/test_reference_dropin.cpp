@@ -259,6 +259,50 @@ int main() {
         }
       }
   }
+  // mpc_run with the CLI's simulator (the model's forward) and disturbances: run log byte-identical
+  {
+    Rng r4(31);
+    PlanProblem prob;
+    prob.sys.n = 3;
+    prob.sys.m = 2;
+    prob.sys.step = random_mlp(r4, 5, {24, 24}, 3, Act::Relu, 0.7);
+    for (auto& w : prob.sys.step.layers.back().w.a) w *= 0.4;
+    prob.x_goal = {0.3, -0.2, 0.1};
+    prob.q_weights = {1.0, 1.0, 1.0};
+    prob.r_weights = {0.05, 0.05};
+    Constraint b;
+    b.type = Constraint::Type::box_stay_in;
+    b.lo = {-1.0, -1.0, -1.0};
+    b.hi = {1.0, 1.0, 1.0};
+    prob.constraints = {b};
+    prob.horizon = 5;
+    prob.u_lo = {-1.0, -1.0};
+    prob.u_hi = {1.0, 1.0};
+    prob.eps = 0.01;
+    SamplerConfig cfg;
+    cfg.population = 32;
+    cfg.iterations = 2;
+    cfg.seed = 11;
+    MPCConfig mc;
+    mc.replan_period = 2;
+    mc.total_steps = 6;
+    mc.dist_action = 0.02;
+    mc.dist_state = 0.01;
+    mc.seed = 5;
+    auto sim = [&](const Vec<double>& x, const Vec<double>& u) {
+      Vec<double> in = x;
+      in.insert(in.end(), u.begin(), u.end());
+      return prob.sys.step.forward(in);
+    };
+    Vec<double> x0{0.05, -0.05, 0.0};
+    auto ref = reach::mpc_run(prob, cfg, mc, sim, x0);
+    auto got = reach_b200::mpc_run(gpu, prob, cfg, mc, sim, x0);
+    if (ref.log_to_csv() != got.log_to_csv() || ref.success != got.success || ref.violated != got.violated ||
+        ref.steps_used != got.steps_used || ref.final_state != got.final_state) {
+      std::printf("mpc_run: mismatch\n");
+      ++failures;
+    }
+  }
   std::printf(failures ? "FAIL (%d)\n" : "OK: reference drop-in parity\n", failures);
   return failures ? 1 : 0;
 }

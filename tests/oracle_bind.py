@@ -402,3 +402,25 @@ def ref_grad_tube_volume(sys, x0, actions, target, method=0, prm=DTReachParams()
     args = A.DTArgs(1, H, sys.n, sys.m, prm.window, int(prm.rebuild_from_box), A.dptr(lo), A.dptr(hi), A.dptr(acts), 0)
     rc = f(C.byref(desc), C.byref(args), int(target), int(method), A.dptr(g), A.iptr(sub))
     return None if rc else (g[:dim], bool(sub[0]))
+
+
+def ref_mpc_run(prob, sampler, cfg, x0):
+    """The reference's mpc_run with the model as simulator -> (success, violated, steps_used, final_state, csv)."""
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    f = _mpc_fn(ref_lib(), "ref_mpc_run", [C.POINTER(A.NetDesc), C.POINTER(A.PlanProblemC),
+                                           C.POINTER(A.SamplerConfigC), C.POINTER(A.MPCConfigC), dp, ip, ip, ip, dp,
+                                           C.c_char_p, C.c_int32])
+    x0 = np.ascontiguousarray(x0, np.float64)
+    succ, viol, used = (np.zeros(1, np.int32) for _ in range(3))
+    fin = np.zeros(prob.sys.n)
+    buf = C.create_string_buffer(1 << 20)
+    gd = np.ascontiguousarray(cfg.goal_dims, dtype=np.int32) if cfg.goal_dims else np.zeros(1, np.int32)
+    mc = A.MPCConfigC(cfg.replan_period, cfg.total_steps, cfg.dist_action, cfg.dist_state, len(cfg.goal_dims),
+                      A.iptr(gd), cfg.goal_radius, cfg.seed)
+    desc, keep = prob.sys.step.desc()
+    p, keep2 = prob.c_struct()
+    sc = sampler.c_struct()
+    rc = f(C.byref(desc), C.byref(p), C.byref(sc), C.byref(mc), A.dptr(x0), A.iptr(succ), A.iptr(viol), A.iptr(used),
+           A.dptr(fin), buf, len(buf))
+    assert rc == 0, rc
+    return bool(succ[0]), bool(viol[0]), int(used[0]), fin, buf.value.decode()
