@@ -42,7 +42,9 @@ enum reach_status {
   REACH_E_CUDA = 2,             /* CUDA runtime / launch failure */
   REACH_E_UNSUPPORTED = 3,      /* shape outside the compiled kernel family */
   REACH_E_NO_DEVICE = 4,
-  REACH_E_OOM = 5
+  REACH_E_OOM = 5,
+  REACH_E_NONFINITE = 6         /* reference: std::runtime_error of grad_forward / grad_fd / gradient_refine
+                                   (non-finite objective or derivative) */
 };
 
 /* Per-sample tube status; reason strings via reach_tube_status_string(). */
@@ -243,7 +245,7 @@ int reach_plan_eval_batch(reach_ctx* ctx, const reach_net* net, const reach_plan
  * candidate (refine.hpp:347-398) with forward-dual gradients computed on the
  * device (reach_plan_objective_grad).  best_actions [H][m], best_history
  * [iterations], best_effort flag, and the final plan's tube (batch 1,
- * optional).  A non-finite dual derivative is REACH_E_INVALID_ARGUMENT, where
+ * optional).  A non-finite dual derivative is REACH_E_NONFINITE, where
  * the reference's grad_forward throws. */
 int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
                    const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
@@ -267,7 +269,7 @@ int reach_plan_objective_grad(reach_ctx* ctx, const reach_net* net, const reach_
  * (grad_fd: central differences, h = 1e-5 * max(1, |p_j|), 2 passes per parameter), all passes in one
  * launch.  `a` describes one tube (batch 1).  grad [dim]; subgradient = Gradient::subgradient (a ReLU
  * preactivation bound sat exactly at zero, neural.hpp:180); volume = the primal tube volume.  A
- * non-finite objective or derivative is REACH_E_INVALID_ARGUMENT (the reference throws). */
+ * non-finite objective or derivative is REACH_E_NONFINITE (the reference throws std::runtime_error). */
 enum reach_grad_target { REACH_GRAD_X0_CENTER = 0, REACH_GRAD_ACTIONS = 1, REACH_GRAD_WEIGHTS = 2 };
 enum reach_grad_method { REACH_GRAD_FORWARD_DUAL = 0, REACH_GRAD_FINITE_DIFFERENCE = 1 };
 int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
@@ -303,6 +305,17 @@ int reach_mpc_run(reach_ctx* ctx, const reach_net* net, const reach_plan_problem
                   const reach_sampler_config* sampler, const reach_mpc_config* cfg, reach_sim_fn sim, void* sim_user,
                   const double* x0, int32_t* success, int32_t* violated, int32_t* steps_used, double* final_state,
                   const reach_mpc_log* log, int32_t* log_rows);
+
+/* gradient_refine (refine.hpp:354-398; RefineParams defaults: step0 1, shrink 0.5, armijo 1e-4, 30
+ * backtracks, forward_dual) of tube_volume(dt_reach(box_from_center(center, radius), actions)) over the X0
+ * centre (target REACH_GRAD_X0_CENTER, dim n) or the flat action sequence (REACH_GRAD_ACTIONS, dim H*m),
+ * inside [lo, hi] -- the reference CLI's `refine` objective.  `a` gives n, m, H, DTReachParams and the
+ * actions (x0_lo / x0_hi unused).  x [dim]: start point in, refined point out; RefineResult's fields out.
+ * A non-finite initial objective or derivative is REACH_E_NONFINITE. */
+int reach_refine_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, const double* center,
+                             const double* radius, int32_t target, const double* lo, const double* hi,
+                             int32_t iters, double* x, double* initial_objective, double* objective,
+                             int32_t* progressed, int32_t* subgradient, int32_t* accepted_steps);
 
 /* The CEM loop in pieces, for multi-GPU drivers that shard each population
  * and all-gather the scores between sample() and update(). */

@@ -841,3 +841,50 @@ extern "C" int ref_mpc_run(const reach_net_desc* desc, const reach_plan_problem*
   }
   return REACH_OK;
 }
+
+// The reference CLI's refine objective (reach_cli.cpp:293-341): gradient_refine of
+// tube_volume(dt_reach(box_from_center(c, eps), acts)) over the centre (target 0) or the actions (1).
+extern "C" int ref_refine_tube_volume(const reach_net_desc* desc, int32_t n, int32_t m, int32_t horizon,
+                                      const double* center, double eps, const double* actions, int32_t target,
+                                      const double* lo, const double* hi, int32_t iters, double* x,
+                                      double* initial_objective, double* objective, int32_t* progressed,
+                                      int32_t* subgradient, int32_t* accepted_steps) {
+  try {
+    DTSystem<double> sys = make_sys(desc, n, m);
+    Vec<double> cen(center, center + n);
+    auto f = [&](const auto& p) {
+      using S = typename std::decay_t<decltype(p)>::value_type;
+      DTSystem<S> s;
+      s.step = net_cast<S>(sys.step);
+      s.n = n;
+      s.m = m;
+      Vec<S> c = to_scalar<S>(cen);
+      std::vector<Vec<S>> acts(static_cast<size_t>(horizon), Vec<S>(static_cast<size_t>(m), S(0.0)));
+      for (int t = 0; t < horizon; ++t)
+        for (int j = 0; j < m; ++j) acts[static_cast<size_t>(t)][static_cast<size_t>(j)] = S(actions[t * m + j]);
+      if (target == 0) {
+        c.assign(p.begin(), p.end());
+      } else {
+        for (int t = 0; t < horizon; ++t)
+          acts[static_cast<size_t>(t)] =
+              Vec<S>(p.begin() + static_cast<long>(t) * m, p.begin() + static_cast<long>(t + 1) * m);
+      }
+      return tube_volume(dt_reach(s, box_from_center(c, S(eps)), acts));
+    };
+    const size_t d = target == 0 ? static_cast<size_t>(n) : static_cast<size_t>(horizon) * m;
+    RefineParams rp;
+    rp.iters = iters;
+    auto res = gradient_refine(f, Vec<double>(x, x + d), Vec<double>(lo, lo + d), Vec<double>(hi, hi + d), rp);
+    std::copy(res.x.begin(), res.x.end(), x);
+    *initial_objective = res.initial_objective;
+    *objective = res.objective;
+    *progressed = res.progressed ? 1 : 0;
+    *subgradient = res.subgradient ? 1 : 0;
+    *accepted_steps = res.accepted_steps;
+  } catch (const std::invalid_argument&) {
+    return REACH_E_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return REACH_E_NONFINITE;
+  }
+  return REACH_OK;
+}

@@ -15,6 +15,7 @@ REACH_E_CUDA = 2
 REACH_E_UNSUPPORTED = 3
 REACH_E_NO_DEVICE = 4
 REACH_E_OOM = 5
+REACH_E_NONFINITE = 6
 
 REACH_FLAG_DEVICE_PTRS = 1
 

@@ -27,6 +27,10 @@ class NativeMissing(ReachError):
     pass
 
 
+class NonFiniteError(ReachError, ArithmeticError):
+    """The reference's std::runtime_error of grad_forward / grad_fd / gradient_refine (non-finite objective)."""
+
+
 def _declare(lib):
     vp = C.c_void_p
     lib.reach_abi_version.restype = C.c_int
@@ -60,6 +64,8 @@ def _declare(lib):
     lib.reach_plan_objective_grad.argtypes = [vp, vp, C.POINTER(A.PlanProblemC), dp, dp, dp, dp]
     lib.reach_mpc_run.argtypes = [vp, vp, C.POINTER(A.PlanProblemC), C.POINTER(A.SamplerConfigC),
                                   C.POINTER(A.MPCConfigC), A.SIM_FN, vp, dp, ip, ip, ip, dp, C.POINTER(A.MPCLogC), ip]
+    lib.reach_refine_tube_volume.argtypes = [vp, vp, C.POINTER(A.DTArgs), dp, dp, C.c_int32, dp, dp, C.c_int32, dp,
+                                             dp, dp, ip, ip, ip]
     lib.reach_grad_tube_volume.argtypes = [vp, vp, C.POINTER(A.DTArgs), C.c_int32, C.c_int32, dp, ip, dp]
     lib.reach_cem_create.argtypes = [C.POINTER(A.PlanProblemC), C.POINTER(A.SamplerConfigC), C.POINTER(vp)]
     lib.reach_cem_destroy.argtypes = [vp]
@@ -67,7 +73,7 @@ def _declare(lib):
     lib.reach_cem_update.argtypes = [vp, dp, ip]
     lib.reach_cem_result.argtypes = [vp, dp, dp, ip, dp]
     for f in ("reach_plan_eval_batch", "reach_plan_cem", "reach_plan_cem_ex", "reach_plan_objective_grad",
-              "reach_grad_tube_volume", "reach_mpc_run",
+              "reach_grad_tube_volume", "reach_mpc_run", "reach_refine_tube_volume",
               "reach_cem_create", "reach_cem_destroy",
               "reach_cem_sample", "reach_cem_update", "reach_cem_result"):
         getattr(lib, f).restype = C.c_int
@@ -111,6 +117,8 @@ class Context:
         msg = self._lib.reach_ctx_last_error(self.handle).decode()
         if rc == A.REACH_E_INVALID_ARGUMENT:
             raise ValueError(f"{what}: {msg}")
+        if rc == A.REACH_E_NONFINITE:
+            raise NonFiniteError(f"{what}: {msg}")
         raise ReachError(f"{what} failed (code {rc}): {msg}")
 
     def set_stream(self, stream_handle: int | None):

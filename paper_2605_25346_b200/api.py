@@ -312,6 +312,52 @@ def grad_tube_volume(sys: DTSystem, x0, actions: Sequence, target: GradTarget,
     return Gradient(g[:dim].copy(), method, bool(sub[0]), float(vol[0]))
 
 
+@dataclass
+class RefineResult:  # refine.hpp:333-340
+    x: np.ndarray
+    initial_objective: float
+    objective: float
+    progressed: bool
+    subgradient: bool
+    accepted_steps: int
+
+
+def refine_tube_volume(sys: DTSystem, center, radius, actions: Sequence, target: GradTarget, lo, hi,
+                       iters: int = 20, x=None, prm: DTReachParams = DTReachParams(),
+                       ctx: Optional[Context] = None) -> RefineResult:
+    """gradient_refine (refine.hpp:354-398) of tube_volume(dt_reach(box_from_center(c, radius), actions)) over
+    the X0 centre or the flat action sequence within [lo, hi] (the reference CLI's `refine`,
+    reach_cli.cpp:293-341).  x = the start point (default: the centre / the actions)."""
+    sys.validate()
+    ctx = ctx or default_context()
+    target = GradTarget(target)
+    if target == GradTarget.weights:
+        raise ValueError("refine: target must be the X0 centre or the actions")
+    c = np.ascontiguousarray(center, dtype=np.float64).reshape(-1)
+    r = np.ascontiguousarray(np.broadcast_to(np.asarray(radius, np.float64), c.shape))
+    if c.size != sys.n:
+        raise ValueError("dt_reach: X0 dimension mismatch")
+    H = len(actions)
+    acts = _actions_array([actions], 1, H, sys.m).reshape(-1)
+    d = sys.n if target == GradTarget.x0_center else H * sys.m
+    xv = np.ascontiguousarray(c if x is None and target == GradTarget.x0_center else
+                              (acts if x is None else x), dtype=np.float64).reshape(-1).copy()
+    lo = np.ascontiguousarray(lo, dtype=np.float64).reshape(-1)
+    hi = np.ascontiguousarray(hi, dtype=np.float64).reshape(-1)
+    if xv.size != d or lo.size != d or hi.size != d:
+        raise ValueError("gradient_refine: bound dimension mismatch")
+    f0, f1 = np.zeros(1), np.zeros(1)
+    pr, sb, ac = (np.zeros(1, np.int32) for _ in range(3))
+    args = A.DTArgs(1, H, sys.n, sys.m, prm.window, int(prm.rebuild_from_box), A.dptr(c), A.dptr(c),
+                    A.dptr(acts if acts.size else np.zeros(1)), 0)
+    net = ctx.upload(sys.step)
+    ctx.check(ctx._lib.reach_refine_tube_volume(ctx.handle, net, C.byref(args), A.dptr(c), A.dptr(r), int(target),
+                                                A.dptr(lo), A.dptr(hi), int(iters), A.dptr(xv if d else np.zeros(1)),
+                                                A.dptr(f0), A.dptr(f1), A.iptr(pr), A.iptr(sb), A.iptr(ac)),
+              "gradient_refine")
+    return RefineResult(xv[:d], float(f0[0]), float(f1[0]), bool(pr[0]), bool(sb[0]), int(ac[0]))
+
+
 # ---------------------------------------------------------------------------
 class SplitPlan:
     """SplitPlan (refine.hpp:25-78)."""

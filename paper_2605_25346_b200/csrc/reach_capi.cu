@@ -1334,7 +1334,7 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
     double fx = 0.0;
     rc = f(x, fx);
     if (rc) return rc;
-    if (!std::isfinite(fx)) return fail(ctx, REACH_E_INVALID_ARGUMENT, "gradient_refine: initial objective non-finite");
+    if (!std::isfinite(fx)) return fail(ctx, REACH_E_NONFINITE, "gradient_refine: initial objective non-finite");
     int accepted_steps = 0;
     std::vector<double> cands, fvals;
     std::vector<int32_t> cdiv;
@@ -1345,7 +1345,7 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
       bool fin = true;
       rc = plan_grad_device(ctx, net, prob, x0, x.data(), g.data(), &v, &fin);
       if (rc) return rc;
-      if (!fin) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_forward: non-finite derivative");
+      if (!fin) return fail(ctx, REACH_E_NONFINITE, "grad_forward: non-finite derivative");
       double gnorm2 = 0.0;
       for (size_t k = 0; k < d; ++k) gnorm2 += g[k] * g[k];
       if (gnorm2 == 0.0) break;
@@ -1414,37 +1414,20 @@ int reach_plan_objective_grad(reach_ctx* ctx, const reach_net* net, const reach_
   rc = plan_grad_device(ctx, net, prob, x0, actions, grad, &v, &fin);
   if (rc) return rc;
   if (objective) *objective = v;
-  if (!fin) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_forward: non-finite derivative");
+  if (!fin) return fail(ctx, REACH_E_NONFINITE, "grad_forward: non-finite derivative");
   return REACH_OK;
 }
 
-int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
-                           int32_t method, double* grad, int32_t* subgradient, double* volume) {
+}  // extern "C"
+
+namespace {
+// grad_tube_volume with X0 = box_from_center(center, radius) given directly (refine.hpp:283, the CLI's
+// refine objective uses box_from_center(c, eps)); a supplies the shapes, actions and DTReachParams.
+int grad_tube_volume_cr(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, const double* center,
+                        const double* radius, int32_t target, int32_t method, double* grad, int32_t* subgradient,
+                        double* volume) {
   namespace rd = rb::dual;
-  if (!ctx || !net || !a || !grad) return REACH_E_INVALID_ARGUMENT;
-  if (a->batch != 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: batch must be 1");
-  if (a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach: negative horizon");
-  if (target < REACH_GRAD_X0_CENTER || target > REACH_GRAD_WEIGHTS || method < REACH_GRAD_FORWARD_DUAL ||
-      method > REACH_GRAD_FINITE_DIFFERENCE)
-    return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: unknown target / method");
-  int rc = validate_system(ctx, net, a->n, a->m);
-  if (rc) return rc;
   const int n = a->n, m = a->m, H = a->horizon;
-  if (!a->x0_lo || !a->x0_hi || (H * m > 0 && !a->actions))
-    return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: missing input");
-  int maxw = 0;
-  for (int l = 0; l <= net->L; ++l) maxw = std::max(maxw, net->dims[l]);
-  const int cap = a->window > 0 ? a->window : 1;
-  if (n > rd::kN || m > rd::kM || maxw > rd::kW || net->L > rd::kL || H > rd::kH || n * (cap + 2) > rd::kZ ||
-      n * (cap + 2) + n > rd::kW || cap + 2 > rd::kQ)
-    return fail(ctx, REACH_E_UNSUPPORTED, "grad_tube_volume: shape outside the Dual kernel family");
-  // box_center / box_radius (interval.hpp:270-281), box_from_center's radius check (interval.hpp:229)
-  std::vector<double> center(n), radius(n);
-  for (int i = 0; i < n; ++i) {
-    center[i] = (a->x0_lo[i] + a->x0_hi[i]) * 0.5;
-    radius[i] = (a->x0_hi[i] - a->x0_lo[i]) * 0.5;
-    if (radius[i] < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "box_from_center: negative radius");
-  }
   rd::VolArgs V{};
   V.poff[0] = 0;
   for (int l = 0; l < net->L; ++l)
@@ -1456,9 +1439,6 @@ int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_
   const long long passes = fd ? 2 * dim + 1 : dim;
   if (passes > (1ll << 30)) return fail(ctx, REACH_E_UNSUPPORTED, "grad_tube_volume: too many parameters");
   if (subgradient) *subgradient = 0;
-  if (passes == 0) {  // nothing to differentiate: grad_forward still evaluates f0
-    if (volume) *volume = 0.0;
-  }
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -1468,12 +1448,12 @@ int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_
   const long long np = std::max<long long>(passes, 1);
   const size_t o_c = take(n * 8), o_r = take(n * 8), o_a = take(static_cast<size_t>(H) * m * 8),
                o_v = take(static_cast<size_t>(np) * 8), o_t = take(static_cast<size_t>(np) * 8), o_s = take(4);
-  rc = ensure_ws(ctx, off);
+  int rc = ensure_ws(ctx, off);
   if (rc) return rc;
   char* w = static_cast<char*>(ctx->ws);
   auto Dp = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
-  RB_CUDA(cudaMemcpyAsync(Dp(o_c), center.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
-  RB_CUDA(cudaMemcpyAsync(Dp(o_r), radius.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_c), center, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_r), radius, n * 8, cudaMemcpyHostToDevice, ctx->stream));
   if (H * m > 0)
     RB_CUDA(cudaMemcpyAsync(Dp(o_a), a->actions, static_cast<size_t>(H) * m * 8, cudaMemcpyHostToDevice, ctx->stream));
   RB_CUDA(cudaMemsetAsync(w + o_s, 0, 4, ctx->stream));
@@ -1515,17 +1495,16 @@ int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_
   const double f0 = (fd || passes == 0) ? val[launch - 1] : val[0];  // primal values are identical across passes
   if (volume) *volume = f0;
   if (!std::isfinite(f0))
-    return fail(ctx, REACH_E_INVALID_ARGUMENT,
-                fd ? "grad_fd: objective non-finite" : "grad_forward: objective non-finite");
+    return fail(ctx, REACH_E_NONFINITE, fd ? "grad_fd: objective non-finite" : "grad_forward: objective non-finite");
   for (long long j = 0; j < dim; ++j) {
     if (!fd) {
       if (!std::isfinite(val[j]) || !std::isfinite(tan[j]))
-        return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_forward: non-finite derivative");
+        return fail(ctx, REACH_E_NONFINITE, "grad_forward: non-finite derivative");
       grad[j] = tan[j];
     } else {
       const double fp = val[2 * j], fm = val[2 * j + 1];
       if (!std::isfinite(fp) || !std::isfinite(fm))
-        return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_fd: objective non-finite near x");
+        return fail(ctx, REACH_E_NONFINITE, "grad_fd: objective non-finite near x");
       double xj;  // the parameter value, for h (refine.hpp:222)
       if (target == REACH_GRAD_X0_CENTER) {
         xj = center[j];
@@ -1540,6 +1519,39 @@ int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_
   }
   if (subgradient) *subgradient = sub ? 1 : 0;
   return REACH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
+                           int32_t method, double* grad, int32_t* subgradient, double* volume) {
+  namespace rd = rb::dual;
+  if (!ctx || !net || !a || !grad) return REACH_E_INVALID_ARGUMENT;
+  if (a->batch != 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: batch must be 1");
+  if (a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach: negative horizon");
+  if (target < REACH_GRAD_X0_CENTER || target > REACH_GRAD_WEIGHTS || method < REACH_GRAD_FORWARD_DUAL ||
+      method > REACH_GRAD_FINITE_DIFFERENCE)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: unknown target / method");
+  int rc = validate_system(ctx, net, a->n, a->m);
+  if (rc) return rc;
+  const int n = a->n, m = a->m, H = a->horizon;
+  if (!a->x0_lo || !a->x0_hi || (H * m > 0 && !a->actions))
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: missing input");
+  int maxw = 0;
+  for (int l = 0; l <= net->L; ++l) maxw = std::max(maxw, net->dims[l]);
+  const int cap = a->window > 0 ? a->window : 1;
+  if (n > rd::kN || m > rd::kM || maxw > rd::kW || net->L > rd::kL || H > rd::kH || n * (cap + 2) > rd::kZ ||
+      n * (cap + 2) + n > rd::kW || cap + 2 > rd::kQ)
+    return fail(ctx, REACH_E_UNSUPPORTED, "grad_tube_volume: shape outside the Dual kernel family");
+  // box_center / box_radius (interval.hpp:270-281), box_from_center's radius check (interval.hpp:229)
+  std::vector<double> center(n), radius(n);
+  for (int i = 0; i < n; ++i) {
+    center[i] = (a->x0_lo[i] + a->x0_hi[i]) * 0.5;
+    radius[i] = (a->x0_hi[i] - a->x0_lo[i]) * 0.5;
+    if (radius[i] < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "box_from_center: negative radius");
+  }
+  return grad_tube_volume_cr(ctx, net, a, center.data(), radius.data(), target, method, grad, subgradient, volume);
 }
 
 // mpc_run (mpc.hpp:425-495): receding-horizon execution around plan_cem.
@@ -1709,6 +1721,128 @@ int reach_mpc_run(reach_ctx* ctx, const reach_net* net, const reach_plan_problem
     }
   }
   return finish(step, goal_reached(x) && !viol);
+}
+
+// gradient_refine (refine.hpp:354-398) of tube_volume(dt_reach(box_from_center(c, r), actions)) over
+// the X0 centre or the action sequence -- the reference CLI's `refine` (reach_cli.cpp:293-341).  Forward-dual
+// gradients from tube_volume_grad_kernel; the Armijo trial points of one iteration are evaluated in one
+// dt_reach batch on the device and the first accepted one is taken in order.
+int reach_refine_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, const double* center,
+                             const double* radius, int32_t target, const double* lo, const double* hi,
+                             int32_t iters, double* x, double* initial_objective, double* objective,
+                             int32_t* progressed, int32_t* subgradient, int32_t* accepted_steps) {
+  if (!ctx || !net || !a || !center || !radius || !lo || !hi || !x) return REACH_E_INVALID_ARGUMENT;
+  if (target != REACH_GRAD_X0_CENTER && target != REACH_GRAD_ACTIONS)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "refine: target must be the X0 centre or the actions");
+  if (iters < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "RefineParams: invalid configuration");
+  int rc = validate_system(ctx, net, a->n, a->m);
+  if (rc) return rc;
+  const int n = a->n, m = a->m, H = a->horizon;
+  if (H < 0 || (H * m > 0 && !a->actions)) return fail(ctx, REACH_E_INVALID_ARGUMENT, "refine: missing actions");
+  for (int i = 0; i < n; ++i)
+    if (radius[i] < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "box_from_center: negative radius");
+  const size_t d = target == REACH_GRAD_X0_CENTER ? n : static_cast<size_t>(H) * m;
+  for (size_t j = 0; j < d; ++j)
+    if (!(lo[j] <= hi[j])) return fail(ctx, REACH_E_INVALID_ARGUMENT, "gradient_refine: empty bound box");
+  std::vector<double> xv(x, x + d), g(d), xn(d);
+  auto project = [&](std::vector<double>& v) {
+    for (size_t j = 0; j < d; ++j) v[j] = std::clamp(v[j], lo[j], hi[j]);
+  };
+  // f of K points (rows of pts): one dt_reach batch, tube_volume per tube (tube.hpp:40-46)
+  const size_t boxes = static_cast<size_t>(H) + 1;
+  auto f_batch = [&](const std::vector<double>& pts, int K, std::vector<double>& fv) -> int {
+    std::vector<double> x0lo(static_cast<size_t>(K) * n), x0hi(x0lo.size()),
+        acts(static_cast<size_t>(K) * H * m), olo(static_cast<size_t>(K) * boxes * n), ohi(olo.size());
+    std::vector<int32_t> nb(K), fs(K), st(K);
+    for (int k = 0; k < K; ++k) {
+      const double* p = pts.data() + static_cast<size_t>(k) * d;
+      for (int i = 0; i < n; ++i) {
+        const double c = target == REACH_GRAD_X0_CENTER ? p[i] : center[i];
+        x0lo[static_cast<size_t>(k) * n + i] = c - radius[i];
+        x0hi[static_cast<size_t>(k) * n + i] = c + radius[i];
+      }
+      for (size_t q = 0; q < static_cast<size_t>(H) * m; ++q)
+        acts[static_cast<size_t>(k) * H * m + q] = target == REACH_GRAD_ACTIONS ? p[q] : a->actions[q];
+    }
+    reach_dt_args b = *a;
+    b.batch = K;
+    b.x0_lo = x0lo.data();
+    b.x0_hi = x0hi.data();
+    b.actions = acts.empty() ? nullptr : acts.data();
+    b.actions_shared = 0;
+    reach_tube_out o{olo.data(), ohi.data(), nb.data(), fs.data(), st.data()};
+    int e = run_dt_batch(ctx, net, nullptr, &b, &o, 0);
+    if (e) return e;
+    fv.assign(K, std::numeric_limits<double>::infinity());
+    for (int k = 0; k < K; ++k) {
+      if (st[k] != REACH_TUBE_OK) continue;
+      double acc = 0.0;
+      for (int t = 0; t < nb[k]; ++t) {
+        double v = 0.0;
+        for (int i = 0; i < n; ++i) {
+          const size_t q = (static_cast<size_t>(k) * boxes + t) * n + i;
+          v += ohi[q] - olo[q];
+        }
+        acc += v;
+      }
+      fv[k] = acc;
+    }
+    return REACH_OK;
+  };
+  project(xv);
+  std::vector<double> fv;
+  if ((rc = f_batch(xv, 1, fv))) return rc;
+  double fx = fv[0];
+  if (!std::isfinite(fx)) return fail(ctx, REACH_E_NONFINITE, "gradient_refine: initial objective non-finite");
+  if (initial_objective) *initial_objective = fx;
+  int acc_steps = 0;
+  bool sub_any = false;
+  std::vector<double> cands, moved_v, cvec(center, center + n);
+  for (int it = 0; it < iters; ++it) {
+    reach_dt_args ga = *a;
+    ga.batch = 1;
+    if (target == REACH_GRAD_ACTIONS) ga.actions = xv.data();
+    int32_t sub = 0;
+    double vol = 0.0;
+    rc = grad_tube_volume_cr(ctx, net, &ga, target == REACH_GRAD_X0_CENTER ? xv.data() : cvec.data(), radius, target,
+                             REACH_GRAD_FORWARD_DUAL, g.data(), &sub, &vol);
+    if (rc) return rc;
+    sub_any = sub_any || sub != 0;
+    double gnorm2 = 0.0;
+    for (size_t j = 0; j < d; ++j) gnorm2 += g[j] * g[j];
+    if (gnorm2 == 0.0) break;
+    cands.clear();
+    moved_v.clear();
+    double t = 1.0;
+    for (int bt = 0; bt < 30; ++bt, t *= 0.5) {
+      for (size_t j = 0; j < d; ++j) xn[j] = xv[j] - t * g[j];
+      project(xn);
+      double moved = 0.0;
+      for (size_t j = 0; j < d; ++j) moved += g[j] * (xv[j] - xn[j]);
+      if (moved <= 0.0) break;
+      cands.insert(cands.end(), xn.begin(), xn.end());
+      moved_v.push_back(moved);
+    }
+    bool accepted = false;
+    if (!moved_v.empty()) {
+      if ((rc = f_batch(cands, static_cast<int>(moved_v.size()), fv))) return rc;
+      for (size_t q = 0; q < moved_v.size(); ++q)
+        if (std::isfinite(fv[q]) && fv[q] <= fx - 1e-4 * moved_v[q]) {
+          std::copy(cands.begin() + q * d, cands.begin() + (q + 1) * d, xv.begin());
+          fx = fv[q];
+          accepted = true;
+          ++acc_steps;
+          break;
+        }
+    }
+    if (!accepted) break;
+  }
+  std::copy(xv.begin(), xv.end(), x);
+  if (objective) *objective = fx;
+  if (progressed) *progressed = acc_steps > 0 ? 1 : 0;
+  if (subgradient) *subgradient = sub_any ? 1 : 0;
+  if (accepted_steps) *accepted_steps = acc_steps;
+  return REACH_OK;
 }
 
 }  // extern "C"

@@ -424,3 +424,27 @@ def ref_mpc_run(prob, sampler, cfg, x0):
            A.dptr(fin), buf, len(buf))
     assert rc == 0, rc
     return bool(succ[0]), bool(viol[0]), int(used[0]), fin, buf.value.decode()
+
+
+def ref_refine_tube_volume(sys, center, eps, actions, target, lo, hi, iters=20, x=None):
+    """The reference's gradient_refine of the CLI refine objective -> RefineResult-like tuple, or None."""
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    f = _mpc_fn(ref_lib(), "ref_refine_tube_volume", [C.POINTER(A.NetDesc), C.c_int32, C.c_int32, C.c_int32, dp,
+                                                     C.c_double, dp, C.c_int32, dp, dp, C.c_int32, dp, dp, dp, ip,
+                                                     ip, ip])
+    c = np.ascontiguousarray(center, np.float64)
+    H = len(actions)
+    acts = np.ascontiguousarray(np.asarray(actions, np.float64).reshape(H * sys.m)) if H * sys.m else np.zeros(1)
+    d = sys.n if int(target) == 0 else H * sys.m
+    xv = np.ascontiguousarray(c if x is None and int(target) == 0 else (acts[:d] if x is None else x),
+                              np.float64).copy()
+    lo = np.ascontiguousarray(lo, np.float64)
+    hi = np.ascontiguousarray(hi, np.float64)
+    f0, f1 = np.zeros(1), np.zeros(1)
+    pr, sb, ac = (np.zeros(1, np.int32) for _ in range(3))
+    desc, keep = sys.step.desc()
+    rc = f(C.byref(desc), sys.n, sys.m, H, A.dptr(c), float(eps), A.dptr(acts), int(target), A.dptr(lo), A.dptr(hi),
+           int(iters), A.dptr(xv), A.dptr(f0), A.dptr(f1), A.iptr(pr), A.iptr(sb), A.iptr(ac))
+    if rc:
+        return None
+    return xv, float(f0[0]), float(f1[0]), bool(pr[0]), bool(sb[0]), int(ac[0])

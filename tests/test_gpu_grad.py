@@ -9,6 +9,7 @@ pytestmark = pytest.mark.gpu
 
 from grad_cases import diverging_case, grad_cases, identity_case
 from oracle_bind import ref_available, ref_grad_tube_volume, same_bits
+from paper_2605_25346_b200._native import NonFiniteError
 from paper_2605_25346_b200.api import GradMethod, GradTarget, grad_tube_volume, tube_volume, dt_reach
 
 needs_ref = pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
@@ -64,9 +65,9 @@ def test_volume_is_the_tube_volume():
 
 def test_diverged_tube_raises_like_grad_forward():
     sys, x0, acts = diverging_case()
-    with pytest.raises(ValueError, match="non-finite"):
+    with pytest.raises(NonFiniteError, match="non-finite"):
         grad_tube_volume(sys, x0, acts, GradTarget.x0_center)
-    with pytest.raises(ValueError, match="non-finite"):
+    with pytest.raises(NonFiniteError, match="non-finite"):
         grad_tube_volume(sys, x0, acts, GradTarget.weights, GradMethod.finite_difference)
 
 
@@ -81,3 +82,21 @@ def test_unit_gain_radius_closed_form_via_center():
     assert g.g.shape == (2,)
     assert abs(g.g[0] - 2 * r * H * (H + 1) / 2) <= 1e-10 * abs(g.g[0])
     assert g.g[1] == 0.0
+
+
+@needs_ref
+@pytest.mark.parametrize("target", [GradTarget.x0_center, GradTarget.actions])
+def test_refine_tube_volume_matches_reference(target):
+    """The reference CLI's refine (gradient_refine of the tube volume, reach_cli.cpp:293-341)."""
+    from oracle_bind import ref_refine_tube_volume
+    from paper_2605_25346_b200.api import refine_tube_volume
+    name, sys, x0, acts, prm, _ = grad_cases()[2]
+    c = (x0[0] + x0[1]) * 0.5
+    eps = 0.08
+    start = c if target == GradTarget.x0_center else np.asarray(acts, np.float64).reshape(-1)
+    lo, hi = start - 0.5, start + 0.5
+    exp = ref_refine_tube_volume(sys, c, eps, acts, int(target), lo, hi, iters=6)
+    got = refine_tube_volume(sys, c, eps, acts, target, lo, hi, iters=6)
+    assert same_bits(got.x, exp[0])
+    assert (got.initial_objective, got.objective, got.progressed, got.subgradient, got.accepted_steps) == exp[1:]
+    assert got.objective <= got.initial_objective
