@@ -36,6 +36,22 @@ class Constraint:
 
     HALFSPACE_AVOID, SPHERE_AVOID, BOX_STAY_IN, MAX_VOLUME = 0, 1, 2, 3
 
+    def validate(self, n: int):
+        """Constraint::validate (mpc.hpp:89-111)."""
+        for d in self.dims:
+            if d < 0 or d >= n:
+                raise ValueError("Constraint: dim out of range")
+        k = len(self.dims) if self.dims else n
+        size = lambda v: 0 if v is None else np.asarray(v).size  # noqa: E731
+        if self.type == self.HALFSPACE_AVOID and size(self.a) != k:
+            raise ValueError("Constraint: halfspace size")
+        if self.type == self.SPHERE_AVOID and (size(self.center) != k or self.radius < 0.0):
+            raise ValueError("Constraint: sphere parameters")
+        if self.type == self.BOX_STAY_IN and (size(self.lo) != k or size(self.hi) != k):
+            raise ValueError("Constraint: stay-in box size")
+        if self.type == self.MAX_VOLUME and self.vmax < 0.0:
+            raise ValueError("Constraint: volume budget")
+
 
 @dataclass
 class PlanProblem:
@@ -51,6 +67,25 @@ class PlanProblem:
     u_hi: Optional[np.ndarray] = None
     eps: float = 0.0
     dt_prm: DTReachParams = field(default_factory=DTReachParams)
+
+    def validate(self):
+        """PlanProblem::validate (mpc.hpp:129-141)."""
+        self.sys.validate()
+        n, m = self.sys.n, self.sys.m
+        if self.horizon < 1:
+            raise ValueError("PlanProblem: horizon < 1")
+        sz = lambda v: 0 if v is None else np.asarray(v).size  # noqa: E731
+        if sz(self.x_goal) != n or sz(self.q_weights) != n or sz(self.r_weights) != m:
+            raise ValueError("PlanProblem: cost dimension mismatch")
+        if sz(self.u_lo) != m or sz(self.u_hi) != m:
+            raise ValueError("PlanProblem: action box dimension mismatch")
+        for lo, hi in zip(np.asarray(self.u_lo if m else [], float), np.asarray(self.u_hi if m else [], float)):
+            if not (lo <= hi) or not np.isfinite(lo) or not np.isfinite(hi):
+                raise ValueError("PlanProblem: action box must be bounded")
+        if self.eps < 0.0 or self.penalty < 0.0:
+            raise ValueError("PlanProblem: negative weight")
+        for c in self.constraints:
+            c.validate(n)
 
     def c_struct(self):
         """(reach_plan_problem, keepalive)."""
