@@ -317,6 +317,15 @@ int reach_refine_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_d
                              int32_t iters, double* x, double* initial_objective, double* objective,
                              int32_t* progressed, int32_t* subgradient, int32_t* accepted_steps);
 
+/* reach_loss (training.hpp:99-126): the certified-training reachability regularizer of a batch of
+ * `episodes` episodes, (1/M) sum_m [tube diverged ? cap : log(1 + predicted_volume(dt_reach(
+ * box_from_center(x0_m, eps), first H actions)))], and (grad != NULL) its gradient over the one-step
+ * model's parameters in net_params order -- grad_forward's Dual passes, one CTA per (parameter, episode),
+ * all in one launch.  a->x0_lo = the episode start states [M][n], a->actions [M][H][m], a->horizon = t_h
+ * (x0_hi, batch unused).  diverged_count = the episodes charged the cap. */
+int reach_reach_loss(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t episodes,
+                     double eps, double cap, double* loss, double* grad, int32_t* diverged_count);
+
 /* The CEM loop in pieces, for multi-GPU drivers that shard each population
  * and all-gather the scores between sample() and update(). */
 typedef struct reach_cem reach_cem;

@@ -20,6 +20,7 @@
 #include "reach/dt_reach.hpp"
 #include "reach/fields.hpp"
 #include "reach/mpc.hpp"
+#include "reach/training.hpp"
 #include "reach/neural.hpp"
 #include "reach/parallel.hpp"
 #include "reach/refine.hpp"
@@ -881,6 +882,44 @@ extern "C" int ref_refine_tube_volume(const reach_net_desc* desc, int32_t n, int
     *progressed = res.progressed ? 1 : 0;
     *subgradient = res.subgradient ? 1 : 0;
     *accepted_steps = res.accepted_steps;
+  } catch (const std::invalid_argument&) {
+    return REACH_E_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return REACH_E_NONFINITE;
+  }
+  return REACH_OK;
+}
+
+// reach::reach_loss (training.hpp:99-126) and its grad_forward over net_params (the training gradient).
+extern "C" int ref_reach_loss(const reach_net_desc* desc, int32_t n, int32_t m, int32_t t_h, int32_t M,
+                              const double* x0s, const double* actions, double eps, double cap, int32_t window,
+                              int32_t rebuild, double* loss, double* grad, int32_t* diverged_count) {
+  try {
+    DTSystem<double> sys = make_sys(desc, n, m);
+    std::vector<Episode> batch(static_cast<size_t>(M));
+    for (int e = 0; e < M; ++e) {
+      Episode& ep = batch[static_cast<size_t>(e)];
+      for (int t = 0; t <= t_h; ++t) ep.states.push_back(Vec<double>(x0s + static_cast<size_t>(e) * n,
+                                                                   x0s + static_cast<size_t>(e + 1) * n));
+      for (int t = 0; t < t_h; ++t) {
+        const double* u = actions + (static_cast<size_t>(e) * t_h + t) * m;
+        ep.actions.push_back(Vec<double>(u, u + m));
+      }
+    }
+    DTReachParams prm;
+    prm.window = window;
+    prm.rebuild_from_box = rebuild != 0;
+    int dc = 0;
+    *loss = reach_loss(sys.step, batch, eps, t_h, cap, &dc, prm);
+    if (diverged_count) *diverged_count = dc;
+    if (grad) {
+      auto f = [&](const auto& p) {
+        using S = typename std::decay_t<decltype(p)>::value_type;
+        return reach_loss(net_with_params<S>(sys.step, p), batch, eps, t_h, cap, nullptr, prm);
+      };
+      Gradient g = grad_forward(f, net_params(sys.step));
+      std::copy(g.g.begin(), g.g.end(), grad);
+    }
   } catch (const std::invalid_argument&) {
     return REACH_E_INVALID_ARGUMENT;
   } catch (const std::exception&) {

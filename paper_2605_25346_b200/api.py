@@ -358,6 +358,51 @@ def refine_tube_volume(sys: DTSystem, center, radius, actions: Sequence, target:
     return RefineResult(xv[:d], float(f0[0]), float(f1[0]), bool(pr[0]), bool(sb[0]), int(ac[0]))
 
 
+@dataclass
+class Episode:  # training.hpp:28-45
+    states: Sequence   # [T+1][n]
+    actions: Sequence  # [T][m]
+    y_ref: Sequence = ()
+
+    def length(self) -> int:
+        return len(self.actions)
+
+
+def _loss_inputs(model: MLPNet, batch: Sequence[Episode], t_h: int):
+    if not batch or t_h < 1:
+        raise ValueError("reach_loss: bad batch/horizon")
+    n = len(batch[0].states[0])
+    m = len(batch[0].actions[0])
+    x0 = np.zeros((len(batch), n))
+    acts = np.zeros((len(batch), t_h, m))
+    for e, ep in enumerate(batch):
+        if ep.length() < t_h:
+            raise ValueError("reach_loss: episode shorter than T_h")
+        x0[e] = np.asarray(ep.states[0], np.float64)
+        acts[e] = np.asarray(ep.actions[:t_h], np.float64).reshape(t_h, m)
+    return DTSystem(model, n, m), x0, acts
+
+
+def reach_loss(model: MLPNet, batch: Sequence[Episode], eps: float, t_h: int, cap: float,
+               prm: DTReachParams = DTReachParams(), with_grad: bool = False, ctx: Optional[Context] = None):
+    """reach_loss (training.hpp:99-126) on the device -> (loss, diverged_count), or with_grad ->
+    (loss, gradient over net_params (neural.hpp:133-140), diverged_count): grad_forward's Dual passes,
+    one CTA per (parameter, episode), one launch."""
+    sys_, x0, acts = _loss_inputs(model, batch, t_h)
+    sys_.validate()
+    ctx = ctx or default_context()
+    M = x0.shape[0]
+    loss = np.zeros(1)
+    dc = np.zeros(1, np.int32)
+    g = np.zeros(model.params().size) if with_grad else None
+    args = A.DTArgs(M, t_h, sys_.n, sys_.m, prm.window, int(prm.rebuild_from_box), A.dptr(x0), A.dptr(x0),
+                    A.dptr(acts if acts.size else np.zeros(1)), 0)
+    net = ctx.upload(model)
+    ctx.check(ctx._lib.reach_reach_loss(ctx.handle, net, C.byref(args), M, float(eps), float(cap), A.dptr(loss),
+                                        A.dptr(g) if with_grad else None, A.iptr(dc)), "reach_loss")
+    return (float(loss[0]), g, int(dc[0])) if with_grad else (float(loss[0]), int(dc[0]))
+
+
 # ---------------------------------------------------------------------------
 class SplitPlan:
     """SplitPlan (refine.hpp:25-78)."""

@@ -716,5 +716,83 @@ __global__ void __launch_bounds__(kThreads, 2) tube_volume_grad_kernel(const Vol
   }
 }
 
+// ---------------------------------------------------------------------------
+// reach_loss (training.hpp:99-126): (1/M) sum_m [diverged ? cap : log(1 + predicted_volume(tube_m))],
+// tube_m = dt_reach from box_from_center(x0_m, eps) under the episode's first t_h actions.  CTA
+// (pass, episode): pass p seeds network parameter p (net_params order) for grad_forward over the
+// parameters (the training objective's gradient); pass -1 (value only) seeds nothing.  The per-episode
+// Dual terms are combined on the host in episode order, as the reference's accumulator does.
+struct LossArgs {
+  DevNet net;
+  int n, m, H, window, rebuild, M;
+  const double* x0;       // [M][n] episode start states
+  const double* actions;  // [M][H][m]
+  double eps, cap;
+  int seeded;             // 0: value only (one pass, no seed)
+  long long poff[kMaxLayers + 1];
+  double* term_v;         // [passes][M]
+  double* term_d;
+  int* diverged;          // [M] (pass 0)
+};
+
+__global__ void __launch_bounds__(kThreads, 2) reach_loss_grad_kernel(const LossArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Work& W = *reinterpret_cast<Work*>(smem_raw);
+  const int tid = threadIdx.x, pass = blockIdx.x, ep = blockIdx.y;
+  const int n = A.n, m = A.m, H = A.H;
+  NetView net{A.net};
+  if (A.seeded) {
+    const long long p = pass;
+    int l = 0;
+    while (l + 1 <= A.net.L && A.poff[l + 1] <= p) ++l;
+    const long long q = p - A.poff[l];
+    const int rows = A.net.dims[l + 1], cols = A.net.dims[l];
+    net.sl = l;
+    if (q < static_cast<long long>(rows) * cols) {
+      net.si = static_cast<int>(q / cols);
+      net.sj = static_cast<int>(q % cols);
+    } else {
+      net.si = static_cast<int>(q - static_cast<long long>(rows) * cols);
+      net.sj = -1;
+    }
+    net.seed = 1.0;
+  }
+  const double* acts = A.actions + static_cast<size_t>(ep) * H * m;
+  for (int e = tid; e < H * m; e += kThreads) W.acts[e / m][e % m] = dc(acts[e]);
+  if (tid == 0) {
+    W.sub = 0;
+    for (int i = 0; i < n; ++i) {  // box_from_center(x0, S(eps))
+      const D c = dc(A.x0[static_cast<size_t>(ep) * n + i]), r = dc(A.eps);
+      W.tlo[0][i] = dsub(c, r);
+      W.thi[0][i] = dadd(c, r);
+    }
+  }
+  __syncthreads();
+  bool failed = false;
+  const int nb = dt_tube_d(net, n, m, H, A.window, A.rebuild, W, tid, failed);
+  if (tid == 0) {
+    bool div = failed;
+    for (int k = 0; !div && k < nb; ++k)
+      for (int i = 0; i < n; ++i) div = div || !(dfin(W.tlo[k][i]) && dfin(W.thi[k][i]));
+    D term;
+    if (div) {
+      term = dc(A.cap);
+    } else {
+      D v = dc(0.0);  // predicted_volume (training.hpp:89-93): boxes 1..
+      for (int k = 1; k < nb; ++k) {
+        D b = dc(0.0);
+        for (int i = 0; i < n; ++i) b = dadd(b, dsub(W.thi[k][i], W.tlo[k][i]));
+        v = dadd(v, b);
+      }
+      const D a = dadd(dc(1.0), v);
+      term = D{log(a.v), __ddiv_rn(a.d, a.v)};  // reach::log (scalar.hpp:47)
+    }
+    const size_t o = static_cast<size_t>(pass) * A.M + ep;
+    A.term_v[o] = term.v;
+    A.term_d[o] = term.d;
+    if (pass == 0) A.diverged[ep] = div ? 1 : 0;
+  }
+}
+
 }  // namespace dual
 }  // namespace rb

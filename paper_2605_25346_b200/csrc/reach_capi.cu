@@ -1845,4 +1845,95 @@ int reach_refine_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_d
   return REACH_OK;
 }
 
+// reach_loss (training.hpp:99-126) of a batch of M episodes and, optionally, its gradient over the
+// network parameters (grad_forward, refine.hpp:186-207, in net_params order).
+int reach_reach_loss(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t episodes,
+                     double eps, double cap, double* loss, double* grad, int32_t* diverged_count) {
+  namespace rd = rb::dual;
+  if (!ctx || !net || !a || !loss) return REACH_E_INVALID_ARGUMENT;
+  if (episodes < 1 || a->horizon < 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "reach_loss: bad batch/horizon");
+  int rc = validate_system(ctx, net, a->n, a->m);
+  if (rc) return rc;
+  const int n = a->n, m = a->m, H = a->horizon, M = episodes;
+  if (!a->x0_lo || (m > 0 && !a->actions)) return fail(ctx, REACH_E_INVALID_ARGUMENT, "reach_loss: missing input");
+  if (eps < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "box_from_center: negative radius");
+  int maxw = 0;
+  for (int l = 0; l <= net->L; ++l) maxw = std::max(maxw, net->dims[l]);
+  const int cap_q = a->window > 0 ? a->window : 1;
+  if (n > rd::kN || m > rd::kM || maxw > rd::kW || net->L > rd::kL || H > rd::kH || n * (cap_q + 2) > rd::kZ ||
+      n * (cap_q + 2) + n > rd::kW || cap_q + 2 > rd::kQ || M > 65535)
+    return fail(ctx, REACH_E_UNSUPPORTED, "reach_loss: shape outside the Dual kernel family");
+  rd::LossArgs L{};
+  L.poff[0] = 0;
+  for (int l = 0; l < net->L; ++l)
+    L.poff[l + 1] = L.poff[l] + static_cast<long long>(net->dims[l + 1]) * net->dims[l] + net->dims[l + 1];
+  const long long P = grad ? L.poff[net->L] : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t o_x = take(static_cast<size_t>(M) * n * 8), o_a = take(static_cast<size_t>(M) * H * m * 8),
+               o_v = take(static_cast<size_t>(P) * M * 8), o_d = take(static_cast<size_t>(P) * M * 8),
+               o_div = take(static_cast<size_t>(M) * 4);
+  rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  RB_CUDA(cudaMemcpyAsync(Dp(o_x), a->x0_lo, static_cast<size_t>(M) * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (m > 0)
+    RB_CUDA(cudaMemcpyAsync(Dp(o_a), a->actions, static_cast<size_t>(M) * H * m * 8, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  L.net = net->dev;
+  L.n = n;
+  L.m = m;
+  L.H = H;
+  L.window = a->window;
+  L.rebuild = a->rebuild_from_box;
+  L.M = M;
+  L.x0 = Dp(o_x);
+  L.actions = Dp(o_a);
+  L.eps = eps;
+  L.cap = cap;
+  L.seeded = grad ? 1 : 0;
+  L.term_v = Dp(o_v);
+  L.term_d = Dp(o_d);
+  L.diverged = reinterpret_cast<int*>(w + o_div);
+  RB_CUDA(cudaFuncSetAttribute(rd::reach_loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sizeof(rd::Work))));
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  rd::reach_loss_grad_kernel<<<dim3(static_cast<unsigned>(P), static_cast<unsigned>(M)), rd::kThreads,
+                               sizeof(rd::Work), ctx->stream>>>(L);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  std::vector<double> tv(static_cast<size_t>(P) * M), td(tv.size());
+  std::vector<int32_t> dv(M);
+  RB_CUDA(cudaMemcpyAsync(tv.data(), Dp(o_v), tv.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(td.data(), Dp(o_d), td.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(dv.data(), w + o_div, static_cast<size_t>(M) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  // acc += term per episode, then acc / S(M) (scalar.hpp:22-28: (a.d*b.v - a.v*b.d) / (b.v*b.v))
+  const double Md = static_cast<double>(M);
+  for (long long p = 0; p < P; ++p) {
+    double av = 0.0, ad = 0.0;
+    for (int e = 0; e < M; ++e) {
+      av = av + tv[static_cast<size_t>(p) * M + e];
+      ad = ad + td[static_cast<size_t>(p) * M + e];
+    }
+    if (p == 0) *loss = av / Md;
+    if (grad) grad[p] = (ad * Md - av * 0.0) / (Md * Md);
+  }
+  if (diverged_count) {
+    int c = 0;
+    for (int e = 0; e < M; ++e) c += dv[e];
+    *diverged_count = c;
+  }
+  return REACH_OK;
+}
+
 }  // extern "C"

@@ -448,3 +448,23 @@ def ref_refine_tube_volume(sys, center, eps, actions, target, lo, hi, iters=20, 
     if rc:
         return None
     return xv, float(f0[0]), float(f1[0]), bool(pr[0]), bool(sb[0]), int(ac[0])
+
+
+def ref_reach_loss(model, x0s, actions, eps, cap, prm=DTReachParams(), with_grad=False):
+    """The reference's reach_loss (+ grad_forward over net_params) -> (loss, grad or None, diverged_count)."""
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    f = _mpc_fn(ref_lib(), "ref_reach_loss", [C.POINTER(A.NetDesc), C.c_int32, C.c_int32, C.c_int32, C.c_int32, dp,
+                                             dp, C.c_double, C.c_double, C.c_int32, C.c_int32, dp, dp, ip])
+    x0s = np.ascontiguousarray(x0s, np.float64)
+    acts = np.ascontiguousarray(actions, np.float64)
+    M, n = x0s.shape
+    t_h, m = acts.shape[1], acts.shape[2]
+    loss = np.zeros(1)
+    dc = np.zeros(1, np.int32)
+    g = np.zeros(model.params().size) if with_grad else None
+    desc, keep = model.desc()
+    rc = f(C.byref(desc), n, m, t_h, M, A.dptr(x0s), A.dptr(acts if acts.size else np.zeros(1)), float(eps),
+           float(cap), prm.window, int(prm.rebuild_from_box), A.dptr(loss), A.dptr(g) if with_grad else None,
+           A.iptr(dc))
+    assert rc == 0, rc
+    return float(loss[0]), g, int(dc[0])
