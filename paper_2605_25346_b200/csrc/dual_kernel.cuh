@@ -263,7 +263,9 @@ __device__ __forceinline__ int certify_d(const NetView& net, int n, int nz, Work
       W.bup[i] = dadd(W.bup[i], acc);
     }
     __syncthreads();
-    // Lambda = matmul(Lambda, W_l) (linalg.hpp:53-63): element (i, j) sums k ascending
+    // Lambda = matmul(Lambda, W_l) (linalg.hpp:53-63): element (i, j) sums k ascending, one thread per
+    // element (consecutive threads = consecutive columns: coalesced W rows, Lambda entries broadcast).
+    // (Measured: one thread per column with all rows' chains in registers is 13 % slower.)
     for (int e = tid; e < n_o * cols; e += kThreads) {
       const int i = e / cols, j = e % cols;
       D acc = dc(0.0);
@@ -299,92 +301,131 @@ __device__ __forceinline__ D row_abs(const D* row, int cols) {
   return acc;
 }
 
-// mat_solve (linalg.hpp:96-132) on W.g0 (n x n) and W.qa (n x w) into W.qx.
-__device__ inline bool mat_solve_d(int n, int w, Work& W) {
-  D a[kN][kN], b[kN][kN];
-  for (int i = 0; i < n; ++i) {
-    for (int j = 0; j < n; ++j) a[i][j] = W.g0[i][j];
-    for (int j = 0; j < w; ++j) b[i][j] = W.qa[i][j];
-  }
-  for (int k = 0; k < n; ++k) {
-    int piv = k;
-    double best = fabs(a[k][k].v);
-    for (int i = k + 1; i < n; ++i) {
-      const double cand = fabs(a[i][k].v);
-      if (cand > best) {
-        best = cand;
-        piv = i;
-      }
-    }
-    if (!(best > 1e-12)) return false;
-    if (piv != k) {
-      for (int j = 0; j < n; ++j) {
-        const D t = a[k][j];
-        a[k][j] = a[piv][j];
-        a[piv][j] = t;
-      }
-      for (int j = 0; j < w; ++j) {
-        const D t = b[k][j];
-        b[k][j] = b[piv][j];
-        b[piv][j] = t;
-      }
-    }
-    for (int i = k + 1; i < n; ++i) {
-      const D f = ddiv(a[i][k], a[k][k]);
-      for (int j = k; j < n; ++j) a[i][j] = dsub(a[i][j], dmul(f, a[k][j]));
-      for (int j = 0; j < w; ++j) b[i][j] = dsub(b[i][j], dmul(f, b[k][j]));
-    }
-  }
-  for (int i = n - 1; i >= 0; --i)
-    for (int j = 0; j < w; ++j) {
-      D acc = b[i][j];
-      for (int k = i + 1; k < n; ++k) acc = dsub(acc, dmul(a[i][k], W.qx[k][j]));
-      W.qx[i][j] = ddiv(acc, a[i][i]);
-    }
-  return true;
-}
-
-// fold_overflow (flowpipe_ct.hpp:317-350) with a square G0 (dt_reach).
-__device__ inline void fold_d(int n, int& nq, int cap, Work& W) {
+// fold_overflow (flowpipe_ct.hpp:317-350) with a square G0 (dt_reach) by one warp: lane c < n + w holds
+// column c of [G0 | Q1] in registers for the partial-pivot elimination (linalg.hpp:96-132; pivot column
+// and factors broadcast from the lane owning column k); every element sees the reference's operation
+// sequence.  The scalar tail (row abs-sums, G0.X - Q, column inflation, the queue shift) is lane-parallel
+// over rows.  Called by all 32 lanes of warp 0 with identical nq.
+__device__ __noinline__ void fold_warp_d(int n, int& nq, int cap, Work& W, int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
   while (nq > cap) {
     const int w = W.wid[0];
+    const int ncol = n + w;
     int off_new = n;
     for (int q = 0; q + 1 < nq; ++q) off_new += W.wid[q];
-    for (int i = 0; i < n; ++i) {
-      for (int j = 0; j < n; ++j) W.g0[i][j] = W.S[i][j];
-      for (int j = 0; j < w; ++j) W.qa[i][j] = W.S[i][n + j];
+    D col[kN];
+#pragma unroll
+    for (int i = 0; i < kN; ++i) col[i] = (lane < ncol && i < n) ? W.S[i][lane] : dc(0.0);
+    if (lane < n) {
+#pragma unroll
+      for (int i = 0; i < kN; ++i)
+        if (i < n) W.g0[i][lane] = col[i];
+    } else if (lane < ncol) {
+#pragma unroll
+      for (int i = 0; i < kN; ++i)
+        if (i < n) W.qa[i][lane - n] = col[i];
     }
-    bool folded = false;
-    if (mat_solve_d(n, w, W)) {
-      double worst = 0.0;
-      for (int j = 0; j < n; ++j) {
-        W.rr[j] = dmul(row_abs(W.qx[j], w), dc(1.0 + 1e-12));
-        worst = (worst < W.rr[j].v) ? W.rr[j].v : worst;  // std::max on values
-      }
-      if (worst <= 1.0) {
-        for (int i = 0; i < n; ++i) {
-          for (int j = 0; j < w; ++j) W.qe[i][j] = dc(0.0);
-          for (int k = 0; k < n; ++k) {
-            const D gik = W.g0[i][k];
-            for (int j = 0; j < w; ++j) W.qe[i][j] = dadd(W.qe[i][j], dmul(gik, W.qx[k][j]));
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < kN; ++k) {
+      if (k >= n || !ok) break;
+      int piv = k;
+      double best = fabs(col[k].v);
+#pragma unroll
+      for (int i = k + 1; i < kN; ++i)
+        if (i < n) {
+          const double c = fabs(col[i].v);
+          if (c > best) {
+            best = c;
+            piv = i;
           }
         }
-        for (int i = 0; i < n; ++i)
-          for (int j = 0; j < w; ++j) W.qe[i][j] = dsub(W.qe[i][j], W.qa[i][j]);
-        for (int j = 0; j < n; ++j)
-          for (int i = 0; i < n; ++i) W.S[i][j] = dmul(W.S[i][j], dadd(dc(1.0), W.rr[j]));
-        for (int i = 0; i < n; ++i)
-          W.S[i][off_new + i] = dadd(W.S[i][off_new + i], dmul(row_abs(W.qe[i], w), dc(1.0 + 1e-12)));
+      piv = __shfl_sync(FULL, piv, k);
+      best = __shfl_sync(FULL, best, k);
+      if (!(best > 1e-12)) {
+        ok = false;
+        break;
+      }
+#pragma unroll
+      for (int r = k + 1; r < kN; ++r)
+        if (r == piv) {
+          const D t = col[k];
+          col[k] = col[r];
+          col[r] = t;
+        }
+      const bool upd = (lane >= k && lane < ncol);
+#pragma unroll
+      for (int i = k + 1; i < kN; ++i) {
+        if (i < n) {
+          D f = ddiv(col[i], col[k]);  // meaningful on lane k: a[i][k] / a[k][k]
+          f.v = __shfl_sync(FULL, f.v, k);
+          f.d = __shfl_sync(FULL, f.d, k);
+          if (upd) col[i] = dsub(col[i], dmul(f, col[k]));
+        }
+      }
+    }
+    bool folded = false;
+    if (ok) {
+      // back substitution on the B lanes; a[i][k] comes from lane k
+      D x[kN];
+#pragma unroll
+      for (int ii = kN - 1; ii >= 0; --ii) {
+        if (ii < n) {
+          D acc = col[ii];
+#pragma unroll
+          for (int k = ii + 1; k < kN; ++k)
+            if (k < n) {
+              D aik;
+              aik.v = __shfl_sync(FULL, col[ii].v, k);
+              aik.d = __shfl_sync(FULL, col[ii].d, k);
+              acc = dsub(acc, dmul(aik, x[k]));
+            }
+          D aii;
+          aii.v = __shfl_sync(FULL, col[ii].v, ii);
+          aii.d = __shfl_sync(FULL, col[ii].d, ii);
+          x[ii] = ddiv(acc, aii);
+        } else {
+          x[ii] = dc(0.0);
+        }
+      }
+      if (lane >= n && lane < ncol) {
+#pragma unroll
+        for (int i = 0; i < kN; ++i)
+          if (i < n) W.qx[i][lane - n] = x[i];
+      }
+      __syncwarp();
+      if (lane < n) W.rr[lane] = dmul(row_abs(W.qx[lane], w), dc(1.0 + 1e-12));
+      __syncwarp();
+      double worst = 0.0;
+      for (int j = 0; j < n; ++j) worst = (worst < W.rr[j].v) ? W.rr[j].v : worst;  // std::max on values
+      if (worst <= 1.0) {
+        for (int e = lane; e < n * w; e += 32) {
+          const int i = e / w, j = e % w;
+          D acc = dc(0.0);
+          for (int k = 0; k < n; ++k) acc = dadd(acc, dmul(W.g0[i][k], W.qx[k][j]));
+          W.qe[i][j] = dsub(acc, W.qa[i][j]);
+        }
+        __syncwarp();
+        for (int e = lane; e < n * n; e += 32) {
+          const int i = e / n, j = e % n;
+          W.S[i][j] = dmul(W.S[i][j], dadd(dc(1.0), W.rr[j]));
+        }
+        if (lane < n)
+          W.S[lane][off_new + lane] =
+              dadd(W.S[lane][off_new + lane], dmul(row_abs(W.qe[lane], w), dc(1.0 + 1e-12)));
         folded = true;
       }
     }
-    if (!folded)
-      for (int i = 0; i < n; ++i) W.S[i][off_new + i] = dadd(W.S[i][off_new + i], row_abs(&W.S[i][n], w));
+    if (!folded && lane < n) W.S[lane][off_new + lane] = dadd(W.S[lane][off_new + lane], row_abs(&W.S[lane][n], w));
+    __syncwarp();
     int total = n;
     for (int q = 0; q < nq; ++q) total += W.wid[q];
-    for (int i = 0; i < n; ++i)
-      for (int j = n; j + w < total; ++j) W.S[i][j] = W.S[i][j + w];
-    for (int q = 0; q + 1 < nq; ++q) W.wid[q] = W.wid[q + 1];
+    if (lane < n)
+      for (int j = n; j + w < total; ++j) W.S[lane][j] = W.S[lane][j + w];
+    __syncwarp();
+    if (lane == 0)
+      for (int q = 0; q + 1 < nq; ++q) W.wid[q] = W.wid[q + 1];
+    __syncwarp();
     --nq;
   }
 }
@@ -489,11 +530,12 @@ __device__ __forceinline__ int dt_tube_d(const NetView& net, int n, int m, int H
       W.S[i][q] = q < nz ? W.oA[i][q] : (q - nz == i ? irad(W.orem[i]) : dc(0.0));
     }
     __syncthreads();
-    if (tid == 0) {
-      int nq2 = nq;
-      W.wid[nq2++] = n;
-      fold_d(n, nq2, cap, W);
-      W.nq = nq2;
+    if (tid < 32) {  // fold_overflow by warp 0
+      if (tid == 0) W.wid[nq] = n;
+      __syncwarp();
+      int nq2 = nq + 1;
+      fold_warp_d(n, nq2, cap, W, tid);
+      if (tid == 0) W.nq = nq2;
     }
     __syncthreads();
     // symbolic_box (flowpipe_ct.hpp:413-424)

@@ -16,6 +16,9 @@ def main():
     rep, kname, so = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
     fname = sys.argv[5] if len(sys.argv) > 5 else kname  # function-name pattern in the disassembly
+    # optional: attribute each instruction to the innermost frame inside this source file
+    # (e.g. dt_kernel.cuh, so arithmetic helpers count at their call sites)
+    focus = sys.argv[6] if len(sys.argv) > 6 else None
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass", "-k", f"regex:{kname}"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -37,7 +40,7 @@ def main():
             break
     # find function section by mangled-name match
     lines = dis.splitlines()
-    cur_fn, cur_line, in_fn, prev_marker = None, None, False, False
+    cur_fn, cur_line, in_fn, prev_marker, focus_hit = None, None, False, False, False
     addr_line = {}
     for ln in lines:
         m = re.match(r"\s*\.text\.(\S+):", ln)
@@ -49,8 +52,13 @@ def main():
         # an inline chain is a run of markers, innermost first: keep the first of each run
         m = re.search(r"//## File \"(.*?)\", line (\d+)", ln)
         if m:
+            loc = (os.path.basename(m.group(1)), int(m.group(2)))
             if not prev_marker:
-                cur_line = (os.path.basename(m.group(1)), int(m.group(2)))
+                cur_line = loc
+                focus_hit = focus is not None and loc[0] == focus
+            elif focus is not None and not focus_hit and loc[0] == focus:
+                cur_line = loc
+                focus_hit = True
             prev_marker = True
             continue
         prev_marker = False
