@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-sample-parts", type=int, default=0, help="parts per CPU sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mpc", action="store_true", help="skip the C3 MPC replan leg")
+    ap.add_argument("--no-grad", action="store_true", help="skip the grad_tube_volume leg")
     ap.add_argument("--no-ct", action="store_true", help="skip the C2 continuous-time closed-loop leg")
     ap.add_argument("--no-cl", action="store_true", help="skip the C5 / C1 DT closed-loop legs")
     return ap.parse_args()
@@ -209,6 +210,28 @@ def mpc_replan(args, ctx, world, rank, dev, barrier):
            "ms_per_replan": 1e3 * t, "target_ms": 50.0, "replans_timed": reps,
            "reach_steps_per_s": steps / t, "objective": obj,
            "parity": "bit-identical plan/objective/history vs the reference plan_cem (tests/test_gpu_mpc.py)"}
+    if world == 1:
+        # the reference default refine_iters = 5: CEM + forward-dual gradient refinement of the top plan
+        import dataclasses
+        from paper_2605_25346_b200.mpc import plan_objective_grad
+        cfg5 = dataclasses.replace(cfg, refine_iters=5)
+        plan_cem(prob, cfg5, x0, ctx=ctx)
+        tr = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            r5 = plan_cem(prob, cfg5, x0, ctx=ctx)
+            tr.append(time.perf_counter() - t0)
+        g_t = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            plan_objective_grad(prob, x0, r5.actions, ctx=ctx)
+            g_t.append(time.perf_counter() - t0)
+        out["refine_iters_5"] = {"ms_per_replan": 1e3 * float(np.mean(tr)), "objective": r5.objective,
+                                 "refined": r5.refined,
+                                 "plan_objective_grad_ms": 1e3 * float(np.median(g_t)),
+                                 "grad_directions": prob.horizon * prob.sys.m,
+                                 "parity": "bit-identical plan / objective / refined flag vs the reference "
+                                           "plan_cem with refinement (tests/test_gpu_refine.py)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle_bind import ref_available, ref_plan_cem, ref_lib
@@ -220,6 +243,47 @@ def mpc_replan(args, ctx, world, rank, dev, barrier):
                 lib.ref_hardware_threads.restype = C.c_int
                 out["cpu_reference_ms_per_replan"] = 1e3 * tc
                 out["cpu_reference_cores"] = int(lib.ref_hardware_threads())
+        except Exception as ex:  # noqa: BLE001
+            out["cpu_reference_error"] = str(ex)
+    return out
+
+
+def gradient_leg(args, ctx):
+    """grad_tube_volume (refine.hpp:263-311) of the C4-shaped map (6->128x3->6 ReLU, H = 30, window 4):
+    the weights target = 34,694 forward-dual passes in one launch.  CPU reference: the reference's
+    grad_tube_volume on the 6-parameter x0_center target timed on one host core (grad_forward is
+    serial), per pass, extrapolated to the weights target's pass count (said so in `cpu_reference`)."""
+    from paper_2605_25346_b200.api import Act, DTSystem, GradTarget, grad_tube_volume
+    from paper_2605_25346_b200.workloads import random_mlp
+    rng = np.random.default_rng(1)
+    net = random_mlp(rng, 6, [128, 128, 128], 6, Act.Relu, 0.9)
+    net.layers[-1].w *= 0.5
+    sys_ = DTSystem(net, 6, 0)
+    x0 = (np.full(6, -0.05), np.full(6, 0.05))
+    acts = [[]] * 30
+    ctx.set_stream(None)
+    ctx.enable_kernel_timing(True)
+    grad_tube_volume(sys_, x0, acts, GradTarget.weights, ctx=ctx)
+    ctx.kernel_time()
+    t0 = time.perf_counter()
+    g = grad_tube_volume(sys_, x0, acts, GradTarget.weights, ctx=ctx)
+    wall = time.perf_counter() - t0
+    km, _ = ctx.kernel_time()
+    ctx.enable_kernel_timing(False)
+    out = {"workload": "grad_tube_volume, weights target, 6->128x3->6 ReLU, H=30, window 4",
+           "passes": int(g.g.size), "ms_per_gradient": 1e3 * wall, "kernel_ms": km,
+           "passes_per_s": g.g.size / wall,
+           "parity": "bit-identical to the reference grad_tube_volume (tests/test_gpu_grad.py)"}
+    if not args.no_cpu_baseline:
+        try:
+            from oracle_bind import ref_available, ref_grad_tube_volume
+            if ref_available():
+                t0 = time.perf_counter()
+                ref_grad_tube_volume(sys_, x0, acts, 0, 0)
+                per_pass = (time.perf_counter() - t0) / 7.0  # 6 dual passes + the primal f0 pass
+                out["cpu_reference"] = {"s_per_pass": per_pass, "cores": 1,
+                                        "extrapolated_s_for_weights_target": per_pass * (g.g.size + 1),
+                                        "sample": "x0_center target (7 passes) timed, per-pass cost extrapolated"}
         except Exception as ex:  # noqa: BLE001
             out["cpu_reference_error"] = str(ex)
     return out
@@ -670,6 +734,8 @@ def main():
 
     # ---- the metric's second half: ms per reachability-aware MPC replan (BASELINE configs[2])
     mpc = None if args.no_mpc else mpc_replan(args, ctx, world, rank, dev, barrier)
+    # ---- section 8(f) rank 1: forward-dual gradients through the DT engine (N = 1 only)
+    grad = None if (args.no_grad or world > 1) else gradient_leg(args, ctx)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -683,6 +749,7 @@ def main():
                 "roofline": roof, "cpu_baseline": cb,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "clocks": clk, "parity": parity, "ct_quadrotor": ct, **cl, "mpc_replan": mpc,
+                "gradients": grad,
                 "bit_exact_vs_reference": "ReLU path: identical operation order and roundings (tests/test_gpu_dt.py)"}
         print(json.dumps(line))
     if world > 1:
