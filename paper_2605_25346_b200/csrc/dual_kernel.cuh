@@ -89,7 +89,7 @@ struct Work {
     D rel[3][kW];       // crown: relaxation (slope, lower, upper intercept) of the current layer
   };
   D lam[2][kN][kW];     // Lambda, double buffered
-  D blo[kN], bup[kN], bf0[kW];
+  D blo[kN], bup[kN], shift[kN], bf0[kW];
   D oc[kN];
   D oA[kN][kZ];
   DI orem[kN];
@@ -198,7 +198,14 @@ __device__ __forceinline__ int certify_d(const NetView& net, int n, int nz, Work
     const int rows = N.dims[t + 1], cols = (t == 0) ? n : N.dims[t];
     for (int u = tid; u < rows; u += kThreads) {
       DI acc{dc(0.0), dc(0.0)};
-      for (int j = 0; j < cols; ++j) acc = iadd(acc, iscale(net.wt(t, u, j), W.hb[cur][j]));
+      if (net.sl != t) {
+        const double* wrow = net.N.blob + net.N.wt_off[t] + u;
+        const int ld = net.N.ldt[t];
+#pragma unroll 4
+        for (int j = 0; j < cols; ++j) acc = iadd(acc, iscale(dc(wrow[static_cast<long long>(j) * ld]), W.hb[cur][j]));
+      } else {
+        for (int j = 0; j < cols; ++j) acc = iadd(acc, iscale(net.wt(t, u, j), W.hb[cur][j]));
+      }
       const D bias = (t == 0) ? W.bf0[u] : net.b(t, u);
       acc = iadd(acc, DI{bias, bias});
       W.pre[t][u] = acc;
@@ -235,50 +242,71 @@ __device__ __forceinline__ int certify_d(const NetView& net, int n, int nz, Work
       __syncthreads();
       if (W.bad) return 1;
     }
-    // per output row i: the relaxation intercepts (ascending j), Lambda *= s,
-    // then shift = matvec(Lambda, b) (linalg.hpp:40-51, 65-71)
-    for (int i = tid; i < n_o; i += kThreads) {
-      if (act != REACH_ACT_IDENTITY) {
-        D lo = W.blo[i], up = W.bup[i];
+    // per output row i: the relaxation intercepts (ascending j) into b_lo / b_up, Lambda *= s, then
+    // shift = matvec(Lambda_s, b) (linalg.hpp:40-51, 65-71) added to both.  The three chains of a row
+    // are independent sequences, so they run on three different warps (lo: warp 0, up: warp 1, shift:
+    // warp 2, which forms Lambda_s entries itself -- the same products), while the other warps write
+    // Lambda_s into the spare buffer; each chain keeps the reference's order.
+    const int src = (act != REACH_ACT_IDENTITY) ? (lb ^ 1) : lb;  // the buffer holding Lambda_s
+    const int dst = src ^ 1;
+    {
+      const int wi = tid >> 5, ln = tid & 31;
+      if (act != REACH_ACT_IDENTITY && wi < 2 && ln < n_o) {
+        const int i = ln;
+        D acc = (wi == 0) ? W.blo[i] : W.bup[i];
         for (int j = 0; j < acols; ++j) {
           const D aij = W.lam[lb][i][j];
-          if (aij.v >= 0.0) {
-            lo = dadd(lo, dmul(aij, W.rel[1][j]));
-            up = dadd(up, dmul(aij, W.rel[2][j]));
-          } else {
-            lo = dadd(lo, dmul(aij, W.rel[2][j]));
-            up = dadd(up, dmul(aij, W.rel[1][j]));
-          }
-          W.lam[lb][i][j] = dmul(aij, W.rel[0][j]);
+          const bool pos = aij.v >= 0.0;
+          // lower bound takes li for Lambda >= 0 (ui otherwise); upper bound the opposite
+          const D r = W.rel[(pos == (wi == 0)) ? 1 : 2][j];
+          acc = dadd(acc, dmul(aij, r));
         }
-        W.blo[i] = lo;
-        W.bup[i] = up;
+        if (wi == 0) W.blo[i] = acc;
+        else W.bup[i] = acc;
+      } else if (wi == 2 && ln < n_o) {
+        const int i = ln;
+        D acc = dc(0.0);
+        for (int j = 0; j < acols; ++j) {
+          const D bj = (l == 0) ? W.c[j] : (t == 0 ? W.bf0[j] : net.b(t, j));
+          const D a = (act != REACH_ACT_IDENTITY) ? dmul(W.lam[lb][i][j], W.rel[0][j]) : W.lam[lb][i][j];
+          acc = dadd(acc, dmul(a, bj));
+        }
+        W.shift[i] = acc;
+      } else if (act != REACH_ACT_IDENTITY && wi >= 3) {
+        for (int e = tid - 96; e < n_o * acols; e += kThreads - 96) {
+          const int i = e / acols, j = e % acols;
+          W.lam[src][i][j] = dmul(W.lam[lb][i][j], W.rel[0][j]);
+        }
       }
-      D acc = dc(0.0);
-      for (int j = 0; j < acols; ++j) {
-        const D bj = (l == 0) ? W.c[j] : (t == 0 ? W.bf0[j] : net.b(t, j));
-        acc = dadd(acc, dmul(W.lam[lb][i][j], bj));
-      }
-      W.blo[i] = dadd(W.blo[i], acc);
-      W.bup[i] = dadd(W.bup[i], acc);
     }
     __syncthreads();
-    // Lambda = matmul(Lambda, W_l) (linalg.hpp:53-63): element (i, j) sums k ascending, one thread per
+    if (tid < n_o) {
+      W.blo[tid] = dadd(W.blo[tid], W.shift[tid]);
+      W.bup[tid] = dadd(W.bup[tid], W.shift[tid]);
+    }
+    // Lambda = matmul(Lambda_s, W_l) (linalg.hpp:53-63): element (i, j) sums k ascending, one thread per
     // element (consecutive threads = consecutive columns: coalesced W rows, Lambda entries broadcast).
     // (Measured: one thread per column with all rows' chains in registers is 13 % slower.)
     for (int e = tid; e < n_o * cols; e += kThreads) {
       const int i = e / cols, j = e % cols;
       D acc = dc(0.0);
-      for (int k = 0; k < acols; ++k) {
-        D wkj;
-        if (l == 0) wkj = (j < nz) ? W.S[k][j] : dc(j - nz == k ? 1.0 : 0.0);
-        else wkj = net.w(t, k, j);
-        acc = dadd(acc, dmul(W.lam[lb][i][k], wkj));
+      if (l == 0) {
+        for (int k = 0; k < acols; ++k) {
+          const D wkj = (j < nz) ? W.S[k][j] : dc(j - nz == k ? 1.0 : 0.0);
+          acc = dadd(acc, dmul(W.lam[src][i][k], wkj));
+        }
+      } else if (net.sl != t) {  // no seeded parameter in this layer: plain constant weights
+        const double* wcol = net.N.blob + net.N.w_off[t] + j;
+        const int ld = net.N.ldw[t];
+#pragma unroll 4
+        for (int k = 0; k < acols; ++k) acc = dadd(acc, dmul(W.lam[src][i][k], dc(wcol[static_cast<long long>(k) * ld])));
+      } else {
+        for (int k = 0; k < acols; ++k) acc = dadd(acc, dmul(W.lam[src][i][k], net.w(t, k, j)));
       }
-      W.lam[lb ^ 1][i][j] = acc;
+      W.lam[dst][i][j] = acc;
     }
     __syncthreads();
-    lb ^= 1;
+    lb = dst;
     acols = cols;
   }
   // tail (neural.hpp:383-391)
