@@ -274,6 +274,12 @@ enum reach_grad_target { REACH_GRAD_X0_CENTER = 0, REACH_GRAD_ACTIONS = 1, REACH
 enum reach_grad_method { REACH_GRAD_FORWARD_DUAL = 0, REACH_GRAD_FINITE_DIFFERENCE = 1 };
 int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
                            int32_t method, double* grad, int32_t* subgradient, double* volume);
+/* The passes of parameters [param_begin, param_end) only (param_end = -1: to the end); grad receives that
+ * slice.  Multi-GPU drivers shard the parameters over ranks and all-gather the slices (the passes are
+ * independent); the subgradient flag and the volume are per call. */
+int reach_grad_tube_volume_range(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
+                                 int32_t method, int64_t param_begin, int64_t param_end, double* grad,
+                                 int32_t* subgradient, double* volume);
 
 /* mpc_run (mpc.hpp:373-495): receding-horizon execution.  MPCConfig (mpc.hpp:373-387). */
 typedef struct reach_mpc_config {

@@ -22,6 +22,8 @@
 //   PlanResult / plan_objective / plan_cem      PlanResult / plan_objective(_batch) / plan_cem
 //   grad_forward(plan_objective) (refine.hpp)   reach_b200::plan_objective_grad
 //   MPCConfig / MPCResult / mpc_run (mpc.hpp)   reach_b200::MPCConfig / MPCResult / mpc_run
+//   reach_loss (+ grad_forward over params)     reach_b200::reach_loss / reach_loss_gradient
+//   gradient_refine of the CLI refine objective reach_b200::refine_tube_volume
 //   GradTarget / GradMethod / Gradient /        reach_b200::GradTarget / GradMethod / Gradient /
 //   grad_tube_volume (refine.hpp:165-311)       grad_tube_volume
 //
@@ -793,6 +795,84 @@ inline Gradient grad_tube_volume(Context& ctx, const DTSystem& sys, const Box& x
   out.g.resize(dim);
   out.subgradient = sub != 0;
   return out;
+}
+
+// reach_loss (training.hpp:99-126) over episodes given by their start states [M][n] and first t_h
+// actions [M][t_h][m]; grad != nullptr also returns its gradient over the model's parameters
+// (net_params order), the training objective's grad_forward.
+inline double reach_loss(Context& ctx, const MLPNet& model, const std::vector<std::vector<double>>& x0s,
+                         const std::vector<std::vector<std::vector<double>>>& actions, double eps, double cap,
+                         int* diverged_count = nullptr, const DTReachParams& prm = {},
+                         std::vector<double>* grad = nullptr) {
+  model.validate();
+  const int M = static_cast<int>(x0s.size());
+  if (M == 0 || actions.size() != x0s.size() || actions.front().empty())
+    throw std::invalid_argument("reach_loss: bad batch/horizon");
+  const int n = static_cast<int>(x0s.front().size()), t_h = static_cast<int>(actions.front().size());
+  const int m = static_cast<int>(actions.front().front().size());
+  std::vector<double> x(static_cast<size_t>(M) * n), a(static_cast<size_t>(M) * t_h * m);
+  for (int e = 0; e < M; ++e) {
+    if (static_cast<int>(x0s[e].size()) != n || static_cast<int>(actions[e].size()) != t_h)
+      throw std::invalid_argument("reach_loss: ragged batch");
+    std::copy(x0s[e].begin(), x0s[e].end(), x.begin() + static_cast<size_t>(e) * n);
+    for (int t = 0; t < t_h; ++t) {
+      if (static_cast<int>(actions[e][t].size()) != m) throw std::invalid_argument("reach_loss: action dims");
+      std::copy(actions[e][t].begin(), actions[e][t].end(), a.begin() + (static_cast<size_t>(e) * t_h + t) * m);
+    }
+  }
+  size_t np = 0;
+  for (const auto& L : model.layers) np += L.w.size() + L.b.size();
+  if (grad) grad->assign(np, 0.0);
+  reach_dt_args args{M, t_h, n, m, prm.window, prm.rebuild_from_box ? 1 : 0, x.data(), x.data(),
+                     a.empty() ? nullptr : a.data(), 0};
+  double loss = 0.0;
+  int32_t dc = 0;
+  ctx.check(reach_reach_loss(ctx.raw(), ctx.upload(model), &args, M, eps, cap, &loss, grad ? grad->data() : nullptr,
+                             &dc),
+            "reach_loss");
+  if (diverged_count) *diverged_count += dc;
+  return loss;
+}
+
+struct RefineResult {  // refine.hpp:333-340
+  std::vector<double> x;
+  double initial_objective = 0.0, objective = 0.0;
+  bool progressed = false, subgradient = false;
+  int accepted_steps = 0;
+};
+
+// gradient_refine (refine.hpp:354-398) of tube_volume(dt_reach(box_from_center(c, radius), actions))
+// over the X0 centre or the flat action sequence within [lo, hi] -- the reference CLI's `refine`.
+inline RefineResult refine_tube_volume(Context& ctx, const DTSystem& sys, const std::vector<double>& center,
+                                       const std::vector<double>& radius,
+                                       const std::vector<std::vector<double>>& actions, GradTarget target,
+                                       const std::vector<double>& x0, const std::vector<double>& lo,
+                                       const std::vector<double>& hi, int iters = 20,
+                                       const DTReachParams& prm = {}) {
+  sys.validate();
+  const int n = sys.n, m = sys.m, H = static_cast<int>(actions.size());
+  std::vector<double> acts;
+  for (const auto& u : actions) {
+    if (static_cast<int>(u.size()) != m) throw std::invalid_argument("dt_reach: action dimension mismatch");
+    acts.insert(acts.end(), u.begin(), u.end());
+  }
+  const size_t d = target == GradTarget::x0_center ? static_cast<size_t>(n) : acts.size();
+  if (center.size() != static_cast<size_t>(n) || radius.size() != static_cast<size_t>(n) || x0.size() != d ||
+      lo.size() != d || hi.size() != d)
+    throw std::invalid_argument("gradient_refine: bound dimension mismatch");
+  RefineResult r;
+  r.x = x0;
+  int32_t pr = 0, sb = 0, ac = 0;
+  reach_dt_args a{1, H, n, m, prm.window, prm.rebuild_from_box ? 1 : 0, center.data(), center.data(),
+                  acts.empty() ? nullptr : acts.data(), 0};
+  ctx.check(reach_refine_tube_volume(ctx.raw(), ctx.upload(sys.step), &a, center.data(), radius.data(),
+                                     static_cast<int32_t>(target), lo.data(), hi.data(), iters, r.x.data(),
+                                     &r.initial_objective, &r.objective, &pr, &sb, &ac),
+            "gradient_refine");
+  r.progressed = pr != 0;
+  r.subgradient = sb != 0;
+  r.accepted_steps = ac;
+  return r;
 }
 
 }  // namespace reach_b200

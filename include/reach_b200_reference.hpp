@@ -20,6 +20,7 @@
 #include "reach/mpc.hpp"
 #include "reach/refine.hpp"
 #include "reach/systems.hpp"
+#include "reach/training.hpp"
 #include "reach_b200.hpp"
 
 namespace reach_b200 {
@@ -255,6 +256,44 @@ inline reach::MPCResult mpc_run(Context& ctx, const reach::PlanProblem& prob, co
     out.log.push_back(std::move(q));
   }
   return out;
+}
+
+// reach::reach_loss (training.hpp:99-126) on the device; reach_loss_gradient = grad_forward of it over
+// net_params(model) (what train_dt_dyn differentiates), one launch over parameters x episodes.
+namespace detail {
+inline void episodes_to_arrays(const std::vector<reach::Episode>& batch, int t_h,
+                               std::vector<std::vector<double>>& x0s,
+                               std::vector<std::vector<std::vector<double>>>& acts) {
+  if (batch.empty() || t_h < 1) throw std::invalid_argument("reach_loss: bad batch/horizon");
+  for (const auto& ep : batch) {
+    if (ep.length() < t_h) throw std::invalid_argument("reach_loss: episode shorter than T_h");
+    x0s.push_back(ep.states.front());
+    acts.emplace_back(ep.actions.begin(), ep.actions.begin() + t_h);
+  }
+}
+}  // namespace detail
+
+inline double reach_loss(Context& ctx, const reach::MLPNet<double>& model, const std::vector<reach::Episode>& batch,
+                         double eps, int t_h, double cap, int* diverged_count = nullptr,
+                         const reach::DTReachParams& prm = {}) {
+  std::vector<std::vector<double>> x0s;
+  std::vector<std::vector<std::vector<double>>> acts;
+  detail::episodes_to_arrays(batch, t_h, x0s, acts);
+  return reach_loss(ctx, from_reference(model), x0s, acts, eps, cap, diverged_count,
+                    DTReachParams{prm.window, prm.rebuild_from_box});
+}
+
+inline reach::Gradient reach_loss_gradient(Context& ctx, const reach::MLPNet<double>& model,
+                                           const std::vector<reach::Episode>& batch, double eps, int t_h,
+                                           double cap, const reach::DTReachParams& prm = {}) {
+  std::vector<std::vector<double>> x0s;
+  std::vector<std::vector<std::vector<double>>> acts;
+  detail::episodes_to_arrays(batch, t_h, x0s, acts);
+  reach::Gradient g;
+  reach_loss(ctx, from_reference(model), x0s, acts, eps, cap, nullptr, DTReachParams{prm.window, prm.rebuild_from_box},
+             &g.g);
+  g.method = reach::GradMethod::forward_dual;
+  return g;
 }
 
 }  // namespace reach_b200

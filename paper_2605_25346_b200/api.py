@@ -285,7 +285,7 @@ class Gradient:  # refine.hpp:171-178
 
 def grad_tube_volume(sys: DTSystem, x0, actions: Sequence, target: GradTarget,
                      method: GradMethod = GradMethod.forward_dual, prm: DTReachParams = DTReachParams(),
-                     ctx: Optional[Context] = None) -> Gradient:
+                     ctx: Optional[Context] = None, param_range: Optional[tuple] = None) -> Gradient:
     """grad_tube_volume (refine.hpp:263-311): d tube_volume(dt_reach(...)) / d target, x0 = (lo, hi).
     Parameter layouts: x0_center [n]; actions [H*m] step-major; weights in net_params order
     (neural.hpp:133-140).  Every pass (one per parameter, two per parameter for finite differences)
@@ -299,16 +299,19 @@ def grad_tube_volume(sys: DTSystem, x0, actions: Sequence, target: GradTarget,
     H = len(actions)
     acts = _actions_array([actions], 1, H, sys.m).reshape(-1)
     target, method = GradTarget(target), GradMethod(method)
-    dim = {GradTarget.x0_center: sys.n, GradTarget.actions: H * sys.m,
-           GradTarget.weights: int(sys.step.params().size)}[target]
+    full = {GradTarget.x0_center: sys.n, GradTarget.actions: H * sys.m,
+            GradTarget.weights: int(sys.step.params().size)}[target]
+    begin, end = (0, full) if param_range is None else (int(param_range[0]), int(param_range[1]))
+    dim = max(end - begin, 0)
     g = np.zeros(max(dim, 1))
     sub = np.zeros(1, np.int32)
     vol = np.zeros(1)
     args = A.DTArgs(1, H, sys.n, sys.m, prm.window, int(prm.rebuild_from_box), A.dptr(lo), A.dptr(hi),
                     A.dptr(acts if acts.size else np.zeros(1)), 0)
     net = ctx.upload(sys.step)
-    ctx.check(ctx._lib.reach_grad_tube_volume(ctx.handle, net, C.byref(args), int(target), int(method), A.dptr(g),
-                                              A.iptr(sub), A.dptr(vol)), "grad_tube_volume")
+    ctx.check(ctx._lib.reach_grad_tube_volume_range(ctx.handle, net, C.byref(args), int(target), int(method),
+                                                    begin, end, A.dptr(g), A.iptr(sub), A.dptr(vol)),
+              "grad_tube_volume")
     return Gradient(g[:dim].copy(), method, bool(sub[0]), float(vol[0]))
 
 

@@ -698,7 +698,8 @@ struct VolArgs {
   const double* center;   // [n]  box_center(x0)
   const double* radius;   // [n]  box_radius(x0)
   const double* actions;  // [H*m]
-  int target, dim, fd;
+  int target, dim, fd;  // dim = the passes' parameter count (a slice [p0, p0 + dim) of the target)
+  long long p0;
   double rel_step;
   long long poff[kMaxLayers + 1];  // net_params offset of each layer's W (then its b)
   double* value;          // [passes] tube volume (primal) seen by each pass
@@ -715,10 +716,10 @@ __global__ void __launch_bounds__(kThreads, 2) tube_volume_grad_kernel(const Vol
   int p = -1;
   double delta = 0.0, seed = 0.0;
   if (!A.fd) {
-    p = pass;
+    p = static_cast<int>(A.p0 + pass);
     seed = 1.0;
   } else if (pass < 2 * A.dim) {
-    p = pass >> 1;
+    p = static_cast<int>(A.p0 + (pass >> 1));
   }
   NetView net{A.net};
   double x = 0.0;

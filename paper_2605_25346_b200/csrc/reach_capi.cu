@@ -1425,16 +1425,21 @@ namespace {
 // refine objective uses box_from_center(c, eps)); a supplies the shapes, actions and DTReachParams.
 int grad_tube_volume_cr(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, const double* center,
                         const double* radius, int32_t target, int32_t method, double* grad, int32_t* subgradient,
-                        double* volume) {
+                        double* volume, long long begin = 0, long long end = -1) {
   namespace rd = rb::dual;
   const int n = a->n, m = a->m, H = a->horizon;
   rd::VolArgs V{};
   V.poff[0] = 0;
   for (int l = 0; l < net->L; ++l)
     V.poff[l + 1] = V.poff[l] + static_cast<long long>(net->dims[l + 1]) * net->dims[l] + net->dims[l + 1];
-  const long long dim = target == REACH_GRAD_X0_CENTER ? n
-                        : target == REACH_GRAD_ACTIONS ? static_cast<long long>(H) * m
-                                                       : V.poff[net->L];
+  const long long full = target == REACH_GRAD_X0_CENTER ? n
+                         : target == REACH_GRAD_ACTIONS ? static_cast<long long>(H) * m
+                                                        : V.poff[net->L];
+  if (end < 0) end = full;
+  if (begin < 0 || begin > end || end > full)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: parameter range out of bounds");
+  const long long dim = end - begin;  // this call's slice of the parameters
+  V.p0 = begin;
   const bool fd = method == REACH_GRAD_FINITE_DIFFERENCE;
   const long long passes = fd ? 2 * dim + 1 : dim;
   if (passes > (1ll << 30)) return fail(ctx, REACH_E_UNSUPPORTED, "grad_tube_volume: too many parameters");
@@ -1506,12 +1511,13 @@ int grad_tube_volume_cr(reach_ctx* ctx, const reach_net* net, const reach_dt_arg
       if (!std::isfinite(fp) || !std::isfinite(fm))
         return fail(ctx, REACH_E_NONFINITE, "grad_fd: objective non-finite near x");
       double xj;  // the parameter value, for h (refine.hpp:222)
+      const long long pj = begin + j;
       if (target == REACH_GRAD_X0_CENTER) {
-        xj = center[j];
+        xj = center[pj];
       } else if (target == REACH_GRAD_ACTIONS) {
-        xj = a->actions[j];
+        xj = a->actions[pj];
       } else {
-        xj = net->params[static_cast<size_t>(j)];  // net_params order == the upload's flat order
+        xj = net->params[static_cast<size_t>(pj)];  // net_params order == the upload's flat order
       }
       const double h = 1e-5 * std::max(1.0, std::abs(xj));
       grad[j] = (fp - fm) / (2.0 * h);
@@ -1526,6 +1532,12 @@ extern "C" {
 
 int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
                            int32_t method, double* grad, int32_t* subgradient, double* volume) {
+  return reach_grad_tube_volume_range(ctx, net, a, target, method, 0, -1, grad, subgradient, volume);
+}
+
+int reach_grad_tube_volume_range(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
+                                 int32_t method, int64_t param_begin, int64_t param_end, double* grad,
+                                 int32_t* subgradient, double* volume) {
   namespace rd = rb::dual;
   if (!ctx || !net || !a || !grad) return REACH_E_INVALID_ARGUMENT;
   if (a->batch != 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: batch must be 1");
@@ -1551,7 +1563,8 @@ int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_
     radius[i] = (a->x0_hi[i] - a->x0_lo[i]) * 0.5;
     if (radius[i] < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "box_from_center: negative radius");
   }
-  return grad_tube_volume_cr(ctx, net, a, center.data(), radius.data(), target, method, grad, subgradient, volume);
+  return grad_tube_volume_cr(ctx, net, a, center.data(), radius.data(), target, method, grad, subgradient, volume,
+                             param_begin, param_end);
 }
 
 // mpc_run (mpc.hpp:425-495): receding-horizon execution around plan_cem.

@@ -148,3 +148,38 @@ def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = N
     best, best_obj, best_effort, hist = cem.result()
     fin, _ = evaluate(prob, x0, best[None])
     return best, float(fin[0]), best_effort, hist
+
+
+def sharded_grad_tube_volume(sys, x0, actions, target, method=0, prm=None, group=None,
+                             evaluate: Optional[Callable] = None):
+    """grad_tube_volume (refine.hpp:263-311) over all ranks: the parameters (one forward-dual pass, or two
+    central-difference passes, each -- independent) are split into contiguous slices, each rank runs its
+    slice's passes in one launch, one all-gather assembles the gradient; the subgradient flag is OR-ed.
+    evaluate(sys, x0, actions, target, method, prm, begin, end) -> (g_slice, subgradient)."""
+    import torch
+    from .api import DTReachParams, GradMethod, GradTarget, Gradient, grad_tube_volume
+    dist = _dist()
+    prm = prm or DTReachParams()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    target = GradTarget(target)
+    full = {GradTarget.x0_center: sys.n, GradTarget.actions: len(actions) * sys.m,
+            GradTarget.weights: int(sys.step.params().size)}[target]
+    b, e = shard_range(full, rank, world)
+    if evaluate is None:
+        def evaluate(s_, x_, a_, t_, m_, p_, b_, e_):
+            g = grad_tube_volume(s_, x_, a_, t_, m_, p_, param_range=(b_, e_))
+            return g.g, g.subgradient
+    g_slice, sub = evaluate(sys, x0, actions, target, method, prm, b, e)
+    dev = _device_for(group)
+    width = max(shard_range(full, r, world)[1] - shard_range(full, r, world)[0] for r in range(world))
+    buf = torch.zeros(width + 1, dtype=torch.float64, device=dev)
+    buf[: e - b] = torch.from_numpy(np.ascontiguousarray(g_slice, dtype=np.float64))
+    buf[width] = 1.0 if sub else 0.0
+    outs = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf, group=group)
+    parts, any_sub = [], False
+    for r, o in enumerate(outs):
+        rb_, re_ = shard_range(full, r, world)
+        parts.append(o[: re_ - rb_].cpu().numpy())
+        any_sub = any_sub or bool(o[width].item() != 0.0)
+    return Gradient(np.concatenate(parts) if parts else np.zeros(0), GradMethod(method), any_sub)

@@ -12,6 +12,7 @@
 #include "reach/mpc.hpp"
 #include "reach/refine.hpp"
 #include "reach/rng.hpp"
+#include "reach/training.hpp"
 #include "reach_b200_reference.hpp"
 
 using namespace reach;
@@ -300,6 +301,30 @@ int main() {
     if (ref.log_to_csv() != got.log_to_csv() || ref.success != got.success || ref.violated != got.violated ||
         ref.steps_used != got.steps_used || ref.final_state != got.final_state) {
       std::printf("mpc_run: mismatch\n");
+      ++failures;
+    }
+  }
+  // reach_loss and its parameter gradient (training.hpp:99-126 under grad_forward): gradient
+  // bit-identical, loss within 1e-14 (CUDA log)
+  {
+    Rng r5(12);
+    MLPNet<double> model = random_mlp(r5, 4, {16}, 2, Act::Relu, 0.6);
+    std::vector<Episode> batch(3);
+    for (auto& ep : batch) {
+      ep.states.assign(5, Vec<double>{r5.uniform(-0.4, 0.4), r5.uniform(-0.4, 0.4)});
+      for (int t = 0; t < 4; ++t) ep.actions.push_back({r5.uniform(-0.5, 0.5), r5.uniform(-0.5, 0.5)});
+    }
+    int d1 = 0, d2 = 0;
+    const double l1 = reach::reach_loss(model, batch, 0.05, 3, 50.0, &d1);
+    const double l2 = reach_b200::reach_loss(gpu, model, batch, 0.05, 3, 50.0, &d2);
+    auto f = [&](const auto& p) {
+      using S = typename std::decay_t<decltype(p)>::value_type;
+      return reach::reach_loss(net_with_params<S>(model, p), batch, 0.05, 3, 50.0);
+    };
+    auto gref = grad_forward(f, net_params(model));
+    auto ggot = reach_b200::reach_loss_gradient(gpu, model, batch, 0.05, 3, 50.0);
+    if (std::fabs(l1 - l2) > 1e-14 * std::fabs(l1) || d1 != d2 || gref.g != ggot.g) {
+      std::printf("reach_loss: mismatch (%.17g / %.17g)\n", l1, l2);
       ++failures;
     }
   }

@@ -64,7 +64,21 @@ def _worker(rank, world, port, q):
         spec, clo, chi, cplan = ct_split_case()
         ch = sharded_cl_split_hull(spec, (clo, chi), cplan,
                                    evaluate=lambda s_, x_, p_, b_, e_: oracle_cl_split_hull(s_, x_[0], x_[1], p_, b_, e_))
-        q.put((rank, h.lo, h.hi, h.n_boxes, h.fail_key, best, obj, be, hist, ch.lo, ch.hi, ch.n_boxes, ch.fail_key))
+        # grad_tube_volume sharded over the parameters (the slices come from the reference here)
+        from grad_cases import grad_cases
+        from oracle_bind import ref_available, ref_grad_tube_volume
+        from paper_2605_25346_b200.distributed import sharded_grad_tube_volume
+        gsys = gx0 = gacts = None
+        gw = None
+        if ref_available():
+            _, gsys, gx0, gacts, gprm, _ = grad_cases()[2]
+
+            def ev_grad(s_, x_, a_, t_, m_, p_, b_, e_):
+                g, sub = ref_grad_tube_volume(s_, x_, a_, int(t_), int(m_), p_)
+                return g[b_:e_], sub
+            gw = sharded_grad_tube_volume(gsys, gx0, gacts, 2, 0, gprm, evaluate=ev_grad).g
+        q.put((rank, h.lo, h.hi, h.n_boxes, h.fail_key, best, obj, be, hist, ch.lo, ch.hi, ch.n_boxes, ch.fail_key,
+               gw))
     finally:
         dist.destroy_process_group()
 
@@ -99,7 +113,15 @@ def test_two_rank_gloo_sharding_matches_single_process():
     from oracle_bind import oracle_cl_split_hull
     spec, clo, chi, cplan = ct_split_case()
     cfull = oracle_cl_split_hull(spec, clo, chi, cplan)
-    for rank, lo, hi, nb, key, best, obj, be, hist, clo_r, chi_r, cnb, ckey in outs:
+    from grad_cases import grad_cases
+    from oracle_bind import ref_available, ref_grad_tube_volume
+    gfull = None
+    if ref_available():
+        _, gsys, gx0, gacts, gprm, _ = grad_cases()[2]
+        gfull = ref_grad_tube_volume(gsys, gx0, gacts, 2, 0, gprm)[0]
+    for rank, lo, hi, nb, key, best, obj, be, hist, clo_r, chi_r, cnb, ckey, gw in outs:
+        if gfull is not None:  # weights gradient assembled from two ranks' parameter slices
+            assert same_bits(gw, gfull)
         k = full.n_boxes
         assert nb == full.n_boxes and key == full.fail_key
         assert same_bits(lo[:k], full.lo[:k]) and same_bits(hi[:k], full.hi[:k])

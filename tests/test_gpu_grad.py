@@ -100,3 +100,17 @@ def test_refine_tube_volume_matches_reference(target):
     assert same_bits(got.x, exp[0])
     assert (got.initial_objective, got.objective, got.progressed, got.subgradient, got.accepted_steps) == exp[1:]
     assert got.objective <= got.initial_objective
+
+
+@pytest.mark.parametrize("method", [GradMethod.forward_dual, GradMethod.finite_difference])
+def test_parameter_slices_assemble_the_full_gradient(method):
+    """reach_grad_tube_volume_range (the multi-GPU shard unit): slices concatenate to the full gradient."""
+    name, sys, x0, acts, prm, _ = grad_cases()[2]
+    full = grad_tube_volume(sys, x0, acts, GradTarget.weights, method, prm)
+    dim = full.g.size
+    cuts = [0, 7, dim // 2, dim - 3, dim]
+    parts = [grad_tube_volume(sys, x0, acts, GradTarget.weights, method, prm, param_range=(b, e)).g
+             for b, e in zip(cuts[:-1], cuts[1:])]
+    assert same_bits(np.concatenate(parts), full.g)
+    with pytest.raises(ValueError):
+        grad_tube_volume(sys, x0, acts, GradTarget.weights, method, prm, param_range=(5, dim + 1))
