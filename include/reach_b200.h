@@ -255,6 +255,12 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
                       const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
                       double* best_history, int32_t* best_effort, int32_t* refined, const reach_tube_out* final_tube);
 
+/* plan_cem's refinement step alone (mpc.hpp:337-361): gradient_refine of the plan objective from
+ * best_actions [H][m] (the CEM result, objective best_objective), replaced in place when the refined
+ * objective is lower; refined = PlanResult::refined.  For drivers running the CEM in pieces. */
+int reach_plan_refine(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
+                      int32_t refine_iters, double best_objective, double* best_actions, int32_t* refined);
+
 /* grad_forward (refine.hpp:186-207) of plan_objective (mpc.hpp:204-208) over
  * the flat action sequence [H][m]: one reach::Dual pass per direction, all
  * directions in one launch.  grad [H*m]; objective (optional) = the primal. */

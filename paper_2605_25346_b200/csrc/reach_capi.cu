@@ -1256,6 +1256,90 @@ int reach_cem_result(const reach_cem* c, double* best_actions, double* best_obje
   return REACH_OK;
 }
 
+// gradient_refine (refine.hpp:347-398) of plan_objective from best_actions (the CEM's top candidate,
+// objective best_obj): forward-dual gradients on the device, batched Armijo trials; best_actions is
+// replaced when the refined objective is lower (mpc.hpp:337-361).
+static int plan_refine_impl(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
+                            int iters, double best_obj, double* best_actions, int32_t* refined) {
+  int rc = REACH_OK;
+  {
+    const size_t d = static_cast<size_t>(prob->horizon) * prob->m;
+    std::vector<double> lo(d), hi(d), x(best_actions, best_actions + d), g(d), xn(d);
+    for (size_t k = 0; k < d; ++k) {
+      lo[k] = prob->u_lo[k % prob->m];
+      hi[k] = prob->u_hi[k % prob->m];
+    }
+    auto project = [&](std::vector<double>& v) {
+      for (size_t k = 0; k < d; ++k) v[k] = std::clamp(v[k], lo[k], hi[k]);
+    };
+    auto f = [&](const std::vector<double>& v, double& out) {
+      int32_t dv2 = 0;
+      return plan_eval_host(ctx, net, prob, x0, 1, v.data(), &out, &dv2, nullptr);
+    };
+    project(x);
+    double fx = 0.0;
+    rc = f(x, fx);
+    if (rc) return rc;
+    if (!std::isfinite(fx)) return fail(ctx, REACH_E_NONFINITE, "gradient_refine: initial objective non-finite");
+    int accepted_steps = 0;
+    std::vector<double> cands, fvals;
+    std::vector<int32_t> cdiv;
+    for (int it = 0; it < iters; ++it) {
+      // grad_forward's primal pass (refine.hpp:190-193) re-evaluates f(x) = fx, finite by construction
+      // (checked above or accepted below): evaluation is deterministic, so it is not repeated here
+      double v = 0.0;
+      bool fin = true;
+      rc = plan_grad_device(ctx, net, prob, x0, x.data(), g.data(), &v, &fin);
+      if (rc) return rc;
+      if (!fin) return fail(ctx, REACH_E_NONFINITE, "grad_forward: non-finite derivative");
+      double gnorm2 = 0.0;
+      for (size_t k = 0; k < d; ++k) gnorm2 += g[k] * g[k];
+      if (gnorm2 == 0.0) break;
+      // Armijo backtracking (RefineParams: step0 1, shrink 0.5, armijo 1e-4, 30 backtracks).  The trial
+      // points do not depend on earlier trials' objectives, so every trial up to the first one that does not
+      // move is evaluated in ONE batch on the device and the first accepted trial is taken in order --
+      // the same point the reference's sequential loop accepts.
+      cands.clear();
+      std::vector<double> moved_v;
+      double t = 1.0;
+      for (int bt = 0; bt < 30; ++bt, t *= 0.5) {
+        for (size_t k = 0; k < d; ++k) xn[k] = x[k] - t * g[k];
+        project(xn);
+        double moved = 0.0;
+        for (size_t k = 0; k < d; ++k) moved += g[k] * (x[k] - xn[k]);
+        if (moved <= 0.0) break;
+        cands.insert(cands.end(), xn.begin(), xn.end());
+        moved_v.push_back(moved);
+      }
+      const int nt = static_cast<int>(moved_v.size());
+      bool accepted = false;
+      if (nt > 0) {
+        fvals.assign(nt, 0.0);
+        cdiv.assign(nt, 0);
+        rc = plan_eval_host(ctx, net, prob, x0, nt, cands.data(), fvals.data(), cdiv.data(), nullptr);
+        if (rc) return rc;
+        for (int q = 0; q < nt; ++q) {
+          const double fn = fvals[q];
+          if (std::isfinite(fn) && fn <= fx - 1e-4 * moved_v[q]) {
+            std::copy(cands.begin() + static_cast<size_t>(q) * d, cands.begin() + static_cast<size_t>(q + 1) * d,
+                      x.begin());
+            fx = fn;
+            accepted = true;
+            ++accepted_steps;
+            break;
+          }
+        }
+      }
+      if (!accepted) break;
+    }
+    if (fx < best_obj) {
+      std::copy(x.begin(), x.end(), best_actions);
+      if (refined) *refined = accepted_steps > 0 ? 1 : 0;
+    }
+  }
+  return REACH_OK;
+}
+
 int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
                       const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
                       double* best_history, int32_t* best_effort, int32_t* refined, const reach_tube_out* final_tube) {
@@ -1317,79 +1401,8 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
   // gradient refinement of the top candidate (mpc.hpp:337-361):
   // gradient_refine (refine.hpp:347-398) with forward-dual gradients on the device
   if (cfg->refine_iters > 0 && std::isfinite(best_obj)) {
-    const size_t d = dim;
-    std::vector<double> lo(d), hi(d), x(best_actions, best_actions + d), g(d), xn(d);
-    for (size_t k = 0; k < d; ++k) {
-      lo[k] = prob->u_lo[k % prob->m];
-      hi[k] = prob->u_hi[k % prob->m];
-    }
-    auto project = [&](std::vector<double>& v) {
-      for (size_t k = 0; k < d; ++k) v[k] = std::clamp(v[k], lo[k], hi[k]);
-    };
-    auto f = [&](const std::vector<double>& v, double& out) {
-      int32_t dv2 = 0;
-      return plan_eval_host(ctx, net, prob, x0, 1, v.data(), &out, &dv2, nullptr);
-    };
-    project(x);
-    double fx = 0.0;
-    rc = f(x, fx);
+    rc = plan_refine_impl(ctx, net, prob, x0, cfg->refine_iters, best_obj, best_actions, refined);
     if (rc) return rc;
-    if (!std::isfinite(fx)) return fail(ctx, REACH_E_NONFINITE, "gradient_refine: initial objective non-finite");
-    int accepted_steps = 0;
-    std::vector<double> cands, fvals;
-    std::vector<int32_t> cdiv;
-    for (int it = 0; it < cfg->refine_iters; ++it) {
-      // grad_forward's primal pass (refine.hpp:190-193) re-evaluates f(x) = fx, finite by construction
-      // (checked above or accepted below): evaluation is deterministic, so it is not repeated here
-      double v = 0.0;
-      bool fin = true;
-      rc = plan_grad_device(ctx, net, prob, x0, x.data(), g.data(), &v, &fin);
-      if (rc) return rc;
-      if (!fin) return fail(ctx, REACH_E_NONFINITE, "grad_forward: non-finite derivative");
-      double gnorm2 = 0.0;
-      for (size_t k = 0; k < d; ++k) gnorm2 += g[k] * g[k];
-      if (gnorm2 == 0.0) break;
-      // Armijo backtracking (RefineParams: step0 1, shrink 0.5, armijo 1e-4, 30 backtracks).  The trial
-      // points do not depend on earlier trials' objectives, so every trial up to the first one that does not
-      // move is evaluated in ONE batch on the device and the first accepted trial is taken in order --
-      // the same point the reference's sequential loop accepts.
-      cands.clear();
-      std::vector<double> moved_v;
-      double t = 1.0;
-      for (int bt = 0; bt < 30; ++bt, t *= 0.5) {
-        for (size_t k = 0; k < d; ++k) xn[k] = x[k] - t * g[k];
-        project(xn);
-        double moved = 0.0;
-        for (size_t k = 0; k < d; ++k) moved += g[k] * (x[k] - xn[k]);
-        if (moved <= 0.0) break;
-        cands.insert(cands.end(), xn.begin(), xn.end());
-        moved_v.push_back(moved);
-      }
-      const int nt = static_cast<int>(moved_v.size());
-      bool accepted = false;
-      if (nt > 0) {
-        fvals.assign(nt, 0.0);
-        cdiv.assign(nt, 0);
-        rc = plan_eval_host(ctx, net, prob, x0, nt, cands.data(), fvals.data(), cdiv.data(), nullptr);
-        if (rc) return rc;
-        for (int q = 0; q < nt; ++q) {
-          const double fn = fvals[q];
-          if (std::isfinite(fn) && fn <= fx - 1e-4 * moved_v[q]) {
-            std::copy(cands.begin() + static_cast<size_t>(q) * d, cands.begin() + static_cast<size_t>(q + 1) * d,
-                      x.begin());
-            fx = fn;
-            accepted = true;
-            ++accepted_steps;
-            break;
-          }
-        }
-      }
-      if (!accepted) break;
-    }
-    if (fx < best_obj) {
-      std::copy(x.begin(), x.end(), best_actions);
-      if (refined) *refined = accepted_steps > 0 ? 1 : 0;
-    }
   }
   // final evaluation of the chosen plan (mpc.hpp:363-367)
   int32_t dv = 0;
@@ -1947,6 +1960,18 @@ int reach_reach_loss(reach_ctx* ctx, const reach_net* net, const reach_dt_args* 
     *diverged_count = c;
   }
   return REACH_OK;
+}
+
+// The refinement step of plan_cem alone (mpc.hpp:337-361), for drivers that run the CEM loop in pieces.
+int reach_plan_refine(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
+                      int32_t refine_iters, double best_objective, double* best_actions, int32_t* refined) {
+  if (!ctx || !net || !prob || !x0 || !best_actions) return REACH_E_INVALID_ARGUMENT;
+  if (refine_iters < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "SamplerConfig: invalid configuration");
+  int rc = validate_problem(ctx, net, prob);
+  if (rc) return rc;
+  if (refined) *refined = 0;
+  if (refine_iters == 0 || !std::isfinite(best_objective)) return REACH_OK;
+  return plan_refine_impl(ctx, net, prob, x0, refine_iters, best_objective, best_actions, refined);
 }
 
 }  // extern "C"

@@ -115,13 +115,18 @@ def sharded_cl_split_hull(spec, x0, plan, group=None, evaluate: Optional[Callabl
     return allreduce_hull(evaluate(spec, x0, plan, b, e), group)
 
 
-def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = None):
+def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = None,
+                     refine: Optional[Callable] = None):
     """plan_cem (mpc.hpp:258-368) over all ranks; returns (actions, objective, best_effort, history).
 
     Every rank draws the full population (same stream), evaluates its slice,
-    and all-gathers (objective, ok) -- identical selection on every rank."""
+    and all-gathers (objective, ok) -- identical selection on every rank.  The top
+    candidate's gradient refinement (refine_iters > 0) is deterministic, so every rank
+    runs it on its own device (no collective) and all ranks keep the same plan."""
+    import dataclasses
+
     import torch
-    from .mpc import CEM, plan_eval_batch
+    from .mpc import CEM, plan_eval_batch, plan_refine
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     dev = _device_for(group)
@@ -129,7 +134,7 @@ def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = N
         def evaluate(prob_, x0_, acts_):
             r = plan_eval_batch(prob_, x0_, acts_)
             return r.objective, r.diverged
-    cem = CEM(prob, cfg)
+    cem = CEM(prob, dataclasses.replace(cfg, refine_iters=0))
     pop = cfg.population
     b, e = shard_range(pop, rank, world)
     sizes = [shard_range(pop, r, world) for r in range(world)]
@@ -146,6 +151,11 @@ def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = N
         ok = np.concatenate([g[: hi - lo, 1].cpu().numpy() for g, (lo, hi) in zip(gathered, sizes)]) > 0.5
         cem.update(scores, ok.astype(np.int32))
     best, best_obj, best_effort, hist = cem.result()
+    if cfg.refine_iters > 0 and np.isfinite(best_obj):
+        if refine is None:
+            def refine(prob_, x0_, acts_, obj_, iters_):
+                return plan_refine(prob_, x0_, acts_, obj_, iters_)[0]
+        best = refine(prob, x0, best, best_obj, cfg.refine_iters)
     fin, _ = evaluate(prob, x0, best[None])
     return best, float(fin[0]), best_effort, hist
 

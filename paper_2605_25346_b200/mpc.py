@@ -195,6 +195,22 @@ def plan_objective_grad(prob: PlanProblem, x0, actions, ctx: Optional[Context] =
     return g, float(obj[0])
 
 
+def plan_refine(prob: PlanProblem, x0, actions, best_objective: float, refine_iters: int = 5,
+                ctx: Optional[Context] = None):
+    """plan_cem's refinement step (mpc.hpp:337-361) alone -> (actions, refined): gradient_refine of the
+    plan objective from `actions` (objective best_objective) with forward-dual gradients on the device."""
+    prob.sys.validate()
+    ctx = ctx or default_context()
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    acts = np.ascontiguousarray(np.asarray(actions, np.float64).reshape(prob.horizon, prob.sys.m)).copy()
+    rf = np.zeros(1, np.int32)
+    p, keep = prob.c_struct()
+    net = ctx.upload(prob.sys.step)
+    ctx.check(ctx._lib.reach_plan_refine(ctx.handle, net, C.byref(p), A.dptr(x0), int(refine_iters),
+                                         float(best_objective), A.dptr(acts), A.iptr(rf)), "plan_refine")
+    return acts, bool(rf[0])
+
+
 def plan_cem(prob: PlanProblem, cfg: SamplerConfig, x0, ctx: Optional[Context] = None) -> PlanResult:
     """plan_cem (mpc.hpp:258-368), including the top-candidate gradient refinement."""
     prob.sys.validate()

@@ -63,3 +63,35 @@ def test_plan_cem_refinement_c3_shape_matches_reference():
     r = plan_cem(prob, cfg, x0)
     assert same_bits(r.actions, eb) and r.objective == eo and same_bits(r.best_history, eh)
     assert r.best_effort == ebe and r.refined == erf
+
+
+def test_refine_step_alone_equals_plan_cem_refinement():
+    """reach_plan_refine (the step the sharded CEM runs after its all-gathered loop) reproduces plan_cem."""
+    from paper_2605_25346_b200.mpc import plan_refine
+    prob, cfg, x0 = small_cem()
+    r0 = plan_cem(prob, cfg, x0)
+    r5 = plan_cem(prob, dataclasses.replace(cfg, refine_iters=5), x0)
+    acts, refined = plan_refine(prob, x0, r0.actions, r0.objective, 5)
+    assert same_bits(acts, r5.actions) and refined == r5.refined
+
+
+def test_sharded_plan_cem_with_refinement_one_rank():
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2605_25346_b200.distributed import sharded_plan_cem
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        prob, cfg, x0 = small_cem()
+        cfg = dataclasses.replace(cfg, refine_iters=5)
+        best, obj, be, hist = sharded_plan_cem(prob, cfg, x0)
+        r = plan_cem(prob, cfg, x0)
+        assert same_bits(best, r.actions) and obj == r.objective and same_bits(hist, r.best_history)
+    finally:
+        dist.destroy_process_group()
