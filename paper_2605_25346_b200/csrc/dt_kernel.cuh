@@ -306,6 +306,33 @@ __device__ __forceinline__ int popc_below(const unsigned* mask, int x) {
   return c;
 }
 
+// popc_below over a per-layer mask held in registers: the CPL words and their prefix counts are read
+// once per layer, so the per-chunk row counts need no shared-memory round trips.
+template <int CPL>
+struct MaskCount {
+  unsigned w[CPL];
+  int below[CPL];
+  __device__ __forceinline__ explicit MaskCount(const unsigned* mask) {
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      w[q] = mask[q];
+      below[q] = c;
+      c += __popc(w[q]);
+    }
+  }
+  // number of set bits below bit x (0 <= x <= 32 * CPL)
+  __device__ __forceinline__ int count(int x) const {
+    const int q = x >> 5, r = x & 31;
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+      if (k == q) c = below[k] + (r ? __popc(w[k] & ((1u << r) - 1u)) : 0);
+    if (q >= CPL) c = below[CPL - 1] + __popc(w[CPL - 1]);
+    return c;
+  }
+};
+
 // Two-deep software pipeline over the rows of `it`: the operands of the next
 // row are loaded before the current row's arithmetic is issued, so shared-
 // memory latency hides behind the FP64 work of the previous row.
@@ -433,12 +460,13 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
     };
     const int rpc = rows_per_chunk(ld, SD);
     int t = 0;
+    const MaskCount<CPL> imc(l > 0 ? in_mask : S.masks);
     for (int r0 = 0; r0 < rows; r0 += rpc) {
       const double* ch = stages + ws_in.acquire() * SD;
       const int nr = min(rpc, rows - r0);
       if (!done) {
         if (l > 0) {
-          const int t1 = popc_below(in_mask, r0 + nr);
+          const int t1 = imc.count(r0 + nr);
 #pragma unroll 2
           for (; t < t1; ++t) ibp_row(ch, r0, in_list[t]);
         } else {
@@ -622,11 +650,12 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) acc[i][cc] = 0.0;
       int t = 0;
+      const MaskCount<CPL> amc(am);
       for (int r0 = 0; r0 < width; r0 += rpc) {
         const double* ch = stages + ws_in.acquire() * SD;
         const int nr = min(rpc, width - r0);
         if (!done) {
-          const int t1 = popc_below(am, r0 + nr);
+          const int t1 = amc.count(r0 + nr);
 #pragma unroll 2
           for (; t < t1; ++t) {
             const int kk = alist[t];
@@ -681,11 +710,12 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
       const int i1 = (p1 < npair ? p1 : 0) / n_i, j1 = (p1 < npair ? p1 : 0) % n_i;
       double a0 = 0.0, a1 = 0.0;
       int t = 0;
+      const MaskCount<CPL> amc(am);
       for (int r0 = 0; r0 < width; r0 += rpc) {
         const double* ch = stages + ws_in.acquire() * SD;
         const int nr = min(rpc, width - r0);
         if (!done) {
-          const int t1 = popc_below(am, r0 + nr);
+          const int t1 = amc.count(r0 + nr);
 #pragma unroll 4
           for (; t < t1; ++t) {
             const int kk = alist[t];
