@@ -114,3 +114,24 @@ def test_parameter_slices_assemble_the_full_gradient(method):
     assert same_bits(np.concatenate(parts), full.g)
     with pytest.raises(ValueError):
         grad_tube_volume(sys, x0, acts, GradTarget.weights, method, prm, param_range=(5, dim + 1))
+
+
+def test_refine_zero_gradient_start_returns_input_unchanged():
+    """test_refine.cpp:286-299 on the tube-volume objective: the identity map's volume does not depend on
+    the centre, so the gradient is exactly zero and gradient_refine stops without moving."""
+    from paper_2605_25346_b200.api import refine_tube_volume
+    sys_, _, x0 = identity_case()
+    c = np.array([0.4, -0.3])
+    r = refine_tube_volume(sys_, c, 0.2, [[]] * 4, GradTarget.x0_center, c - 1.0, c + 1.0, iters=5)
+    assert not r.progressed and r.accepted_steps == 0
+    assert r.objective == r.initial_objective and same_bits(r.x, c)
+
+
+def test_refine_stays_in_the_box_and_never_worsens():
+    from paper_2605_25346_b200.api import refine_tube_volume
+    name, sys_, x0, acts, prm, _ = grad_cases()[2]
+    c = (x0[0] + x0[1]) * 0.5
+    lo, hi = c - 0.05, c + 0.05
+    r = refine_tube_volume(sys_, c, 0.08, acts, GradTarget.x0_center, lo, hi, iters=10)
+    assert r.objective <= r.initial_objective
+    assert np.all(r.x >= lo) and np.all(r.x <= hi)
