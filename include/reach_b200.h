@@ -212,6 +212,13 @@ int reach_net_free(reach_ctx* ctx, reach_net* net);
 int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* args,
                    const reach_tube_out* out, int32_t flags);
 
+/* dt_interval_baseline (dt_reach.hpp:129-149): the naive per-step interval tube of the same one-step map
+ * (freeze the action, interval_forward the box), the CLI's `reach-dt --baseline interval`.  Same
+ * arguments and tube layout as reach_dt_batch (host pointers). */
+int reach_dt_interval_baseline_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a,
+                                     const reach_tube_out* out);
+
+
 /* DT closed loop (the cl_reach stacking of closed_loop.hpp:
  * 118-153 on a discrete-time one-step network): per step u = ctl_crown(x_tm,
  * ctl) (neural.hpp:418), the symbolic state is stacked to [x; u] over the shared

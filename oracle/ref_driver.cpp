@@ -927,3 +927,30 @@ extern "C" int ref_reach_loss(const reach_net_desc* desc, int32_t n, int32_t m, 
   }
   return REACH_OK;
 }
+
+// reach::dt_interval_baseline (dt_reach.hpp:129-149) per sample; same layout as ref_dt_batch.
+extern "C" int ref_dt_interval_baseline_batch(const reach_net_desc* desc, const reach_dt_args* a,
+                                              const reach_tube_out* out) {
+  try {
+    DTSystem<double> sys = make_sys(desc, a->n, a->m);
+    const int H = a->horizon, n = a->n, m = a->m;
+    for (int b = 0; b < a->batch; ++b) {
+      const double* act = a->actions_shared ? a->actions : a->actions + static_cast<size_t>(b) * H * m;
+      ReachTube<double> tube = dt_interval_baseline(
+          sys, box_at(a->x0_lo + static_cast<size_t>(b) * n, a->x0_hi + static_cast<size_t>(b) * n, n),
+          actions_at(act, H, m));
+      out->n_boxes[b] = tube.steps();
+      out->failed_step[b] = tube.failed_step;
+      out->status[b] = status_of(tube);
+      for (int k = 0; k < tube.steps(); ++k)
+        for (int d = 0; d < n; ++d) {
+          size_t o = (static_cast<size_t>(b) * (H + 1) + k) * n + d;
+          out->lo[o] = tube.boxes[static_cast<size_t>(k)][d].lo;
+          out->hi[o] = tube.boxes[static_cast<size_t>(k)][d].hi;
+        }
+    }
+  } catch (const std::exception&) {
+    return REACH_E_INVALID_ARGUMENT;
+  }
+  return REACH_OK;
+}

@@ -47,6 +47,8 @@ def _declare(lib):
     lib.reach_net_upload.argtypes = [vp, C.POINTER(A.NetDesc), C.POINTER(vp)]
     lib.reach_net_free.argtypes = [vp, vp]
     lib.reach_dt_batch.argtypes = [vp, vp, C.POINTER(A.DTArgs), C.POINTER(A.TubeOut), C.c_int32]
+    lib.reach_dt_interval_baseline_batch.argtypes = [vp, vp, C.POINTER(A.DTArgs), C.POINTER(A.TubeOut)]
+    lib.reach_dt_interval_baseline_batch.restype = C.c_int
     lib.reach_split_hull.argtypes = [vp, vp, C.POINTER(A.SplitArgs), C.POINTER(A.HullOut), C.c_int32]
     lib.reach_dtcl_batch.argtypes = [vp, vp, vp, C.POINTER(A.DTArgs), C.POINTER(A.TubeOut), C.c_int32]
     lib.reach_dtcl_batch.restype = C.c_int

@@ -242,6 +242,41 @@ def dt_reach_batch_arrays(sys: DTSystem, x0_lo: np.ndarray, x0_hi: np.ndarray, a
     return out
 
 
+def dt_interval_baseline_batch_arrays(sys: DTSystem, x0_lo: np.ndarray, x0_hi: np.ndarray, actions: np.ndarray,
+                                      ctx: Optional[Context] = None, actions_shared: bool = False) -> TubeBatch:
+    """dt_interval_baseline (dt_reach.hpp:129-149) on arrays, one tube per row: the naive interval tube."""
+    sys.validate()
+    ctx = ctx or default_context()
+    x0_lo = np.ascontiguousarray(x0_lo, dtype=np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, dtype=np.float64)
+    B = x0_lo.shape[0]
+    if x0_lo.shape != (B, sys.n) or x0_hi.shape != (B, sys.n):
+        raise ValueError("dt_reach: X0 dimension mismatch")
+    actions = np.ascontiguousarray(actions, dtype=np.float64)
+    H = actions.shape[0] if actions_shared else actions.shape[1]
+    if actions.shape[-1] != sys.m and not (sys.m == 0 and actions.size == 0):
+        raise ValueError("dt_reach: action dimension mismatch")
+    out = TubeBatch(np.full((B, H + 1, sys.n), np.nan), np.full((B, H + 1, sys.n), np.nan),
+                    np.zeros(B, np.int32), np.zeros(B, np.int32), np.zeros(B, np.int32))
+    args = A.DTArgs(B, H, sys.n, sys.m, 0, 0, A.dptr(x0_lo), A.dptr(x0_hi),
+                    A.dptr(actions if actions.size else np.zeros(1)), int(actions_shared))
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step),
+                   A.iptr(out.status))
+    net = ctx.upload(sys.step)
+    ctx.check(ctx._lib.reach_dt_interval_baseline_batch(ctx.handle, net, C.byref(args), C.byref(to)),
+              "dt_interval_baseline")
+    return out
+
+
+def dt_interval_baseline(sys: DTSystem, x0, actions: Sequence, ctx: Optional[Context] = None) -> ReachTube:
+    """dt_interval_baseline (dt_reach.hpp:129-149): x0 = (lo, hi)."""
+    H = len(actions)
+    acts = _actions_array([actions], 1, H, sys.m)
+    lo = np.asarray(x0[0], np.float64).reshape(1, -1)
+    hi = np.asarray(x0[1], np.float64).reshape(1, -1)
+    return dt_interval_baseline_batch_arrays(sys, lo, hi, acts, ctx).tube(0)
+
+
 def dt_reach_batch(sys: DTSystem, x0s: Sequence, action_seqs: Sequence, prm: DTReachParams = DTReachParams(),
                    ctx: Optional[Context] = None) -> List[ReachTube]:
     """dt_reach_batch (dt_reach.hpp:108-125): x0s = [(lo, hi), ...], action_seqs = [[u_0..u_{H-1}], ...]."""

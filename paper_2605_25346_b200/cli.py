@@ -19,7 +19,7 @@ from typing import List, Tuple
 import numpy as np
 
 from . import formats as F
-from .api import (DTSystem, FlowpipeParams, ClosedLoopSpec, GradTarget, QuadrotorParams, SplitPlan, box_from_center,
+from .api import (DTSystem, FlowpipeParams, dt_interval_baseline, ClosedLoopSpec, GradTarget, QuadrotorParams, SplitPlan, box_from_center,
                   cl_reach, ct_reach, ct_reach_with_splitting, diag_linear_field, dt_reach, quadrotor_field,
                   quadrotor_hover_input, reach_with_splitting, refine_tube_volume, rotation_field)
 
@@ -81,9 +81,9 @@ def make_field(name: str):
     raise ConfigError('unknown system "' + name + '" (known: quadrotor, swarm, arm, rotation, decay)')
 
 
-def _unsupported_modes(cfg: dict):
-    if cfg.get("baseline", "") == "interval":
-        raise ConfigError("the interval baselines (baseline.hpp) are not part of the device build")
+def _unsupported_modes(cfg: dict, dt: bool = False):
+    if cfg.get("baseline", "") == "interval" and not dt:
+        raise ConfigError("the continuous-time interval baseline (baseline.hpp) is not part of the device build")
     if cfg.get("sound_rounding", False):
         raise ConfigError("outward rounding is not supported by the device kernels")
 
@@ -143,10 +143,16 @@ def cmd_reach_dt(cfg: dict, out_dir: str) -> int:
     else:
         actions = [[0.0] * m for _ in range(int(cfg.get("steps", 10)))]
     x0 = box_from_center(center, float(cfg.get("eps", 0.0)))
-    _unsupported_modes(cfg)
+    _unsupported_modes(cfg, dt=True)
+    baseline = cfg.get("baseline", "") == "interval"
     split = cfg.get("split", "")
-    tube = dt_reach(sys_, x0, actions) if not split else reach_with_splitting(sys_, x0, make_split_plan(split, n),
-                                                                              actions)
+    if baseline and split:
+        raise ConfigError("--baseline interval with --split: the split engine is dt_reach on the device")
+    if baseline:
+        tube = dt_interval_baseline(sys_, x0, actions)
+    else:
+        tube = dt_reach(sys_, x0, actions) if not split else reach_with_splitting(sys_, x0,
+                                                                                  make_split_plan(split, n), actions)
     out = Outputs()
     emit_tube(out, tube, False)
     return finish("reach-dt", cfg, out_dir, out, tube.diverged, tube.failure_reason)

@@ -214,4 +214,118 @@ __global__ void model_step_kernel(const DevNet N, const double* xu, double* out,
   for (int j = threadIdx.x; j < N.dims[N.L]; j += blockDim.x) out[j] = a[j];
 }
 
+// dt_interval_baseline (dt_reach.hpp:129-149): per step, freeze_trailing_inputs (neural.hpp:398-413)
+// then interval_forward (neural.hpp:261-272: box_affine_image, + bias, act_interval) of the box; the
+// naive tightness baseline.  One warp per sample; lane o owns output rows o, o + 32, ... of a layer,
+// each a sequential iv_add(iv_scale) chain over the inputs as the reference's.
+struct IBLArgs {
+  DevNet net;
+  int B, H, n, m, maxw;
+  const double* x0_lo;    // [B][n]
+  const double* x0_hi;
+  const double* actions;  // [B][H][m] (or [H][m] shared)
+  int actions_shared;
+  double* out_lo;         // [B][H+1][n]
+  double* out_hi;
+  int* n_boxes;
+  int* failed_step;
+  int* status;
+};
+
+constexpr int kIblWarps = 8;
+
+__global__ void __launch_bounds__(kIblWarps * 32) interval_baseline_kernel(const IBLArgs A) {
+  extern __shared__ __align__(16) double ibl[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kIblWarps + warp;
+  if (b >= A.B) return;
+  const DevNet& N = A.net;
+  const int n = A.n, m = A.m, W = A.maxw;
+  double* lo0 = ibl + static_cast<size_t>(warp) * 4 * W;  // ping-pong boxes + the frozen first-layer bias
+  double* hi0 = lo0 + W;
+  double* lo1 = hi0 + W;
+  double* hi1 = lo1 + W;
+  double* bf = ibl + static_cast<size_t>(kIblWarps) * 4 * W + static_cast<size_t>(warp) * W;
+  const double* acts = A.actions + (A.actions_shared ? 0 : static_cast<size_t>(b) * A.H * m);
+  double* olo = A.out_lo + static_cast<size_t>(b) * (A.H + 1) * n;
+  double* ohi = A.out_hi + static_cast<size_t>(b) * (A.H + 1) * n;
+  for (int i = lane; i < n; i += 32) {
+    lo0[i] = A.x0_lo[static_cast<size_t>(b) * n + i];
+    hi0[i] = A.x0_hi[static_cast<size_t>(b) * n + i];
+    olo[i] = lo0[i];
+    ohi[i] = hi0[i];
+  }
+  __syncwarp();
+  int nb = 1, fs = -1, st = 0;
+  for (int k = 0; k < A.H; ++k) {
+    // freeze_trailing_inputs: b'_i = b_i + sum_j W(i, n + j) u_j (j ascending)
+    const double* u = acts + static_cast<size_t>(k) * m;
+    for (int i = lane; i < N.dims[1]; i += 32) {
+      const double* w = N.blob + N.w_off[0] + static_cast<size_t>(i) * N.ldw[0];
+      double bi = N.blob[N.b_off[0] + i];
+      for (int j = 0; j < m; ++j) bi = add(bi, mul(w[n + j], u[j]));
+      bf[i] = bi;
+    }
+    __syncwarp();
+    double *hl = lo0, *hh = hi0, *ol = lo1, *oh = hi1;
+    for (int l = 0; l < N.L; ++l) {
+      const int rows = N.dims[l + 1], cols = (l == 0) ? n : N.dims[l];
+      const int act = N.acts[l];
+      for (int i = lane; i < rows; i += 32) {
+        const double* w = N.blob + N.w_off[l] + static_cast<size_t>(i) * N.ldw[l];
+        double al = 0.0, ah = 0.0;  // box_affine_image: acc = iv_add(acc, iv_scale(W(i, j), x_j))
+        for (int j = 0; j < cols; ++j) {
+          const double a = w[j];
+          const bool pos = a >= 0.0;
+          al = add(al, mul(a, pos ? hl[j] : hh[j]));
+          ah = add(ah, mul(a, pos ? hh[j] : hl[j]));
+        }
+        const double bb = (l == 0) ? bf[i] : N.blob[N.b_off[l] + i];
+        double pl = add(al, bb), ph = add(ah, bb);  // iv_add(p, [b, b])
+        if (act == 0) {  // act_interval: std::max(x, 0.0)
+          pl = (pl < 0.0) ? 0.0 : pl;
+          ph = (ph < 0.0) ? 0.0 : ph;
+        } else if (act == 1) {
+          pl = tanh(pl);
+          ph = tanh(ph);
+        }
+        ol[i] = pl;
+        oh[i] = ph;
+      }
+      __syncwarp();
+      double* t0 = hl;
+      double* t1 = hh;
+      hl = ol;
+      hh = oh;
+      ol = t0;
+      oh = t1;
+    }
+    bool fin = true;
+    for (int i = lane; i < n; i += 32) {
+      olo[static_cast<size_t>(k + 1) * n + i] = hl[i];
+      ohi[static_cast<size_t>(k + 1) * n + i] = hh[i];
+      fin = fin && finite(hl[i]) && finite(hh[i]);
+    }
+    fin = __all_sync(0xffffffffu, fin);
+    nb = k + 2;
+    if (!fin) {  // tube.mark_failed(k, "diverged box")
+      fs = k;
+      st = 3;
+      break;
+    }
+    if (hl != lo0) {  // keep the box in the (lo0, hi0) slot for the next step
+      for (int i = lane; i < n; i += 32) {
+        lo0[i] = hl[i];
+        hi0[i] = hh[i];
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    A.n_boxes[b] = nb;
+    A.failed_step[b] = fs;
+    A.status[b] = st;
+  }
+}
+
 }  // namespace rb

@@ -1974,4 +1974,68 @@ int reach_plan_refine(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
   return plan_refine_impl(ctx, net, prob, x0, refine_iters, best_objective, best_actions, refined);
 }
 
+// dt_interval_baseline (dt_reach.hpp:129-149) for a batch: the naive interval tube of the same map.
+int reach_dt_interval_baseline_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a,
+                                     const reach_tube_out* out) {
+  if (!ctx || !net || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach_batch: negative size");
+  int rc = validate_system(ctx, net, a->n, a->m);
+  if (rc) return rc;
+  if (a->batch == 0) return REACH_OK;
+  const size_t B = a->batch, H = a->horizon, n = a->n, m = a->m;
+  int maxw = 0;
+  for (int l = 0; l <= net->L; ++l) maxw = std::max(maxw, net->dims[l]);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t act_bytes = (a->actions_shared ? 1 : B) * H * m * 8, box_bytes = B * (H + 1) * n * 8;
+  const size_t o_xl = take(B * n * 8), o_xh = take(B * n * 8), o_a = take(act_bytes), o_ol = take(box_bytes),
+               o_oh = take(box_bytes), o_nb = take(B * 4), o_fs = take(B * 4), o_st = take(B * 4);
+  rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  RB_CUDA(cudaMemcpyAsync(Dp(o_xl), a->x0_lo, B * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_xh), a->x0_hi, B * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (act_bytes) RB_CUDA(cudaMemcpyAsync(Dp(o_a), a->actions, act_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  rb::IBLArgs A{};
+  A.net = net->dev;
+  A.B = static_cast<int>(B);
+  A.H = static_cast<int>(H);
+  A.n = static_cast<int>(n);
+  A.m = static_cast<int>(m);
+  A.maxw = maxw;
+  A.x0_lo = Dp(o_xl);
+  A.x0_hi = Dp(o_xh);
+  A.actions = Dp(o_a);
+  A.actions_shared = a->actions_shared;
+  A.out_lo = Dp(o_ol);
+  A.out_hi = Dp(o_oh);
+  A.n_boxes = reinterpret_cast<int*>(w + o_nb);
+  A.failed_step = reinterpret_cast<int*>(w + o_fs);
+  A.status = reinterpret_cast<int*>(w + o_st);
+  const size_t smem = static_cast<size_t>(rb::kIblWarps) * 5 * maxw * sizeof(double);
+  RB_CUDA(cudaFuncSetAttribute(rb::interval_baseline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  rb::interval_baseline_kernel<<<static_cast<unsigned>((B + rb::kIblWarps - 1) / rb::kIblWarps),
+                                 rb::kIblWarps * 32, smem, ctx->stream>>>(A);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  RB_CUDA(cudaMemcpyAsync(out->lo, Dp(o_ol), box_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(out->hi, Dp(o_oh), box_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(out->n_boxes, w + o_nb, B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(out->failed_step, w + o_fs, B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(out->status, w + o_st, B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return REACH_OK;
+}
+
 }  // extern "C"

@@ -468,3 +468,20 @@ def ref_reach_loss(model, x0s, actions, eps, cap, prm=DTReachParams(), with_grad
            A.iptr(dc))
     assert rc == 0, rc
     return float(loss[0]), g, int(dc[0])
+
+
+def ref_dt_interval_baseline_batch(sys, x0_lo, x0_hi, actions):
+    f = _mpc_fn(ref_lib(), "ref_dt_interval_baseline_batch", [C.POINTER(A.NetDesc), C.POINTER(A.DTArgs),
+                                                              C.POINTER(A.TubeOut)])
+    x0_lo = np.ascontiguousarray(x0_lo, np.float64)
+    x0_hi = np.ascontiguousarray(x0_hi, np.float64)
+    acts = np.ascontiguousarray(actions, np.float64)
+    B, H = x0_lo.shape[0], acts.shape[1]
+    out = TubeBatch(np.full((B, H + 1, sys.n), np.nan), np.full((B, H + 1, sys.n), np.nan),
+                    np.zeros(B, np.int32), np.zeros(B, np.int32), np.zeros(B, np.int32))
+    desc, keep = sys.step.desc()
+    args = A.DTArgs(B, H, sys.n, sys.m, 0, 0, A.dptr(x0_lo), A.dptr(x0_hi), A.dptr(acts if acts.size else np.zeros(1)),
+                    0)
+    to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step), A.iptr(out.status))
+    assert f(C.byref(desc), C.byref(args), C.byref(to)) == 0
+    return out
