@@ -875,4 +875,38 @@ inline RefineResult refine_tube_volume(Context& ctx, const DTSystem& sys, const 
   return r;
 }
 
+// dt_interval_baseline (dt_reach.hpp:129-149): the naive interval tube of the same map.
+inline ReachTube dt_interval_baseline(Context& ctx, const DTSystem& sys, const Box& x0,
+                                      const std::vector<std::vector<double>>& actions) {
+  sys.validate();
+  const int n = sys.n, m = sys.m, H = static_cast<int>(actions.size());
+  if (static_cast<int>(x0.size()) != n) throw std::invalid_argument("dt_reach: X0 dimension mismatch");
+  std::vector<double> lo(n), hi(n), acts;
+  for (int d = 0; d < n; ++d) {
+    lo[d] = x0[d].lo;
+    hi[d] = x0[d].hi;
+  }
+  for (const auto& u : actions) {
+    if (static_cast<int>(u.size()) != m) throw std::invalid_argument("dt_reach: action dimension mismatch");
+    acts.insert(acts.end(), u.begin(), u.end());
+  }
+  std::vector<double> olo(static_cast<size_t>(H + 1) * n), ohi(olo.size());
+  int32_t nb = 0, fs = -1, st = 0;
+  reach_dt_args a{1, H, n, m, 0, 0, lo.data(), hi.data(), acts.empty() ? nullptr : acts.data(), 0};
+  reach_tube_out o{olo.data(), ohi.data(), &nb, &fs, &st};
+  ctx.check(reach_dt_interval_baseline_batch(ctx.raw(), ctx.upload(sys.step), &a, &o), "dt_interval_baseline");
+  ReachTube t;
+  for (int k = 0; k < nb; ++k) {
+    Box box(n);
+    for (int d = 0; d < n; ++d) box[d] = {olo[static_cast<size_t>(k) * n + d], ohi[static_cast<size_t>(k) * n + d]};
+    t.boxes.push_back(std::move(box));
+    t.t_lo.push_back(k);
+    t.t_hi.push_back(k);
+  }
+  t.failed_step = fs;
+  t.diverged = st != REACH_TUBE_OK;
+  t.failure_reason = st != REACH_TUBE_OK ? failure_reason(st) : "";
+  return t;
+}
+
 }  // namespace reach_b200

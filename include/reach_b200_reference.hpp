@@ -296,4 +296,11 @@ inline reach::Gradient reach_loss_gradient(Context& ctx, const reach::MLPNet<dou
   return g;
 }
 
+// reach::dt_interval_baseline (dt_reach.hpp:129-149)
+inline reach::ReachTube<double> dt_interval_baseline(Context& ctx, const reach::DTSystem<double>& sys,
+                                                     const reach::IntervalBox<double>& x0,
+                                                     const std::vector<reach::Vec<double>>& actions) {
+  return to_reference(dt_interval_baseline(ctx, from_reference(sys), from_reference(x0), actions));
+}
+
 }  // namespace reach_b200

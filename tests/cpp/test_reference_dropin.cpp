@@ -328,6 +328,19 @@ int main() {
       ++failures;
     }
   }
+  // dt_interval_baseline (dt_reach.hpp:129-149): bit-identical tube
+  {
+    Rng r6(5);
+    DTSystem<double> sys;
+    sys.n = 3;
+    sys.m = 1;
+    sys.step = random_mlp(r6, 4, {24, 24}, 3, Act::Relu, 0.6);
+    Box x0 = box_from_center<double>({0.1, -0.2, 0.05}, 0.05);
+    std::vector<Vec<double>> acts;
+    for (int k = 0; k < 8; ++k) acts.push_back({r6.uniform(-0.5, 0.5)});
+    failures += compare(reach::dt_interval_baseline(sys, x0, acts), reach_b200::dt_interval_baseline(gpu, sys, x0, acts),
+                        "dt_interval_baseline") ? 1 : 0;
+  }
   std::printf(failures ? "FAIL (%d)\n" : "OK: reference drop-in parity\n", failures);
   return failures ? 1 : 0;
 }
