@@ -50,8 +50,11 @@ struct DTLayout {
   int rd = 0, rc = 0, grid = 0;
 };
 
-constexpr int kStageDoublesDefault = 2048;  // 16 KB bulk-copy stages
-constexpr int kNStageDefault = 6;
+// Two 48 KB bulk-copy stages (double buffering with 48-row chunks of a 128-wide layer): fewer, larger
+// chunks than the earlier 6 x 16 KB ring cut the per-chunk acquire / release / row-count overhead
+// (C4 sweep 116.7 -> 104.1 ms; measured sweep in profiles/r01_c4_summary.md).
+constexpr int kStageDoublesDefault = 6144;
+constexpr int kNStageDefault = 2;
 
 // Weight-stream ring geometry; RB_NSTAGE / RB_STAGE_DOUBLES override it for tuning runs.
 int env_int(const char* name, int dflt, int lo, int hi) {
