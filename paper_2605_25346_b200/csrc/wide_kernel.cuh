@@ -24,8 +24,14 @@
 namespace rb {
 
 constexpr int kWideThreads = 256;
-constexpr int kWideNS = 3;    // cp.async ring stages
-constexpr int kWideRS = 8;    // rows per stage
+#ifndef RB_WIDE_NS
+#define RB_WIDE_NS 3
+#endif
+#ifndef RB_WIDE_RS
+#define RB_WIDE_RS 8
+#endif
+constexpr int kWideNS = RB_WIDE_NS;  // cp.async ring stages
+constexpr int kWideRS = RB_WIDE_RS;  // rows per stage
 constexpr int kWideSW = 256;  // stage row stride (doubles): widest streamed row segment
 constexpr int kWideMaxL = kMaxLayers;
 
