@@ -371,6 +371,14 @@ __device__ __forceinline__ void pipelined_rows(RowIter& it, Load&& load, Comp&& 
 #define RB_MIN_BLOCKS 1
 #endif
 constexpr int kSampleWarps = RB_SAMPLE_WARPS;
+#ifndef RB_GEMM_UNROLL
+#define RB_GEMM_UNROLL 4
+#endif
+#ifndef RB_IBP_UNROLL
+#define RB_IBP_UNROLL 4
+#endif
+constexpr int kGemmUnroll = RB_GEMM_UNROLL;  // row-loop unroll of the Lambda.W contraction
+constexpr int kIbpUnroll = RB_IBP_UNROLL;    // row-loop unroll of the IBP stream
 constexpr int kNZG = 2;  // 32-column groups of a generator matrix (<= 64 columns)
 
 // Per-warp scratch of one certification (shared memory).
@@ -467,11 +475,11 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
       if (!done) {
         if (l > 0) {
           const int t1 = imc.count(r0 + nr);
-#pragma unroll 2
+#pragma unroll kIbpUnroll
           for (; t < t1; ++t) ibp_row(ch, r0, in_list[t]);
         } else {
           const int nx = min(n_i, r0 + nr);
-#pragma unroll 2
+#pragma unroll kIbpUnroll
           for (int j = r0; j < nx; ++j) ibp_row(ch, r0, j);
           // freeze_trailing_inputs (neural.hpp:410): b += W[:, n_i + j] u_j
           for (int r = max(n_i - r0, 0); r < nr; ++r) {
@@ -656,7 +664,7 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
         const int nr = min(rpc, width - r0);
         if (!done) {
           const int t1 = amc.count(r0 + nr);
-#pragma unroll 2
+#pragma unroll kGemmUnroll
           for (; t < t1; ++t) {
             const int kk = alist[t];
             const double* lrow = LT + kk * NOP;
