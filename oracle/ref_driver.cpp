@@ -954,3 +954,42 @@ extern "C" int ref_dt_interval_baseline_batch(const reach_net_desc* desc, const 
   }
   return REACH_OK;
 }
+
+// reach::ctl_reach_loss (training.hpp:183-213) with the quadrotor plant of `sp` and FlowpipeParams
+// sp->fp as fp_base; episodes: start states x0s [M][n], optional y_ref [M][t_h][ref_dim] (has_yref[e]).
+extern "C" int ref_ctl_reach_loss(const reach_net_desc* ctl_desc, const reach_cl_spec* sp, int32_t M,
+                                  const double* x0s, const double* yrefs, const int32_t* has_yref, int32_t ref_dim,
+                                  double eps, int32_t t_h, double delta, double cap, double* loss,
+                                  int32_t* diverged_count) {
+  try {
+    ClosedLoopSpec<double> base = cl_spec_from(ctl_desc, sp);
+    QuadrotorParams prm;
+    prm.mass = sp->plant_params[0];
+    prm.gravity = sp->plant_params[1];
+    prm.jx = sp->plant_params[2];
+    prm.jy = sp->plant_params[3];
+    prm.jz = sp->plant_params[4];
+    auto plant = [prm](const auto& x, const auto& u, auto& dx) { quadrotor_ode(x, u, prm, dx); };
+    std::vector<Episode> batch(static_cast<size_t>(M));
+    for (int e = 0; e < M; ++e) {
+      Episode& ep = batch[static_cast<size_t>(e)];
+      Vec<double> s(x0s + static_cast<size_t>(e) * sp->n, x0s + static_cast<size_t>(e + 1) * sp->n);
+      ep.states.assign(static_cast<size_t>(t_h) + 1, s);
+      ep.actions.assign(static_cast<size_t>(t_h), Vec<double>(static_cast<size_t>(sp->l), 0.0));
+      if (has_yref && has_yref[e])
+        for (int t = 0; t < t_h; ++t) {
+          const double* r = yrefs + (static_cast<size_t>(e) * t_h + t) * ref_dim;
+          ep.y_ref.emplace_back(r, r + ref_dim);
+        }
+    }
+    int dc = 0;
+    *loss = ctl_reach_loss(base.controller, plant, batch, eps, t_h, sp->n, sp->l, delta, sp->k_atomic, cap, &dc,
+                           base.fp);
+    if (diverged_count) *diverged_count = dc;
+  } catch (const std::invalid_argument&) {
+    return REACH_E_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return REACH_E_NONFINITE;
+  }
+  return REACH_OK;
+}

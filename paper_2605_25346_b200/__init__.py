@@ -10,6 +10,6 @@ from .api import (  # noqa: F401
     QuadrotorParams, FlowpipeParams, ClosedLoopSpec, cl_reach, cl_reach_batch_arrays, cl_split_hull,
     cl_reach_with_splitting, AnalyticField, zero_field, diag_linear_field, rotation_field, quadrotor_field,
     quadrotor_hover_input, ct_reach, ct_reach_batch_arrays, ct_split_hull, ct_reach_with_splitting,
-    GradTarget, GradMethod, Gradient, grad_tube_volume, RefineResult, refine_tube_volume, Episode, reach_loss,
+    GradTarget, GradMethod, Gradient, grad_tube_volume, RefineResult, refine_tube_volume, Episode, reach_loss, ctl_reach_loss,
 )
 from ._native import Context, default_context, ReachError, NativeMissing, NonFiniteError, LIB_PATH  # noqa: F401

@@ -27,6 +27,7 @@ ValueError where the reference throws std::invalid_argument.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import enum
 import math
 from dataclasses import dataclass, field
@@ -836,3 +837,52 @@ def ct_reach_with_splitting(f: AnalyticField, x0, plan: SplitPlan, prm: Flowpipe
                             ctx: Optional[Context] = None) -> ReachTube:
     """reach_with_splitting(ct_reach engine, x0, plan) (refine.hpp:121-160)."""
     return ct_split_hull(f, x0, plan, prm, ctx=ctx).tube()
+
+
+def _predicted_volume(lo: np.ndarray, hi: np.ndarray) -> float:
+    """predicted_volume (training.hpp:86-93): box volume proxies of boxes 1.. (the input box excluded)."""
+    v = 0.0
+    for k in range(1, lo.shape[0]):
+        v += box_volume_proxy(lo[k], hi[k])
+    return v
+
+
+def ctl_reach_loss(controller: MLPNet, batch: Sequence[Episode], eps: float, t_h: int, delta: float,
+                   k_atomic: int, cap: float, fp_base: Optional[FlowpipeParams] = None,
+                   plant: Optional[QuadrotorParams] = None, n: int = 12, l: int = 4,
+                   ctx: Optional[Context] = None):
+    """ctl_reach_loss (training.hpp:183-213) value with the quadrotor plant: cl_reach from the eps-ball
+    around each episode start, every tube on the device (episodes sharing a reference sequence in one
+    batch) -> (loss, diverged_count).  As the reference, an episode without y_ref keeps the previous
+    episode's reference sequence."""
+    if not batch or t_h < 1:
+        raise ValueError("ctl_reach_loss: bad batch/horizon")
+    fp = dataclasses.replace(fp_base or FlowpipeParams())
+    fp.h = delta / k_atomic
+    yrefs, cur = [], None
+    for ep in batch:
+        if len(ep.y_ref):
+            cur = np.ascontiguousarray(np.asarray(ep.y_ref[:t_h], np.float64).reshape(t_h, -1))
+        yrefs.append(cur)
+    groups = {}
+    for e, yr in enumerate(yrefs):
+        groups.setdefault(None if yr is None else yr.tobytes(), []).append(e)
+    terms = [0.0] * len(batch)
+    diverged = [False] * len(batch)
+    for key, idx in groups.items():
+        yr = yrefs[idx[0]]
+        spec = ClosedLoopSpec(controller, n=n, l=l, ctl_steps=t_h, k_atomic=k_atomic, y_ref=yr,
+                              fp=dataclasses.replace(fp), plant_params=plant or QuadrotorParams())
+        x0 = np.array([np.asarray(batch[e].states[0], np.float64) for e in idx])
+        tb = cl_reach_batch_arrays(spec, x0 - eps, x0 + eps, ctx)
+        for r, e in enumerate(idx):
+            t = tb.tube(r)
+            if t.diverged:
+                diverged[e] = True
+                terms[e] = cap
+            else:
+                terms[e] = math.log(1.0 + _predicted_volume(t.lo, t.hi))
+    acc = 0.0
+    for v in terms:
+        acc += v
+    return acc / float(len(batch)), int(sum(diverged))

@@ -485,3 +485,26 @@ def ref_dt_interval_baseline_batch(sys, x0_lo, x0_hi, actions):
     to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step), A.iptr(out.status))
     assert f(C.byref(desc), C.byref(args), C.byref(to)) == 0
     return out
+
+
+def ref_ctl_reach_loss(spec, x0s, yrefs, eps, t_h, delta, cap):
+    """The reference's ctl_reach_loss (quadrotor plant, fp_base = spec.fp) -> (loss, diverged_count)."""
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+    f = _mpc_fn(ref_lib(), "ref_ctl_reach_loss", [C.POINTER(A.NetDesc), C.POINTER(A.CLSpecC), C.c_int32, dp, dp, ip,
+                                                 C.c_int32, C.c_double, C.c_int32, C.c_double, C.c_double, dp, ip])
+    x0s = np.ascontiguousarray(x0s, np.float64)
+    M = x0s.shape[0]
+    has = np.array([0 if y is None else 1 for y in yrefs], np.int32)
+    rd = max([np.asarray(y).shape[-1] for y in yrefs if y is not None] or [1])
+    yr = np.zeros((M, t_h, rd))
+    for e, y in enumerate(yrefs):
+        if y is not None:
+            yr[e] = np.asarray(y, np.float64).reshape(t_h, rd)
+    loss = np.zeros(1)
+    dc = np.zeros(1, np.int32)
+    desc, keep = spec.controller.desc()
+    cs, keep2 = spec.c_struct()
+    rc = f(C.byref(desc), C.byref(cs), M, A.dptr(x0s), A.dptr(yr), A.iptr(has), rd, float(eps), t_h, float(delta),
+           float(cap), A.dptr(loss), A.iptr(dc))
+    assert rc == 0, rc
+    return float(loss[0]), int(dc[0])

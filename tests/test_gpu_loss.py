@@ -64,3 +64,39 @@ def test_bad_batch_raises():
     ep = Episode([np.zeros(2)] * 3, [np.zeros(2)] * 2)
     with pytest.raises(ValueError):
         reach_loss(model, [ep], 0.1, 3, 1.0)
+
+
+@needs_ref
+@pytest.mark.parametrize("with_ref", [False, True])
+def test_ctl_reach_loss_matches_reference(with_ref):
+    """ctl_reach_loss (training.hpp:183-213) value: the quadrotor closed loop from each episode start on the
+    device.  CT tubes agree to ~1e-15 relative (CUDA libm in the tanh controller), so the loss within 1e-12."""
+    from oracle_bind import ref_ctl_reach_loss
+    from paper_2605_25346_b200.api import ClosedLoopSpec, FlowpipeParams, ctl_reach_loss
+    from paper_2605_25346_b200.workloads import quadrotor_controller, random_mlp
+    rng = np.random.default_rng(8)
+    if with_ref:
+        ctl = quadrotor_controller(rng, (16, 16))
+    else:
+        ctl = random_mlp(rng, 12, [16, 16], 4, Act.Tanh, 0.4)
+        ctl.layers[-1].w *= 0.1
+        ctl.layers[-1].b[0] += 9.81
+    t_h, k_atomic, delta, eps, cap = 3, 2, 0.02, 0.01, 40.0
+    batch, yrefs, cur = [], [], None
+    for e in range(4):
+        x0 = np.zeros(12)
+        x0[:6] = rng.uniform(-0.05, 0.05, 6)
+        yr = None
+        if with_ref and e != 2:  # episode 2 keeps episode 1's reference (the reference's carry-over)
+            yr = np.tile(rng.uniform(-0.1, 0.1, 3), (t_h, 1))
+        batch.append(Episode([x0] * (t_h + 1), [np.zeros(4)] * t_h, [] if yr is None else list(yr)))
+        cur = yr if yr is not None else cur
+        yrefs.append(cur)
+    loss, dcount = ctl_reach_loss(ctl, batch, eps, t_h, delta, k_atomic, cap)
+    spec = ClosedLoopSpec(ctl, ctl_steps=t_h, k_atomic=k_atomic, fp=FlowpipeParams(h=delta / k_atomic),
+                          y_ref=yrefs[0])
+    el, ed = ref_ctl_reach_loss(spec, np.array([b.states[0] for b in batch]),
+                                [None if not len(b.y_ref) else np.asarray(b.y_ref) for b in batch],
+                                eps, t_h, delta, cap)
+    assert dcount == ed
+    assert abs(loss - el) <= 1e-12 * abs(el), (loss, el)
