@@ -30,6 +30,10 @@ constexpr int kWideThreads = 256;
 #ifndef RB_WIDE_RS
 #define RB_WIDE_RS 8
 #endif
+#ifndef RB_WIDE_UNROLL
+#define RB_WIDE_UNROLL 4
+#endif
+constexpr int kWideUnroll = RB_WIDE_UNROLL;  // unroll of the per-row functor over a full stage
 constexpr int kWideNS = RB_WIDE_NS;  // cp.async ring stages
 constexpr int kWideRS = RB_WIDE_RS;  // rows per stage
 constexpr int kWideSW = 256;  // stage row stride (doubles): widest streamed row segment
@@ -117,7 +121,7 @@ __device__ __forceinline__ void stream_rows(double* stages, const double* base, 
     const int t0 = c * RS;
     const int nr = min(RS, nk - t0);
     if (nr == RS) {
-#pragma unroll 4
+#pragma unroll kWideUnroll
       for (int rr = 0; rr < RS; ++rr) f(st + rr * kWideSW, list ? static_cast<int>(list[t0 + rr]) : t0 + rr);
     } else {
       for (int rr = 0; rr < nr; ++rr) f(st + rr * kWideSW, list ? static_cast<int>(list[t0 + rr]) : t0 + rr);
