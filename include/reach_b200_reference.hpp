@@ -15,6 +15,8 @@
 // tube.hpp:23-34), computed by the B200 kernels.
 #pragma once
 
+#include <cmath>
+
 #include "reach/closed_loop.hpp"
 #include "reach/dt_reach.hpp"
 #include "reach/mpc.hpp"
@@ -301,6 +303,73 @@ inline reach::ReachTube<double> dt_interval_baseline(Context& ctx, const reach::
                                                      const reach::IntervalBox<double>& x0,
                                                      const std::vector<reach::Vec<double>>& actions) {
   return to_reference(dt_interval_baseline(ctx, from_reference(sys), from_reference(x0), actions));
+}
+
+// reach::ctl_reach_loss (training.hpp:183-213) with the quadrotor plant (the reference takes the plant
+// body as a template argument; the device runs quadrotor_ode with `plant`): every episode's closed loop
+// on the device -- episodes sharing a reference sequence in one batch -- and the loss summed in episode
+// order on the host.  As the reference, an episode without y_ref keeps the previous one's.
+inline double ctl_reach_loss(Context& ctx, const reach::MLPNet<double>& controller,
+                             const reach::QuadrotorParams& plant, const std::vector<reach::Episode>& batch,
+                             double eps, int t_h, int n, int l, double delta, int k_atomic, double cap,
+                             int* diverged_count = nullptr, const reach::FlowpipeParams& fp_base = {}) {
+  if (batch.empty() || t_h < 1) throw std::invalid_argument("ctl_reach_loss: bad batch/horizon");
+  ClosedLoopSpec spec;
+  spec.plant = {plant.mass, plant.gravity, plant.jx, plant.jy, plant.jz};
+  spec.controller = from_reference(controller);
+  spec.n = n;
+  spec.l = l;
+  spec.ctl_steps = t_h;
+  spec.k_atomic = k_atomic;
+  spec.fp = {delta / k_atomic, fp_base.steps, fp_base.order, fp_base.eps_init, fp_base.refine_rounds,
+             fp_base.enlargement, fp_base.max_enlargements, fp_base.window};
+  std::vector<std::vector<std::vector<double>>> refs;  // per episode, after the carry-over
+  std::vector<std::vector<double>> cur;
+  for (const auto& ep : batch) {
+    if (!ep.y_ref.empty()) cur.assign(ep.y_ref.begin(), ep.y_ref.begin() + t_h);
+    refs.push_back(cur);
+  }
+  std::vector<double> terms(batch.size(), 0.0);
+  std::vector<bool> done(batch.size(), false);
+  int dc = 0;
+  for (size_t e0 = 0; e0 < batch.size(); ++e0) {
+    if (done[e0]) continue;
+    std::vector<size_t> idx;
+    std::vector<Box> x0s;
+    for (size_t e = e0; e < batch.size(); ++e)
+      if (!done[e] && refs[e] == refs[e0]) {
+        idx.push_back(e);
+        Box b(static_cast<size_t>(n));
+        for (int d = 0; d < n; ++d) b[d] = {batch[e].states.front()[d] - eps, batch[e].states.front()[d] + eps};
+        x0s.push_back(std::move(b));
+        done[e] = true;
+      }
+    spec.y_ref = refs[e0];
+    auto tubes = cl_reach_batch(ctx, spec, x0s);
+    for (size_t q = 0; q < idx.size(); ++q) {
+      const ReachTube& t = tubes[q];
+      if (t.diverged) {
+        terms[idx[q]] = cap;
+        ++dc;
+      } else {
+        double v = 0.0;  // predicted_volume (training.hpp:89-93)
+        for (size_t k = 1; k < t.boxes.size(); ++k) {
+          double w = 0.0;
+          bool fin = true;
+          for (const auto& iv : t.boxes[k]) {
+            fin = fin && std::isfinite(iv.lo) && std::isfinite(iv.hi);
+            w += iv.hi - iv.lo;
+          }
+          v += fin ? w : std::numeric_limits<double>::infinity();
+        }
+        terms[idx[q]] = std::log(1.0 + v);
+      }
+    }
+  }
+  double acc = 0.0;
+  for (double v : terms) acc += v;
+  if (diverged_count) *diverged_count += dc;
+  return acc / static_cast<double>(batch.size());
 }
 
 }  // namespace reach_b200

@@ -341,6 +341,30 @@ int main() {
     failures += compare(reach::dt_interval_baseline(sys, x0, acts), reach_b200::dt_interval_baseline(gpu, sys, x0, acts),
                         "dt_interval_baseline") ? 1 : 0;
   }
+  // ctl_reach_loss (training.hpp:183-213), quadrotor plant, tanh controller with y_ref: within 1e-12
+  {
+    Rng r7(3);
+    QuadrotorParams qp;
+    MLPNet<double> ctl = random_mlp(r7, 15, {16, 16}, 4, Act::Tanh, 0.4);
+    for (auto& w : ctl.layers.back().w.a) w *= 0.1;
+    ctl.layers.back().b[0] += qp.mass * qp.gravity;
+    std::vector<Episode> batch(3);
+    for (size_t e = 0; e < batch.size(); ++e) {
+      Vec<double> x0(12, 0.0);
+      for (int d = 0; d < 6; ++d) x0[d] = r7.uniform(-0.05, 0.05);
+      batch[e].states.assign(4, x0);
+      batch[e].actions.assign(3, Vec<double>(4, 0.0));
+      if (e != 1) batch[e].y_ref.assign(3, Vec<double>{r7.uniform(-0.1, 0.1), 0.0, 0.0});
+    }
+    auto plant = [qp](const auto& x, const auto& u, auto& dx) { quadrotor_ode(x, u, qp, dx); };
+    int d1 = 0, d2 = 0;
+    const double l1 = reach::ctl_reach_loss(ctl, plant, batch, 0.01, 3, 12, 4, 0.02, 2, 40.0, &d1);
+    const double l2 = reach_b200::ctl_reach_loss(gpu, ctl, qp, batch, 0.01, 3, 12, 4, 0.02, 2, 40.0, &d2);
+    if (std::fabs(l1 - l2) > 1e-12 * std::fabs(l1) || d1 != d2) {
+      std::printf("ctl_reach_loss: %.17g / %.17g\n", l1, l2);
+      ++failures;
+    }
+  }
   std::printf(failures ? "FAIL (%d)\n" : "OK: reference drop-in parity\n", failures);
   return failures ? 1 : 0;
 }
