@@ -1361,11 +1361,58 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
   const size_t per_it0 = pop * dim, per_it = (pop - 1) * dim;
   std::vector<double> z(per_it0 + static_cast<size_t>(iters - 1) * per_it);
   std::atomic<int> ready{0};
+  // Rng::normal (rng.hpp:24-37) split in two: the uniform pairs (u1, u2; u1 redrawn while <= 0) are
+  // drawn in stream order on the worker, then the Box-Muller transforms -- the same libm calls per
+  // pair, independent of each other -- run on a few host threads; value k of the stream is bit for
+  // bit what the sequential generator returns (cos first, sin cached as the spare).
   std::thread gen([&] {
+    const unsigned nth = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    std::vector<double> u1s, u2s;
     size_t o = 0;
     for (int it = 0; it < iters; ++it) {
       const size_t cnt = it == 0 ? per_it0 : per_it;
-      for (size_t q = 0; q < cnt; ++q) z[o + q] = c->normal();
+      size_t q = 0;
+      if (cnt > 0 && c->has_spare) {
+        z[o] = c->spare;
+        c->has_spare = false;
+        q = 1;
+      }
+      const size_t np = (cnt - q + 1) / 2;
+      u1s.resize(np);
+      u2s.resize(np);
+      for (size_t p = 0; p < np; ++p) {
+        double u1 = c->uniform01(), u2 = c->uniform01();
+        while (u1 <= 0.0) u1 = c->uniform01();
+        u1s[p] = u1;
+        u2s[p] = u2;
+      }
+      double* zz = z.data() + o + q;
+      const size_t left = cnt - q;
+      auto work = [&](size_t p0, size_t p1) {
+        for (size_t p = p0; p < p1; ++p) {
+          const double r = std::sqrt(-2.0 * std::log(u1s[p]));
+          const double a = 6.28318530717958647692 * u2s[p];
+          zz[2 * p] = r * std::cos(a);
+          if (2 * p + 1 < left) zz[2 * p + 1] = r * std::sin(a);
+        }
+      };
+      if (np < 4096 || nth == 1) {
+        work(0, np);
+      } else {
+        std::vector<std::thread> pool;
+        const size_t per = (np + nth - 1) / nth;
+        for (unsigned t = 1; t < nth; ++t) {
+          const size_t p0 = std::min(np, t * per), p1 = std::min(np, (t + 1) * per);
+          if (p0 < p1) pool.emplace_back(work, p0, p1);
+        }
+        work(0, std::min(np, per));
+        for (auto& th : pool) th.join();
+      }
+      if ((left & 1u) && np > 0) {  // the last pair's sine is the next draw (Rng's cached spare)
+        const size_t p = np - 1;
+        c->spare = std::sqrt(-2.0 * std::log(u1s[p])) * std::sin(6.28318530717958647692 * u2s[p]);
+        c->has_spare = true;
+      }
       o += cnt;
       ready.store(it + 1, std::memory_order_release);
     }
