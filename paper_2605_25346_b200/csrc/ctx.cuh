@@ -27,6 +27,9 @@ struct reach_ctx {
   // plan-problem staging buffer (goal, weights, constraints) for the MPC kernels
   void* pbuf = nullptr;
   size_t pbuf_bytes = 0;
+  // pinned host staging (MPC candidate populations, scores), grown on demand
+  void* hpin = nullptr;
+  size_t hpin_bytes = 0;
   // per-CTA symbolic-state buffers of the wide kernel family
   void* wws = nullptr;
   size_t wws_bytes = 0;
@@ -76,6 +79,19 @@ inline int ensure_ws(reach_ctx* ctx, size_t bytes) {
   }
   RB_CUDA(cudaMalloc(&ctx->ws, bytes));
   ctx->ws_bytes = bytes;
+  return REACH_OK;
+}
+
+inline int ensure_pinned(reach_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->hpin_bytes) return REACH_OK;
+  if (ctx->hpin) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFreeHost(ctx->hpin);
+    ctx->hpin = nullptr;
+    ctx->hpin_bytes = 0;
+  }
+  RB_CUDA(cudaMallocHost(&ctx->hpin, bytes));
+  ctx->hpin_bytes = bytes;
   return REACH_OK;
 }
 

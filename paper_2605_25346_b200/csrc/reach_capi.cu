@@ -372,6 +372,7 @@ int reach_ctx_destroy(reach_ctx* ctx) {
   if (ctx->pbuf) cudaFree(ctx->pbuf);
   if (ctx->wws) cudaFree(ctx->wws);
   if (ctx->wphase) cudaFree(ctx->wphase);
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
   for (auto& p : ctx->ev_used) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   for (auto& p : ctx->ev_free) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -1423,8 +1424,14 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
       if (t.joinable()) t.join();
     }
   } joiner{gen};
-  std::vector<double> cand(pop * dim), scores(pop);
-  std::vector<int32_t> okv(pop), div(pop);
+  // candidate population and scores in pinned host memory (full-bandwidth async copies)
+  const size_t cand_bytes = align_up(pop * dim * sizeof(double), 256);
+  rc = ensure_pinned(ctx, cand_bytes + pop * (sizeof(double) + sizeof(int32_t)));
+  if (rc) return rc;
+  double* cand = static_cast<double*>(ctx->hpin);
+  double* scores = reinterpret_cast<double*>(static_cast<char*>(ctx->hpin) + cand_bytes);
+  int32_t* div = reinterpret_cast<int32_t*>(scores + pop);
+  std::vector<int32_t> okv(pop);
   size_t zo = 0;
   for (int it = 0; it < iters; ++it) {
     while (ready.load(std::memory_order_acquire) <= it) std::this_thread::yield();
@@ -1436,12 +1443,12 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
         for (size_t q = 0; q < dim; ++q) u[q] = c->mean[q] + c->stdv[q] * z[zo++];
         c->clip(u);
       }
-      std::copy(u.begin(), u.end(), cand.begin() + k * dim);
+      std::copy(u.begin(), u.end(), cand + k * dim);
     }
-    rc = plan_eval_host(ctx, net, prob, x0, static_cast<int>(pop), cand.data(), scores.data(), div.data(), nullptr);
+    rc = plan_eval_host(ctx, net, prob, x0, static_cast<int>(pop), cand, scores, div, nullptr);
     if (rc) return rc;
     for (size_t k = 0; k < pop; ++k) okv[k] = div[k] ? 0 : 1;
-    reach_cem_update(c, scores.data(), okv.data());
+    reach_cem_update(c, scores, okv.data());
   }
   double best_obj = 0.0;
   int32_t be = 0;
