@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-grad", action="store_true", help="skip the grad_tube_volume leg")
     ap.add_argument("--no-ct", action="store_true", help="skip the C2 continuous-time closed-loop leg")
     ap.add_argument("--no-cl", action="store_true", help="skip the C5 / C1 DT closed-loop legs")
+    ap.add_argument("--dist-dry-run", action="store_true", help="launcher logic check on CPU (gloo), no GPU work")
     return ap.parse_args()
 
 
@@ -64,6 +65,55 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return int(s.getsockname()[1])
+
+
+def launch_command(argv, gpus: int, port: int):
+    """The torchrun command that runs this script with one rank per GPU (the
+    reference's fork-join parallel_for, parallel.hpp:17-37, becomes N processes)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def ensure_world(args, argv=None) -> int | None:
+    """`--gpus N` without torchrun (WORLD_SIZE unset): re-exec under torch.distributed.run with N
+    ranks and return its exit code.  Under torchrun the world size must equal --gpus.
+    Returns None when the current process should run the benchmark itself."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None:
+        if args.gpus <= 1:
+            return None
+        cmd = launch_command(sys.argv[1:] if argv is None else argv, args.gpus, _free_port())
+        return subprocess.call(cmd)
+    if int(env_world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world} (torchrun "
+                         f"--nproc-per-node must equal --gpus)")
+    return None
+
+
+def dist_dry_run(args):
+    """--dist-dry-run: the N-rank launch / rendezvous / max-over-ranks path on CPU (gloo), no GPU
+    work -- a logic check of the launcher, never a measurement."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "max_over_ranks": float(t[0]),
+                          "config": {"parallelism": f"dp{world}"}}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def algorithmic_flops_per_part(net_dims, n, m, H, window):
@@ -561,6 +611,13 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.impl == "reference" and os.environ.get("WORLD_SIZE") is None:
+        return run_reference(args)  # rank 0's work only: no ranks to launch
+    rc = ensure_world(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.dist_dry_run:
+        return dist_dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -574,6 +631,9 @@ def main():
     # RB_BENCH_SHARE_GPU=1 (logic check of the N > 1 path on a 1-GPU box, never a measurement):
     # ranks share the visible GPUs and reduce over gloo
     share = os.environ.get("RB_BENCH_SHARE_GPU") == "1"
+    if world > torch.cuda.device_count() and not share:
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPU(s); "
+                         "set RB_BENCH_SHARE_GPU=1 for a shared-GPU logic check (gloo)")
     if share:
         local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)

@@ -36,6 +36,7 @@
 #include <limits>
 #include <memory>
 #include <stdexcept>
+#include <list>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -113,7 +114,7 @@ class Context {
     if (rc != REACH_OK) throw Error("reach_ctx_create failed (no usable CUDA device)");
   }
   ~Context() {
-    for (auto& kv : nets_) reach_net_free(ctx_, kv.second);
+    for (auto& c : nets_) reach_net_free(ctx_, c.handle);
     reach_ctx_destroy(ctx_);
   }
   Context(const Context&) = delete;
@@ -147,18 +148,34 @@ class Context {
     mix(dims.data(), dims.size() * sizeof(int32_t));
     mix(acts.data(), acts.size() * sizeof(int32_t));
     mix(params.data(), params.size() * sizeof(double));
-    auto it = nets_.find(key);
-    if (it != nets_.end()) return it->second;
+    // hit only on an equal value (the hash is a bucket key, never the identity)
+    for (auto it = nets_.begin(); it != nets_.end(); ++it) {
+      if (it->key == key && it->dims == dims && it->acts == acts && it->params == params) {
+        nets_.splice(nets_.begin(), nets_, it);  // most recently used first
+        return it->handle;
+      }
+    }
     reach_net_desc d{static_cast<int32_t>(net.layers.size()), dims.data(), acts.data(), params.data()};
     reach_net* h = nullptr;
     check(reach_net_upload(ctx_, &d, &h), "reach_net_upload");
-    nets_[key] = h;
+    nets_.push_front(Cached{key, std::move(dims), std::move(acts), std::move(params), h});
+    while (nets_.size() > kMaxCachedNets) {  // bounded: weight-update loops upload a new value each step
+      reach_net_free(ctx_, nets_.back().handle);
+      nets_.pop_back();
+    }
     return h;
   }
 
  private:
+  struct Cached {
+    uint64_t key;
+    std::vector<int32_t> dims, acts;
+    std::vector<double> params;
+    reach_net* handle;
+  };
+  static constexpr size_t kMaxCachedNets = 32;
   reach_ctx* ctx_ = nullptr;
-  std::unordered_map<uint64_t, reach_net*> nets_;
+  std::list<Cached> nets_;
 };
 
 inline const char* failure_reason(int32_t status) { return reach_tube_status_string(status); }

@@ -6,6 +6,7 @@ __graft_entry__ as g; g.build()"` or `make -C paper_2605_25346_b200/csrc`.
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import os
 import threading
@@ -115,7 +116,7 @@ class Context:
             raise ReachError(f"reach_ctx_create failed (code {rc}): no usable CUDA device {device}")
         self.handle = h
         self.device = device
-        self._nets = {}
+        self._nets = collections.OrderedDict()  # content key -> (net, handle), most recent last
 
     def check(self, rc: int, what: str):
         if rc == A.REACH_OK:
@@ -158,18 +159,27 @@ class Context:
         rc = self._lib.reach_debug_phase_cycles(self.handle, arr, 16)
         return list(arr) if rc == A.REACH_OK else None
 
+    MAX_CACHED_NETS = 32
+
     def upload(self, net) -> "C.c_void_p":
-        """Device handle of `net` (cached by content: nets are values, SPEC.md)."""
+        """Device handle of `net` (cached by content: nets are values, SPEC.md).  The cache is a
+        bounded LRU: a weight-update loop uploads a new value every step, and the oldest
+        handles are freed (reach_net_free) beyond MAX_CACHED_NETS."""
         import hashlib
         desc, keep = net.desc()
-        key = hashlib.blake2b(b"".join(a.tobytes() for a in keep), digest_size=16).digest()
+        blob = b"".join(a.tobytes() for a in keep)
+        key = hashlib.blake2b(blob, digest_size=16).digest() + len(blob).to_bytes(8, "little")
         hit = self._nets.get(key)
         if hit is not None:
+            self._nets.move_to_end(key)
             return hit[1]
         h = C.c_void_p()
         self.check(self._lib.reach_net_upload(self.handle, C.byref(desc), C.byref(h)), "reach_net_upload")
         del keep
         self._nets[key] = (net, h)
+        while len(self._nets) > self.MAX_CACHED_NETS:
+            _, (_, old) = self._nets.popitem(last=False)
+            self._lib.reach_net_free(self.handle, old)
         return h
 
     def close(self):
@@ -190,7 +200,31 @@ class Context:
 _default = {}
 
 
-def default_context(device: int = 0) -> Context:
+def _current_device() -> int:
+    """The calling thread's CUDA device: torch's current device when torch is in use (one rank
+    per GPU under torchrun sets it), else LOCAL_RANK modulo the visible devices, else 0."""
+    import sys
+    torch = sys.modules.get("torch")
+    try:
+        if torch is not None and torch.cuda.is_available():
+            return int(torch.cuda.current_device())
+    except Exception:  # noqa: BLE001
+        pass
+    local = os.environ.get("LOCAL_RANK")
+    if local is not None:
+        try:
+            import torch as _t
+            n = _t.cuda.device_count()
+            return int(local) % n if n else 0
+        except Exception:  # noqa: BLE001
+            return 0
+    return 0
+
+
+def default_context(device: int | None = None) -> Context:
+    """The per-thread context of `device` (default: the calling thread's current CUDA device)."""
+    if device is None:
+        device = _current_device()
     tid = (threading.get_ident(), device)
     ctx = _default.get(tid)
     if ctx is None:

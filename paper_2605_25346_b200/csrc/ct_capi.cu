@@ -332,6 +332,7 @@ extern "C" {
 
 int reach_cl_batch(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s, int32_t batch, const double* x0_lo,
                    const double* x0_hi, const reach_tube_out* out, int32_t flags) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !ctl || !s || !out) return REACH_E_INVALID_ARGUMENT;
   if (batch < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "cl_reach: negative batch");
   int rc = validate_cl(ctx, ctl, s);
@@ -419,6 +420,7 @@ int reach_cl_batch(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s,
 
 int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s, const reach_cl_split_args* a,
                         const reach_hull_out* out, int32_t flags) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !ctl || !s || !a || !out) return REACH_E_INVALID_ARGUMENT;
   int rc = validate_cl(ctx, ctl, s);
   if (rc) return rc;
@@ -562,6 +564,7 @@ extern "C" {
 
 int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowpipe_params* fp, int32_t batch,
                    const double* x0_lo, const double* x0_hi, const reach_tube_out* out, int32_t flags) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !fd || !fp || !out) return REACH_E_INVALID_ARGUMENT;
   if (batch < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: negative batch");
   rb::ct::CTParams P{};
@@ -637,6 +640,7 @@ int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowp
 
 int reach_ct_split_hull(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowpipe_params* fp,
                         const reach_cl_split_args* a, const reach_hull_out* out, int32_t flags) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !fd || !fp || !a || !out) return REACH_E_INVALID_ARGUMENT;
   rb::ct::CTParams P{};
   int rc = ct_params(ctx, fd, fp, P);

@@ -67,6 +67,25 @@ inline int cuda_fail(reach_ctx* ctx, cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
   } while (0)
 
+// Every entry point runs on its context's device and leaves the caller's current
+// device as it found it (contexts on different GPUs may alternate in one thread).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const reach_ctx* c) {
+    if (!c) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != c->device) {
+      cudaSetDevice(c->device);
+      prev = cur;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 inline int ensure_ws(reach_ctx* ctx, size_t bytes) {

@@ -366,6 +366,7 @@ int reach_ctx_create(int32_t device, reach_ctx** out) {
 }
 
 int reach_ctx_destroy(reach_ctx* ctx) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx) return REACH_OK;
   cudaSetDevice(ctx->device);
   if (ctx->ws) cudaFree(ctx->ws);
@@ -381,24 +382,28 @@ int reach_ctx_destroy(reach_ctx* ctx) {
 }
 
 int reach_ctx_set_stream(reach_ctx* ctx, void* s) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx) return REACH_E_INVALID_ARGUMENT;
   ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
   return REACH_OK;
 }
 
 int reach_ctx_synchronize(reach_ctx* ctx) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx) return REACH_E_INVALID_ARGUMENT;
   RB_CUDA(cudaStreamSynchronize(ctx->stream));
   return REACH_OK;
 }
 
 int reach_ctx_enable_kernel_timing(reach_ctx* ctx, int32_t on) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx) return REACH_E_INVALID_ARGUMENT;
   ctx->timing = on != 0;
   return REACH_OK;
 }
 
 int reach_ctx_kernel_time(reach_ctx* ctx, double* total_ms, int64_t* launches) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !total_ms || !launches) return REACH_E_INVALID_ARGUMENT;
   RB_CUDA(cudaSetDevice(ctx->device));
   RB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -416,6 +421,7 @@ int reach_ctx_kernel_time(reach_ctx* ctx, double* total_ms, int64_t* launches) {
 }
 
 int reach_measure_fp64_peak(reach_ctx* ctx, double* tflops_fma, double* tflops_muladd) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !tflops_fma || !tflops_muladd) return REACH_E_INVALID_ARGUMENT;
   RB_CUDA(cudaSetDevice(ctx->device));
   double* dout = nullptr;
@@ -450,6 +456,7 @@ int reach_measure_fp64_peak(reach_ctx* ctx, double* tflops_fma, double* tflops_m
 }
 
 int reach_debug_phase_cycles(reach_ctx* ctx, uint64_t* out, int32_t count) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !out || count <= 0) return REACH_E_INVALID_ARGUMENT;
   if (ctx->wphase) {  // wide family, runtime-enabled counters
     RB_CUDA(cudaSetDevice(ctx->device));
@@ -479,6 +486,7 @@ const char* reach_ctx_last_error(const reach_ctx* ctx) { return ctx ? ctx->err.c
 int64_t reach_ctx_launch_count(const reach_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int reach_net_upload(reach_ctx* ctx, const reach_net_desc* d, reach_net** out) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !d || !out) return REACH_E_INVALID_ARGUMENT;
   *out = nullptr;
   if (d->n_layers < 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "MLPNet: empty");
@@ -548,6 +556,7 @@ int reach_net_upload(reach_ctx* ctx, const reach_net_desc* d, reach_net** out) {
 }
 
 int reach_net_free(reach_ctx* ctx, reach_net* net) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!net) return REACH_OK;
   if (ctx) cudaSetDevice(ctx->device);
   if (net->blob) cudaFree(net->blob);
@@ -654,6 +663,7 @@ extern "C" {
 
 int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, const reach_tube_out* out,
                    int32_t flags) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !a || !out) return REACH_E_INVALID_ARGUMENT;
   if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach_batch: negative size");
   int rc = validate_system(ctx, net, a->n, a->m);
@@ -663,6 +673,7 @@ int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a,
 
 int reach_dtcl_batch(reach_ctx* ctx, const reach_net* dyn, const reach_net* ctl, const reach_dt_args* a,
                      const reach_tube_out* out, int32_t flags) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !dyn || !ctl || !a || !out) return REACH_E_INVALID_ARGUMENT;
   if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt closed loop: negative size");
   if (a->m != 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt closed loop: actions come from the controller (m = 0)");
@@ -698,6 +709,7 @@ extern "C" {
 
 int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_args* a, const reach_hull_out* out,
                      int32_t flags) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !a || !out) return REACH_E_INVALID_ARGUMENT;
   int rc = validate_system(ctx, net, a->n, a->m);
   if (rc) return rc;
@@ -1118,6 +1130,7 @@ extern "C" {
 int reach_plan_eval_batch(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
                           int32_t batch, const double* actions, double* objective, int32_t* diverged,
                           const reach_tube_out* tubes, int32_t flags) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !prob || !x0 || !objective || !diverged || batch < 0) return REACH_E_INVALID_ARGUMENT;
   int rc = validate_problem(ctx, net, prob);
   if (rc) return rc;
@@ -1347,6 +1360,7 @@ static int plan_refine_impl(reach_ctx* ctx, const reach_net* net, const reach_pl
 int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
                       const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
                       double* best_history, int32_t* best_effort, int32_t* refined, const reach_tube_out* final_tube) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !prob || !cfg || !x0 || !best_actions || !objective) return REACH_E_INVALID_ARGUMENT;
   int rc = validate_problem(ctx, net, prob);
   if (rc) return rc;
@@ -1470,12 +1484,14 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
 int reach_plan_cem(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob,
                    const reach_sampler_config* cfg, const double* x0, double* best_actions, double* objective,
                    double* best_history, int32_t* best_effort, const reach_tube_out* final_tube) {
+  rbh::DeviceGuard device_guard_(ctx);
   return reach_plan_cem_ex(ctx, net, prob, cfg, x0, best_actions, objective, best_history, best_effort, nullptr,
                            final_tube);
 }
 
 int reach_plan_objective_grad(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
                               const double* actions, double* grad, double* objective) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !prob || !x0 || !actions || !grad) return REACH_E_INVALID_ARGUMENT;
   int rc = validate_problem(ctx, net, prob);
   if (rc) return rc;
@@ -1602,12 +1618,14 @@ extern "C" {
 
 int reach_grad_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
                            int32_t method, double* grad, int32_t* subgradient, double* volume) {
+  rbh::DeviceGuard device_guard_(ctx);
   return reach_grad_tube_volume_range(ctx, net, a, target, method, 0, -1, grad, subgradient, volume);
 }
 
 int reach_grad_tube_volume_range(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t target,
                                  int32_t method, int64_t param_begin, int64_t param_end, double* grad,
                                  int32_t* subgradient, double* volume) {
+  rbh::DeviceGuard device_guard_(ctx);
   namespace rd = rb::dual;
   if (!ctx || !net || !a || !grad) return REACH_E_INVALID_ARGUMENT;
   if (a->batch != 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "grad_tube_volume: batch must be 1");
@@ -1646,6 +1664,7 @@ int reach_mpc_run(reach_ctx* ctx, const reach_net* net, const reach_plan_problem
                   const reach_sampler_config* sampler, const reach_mpc_config* cfg, reach_sim_fn sim, void* sim_user,
                   const double* x0, int32_t* success, int32_t* violated, int32_t* steps_used, double* final_state,
                   const reach_mpc_log* log, int32_t* log_rows) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !prob || !sampler || !cfg || !x0) return REACH_E_INVALID_ARGUMENT;
   int rc = validate_problem(ctx, net, prob);
   if (rc) return rc;
@@ -1814,6 +1833,7 @@ int reach_refine_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_d
                              const double* radius, int32_t target, const double* lo, const double* hi,
                              int32_t iters, double* x, double* initial_objective, double* objective,
                              int32_t* progressed, int32_t* subgradient, int32_t* accepted_steps) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !a || !center || !radius || !lo || !hi || !x) return REACH_E_INVALID_ARGUMENT;
   if (target != REACH_GRAD_X0_CENTER && target != REACH_GRAD_ACTIONS)
     return fail(ctx, REACH_E_INVALID_ARGUMENT, "refine: target must be the X0 centre or the actions");
@@ -1932,6 +1952,7 @@ int reach_refine_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_d
 // network parameters (grad_forward, refine.hpp:186-207, in net_params order).
 int reach_reach_loss(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t episodes,
                      double eps, double cap, double* loss, double* grad, int32_t* diverged_count) {
+  rbh::DeviceGuard device_guard_(ctx);
   namespace rd = rb::dual;
   if (!ctx || !net || !a || !loss) return REACH_E_INVALID_ARGUMENT;
   if (episodes < 1 || a->horizon < 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "reach_loss: bad batch/horizon");
@@ -2022,6 +2043,7 @@ int reach_reach_loss(reach_ctx* ctx, const reach_net* net, const reach_dt_args* 
 // The refinement step of plan_cem alone (mpc.hpp:337-361), for drivers that run the CEM loop in pieces.
 int reach_plan_refine(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
                       int32_t refine_iters, double best_objective, double* best_actions, int32_t* refined) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !prob || !x0 || !best_actions) return REACH_E_INVALID_ARGUMENT;
   if (refine_iters < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "SamplerConfig: invalid configuration");
   int rc = validate_problem(ctx, net, prob);
@@ -2034,6 +2056,7 @@ int reach_plan_refine(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
 // dt_interval_baseline (dt_reach.hpp:129-149) for a batch: the naive interval tube of the same map.
 int reach_dt_interval_baseline_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a,
                                      const reach_tube_out* out) {
+  rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !a || !out) return REACH_E_INVALID_ARGUMENT;
   if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach_batch: negative size");
   int rc = validate_system(ctx, net, a->n, a->m);

@@ -55,6 +55,14 @@ def combine_hulls(partials):
     return lo, hi, div, nb, key
 
 
+def empty_hull(rows: int, n: int, h: float = 0.0):
+    """The identity of the hull all-reduce: a rank with an empty part range contributes nothing
+    (lo = +inf, hi = -inf, no failure, the largest box count)."""
+    from .api import HullResult
+    return HullResult(np.full((rows, n), np.inf), np.full((rows, n), -np.inf), np.zeros(rows, np.int32),
+                      np.iinfo(np.int32).max, np.iinfo(np.int64).max, h)
+
+
 def allreduce_hull(res, group=None):
     """All-reduces a rank's partial HullResult in place (NaN only survives from part 0, as the reference)."""
     import torch
@@ -87,7 +95,7 @@ def allreduce_hull(res, group=None):
 
 
 def sharded_split_hull(sys, x0, plan, actions, prm, group=None,
-                       evaluate: Optional[Callable] = None):
+                       evaluate: Optional[Callable] = None, ctx=None):
     """reach_with_splitting over all ranks: each evaluates its contiguous part range, then one all-reduce."""
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -97,12 +105,15 @@ def sharded_split_hull(sys, x0, plan, actions, prm, group=None,
         from .api import reach_split_hull
 
         def evaluate(sys_, x0_, plan_, acts_, prm_, begin, end):
-            return reach_split_hull(sys_, x0_, plan_, acts_, prm_, part_begin=begin, part_end=end)
-    res = evaluate(sys, x0, plan, actions, prm, b, e)
+            return reach_split_hull(sys_, x0_, plan_, acts_, prm_, part_begin=begin, part_end=end, ctx=ctx)
+    if e <= b:  # more ranks than parts: this rank contributes the identity of the reduction
+        res = empty_hull(len(actions) + 1, sys.n)
+    else:
+        res = evaluate(sys, x0, plan, actions, prm, b, e)
     return allreduce_hull(res, group)
 
 
-def sharded_cl_split_hull(spec, x0, plan, group=None, evaluate: Optional[Callable] = None):
+def sharded_cl_split_hull(spec, x0, plan, group=None, evaluate: Optional[Callable] = None, ctx=None):
     """reach_with_splitting(cl_reach) over all ranks (C2): contiguous part ranges, one all-reduce."""
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -111,12 +122,14 @@ def sharded_cl_split_hull(spec, x0, plan, group=None, evaluate: Optional[Callabl
         from .api import cl_split_hull
 
         def evaluate(spec_, x0_, plan_, begin, end):
-            return cl_split_hull(spec_, x0_, plan_, part_begin=begin, part_end=end)
+            return cl_split_hull(spec_, x0_, plan_, part_begin=begin, part_end=end, ctx=ctx)
+    if e <= b:
+        return allreduce_hull(empty_hull(spec.steps(), spec.n + spec.l, spec.fp.h), group)
     return allreduce_hull(evaluate(spec, x0, plan, b, e), group)
 
 
 def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = None,
-                     refine: Optional[Callable] = None):
+                     refine: Optional[Callable] = None, ctx=None):
     """plan_cem (mpc.hpp:258-368) over all ranks; returns (actions, objective, best_effort, history).
 
     Every rank draws the full population (same stream), evaluates its slice,
@@ -132,7 +145,7 @@ def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = N
     dev = _device_for(group)
     if evaluate is None:
         def evaluate(prob_, x0_, acts_):
-            r = plan_eval_batch(prob_, x0_, acts_)
+            r = plan_eval_batch(prob_, x0_, acts_, ctx=ctx)
             return r.objective, r.diverged
     cem = CEM(prob, dataclasses.replace(cfg, refine_iters=0))
     pop = cfg.population
@@ -154,14 +167,14 @@ def sharded_plan_cem(prob, cfg, x0, group=None, evaluate: Optional[Callable] = N
     if cfg.refine_iters > 0 and np.isfinite(best_obj):
         if refine is None:
             def refine(prob_, x0_, acts_, obj_, iters_):
-                return plan_refine(prob_, x0_, acts_, obj_, iters_)[0]
+                return plan_refine(prob_, x0_, acts_, obj_, iters_, ctx=ctx)[0]
         best = refine(prob, x0, best, best_obj, cfg.refine_iters)
     fin, _ = evaluate(prob, x0, best[None])
     return best, float(fin[0]), best_effort, hist
 
 
 def sharded_grad_tube_volume(sys, x0, actions, target, method=0, prm=None, group=None,
-                             evaluate: Optional[Callable] = None):
+                             evaluate: Optional[Callable] = None, ctx=None):
     """grad_tube_volume (refine.hpp:263-311) over all ranks: the parameters (one forward-dual pass, or two
     central-difference passes, each -- independent) are split into contiguous slices, each rank runs its
     slice's passes in one launch, one all-gather assembles the gradient; the subgradient flag is OR-ed.
@@ -177,7 +190,7 @@ def sharded_grad_tube_volume(sys, x0, actions, target, method=0, prm=None, group
     b, e = shard_range(full, rank, world)
     if evaluate is None:
         def evaluate(s_, x_, a_, t_, m_, p_, b_, e_):
-            g = grad_tube_volume(s_, x_, a_, t_, m_, p_, param_range=(b_, e_))
+            g = grad_tube_volume(s_, x_, a_, t_, m_, p_, param_range=(b_, e_), ctx=ctx)
             return g.g, g.subgradient
     g_slice, sub = evaluate(sys, x0, actions, target, method, prm, b, e)
     dev = _device_for(group)

@@ -57,3 +57,18 @@ def small_cem():
     prob = relu_problem(horizon=6)
     return prob, SamplerConfig(population=48, elite_frac=0.1, iterations=4, init_std=0.3, smoothing=0.5,
                                refine_iters=0, seed=3), np.array([0.05, -0.05, 0.0])
+
+
+def odd_cem():
+    """An odd draw count per iteration (1201 candidates x H=7 x m=1 = 8407 normals, then 8400 >= the 4096-pair
+    threshold of the threaded Box-Muller transform): the cached spare normal carries over between
+    iterations (rng.hpp:24-37), and the multi-threaded transform branch runs."""
+    rng = np.random.default_rng(17)
+    net = random_mlp(rng, 4, [24, 24], 3, scale=0.7)
+    net.layers[-1].w *= 0.4
+    sys = DTSystem(net, 3, 1)
+    cons = [Constraint(type=Constraint.BOX_STAY_IN, lo=np.full(3, -1.0), hi=np.full(3, 1.0))]
+    prob = PlanProblem(sys, np.array([0.2, -0.1, 0.05]), np.ones(3), np.full(1, 0.05), cons, horizon=7,
+                       u_lo=np.full(1, -1.0), u_hi=np.full(1, 1.0), eps=0.01)
+    return prob, SamplerConfig(population=1201, elite_frac=0.05, iterations=3, init_std=0.4, smoothing=0.3,
+                               refine_iters=0, seed=9), np.array([0.02, 0.0, -0.03])

@@ -52,6 +52,9 @@ def _worker(rank, world, port, q):
         def ev_hull(s, x0, p, a, prm, b, e):
             return oracle_split_hull(s, x0[0], x0[1], p, a, prm, b, e)
         h = sharded_split_hull(sys_, (c - 0.01, c + 0.01), plan, acts, DTReachParams(), evaluate=ev_hull)
+        # one part over two ranks: rank 1's slice is empty and contributes the reduction's identity
+        h1 = sharded_split_hull(sys_, (c - 0.01, c + 0.01), SplitPlan([1, 1, 1, 1]), acts, DTReachParams(),
+                                evaluate=ev_hull)
 
         prob, cfg, x0 = small_cem()
 
@@ -78,7 +81,7 @@ def _worker(rank, world, port, q):
                 return g[b_:e_], sub
             gw = sharded_grad_tube_volume(gsys, gx0, gacts, 2, 0, gprm, evaluate=ev_grad).g
         q.put((rank, h.lo, h.hi, h.n_boxes, h.fail_key, best, obj, be, hist, ch.lo, ch.hi, ch.n_boxes, ch.fail_key,
-               gw))
+               gw, h1.lo, h1.hi, h1.n_boxes, h1.fail_key))
     finally:
         dist.destroy_process_group()
 
@@ -119,7 +122,10 @@ def test_two_rank_gloo_sharding_matches_single_process():
     if ref_available():
         _, gsys, gx0, gacts, gprm, _ = grad_cases()[2]
         gfull = ref_grad_tube_volume(gsys, gx0, gacts, 2, 0, gprm)[0]
-    for rank, lo, hi, nb, key, best, obj, be, hist, clo_r, chi_r, cnb, ckey, gw in outs:
+    one = oracle_split_hull(sys_, c - 0.01, c + 0.01, SplitPlan([1, 1, 1, 1]), acts, DTReachParams())
+    for rank, lo, hi, nb, key, best, obj, be, hist, clo_r, chi_r, cnb, ckey, gw, lo1, hi1, nb1, key1 in outs:
+        assert nb1 == one.n_boxes and key1 == one.fail_key
+        assert same_bits(lo1[:nb1], one.lo[:nb1]) and same_bits(hi1[:nb1], one.hi[:nb1])
         if gfull is not None:  # weights gradient assembled from two ranks' parameter slices
             assert same_bits(gw, gfull)
         k = full.n_boxes

@@ -54,3 +54,15 @@ def test_c3_full_replan_matches_reference():
     r = plan_cem(prob, cfg, x0)
     assert same_bits(r.actions, eb) and r.objective == eo and same_bits(r.best_history, eh)
     assert r.best_effort == ebe
+
+
+def test_plan_cem_odd_draw_count_threaded_normals():
+    from mpc_cases import odd_cem
+    prob, cfg, x0 = odd_cem()
+    eb, eo, eh, ebe = oracle_plan_cem(prob, cfg, x0)
+    r = plan_cem(prob, cfg, x0)
+    assert same_bits(r.actions, eb) and r.objective == eo and same_bits(r.best_history, eh)
+    assert r.best_effort == ebe
+    if ref_available():
+        rb, ro, rh, rbe = ref_plan_cem(prob, cfg, x0)
+        assert same_bits(r.actions, rb) and r.objective == ro
