@@ -202,6 +202,13 @@ int reach_measure_fp64_peak(reach_ctx* ctx, double* tflops_fma, double* tflops_m
  * box, drain).  The product build returns REACH_E_UNSUPPORTED. */
 int reach_debug_phase_cycles(reach_ctx* ctx, uint64_t* out, int32_t count);
 
+// Test hook of the tensor-core contraction (not part of the reference API): one
+// Ozaki int8 tcgen05 product D = A . B^T (A M x K, B N x K row-major, host
+// pointers; N in 8..64, multiple of 8; K <= 256) with the per-element rigorous
+// bound |A . B^T - D| <= bound.
+int reach_debug_ozaki_gemm(reach_ctx* ctx, int32_t M, int32_t N, int32_t K, const double* A, const double* B,
+                           double* D, double* bound);
+
 /* Uploads an immutable network (SPEC: nets are values). */
 int reach_net_upload(reach_ctx* ctx, const reach_net_desc* desc, reach_net** out);
 int reach_net_free(reach_ctx* ctx, reach_net* net);

@@ -85,6 +85,8 @@ def _declare(lib):
               "reach_cem_sample", "reach_cem_update", "reach_cem_result"):
         getattr(lib, f).restype = C.c_int
     lib.reach_debug_phase_cycles.restype = C.c_int
+    lib.reach_debug_ozaki_gemm.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, dp, dp, dp, dp]
+    lib.reach_debug_ozaki_gemm.restype = C.c_int
     for f in ("reach_ctx_create", "reach_ctx_destroy", "reach_ctx_set_stream", "reach_ctx_synchronize",
               "reach_net_upload", "reach_net_free", "reach_dt_batch", "reach_split_hull",
               "reach_ctx_enable_kernel_timing", "reach_ctx_kernel_time", "reach_measure_fp64_peak"):
@@ -160,6 +162,20 @@ class Context:
         return list(arr) if rc == A.REACH_OK else None
 
     MAX_CACHED_NETS = 32
+
+    def ozaki_gemm(self, A, B):
+        """Test hook: the tensor-core (Ozaki int8 tcgen05) product A . B^T and its rigorous error bound."""
+        import numpy as np
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        M, K = A.shape
+        N = B.shape[0]
+        D = np.empty((M, N))
+        E = np.empty((M, N))
+        dp = C.POINTER(C.c_double)
+        self.check(self._lib.reach_debug_ozaki_gemm(self.handle, M, N, K, A.ctypes.data_as(dp), B.ctypes.data_as(dp),
+                                                     D.ctypes.data_as(dp), E.ctypes.data_as(dp)), "ozaki_gemm")
+        return D, E
 
     def upload(self, net) -> "C.c_void_p":
         """Device handle of `net` (cached by content: nets are values, SPEC.md).  The cache is a
