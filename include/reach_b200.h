@@ -65,6 +65,16 @@ enum reach_tube_status {
 
 /* Flags for the batch entry points. */
 #define REACH_FLAG_DEVICE_PTRS 1 /* every pointer in args/out is a device pointer */
+/* Precision mode (flags bits 8..11) of the DT engines (reach_dt_batch, reach_dtcl_batch,
+ * reach_split_hull).  REACH_PREC_EXACT (default): the reference's arithmetic, bit for bit.
+ * REACH_PREC_TC: the CROWN contractions Lambda_s . W_l (neural.hpp:326) on the int8 tensor
+ * cores (tcgen05.mma kind::i8, Ozaki split into 7 slices, exact int32 accumulation); the
+ * rigorous contraction-error bound widens the intercepts, so tubes stay sound and match the
+ * exact mode to ~1e-9 relative.  Wide (CTA-per-sample) family only:
+ * n <= 72, controller outputs <= 72, hidden widths <= 256. */
+#define REACH_FLAG_PREC_MASK 0xF00
+#define REACH_PREC_EXACT 0x000
+#define REACH_PREC_TC 0x100
 
 /* MLPNet<double> (neural.hpp:42-88), flattened. */
 typedef struct reach_net_desc {
@@ -204,8 +214,10 @@ int reach_debug_phase_cycles(reach_ctx* ctx, uint64_t* out, int32_t count);
 
 // Test hook of the tensor-core contraction (not part of the reference API): one
 // Ozaki int8 tcgen05 product D = A . B^T (A M x K, B N x K row-major, host
-// pointers; N in 8..64, multiple of 8; K <= 256) with the per-element rigorous
+// pointers; N in 8..56, multiple of 8; K <= 256) with the per-element rigorous
 // bound |A . B^T - D| <= bound.
+// Test hook: cycles per tcgen05.mma.kind::i8 (M = 128, N, K = 32, SS) issued back to back by one thread.
+int reach_debug_mma_rate(reach_ctx* ctx, int32_t count, int32_t N, int32_t naccum, double* cycles_per_mma);
 int reach_debug_ozaki_gemm(reach_ctx* ctx, int32_t M, int32_t N, int32_t K, const double* A, const double* B,
                            double* D, double* bound);
 

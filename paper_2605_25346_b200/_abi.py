@@ -18,6 +18,19 @@ REACH_E_OOM = 5
 REACH_E_NONFINITE = 6
 
 REACH_FLAG_DEVICE_PTRS = 1
+REACH_FLAG_PREC_MASK = 0xF00
+REACH_PREC_EXACT = 0x000
+REACH_PREC_TC = 0x100
+PRECISIONS = {"exact": REACH_PREC_EXACT, "tc": REACH_PREC_TC}
+
+
+def prec_flag(precision: str) -> int:
+    """Flags bits of a precision mode: "exact" (the reference's arithmetic, bit for bit) or "tc"
+    (CROWN contractions on the int8 tensor cores, Ozaki split, rigorous error bound)."""
+    try:
+        return PRECISIONS[precision]
+    except KeyError:
+        raise ValueError(f"unknown precision mode {precision!r} (exact | tc)") from None
 
 ACT_RELU, ACT_TANH, ACT_IDENTITY = 0, 1, 2
 

@@ -219,8 +219,10 @@ def _actions_array(seqs, B, H, m) -> np.ndarray:
 
 def dt_reach_batch_arrays(sys: DTSystem, x0_lo: np.ndarray, x0_hi: np.ndarray, actions: np.ndarray,
                           prm: DTReachParams = DTReachParams(), ctx: Optional[Context] = None,
-                          actions_shared: bool = False) -> TubeBatch:
-    """dt_reach_batch (dt_reach.hpp:108-125) on arrays: x0 [B][n], actions [B][H][m] (or [H][m] shared)."""
+                          actions_shared: bool = False, precision: str = "exact") -> TubeBatch:
+    """dt_reach_batch (dt_reach.hpp:108-125) on arrays: x0 [B][n], actions [B][H][m] (or [H][m] shared).
+    precision "tc": the CROWN contractions on the int8 tensor cores (A.REACH_PREC_TC)."""
+    pflag = A.prec_flag(precision)
     sys.validate()
     ctx = ctx or default_context()
     x0_lo = np.ascontiguousarray(x0_lo, dtype=np.float64)
@@ -239,7 +241,7 @@ def dt_reach_batch_arrays(sys: DTSystem, x0_lo: np.ndarray, x0_hi: np.ndarray, a
     to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step),
                    A.iptr(out.status))
     net = ctx.upload(sys.step)
-    ctx.check(ctx._lib.reach_dt_batch(ctx.handle, net, C.byref(args), C.byref(to), 0), "dt_reach_batch")
+    ctx.check(ctx._lib.reach_dt_batch(ctx.handle, net, C.byref(args), C.byref(to), pflag), "dt_reach_batch")
     return out
 
 
@@ -531,8 +533,10 @@ class HullResult:
 
 
 def reach_split_hull(sys: DTSystem, x0, plan: SplitPlan, actions, prm: DTReachParams = DTReachParams(),
-                     part_begin: int = 0, part_end: int = 0, ctx: Optional[Context] = None) -> HullResult:
+                     part_begin: int = 0, part_end: int = 0, ctx: Optional[Context] = None,
+                     precision: str = "exact") -> HullResult:
     """Hull over sub-boxes [part_begin, part_end) of reach_with_splitting (C ABI reach_split_hull)."""
+    pflag = A.prec_flag(precision)
     sys.validate()
     ctx = ctx or default_context()
     lo0 = np.ascontiguousarray(x0[0], dtype=np.float64)
@@ -548,7 +552,7 @@ def reach_split_hull(sys: DTSystem, x0, plan: SplitPlan, actions, prm: DTReachPa
                        A.iptr(counts), A.dptr(acts if acts.size else np.zeros(1)), int(part_begin), int(part_end))
     ho = A.HullOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.box_diverged), A.iptr(nb), A.lptr(key))
     net = ctx.upload(sys.step)
-    ctx.check(ctx._lib.reach_split_hull(ctx.handle, net, C.byref(args), C.byref(ho), 0), "reach_with_splitting")
+    ctx.check(ctx._lib.reach_split_hull(ctx.handle, net, C.byref(args), C.byref(ho), pflag), "reach_with_splitting")
     out.n_boxes = int(nb[0])
     out.fail_key = int(key[0])
     return out
@@ -562,10 +566,13 @@ def reach_with_splitting(sys: DTSystem, x0, plan: SplitPlan, actions, prm: DTRea
 
 # ---------------------------------------------------------------------------
 def dt_closed_loop_batch(dyn: MLPNet, ctl: MLPNet, n: int, x0_lo: np.ndarray, x0_hi: np.ndarray, horizon: int,
-                         prm: DTReachParams = DTReachParams(), ctx: Optional[Context] = None) -> TubeBatch:
+                         prm: DTReachParams = DTReachParams(), ctx: Optional[Context] = None,
+                         precision: str = "exact") -> TubeBatch:
     """DT closed loop: per step u = ctl_crown(x_tm, ctl) (neural.hpp:418),
     [x; u] stacked as cl_reach does (closed_loop.hpp:118-153), certify_tm_input(dyn, .), then
-    dt_reach's re-seed / fold / box.  dyn: (n + l) -> n, ctl: n -> l."""
+    dt_reach's re-seed / fold / box.  dyn: (n + l) -> n, ctl: n -> l.  precision "tc": the CROWN
+    contractions on the int8 tensor cores (A.REACH_PREC_TC)."""
+    pflag = A.prec_flag(precision)
     dyn.validate()
     ctl.validate()
     l = ctl.output_dim()
@@ -584,7 +591,7 @@ def dt_closed_loop_batch(dyn: MLPNet, ctl: MLPNet, n: int, x0_lo: np.ndarray, x0
     to = A.TubeOut(A.dptr(out.lo), A.dptr(out.hi), A.iptr(out.n_boxes), A.iptr(out.failed_step),
                    A.iptr(out.status))
     hd, hc = ctx.upload(dyn), ctx.upload(ctl)
-    ctx.check(ctx._lib.reach_dtcl_batch(ctx.handle, hd, hc, C.byref(args), C.byref(to), 0), "dt closed loop")
+    ctx.check(ctx._lib.reach_dtcl_batch(ctx.handle, hd, hc, C.byref(args), C.byref(to), pflag), "dt closed loop")
     return out
 
 

@@ -12,6 +12,7 @@
 
 #include "../../include/reach_b200.h"
 #include "dt_kernel.cuh"
+#include "tcw_types.cuh"
 
 struct reach_ctx {
   int device = 0;
@@ -47,6 +48,10 @@ struct reach_net {
   int hp = 0;   // padded hidden width 32 * cpl
   std::vector<int> dims, acts;
   std::vector<double> params;  // host copy in net_params order (neural.hpp:133-140)
+  // tensor-core mode (tc_capi.cu, built on first use): Ozaki split planes of W_l^T,
+  // their TMA tensor maps, row scale exponents and L1 norms, in one device allocation
+  mutable void* oz_mem = nullptr;
+  mutable rb::OzNet oz{};
 };
 
 namespace rbh {

@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "tc_capi.h"
 #include "../../include/reach_b200.h"
 #include "diag.cuh"
 #include "dual_kernel.cuh"
@@ -48,6 +49,8 @@ struct DTLayout {
   size_t smem = 0;
   bool wide = false;  // dt_wide_kernel<rd, rc>, grid CTAs persistent over the batch
   int rd = 0, rc = 0, grid = 0;
+  bool tcw = false;   // dt_tcw_kernel (REACH_PREC_TC), grid CTAs persistent over the batch
+  rb::TcwParams tx{};
 };
 
 // Two 48 KB bulk-copy stages (double buffering with 48-row chunks of a 128-wide layer): fewer, larger
@@ -270,7 +273,16 @@ int plan_wide(reach_ctx* ctx, const reach_net* net, int n, int m, int window, lo
 // warp's shared-memory slice, else the wide CTA-per-sample kernel
 // (RB_FORCE_WIDE=1 forces the wide family, for parity runs of both).
 int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, long long B, rb::DTParams& P,
-            DTLayout& lay, const reach_net* ctl = nullptr) {
+            DTLayout& lay, const reach_net* ctl = nullptr, int prec = REACH_PREC_EXACT) {
+  if (prec == REACH_PREC_TC) {
+    const int rc = plan_wide(ctx, net, n, m, window, B, P, lay, ctl);
+    if (rc) return rc;
+    const int rt = rbh::plan_tcw(ctx, net, ctl, n, B, P, lay.smem, lay.grid, lay.tx);
+    if (rt) return rt;
+    lay.tcw = true;
+    return REACH_OK;
+  }
+  if (prec != REACH_PREC_EXACT) return fail(ctx, REACH_E_INVALID_ARGUMENT, "unknown precision mode");
   if (!env_int("RB_FORCE_WIDE", 0, 0, 1)) {
     const int rc = plan_warp(ctx, net, n, m, window, P, lay, ctl);
     if (rc != REACH_E_UNSUPPORTED) return rc;
@@ -306,6 +318,7 @@ cudaError_t launch_dt_no(const rb::DTParams& P, const DTLayout& lay, long long B
 }
 
 cudaError_t launch_dt(const rb::DTParams& P, const DTLayout& lay, long long B, cudaStream_t s) {
+  if (lay.tcw) return rbh::tcw_launch(P, lay.tx, lay.smem, lay.grid, s);
   if (lay.wide) return wide_dispatch(&P, lay, nullptr, s);
   switch (lay.no) {
     case 2: return launch_dt_no<2>(P, lay, B, s);
@@ -560,6 +573,7 @@ int reach_net_free(reach_ctx* ctx, reach_net* net) {
   if (!net) return REACH_OK;
   if (ctx) cudaSetDevice(ctx->device);
   if (net->blob) cudaFree(net->blob);
+  rbh::free_oz(net);
   delete net;
   return REACH_OK;
 }
@@ -574,7 +588,7 @@ int run_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_net* ctl, con
   RB_CUDA(cudaSetDevice(ctx->device));
   rb::DTParams P{};
   DTLayout lay;
-  rc = plan_dt(ctx, net, a->n, a->m, a->window, a->batch, P, lay, ctl);
+  rc = plan_dt(ctx, net, a->n, a->m, a->window, a->batch, P, lay, ctl, flags & REACH_FLAG_PREC_MASK);
   if (rc) return rc;
   P.net = net->dev;
   P.B = a->batch;
@@ -726,7 +740,7 @@ int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_arg
   RB_CUDA(cudaSetDevice(ctx->device));
   rb::DTParams P{};
   DTLayout lay;
-  rc = plan_dt(ctx, net, a->n, a->m, a->window, end - begin, P, lay);
+  rc = plan_dt(ctx, net, a->n, a->m, a->window, end - begin, P, lay, nullptr, flags & REACH_FLAG_PREC_MASK);
   if (rc) return rc;
   const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
   const int n = a->n, H = a->horizon, m = a->m;

@@ -76,10 +76,36 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// The same MMA issued by a converged warp: one lane is elected inside the instruction sequence, so
+// the warp stays convergent (no per-MMA divergent-branch handling of the uniform operands).
+__device__ __forceinline__ void mma_i8_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 r;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync r|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // arrive on `bar` when every previously issued MMA of this thread has completed
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+// commit from a converged warp (one elected lane)
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      ".reg .b32 r;\n"
+      "elect.sync r|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 // ---- TMEM -> registers: 32 lanes x 16 consecutive 32-bit columns (warp w reads lanes 32 (w % 4) ..)
@@ -116,16 +142,18 @@ __device__ __forceinline__ void tma_prefetch(const void* tmap) {
 // tensor cores).  A row x with scale exponent E (|x_k| < 2^(E-1)) is
 //   x_k = 2^E (sum_{t<7} s_t,k 2^-7(t+1) + r_k 2^-49),  |r_k| <= 1/2,  |s_t,k| <= 64,
 // with slices s_t from round-to-nearest steps (exact in fp64).  A product of two
-// split rows keeps the slice pairs with t + u <= 6 (28 int8 MMAs per 32-wide K
-// step, grouped by level g = t + u into 7 exact int32 accumulators); the value is
-//   2^(EA + EB - 56) sum_g acc_g 2^(7 (6 - g)),
-// and the dropped pairs and residuals are bounded per output element by
-//   2^-50 (2^EA |b|_1 + 2^EB |a|_1) + K 2^-48 2^(EA + EB)     (oz_bound).
+// split rows keeps the slice pairs with t + u <= 8 (39 int8 MMAs per 32-wide K
+// step, grouped by level g = t + u into 9 exact int32 accumulators); the value is
+//   2^(EA + EB - 70) sum_g acc_g 2^(7 (8 - g)),
+// and the residuals (2^-50 relative to the row scales) and the dropped pairs
+// (levels >= 9: 4 pairs of at most 2^(EA+EB-65) per k, and smaller) are bounded
+// per output element by
+//   2^-50 (2^EA |b|_1 + 2^EB |a|_1) + K 2^(EA + EB - 62)             (bound).
 namespace oz {
 
 constexpr int kSlices = 7;
-constexpr int kGroups = 7;  // levels g = t + u = 0 .. 6
-constexpr int kPairs = 28;
+constexpr int kGroups = 9;  // levels g = t + u = 0 .. 8
+constexpr int kPairs = 39;
 
 // scale exponent of a row with max |x| = amax: 2^(E-1) > amax (E = 0 for a zero row)
 __host__ __device__ __forceinline__ int scale_exp(double amax) {
@@ -147,18 +175,20 @@ __device__ __forceinline__ void split7(double x, int E, int8_t (&s)[kSlices]) {
   }
 }
 
-// combine the 7 level accumulators of one output element (exact up to the final rounding)
+// combine the 9 level accumulators of one output element (exact up to the final rounding):
+// sum_g acc_g 2^(7 (8 - g)) = hi 2^35 + lo with |hi| < 2^42, |lo| < 2^51
 __device__ __forceinline__ double combine(const int32_t (&acc)[kGroups], int ea_eb) {
   const long long hi = ((static_cast<long long>(acc[0]) * 128 + acc[1]) * 128 + acc[2]) * 128 + acc[3];
-  const long long lo = (static_cast<long long>(acc[4]) * 128 + acc[5]) * 128 + acc[6];
-  const double v = fma(static_cast<double>(hi), 2097152.0, static_cast<double>(lo));  // hi 2^21 + lo
-  return ldexp(v, ea_eb - 56);
+  const long long lo =
+      (((static_cast<long long>(acc[4]) * 128 + acc[5]) * 128 + acc[6]) * 128 + acc[7]) * 128 + acc[8];
+  const double v = fma(static_cast<double>(hi), 34359738368.0, static_cast<double>(lo));  // hi 2^35 + lo
+  return ldexp(v, ea_eb - 70);
 }
 
 // rigorous bound of |a.b - combine(..)| for rows a (scale EA, |a|_1 = l1a) and b over K terms
 __host__ __device__ __forceinline__ double bound(int ea, double l1a, int eb, double l1b, int K) {
   if (!(l1a > 0.0) || !(l1b > 0.0)) return 0.0;  // a zero row splits exactly into zero slices
-  return ldexp(1.0, -50) * (ldexp(l1b, ea) + ldexp(l1a, eb)) + static_cast<double>(K) * ldexp(1.0, ea + eb - 48);
+  return ldexp(1.0, -50) * (ldexp(l1b, ea) + ldexp(l1a, eb)) + static_cast<double>(K) * ldexp(1.0, ea + eb - 62);
 }
 
 }  // namespace oz

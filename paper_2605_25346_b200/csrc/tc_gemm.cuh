@@ -8,8 +8,8 @@
 //   oz_gemm_kernel        D = A . B^T (+ the per-element rigorous error bound) for one
 //                         128-row M tile per CTA: B rows split in the CTA into
 //                         swizzled shared-memory tiles, A tiles streamed by TMA
-//                         through a 2-stage mbarrier ring, 28 tcgen05.mma.kind::i8 per
-//                         32-wide K step into 7 TMEM accumulators, tcgen05.ld epilogue.
+//                         through a 2-stage mbarrier ring, 39 tcgen05.mma.kind::i8 per
+//                         32-wide K step into 9 TMEM accumulators, tcgen05.ld epilogue.
 #pragma once
 
 #include "tc_common.cuh"
@@ -56,7 +56,7 @@ __global__ void oz_split_rows_kernel(const double* __restrict__ X, int rows, int
 
 struct GemmArgs {
   const double* B;  // N x K row-major (fp64)
-  int M, N, K, Kp;  // N multiple of 8, <= 64; Kp multiple of 128, <= 256
+  int M, N, K, Kp;  // N multiple of 8, <= 56; Kp multiple of 128, <= 256
   const int* ea;    // [Mp] A row scale exponents
   const double* l1a;
   double* D;        // M x N
@@ -126,10 +126,10 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
       const uint64_t adesc = tc::sdesc_sw128(aring + s * kTileBytes);
 #pragma unroll 1
       for (int kk = 0; kk < kTileK / 32; ++kk) {
-        for (int u = 0; u + t < kGroups; ++u) {
+        for (int u = 0; u < kSlices && u + t < kGroups; ++u) {
           const uint64_t bdesc = tc::sdesc_sw128(bsl + (u * nkc + kc) * btile);
           tc::mma_i8(tmem + (t + u) * N, tc::sdesc_add(adesc, 32 * kk), tc::sdesc_add(bdesc, 32 * kk), idesc,
-                     (kc | t | kk) != 0);
+                     !(kc == 0 && kk == 0 && (t == 0 || u == kSlices - 1)));  // first write of level t + u
         }
       }
       tc::mma_commit(bar + 2 + s);
@@ -169,6 +169,63 @@ __global__ void __launch_bounds__(128, 1) oz_gemm_kernel(const __grid_constant__
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_free(tmem, 512);
+}
+
+// Issue-rate probe: `count` back-to-back MMAs (M = 128, N, K = 32, A and B from shared memory, one
+// accumulator; `naccum` > 1 rotates the destination over that many accumulators), timed by thread 0.
+__global__ void __launch_bounds__(128, 1) oz_mma_rate_kernel(int count, int N, int naccum, long long* cycles) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 65536);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 65536 / 4; i += blockDim.x) reinterpret_cast<int*>(sm)[i] = 0x01010101 * (i & 3);
+  if (tid < 32) tc::tmem_alloc(slot, 512);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *slot;
+  const int mode = naccum >> 8;
+  naccum &= 255;
+  if (mode == 0 && tid == 0) {
+    const uint32_t idesc = tc::idesc_i8(128, N);
+    const uint64_t a = tc::sdesc_sw128(sm), b = tc::sdesc_sw128(sm + 32768);
+    const long long t0 = clock64();
+    for (int i = 0; i < count; ++i)
+      tc::mma_i8(tmem + (i % naccum) * N, tc::sdesc_add(a, 32 * (i & 3)), tc::sdesc_add(b, 32 * (i & 3)), idesc, 1);
+    tc::mma_commit(bar);
+    mbar_wait(bar, 0);
+    const long long t1 = clock64();
+    cycles[0] = t1 - t0;
+  } else if (mode == 1 && tid < 32) {  // converged warp, elected lane inside the asm
+    const uint32_t idesc = tc::idesc_i8(128, N);
+    const uint64_t a = tc::sdesc_sw128(sm), b = tc::sdesc_sw128(sm + 32768);
+    const long long t0 = clock64();
+    for (int i = 0; i < count; ++i)
+      tc::mma_i8_warp(tmem + (i % naccum) * N, tc::sdesc_add(a, 32 * (i & 3)), tc::sdesc_add(b, 32 * (i & 3)), idesc,
+                      1);
+    tc::mma_commit_warp(bar);
+    mbar_wait(bar, 0);
+    const long long t1 = clock64();
+    if (tid == 0) cycles[0] = t1 - t0;
+  } else if (mode == 2 && tid == 0) {  // one thread, loop-invariant operands
+    const uint32_t idesc = tc::idesc_i8(128, N);
+    const uint64_t a = tc::sdesc_sw128(sm), b = tc::sdesc_sw128(sm + 32768);
+    const long long t0 = clock64();
+    for (int i = 0; i < count; ++i) tc::mma_i8(tmem, a, b, idesc, 1);
+    tc::mma_commit(bar);
+    mbar_wait(bar, 0);
+    const long long t1 = clock64();
+    cycles[0] = t1 - t0;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (tid < 32) tc::tmem_free(tmem, 512);
 }
 
 }  // namespace oz

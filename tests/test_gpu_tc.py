@@ -1,5 +1,5 @@
 """GPU: the tensor-core contraction primitive (tcgen05.mma kind::i8, Ozaki split into 7 int8
-slices, 28 slice pairs in 7 exact int32 TMEM accumulators, TMA-fed A tiles) against an
+slices, 39 slice pairs in 9 exact int32 TMEM accumulators, TMA-fed A tiles) against an
 extended-precision product.  Checks the value (fp64-grade) and that the rigorous per-element
 bound really bounds the error."""
 import numpy as np
@@ -12,7 +12,7 @@ def _exact(A, B):
     return (A.astype(np.longdouble) @ B.astype(np.longdouble).T)
 
 
-@pytest.mark.parametrize("M,N,K,seed", [(128, 8, 32, 0), (200, 64, 256, 1), (90, 72 - 8, 90, 2), (256, 24, 256, 3),
+@pytest.mark.parametrize("M,N,K,seed", [(128, 8, 32, 0), (200, 56, 256, 1), (90, 72 - 8, 90, 2), (256, 24, 256, 3),
                                         (37, 16, 7, 4)])
 def test_ozaki_gemm_value_and_bound(M, N, K, seed):
     from paper_2605_25346_b200 import default_context
