@@ -191,6 +191,42 @@ int reach_ctx_create(int32_t device, reach_ctx** out);
 int reach_ctx_destroy(reach_ctx* ctx);
 /* Work is enqueued on this stream (cudaStream_t; NULL = the ctx's own). */
 int reach_ctx_set_stream(reach_ctx* ctx, void* cuda_stream);
+
+/* ---- Multi-GPU: one process (or host thread) per GPU, each with its own ctx.
+ * Once a ctx has collectives, the batch entry points that the reference runs in
+ * one parallel_for -- reach_split_hull, reach_cl_split_hull, reach_ct_split_hull
+ * (refine.hpp:121-160) and reach_plan_cem / reach_plan_cem_ex (mpc.hpp:300-304) --
+ * shard their batch over the ranks (contiguous part / candidate ranges) and
+ * combine on the ctx stream: the hull with one all-reduce per buffer (min / max of
+ * order-preserving keys -- exact and order independent), the CEM scores with one
+ * all-gather per iteration.  Every rank passes the full problem and receives the
+ * full result, bit-identical to the single-GPU call.
+ *
+ * Built-in NCCL (over NVLink / NVSwitch): rank 0 calls reach_nccl_unique_id, the
+ * 128-byte id reaches every rank out of band, every rank calls
+ * reach_ctx_init_nccl on its ctx.  NCCL is loaded at run time (dlopen of
+ * libnccl.so.2), so the library has no link dependency on it.
+ * User collectives: reach_ctx_set_collectives with callbacks that reduce /
+ * gather device buffers ordered on the given stream (e.g. torch.distributed). */
+#define REACH_DT_U64 0
+#define REACH_DT_I32 1
+#define REACH_DT_F64 2
+#define REACH_OP_MIN 0
+#define REACH_OP_MAX 1
+typedef struct reach_collectives {
+  int32_t rank;
+  int32_t world;
+  /* in-place all-reduce of `count` elements (REACH_DT_*, REACH_OP_*) at device pointer `buf` */
+  int (*allreduce)(void* user, void* buf, size_t count, int32_t dtype, int32_t op, void* cuda_stream);
+  /* all-gather: `count` elements per rank from `send` into `recv` ([world][count], rank order) */
+  int (*allgather)(void* user, const void* send, void* recv, size_t count, int32_t dtype, void* cuda_stream);
+  void* user;
+} reach_collectives;
+int reach_nccl_unique_id(uint8_t out_id[128]);
+int reach_ctx_init_nccl(reach_ctx* ctx, const uint8_t unique_id[128], int32_t world, int32_t rank);
+int reach_ctx_set_collectives(reach_ctx* ctx, const reach_collectives* coll); /* NULL: back to one GPU */
+/* Blocking copy between host / device memory of this ctx's device (cudaMemcpyDefault). */
+int reach_ctx_memcpy(reach_ctx* ctx, void* dst, const void* src, size_t bytes);
 int reach_ctx_synchronize(reach_ctx* ctx);
 const char* reach_ctx_last_error(const reach_ctx* ctx);
 /* Number of kernels this ctx has launched so far. */

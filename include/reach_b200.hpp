@@ -31,6 +31,7 @@
 // reach_b200_reference.hpp (drop-in overloads taking reach:: types).
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <functional>
 #include <limits>
@@ -121,6 +122,20 @@ class Context {
   Context& operator=(const Context&) = delete;
 
   reach_ctx* raw() const { return ctx_; }
+
+  // Multi-GPU (one Context per GPU, one process or host thread each): after init_nccl, the batch
+  // calls -- reach_with_splitting*, plan_cem -- shard over the ranks inside the library and every
+  // rank returns the full single-GPU result (include/reach_b200.h, "Multi-GPU").
+  static std::array<uint8_t, 128> nccl_unique_id() {
+    std::array<uint8_t, 128> id{};
+    if (reach_nccl_unique_id(id.data()) != REACH_OK) throw Error("reach_nccl_unique_id: NCCL not loadable");
+    return id;
+  }
+  void init_nccl(const std::array<uint8_t, 128>& id, int world, int rank) {
+    check(reach_ctx_init_nccl(ctx_, id.data(), world, rank), "reach_ctx_init_nccl");
+  }
+  void set_collectives(const reach_collectives& c) { check(reach_ctx_set_collectives(ctx_, &c), "set_collectives"); }
+  void single_gpu() { check(reach_ctx_set_collectives(ctx_, nullptr), "set_collectives"); }
 
   void check(int rc, const char* what) const {
     if (rc == REACH_OK) return;

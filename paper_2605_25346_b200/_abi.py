@@ -203,3 +203,15 @@ FIELD_ZERO, FIELD_DIAG_LINEAR, FIELD_ROTATION, FIELD_QUADROTOR = 0, 1, 2, 3
 
 class FieldDescC(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("params", C.c_double * 16)]
+
+
+# ---- multi-GPU collectives (include/reach_b200.h, "Multi-GPU")
+REACH_DT_U64, REACH_DT_I32, REACH_DT_F64 = 0, 1, 2
+REACH_OP_MIN, REACH_OP_MAX = 0, 1
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+
+
+class Collectives(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("allreduce", ALLREDUCE_FN), ("allgather", ALLGATHER_FN),
+                ("user", C.c_void_p)]

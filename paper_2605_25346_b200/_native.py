@@ -85,6 +85,14 @@ def _declare(lib):
               "reach_cem_sample", "reach_cem_update", "reach_cem_result"):
         getattr(lib, f).restype = C.c_int
     lib.reach_debug_phase_cycles.restype = C.c_int
+    lib.reach_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+    lib.reach_nccl_unique_id.restype = C.c_int
+    lib.reach_ctx_init_nccl.argtypes = [vp, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]
+    lib.reach_ctx_init_nccl.restype = C.c_int
+    lib.reach_ctx_set_collectives.argtypes = [vp, C.POINTER(A.Collectives)]
+    lib.reach_ctx_set_collectives.restype = C.c_int
+    lib.reach_ctx_memcpy.argtypes = [vp, vp, vp, C.c_size_t]
+    lib.reach_ctx_memcpy.restype = C.c_int
     lib.reach_debug_ozaki_gemm.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, dp, dp, dp, dp]
     lib.reach_debug_ozaki_gemm.restype = C.c_int
     for f in ("reach_ctx_create", "reach_ctx_destroy", "reach_ctx_set_stream", "reach_ctx_synchronize",
@@ -163,6 +171,47 @@ class Context:
 
     MAX_CACHED_NETS = 32
 
+    # ---- multi-GPU (the batch entry points shard over the ranks once collectives are set)
+    def init_nccl(self, unique_id: bytes, world: int, rank: int):
+        """The built-in NCCL communicator (one rank per GPU); `unique_id` from nccl_unique_id() on rank 0."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        self.check(self._lib.reach_ctx_init_nccl(self.handle, buf, int(world), int(rank)), "reach_ctx_init_nccl")
+
+    def set_collectives(self, rank: int, world: int, allreduce, allgather):
+        """User collectives: allreduce(np_array, op) -> np_array and allgather(np_array) -> np_array
+        [world * count] on host arrays; the library's device buffers are staged through the host."""
+        import numpy as np
+        dtypes = {A.REACH_DT_U64: np.uint64, A.REACH_DT_I32: np.int32, A.REACH_DT_F64: np.float64}
+        lib, h = self._lib, self.handle
+
+        def ar(user, buf, count, dtype, op, stream):
+            try:
+                a = np.empty(count, dtypes[dtype])
+                lib.reach_ctx_memcpy(h, a.ctypes.data, buf, a.nbytes)
+                r = np.ascontiguousarray(allreduce(a, "min" if op == A.REACH_OP_MIN else "max"), dtypes[dtype])
+                lib.reach_ctx_memcpy(h, buf, r.ctypes.data, r.nbytes)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def ag(user, send, recv, count, dtype, stream):
+            try:
+                a = np.empty(count, dtypes[dtype])
+                lib.reach_ctx_memcpy(h, a.ctypes.data, send, a.nbytes)
+                r = np.ascontiguousarray(allgather(a), dtypes[dtype])
+                lib.reach_ctx_memcpy(h, recv, r.ctypes.data, r.nbytes)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self._coll_keep = (A.ALLREDUCE_FN(ar), A.ALLGATHER_FN(ag))
+        c = A.Collectives(int(rank), int(world), self._coll_keep[0], self._coll_keep[1], None)
+        self.check(self._lib.reach_ctx_set_collectives(self.handle, C.byref(c)), "reach_ctx_set_collectives")
+
+    def clear_collectives(self):
+        self.check(self._lib.reach_ctx_set_collectives(self.handle, None), "reach_ctx_set_collectives")
+        self._coll_keep = None
+
     def ozaki_gemm(self, A, B):
         """Test hook: the tensor-core (Ozaki int8 tcgen05) product A . B^T and its rigorous error bound."""
         import numpy as np
@@ -214,6 +263,15 @@ class Context:
 
 
 _default = {}
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0; broadcast it to the other ranks out of band)."""
+    buf = (C.c_uint8 * 128)()
+    rc = lib().reach_nccl_unique_id(buf)
+    if rc != A.REACH_OK:
+        raise ReachError(f"reach_nccl_unique_id failed (code {rc}): NCCL not loadable")
+    return bytes(buf)
 
 
 def _current_device() -> int:

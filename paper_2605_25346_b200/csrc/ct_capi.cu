@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "coll.h"
 #include "ct_kernel.cuh"
 #include "ctx.cuh"
 
@@ -434,8 +435,10 @@ int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spe
     if (!std::isfinite(a->x0_lo[d]) || !std::isfinite(a->x0_hi[d]))
       return fail(ctx, REACH_E_INVALID_ARGUMENT, "build_linear_tm: diverged box");
   }
-  const long long begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
-  if (begin < 0 || begin >= end || end > total) return fail(ctx, REACH_E_INVALID_ARGUMENT, "bad part range");
+  const long long begin0 = a->part_begin, end0 = a->part_end <= 0 ? total : a->part_end;
+  if (begin0 < 0 || begin0 >= end0 || end0 > total) return fail(ctx, REACH_E_INVALID_ARGUMENT, "bad part range");
+  long long begin, end;  // multi-GPU: this rank's slice; the hull is all-reduced below
+  rbh::coll_shard(ctx, begin0, end0, begin, end);
   RB_CUDA(cudaSetDevice(ctx->device));
   const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
   rb::ct::CTParams P{};
@@ -473,7 +476,12 @@ int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spe
   ct_hull_init_kernel<<<std::max((std::max(icount, static_cast<int>(T)) + tpb - 1) / tpb, 1), tpb, 0, ctx->stream>>>(
       P.hull_lo, P.hull_hi, P.hull_nan0, P.hull_div, icount, static_cast<int>(T), P.hull_nboxes, P.hull_fail_key);
   RB_CUDA(cudaGetLastError());
-  rc = launch_cl(ctx, P);
+  if (P.B > 0) {
+    rc = launch_cl(ctx, P);
+    if (rc) return rc;
+  }
+  rc = rbh::coll_hull(ctx, P.hull_lo, P.hull_hi, P.hull_nan0, 2 * icount, P.hull_div, static_cast<int>(T),
+                      P.hull_nboxes, P.hull_fail_key);
   if (rc) return rc;
   double* dlo = dev ? out->lo : reinterpret_cast<double*>(w + o_lo);
   double* dhi = dev ? out->hi : reinterpret_cast<double*>(w + o_hi);
@@ -654,8 +662,10 @@ int reach_ct_split_hull(reach_ctx* ctx, const reach_field_desc* fd, const reach_
     if (!std::isfinite(a->x0_lo[d]) || !std::isfinite(a->x0_hi[d]))
       return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: non-finite X0");
   }
-  const long long begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
-  if (begin < 0 || begin >= end || end > total) return fail(ctx, REACH_E_INVALID_ARGUMENT, "bad part range");
+  const long long begin0 = a->part_begin, end0 = a->part_end <= 0 ? total : a->part_end;
+  if (begin0 < 0 || begin0 >= end0 || end0 > total) return fail(ctx, REACH_E_INVALID_ARGUMENT, "bad part range");
+  long long begin, end;  // multi-GPU: this rank's slice; the hull is all-reduced below
+  rbh::coll_shard(ctx, begin0, end0, begin, end);
   RB_CUDA(cudaSetDevice(ctx->device));
   const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
   P.B = static_cast<int>(end - begin);
@@ -687,7 +697,12 @@ int reach_ct_split_hull(reach_ctx* ctx, const reach_field_desc* fd, const reach_
   ct_hull_init_kernel<<<std::max((std::max(icount, static_cast<int>(T)) + tpb - 1) / tpb, 1), tpb, 0, ctx->stream>>>(
       P.hull_lo, P.hull_hi, P.hull_nan0, P.hull_div, icount, static_cast<int>(T), P.hull_nboxes, P.hull_fail_key);
   RB_CUDA(cudaGetLastError());
-  rc = launch_ct(ctx, P);
+  if (P.B > 0) {
+    rc = launch_ct(ctx, P);
+    if (rc) return rc;
+  }
+  rc = rbh::coll_hull(ctx, P.hull_lo, P.hull_hi, P.hull_nan0, 2 * icount, P.hull_div, static_cast<int>(T),
+                      P.hull_nboxes, P.hull_fail_key);
   if (rc) return rc;
   double* dlo = dev ? out->lo : reinterpret_cast<double*>(w + o_lo);
   double* dhi = dev ? out->hi : reinterpret_cast<double*>(w + o_hi);

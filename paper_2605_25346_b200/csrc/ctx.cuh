@@ -35,6 +35,10 @@ struct reach_ctx {
   void* wws = nullptr;
   size_t wws_bytes = 0;
   unsigned long long* wphase = nullptr;  // wide-kernel phase counters (RB_WIDE_PHASE=1)
+  // multi-GPU collectives (coll.cu): user callbacks or the built-in NCCL communicator
+  reach_collectives coll{};
+  bool has_coll = false;
+  void* nccl_comm = nullptr;
   // kernel timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;

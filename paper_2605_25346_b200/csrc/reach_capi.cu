@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "coll.h"
 #include "tc_capi.h"
 #include "../../include/reach_b200.h"
 #include "diag.cuh"
@@ -382,6 +383,7 @@ int reach_ctx_destroy(reach_ctx* ctx) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx) return REACH_OK;
   cudaSetDevice(ctx->device);
+  rbh::coll_release(ctx);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->pbuf) cudaFree(ctx->pbuf);
   if (ctx->wws) cudaFree(ctx->wws);
@@ -735,12 +737,16 @@ int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_arg
     total *= a->counts[d];
     if (total > (1ll << 20)) return fail(ctx, REACH_E_INVALID_ARGUMENT, "SplitPlan: total part count overflow");
   }
-  const long long begin = a->part_begin, end = a->part_end <= 0 ? total : a->part_end;
-  if (begin < 0 || begin >= end || end > total) return fail(ctx, REACH_E_INVALID_ARGUMENT, "bad part range");
+  const long long begin0 = a->part_begin, end0 = a->part_end <= 0 ? total : a->part_end;
+  if (begin0 < 0 || begin0 >= end0 || end0 > total) return fail(ctx, REACH_E_INVALID_ARGUMENT, "bad part range");
+  // multi-GPU: this rank's contiguous slice of the parts; the hull is all-reduced below
+  long long begin, end;
+  rbh::coll_shard(ctx, begin0, end0, begin, end);
   RB_CUDA(cudaSetDevice(ctx->device));
   rb::DTParams P{};
   DTLayout lay;
-  rc = plan_dt(ctx, net, a->n, a->m, a->window, end - begin, P, lay, nullptr, flags & REACH_FLAG_PREC_MASK);
+  rc = plan_dt(ctx, net, a->n, a->m, a->window, std::max(end - begin, 1ll), P, lay, nullptr,
+               flags & REACH_FLAG_PREC_MASK);
   if (rc) return rc;
   const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
   const int n = a->n, H = a->horizon, m = a->m;
@@ -794,11 +800,16 @@ int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_arg
   hull_init_kernel<<<blocks, tpb, 0, ctx->stream>>>(P.hull_lo, P.hull_hi, P.hull_nan0, P.hull_div, icount, H + 1,
                                                      P.hull_nboxes, P.hull_fail_key);
   RB_CUDA(cudaGetLastError());
-  cudaEvent_t stop;
-  rc = timed_begin(ctx, &stop);
-  if (rc) return rc;
-  RB_CUDA(launch_dt(P, lay, P.B, ctx->stream));
-  rc = timed_end(ctx, stop);
+  if (P.B > 0) {
+    cudaEvent_t stop;
+    rc = timed_begin(ctx, &stop);
+    if (rc) return rc;
+    RB_CUDA(launch_dt(P, lay, P.B, ctx->stream));
+    rc = timed_end(ctx, stop);
+    if (rc) return rc;
+  }
+  rc = rbh::coll_hull(ctx, P.hull_lo, P.hull_hi, P.hull_nan0, 2 * icount, P.hull_div, H + 1, P.hull_nboxes,
+                      P.hull_fail_key);
   if (rc) return rc;
   double* dlo = dev ? out->lo : reinterpret_cast<double*>(w + o_lo);
   double* dhi = dev ? out->hi : reinterpret_cast<double*>(w + o_hi);
@@ -1023,6 +1034,60 @@ int plan_eval_host(reach_ctx* ctx, const reach_net* net, const reach_plan_proble
     RB_CUDA(cudaMemcpyAsync(tubes->status, I(o_st), B * 4, cudaMemcpyDeviceToHost, ctx->stream));
   }
   RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return REACH_OK;
+}
+
+// plan_eval of a CEM population with multi-GPU collectives: this rank evaluates its contiguous slice,
+// one all-gather per output array (padded to ceil(pop / world) per rank) assembles every rank's
+// scores in candidate order, so all ranks run the identical sort / refit (mpc.hpp:300-333).
+int plan_eval_sharded(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* p, const double* x0, int pop,
+                      const double* actions, double* objective, int32_t* diverged) {
+  if (!ctx->has_coll || ctx->coll.world <= 1)
+    return plan_eval_host(ctx, net, p, x0, pop, actions, objective, diverged, nullptr);
+  const int world = ctx->coll.world;
+  long long b, e;
+  rbh::coll_shard(ctx, 0, pop, b, e);
+  const size_t width = (static_cast<size_t>(pop) + world - 1) / world, B = static_cast<size_t>(e - b);
+  const size_t H = p->horizon, n = p->n, m = p->m, box = std::max<size_t>(B, 1) * (H + 1) * n * 8;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t o_x0 = take(n * 8), o_a = take(B * H * m * 8), o_obj = take(width * 8), o_div = take(width * 4),
+               o_go = take(world * width * 8), o_gd = take(world * width * 4), o_lo = take(box), o_hi = take(box),
+               o_nb = take(B * 4), o_fs = take(B * 4), o_st = take(B * 4);
+  int rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto D = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  auto I = [&](size_t o) { return reinterpret_cast<int*>(w + o); };
+  RB_CUDA(cudaMemsetAsync(w + o_obj, 0, width * 8, ctx->stream));
+  RB_CUDA(cudaMemsetAsync(w + o_div, 0, width * 4, ctx->stream));
+  if (B > 0) {
+    RB_CUDA(cudaMemcpyAsync(D(o_x0), x0, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (m) RB_CUDA(cudaMemcpyAsync(D(o_a), actions + b * H * m, B * H * m * 8, cudaMemcpyHostToDevice, ctx->stream));
+    rc = plan_eval_device(ctx, net, p, D(o_x0), static_cast<int>(B), D(o_a), D(o_obj), I(o_div), D(o_lo), D(o_hi),
+                          I(o_nb), I(o_fs), I(o_st));
+    if (rc) return rc;
+  }
+  rc = rbh::coll_allgather(ctx, D(o_obj), D(o_go), width, REACH_DT_F64);
+  if (!rc) rc = rbh::coll_allgather(ctx, I(o_div), I(o_gd), width, REACH_DT_I32);
+  if (rc) return rc;
+  std::vector<double> go(world * width);
+  std::vector<int32_t> gd(world * width);
+  RB_CUDA(cudaMemcpyAsync(go.data(), D(o_go), go.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(gd.data(), I(o_gd), gd.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int r = 0; r < world; ++r) {
+    const long long total = pop, base = total / world, rem = total % world;
+    const long long rb0 = r * base + std::min<long long>(r, rem), cnt = base + (r < rem ? 1 : 0);
+    for (long long k = 0; k < cnt; ++k) {
+      objective[rb0 + k] = go[r * width + k];
+      diverged[rb0 + k] = gd[r * width + k];
+    }
+  }
   return REACH_OK;
 }
 
@@ -1473,7 +1538,7 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
       }
       std::copy(u.begin(), u.end(), cand + k * dim);
     }
-    rc = plan_eval_host(ctx, net, prob, x0, static_cast<int>(pop), cand, scores, div, nullptr);
+    rc = plan_eval_sharded(ctx, net, prob, x0, static_cast<int>(pop), cand, scores, div);
     if (rc) return rc;
     for (size_t k = 0; k < pop; ++k) okv[k] = div[k] ? 0 : 1;
     reach_cem_update(c, scores, okv.data());

@@ -206,3 +206,44 @@ def sharded_grad_tube_volume(sys, x0, actions, target, method=0, prm=None, group
         parts.append(o[: re_ - rb_].cpu().numpy())
         any_sub = any_sub or bool(o[width].item() != 0.0)
     return Gradient(np.concatenate(parts) if parts else np.zeros(0), GradMethod(method), any_sub)
+
+
+def torch_collectives(ctx, group=None):
+    """Gives `ctx` the collectives of a torch.distributed group (gloo or NCCL process groups; the
+    library's device buffers are staged through host tensors).  Afterwards reach_split_hull,
+    cl_split_hull, ct_split_hull and plan_cem on `ctx` shard over the group inside the library
+    (include/reach_b200.h, "Multi-GPU") -- the C-ABI counterpart of the sharded_* helpers above."""
+    import torch
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = _device_for(group)
+    sign = np.uint64(1 << 63)
+
+    def allreduce(a, op):
+        u64 = a.dtype == np.uint64
+        v = (a ^ sign).view(np.int64) if u64 else a  # order keys: flip the sign bit, compare as int64
+        t = torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN if op == "min" else dist.ReduceOp.MAX, group=group)
+        r = t.cpu().numpy()
+        return (r.view(np.uint64) ^ sign) if u64 else r
+
+    def allgather(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t, group=group)
+        return np.concatenate([o.cpu().numpy() for o in out])
+
+    ctx.set_collectives(rank, world, allreduce, allgather)
+    return ctx
+
+
+def nccl_collectives(ctx, group=None):
+    """Gives `ctx` the library's built-in NCCL communicator over the ranks of `group` (the unique id
+    travels by torch.distributed.broadcast_object_list)."""
+    from ._native import nccl_unique_id
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.init_nccl(obj[0], world, rank)
+    return ctx
