@@ -232,13 +232,9 @@ def mpc_replan(args, ctx, world, rank, dev, barrier):
     prob, cfg, x0 = c3_tpushing()
     ctx.set_stream(None)
 
-    def once():
-        if world == 1:
-            r = plan_cem(prob, cfg, x0, ctx=ctx)
-            return r.actions, r.objective
-        from paper_2605_25346_b200.distributed import sharded_plan_cem
-        best, obj, _, _ = sharded_plan_cem(prob, cfg, x0)
-        return best, obj
+    def once():  # N > 1: the library shards the population (ctx collectives), same pipeline as N = 1
+        r = plan_cem(prob, cfg, x0, ctx=ctx)
+        return r.actions, r.objective
 
     reps = max(2, min(args.steps, 5))
     once()
@@ -382,7 +378,7 @@ def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
     cs, keep = spec.c_struct()
     cts = np.array(counts, dtype=np.int32)
     x0lo, x0hi = np.ascontiguousarray(w.x0_lo), np.ascontiguousarray(w.x0_hi)
-    args_c = A.CLSplitArgs(A.dptr(x0lo), A.dptr(x0hi), A.iptr(cts), begin, end)
+    args_c = A.CLSplitArgs(A.dptr(x0lo), A.dptr(x0hi), A.iptr(cts), 0, 0)  # full plan; the library shards
     out_c = A.HullOut(A.dptr(d_lo.data_ptr()), A.dptr(d_hi.data_ptr()), A.iptr(d_div.data_ptr()),
                       A.iptr(d_nb.data_ptr()), A.lptr(d_key.data_ptr()))
     net = ctx.upload(spec.controller)
@@ -390,13 +386,6 @@ def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
     def step():
         ctx.check(ctx._lib.reach_cl_split_hull(ctx.handle, net, C.byref(cs), C.byref(args_c), C.byref(out_c),
                                                A.REACH_FLAG_DEVICE_PTRS), "reach_cl_split_hull")
-        if world > 1:
-            lo_ = torch.where(torch.isnan(d_lo), torch.full_like(d_lo, float("inf")), d_lo)
-            dist.all_reduce(lo_, op=dist.ReduceOp.MIN)
-            dist.all_reduce(d_hi, op=dist.ReduceOp.MAX)
-            dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
-            dist.all_reduce(d_nb, op=dist.ReduceOp.MIN)
-            d_lo.copy_(lo_)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -424,11 +413,7 @@ def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
     for i in range(5):
         barrier()
         t0 = time.perf_counter()
-        hres = cl_split_hull(spec, (w.x0_lo, w.x0_hi), plan, begin, end, ctx=_host_ctx(ctx))
-        if world > 1:
-            hl = torch.tensor(np.where(np.isnan(hres.lo), np.inf, hres.lo), device=dev)
-            dist.all_reduce(hl, op=dist.ReduceOp.MIN)
-            hl.cpu()
+        hres = cl_split_hull(spec, (w.x0_lo, w.x0_hi), plan, ctx=_host_ctx(ctx))
         if i >= 2:
             e2e.append(time.perf_counter() - t0)
     ctx.set_stream(stream.cuda_stream)
@@ -652,6 +637,11 @@ def main():
     H, n, m = w.horizon, w.sys.n, w.sys.m
 
     ctx = Context(local)
+    if world > 1:
+        # the library shards every batch call over the ranks and combines on its stream (NCCL over
+        # NVLink; gloo staging only for the shared-GPU logic check)
+        from paper_2605_25346_b200.distributed import nccl_collectives, torch_collectives
+        (torch_collectives if share else nccl_collectives)(ctx)
     stream = torch.cuda.Stream(dev)  # the library launches here; torch work joins it below
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
@@ -669,8 +659,8 @@ def main():
     x0lo = np.ascontiguousarray(w.x0_lo)
     x0hi = np.ascontiguousarray(w.x0_hi)
     cts = np.array(counts, dtype=np.int32)
-    args_c = A.SplitArgs(n, m, H, 4, 0, A.dptr(x0lo), A.dptr(x0hi), A.iptr(cts), A.dptr(d_act.data_ptr()),
-                         begin, end)
+    # the full global plan on every rank: the library takes this rank's contiguous slice of the parts
+    args_c = A.SplitArgs(n, m, H, 4, 0, A.dptr(x0lo), A.dptr(x0hi), A.iptr(cts), A.dptr(d_act.data_ptr()), 0, 0)
     out_c = A.HullOut(A.dptr(d_lo.data_ptr()), A.dptr(d_hi.data_ptr()), A.iptr(d_div.data_ptr()),
                       A.iptr(d_nb.data_ptr()), A.lptr(d_key.data_ptr()))
     net = ctx.upload(w.sys.step)
@@ -679,13 +669,6 @@ def main():
     def device_step():
         ctx.check(ctx._lib.reach_split_hull(ctx.handle, net, C.byref(args_c), C.byref(out_c),
                                             A.REACH_FLAG_DEVICE_PTRS), "reach_split_hull")
-        if world > 1:
-            lo_ = torch.where(torch.isnan(d_lo), torch.full_like(d_lo, float("inf")), d_lo)
-            dist.all_reduce(lo_, op=dist.ReduceOp.MIN)
-            dist.all_reduce(d_hi, op=dist.ReduceOp.MAX)
-            dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
-            dist.all_reduce(d_nb, op=dist.ReduceOp.MIN)
-            d_lo.copy_(lo_)
 
     def barrier():
         if world > 1:
@@ -735,13 +718,7 @@ def main():
     for i in range(args.warmup + args.steps):
         barrier()
         t0 = time.perf_counter()
-        res = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, DTReachParams(), begin, end, ctx=ctx)
-        if world > 1:
-            hl = torch.tensor(np.where(np.isnan(res.lo), np.inf, res.lo), device=dev)
-            hh = torch.tensor(res.hi, device=dev)
-            dist.all_reduce(hl, op=dist.ReduceOp.MIN)
-            dist.all_reduce(hh, op=dist.ReduceOp.MAX)
-            hl.cpu(), hh.cpu()
+        res = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, DTReachParams(), ctx=ctx)
         dt_ = time.perf_counter() - t0
         if i >= args.warmup:
             e2e_t.append(dt_)
@@ -776,7 +753,8 @@ def main():
     if rank == 0:
         try:
             from oracle_bind import oracle_split_hull, same_bits
-            g = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=0, part_end=64, ctx=ctx)
+            solo = ctx if world == 1 else Context(local)  # rank-0-only call: a context without collectives
+            g = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=0, part_end=64, ctx=solo)
             e = oracle_split_hull(w.sys, w.x0_lo, w.x0_hi, plan, w.actions, begin=0, end=64)
             parity = {"parts": 64, "bit_exact": bool(same_bits(g.lo, e.lo) and same_bits(g.hi, e.hi)
                                                      and g.n_boxes == e.n_boxes)}
