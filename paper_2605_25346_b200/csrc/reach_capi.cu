@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "cem_kernel.cuh"
 #include "coll.h"
 #include "tc_capi.h"
 #include "../../include/reach_b200.h"
@@ -954,8 +955,6 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
   if (need > ctx->pbuf_bytes) {
     RB_CUDA(cudaStreamSynchronize(ctx->stream));
     if (ctx->pbuf) cudaFree(ctx->pbuf);
-  if (ctx->wws) cudaFree(ctx->wws);
-  if (ctx->wphase) cudaFree(ctx->wphase);
     ctx->pbuf = nullptr;
     RB_CUDA(cudaMalloc(&ctx->pbuf, need));
     ctx->pbuf_bytes = need;
@@ -1453,7 +1452,11 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
   // worker thread (same sequential order as mpc.hpp:290-299) while the device
   // evaluates the previous population.
   const size_t per_it0 = pop * dim, per_it = (pop - 1) * dim;
-  std::vector<double> z(per_it0 + static_cast<size_t>(iters - 1) * per_it);
+  // the whole normal stream of the replan in pinned host memory: uploaded per iteration, async
+  const size_t z_count = per_it0 + static_cast<size_t>(iters - 1) * per_it;
+  rc = ensure_pinned(ctx, z_count * sizeof(double));
+  if (rc) return rc;
+  double* z = static_cast<double*>(ctx->hpin);
   std::atomic<int> ready{0};
   // Rng::normal (rng.hpp:24-37) split in two: the uniform pairs (u1, u2; u1 redrawn while <= 0) are
   // drawn in stream order on the worker, then the Box-Muller transforms -- the same libm calls per
@@ -1480,7 +1483,7 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
         u1s[p] = u1;
         u2s[p] = u2;
       }
-      double* zz = z.data() + o + q;
+      double* zz = z + o + q;
       const size_t left = cnt - q;
       auto work = [&](size_t p0, size_t p1) {
         for (size_t p = p0; p < p1; ++p) {
@@ -1517,35 +1520,102 @@ int reach_plan_cem_ex(reach_ctx* ctx, const reach_net* net, const reach_plan_pro
       if (t.joinable()) t.join();
     }
   } joiner{gen};
-  // candidate population and scores in pinned host memory (full-bandwidth async copies)
-  const size_t cand_bytes = align_up(pop * dim * sizeof(double), 256);
-  rc = ensure_pinned(ctx, cand_bytes + pop * (sizeof(double) + sizeof(int32_t)));
+  // The sampler runs on the device (cem_kernel.cuh): the population, its scores and the CEM state stay
+  // in HBM across the iterations; the host only uploads each iteration's normals (async, pinned) and
+  // reads the result once.
+  const int H = prob->horizon, n = prob->n, m = prob->m;
+  const int world = (ctx->has_coll && ctx->coll.world > 1) ? ctx->coll.world : 1;
+  long long sb, se;
+  rbh::coll_shard(ctx, 0, static_cast<long long>(pop), sb, se);
+  const size_t width = (pop + world - 1) / world, nloc = static_cast<size_t>(se - sb);
+  const size_t box = std::max<size_t>(nloc, 1) * (H + 1) * n * 8;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t o_x0 = take(n * 8), o_z = take(pop * dim * 8), o_c = take(pop * dim * 8), o_s = take(pop * 8),
+               o_d = take(pop * 4), o_ls = take(width * 8), o_ld = take(width * 4), o_gs = take(world * width * 8),
+               o_gd = take(world * width * 4), o_mean = take(dim * 8), o_std = take(dim * 8), o_best = take(dim * 8),
+               o_bo = take(8), o_any = take(4), o_hist = take(iters * 8), o_lo = take(m * 8), o_hi = take(m * 8),
+               o_tlo = take(box), o_thi = take(box), o_nb = take(width * 4), o_fs = take(width * 4),
+               o_st = take(width * 4);
+  rc = ensure_ws(ctx, off);
   if (rc) return rc;
-  double* cand = static_cast<double*>(ctx->hpin);
-  double* scores = reinterpret_cast<double*>(static_cast<char*>(ctx->hpin) + cand_bytes);
-  int32_t* div = reinterpret_cast<int32_t*>(scores + pop);
-  std::vector<int32_t> okv(pop);
+  char* w = static_cast<char*>(ctx->ws);
+  auto D = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  auto I = [&](size_t o) { return reinterpret_cast<int*>(w + o); };
+  rb::cem::CemDev S{};
+  S.cand = D(o_c);
+  S.z = D(o_z);
+  S.score = D(o_s);
+  S.div = I(o_d);
+  S.mean = D(o_mean);
+  S.stdv = D(o_std);
+  S.best = D(o_best);
+  S.best_obj = D(o_bo);
+  S.any_finite = I(o_any);
+  S.hist = D(o_hist);
+  S.lo = D(o_lo);
+  S.hi = D(o_hi);
+  S.pop = static_cast<int>(pop);
+  S.dim = static_cast<int>(dim);
+  S.m = m;
+  S.n_elite = c->n_elite;
+  S.smoothing = cfg->smoothing;
+  RB_CUDA(cudaMemcpyAsync(D(o_x0), x0, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(D(o_lo), prob->u_lo, m * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(D(o_hi), prob->u_hi, m * 8, cudaMemcpyHostToDevice, ctx->stream));
+  rb::cem::cem_init_kernel<<<1, 256, 0, ctx->stream>>>(S, cfg->init_std);
+  RB_CUDA(cudaGetLastError());
+  int p2 = 1;
+  while (p2 < static_cast<int>(pop)) p2 <<= 1;
+  const size_t usmem = static_cast<size_t>(p2) * (8 + 4);
+  if (usmem > static_cast<size_t>(ctx->max_smem)) return fail(ctx, REACH_E_UNSUPPORTED, "CEM population too large");
+  RB_CUDA(cudaFuncSetAttribute(rb::cem::cem_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(usmem)));
+  const int gen_blocks = static_cast<int>(std::min<size_t>((pop * dim + 255) / 256, 4 * ctx->num_sms));
   size_t zo = 0;
   for (int it = 0; it < iters; ++it) {
     while (ready.load(std::memory_order_acquire) <= it) std::this_thread::yield();
-    for (size_t k = 0; k < pop; ++k) {  // reach_cem_sample with the pre-drawn normals
-      std::vector<double>& u = c->cands[k];
-      if (it > 0 && k == 0) {
-        u = c->best;
-      } else {
-        for (size_t q = 0; q < dim; ++q) u[q] = c->mean[q] + c->stdv[q] * z[zo++];
-        c->clip(u);
+    const size_t cnt = it == 0 ? per_it0 : per_it;
+    RB_CUDA(cudaMemcpyAsync(D(o_z), z + zo, cnt * 8, cudaMemcpyHostToDevice, ctx->stream));
+    zo += cnt;
+    rb::cem::cem_generate_kernel<<<gen_blocks, 256, 0, ctx->stream>>>(S, it);
+    RB_CUDA(cudaGetLastError());
+    if (world == 1) {
+      rc = plan_eval_device(ctx, net, prob, D(o_x0), static_cast<int>(pop), S.cand, D(o_s), I(o_d), D(o_tlo),
+                            D(o_thi), I(o_nb), I(o_fs), I(o_st));
+      if (rc) return rc;
+    } else {
+      RB_CUDA(cudaMemsetAsync(w + o_ls, 0, width * 8, ctx->stream));
+      RB_CUDA(cudaMemsetAsync(w + o_ld, 0, width * 4, ctx->stream));
+      if (nloc > 0) {
+        rc = plan_eval_device(ctx, net, prob, D(o_x0), static_cast<int>(nloc), S.cand + sb * dim, D(o_ls), I(o_ld),
+                              D(o_tlo), D(o_thi), I(o_nb), I(o_fs), I(o_st));
+        if (rc) return rc;
       }
-      std::copy(u.begin(), u.end(), cand + k * dim);
+      rc = rbh::coll_allgather(ctx, D(o_ls), D(o_gs), width, REACH_DT_F64);
+      if (!rc) rc = rbh::coll_allgather(ctx, I(o_ld), I(o_gd), width, REACH_DT_I32);
+      if (rc) return rc;
+      rb::cem::cem_unpad_kernel<<<std::max<int>(1, static_cast<int>((pop + 255) / 256)), 256, 0, ctx->stream>>>(
+          D(o_gs), I(o_gd), world, static_cast<int>(width), static_cast<int>(pop), D(o_s), I(o_d));
+      RB_CUDA(cudaGetLastError());
     }
-    rc = plan_eval_sharded(ctx, net, prob, x0, static_cast<int>(pop), cand, scores, div);
-    if (rc) return rc;
-    for (size_t k = 0; k < pop; ++k) okv[k] = div[k] ? 0 : 1;
-    reach_cem_update(c, scores, okv.data());
+    rb::cem::cem_update_kernel<<<1, 1024, usmem, ctx->stream>>>(S, it, p2);
+    RB_CUDA(cudaGetLastError());
+    ctx->launches += 2;
   }
+  // the one read-back of the replan
   double best_obj = 0.0;
-  int32_t be = 0;
-  reach_cem_result(c, best_actions, &best_obj, &be, best_history);
+  int32_t any = 0;
+  RB_CUDA(cudaMemcpyAsync(best_actions, S.best, dim * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(&best_obj, S.best_obj, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(&any, S.any_finite, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (best_history) RB_CUDA(cudaMemcpyAsync(best_history, S.hist, iters * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int32_t be = any ? 0 : 1;
   if (best_effort) *best_effort = be;
   if (refined) *refined = 0;
   // gradient refinement of the top candidate (mpc.hpp:337-361):
