@@ -121,11 +121,13 @@ int ref_dt_batch(const reach_net_desc* desc, const reach_dt_args* a, const reach
   return REACH_OK;
 }
 
-// reach_with_splitting(dt_reach, x0, plan) (refine.hpp:121-160).  With the full
-// part range and threads == 0 this calls the reference driver verbatim; with
-// a sub-range (a bounded CPU sample / one shard) it runs the same reference
-// pieces -- split_box, dt_reach per part in parallel_for, box_hull in
-// ascending index order -- on parts [begin, end).
+// reach_with_splitting(dt_reach, x0, plan) (refine.hpp:121-160) restricted to
+// parts [begin, end): it always reassembles the reference pieces -- split_box,
+// dt_reach per part in parallel_for, box_hull in ascending index order, the
+// failure key -- because the reference driver itself has no part range (a
+// bounded CPU sample / one shard needs one).  The driver verbatim is
+// ref_reach_with_splitting below; tests/test_oracle.py checks the two agree on
+// full plans.
 int ref_split_hull(const reach_net_desc* desc, const reach_split_args* a, const reach_hull_out* out,
                    int32_t threads) {
   try {

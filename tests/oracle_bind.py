@@ -111,6 +111,29 @@ def ref_split_hull(sys, x0_lo, x0_hi, plan, actions, prm=DTReachParams(), begin=
     return _hull(ref_lib(), "ref_", sys, x0_lo, x0_hi, plan, actions, prm, begin, end, threads)
 
 
+def ref_reach_with_splitting(sys, x0_lo, x0_hi, plan: SplitPlan, actions, prm=DTReachParams()):
+    """The reference's reach_with_splitting(dt_reach) driver verbatim (refine.hpp:121-160), full plan."""
+    acts = np.ascontiguousarray(np.asarray(actions, np.float64).reshape(-1, sys.m) if sys.m else np.zeros((0, 0)))
+    H = acts.shape[0] if sys.m else len(actions)
+    lo0 = np.ascontiguousarray(x0_lo, np.float64)
+    hi0 = np.ascontiguousarray(x0_hi, np.float64)
+    counts = np.array(plan.counts, np.int32)
+    lo = np.full((H + 1, sys.n), np.nan)
+    hi = np.full((H + 1, sys.n), np.nan)
+    nb = np.zeros(1, np.int32)
+    fs = np.zeros(1, np.int32)
+    desc, keep = sys.step.desc()
+    args = A.SplitArgs(sys.n, sys.m, H, prm.window, int(prm.rebuild_from_box), A.dptr(lo0), A.dptr(hi0),
+                       A.iptr(counts), A.dptr(acts if acts.size else np.zeros(1)), 0, 0)
+    f = ref_lib().ref_reach_with_splitting
+    f.argtypes = [C.POINTER(A.NetDesc), C.POINTER(A.SplitArgs), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                  C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    f.restype = C.c_int
+    rc = f(C.byref(desc), C.byref(args), A.dptr(lo), A.dptr(hi), A.iptr(nb), A.iptr(fs))
+    assert rc == 0, rc
+    return lo, hi, int(nb[0]), int(fs[0])
+
+
 def same_bits(a: np.ndarray, b: np.ndarray) -> bool:
     """Bitwise equality up to the sign of zero (NaN == NaN)."""
     a = np.asarray(a, np.float64)

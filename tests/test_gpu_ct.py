@@ -132,7 +132,10 @@ def test_cl_monte_carlo_enclosure():
     assert (t.status == 0).all()
     rng = np.random.default_rng(5)
     for bi in range(len(idx)):
-        x = rng.uniform(lo[idx[bi]], hi[idx[bi]], size=(500, 12)).T
+        # >= 1e3 rollouts per checked sub-box, the first 64 at box vertices
+        x = rng.uniform(lo[idx[bi]], hi[idx[bi]], size=(1000, 12))
+        x[:64] = np.where(rng.random((64, 12)) < 0.5, lo[idx[bi]], hi[idx[bi]])
+        x = x.T
         states = simulate_zoh(w.spec, x)
         for k in range(1, len(states)):
             assert (states[k].T >= t.lo[bi, k, :12] - 1e-10).all(), k

@@ -71,3 +71,35 @@ def test_c5_enclosure_monte_carlo():
         u = w.ctl.forward(x)
         x = w.dyn.forward(np.concatenate([x, u], axis=0))
         assert (x.T >= t.lo[0, k] - 1e-12).all() and (x.T <= t.hi[0, k] + 1e-12).all()
+
+
+@pytest.mark.parametrize("precision", ["exact", "tc"])
+def test_c5_full_batch_strided(precision):
+    """The bench's C5 workload at its full size (batch 1024): 32 strided samples against the oracle --
+    bit for bit in the exact mode, within the north_star's rtol = 1e-5 in the tensor-core mode."""
+    from test_gpu_tcw import rel_dev
+    w = c5_closed_loop(batch=1024)
+    got = dt_closed_loop_batch(w.dyn, w.ctl, w.n, w.x0_lo, w.x0_hi, w.horizon, precision=precision)
+    idx = np.arange(0, 1024, 32)
+    exp = oracle_dtcl_batch(w.dyn, w.ctl, w.n, w.x0_lo[idx], w.x0_hi[idx], w.horizon)
+    assert (exp.status == 0).all() and (got.status == 0).all()
+    sub = type(got)(got.lo[idx], got.hi[idx], got.n_boxes[idx], got.failed_step[idx], got.status[idx])
+    if precision == "exact":
+        assert_tubes_equal(sub, exp, exact=True)
+    else:
+        assert rel_dev(sub, exp) <= 1e-5
+
+
+def test_c5_enclosure_monte_carlo_boxes():
+    """>= 1e3 exact rollouts (with the box vertices among them) on four C5 samples."""
+    w = c5_closed_loop(batch=64)
+    t = dt_closed_loop_batch(w.dyn, w.ctl, w.n, w.x0_lo, w.x0_hi, w.horizon)
+    rng = np.random.default_rng(11)
+    for b in (0, 21, 42, 63):
+        x = rng.uniform(w.x0_lo[b], w.x0_hi[b], size=(1000, w.n))
+        x[:64] = np.where(rng.random((64, w.n)) < 0.5, w.x0_lo[b], w.x0_hi[b])
+        x = x.T
+        for k in range(1, t.n_boxes[b]):
+            u = w.ctl.forward(x)
+            x = w.dyn.forward(np.concatenate([x, u], axis=0))
+            assert (x.T >= t.lo[b, k] - 1e-12).all() and (x.T <= t.hi[b, k] + 1e-12).all()

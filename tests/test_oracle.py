@@ -5,7 +5,7 @@ import pytest
 
 from cases import cases, golden_fixture
 from oracle_bind import (assert_tubes_equal, oracle_dt_batch, oracle_split_hull, ref_available, ref_dt_batch,
-                         ref_split_hull, same_bits)
+                         ref_split_hull, ref_reach_with_splitting, same_bits)
 from paper_2605_25346_b200 import _abi as A
 from paper_2605_25346_b200.api import DTReachParams, DTSystem, SplitPlan, affine_net
 from paper_2605_25346_b200.workloads import residual_relu_dynamics
@@ -64,6 +64,22 @@ def test_split_hull_oracle_matches_reference(window):
         assert got.n_boxes == exp.n_boxes and got.fail_key == exp.fail_key
         k = exp.n_boxes
         assert same_bits(got.lo[:k], exp.lo[:k]) and same_bits(got.hi[:k], exp.hi[:k])
+
+
+@needs_ref
+def test_split_hull_full_range_equals_reference_driver():
+    """ref_split_hull reassembles reach_with_splitting's pieces (it needs a part range); on a full plan it
+    must equal the reference driver itself bit for bit (refine.hpp:121-160)."""
+    rng = np.random.default_rng(31)
+    net = residual_relu_dynamics(rng, 4, 1, [32, 32], dt=0.1)
+    sys = DTSystem(net, 4, 1)
+    c = rng.uniform(-0.5, 0.5, 4)
+    plan = SplitPlan([3, 2, 2, 3])
+    acts = rng.uniform(-0.5, 0.5, size=(10, 1))
+    lo, hi, nb, fs = ref_reach_with_splitting(sys, c - 0.02, c + 0.02, plan, acts)
+    got = ref_split_hull(sys, c - 0.02, c + 0.02, plan, acts, threads=2)
+    assert got.n_boxes == nb and fs == -1 and A.decode_fail_key(got.fail_key) is None
+    assert same_bits(got.lo[:nb], lo[:nb]) and same_bits(got.hi[:nb], hi[:nb])
 
 
 @needs_ref
