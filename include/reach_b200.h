@@ -75,6 +75,12 @@ enum reach_tube_status {
 #define REACH_FLAG_PREC_MASK 0xF00
 #define REACH_PREC_EXACT 0x000
 #define REACH_PREC_TC 0x100
+/* REACH_PREC_FUSED: the exact mode's kernels and operation order with every a*b+c contracted into
+ * one fused multiply-add (DFMA, one rounding) -- about half the FP64 instructions of the CROWN
+ * contractions and IBP.  Not bit-identical to the reference (which rounds twice); bounds match it
+ * within the north_star's fp64 tolerance (measured ~1e-12 relative, tests/test_gpu_fused.py) and
+ * enclose Monte-Carlo rollouts.  All DT engines (warp and wide families). */
+#define REACH_PREC_FUSED 0x200
 
 /* MLPNet<double> (neural.hpp:42-88), flattened. */
 typedef struct reach_net_desc {

@@ -21,16 +21,18 @@ REACH_FLAG_DEVICE_PTRS = 1
 REACH_FLAG_PREC_MASK = 0xF00
 REACH_PREC_EXACT = 0x000
 REACH_PREC_TC = 0x100
-PRECISIONS = {"exact": REACH_PREC_EXACT, "tc": REACH_PREC_TC}
+REACH_PREC_FUSED = 0x200
+PRECISIONS = {"exact": REACH_PREC_EXACT, "tc": REACH_PREC_TC, "fused": REACH_PREC_FUSED}
 
 
 def prec_flag(precision: str) -> int:
-    """Flags bits of a precision mode: "exact" (the reference's arithmetic, bit for bit) or "tc"
-    (CROWN contractions on the int8 tensor cores, Ozaki split, rigorous error bound)."""
+    """Flags bits of a precision mode: "exact" (the reference's arithmetic, bit for bit), "fused" (the
+    same kernels with every a*b+c a DFMA; fp64 tolerance mode) or "tc" (CROWN contractions on the
+    int8 tensor cores, Ozaki split, rigorous error bound)."""
     try:
         return PRECISIONS[precision]
     except KeyError:
-        raise ValueError(f"unknown precision mode {precision!r} (exact | tc)") from None
+        raise ValueError(f"unknown precision mode {precision!r} (exact | fused | tc)") from None
 
 ACT_RELU, ACT_TANH, ACT_IDENTITY = 0, 1, 2
 

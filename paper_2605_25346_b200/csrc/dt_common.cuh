@@ -10,10 +10,21 @@ namespace rb {
 // Arithmetic.  The reference is compiled at -O2 for x86-64 without FMA, so
 // every a*b+c it evaluates is two roundings.  The exact kernels use the _rn
 // intrinsics, which nvcc never contracts into DFMA, to reproduce it bit for bit.
+//
+// RB_FUSED (the REACH_PREC_FUSED build of the same kernels, dt_fused.cu): plain operators, so nvcc
+// contracts every a*b+c into one DFMA -- half the FP64 instructions of the contractions, one
+// rounding instead of two; results within ~1e-15 relative of the exact mode per operation.
+#if RB_FUSED
+__device__ __forceinline__ double mul(double a, double b) { return a * b; }
+__device__ __forceinline__ double add(double a, double b) { return a + b; }
+__device__ __forceinline__ double sub(double a, double b) { return a - b; }
+__device__ __forceinline__ double mac(double acc, double a, double b) { return fma(a, b, acc); }
+#else
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double mac(double acc, double a, double b) { return __dadd_rn(acc, __dmul_rn(a, b)); }
+#endif
 
 // std::min / std::max semantics (first argument wins ties; NaN-asymmetric).
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }

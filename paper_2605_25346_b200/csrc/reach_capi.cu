@@ -34,6 +34,17 @@ cudaError_t wide_call_rd2(int rc, const DTParams* P, size_t smem, int grid, int*
 cudaError_t wide_call_rd4(int rc, const DTParams* P, size_t smem, int grid, int* occ, cudaStream_t s);
 cudaError_t wide_call_rd9(int rc, const DTParams* P, size_t smem, int grid, int* occ, cudaStream_t s);
 }  // namespace rb
+namespace rbh {  // REACH_PREC_FUSED builds (dt_fused.cu)
+cudaError_t wide_call_fused_rd1(int rc, const void* P, size_t smem, int grid, int* occ, cudaStream_t s);
+cudaError_t wide_call_fused_rd2(int rc, const void* P, size_t smem, int grid, int* occ, cudaStream_t s);
+cudaError_t wide_call_fused_rd4(int rc, const void* P, size_t smem, int grid, int* occ, cudaStream_t s);
+cudaError_t wide_call_fused_rd9(int rc, const void* P, size_t smem, int grid, int* occ, cudaStream_t s);
+cudaError_t launch_dt_fused(const void* P, int no, int cpl, unsigned grid, unsigned threads, size_t smem,
+                            cudaStream_t s);
+size_t fused_params_size();
+}  // namespace rbh
+namespace rb {
+}  // namespace rb
 
 #include <atomic>
 #include <random>
@@ -52,6 +63,7 @@ struct DTLayout {
   bool wide = false;  // dt_wide_kernel<rd, rc>, grid CTAs persistent over the batch
   int rd = 0, rc = 0, grid = 0;
   bool tcw = false;   // dt_tcw_kernel (REACH_PREC_TC), grid CTAs persistent over the batch
+  bool fused = false; // REACH_PREC_FUSED: the same kernel from the RB_FUSED build (dt_fused.cu)
   rb::TcwParams tx{};
 };
 
@@ -186,6 +198,15 @@ int plan_warp(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb
 int wide_rows_pick(int rows) { return rows <= 8 ? 1 : rows <= 16 ? 2 : rows <= 32 ? 4 : rows <= 72 ? 9 : 0; }
 
 cudaError_t wide_dispatch(const rb::DTParams* P, const DTLayout& lay, int* occ, cudaStream_t s) {
+  if (lay.fused) {
+    switch (lay.rd) {
+      case 1: return rbh::wide_call_fused_rd1(lay.rc, P, lay.smem, lay.grid, occ, s);
+      case 2: return rbh::wide_call_fused_rd2(lay.rc, P, lay.smem, lay.grid, occ, s);
+      case 4: return rbh::wide_call_fused_rd4(lay.rc, P, lay.smem, lay.grid, occ, s);
+      case 9: return rbh::wide_call_fused_rd9(lay.rc, P, lay.smem, lay.grid, occ, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (lay.rd) {
     case 1: return rb::wide_call_rd1(lay.rc, P, lay.smem, lay.grid, occ, s);
     case 2: return rb::wide_call_rd2(lay.rc, P, lay.smem, lay.grid, occ, s);
@@ -284,17 +305,25 @@ int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, long
     lay.tcw = true;
     return REACH_OK;
   }
-  if (prec != REACH_PREC_EXACT) return fail(ctx, REACH_E_INVALID_ARGUMENT, "unknown precision mode");
+  if (prec != REACH_PREC_EXACT && prec != REACH_PREC_FUSED)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "unknown precision mode");
+  static_assert(sizeof(rb::DTParams) > 0, "");
+  if (prec == REACH_PREC_FUSED && rbh::fused_params_size() != sizeof(rb::DTParams))
+    return fail(ctx, REACH_E_CUDA, "fused build out of step with the exact build (DTParams layout)");
+  const bool fused = prec == REACH_PREC_FUSED;
   if (!env_int("RB_FORCE_WIDE", 0, 0, 1)) {
+    lay.fused = fused;
     const int rc = plan_warp(ctx, net, n, m, window, P, lay, ctl);
     if (rc != REACH_E_UNSUPPORTED) return rc;
     const std::string why = ctx->err;
     P = rb::DTParams{};
     lay = DTLayout{};
+    lay.fused = fused;
     const int rw = plan_wide(ctx, net, n, m, window, B, P, lay, ctl);
     if (rw == REACH_E_UNSUPPORTED) ctx->err = why + "; " + ctx->err;
     return rw;
   }
+  lay.fused = fused;
   return plan_wide(ctx, net, n, m, window, B, P, lay, ctl);
 }
 
@@ -322,6 +351,9 @@ cudaError_t launch_dt_no(const rb::DTParams& P, const DTLayout& lay, long long B
 cudaError_t launch_dt(const rb::DTParams& P, const DTLayout& lay, long long B, cudaStream_t s) {
   if (lay.tcw) return rbh::tcw_launch(P, lay.tx, lay.smem, lay.grid, s);
   if (lay.wide) return wide_dispatch(&P, lay, nullptr, s);
+  if (lay.fused)
+    return rbh::launch_dt_fused(&P, lay.no, lay.cpl, static_cast<unsigned>((B + lay.spc - 1) / lay.spc),
+                                32u * lay.spc, lay.smem, s);
   switch (lay.no) {
     case 2: return launch_dt_no<2>(P, lay, B, s);
     case 4: return launch_dt_no<4>(P, lay, B, s);

@@ -196,8 +196,10 @@ int reach_debug_ozaki_gemm(reach_ctx* ctx, int32_t M, int32_t N, int32_t K, cons
                            double* D, double* bound) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !A || !B || !D || !bound) return REACH_E_INVALID_ARGUMENT;
-  if (M <= 0 || N <= 0 || N > 56 || (N & 7) || K <= 0 || K > 256)
-    return fail(ctx, REACH_E_INVALID_ARGUMENT, "ozaki_gemm: need N in 8..56 (multiple of 8), K <= 256");
+  // UMMA N at M = 128 (measured on B200, tools/tc_shape_probe.py): 8, 16, 24 and multiples of 16 issue;
+  // 40 and 56 raise an illegal instruction.  9 level accumulators x N <= 512 TMEM columns.
+  if (M <= 0 || N <= 0 || N > 48 || (N & 7) || (N > 24 && (N & 15)) || K <= 0 || K > 256)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "ozaki_gemm: need N in {8, 16, 24, 32, 48}, K <= 256");
   const int Mp = (M + 127) / 128 * 128, Kp = (K + 127) / 128 * 128;
   const size_t planes = static_cast<size_t>(rb::oz::kSlices) * Mp * Kp;
   double *dA, *dB, *dD, *dE, *dl1;

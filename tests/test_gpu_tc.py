@@ -12,7 +12,7 @@ def _exact(A, B):
     return (A.astype(np.longdouble) @ B.astype(np.longdouble).T)
 
 
-@pytest.mark.parametrize("M,N,K,seed", [(128, 8, 32, 0), (200, 56, 256, 1), (90, 72 - 8, 90, 2), (256, 24, 256, 3),
+@pytest.mark.parametrize("M,N,K,seed", [(128, 8, 32, 0), (200, 48, 256, 1), (90, 32, 90, 2), (256, 24, 256, 3),
                                         (37, 16, 7, 4)])
 def test_ozaki_gemm_value_and_bound(M, N, K, seed):
     from paper_2605_25346_b200 import default_context
@@ -32,3 +32,12 @@ def test_ozaki_gemm_value_and_bound(M, N, K, seed):
     assert float(np.max(E[nz] / mag[nz])) < 1e-9
     assert float(np.max(err[nz] / mag[nz])) < 1e-11  # wide dynamic range within rows: error ~ 2^-48 of the row maxima
     assert np.all(D[:, 0] == 0.0)
+
+
+@pytest.mark.parametrize("N", [40, 56, 64])
+def test_ozaki_gemm_rejects_illegal_umma_n(N):
+    """N = 40 / 56 raise an illegal instruction on the tensor core at M = 128 (tools/tc_shape_probe.py);
+    the entry point refuses them (and N > 48, which overflows the 512 TMEM columns) up front."""
+    from paper_2605_25346_b200 import default_context
+    with pytest.raises(ValueError):
+        default_context().ozaki_gemm(np.ones((128, 32)), np.ones((N, 32)))
