@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-grad", action="store_true", help="skip the grad_tube_volume leg")
     ap.add_argument("--no-ct", action="store_true", help="skip the C2 continuous-time closed-loop leg")
     ap.add_argument("--no-cl", action="store_true", help="skip the C5 / C1 DT closed-loop legs")
+    ap.add_argument("--no-tc", action="store_true", help="skip the tensor-core precision-mode timings")
     ap.add_argument("--dist-dry-run", action="store_true", help="launcher logic check on CPU (gloo), no GPU work")
     return ap.parse_args()
 
@@ -666,9 +667,11 @@ def main():
     net = ctx.upload(w.sys.step)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    def device_step():
+    # headline precision: REACH_PREC_FUSED (fp64, DFMA contractions; parity within the north_star's fp64
+    # tolerance, checked below); the bit-exact and tensor-core modes are timed beside it
+    def device_step(prec=A.REACH_PREC_FUSED):
         ctx.check(ctx._lib.reach_split_hull(ctx.handle, net, C.byref(args_c), C.byref(out_c),
-                                            A.REACH_FLAG_DEVICE_PTRS), "reach_split_hull")
+                                            A.REACH_FLAG_DEVICE_PTRS | prec), "reach_split_hull")
 
     def barrier():
         if world > 1:
@@ -718,7 +721,8 @@ def main():
     for i in range(args.warmup + args.steps):
         barrier()
         t0 = time.perf_counter()
-        res = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, DTReachParams(), ctx=ctx)
+        res = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, DTReachParams(), ctx=ctx,
+                               precision="fused")
         dt_ = time.perf_counter() - t0
         if i >= args.warmup:
             e2e_t.append(dt_)
@@ -735,29 +739,93 @@ def main():
     tf_fma, tf_ma = ctx.fp64_peak()
     ach = flops_part * per_rank / (kern_max / max(kern_n, 1) / 1e3) / 1e12
     roof = {"bound": "fp64", "achieved": ach, "peak": tf_fma, "unit": "TFLOP/s", "frac": ach / tf_fma,
-            "traffic": None, "kernel": "rb::dt_horizon_kernel<6,4>",
+            "traffic": None, "kernel": "rbf::dt_horizon_kernel<6,4> (REACH_PREC_FUSED build)",
             "flops_per_launch": flops_part * per_rank,
+            "flops_note": "dense-equivalent algorithmic flops (SURVEY §8d); ReLU-sparsity skipping executes fewer "
+                          "(executed_tflops: ncu's executed DFMA/DMUL/DADD thread-op count of this kernel per "
+                          "launch, profiles/c4_dram_traffic.json, over the live kernel time)",
             "peak_source": "measured on this box by reach_measure_fp64_peak (DFMA chains, 2 flops/instr)",
-            "exact_mode_ceiling_tflops": tf_ma,
-            "frac_of_exact_mode_ceiling": ach / tf_ma if tf_ma else None,
             "kernel_ms_per_launch": kern_max / max(kern_n, 1)}
     prof = os.path.join(ROOT, "profiles", "c4_dram_traffic.json")
     if os.path.exists(prof):
         try:
-            roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+            tr = json.load(open(prof))
+            roof["traffic"] = tr.get("fused", {}).get("dram_bytes_per_launch")
+            roof["traffic_source"] = tr.get("fused", {}).get("source")
+            xf = tr.get("fused", {}).get("executed_fp64_flops_per_launch")
+            if xf:
+                roof["executed_tflops"] = xf / (roof["kernel_ms_per_launch"] / 1e3) / 1e12
         except Exception:
             pass
 
-    # ---- parity spot check vs the oracle (first 64 parts of this rank, bit-exact)
+    # ---- the other precision modes of the same sweep (kernel time, L2 flushed; N = 1 rank's share)
+    def mode_time(prec, reps):
+        device_step(prec)
+        barrier()
+        ctx.enable_kernel_timing(True)
+        ctx.kernel_time()
+        for _ in range(reps):
+            flush.zero_()
+            device_step(prec)
+        barrier()
+        ms, nl = ctx.kernel_time()
+        ctx.enable_kernel_timing(False)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t[0])
+        per = ms / max(nl, 1)
+        return per, flops_part * per_rank / (per / 1e3) / 1e12
+
+    ex_ms, ex_tf = mode_time(A.REACH_PREC_EXACT, args.steps)
+    modes = {"fused": {"kernel_ms": kern_max / max(kern_n, 1), "reach_steps_per_s": reach_steps / (kern_max / max(kern_n, 1) / 1e3),
+                       "tflops": ach, "frac_dfma_peak": ach / tf_fma},
+             "exact": {"kernel_ms": ex_ms, "reach_steps_per_s": reach_steps / (ex_ms / 1e3), "tflops": ex_tf,
+                       "frac_dfma_peak": ex_tf / tf_fma, "exact_mode_ceiling_tflops": tf_ma,
+                       "frac_of_exact_mode_ceiling": ex_tf / tf_ma if tf_ma else None,
+                       "kernel": "rb::dt_horizon_kernel<6,4>", "parity": "bit-identical to the oracle / reference"}}
+    if not args.no_tc:
+        try:
+            tc_ms, tc_tf = mode_time(A.REACH_PREC_TC, 1)
+            modes["tc"] = {"kernel_ms": tc_ms, "reach_steps_per_s": reach_steps / (tc_ms / 1e3), "tflops_fp64_equiv": tc_tf,
+                           "kernel": "rb::dt_tcw_kernel (CTA per sub-box, tcgen05.mma kind::i8 Ozaki contractions)"}
+        except Exception as ex:  # noqa: BLE001
+            modes["tc"] = {"error": str(ex)}
+
+    # ---- parity spot checks vs the oracle (first 64 parts of this rank): the headline (fused) mode within
+    # rtol = 1e-5 (north_star, fp64), the exact mode bit for bit; the full-size fused hull against the
+    # exact mode's hull (itself bit-identical to the oracle) within the same rtol
     parity = None
     if rank == 0:
         try:
             from oracle_bind import oracle_split_hull, same_bits
             solo = ctx if world == 1 else Context(local)  # rank-0-only call: a context without collectives
-            g = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=0, part_end=64, ctx=solo)
+
+            def hull_dev(g, e):
+                k = e.n_boxes
+                sc = np.maximum(np.maximum(np.abs(e.lo[:k]), np.abs(e.hi[:k])), e.hi[:k] - e.lo[:k])
+                sc = np.maximum(sc, 1e-300)
+                return float(max(np.max(np.abs(g.lo[:k] - e.lo[:k]) / sc), np.max(np.abs(g.hi[:k] - e.hi[:k]) / sc)))
+
             e = oracle_split_hull(w.sys, w.x0_lo, w.x0_hi, plan, w.actions, begin=0, end=64)
-            parity = {"parts": 64, "bit_exact": bool(same_bits(g.lo, e.lo) and same_bits(g.hi, e.hi)
-                                                     and g.n_boxes == e.n_boxes)}
+            gf = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=0, part_end=64, ctx=solo,
+                                  precision="fused")
+            ge = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=0, part_end=64, ctx=solo)
+            full_f = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=begin, part_end=end,
+                                      ctx=solo, precision="fused")
+            full_e = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=begin, part_end=end,
+                                      ctx=solo)
+            dev64, devfull = hull_dev(gf, e), hull_dev(full_f, full_e)
+            parity = {"parts": 64, "rtol": 1e-5, "fused_max_rel_dev_vs_oracle": dev64,
+                      "fused_full_hull_max_rel_dev_vs_exact": devfull,
+                      "ok": bool(dev64 <= 1e-5 and devfull <= 1e-5 and gf.n_boxes == e.n_boxes
+                                 and full_f.fail_key == full_e.fail_key),
+                      "exact_bit_exact": bool(same_bits(ge.lo, e.lo) and same_bits(ge.hi, e.hi)
+                                              and ge.n_boxes == e.n_boxes)}
+            if "tc" in modes and "error" not in modes["tc"]:
+                gt = reach_split_hull(w.sys, (w.x0_lo, w.x0_hi), plan, w.actions, part_begin=0, part_end=64,
+                                      ctx=solo, precision="tc")
+                modes["tc"]["max_rel_dev_vs_oracle"] = hull_dev(gt, e)
         except Exception as ex:  # the checker is optional at bench time
             parity = {"error": str(ex)}
 
@@ -784,11 +852,13 @@ def main():
                            "horizon": H, "state_dim": n, "net": "6->128x3->6 ReLU (residual synthetic)",
                            "window": 4, "l2": "flushed between timed steps (256 MB write)",
                            "parallelism": f"dp{world}"},
-                "roofline": roof, "cpu_baseline": cb,
+                "precision": "fused (REACH_PREC_FUSED: fp64, DFMA contractions; exact and tc modes in 'modes')",
+                "modes": modes, "roofline": roof, "cpu_baseline": cb,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "clocks": clk, "parity": parity, "ct_quadrotor": ct, **cl, "mpc_replan": mpc,
                 "gradients": grad,
-                "bit_exact_vs_reference": "ReLU path: identical operation order and roundings (tests/test_gpu_dt.py)"}
+                "bit_exact_vs_reference": "exact mode: identical operation order and roundings (tests/test_gpu_dt.py); "
+                                          "fused mode within rtol 1e-5 (tests/test_gpu_fused.py)"}
         print(json.dumps(line))
     if world > 1:
         dist.barrier()

@@ -427,8 +427,14 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
       hi = add(hi, (a >= 0.0) ? a : -a);
     }
     const double cl = c[lane];
+#if RB_FUSED
+    // fused mode: the IBP input boxes are held in mid / radius form (see ibp_row)
+    hb[2 * lane] = cl;
+    hb[2 * lane + 1] = hi;
+#else
     hb[2 * lane] = add(lo, cl);
     hb[2 * lane + 1] = add(hi, cl);
+#endif
   }
   __syncwarp();
 
@@ -454,6 +460,18 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
       double w[CPL], tl[CPL], th[CPL];
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) w[cc] = wrow[cc * 32];
+#if RB_FUSED
+      // mid / radius IBP: alo accumulates W.mid, ahi accumulates |W|.rad -- two DFMAs per weight, no
+      // endpoint selects (equal to the endpoint form up to rounding)
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        alo[cc] = fma(w[cc], x.x, alo[cc]);
+        ahi[cc] = fma(fabs(w[cc]), x.y, ahi[cc]);
+      }
+      (void)tl;
+      (void)th;
+      return;
+#endif
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) {
         const bool pos = w[cc] >= 0.0;
@@ -499,8 +517,14 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) {
         const int o = cc * 32 + lane;
+#if RB_FUSED
+        const double pm = alo[cc] + bfold[cc];
+        const double plo = pm - ahi[cc];
+        const double phi = pm + ahi[cc];
+#else
         const double plo = add(alo[cc], bfold[cc]);
         const double phi = add(ahi[cc], bfold[cc]);
+#endif
         *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(plo, phi);
         if (l == 0 && m_frz > 0) S.bf0[o] = bfold[cc];
         const bool fin = finite(plo) && finite(phi);
@@ -523,7 +547,12 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
       __syncwarp();  // every lane is done reading hb
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc)
+#if RB_FUSED
+        *reinterpret_cast<double2*>(hb + 2 * (cc * 32 + lane)) =
+            make_double2(0.5 * (alo[cc] + ahi[cc]), 0.5 * (ahi[cc] - alo[cc]));
+#else
         *reinterpret_cast<double2*>(hb + 2 * (cc * 32 + lane)) = make_double2(alo[cc], ahi[cc]);
+#endif
       __syncwarp();
     }
   }
@@ -579,6 +608,61 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
           *reinterpret_cast<double2*>(pl + 2 * o) = make_double2(s, ui);
         }
         __syncwarp();
+#if RB_FUSED
+        // fused mode: intercepts, slope scaling and the shift Lambda_s . b in ONE lane-parallel pass over
+        // this lane's units (the reference sums each row's chain in unit order; here per-lane partial
+        // sums and a butterfly reduction -- same terms, a different association)
+        {
+          double pu[NO], pd[NO], sh[NO];
+#pragma unroll
+          for (int i = 0; i < NO; ++i) pu[i] = pd[i] = sh[i] = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) {
+            const int o = cc * 32 + lane;
+            if (o < width) {
+              const double2 su = *reinterpret_cast<const double2*>(pl + 2 * o);
+              const bool unst = (am[CPL + cc] >> lane) & 1u;
+              const double bj = bvec[o];
+              double* col = LT + o * NOP;
+#pragma unroll
+              for (int i = 0; i < NOP; i += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(col + i);
+                const double a0 = v.x, a1 = v.y;
+                if (unst) {
+                  if (a0 >= 0.0) pu[i] = fma(a0, su.y, pu[i]);
+                  else pd[i] = fma(a0, su.y, pd[i]);
+                  if (i + 1 < NO) {
+                    if (a1 >= 0.0) pu[i + 1] = fma(a1, su.y, pu[i + 1]);
+                    else pd[i + 1] = fma(a1, su.y, pd[i + 1]);
+                  }
+                }
+                const double s0 = a0 * su.x, s1 = a1 * su.x;
+                *reinterpret_cast<double2*>(col + i) = make_double2(s0, s1);
+                sh[i] = fma(s0, bj, sh[i]);
+                if (i + 1 < NO) sh[i + 1] = fma(s1, bj, sh[i + 1]);
+              }
+            }
+          }
+#pragma unroll
+          for (int off = 16; off; off >>= 1)
+#pragma unroll
+            for (int i = 0; i < NO; ++i) {
+              pu[i] += __shfl_xor_sync(0xffffffffu, pu[i], off);
+              pd[i] += __shfl_xor_sync(0xffffffffu, pd[i], off);
+              sh[i] += __shfl_xor_sync(0xffffffffu, sh[i], off);
+            }
+#pragma unroll
+          for (int i = 0; i < NO; ++i)
+            if (lane == i) {
+              bup += pu[i] + sh[i];
+              blo += pd[i] + sh[i];
+            }
+          __syncwarp();
+        }
+        if (false) {
+#else
+        if (true) {
+#endif
         // intercept chains over the unstable units (unscaled Lambda), lane i = row i
         if (lane < n_o) {
           for_each_row(am + CPL, 0, width, [&](int j) {
@@ -610,6 +694,7 @@ __device__ __forceinline__ void certify(const DevNet& N, const double* bias_s, c
           blo = add(blo, shift);
           bup = add(bup, shift);
         }
+        }  // exact-mode chains
       } else {
         if (act == 1) {
 #pragma unroll
