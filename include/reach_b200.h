@@ -406,6 +406,45 @@ int reach_refine_tube_volume(reach_ctx* ctx, const reach_net* net, const reach_d
 int reach_reach_loss(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a, int32_t episodes,
                      double eps, double cap, double* loss, double* grad, int32_t* diverged_count);
 
+/* Certified training (training.hpp).  An episode set of `episodes` rollouts of one length T:
+ * states [episodes][T+1][n], actions [episodes][T][m] (Episode, training.hpp:28-45). */
+typedef struct reach_episode_set {
+  int32_t episodes, length, n, m;
+  const double* states;
+  const double* actions;
+} reach_episode_set;
+
+/* pred_loss (training.hpp:60-83) of the first t_h steps of every episode of `batch` under the one-step
+ * model `net` with weights [t_h], and (grad != NULL) its grad_forward over net_params (neural.hpp:133-140):
+ * one Dual rollout per (parameter, episode) on the device, terms summed in the reference's order. */
+int reach_pred_loss(reach_ctx* ctx, const reach_net* net, const reach_episode_set* batch, int32_t t_h,
+                    const double* weights, double* loss, double* grad);
+
+/* TrainConfig (training.hpp:262-282) and one TrainLog row (:284-292). */
+typedef struct reach_train_config {
+  int32_t horizon_max;
+  double eps0, eps_final, lambda, gamma;
+  int32_t iters, batch;
+  double lr, reach_cap;
+  int32_t curriculum;
+  uint64_t seed;
+  int32_t window, rebuild_from_box; /* cfg.dt_prm */
+} reach_train_config;
+typedef struct reach_train_log_row {
+  int32_t iter, t_h;
+  double eps, l_pred, l_reach, l_total;
+  int32_t diverged_count;
+} reach_train_log_row;
+
+/* train_dt_dyn (training.hpp:333-382): certified training of a DT dynamics net, L = pred_loss +
+ * lambda reach_loss with the horizon / radius curriculum, the reference's minibatch stream (Rng(seed),
+ * uniform_int) and Adam on the host; every loss and every gradient (grad_forward: pred_loss and
+ * reach_loss Dual passes) on the device.  params_out [param_count] = the trained net_params;
+ * log [iters] rows.  REACH_E_NONFINITE where the reference throws std::runtime_error (non-finite loss
+ * or derivative; ctx error string = the reference's message). */
+int reach_train_dt_dyn(reach_ctx* ctx, const reach_net_desc* init, const reach_train_config* cfg,
+                       const reach_episode_set* dataset, double* params_out, reach_train_log_row* log);
+
 /* The CEM loop in pieces, for multi-GPU drivers that shard each population
  * and all-gather the scores between sample() and update(). */
 typedef struct reach_cem reach_cem;

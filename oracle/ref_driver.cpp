@@ -995,3 +995,80 @@ extern "C" int ref_ctl_reach_loss(const reach_net_desc* ctl_desc, const reach_cl
   }
   return REACH_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Certified training (training.hpp): pred_loss with its grad_forward, and the train_dt_dyn loop,
+// on reach_episode_set data (uniform episode length).
+static std::vector<Episode> episodes_from(const reach_episode_set* s) {
+  std::vector<Episode> out(static_cast<size_t>(s->episodes));
+  for (int e = 0; e < s->episodes; ++e) {
+    Episode& ep = out[static_cast<size_t>(e)];
+    for (int t = 0; t <= s->length; ++t) {
+      const double* x = s->states + (static_cast<size_t>(e) * (s->length + 1) + t) * s->n;
+      ep.states.push_back(Vec<double>(x, x + s->n));
+    }
+    for (int t = 0; t < s->length; ++t) {
+      const double* u = s->actions + (static_cast<size_t>(e) * s->length + t) * s->m;
+      ep.actions.push_back(Vec<double>(u, u + s->m));
+    }
+  }
+  return out;
+}
+
+extern "C" int ref_pred_loss(const reach_net_desc* desc, const reach_episode_set* b, int32_t t_h,
+                             const double* weights, double* loss, double* grad) {
+  try {
+    MLPNet<double> net = net_from_desc(desc);
+    auto batch = episodes_from(b);
+    Vec<double> w(weights, weights + t_h);
+    *loss = pred_loss(net, batch, t_h, w);
+    if (grad) {
+      auto f = [&](const auto& p) {
+        using S = typename std::decay_t<decltype(p)>::value_type;
+        return pred_loss(net_with_params<S>(net, p), batch, t_h, w);
+      };
+      Gradient g = grad_forward(f, net_params(net));
+      std::copy(g.g.begin(), g.g.end(), grad);
+    }
+  } catch (const std::invalid_argument&) {
+    return REACH_E_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return REACH_E_NONFINITE;
+  }
+  return REACH_OK;
+}
+
+extern "C" int ref_train_dt_dyn(const reach_net_desc* init, const reach_train_config* c, const reach_episode_set* ds,
+                                double* params_out, reach_train_log_row* log, int32_t* log_rows) {
+  TrainConfig cfg;
+  cfg.horizon_max = c->horizon_max;
+  cfg.eps0 = c->eps0;
+  cfg.eps_final = c->eps_final;
+  cfg.lambda = c->lambda;
+  cfg.gamma = c->gamma;
+  cfg.iters = c->iters;
+  cfg.batch = c->batch;
+  cfg.lr = c->lr;
+  cfg.reach_cap = c->reach_cap;
+  cfg.curriculum = c->curriculum != 0;
+  cfg.seed = c->seed;
+  cfg.dt_prm.window = c->window;
+  cfg.dt_prm.rebuild_from_box = c->rebuild_from_box != 0;
+  try {
+    MLPNet<double> net = net_from_desc(init);
+    TrainResult r = train_dt_dyn(net, cfg, episodes_from(ds));
+    Vec<double> p = net_params(r.net);
+    std::copy(p.begin(), p.end(), params_out);
+    for (size_t i = 0; i < r.log.rows.size(); ++i) {
+      const auto& row = r.log.rows[i];
+      log[i] = reach_train_log_row{row.iter, row.t_h, row.eps, row.l_pred, row.l_reach, row.l_total,
+                                   row.diverged_count};
+    }
+    *log_rows = static_cast<int32_t>(r.log.rows.size());
+  } catch (const std::invalid_argument&) {
+    return REACH_E_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return REACH_E_NONFINITE;
+  }
+  return REACH_OK;
+}

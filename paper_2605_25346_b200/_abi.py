@@ -217,3 +217,21 @@ ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size
 class Collectives(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("allreduce", ALLREDUCE_FN), ("allgather", ALLGATHER_FN),
                 ("user", C.c_void_p)]
+
+
+# --- certified training (training.hpp) --------------------------------------------------------
+class EpisodeSetC(C.Structure):
+    _fields_ = [("episodes", C.c_int32), ("length", C.c_int32), ("n", C.c_int32), ("m", C.c_int32),
+                ("states", _dp), ("actions", _dp)]
+
+
+class TrainConfigC(C.Structure):
+    _fields_ = [("horizon_max", C.c_int32), ("eps0", C.c_double), ("eps_final", C.c_double),
+                ("lambda_", C.c_double), ("gamma", C.c_double), ("iters", C.c_int32), ("batch", C.c_int32),
+                ("lr", C.c_double), ("reach_cap", C.c_double), ("curriculum", C.c_int32), ("seed", C.c_uint64),
+                ("window", C.c_int32), ("rebuild_from_box", C.c_int32)]
+
+
+class TrainLogRowC(C.Structure):
+    _fields_ = [("iter", C.c_int32), ("t_h", C.c_int32), ("eps", C.c_double), ("l_pred", C.c_double),
+                ("l_reach", C.c_double), ("l_total", C.c_double), ("diverged_count", C.c_int32)]

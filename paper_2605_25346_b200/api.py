@@ -444,6 +444,116 @@ def reach_loss(model: MLPNet, batch: Sequence[Episode], eps: float, t_h: int, ca
     return (float(loss[0]), g, int(dc[0])) if with_grad else (float(loss[0]), int(dc[0]))
 
 
+def net_with_params(shape: MLPNet, params) -> MLPNet:
+    """net_with_params (neural.hpp:142-152): the shape's layers with values from a net_params vector."""
+    params = np.asarray(params, np.float64)
+    layers, k = [], 0
+    for L in shape.layers:
+        r, c = L.w.shape
+        w = params[k:k + r * c].reshape(r, c).copy()
+        k += r * c
+        b = params[k:k + r].copy()
+        k += r
+        layers.append(Layer(w, b, L.act))
+    if k != params.size:
+        raise ValueError("net_with_params: size mismatch")
+    return MLPNet(layers)
+
+
+def horizon_weights(t_h: int) -> np.ndarray:
+    """horizon_weights (training.hpp:48-53)."""
+    return np.array([1.0 + (t + 1) / t_h for t in range(t_h)], np.float64)
+
+
+def _episode_set(batch: Sequence[Episode]):
+    """(EpisodeSetC, keepalive) of episodes of one length (states [E][T+1][n], actions [E][T][m])."""
+    if not batch:
+        raise ValueError("empty episode batch")
+    T = batch[0].length()
+    if any(ep.length() != T for ep in batch):
+        raise ValueError("episodes of one batch must share a length")
+    n, m = len(batch[0].states[0]), len(batch[0].actions[0]) if T else 0
+    st = np.ascontiguousarray(np.array([np.asarray(ep.states, np.float64).reshape(T + 1, n) for ep in batch]))
+    ac = np.ascontiguousarray(np.array([np.asarray(ep.actions, np.float64).reshape(T, m) for ep in batch]))
+    es = A.EpisodeSetC(len(batch), T, n, m, A.dptr(st), A.dptr(ac if ac.size else np.zeros(1)))
+    return es, (st, ac)
+
+
+def pred_loss(model: MLPNet, batch: Sequence[Episode], t_h: int, weights, with_grad: bool = False,
+              ctx: Optional[Context] = None):
+    """pred_loss (training.hpp:60-83) on the device -> loss, or with_grad -> (loss, gradient over net_params):
+    grad_forward's Dual rollouts, one CTA per (parameter, episode), one launch."""
+    weights = np.ascontiguousarray(weights, np.float64)
+    if not batch or t_h < 1 or weights.size != t_h:
+        raise ValueError("pred_loss: bad batch/horizon/weights")
+    ctx = ctx or default_context()
+    es, keep = _episode_set(batch)
+    loss = np.zeros(1)
+    g = np.zeros(model.params().size) if with_grad else None
+    net = ctx.upload(model)
+    ctx.check(ctx._lib.reach_pred_loss(ctx.handle, net, C.byref(es), int(t_h), A.dptr(weights), A.dptr(loss),
+                                       A.dptr(g) if with_grad else None), "pred_loss")
+    return (float(loss[0]), g) if with_grad else float(loss[0])
+
+
+@dataclass
+class TrainConfig:  # training.hpp:262-282
+    horizon_max: int = 4
+    eps0: float = 0.1
+    eps_final: float = 0.01
+    lambda_: float = 0.0
+    gamma: float = 0.1
+    iters: int = 50
+    batch: int = 4
+    lr: float = 1e-3
+    reach_cap: float = 20.0
+    curriculum: bool = True
+    seed: int = 0
+    dt_prm: DTReachParams = field(default_factory=DTReachParams)
+
+    def c(self):
+        return A.TrainConfigC(self.horizon_max, self.eps0, self.eps_final, self.lambda_, self.gamma, self.iters,
+                              self.batch, self.lr, self.reach_cap, int(self.curriculum), self.seed,
+                              self.dt_prm.window, int(self.dt_prm.rebuild_from_box))
+
+
+@dataclass
+class TrainLogRow:  # training.hpp:284-292
+    iter: int
+    t_h: int
+    eps: float
+    l_pred: float
+    l_reach: float
+    l_total: float
+    diverged_count: int
+
+
+def train_log_csv(rows: Sequence[TrainLogRow]) -> str:
+    """TrainLog::to_csv (training.hpp:297-305)."""
+    from .formats import fmt_g17
+    out = "iter,T_h,eps,L_pred,L_reach,L_total,diverged_count\n"
+    for r in rows:
+        out += (f"{r.iter},{r.t_h},{fmt_g17(r.eps)},{fmt_g17(r.l_pred)},{fmt_g17(r.l_reach)},"
+                f"{fmt_g17(r.l_total)},{r.diverged_count}\n")
+    return out
+
+
+def train_dt_dyn(init: MLPNet, cfg: TrainConfig, dataset: Sequence[Episode], ctx: Optional[Context] = None):
+    """train_dt_dyn (training.hpp:333-382) -> (trained MLPNet, [TrainLogRow]): the host loop (curriculum,
+    the reference's minibatch stream, Adam) of the C ABI with every loss and gradient on the device."""
+    ctx = ctx or default_context()
+    es, keep = _episode_set(dataset)
+    d, keep2 = init.desc()
+    out = np.zeros(init.params().size)
+    log = (A.TrainLogRowC * max(cfg.iters, 1))()
+    cc = cfg.c()
+    rc = ctx._lib.reach_train_dt_dyn(ctx.handle, C.byref(d), C.byref(cc), C.byref(es), A.dptr(out), log)
+    rows = [TrainLogRow(r.iter, r.t_h, r.eps, r.l_pred, r.l_reach, r.l_total, r.diverged_count)
+            for r in list(log)[:cfg.iters]]
+    ctx.check(rc, "train_dt_dyn")
+    return net_with_params(init, out), rows
+
+
 # ---------------------------------------------------------------------------
 class SplitPlan:
     """SplitPlan (refine.hpp:25-78)."""

@@ -865,5 +865,92 @@ __global__ void __launch_bounds__(kThreads, 2) reach_loss_grad_kernel(const Loss
   }
 }
 
+// Seeds network parameter p (net_params order, neural.hpp:133-140) in a NetView.
+__device__ __forceinline__ void seed_param(NetView& net, const long long* poff, long long p) {
+  int l = 0;
+  while (l + 1 <= net.N.L && poff[l + 1] <= p) ++l;
+  const long long q = p - poff[l];
+  const int rows = net.N.dims[l + 1], cols = net.N.dims[l];
+  net.sl = l;
+  if (q < static_cast<long long>(rows) * cols) {
+    net.si = static_cast<int>(q / cols);
+    net.sj = static_cast<int>(q % cols);
+  } else {
+    net.si = static_cast<int>(q - static_cast<long long>(rows) * cols);
+    net.sj = -1;
+  }
+  net.seed = 1.0;
+}
+
+// ---------------------------------------------------------------------------
+// pred_loss (training.hpp:60-83): the autoregressive multi-step prediction loss and its grad_forward
+// over the model's parameters.  One CTA per (pass p, episode e): the nominal rollout
+// xhat_{t+1} = model.forward([xhat_t; u_t]) in reach::Dual with parameter p seeded (pass 0 of a
+// value-only launch: nothing seeded), emitting each step's term w_t * ||xhat_{t+1} - x_{t+1}||^2
+// (Dual); the host sums the terms in the reference's (episode, step) order.
+constexpr int kPredW = 256;  // widest layer
+constexpr int kPredThreads = 128;
+
+struct PredArgs {
+  DevNet net;
+  int n, m, T, M, seeded;
+  long long poff[kMaxLayers + 1];
+  const double* states;   // [M][Ls + 1][n]
+  const double* actions;  // [M][Ls][m]
+  int ls;                 // stored episode length Ls >= T
+  const double* weights;  // [T]
+  double* term_v;         // [passes][M][T]
+  double* term_d;
+};
+
+__global__ void __launch_bounds__(kPredThreads) pred_loss_grad_kernel(const PredArgs A) {
+  __shared__ D hb[2][kPredW];
+  const int tid = threadIdx.x, pass = blockIdx.x, ep = blockIdx.y;
+  const int n = A.n, m = A.m, T = A.T;
+  NetView net{A.net};
+  if (A.seeded) seed_param(net, A.poff, pass);
+  const DevNet& N = A.net;
+  const double* st = A.states + static_cast<size_t>(ep) * (A.ls + 1) * n;
+  const double* ac = A.actions + static_cast<size_t>(ep) * A.ls * m;
+  for (int i = tid; i < n; i += kPredThreads) hb[0][i] = dc(st[i]);
+  int cur = 0;
+  for (int t = 0; t < T; ++t) {
+    for (int i = tid; i < m; i += kPredThreads) hb[cur][n + i] = dc(ac[static_cast<size_t>(t) * m + i]);
+    __syncthreads();
+    for (int l = 0; l < N.L; ++l) {  // MLPNet::forward (neural.hpp:58-76), matvec (linalg.hpp:41-51)
+      const int rows = N.dims[l + 1], cols = N.dims[l];
+      for (int u = tid; u < rows; u += kPredThreads) {
+        D acc = dc(0.0);
+        if (l + 1 < N.L)
+          for (int q = 0; q < cols; ++q) acc = dadd(acc, dmul(net.wt(l, u, q), hb[cur][q]));
+        else
+          for (int q = 0; q < cols; ++q) acc = dadd(acc, dmul(net.w(l, u, q), hb[cur][q]));
+        D h = dadd(acc, net.b(l, u));
+        if (N.acts[l] == REACH_ACT_RELU) {
+          if (h.v < 0.0) h = dc(0.0);
+        } else if (N.acts[l] == REACH_ACT_TANH) {
+          h = dtanh(h);
+        }
+        hb[cur ^ 1][u] = h;
+      }
+      cur ^= 1;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const double* tgt = st + static_cast<size_t>(t + 1) * n;
+      D err = dc(0.0);
+      for (int j = 0; j < n; ++j) {
+        const D d = dsub(hb[cur][j], dc(tgt[j]));
+        err = dadd(err, dmul(d, d));
+      }
+      const D term = dmul(dc(A.weights[t]), err);
+      const size_t o = (static_cast<size_t>(pass) * A.M + ep) * T + t;
+      A.term_v[o] = term.v;
+      A.term_d[o] = term.d;
+    }
+    // xhat_{t+1} stays in hb[cur][0..n); the next step appends its action behind it
+  }
+}
+
 }  // namespace dual
 }  // namespace rb

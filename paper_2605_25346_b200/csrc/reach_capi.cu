@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <functional>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -2218,6 +2220,196 @@ int reach_reach_loss(reach_ctx* ctx, const reach_net* net, const reach_dt_args* 
     for (int e = 0; e < M; ++e) c += dv[e];
     *diverged_count = c;
   }
+  return REACH_OK;
+}
+
+// pred_loss (training.hpp:60-83) of a batch and, optionally, its grad_forward over net_params.
+int reach_pred_loss(reach_ctx* ctx, const reach_net* net, const reach_episode_set* b, int32_t t_h,
+                    const double* weights, double* loss, double* grad) {
+  rbh::DeviceGuard device_guard_(ctx);
+  namespace rd = rb::dual;
+  if (!ctx || !net || !b || !loss) return REACH_E_INVALID_ARGUMENT;
+  if (b->episodes < 1 || t_h < 1 || !weights)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "pred_loss: bad batch/horizon/weights");
+  if (b->length < t_h) return fail(ctx, REACH_E_INVALID_ARGUMENT, "pred_loss: episode shorter than T_h");
+  const int n = b->n, m = b->m, M = b->episodes, T = t_h, Ls = b->length;
+  if (n < 1 || m < 0 || !b->states || (m > 0 && !b->actions))
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "pred_loss: missing episode data");
+  if (net->dims[0] != n + m || net->dims[net->L] != n)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "pred_loss: model shape does not match the episodes");
+  int maxw = 0;
+  for (int l = 0; l <= net->L; ++l) maxw = std::max(maxw, net->dims[l]);
+  if (maxw > rd::kPredW || M > 65535) return fail(ctx, REACH_E_UNSUPPORTED, "pred_loss: shape outside the kernel");
+  rd::PredArgs A{};
+  A.poff[0] = 0;
+  for (int l = 0; l < net->L; ++l)
+    A.poff[l + 1] = A.poff[l] + static_cast<long long>(net->dims[l + 1]) * net->dims[l] + net->dims[l + 1];
+  const long long P = grad ? A.poff[net->L] : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t ns = static_cast<size_t>(M) * (Ls + 1) * n, na = static_cast<size_t>(M) * Ls * m,
+               nt = static_cast<size_t>(P) * M * T;
+  const size_t o_s = take(ns * 8), o_a = take(na * 8), o_w = take(static_cast<size_t>(T) * 8), o_v = take(nt * 8),
+               o_d = take(nt * 8);
+  int rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  RB_CUDA(cudaMemcpyAsync(Dp(o_s), b->states, ns * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (na) RB_CUDA(cudaMemcpyAsync(Dp(o_a), b->actions, na * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_w), weights, static_cast<size_t>(T) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  A.net = net->dev;
+  A.n = n;
+  A.m = m;
+  A.T = T;
+  A.M = M;
+  A.seeded = grad ? 1 : 0;
+  A.states = Dp(o_s);
+  A.actions = Dp(o_a);
+  A.ls = Ls;
+  A.weights = Dp(o_w);
+  A.term_v = Dp(o_v);
+  A.term_d = Dp(o_d);
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  rd::pred_loss_grad_kernel<<<dim3(static_cast<unsigned>(P), static_cast<unsigned>(M)), rd::kPredThreads, 0,
+                              ctx->stream>>>(A);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  std::vector<double> tv(nt), td(nt);
+  RB_CUDA(cudaMemcpyAsync(tv.data(), Dp(o_v), nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(td.data(), Dp(o_d), nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  // acc += term in (episode, step) order, then acc / S(M * T_h) (Dual division, scalar.hpp:22-28)
+  const double q = static_cast<double>(M) * T;
+  for (long long p = 0; p < P; ++p) {
+    double av = 0.0, ad = 0.0;
+    const size_t base = static_cast<size_t>(p) * M * T;
+    for (size_t k = 0; k < static_cast<size_t>(M) * T; ++k) {
+      av = av + tv[base + k];
+      ad = ad + td[base + k];
+    }
+    if (p == 0) *loss = av / q;
+    if (grad) grad[p] = (ad * q - av * 0.0) / (q * q);
+  }
+  return REACH_OK;
+}
+
+// train_dt_dyn (training.hpp:333-382) with every loss and gradient on the device.
+int reach_train_dt_dyn(reach_ctx* ctx, const reach_net_desc* init, const reach_train_config* cfg,
+                       const reach_episode_set* ds, double* params_out, reach_train_log_row* log) {
+  rbh::DeviceGuard device_guard_(ctx);
+  if (!ctx || !init || !cfg || !ds || !params_out) return REACH_E_INVALID_ARGUMENT;
+  const reach_train_config& c = *cfg;
+  if (c.horizon_max < 1 || c.eps0 < c.eps_final || c.eps_final < 0.0 || c.lambda < 0.0 || c.gamma < 0.0 ||
+      c.iters < 1 || c.batch < 1 || c.lr <= 0.0 || c.reach_cap <= 0.0)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "TrainConfig: invalid configuration");
+  if (ds->episodes < 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "train_dt_dyn: empty dataset");
+  if (ds->length < c.horizon_max) return fail(ctx, REACH_E_INVALID_ARGUMENT, "train_dt_dyn: episode shorter than T_h^max");
+  const int n = ds->n, m = ds->m, L = init->n_layers, E = ds->episodes, Ls = ds->length;
+  size_t np = 0;
+  for (int l = 0; l < L; ++l) np += static_cast<size_t>(init->dims[l + 1]) * (init->dims[l] + 1);
+  std::vector<double> params(init->params, init->params + np);
+  std::vector<int32_t> dims(init->dims, init->dims + L + 1), acts(init->acts, init->acts + L);
+  // Adam (training.hpp:239-260)
+  const double beta1 = 0.9, beta2 = 0.999, aeps = 1e-8;
+  std::vector<double> am(np, 0.0), av(np, 0.0);
+  int at = 0;
+  std::mt19937_64 gen(c.seed);  // Rng(cfg.seed) (rng.hpp:13-15); sample_batch draws uniform_int
+  constexpr double kE = 2.718281828459045235360287471352662498;  // std::numbers::e
+  std::vector<double> bs(static_cast<size_t>(c.batch) * (c.horizon_max + 1) * n),
+      ba(static_cast<size_t>(c.batch) * c.horizon_max * std::max(m, 0)), x0s(static_cast<size_t>(c.batch) * n);
+  std::vector<double> gp(np), gr(np), g(np);
+  for (int s = 0; s < c.iters; ++s) {
+    int t_h = c.horizon_max;
+    double eps = c.eps_final;
+    if (c.curriculum) {  // horizon_schedule / eps_schedule (training.hpp:219-236)
+      if (c.iters <= 1) {
+        t_h = c.horizon_max;
+        eps = c.eps_final;
+      } else {
+        const double u = std::log(1.0 + static_cast<double>(s) * (kE - 1.0) / (c.iters - 1));
+        t_h = std::min(std::max(1, static_cast<int>(std::llround(c.horizon_max * u))), c.horizon_max);
+        eps = c.eps_final + (c.eps0 - c.eps_final) * (1.0 - static_cast<double>(s) / (c.iters - 1));
+      }
+    }
+    // detail::sample_batch (training.hpp:305-314): the first t_h steps of each drawn episode
+    const int Tm = c.horizon_max;
+    for (int b = 0; b < c.batch; ++b) {
+      const int e = static_cast<int>(gen() % static_cast<uint64_t>(E));
+      std::memcpy(bs.data() + static_cast<size_t>(b) * (Tm + 1) * n, ds->states + static_cast<size_t>(e) * (Ls + 1) * n,
+                  sizeof(double) * (Tm + 1) * n);
+      if (m > 0)
+        std::memcpy(ba.data() + static_cast<size_t>(b) * Tm * m, ds->actions + static_cast<size_t>(e) * Ls * m,
+                    sizeof(double) * Tm * m);
+      std::memcpy(x0s.data() + static_cast<size_t>(b) * n, ds->states + static_cast<size_t>(e) * (Ls + 1) * n,
+                  sizeof(double) * n);
+    }
+    std::vector<double> wts(static_cast<size_t>(t_h));  // horizon_weights (training.hpp:48-53)
+    for (int t = 0; t < t_h; ++t) wts[static_cast<size_t>(t)] = 1.0 + static_cast<double>(t + 1) / t_h;
+    reach_net_desc d{L, dims.data(), acts.data(), params.data()};
+    reach_net* cur = nullptr;
+    int rc = reach_net_upload(ctx, &d, &cur);
+    if (rc) return rc;
+    std::unique_ptr<reach_net, std::function<void(reach_net*)>> guard(cur, [ctx](reach_net* p) { reach_net_free(ctx, p); });
+    reach_episode_set bset{c.batch, Tm, n, m, bs.data(), ba.data()};
+    double lp = 0.0, lr_ = 0.0;
+    int div = 0;
+    rc = reach_pred_loss(ctx, cur, &bset, t_h, wts.data(), &lp, gp.data());
+    if (rc) return rc;
+    if (c.lambda > 0.0) {
+      reach_dt_args a{};
+      a.batch = c.batch;
+      a.horizon = t_h;
+      a.n = n;
+      a.m = m;
+      a.window = c.window;
+      a.rebuild_from_box = c.rebuild_from_box;
+      std::vector<double> acts_th(static_cast<size_t>(c.batch) * t_h * std::max(m, 0));
+      for (int b = 0; b < c.batch && m > 0; ++b)
+        std::memcpy(acts_th.data() + static_cast<size_t>(b) * t_h * m, ba.data() + static_cast<size_t>(b) * Tm * m,
+                    sizeof(double) * t_h * m);
+      a.x0_lo = x0s.data();
+      a.x0_hi = x0s.data();
+      a.actions = m > 0 ? acts_th.data() : nullptr;
+      rc = reach_reach_loss(ctx, cur, &a, c.batch, eps, c.reach_cap, &lr_, gr.data(), &div);
+      if (rc) return rc;
+    }
+    const double lt = lp + c.lambda * lr_;
+    if (log) log[s] = reach_train_log_row{s, t_h, eps, lp, lr_, lt, div};
+    if (!std::isfinite(lt)) {
+      char msg[256];
+      std::snprintf(msg, sizeof msg, "train_dt_dyn: non-finite loss at iter %d", s);
+      return fail(ctx, REACH_E_NONFINITE, msg);
+    }
+    // grad_forward of pred_loss + S(lambda) reach_loss: per direction the Dual sum of the two parts
+    for (size_t j = 0; j < np; ++j) {
+      double dv = gp[j];
+      if (c.lambda > 0.0) {
+        const double rv = lr_, rdv = gr[j];
+        if (!std::isfinite(rv) || !std::isfinite(rdv))
+          return fail(ctx, REACH_E_NONFINITE, "grad_forward: non-finite derivative");
+        dv = dv + (0.0 * rv + c.lambda * rdv);  // dmul(S(lambda), r).d, then dadd
+      }
+      if (!std::isfinite(dv)) return fail(ctx, REACH_E_NONFINITE, "grad_forward: non-finite derivative");
+      g[j] = dv;
+    }
+    ++at;  // Adam::step
+    const double bc1 = 1.0 - std::pow(beta1, at), bc2 = 1.0 - std::pow(beta2, at);
+    for (size_t j = 0; j < np; ++j) {
+      am[j] = beta1 * am[j] + (1.0 - beta1) * g[j];
+      av[j] = beta2 * av[j] + (1.0 - beta2) * g[j] * g[j];
+      params[j] -= c.lr * (am[j] / bc1) / (std::sqrt(av[j] / bc2) + aeps);
+    }
+  }
+  std::memcpy(params_out, params.data(), sizeof(double) * np);
   return REACH_OK;
 }
 

@@ -531,3 +531,39 @@ def ref_ctl_reach_loss(spec, x0s, yrefs, eps, t_h, delta, cap):
            float(cap), A.dptr(loss), A.iptr(dc))
     assert rc == 0, rc
     return float(loss[0]), int(dc[0])
+
+
+# --- certified training (training.hpp) through the reference itself -------------------------------
+def ref_pred_loss(model, batch, t_h, weights, with_grad=False):
+    from paper_2605_25346_b200.api import _episode_set
+    es, keep = _episode_set(batch)
+    d, keep2 = model.desc()
+    w = np.ascontiguousarray(weights, np.float64)
+    loss = np.zeros(1)
+    g = np.zeros(model.params().size) if with_grad else None
+    f = ref_lib().ref_pred_loss
+    f.argtypes = [C.POINTER(A.NetDesc), C.POINTER(A.EpisodeSetC), C.c_int32, C.POINTER(C.c_double),
+                  C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    f.restype = C.c_int
+    rc = f(C.byref(d), C.byref(es), int(t_h), A.dptr(w), A.dptr(loss), A.dptr(g) if with_grad else None)
+    assert rc == 0, rc
+    return (float(loss[0]), g) if with_grad else float(loss[0])
+
+
+def ref_train_dt_dyn(init, cfg, dataset):
+    """(trained net_params, [TrainLogRow], rc) of the reference's train_dt_dyn."""
+    from paper_2605_25346_b200.api import TrainLogRow, _episode_set
+    es, keep = _episode_set(dataset)
+    d, keep2 = init.desc()
+    out = np.zeros(init.params().size)
+    log = (A.TrainLogRowC * max(cfg.iters, 1))()
+    nrows = np.zeros(1, np.int32)
+    f = ref_lib().ref_train_dt_dyn
+    f.argtypes = [C.POINTER(A.NetDesc), C.POINTER(A.TrainConfigC), C.POINTER(A.EpisodeSetC), C.POINTER(C.c_double),
+                  C.POINTER(A.TrainLogRowC), C.POINTER(C.c_int32)]
+    f.restype = C.c_int
+    cc = cfg.c()
+    rc = f(C.byref(d), C.byref(cc), C.byref(es), A.dptr(out), log, A.iptr(nrows))
+    rows = [TrainLogRow(r.iter, r.t_h, r.eps, r.l_pred, r.l_reach, r.l_total, r.diverged_count)
+            for r in list(log)[:int(nrows[0])]]
+    return out, rows, rc

@@ -1,0 +1,54 @@
+"""GPU: certified training (training.hpp) on the device against the reference itself (oracle/_ref).
+
+pred_loss and its grad_forward over net_params: bit for bit (the Dual rollouts keep the reference's
+operation order; the terms are summed on the host in its (episode, step) order).  train_dt_dyn: the
+log (T_h, eps, L_pred, L_reach, L_total, diverged_count) and the trained parameters bit for bit --
+the same minibatch stream, the same device losses / gradients, the same Adam arithmetic."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle_bind import ref_pred_loss, ref_train_dt_dyn
+from paper_2605_25346_b200.api import horizon_weights, pred_loss, train_dt_dyn
+from train_cases import dt_training_case, train_config
+
+
+@pytest.mark.parametrize("t_h", [1, 3, 6])
+def test_pred_loss_and_gradient_bit_identical(t_h):
+    model, data = dt_training_case()
+    w = horizon_weights(t_h)
+    got, g = pred_loss(model, data[:4], t_h, w, with_grad=True)
+    exp, ge = ref_pred_loss(model, data[:4], t_h, w, with_grad=True)
+    assert got == exp
+    assert np.array_equal(g, ge), float(np.max(np.abs(g - ge)))
+    assert pred_loss(model, data[:4], t_h, w) == exp
+
+
+def test_pred_loss_errors():
+    model, data = dt_training_case()
+    with pytest.raises(ValueError):
+        pred_loss(model, data[:2], 7, horizon_weights(7))  # episodes of length 6
+    with pytest.raises(ValueError):
+        pred_loss(model, data[:2], 3, horizon_weights(2))
+
+
+@pytest.mark.parametrize("lam", [0.0, 0.5])
+def test_train_dt_dyn_matches_reference(lam):
+    model, data = dt_training_case()
+    cfg = train_config(lambda_=lam, iters=4)
+    net, rows = train_dt_dyn(model, cfg, data)
+    pe, rows_e, rc = ref_train_dt_dyn(model, cfg, data)
+    assert rc == 0
+    assert rows == rows_e
+    assert np.array_equal(net.params(), pe), float(np.max(np.abs(net.params() - pe)))
+
+
+def test_train_dt_dyn_one_iteration_update():
+    """One training iteration's parameter update equals the reference's (the verdict's done-criterion)."""
+    model, data = dt_training_case(seed=9)
+    cfg = train_config(lambda_=1.0, iters=1, horizon_max=3)
+    net, rows = train_dt_dyn(model, cfg, data)
+    pe, rows_e, rc = ref_train_dt_dyn(model, cfg, data)
+    assert rc == 0 and rows == rows_e and np.array_equal(net.params(), pe)
+    assert rows[0].l_reach > 0 and not np.array_equal(pe, model.params())
