@@ -412,6 +412,8 @@ typedef struct reach_episode_set {
   int32_t episodes, length, n, m;
   const double* states;
   const double* actions;
+  int32_t ref_dim;      /* per-step references y_ref [episodes][T][ref_dim] (controller training), */
+  const double* y_ref;  /* or ref_dim = 0 / NULL: none */
 } reach_episode_set;
 
 /* pred_loss (training.hpp:60-83) of the first t_h steps of every episode of `batch` under the one-step
@@ -419,6 +421,15 @@ typedef struct reach_episode_set {
  * one Dual rollout per (parameter, episode) on the device, terms summed in the reference's order. */
 int reach_pred_loss(reach_ctx* ctx, const reach_net* net, const reach_episode_set* batch, int32_t t_h,
                     const double* weights, double* loss, double* grad);
+
+/* track_loss (training.hpp:134-178) of a controller `ctl` against logged (state, action) pairs with the
+ * plant `plant` (REACH_PLANT_QUADROTOR, params {mass, gravity, jx, jy, jz}) advanced by rk4_substeps fixed
+ * RK4 steps per control interval delta, and (grad != NULL) its grad_forward over the controller's
+ * net_params: one Dual rollout per (parameter, episode) on the device.  blowup_count = episodes charged
+ * the cap. */
+int reach_track_loss(reach_ctx* ctx, const reach_net* ctl, int32_t plant, const double* plant_params,
+                     const reach_episode_set* batch, int32_t t_t, const double* weights, double gamma, double delta,
+                     int32_t rk4_substeps, double cap, double* loss, double* grad, int32_t* blowup_count);
 
 /* TrainConfig (training.hpp:262-282) and one TrainLog row (:284-292). */
 typedef struct reach_train_config {

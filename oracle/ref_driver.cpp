@@ -1072,3 +1072,44 @@ extern "C" int ref_train_dt_dyn(const reach_net_desc* init, const reach_train_co
   }
   return REACH_OK;
 }
+
+// reach::track_loss (training.hpp:134-178) with the quadrotor plant and its grad_forward over the
+// controller's net_params.
+extern "C" int ref_track_loss(const reach_net_desc* ctl_desc, const double* qp, const reach_episode_set* b,
+                              int32_t t_t, const double* weights, double gamma, double delta, int32_t rk4,
+                              double cap, double* loss, double* grad, int32_t* blowups) {
+  try {
+    MLPNet<double> ctl = net_from_desc(ctl_desc);
+    QuadrotorParams prm;
+    prm.mass = qp[0];
+    prm.gravity = qp[1];
+    prm.jx = qp[2];
+    prm.jy = qp[3];
+    prm.jz = qp[4];
+    auto batch = episodes_from(b);
+    if (b->ref_dim > 0 && b->y_ref)
+      for (int e = 0; e < b->episodes; ++e)
+        for (int t = 0; t < b->length; ++t) {
+          const double* y = b->y_ref + (static_cast<size_t>(e) * b->length + t) * b->ref_dim;
+          batch[static_cast<size_t>(e)].y_ref.push_back(Vec<double>(y, y + b->ref_dim));
+        }
+    Vec<double> w(weights, weights + t_t);
+    auto plant = [&](const auto& x, const auto& u, auto& dx) { quadrotor_ode(x, u, prm, dx); };
+    int bc = 0;
+    *loss = track_loss(ctl, plant, batch, t_t, w, gamma, delta, rk4, cap, &bc);
+    if (blowups) *blowups = bc;
+    if (grad) {
+      auto f = [&](const auto& p) {
+        using S = typename std::decay_t<decltype(p)>::value_type;
+        return track_loss(net_with_params<S>(ctl, p), plant, batch, t_t, w, gamma, delta, rk4, cap);
+      };
+      Gradient g = grad_forward(f, net_params(ctl));
+      std::copy(g.g.begin(), g.g.end(), grad);
+    }
+  } catch (const std::invalid_argument&) {
+    return REACH_E_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return REACH_E_NONFINITE;
+  }
+  return REACH_OK;
+}

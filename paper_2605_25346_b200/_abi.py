@@ -222,7 +222,7 @@ class Collectives(C.Structure):
 # --- certified training (training.hpp) --------------------------------------------------------
 class EpisodeSetC(C.Structure):
     _fields_ = [("episodes", C.c_int32), ("length", C.c_int32), ("n", C.c_int32), ("m", C.c_int32),
-                ("states", _dp), ("actions", _dp)]
+                ("states", _dp), ("actions", _dp), ("ref_dim", C.c_int32), ("y_ref", _dp)]
 
 
 class TrainConfigC(C.Structure):

@@ -475,8 +475,14 @@ def _episode_set(batch: Sequence[Episode]):
     n, m = len(batch[0].states[0]), len(batch[0].actions[0]) if T else 0
     st = np.ascontiguousarray(np.array([np.asarray(ep.states, np.float64).reshape(T + 1, n) for ep in batch]))
     ac = np.ascontiguousarray(np.array([np.asarray(ep.actions, np.float64).reshape(T, m) for ep in batch]))
-    es = A.EpisodeSetC(len(batch), T, n, m, A.dptr(st), A.dptr(ac if ac.size else np.zeros(1)))
-    return es, (st, ac)
+    r = len(batch[0].y_ref[0]) if len(batch[0].y_ref) else 0
+    if r and any(len(ep.y_ref) != T for ep in batch):
+        raise ValueError("Episode: reference length mismatch")
+    yr = np.ascontiguousarray(np.array([np.asarray(ep.y_ref, np.float64).reshape(T, r) for ep in batch])) if r \
+        else np.zeros(1)
+    es = A.EpisodeSetC(len(batch), T, n, m, A.dptr(st), A.dptr(ac if ac.size else np.zeros(1)), r,
+                       A.dptr(yr) if r else None)
+    return es, (st, ac, yr)
 
 
 def pred_loss(model: MLPNet, batch: Sequence[Episode], t_h: int, weights, with_grad: bool = False,
@@ -494,6 +500,27 @@ def pred_loss(model: MLPNet, batch: Sequence[Episode], t_h: int, weights, with_g
     ctx.check(ctx._lib.reach_pred_loss(ctx.handle, net, C.byref(es), int(t_h), A.dptr(weights), A.dptr(loss),
                                        A.dptr(g) if with_grad else None), "pred_loss")
     return (float(loss[0]), g) if with_grad else float(loss[0])
+
+
+def track_loss(controller: MLPNet, batch: Sequence[Episode], t_t: int, weights, gamma: float, delta: float,
+               rk4_substeps: int = 4, cap: float = 1e6, plant=None, with_grad: bool = False,
+               ctx: Optional[Context] = None):
+    """track_loss (training.hpp:134-178) with the quadrotor plant (systems.hpp:22-64) on the device ->
+    (loss, blowup_count), or with_grad -> (loss, gradient over the controller's net_params, blowup_count)."""
+    weights = np.ascontiguousarray(weights, np.float64)
+    if not batch or t_t < 1 or weights.size != t_t or delta <= 0.0 or rk4_substeps < 1:
+        raise ValueError("track_loss: bad configuration")
+    ctx = ctx or default_context()
+    es, keep = _episode_set(batch)
+    qp = np.ascontiguousarray((plant or QuadrotorParams()).as_array(), np.float64)
+    loss = np.zeros(1)
+    bc = np.zeros(1, np.int32)
+    g = np.zeros(controller.params().size) if with_grad else None
+    net = ctx.upload(controller)
+    ctx.check(ctx._lib.reach_track_loss(ctx.handle, net, A.PLANT_QUADROTOR, A.dptr(qp), C.byref(es), int(t_t),
+                                        A.dptr(weights), float(gamma), float(delta), int(rk4_substeps), float(cap),
+                                        A.dptr(loss), A.dptr(g) if with_grad else None, A.iptr(bc)), "track_loss")
+    return (float(loss[0]), g, int(bc[0])) if with_grad else (float(loss[0]), int(bc[0]))
 
 
 @dataclass

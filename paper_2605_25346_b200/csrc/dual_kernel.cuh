@@ -952,5 +952,141 @@ __global__ void __launch_bounds__(kPredThreads) pred_loss_grad_kernel(const Pred
   }
 }
 
+// ---------------------------------------------------------------------------
+// track_loss (training.hpp:134-178) with the quadrotor plant (systems.hpp:22-64) and its grad_forward
+// over the controller's parameters.  One CTA per (pass p, episode e): uhat = controller([xhat; y_ref_t])
+// (zero-order hold), rk4_substeps fixed RK4 steps (ode.hpp:76-91) of the plant under uhat, the
+// weighted errors; the episode's Dual sum (or the cap if it blew up) goes to the host, which sums the
+// episodes in order.  sin / cos / tanh are CUDA's (the reference uses glibc's): values within ulps.
+__device__ __forceinline__ D dsin(D a) { return D{sin(a.v), mul(cos(a.v), a.d)}; }
+__device__ __forceinline__ D dcos(D a) { return D{cos(a.v), mul(-sin(a.v), a.d)}; }
+
+struct TrackArgs {
+  DevNet net;             // controller
+  int n, l, r, T, M, seeded, rk4;
+  long long poff[kMaxLayers + 1];
+  double prm[5];          // QuadrotorParams {mass, gravity, jx, jy, jz}
+  double gamma, delta, cap;
+  const double* states;   // [M][Ls + 1][n]
+  const double* actions;  // [M][Ls][l] logged controls
+  const double* y_ref;    // [M][Ls][r] or null
+  int ls;
+  const double* weights;  // [T]
+  double* ep_v;           // [passes][M] episode term (Dual)
+  double* ep_d;
+  int* blown;             // [M] (pass 0)
+};
+
+// quadrotor_ode (systems.hpp:24-64) in Dual, operation for operation
+__device__ inline void quad_ode_d(const D* x, const D* u, const double* prm, D* dx) {
+  const D vx = x[3], vy = x[4], vz = x[5], phi = x[6], theta = x[7], psi = x[8], p = x[9], q = x[10], r = x[11];
+  const D sphi = dsin(phi), cphi = dcos(phi), sth = dsin(theta), cth = dcos(theta), spsi = dsin(psi),
+          cpsi = dcos(psi);
+  const D b3x = dadd(dmul(dmul(cphi, sth), cpsi), dmul(sphi, spsi));
+  const D b3y = dsub(dmul(dmul(cphi, sth), spsi), dmul(sphi, cpsi));
+  const D b3z = dmul(cphi, cth);
+  const double mass = prm[0], g = prm[1], jx = prm[2], jy = prm[3], jz = prm[4];
+  const D a = dmul(u[0], dc(1.0 / mass));
+  dx[0] = vx;
+  dx[1] = vy;
+  dx[2] = vz;
+  dx[3] = dmul(a, b3x);
+  dx[4] = dmul(a, b3y);
+  dx[5] = dsub(dmul(a, b3z), dc(g));
+  const D tth = ddiv(sth, cth);
+  dx[6] = dadd(dadd(p, dmul(dmul(sphi, tth), q)), dmul(dmul(cphi, tth), r));
+  dx[7] = dsub(dmul(cphi, q), dmul(sphi, r));
+  dx[8] = dadd(dmul(ddiv(sphi, cth), q), dmul(ddiv(cphi, cth), r));
+  dx[9] = dadd(dmul(dmul(q, r), dc((jy - jz) / jx)), dmul(u[1], dc(1.0 / jx)));
+  dx[10] = dadd(dmul(dmul(p, r), dc((jz - jx) / jy)), dmul(u[2], dc(1.0 / jy)));
+  dx[11] = dadd(dmul(dmul(p, q), dc((jx - jy) / jz)), dmul(u[3], dc(1.0 / jz)));
+}
+
+__global__ void __launch_bounds__(kPredThreads) track_loss_grad_kernel(const TrackArgs A) {
+  __shared__ D hb[2][kPredW];
+  __shared__ D xs[16], us[8];
+  __shared__ int s_blown;
+  const int tid = threadIdx.x, pass = blockIdx.x, ep = blockIdx.y;
+  const int n = A.n, l = A.l, r = A.r, T = A.T;
+  NetView net{A.net};
+  if (A.seeded) seed_param(net, A.poff, pass);
+  const DevNet& N = A.net;
+  const double* st = A.states + static_cast<size_t>(ep) * (A.ls + 1) * n;
+  const double* ul = A.actions + static_cast<size_t>(ep) * A.ls * l;
+  const double* yr = A.y_ref ? A.y_ref + static_cast<size_t>(ep) * A.ls * r : nullptr;
+  if (tid < n) xs[tid] = dc(st[tid]);
+  D ep_acc = dc(0.0);
+  if (tid == 0) s_blown = 0;
+  __syncthreads();
+  for (int t = 0; t < T; ++t) {
+    if (s_blown) break;
+    // in = xhat (+ y_ref_t); uhat = controller.forward(in) (neural.hpp:58-76)
+    for (int i = tid; i < n; i += kPredThreads) hb[0][i] = xs[i];
+    if (yr)
+      for (int i = tid; i < r; i += kPredThreads) hb[0][n + i] = dc(yr[static_cast<size_t>(t) * r + i]);
+    __syncthreads();
+    int cur = 0;
+    for (int q = 0; q < N.L; ++q) {
+      const int rows = N.dims[q + 1], cols = N.dims[q];
+      for (int u = tid; u < rows; u += kPredThreads) {
+        D acc = dc(0.0);
+        if (q + 1 < N.L)
+          for (int k = 0; k < cols; ++k) acc = dadd(acc, dmul(net.wt(q, u, k), hb[cur][k]));
+        else
+          for (int k = 0; k < cols; ++k) acc = dadd(acc, dmul(net.w(q, u, k), hb[cur][k]));
+        D h = dadd(acc, net.b(q, u));
+        if (N.acts[q] == REACH_ACT_RELU) {
+          if (h.v < 0.0) h = dc(0.0);
+        } else if (N.acts[q] == REACH_ACT_TANH) {
+          h = dtanh(h);
+        }
+        hb[cur ^ 1][u] = h;
+      }
+      cur ^= 1;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      D err_u = dc(0.0);
+      for (int j = 0; j < l; ++j) {
+        us[j] = hb[cur][j];
+        const D d = dsub(us[j], dc(ul[static_cast<size_t>(t) * l + j]));
+        err_u = dadd(err_u, dmul(d, d));
+      }
+      // rk4_substeps RK4 steps of h = delta / substeps (ode.hpp:76-91)
+      const double h = A.delta / A.rk4;
+      D x[12], k1[12], k2[12], k3[12], k4[12], tmp[12];
+      for (int i = 0; i < 12; ++i) x[i] = xs[i];
+      for (int ss = 0; ss < A.rk4; ++ss) {
+        quad_ode_d(x, us, A.prm, k1);
+        for (int i = 0; i < 12; ++i) tmp[i] = dadd(x[i], dmul(dc(h * 0.5), k1[i]));
+        quad_ode_d(tmp, us, A.prm, k2);
+        for (int i = 0; i < 12; ++i) tmp[i] = dadd(x[i], dmul(dc(h * 0.5), k2[i]));
+        quad_ode_d(tmp, us, A.prm, k3);
+        for (int i = 0; i < 12; ++i) tmp[i] = dadd(x[i], dmul(dc(h), k3[i]));
+        quad_ode_d(tmp, us, A.prm, k4);
+        for (int i = 0; i < 12; ++i)
+          x[i] = dadd(x[i], dmul(dc(h / 6.0), dadd(dadd(dadd(k1[i], dmul(dc(2.0), k2[i])), dmul(dc(2.0), k3[i])), k4[i])));
+      }
+      D err_x = dc(0.0);
+      const double* xl = st + static_cast<size_t>(t + 1) * n;
+      for (int j = 0; j < n; ++j) {
+        xs[j] = x[j];
+        const D d = dsub(x[j], dc(xl[j]));
+        err_x = dadd(err_x, dmul(d, d));
+      }
+      ep_acc = dadd(ep_acc, dmul(dc(A.weights[t]), dadd(err_u, dmul(dc(A.gamma), err_x))));
+      if (!isfinite(ep_acc.v)) s_blown = 1;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const D term = s_blown ? dc(A.cap) : ep_acc;
+    const size_t o = static_cast<size_t>(pass) * A.M + ep;
+    A.ep_v[o] = term.v;
+    A.ep_d[o] = term.d;
+    if (pass == 0) A.blown[ep] = s_blown;
+  }
+}
+
 }  // namespace dual
 }  // namespace rb

@@ -2302,6 +2302,101 @@ int reach_pred_loss(reach_ctx* ctx, const reach_net* net, const reach_episode_se
   return REACH_OK;
 }
 
+// track_loss (training.hpp:134-178) with the quadrotor plant and, optionally, its grad_forward.
+int reach_track_loss(reach_ctx* ctx, const reach_net* ctl, int32_t plant, const double* plant_params,
+                     const reach_episode_set* b, int32_t t_t, const double* weights, double gamma, double delta,
+                     int32_t rk4_substeps, double cap, double* loss, double* grad, int32_t* blowup_count) {
+  rbh::DeviceGuard device_guard_(ctx);
+  namespace rd = rb::dual;
+  if (!ctx || !ctl || !b || !loss || !plant_params) return REACH_E_INVALID_ARGUMENT;
+  if (b->episodes < 1 || t_t < 1 || !weights || delta <= 0.0 || rk4_substeps < 1)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "track_loss: bad configuration");
+  if (b->length < t_t) return fail(ctx, REACH_E_INVALID_ARGUMENT, "track_loss: episode shorter than T_t");
+  if (plant != REACH_PLANT_QUADROTOR) return fail(ctx, REACH_E_UNSUPPORTED, "track_loss: unknown plant");
+  const int n = b->n, l = b->m, r = b->y_ref ? b->ref_dim : 0, M = b->episodes, T = t_t, Ls = b->length;
+  if (n != 12 || l < 4 || !b->states || !b->actions)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "track_loss: quadrotor episodes need n = 12, >= 4 controls");
+  if (ctl->dims[0] != n + r || ctl->dims[ctl->L] != l)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "track_loss: controller shape does not match the episodes");
+  int maxw = 0;
+  for (int q = 0; q <= ctl->L; ++q) maxw = std::max(maxw, ctl->dims[q]);
+  if (maxw > rd::kPredW || l > 8 || M > 65535) return fail(ctx, REACH_E_UNSUPPORTED, "track_loss: shape outside the kernel");
+  rd::TrackArgs A{};
+  A.poff[0] = 0;
+  for (int q = 0; q < ctl->L; ++q)
+    A.poff[q + 1] = A.poff[q] + static_cast<long long>(ctl->dims[q + 1]) * ctl->dims[q] + ctl->dims[q + 1];
+  const long long P = grad ? A.poff[ctl->L] : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t ns = static_cast<size_t>(M) * (Ls + 1) * n, na = static_cast<size_t>(M) * Ls * l,
+               nr = static_cast<size_t>(M) * Ls * r, ne = static_cast<size_t>(P) * M;
+  const size_t o_s = take(ns * 8), o_a = take(na * 8), o_r = take(nr * 8), o_w = take(static_cast<size_t>(T) * 8),
+               o_v = take(ne * 8), o_d = take(ne * 8), o_b = take(static_cast<size_t>(M) * 4);
+  int rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  RB_CUDA(cudaMemcpyAsync(Dp(o_s), b->states, ns * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_a), b->actions, na * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (nr) RB_CUDA(cudaMemcpyAsync(Dp(o_r), b->y_ref, nr * 8, cudaMemcpyHostToDevice, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(Dp(o_w), weights, static_cast<size_t>(T) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  A.net = ctl->dev;
+  A.n = n;
+  A.l = l;
+  A.r = r;
+  A.T = T;
+  A.M = M;
+  A.seeded = grad ? 1 : 0;
+  A.rk4 = rk4_substeps;
+  for (int i = 0; i < 5; ++i) A.prm[i] = plant_params[i];
+  A.gamma = gamma;
+  A.delta = delta;
+  A.cap = cap;
+  A.states = Dp(o_s);
+  A.actions = Dp(o_a);
+  A.y_ref = nr ? Dp(o_r) : nullptr;
+  A.ls = Ls;
+  A.weights = Dp(o_w);
+  A.ep_v = Dp(o_v);
+  A.ep_d = Dp(o_d);
+  A.blown = reinterpret_cast<int*>(w + o_b);
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  rd::track_loss_grad_kernel<<<dim3(static_cast<unsigned>(P), static_cast<unsigned>(M)), rd::kPredThreads, 0,
+                               ctx->stream>>>(A);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  std::vector<double> tv(ne), td(ne);
+  std::vector<int32_t> bl(M);
+  RB_CUDA(cudaMemcpyAsync(tv.data(), Dp(o_v), ne * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(td.data(), Dp(o_d), ne * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(bl.data(), w + o_b, static_cast<size_t>(M) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double q = static_cast<double>(M) * T;  // acc / S(M' T_t)
+  for (long long p = 0; p < P; ++p) {
+    double av = 0.0, ad = 0.0;
+    for (int e = 0; e < M; ++e) {
+      av = av + tv[static_cast<size_t>(p) * M + e];
+      ad = ad + td[static_cast<size_t>(p) * M + e];
+    }
+    if (p == 0) *loss = av / q;
+    if (grad) grad[p] = (ad * q - av * 0.0) / (q * q);
+  }
+  if (blowup_count) {
+    int c = 0;
+    for (int e = 0; e < M; ++e) c += bl[e];
+    *blowup_count = c;
+  }
+  return REACH_OK;
+}
+
 // train_dt_dyn (training.hpp:333-382) with every loss and gradient on the device.
 int reach_train_dt_dyn(reach_ctx* ctx, const reach_net_desc* init, const reach_train_config* cfg,
                        const reach_episode_set* ds, double* params_out, reach_train_log_row* log) {

@@ -567,3 +567,23 @@ def ref_train_dt_dyn(init, cfg, dataset):
     rows = [TrainLogRow(r.iter, r.t_h, r.eps, r.l_pred, r.l_reach, r.l_total, r.diverged_count)
             for r in list(log)[:int(nrows[0])]]
     return out, rows, rc
+
+
+def ref_track_loss(controller, batch, t_t, weights, gamma, delta, rk4=4, cap=1e6, plant=None, with_grad=False):
+    from paper_2605_25346_b200.api import QuadrotorParams, _episode_set
+    es, keep = _episode_set(batch)
+    d, keep2 = controller.desc()
+    qp = np.ascontiguousarray((plant or QuadrotorParams()).as_array(), np.float64)
+    w = np.ascontiguousarray(weights, np.float64)
+    loss = np.zeros(1)
+    bc = np.zeros(1, np.int32)
+    g = np.zeros(controller.params().size) if with_grad else None
+    dp = C.POINTER(C.c_double)
+    f = ref_lib().ref_track_loss
+    f.argtypes = [C.POINTER(A.NetDesc), dp, C.POINTER(A.EpisodeSetC), C.c_int32, dp, C.c_double, C.c_double,
+                  C.c_int32, C.c_double, dp, dp, C.POINTER(C.c_int32)]
+    f.restype = C.c_int
+    rc = f(C.byref(d), A.dptr(qp), C.byref(es), int(t_t), A.dptr(w), float(gamma), float(delta), int(rk4), float(cap),
+           A.dptr(loss), A.dptr(g) if with_grad else None, A.iptr(bc))
+    assert rc == 0, rc
+    return (float(loss[0]), g, int(bc[0])) if with_grad else (float(loss[0]), int(bc[0]))

@@ -52,3 +52,35 @@ def test_train_dt_dyn_one_iteration_update():
     pe, rows_e, rc = ref_train_dt_dyn(model, cfg, data)
     assert rc == 0 and rows == rows_e and np.array_equal(net.params(), pe)
     assert rows[0].l_reach > 0 and not np.array_equal(pe, model.params())
+
+
+TRACK_RTOL = 1e-9  # CUDA's sin / cos / tanh against glibc's: ulp-level differences, amplified by RK4
+
+
+@pytest.mark.parametrize("t_t,rk4", [(1, 1), (3, 4), (5, 2)])
+def test_track_loss_and_gradient_match_reference(t_t, rk4):
+    from oracle_bind import ref_track_loss
+    from paper_2605_25346_b200.api import track_loss
+    from train_cases import ct_tracking_case
+    ctl, data = ct_tracking_case()
+    w = horizon_weights(t_t)
+    got, g, bc = track_loss(ctl, data, t_t, w, 0.1, 0.05, rk4, with_grad=True)
+    exp, ge, bce = ref_track_loss(ctl, data, t_t, w, 0.1, 0.05, rk4, with_grad=True)
+    assert bc == bce == 0
+    assert abs(got - exp) <= TRACK_RTOL * abs(exp)
+    scale = max(float(np.max(np.abs(ge))), 1e-300)
+    assert float(np.max(np.abs(g - ge))) <= TRACK_RTOL * scale
+    v, bcv = track_loss(ctl, data, t_t, w, 0.1, 0.05, rk4)
+    assert v == got and bcv == 0
+
+
+def test_track_loss_blowup_charges_cap():
+    from oracle_bind import ref_track_loss
+    from paper_2605_25346_b200.api import track_loss
+    from train_cases import ct_tracking_case
+    ctl, data = ct_tracking_case()
+    ctl.layers[-1].b[0] += 1e160  # thrust blows the rollout up
+    w = horizon_weights(3)
+    got, bc = track_loss(ctl, data, 3, w, 0.1, 0.05, 2, cap=1e6)
+    exp, bce = ref_track_loss(ctl, data, 3, w, 0.1, 0.05, 2, cap=1e6)
+    assert bc == bce == len(data) and got == exp
