@@ -11,7 +11,8 @@
 //     with a non-zero slope, or the generator rows of the input TM -- streamed
 //     through a cp.async ring;
 //   * the symbolic state (c, [G0 | Q1 .. Qnq] for x and the controller's u rows)
-//     lives in two ping-pong buffers in global memory (L2-resident per CTA);
+//     lives in ONE buffer per CTA in global memory (L2-resident): the certified
+//     output overwrites its input in place (column j from column base + j);
 //     fold_overflow runs as a CTA-parallel partial-pivot elimination in shared
 //     memory; popping the oldest block moves G0 right instead of moving the queue.
 // Every reduction keeps the reference's order with separate roundings, so the
@@ -767,7 +768,6 @@ __global__ void __launch_bounds__(kWideThreads, 1) dt_wide_kernel(const DTParams
 
   const long long lds = P.w_lds;
   double* buf0 = P.wws + static_cast<long long>(blockIdx.x) * P.wws_stride;
-  double* buf1 = buf0 + static_cast<long long>(P.w_rows) * lds;
   WPhase ph{P.w_phase, clock64(), WP_SETUP};
 
   for (long long b = blockIdx.x; b < P.B; b += gridDim.x) {
@@ -809,7 +809,6 @@ __global__ void __launch_bounds__(kWideThreads, 1) dt_wide_kernel(const DTParams
       }
     };
     double* cur = buf0;
-    double* oth = buf1;
     int base = 0, nq = 0;
     auto init_state = [&]() {  // from the box in xlo / xhi
       for (int e = tid; e < n * n; e += kWideThreads) {
@@ -854,8 +853,10 @@ __global__ void __launch_bounds__(kWideThreads, 1) dt_wide_kernel(const DTParams
         cin = W.cag;
         frad = W.urad;
       }
-      // ---- dynamics / one-step map: certify_tm_input (neural.hpp:342-394) into the other buffer
-      const int rc = wide_certify<RD>(P.net, n_i, n, n, u, cur + base, lds, nz, frad, cin, oth, lds, W, ph, 5);
+      // ---- dynamics / one-step map: certify_tm_input (neural.hpp:342-394), its output written in place at
+      // column 0 of the same buffer: output column j depends only on input column base + j >= j, and every
+      // column pass of the prepend GEMM has read its input before it writes (one state buffer per CTA)
+      const int rc = wide_certify<RD>(P.net, n_i, n, n, u, cur + base, lds, nz, frad, cin, cur, lds, W, ph, 5);
       if (rc != WC_OK) {
         status = (rc == WC_PREACT) ? ST_PREACT : ST_CERT;
         failed_step = k;
@@ -875,15 +876,10 @@ __global__ void __launch_bounds__(kWideThreads, 1) dt_wide_kernel(const DTParams
       __syncthreads();
       for (int e = tid; e < n * n; e += kWideThreads) {
         const int i = e / n, j = e - i * n;
-        oth[i * lds + nza + j] = (i == j) ? W.radv[i] : 0.0;
+        cur[i * lds + nza + j] = (i == j) ? W.radv[i] : 0.0;
       }
       nq += (lc > 0) ? 2 : 1;
       base = 0;
-      {
-        double* t = cur;
-        cur = oth;
-        oth = t;
-      }
       __syncthreads();
       // ---- fold_overflow (flowpipe_ct.hpp:317-350)
       ph.mark(WP_FOLD);
