@@ -512,6 +512,56 @@ def closed_loop_legs(args, ctx, world, rank, dev, barrier, stream):
           "roofline": {"bound": "fp64", "achieved": ach, "peak": tf_fma, "unit": "TFLOP/s", "frac": ach / tf_fma,
                        "flops_per_reach_step": fl, "exact_mode_ceiling_tflops": tf_ma},
           "parity": "bit-identical to the oracle / reference composition (tests/test_gpu_wide.py)"}
+    # the tolerance modes of the same batch (kernel time) and an in-bench parity spot check: 8 strided
+    # samples against the oracle -- exact bit for bit, fused / tc within rtol = 1e-5
+    modes = {}
+    outs = {"exact": r}
+    for prec in ("fused", "tc"):
+        if prec == "tc" and args.no_tc:
+            continue
+        try:
+            dt_closed_loop_batch(w.dyn, w.ctl, w.n, w.x0_lo, w.x0_hi, w.horizon, ctx=ctx, precision=prec)
+            barrier()
+            ctx.enable_kernel_timing(True)
+            ctx.kernel_time()
+            rp = dt_closed_loop_batch(w.dyn, w.ctl, w.n, w.x0_lo, w.x0_hi, w.horizon, ctx=ctx, precision=prec)
+            ms, nl = ctx.kernel_time()
+            ctx.enable_kernel_timing(False)
+            outs[prec] = rp
+            modes[prec] = {"ms_per_batch": ms, "reach_steps_per_s": B * w.horizon / (ms / 1e3),
+                           "ok": int((rp.status == 0).sum()),
+                           "kernel": "rbf::dt_wide_kernel<9,3>" if prec == "fused" else "rb::dt_tcw_kernel"}
+            if prec == "fused":
+                a = fl * B * w.horizon / (ms / 1e3) / 1e12
+                modes[prec]["tflops"] = a
+                modes[prec]["frac_dfma_peak"] = a / tf_fma
+        except Exception as ex:  # noqa: BLE001
+            modes[prec] = {"error": str(ex)}
+    c5["modes"] = modes
+    if rank == 0:
+        try:
+            from oracle_bind import oracle_dtcl_batch, same_bits
+            idx = np.arange(0, B, max(B // 8, 1))[:8]
+            e = oracle_dtcl_batch(w.dyn, w.ctl, w.n, w.x0_lo[idx], w.x0_hi[idx], w.horizon)
+            chk = {"samples": int(len(idx)), "rtol": 1e-5}
+            for prec, rr in outs.items():
+                k = e.n_boxes
+                glo, ghi = rr.lo[idx], rr.hi[idx]
+                if prec == "exact":
+                    chk["exact_bit_exact"] = bool(np.array_equal(rr.n_boxes[idx], k) and
+                                                  all(same_bits(glo[i, :k[i]], e.lo[i, :k[i]]) and
+                                                      same_bits(ghi[i, :k[i]], e.hi[i, :k[i]]) for i in range(len(idx))))
+                else:
+                    dev_ = 0.0
+                    for i in range(len(idx)):
+                        el, eh = e.lo[i, :k[i]], e.hi[i, :k[i]]
+                        sc = np.maximum(np.maximum(np.abs(el), np.abs(eh)), eh - el)
+                        dev_ = max(dev_, float(np.max(np.abs(glo[i, :k[i]] - el) / sc)),
+                                   float(np.max(np.abs(ghi[i, :k[i]] - eh) / sc)))
+                    chk[f"{prec}_max_rel_dev"] = dev_
+            c5["parity_check"] = chk
+        except Exception as ex:  # noqa: BLE001
+            c5["parity_check"] = {"error": str(ex)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle_bind import ref_available, ref_dtcl_batch, ref_lib
