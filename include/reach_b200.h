@@ -563,6 +563,16 @@ int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* field, const reach_fl
 int reach_ct_split_hull(reach_ctx* ctx, const reach_field_desc* field, const reach_flowpipe_params* fp,
                         const reach_cl_split_args* args, const reach_hull_out* out, int32_t flags);
 
+/* ctl_reach_loss (training.hpp:183-213) with the quadrotor plant: (1/M) sum_e [tube diverged ? cap :
+ * log(1 + predicted_volume(cl_reach(spec, box_from_center(x0_e, eps))))] with spec->ctl_steps = t_h,
+ * spec->fp.h = delta / k_atomic, and (grad != NULL) its grad_forward over the controller's net_params:
+ * one Dual cl_reach per (parameter, episode) on the device (warp per pass, working set in shared
+ * memory).  x0s [M][n]; y_refs [M][ctl_steps][ref_dim] per episode (spec->y_ref unused), NULL when
+ * spec->ref_dim = 0.  diverged_count = episodes charged the cap. */
+int reach_ctl_reach_loss(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* spec, int32_t episodes,
+                         const double* x0s, const double* y_refs, double eps, double cap, double* loss, double* grad,
+                         int32_t* diverged_count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1113,3 +1113,49 @@ extern "C" int ref_track_loss(const reach_net_desc* ctl_desc, const double* qp, 
   }
   return REACH_OK;
 }
+
+// reach::ctl_reach_loss with its grad_forward over the controller's net_params (training.hpp:183-213,
+// refine.hpp:186-207); episodes as ref_ctl_reach_loss.
+extern "C" int ref_ctl_reach_loss_grad(const reach_net_desc* ctl_desc, const reach_cl_spec* sp, int32_t M,
+                                       const double* x0s, const double* yrefs, const int32_t* has_yref,
+                                       int32_t ref_dim, double eps, int32_t t_h, double delta, double cap,
+                                       double* loss, double* grad, int32_t* diverged_count) {
+  try {
+    ClosedLoopSpec<double> base = cl_spec_from(ctl_desc, sp);
+    QuadrotorParams prm;
+    prm.mass = sp->plant_params[0];
+    prm.gravity = sp->plant_params[1];
+    prm.jx = sp->plant_params[2];
+    prm.jy = sp->plant_params[3];
+    prm.jz = sp->plant_params[4];
+    auto plant = [prm](const auto& x, const auto& u, auto& dx) { quadrotor_ode(x, u, prm, dx); };
+    std::vector<Episode> batch(static_cast<size_t>(M));
+    for (int e = 0; e < M; ++e) {
+      Episode& ep = batch[static_cast<size_t>(e)];
+      Vec<double> s(x0s + static_cast<size_t>(e) * sp->n, x0s + static_cast<size_t>(e + 1) * sp->n);
+      ep.states.assign(static_cast<size_t>(t_h) + 1, s);
+      ep.actions.assign(static_cast<size_t>(t_h), Vec<double>(static_cast<size_t>(sp->l), 0.0));
+      if (has_yref && has_yref[e])
+        for (int t = 0; t < t_h; ++t) {
+          const double* r = yrefs + (static_cast<size_t>(e) * t_h + t) * ref_dim;
+          ep.y_ref.emplace_back(r, r + ref_dim);
+        }
+    }
+    int dc = 0;
+    *loss = ctl_reach_loss(base.controller, plant, batch, eps, t_h, sp->n, sp->l, delta, sp->k_atomic, cap, &dc,
+                           base.fp);
+    if (diverged_count) *diverged_count = dc;
+    auto f = [&](const auto& p) {
+      using S = typename std::decay_t<decltype(p)>::value_type;
+      return ctl_reach_loss(net_with_params<S>(base.controller, p), plant, batch, eps, t_h, sp->n, sp->l, delta,
+                            sp->k_atomic, cap, nullptr, base.fp);
+    };
+    Gradient g = grad_forward(f, net_params(base.controller));
+    std::copy(g.g.begin(), g.g.end(), grad);
+  } catch (const std::invalid_argument&) {
+    return REACH_E_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return REACH_E_NONFINITE;
+  }
+  return REACH_OK;
+}

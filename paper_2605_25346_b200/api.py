@@ -994,11 +994,12 @@ def _predicted_volume(lo: np.ndarray, hi: np.ndarray) -> float:
 def ctl_reach_loss(controller: MLPNet, batch: Sequence[Episode], eps: float, t_h: int, delta: float,
                    k_atomic: int, cap: float, fp_base: Optional[FlowpipeParams] = None,
                    plant: Optional[QuadrotorParams] = None, n: int = 12, l: int = 4,
-                   ctx: Optional[Context] = None):
-    """ctl_reach_loss (training.hpp:183-213) value with the quadrotor plant: cl_reach from the eps-ball
-    around each episode start, every tube on the device (episodes sharing a reference sequence in one
-    batch) -> (loss, diverged_count).  As the reference, an episode without y_ref keeps the previous
-    episode's reference sequence."""
+                   ctx: Optional[Context] = None, with_grad: bool = False):
+    """ctl_reach_loss (training.hpp:183-213) with the quadrotor plant: cl_reach from the eps-ball around
+    each episode start, every tube on the device (episodes sharing a reference sequence in one batch)
+    -> (loss, diverged_count); with_grad -> (loss, grad_forward over the controller's net_params,
+    diverged_count): one Dual cl_reach per (parameter, episode) in one launch (reach_ctl_reach_loss).
+    As the reference, an episode without y_ref keeps the previous episode's reference sequence."""
     if not batch or t_h < 1:
         raise ValueError("ctl_reach_loss: bad batch/horizon")
     fp = dataclasses.replace(fp_base or FlowpipeParams())
@@ -1008,6 +1009,25 @@ def ctl_reach_loss(controller: MLPNet, batch: Sequence[Episode], eps: float, t_h
         if len(ep.y_ref):
             cur = np.ascontiguousarray(np.asarray(ep.y_ref[:t_h], np.float64).reshape(t_h, -1))
         yrefs.append(cur)
+    if with_grad:
+        ctx = ctx or default_context()
+        rd = 0 if yrefs[0] is None else yrefs[0].shape[1]
+        if rd and any(y is None for y in yrefs):
+            raise ValueError("freeze_trailing_inputs: dimension mismatch")
+        spec = ClosedLoopSpec(controller, n=n, l=l, ctl_steps=t_h, k_atomic=k_atomic,
+                              y_ref=yrefs[0] if rd else None, fp=dataclasses.replace(fp),
+                              plant_params=plant or QuadrotorParams())
+        cs, keep = spec.c_struct()
+        x0 = np.ascontiguousarray([np.asarray(ep.states[0], np.float64) for ep in batch])
+        yr = np.ascontiguousarray(np.array(yrefs, np.float64)) if rd else np.zeros(1)
+        loss = np.zeros(1)
+        g = np.zeros(controller.params().size)
+        dc = np.zeros(1, np.int32)
+        net = ctx.upload(controller)
+        ctx.check(ctx._lib.reach_ctl_reach_loss(ctx.handle, net, C.byref(cs), len(batch), A.dptr(x0),
+                                                A.dptr(yr) if rd else None, float(eps), float(cap), A.dptr(loss),
+                                                A.dptr(g), A.iptr(dc)), "ctl_reach_loss")
+        return float(loss[0]), g, int(dc[0])
     groups = {}
     for e, yr in enumerate(yrefs):
         groups.setdefault(None if yr is None else yr.tobytes(), []).append(e)

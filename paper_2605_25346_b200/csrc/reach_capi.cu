@@ -26,6 +26,7 @@
 #include "../../include/reach_b200.h"
 #include "diag.cuh"
 #include "dual_kernel.cuh"
+#include "ct_dual.cuh"
 #include "dt_kernel.cuh"
 #include "plan.cuh"
 #include "wide_kernel.cuh"
@@ -2393,6 +2394,107 @@ int reach_track_loss(reach_ctx* ctx, const reach_net* ctl, int32_t plant, const 
     int c = 0;
     for (int e = 0; e < M; ++e) c += bl[e];
     *blowup_count = c;
+  }
+  return REACH_OK;
+}
+
+// ctl_reach_loss (training.hpp:183-213) with the quadrotor plant: value and, optionally, its grad_forward
+// over the controller's parameters -- one Dual cl_reach per (parameter, episode) (ct_dual.cuh).
+int reach_ctl_reach_loss(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* sp, int32_t episodes,
+                         const double* x0s, const double* y_refs, double eps, double cap, double* loss, double* grad,
+                         int32_t* diverged_count) {
+  rbh::DeviceGuard device_guard_(ctx);
+  namespace cd = rb::ctd;
+  if (!ctx || !ctl || !sp || !x0s || !loss) return REACH_E_INVALID_ARGUMENT;
+  if (episodes < 1 || sp->ctl_steps < 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "ctl_reach_loss: bad batch/horizon");
+  if (sp->plant != REACH_PLANT_QUADROTOR || sp->n != 12 || sp->l != 4)
+    return fail(ctx, REACH_E_UNSUPPORTED, "ctl_reach_loss: the quadrotor plant (n = 12, l = 4) only");
+  if (eps < 0.0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "box_from_center: negative radius");
+  const int n = sp->n, l = sp->l, na = n + l, M = episodes, r = sp->ref_dim;
+  if (ctl->dims[0] != n + r || ctl->dims[ctl->L] != l)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "ClosedLoopSpec: controller input dim mismatch");
+  if (r > 0 && !y_refs) return fail(ctx, REACH_E_INVALID_ARGUMENT, "ctl_reach_loss: missing reference sequences");
+  if (sp->k_atomic < 1 || !(sp->fp.h > 0.0) || sp->fp.order < 1)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "ClosedLoopSpec: invalid flowpipe parameters");
+  const int cap_q = sp->fp.window > 0 ? sp->fp.window : 1;
+  int maxw = 0;
+  for (int q = 1; q < ctl->L; ++q) maxw = std::max(maxw, ctl->dims[q]);
+  if (na > cd::MR || n + (cap_q + 1) * na > cd::MZ || maxw > cd::CW || l > cd::CO || M > 65535 ||
+      n + (cap_q + 1) * na + n > cd::CA)
+    return fail(ctx, REACH_E_UNSUPPORTED, "ctl_reach_loss: shape outside the Dual CT kernel");
+  cd::CtlLossArgs A{};
+  A.poff[0] = 0;
+  for (int q = 0; q < ctl->L; ++q)
+    A.poff[q + 1] = A.poff[q] + static_cast<long long>(ctl->dims[q + 1]) * ctl->dims[q] + ctl->dims[q + 1];
+  const long long P = grad ? A.poff[ctl->L] : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 8), 256);
+    return o;
+  };
+  const size_t nyr = static_cast<size_t>(M) * sp->ctl_steps * std::max(r, 0);
+  const size_t o_x = take(static_cast<size_t>(M) * n * 8), o_y = take(nyr * 8),
+               o_v = take(static_cast<size_t>(P) * M * 8), o_d = take(static_cast<size_t>(P) * M * 8),
+               o_dv = take(static_cast<size_t>(M) * 4);
+  int rc = ensure_ws(ctx, off);
+  if (rc) return rc;
+  char* w = static_cast<char*>(ctx->ws);
+  auto Dp = [&](size_t o) { return reinterpret_cast<double*>(w + o); };
+  RB_CUDA(cudaMemcpyAsync(Dp(o_x), x0s, static_cast<size_t>(M) * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (nyr) RB_CUDA(cudaMemcpyAsync(Dp(o_y), y_refs, nyr * 8, cudaMemcpyHostToDevice, ctx->stream));
+  A.net = ctl->dev;
+  A.n = n;
+  A.l = l;
+  A.rdim = r;
+  A.ctl_steps = sp->ctl_steps;
+  A.k_atomic = sp->k_atomic;
+  A.intervalize = sp->intervalize_boundary;
+  A.M = M;
+  A.seeded = grad ? 1 : 0;
+  for (int i = 0; i < 5; ++i) A.prm[i] = sp->plant_params[i];
+  A.F = cd::FlowCfg{sp->fp.h, sp->fp.eps_init, sp->fp.enlargement, sp->fp.order, sp->fp.refine_rounds,
+                    sp->fp.max_enlargements, sp->fp.window};
+  A.eps = eps;
+  A.cap = cap;
+  A.x0 = Dp(o_x);
+  A.yref = nyr ? Dp(o_y) : nullptr;
+  A.term_v = Dp(o_v);
+  A.term_d = Dp(o_d);
+  A.diverged = reinterpret_cast<int*>(w + o_dv);
+  const size_t smem = sizeof(cd::Work);
+  if (smem > static_cast<size_t>(ctx->max_smem))
+    return fail(ctx, REACH_E_UNSUPPORTED, "ctl_reach_loss: Dual working set exceeds shared memory");
+  RB_CUDA(cudaFuncSetAttribute(cd::ctl_reach_loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  cd::ctl_reach_loss_grad_kernel<<<dim3(static_cast<unsigned>(P), static_cast<unsigned>(M)), 32, smem, ctx->stream>>>(A);
+  RB_CUDA(cudaGetLastError());
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
+  ctx->launches += 1;
+  std::vector<double> tv(static_cast<size_t>(P) * M), td(tv.size());
+  std::vector<int32_t> dv(M);
+  RB_CUDA(cudaMemcpyAsync(tv.data(), Dp(o_v), tv.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(td.data(), Dp(o_d), td.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaMemcpyAsync(dv.data(), w + o_dv, static_cast<size_t>(M) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double Md = static_cast<double>(M);  // acc / S(batch.size())
+  for (long long p = 0; p < P; ++p) {
+    double av = 0.0, ad = 0.0;
+    for (int e = 0; e < M; ++e) {
+      av = av + tv[static_cast<size_t>(p) * M + e];
+      ad = ad + td[static_cast<size_t>(p) * M + e];
+    }
+    if (p == 0) *loss = av / Md;
+    if (grad) grad[p] = (ad * Md - av * 0.0) / (Md * Md);
+  }
+  if (diverged_count) {
+    int c = 0;
+    for (int e = 0; e < M; ++e) c += dv[e];
+    *diverged_count = c;
   }
   return REACH_OK;
 }

@@ -510,11 +510,14 @@ def ref_dt_interval_baseline_batch(sys, x0_lo, x0_hi, actions):
     return out
 
 
-def ref_ctl_reach_loss(spec, x0s, yrefs, eps, t_h, delta, cap):
-    """The reference's ctl_reach_loss (quadrotor plant, fp_base = spec.fp) -> (loss, diverged_count)."""
+def ref_ctl_reach_loss(spec, x0s, yrefs, eps, t_h, delta, cap, with_grad=False):
+    """The reference's ctl_reach_loss (quadrotor plant, fp_base = spec.fp) -> (loss, diverged_count), or
+    with_grad -> (loss, grad_forward over the controller's net_params, diverged_count)."""
     dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
-    f = _mpc_fn(ref_lib(), "ref_ctl_reach_loss", [C.POINTER(A.NetDesc), C.POINTER(A.CLSpecC), C.c_int32, dp, dp, ip,
-                                                 C.c_int32, C.c_double, C.c_int32, C.c_double, C.c_double, dp, ip])
+    name = "ref_ctl_reach_loss_grad" if with_grad else "ref_ctl_reach_loss"
+    f = _mpc_fn(ref_lib(), name, [C.POINTER(A.NetDesc), C.POINTER(A.CLSpecC), C.c_int32, dp, dp, ip,
+                                  C.c_int32, C.c_double, C.c_int32, C.c_double, C.c_double, dp]
+                + ([dp] if with_grad else []) + [ip])
     x0s = np.ascontiguousarray(x0s, np.float64)
     M = x0s.shape[0]
     has = np.array([0 if y is None else 1 for y in yrefs], np.int32)
@@ -527,10 +530,11 @@ def ref_ctl_reach_loss(spec, x0s, yrefs, eps, t_h, delta, cap):
     dc = np.zeros(1, np.int32)
     desc, keep = spec.controller.desc()
     cs, keep2 = spec.c_struct()
+    g = np.zeros(spec.controller.params().size) if with_grad else None
     rc = f(C.byref(desc), C.byref(cs), M, A.dptr(x0s), A.dptr(yr), A.iptr(has), rd, float(eps), t_h, float(delta),
-           float(cap), A.dptr(loss), A.iptr(dc))
+           float(cap), A.dptr(loss), *([A.dptr(g)] if with_grad else []), A.iptr(dc))
     assert rc == 0, rc
-    return float(loss[0]), int(dc[0])
+    return (float(loss[0]), g, int(dc[0])) if with_grad else (float(loss[0]), int(dc[0]))
 
 
 # --- certified training (training.hpp) through the reference itself -------------------------------
