@@ -573,6 +573,15 @@ int reach_ctl_reach_loss(reach_ctx* ctx, const reach_net* ctl, const reach_cl_sp
                          const double* x0s, const double* y_refs, double eps, double cap, double* loss, double* grad,
                          int32_t* diverged_count);
 
+/* train_ct_ctl (training.hpp:389-442): certified training of a controller against the quadrotor plant
+ * (base: plant, params, n, l, k_atomic, fp_base, ref_dim), L = track_loss (rk4_substeps RK4 steps per
+ * control interval delta) + lambda ctl_reach_loss (cl_reach with fp.h = delta / k_atomic), the
+ * reference's curriculum / minibatch stream / Adam on the host, every loss and gradient on the device.
+ * dataset: states [E][T+1][12], actions [E][T][4] (logged controls), y_ref [E][T][ref_dim]. */
+int reach_train_ct_ctl(reach_ctx* ctx, const reach_net_desc* init, const reach_train_config* cfg,
+                       const reach_episode_set* dataset, const reach_cl_spec* base, double delta,
+                       int32_t rk4_substeps, double* params_out, reach_train_log_row* log);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1159,3 +1159,59 @@ extern "C" int ref_ctl_reach_loss_grad(const reach_net_desc* ctl_desc, const rea
   }
   return REACH_OK;
 }
+
+// reach::train_ct_ctl (training.hpp:389-442) with the quadrotor plant.
+extern "C" int ref_train_ct_ctl(const reach_net_desc* init, const reach_train_config* c, const reach_episode_set* ds,
+                                const reach_cl_spec* sp, double delta, int32_t rk4, double* params_out,
+                                reach_train_log_row* log, int32_t* log_rows) {
+  TrainConfig cfg;
+  cfg.horizon_max = c->horizon_max;
+  cfg.eps0 = c->eps0;
+  cfg.eps_final = c->eps_final;
+  cfg.lambda = c->lambda;
+  cfg.gamma = c->gamma;
+  cfg.iters = c->iters;
+  cfg.batch = c->batch;
+  cfg.lr = c->lr;
+  cfg.reach_cap = c->reach_cap;
+  cfg.curriculum = c->curriculum != 0;
+  cfg.seed = c->seed;
+  try {
+    MLPNet<double> net = net_from_desc(init);
+    QuadrotorParams prm;
+    prm.mass = sp->plant_params[0];
+    prm.gravity = sp->plant_params[1];
+    prm.jx = sp->plant_params[2];
+    prm.jy = sp->plant_params[3];
+    prm.jz = sp->plant_params[4];
+    auto plant = [prm](const auto& x, const auto& u, auto& dx) { quadrotor_ode(x, u, prm, dx); };
+    auto data = episodes_from(ds);
+    if (ds->ref_dim > 0 && ds->y_ref)
+      for (int e = 0; e < ds->episodes; ++e)
+        for (int t = 0; t < ds->length; ++t) {
+          const double* y = ds->y_ref + (static_cast<size_t>(e) * ds->length + t) * ds->ref_dim;
+          data[static_cast<size_t>(e)].y_ref.push_back(Vec<double>(y, y + ds->ref_dim));
+        }
+    FlowpipeParams fp;
+    fp.order = sp->fp.order;
+    fp.eps_init = sp->fp.eps_init;
+    fp.refine_rounds = sp->fp.refine_rounds;
+    fp.enlargement = sp->fp.enlargement;
+    fp.max_enlargements = sp->fp.max_enlargements;
+    fp.window = sp->fp.window;
+    TrainResult r = train_ct_ctl(net, cfg, data, plant, sp->n, sp->l, delta, sp->k_atomic, rk4, fp);
+    Vec<double> p = net_params(r.net);
+    std::copy(p.begin(), p.end(), params_out);
+    for (size_t i = 0; i < r.log.rows.size(); ++i) {
+      const auto& row = r.log.rows[i];
+      log[i] = reach_train_log_row{row.iter, row.t_h, row.eps, row.l_pred, row.l_reach, row.l_total,
+                                   row.diverged_count};
+    }
+    *log_rows = static_cast<int32_t>(r.log.rows.size());
+  } catch (const std::invalid_argument&) {
+    return REACH_E_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return REACH_E_NONFINITE;
+  }
+  return REACH_OK;
+}

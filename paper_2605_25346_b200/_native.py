@@ -72,6 +72,8 @@ def _declare(lib):
     lib.reach_reach_loss.argtypes = [vp, vp, C.POINTER(A.DTArgs), C.c_int32, C.c_double, C.c_double, dp, dp, ip]
     lib.reach_plan_refine.argtypes = [vp, vp, C.POINTER(A.PlanProblemC), dp, C.c_int32, C.c_double, dp, ip]
     lib.reach_pred_loss.argtypes = [vp, vp, C.POINTER(A.EpisodeSetC), C.c_int32, dp, dp, dp]
+    lib.reach_train_ct_ctl.argtypes = [vp, C.POINTER(A.NetDesc), C.POINTER(A.TrainConfigC), C.POINTER(A.EpisodeSetC),
+                                       C.POINTER(A.CLSpecC), C.c_double, C.c_int32, dp, C.POINTER(A.TrainLogRowC)]
     lib.reach_ctl_reach_loss.argtypes = [vp, vp, C.POINTER(A.CLSpecC), C.c_int32, dp, dp, C.c_double, C.c_double,
                                          dp, dp, ip]
     lib.reach_track_loss.argtypes = [vp, vp, C.c_int32, dp, C.POINTER(A.EpisodeSetC), C.c_int32, dp, C.c_double,
@@ -88,7 +90,7 @@ def _declare(lib):
     lib.reach_cem_result.argtypes = [vp, dp, dp, ip, dp]
     for f in ("reach_plan_eval_batch", "reach_plan_cem", "reach_plan_cem_ex", "reach_plan_objective_grad",
               "reach_grad_tube_volume", "reach_mpc_run", "reach_refine_tube_volume", "reach_reach_loss", "reach_grad_tube_volume_range", "reach_plan_refine",
-              "reach_pred_loss", "reach_train_dt_dyn", "reach_track_loss", "reach_ctl_reach_loss",
+              "reach_pred_loss", "reach_train_dt_dyn", "reach_track_loss", "reach_ctl_reach_loss", "reach_train_ct_ctl",
               "reach_cem_create", "reach_cem_destroy",
               "reach_cem_sample", "reach_cem_update", "reach_cem_result"):
         getattr(lib, f).restype = C.c_int

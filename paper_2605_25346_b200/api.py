@@ -819,6 +819,31 @@ class ClosedLoopSpec:
         return s, (yr, prm)
 
 
+def train_ct_ctl(init: MLPNet, cfg: "TrainConfig", dataset: Sequence[Episode], delta: float, k_atomic: int = 1,
+                 rk4_substeps: int = 4, fp_base: Optional[FlowpipeParams] = None,
+                 plant: Optional[QuadrotorParams] = None, ctx: Optional[Context] = None):
+    """train_ct_ctl (training.hpp:389-442) with the quadrotor plant -> (trained controller, [TrainLogRow]):
+    L = track_loss + lambda ctl_reach_loss; the host loop of the C ABI (curriculum, the reference's
+    minibatch stream, Adam) with every loss and gradient on the device."""
+    ctx = ctx or default_context()
+    es, keep = _episode_set(dataset)
+    r = len(dataset[0].y_ref[0]) if len(dataset[0].y_ref) else 0
+    base = ClosedLoopSpec(init, n=12, l=4, ctl_steps=1, k_atomic=k_atomic,
+                          y_ref=np.zeros((1, r)) if r else None, fp=dataclasses.replace(fp_base or FlowpipeParams()),
+                          plant_params=plant or QuadrotorParams())
+    cs, keep2 = base.c_struct()
+    d, keep3 = init.desc()
+    out = np.zeros(init.params().size)
+    log = (A.TrainLogRowC * max(cfg.iters, 1))()
+    cc = cfg.c()
+    rc = ctx._lib.reach_train_ct_ctl(ctx.handle, C.byref(d), C.byref(cc), C.byref(es), C.byref(cs), float(delta),
+                                     int(rk4_substeps), A.dptr(out), log)
+    rows = [TrainLogRow(q.iter, q.t_h, q.eps, q.l_pred, q.l_reach, q.l_total, q.diverged_count)
+            for q in list(log)[:cfg.iters]]
+    ctx.check(rc, "train_ct_ctl")
+    return net_with_params(init, out), rows
+
+
 def cl_reach_batch_arrays(spec: ClosedLoopSpec, x0_lo: np.ndarray, x0_hi: np.ndarray,
                           ctx: Optional[Context] = None) -> TubeBatch:
     """cl_reach (closed_loop.hpp:76-182) for a batch of initial boxes x0 [B][n]; boxes have n + l dims."""

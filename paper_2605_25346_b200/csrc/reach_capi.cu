@@ -2610,6 +2610,108 @@ int reach_train_dt_dyn(reach_ctx* ctx, const reach_net_desc* init, const reach_t
   return REACH_OK;
 }
 
+// train_ct_ctl (training.hpp:389-442) with the quadrotor plant: L = track_loss + lambda ctl_reach_loss, the
+// same curriculum / minibatch stream / Adam as train_dt_dyn; every loss and gradient on the device.
+int reach_train_ct_ctl(reach_ctx* ctx, const reach_net_desc* init, const reach_train_config* cfg,
+                       const reach_episode_set* ds, const reach_cl_spec* base, double delta, int32_t rk4_substeps,
+                       double* params_out, reach_train_log_row* log) {
+  rbh::DeviceGuard device_guard_(ctx);
+  if (!ctx || !init || !cfg || !ds || !base || !params_out) return REACH_E_INVALID_ARGUMENT;
+  const reach_train_config& c = *cfg;
+  if (c.horizon_max < 1 || c.eps0 < c.eps_final || c.eps_final < 0.0 || c.lambda < 0.0 || c.gamma < 0.0 ||
+      c.iters < 1 || c.batch < 1 || c.lr <= 0.0 || c.reach_cap <= 0.0)
+    return fail(ctx, REACH_E_INVALID_ARGUMENT, "TrainConfig: invalid configuration");
+  if (ds->episodes < 1) return fail(ctx, REACH_E_INVALID_ARGUMENT, "train_ct_ctl: empty dataset");
+  if (ds->length < c.horizon_max) return fail(ctx, REACH_E_INVALID_ARGUMENT, "train_ct_ctl: episode shorter than T_h^max");
+  const int n = ds->n, l = ds->m, L = init->n_layers, E = ds->episodes, Ls = ds->length;
+  const int r = ds->y_ref ? ds->ref_dim : 0;
+  size_t np = 0;
+  for (int q = 0; q < L; ++q) np += static_cast<size_t>(init->dims[q + 1]) * (init->dims[q] + 1);
+  std::vector<double> params(init->params, init->params + np);
+  std::vector<int32_t> dims(init->dims, init->dims + L + 1), acts(init->acts, init->acts + L);
+  const double beta1 = 0.9, beta2 = 0.999, aeps = 1e-8;
+  std::vector<double> am(np, 0.0), av(np, 0.0);
+  int at = 0;
+  std::mt19937_64 gen(c.seed);
+  constexpr double kE = 2.718281828459045235360287471352662498;
+  const int Tm = c.horizon_max;
+  std::vector<double> bs(static_cast<size_t>(c.batch) * (Tm + 1) * n), ba(static_cast<size_t>(c.batch) * Tm * l),
+      br(static_cast<size_t>(c.batch) * Tm * std::max(r, 1)), x0s(static_cast<size_t>(c.batch) * n);
+  std::vector<double> gt(np), gr(np), g(np);
+  for (int s = 0; s < c.iters; ++s) {
+    int t_h = c.horizon_max;
+    double eps = c.eps_final;
+    if (c.curriculum && c.iters > 1) {
+      const double u = std::log(1.0 + static_cast<double>(s) * (kE - 1.0) / (c.iters - 1));
+      t_h = std::min(std::max(1, static_cast<int>(std::llround(c.horizon_max * u))), c.horizon_max);
+      eps = c.eps_final + (c.eps0 - c.eps_final) * (1.0 - static_cast<double>(s) / (c.iters - 1));
+    }
+    for (int b = 0; b < c.batch; ++b) {
+      const int e = static_cast<int>(gen() % static_cast<uint64_t>(E));
+      std::memcpy(bs.data() + static_cast<size_t>(b) * (Tm + 1) * n, ds->states + static_cast<size_t>(e) * (Ls + 1) * n,
+                  sizeof(double) * (Tm + 1) * n);
+      std::memcpy(ba.data() + static_cast<size_t>(b) * Tm * l, ds->actions + static_cast<size_t>(e) * Ls * l,
+                  sizeof(double) * Tm * l);
+      if (r > 0)
+        std::memcpy(br.data() + static_cast<size_t>(b) * Tm * r, ds->y_ref + static_cast<size_t>(e) * Ls * r,
+                    sizeof(double) * Tm * r);
+      std::memcpy(x0s.data() + static_cast<size_t>(b) * n, ds->states + static_cast<size_t>(e) * (Ls + 1) * n,
+                  sizeof(double) * n);
+    }
+    std::vector<double> wts(static_cast<size_t>(t_h));
+    for (int t = 0; t < t_h; ++t) wts[static_cast<size_t>(t)] = 1.0 + static_cast<double>(t + 1) / t_h;
+    reach_net_desc d{L, dims.data(), acts.data(), params.data()};
+    reach_net* cur = nullptr;
+    int rc = reach_net_upload(ctx, &d, &cur);
+    if (rc) return rc;
+    std::unique_ptr<reach_net, std::function<void(reach_net*)>> guard(cur, [ctx](reach_net* p) { reach_net_free(ctx, p); });
+    reach_episode_set bset{c.batch, Tm, n, l, bs.data(), ba.data(), r, r > 0 ? br.data() : nullptr};
+    double ltr = 0.0, lr_ = 0.0;
+    int div = 0;
+    rc = reach_track_loss(ctx, cur, base->plant, base->plant_params, &bset, t_h, wts.data(), c.gamma, delta,
+                          rk4_substeps, 1e6, &ltr, gt.data(), nullptr);
+    if (rc) return rc;
+    if (c.lambda > 0.0) {
+      reach_cl_spec sp = *base;
+      sp.n = n;
+      sp.l = l;
+      sp.ctl_steps = t_h;
+      sp.ref_dim = r;
+      sp.y_ref = nullptr;
+      sp.fp.h = delta / base->k_atomic;
+      std::vector<double> yr(static_cast<size_t>(c.batch) * t_h * std::max(r, 1));
+      for (int b = 0; b < c.batch && r > 0; ++b)
+        std::memcpy(yr.data() + static_cast<size_t>(b) * t_h * r, br.data() + static_cast<size_t>(b) * Tm * r,
+                    sizeof(double) * t_h * r);
+      rc = reach_ctl_reach_loss(ctx, cur, &sp, c.batch, x0s.data(), r > 0 ? yr.data() : nullptr, eps, c.reach_cap,
+                                &lr_, gr.data(), &div);
+      if (rc) return rc;
+    }
+    const double lt = ltr + c.lambda * lr_;
+    if (log) log[s] = reach_train_log_row{s, t_h, eps, ltr, lr_, lt, div};
+    if (!std::isfinite(lt)) {
+      char msg[256];
+      std::snprintf(msg, sizeof msg, "train_ct_ctl: non-finite loss at iter %d", s);
+      return fail(ctx, REACH_E_NONFINITE, msg);
+    }
+    for (size_t j = 0; j < np; ++j) {
+      double dv = gt[j];
+      if (c.lambda > 0.0) dv = dv + (0.0 * lr_ + c.lambda * gr[j]);
+      if (!std::isfinite(dv)) return fail(ctx, REACH_E_NONFINITE, "grad_forward: non-finite derivative");
+      g[j] = dv;
+    }
+    ++at;
+    const double bc1 = 1.0 - std::pow(beta1, at), bc2 = 1.0 - std::pow(beta2, at);
+    for (size_t j = 0; j < np; ++j) {
+      am[j] = beta1 * am[j] + (1.0 - beta1) * g[j];
+      av[j] = beta2 * av[j] + (1.0 - beta2) * g[j] * g[j];
+      params[j] -= c.lr * (am[j] / bc1) / (std::sqrt(av[j] / bc2) + aeps);
+    }
+  }
+  std::memcpy(params_out, params.data(), sizeof(double) * np);
+  return REACH_OK;
+}
+
 // The refinement step of plan_cem alone (mpc.hpp:337-361), for drivers that run the CEM loop in pieces.
 int reach_plan_refine(reach_ctx* ctx, const reach_net* net, const reach_plan_problem* prob, const double* x0,
                       int32_t refine_iters, double best_objective, double* best_actions, int32_t* refined) {

@@ -591,3 +591,27 @@ def ref_track_loss(controller, batch, t_t, weights, gamma, delta, rk4=4, cap=1e6
            A.dptr(loss), A.dptr(g) if with_grad else None, A.iptr(bc))
     assert rc == 0, rc
     return (float(loss[0]), g, int(bc[0])) if with_grad else (float(loss[0]), int(bc[0]))
+
+
+def ref_train_ct_ctl(init, cfg, dataset, delta, k_atomic=1, rk4=4, fp_base=None):
+    """(trained net_params, [TrainLogRow], rc) of the reference's train_ct_ctl with the quadrotor plant."""
+    import dataclasses as _dc
+    from paper_2605_25346_b200.api import ClosedLoopSpec, FlowpipeParams, TrainLogRow, _episode_set
+    es, keep = _episode_set(dataset)
+    r = len(dataset[0].y_ref[0]) if len(dataset[0].y_ref) else 0
+    base = ClosedLoopSpec(init, ctl_steps=1, k_atomic=k_atomic, y_ref=np.zeros((1, r)) if r else None,
+                          fp=_dc.replace(fp_base or FlowpipeParams()))
+    cs, keep2 = base.c_struct()
+    d, keep3 = init.desc()
+    out = np.zeros(init.params().size)
+    log = (A.TrainLogRowC * max(cfg.iters, 1))()
+    nrows = np.zeros(1, np.int32)
+    f = ref_lib().ref_train_ct_ctl
+    f.argtypes = [C.POINTER(A.NetDesc), C.POINTER(A.TrainConfigC), C.POINTER(A.EpisodeSetC), C.POINTER(A.CLSpecC),
+                  C.c_double, C.c_int32, C.POINTER(C.c_double), C.POINTER(A.TrainLogRowC), C.POINTER(C.c_int32)]
+    f.restype = C.c_int
+    cc = cfg.c()
+    rc = f(C.byref(d), C.byref(cc), C.byref(es), C.byref(cs), float(delta), int(rk4), A.dptr(out), log, A.iptr(nrows))
+    rows = [TrainLogRow(q.iter, q.t_h, q.eps, q.l_pred, q.l_reach, q.l_total, q.diverged_count)
+            for q in list(log)[:int(nrows[0])]]
+    return out, rows, rc

@@ -84,3 +84,28 @@ def test_track_loss_blowup_charges_cap():
     got, bc = track_loss(ctl, data, 3, w, 0.1, 0.05, 2, cap=1e6)
     exp, bce = ref_track_loss(ctl, data, 3, w, 0.1, 0.05, 2, cap=1e6)
     assert bc == bce == len(data) and got == exp
+
+
+@pytest.mark.parametrize("lam", [0.0, 0.5])
+def test_train_ct_ctl_matches_reference(lam):
+    """train_ct_ctl (training.hpp:389-442): track_loss + lambda ctl_reach_loss, both gradients on the device.
+    The CT values agree to ~1e-15 and the gradients to ~1e-16..1e-9 (CUDA transcendentals), so the log within
+    1e-9 relative and the trained parameters' update within 1e-6 of the reference's."""
+    from oracle_bind import ref_train_ct_ctl
+    from paper_2605_25346_b200.api import train_ct_ctl
+    from train_cases import ct_tracking_case
+    ctl, data = ct_tracking_case(seed=4, episodes=4, length=3)
+    from paper_2605_25346_b200.api import TrainConfig
+    cfg = TrainConfig(horizon_max=2, eps0=0.01, eps_final=0.005, lambda_=lam, gamma=0.1, iters=3, batch=2, lr=1e-3,
+                      reach_cap=40.0, curriculum=True, seed=7)
+    net, rows = train_ct_ctl(ctl, cfg, data, delta=0.02, k_atomic=2, rk4_substeps=2)
+    pe, rows_e, rc = ref_train_ct_ctl(ctl, cfg, data, delta=0.02, k_atomic=2, rk4=2)
+    assert rc == 0 and len(rows) == len(rows_e)
+    for a, b in zip(rows, rows_e):
+        assert (a.iter, a.t_h, a.eps, a.diverged_count) == (b.iter, b.t_h, b.eps, b.diverged_count)
+        for x, y in ((a.l_pred, b.l_pred), (a.l_reach, b.l_reach), (a.l_total, b.l_total)):
+            assert abs(x - y) <= 1e-9 * max(abs(y), 1e-300)
+    du, de = net.params() - ctl.params(), pe - ctl.params()
+    assert float(np.max(np.abs(du - de))) <= 1e-6 * float(np.max(np.abs(de)))
+    if lam > 0:
+        assert rows[-1].l_reach > 0
