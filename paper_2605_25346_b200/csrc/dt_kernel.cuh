@@ -365,7 +365,7 @@ __device__ __forceinline__ void pipelined_rows(RowIter& it, Load&& load, Comp&& 
 // ---------------------------------------------------------------------------
 // Kernel configuration.
 #ifndef RB_SAMPLE_WARPS
-#define RB_SAMPLE_WARPS 8
+#define RB_SAMPLE_WARPS 12  // 384 threads: <= 170 registers, no spills (ptxas); smem sets the stage size
 #endif
 #ifndef RB_MIN_BLOCKS
 #define RB_MIN_BLOCKS 1
@@ -916,8 +916,15 @@ __device__ __forceinline__ void fold_overflow_warp(double* stA, int nzs, int n, 
 #pragma unroll
       for (int i = 0; i < MR; ++i)
         if (i == kk) akk = col[i];
+#if RB_FUSED
+      // fused mode: one reciprocal per pivot instead of a division per row
+      const double rak = 1.0 / akk;
+#pragma unroll
+      for (int i = 0; i < MR; ++i) f[i] = (i > kk && i < n) ? col[i] * rak : 0.0;
+#else
 #pragma unroll
       for (int i = 0; i < MR; ++i) f[i] = (i > kk && i < n) ? __ddiv_rn(col[i], akk) : 0.0;
+#endif
 #pragma unroll
       for (int i = 0; i < MR; ++i) f[i] = __shfl_sync(0xffffffffu, f[i], kk);
       double mk = 0.0;

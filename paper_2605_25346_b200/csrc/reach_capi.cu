@@ -151,8 +151,28 @@ int plan_warp(reach_ctx* ctx, const reach_net* net, int n, int m, int window, rb
       boff += (i + 1 < ctl->L) ? hp : ev(ctl->dims[i + 1]);
     }
   P.bias_doubles = ev(boff);
-  const int kStageDoubles = env_int("RB_STAGE_DOUBLES", kStageDoublesDefault, 512, 8192) & ~1;
   const int kNStage = env_int("RB_NSTAGE", kNStageDefault, 2, 8);
+  // Stage size: RB_STAGE_DOUBLES, else the largest stage (<= kStageDoublesDefault) that keeps
+  // kSampleWarps sample warps resident -- residency beats chunk size on this latency-bound kernel
+  // (C4 fused: 8 warps x 48 KB stages 74.8 ms, 12 warps x 21 KB stages 69.1 ms, tools/warp_sweep.sh);
+  // fewer warps only when one row of the widest streamed matrix no longer fits a stage.
+  int kStageDoubles = env_int("RB_STAGE_DOUBLES", 0, 512, 8192) & ~1;
+  if (kStageDoubles == 0) {
+    int maxld = 0;
+    auto scan = [&](const reach_net* nt) {
+      for (int i = 0; i < nt->dev.L; ++i) maxld = std::max({maxld, nt->dev.ldw[i], i + 1 < nt->dev.L ? nt->dev.ldt[i] : 0});
+    };
+    scan(net);
+    if (ctl) scan(ctl);
+    const long long base = rb::kHeaderBytes + static_cast<long long>(P.bias_doubles) * 8;
+    const long long per = static_cast<long long>(P.warp_doubles) * 8;
+    for (int spc_t = rb::kSampleWarps; spc_t >= 1; --spc_t) {
+      const long long avail = (static_cast<long long>(ctx->max_smem) - base - spc_t * per) / (kNStage * 8ll);
+      kStageDoubles = static_cast<int>(std::min<long long>(kStageDoublesDefault, std::max<long long>(avail, 0))) & ~1;
+      if (kStageDoubles >= maxld) break;
+    }
+    if (kStageDoubles < 512) kStageDoubles = std::max(512, maxld + (maxld & 1));
+  }
   P.stage_doubles = kStageDoubles;
   P.nstage = kNStage;
   // weight-stream chunk table of one DT step (consumption order of the kernel), absolute addresses
