@@ -298,6 +298,190 @@ inline reach::Gradient reach_loss_gradient(Context& ctx, const reach::MLPNet<dou
   return g;
 }
 
+// ---- certified training (training.hpp) on the device ------------------------------------------------
+namespace detail {
+// Episodes of one length as a reach_episode_set (storage kept in `buf`).
+struct EpisodeArrays {
+  std::vector<double> states, actions, y_ref;
+  reach_episode_set set{};
+};
+inline EpisodeArrays episode_arrays(const std::vector<reach::Episode>& batch) {
+  EpisodeArrays a;
+  if (batch.empty()) throw std::invalid_argument("empty episode batch");
+  const int T = batch.front().length();
+  const int n = static_cast<int>(batch.front().states.front().size());
+  const int m = T > 0 ? static_cast<int>(batch.front().actions.front().size()) : 0;
+  const int r = batch.front().y_ref.empty() ? 0 : static_cast<int>(batch.front().y_ref.front().size());
+  for (const auto& ep : batch) {
+    ep.validate();
+    if (ep.length() != T) throw std::invalid_argument("episodes of one batch must share a length");
+    for (const auto& x : ep.states) a.states.insert(a.states.end(), x.begin(), x.end());
+    for (const auto& u : ep.actions) a.actions.insert(a.actions.end(), u.begin(), u.end());
+    if (r > 0) {
+      if (static_cast<int>(ep.y_ref.size()) != T) throw std::invalid_argument("Episode: reference length mismatch");
+      for (const auto& y : ep.y_ref) a.y_ref.insert(a.y_ref.end(), y.begin(), y.end());
+    }
+  }
+  a.set = reach_episode_set{static_cast<int32_t>(batch.size()), T, n, m, a.states.data(),
+                            a.actions.empty() ? nullptr : a.actions.data(), r, r > 0 ? a.y_ref.data() : nullptr};
+  return a;
+}
+inline reach_net_desc net_desc(const MLPNet& net, std::vector<int32_t>& dims, std::vector<int32_t>& acts,
+                               std::vector<double>& params) {
+  net.validate();
+  dims.assign(1, net.input_dim());
+  for (const auto& L : net.layers) {
+    dims.push_back(L.rows);
+    acts.push_back(static_cast<int32_t>(L.act));
+    params.insert(params.end(), L.w.begin(), L.w.end());
+    params.insert(params.end(), L.b.begin(), L.b.end());
+  }
+  return reach_net_desc{static_cast<int32_t>(net.layers.size()), dims.data(), acts.data(), params.data()};
+}
+inline reach_train_config train_config(const reach::TrainConfig& c) {
+  return reach_train_config{c.horizon_max, c.eps0, c.eps_final, c.lambda, c.gamma, c.iters, c.batch, c.lr,
+                            c.reach_cap, c.curriculum ? 1 : 0, c.seed, c.dt_prm.window,
+                            c.dt_prm.rebuild_from_box ? 1 : 0};
+}
+inline reach::TrainLog train_log(const std::vector<reach_train_log_row>& rows) {
+  reach::TrainLog log;
+  for (const auto& r : rows) log.rows.push_back({r.iter, r.t_h, r.eps, r.l_pred, r.l_reach, r.l_total, r.diverged_count});
+  return log;
+}
+inline reach_cl_spec quad_spec(const reach::QuadrotorParams& plant, int n, int l, int k_atomic, int ref_dim,
+                               const reach::FlowpipeParams& fp) {
+  reach_cl_spec sp{};
+  sp.plant = REACH_PLANT_QUADROTOR;
+  sp.plant_params[0] = plant.mass;
+  sp.plant_params[1] = plant.gravity;
+  sp.plant_params[2] = plant.jx;
+  sp.plant_params[3] = plant.jy;
+  sp.plant_params[4] = plant.jz;
+  sp.n = n;
+  sp.l = l;
+  sp.ctl_steps = 1;
+  sp.k_atomic = k_atomic;
+  sp.ref_dim = ref_dim;
+  sp.fp = reach_flowpipe_params{fp.h, fp.steps, fp.order, fp.eps_init, fp.refine_rounds, fp.enlargement,
+                                fp.max_enlargements, fp.window};
+  return sp;
+}
+}  // namespace detail
+
+// reach::pred_loss (training.hpp:60-83) and its grad_forward over net_params.
+inline double pred_loss(Context& ctx, const reach::MLPNet<double>& model, const std::vector<reach::Episode>& batch,
+                        int t_h, const reach::Vec<double>& weights, reach::Gradient* grad = nullptr) {
+  if (batch.empty() || t_h < 1 || static_cast<int>(weights.size()) != t_h)
+    throw std::invalid_argument("pred_loss: bad batch/horizon/weights");
+  auto a = detail::episode_arrays(batch);
+  double loss = 0.0;
+  if (grad) {
+    grad->g.assign(static_cast<size_t>(model.param_count()), 0.0);
+    grad->method = reach::GradMethod::forward_dual;
+  }
+  ctx.check(reach_pred_loss(ctx.raw(), ctx.upload(from_reference(model)), &a.set, t_h, weights.data(), &loss,
+                            grad ? grad->g.data() : nullptr),
+            "pred_loss");
+  return loss;
+}
+
+// reach::track_loss (training.hpp:134-178) with the quadrotor plant, and its grad_forward.
+inline double track_loss(Context& ctx, const reach::MLPNet<double>& controller, const reach::QuadrotorParams& plant,
+                         const std::vector<reach::Episode>& batch, int t_t, const reach::Vec<double>& weights,
+                         double gamma, double delta, int rk4_substeps = 4, double cap = 1e6,
+                         int* blowup_count = nullptr, reach::Gradient* grad = nullptr) {
+  auto a = detail::episode_arrays(batch);
+  const double prm[5] = {plant.mass, plant.gravity, plant.jx, plant.jy, plant.jz};
+  double loss = 0.0;
+  int32_t bc = 0;
+  if (grad) {
+    grad->g.assign(static_cast<size_t>(controller.param_count()), 0.0);
+    grad->method = reach::GradMethod::forward_dual;
+  }
+  ctx.check(reach_track_loss(ctx.raw(), ctx.upload(from_reference(controller)), REACH_PLANT_QUADROTOR, prm, &a.set,
+                             t_t, weights.data(), gamma, delta, rk4_substeps, cap, &loss,
+                             grad ? grad->g.data() : nullptr, &bc),
+            "track_loss");
+  if (blowup_count) *blowup_count += bc;
+  return loss;
+}
+
+// grad_forward of reach::ctl_reach_loss over the controller's net_params (Dual cl_reach per parameter
+// and episode on the device).  Every episode must carry its t_h references when the controller takes
+// them (the reference's carry-over of an empty y_ref is resolved here).
+inline reach::Gradient ctl_reach_loss_gradient(Context& ctx, const reach::MLPNet<double>& controller,
+                                               const reach::QuadrotorParams& plant,
+                                               const std::vector<reach::Episode>& batch, double eps, int t_h, int n,
+                                               int l, double delta, int k_atomic, double cap,
+                                               const reach::FlowpipeParams& fp_base = {},
+                                               double* loss = nullptr, int* diverged_count = nullptr) {
+  if (batch.empty() || t_h < 1) throw std::invalid_argument("ctl_reach_loss: bad batch/horizon");
+  std::vector<double> x0s, yr;
+  std::vector<reach::Vec<double>> cur;
+  int r = 0;
+  for (const auto& ep : batch) {
+    x0s.insert(x0s.end(), ep.states.front().begin(), ep.states.front().end());
+    if (!ep.y_ref.empty()) cur.assign(ep.y_ref.begin(), ep.y_ref.begin() + t_h);
+    if (!cur.empty()) r = static_cast<int>(cur.front().size());
+    for (const auto& y : cur) yr.insert(yr.end(), y.begin(), y.end());
+  }
+  if (r > 0 && yr.size() != batch.size() * static_cast<size_t>(t_h) * r)
+    throw std::invalid_argument("freeze_trailing_inputs: dimension mismatch");
+  reach::FlowpipeParams fp = fp_base;
+  fp.h = delta / k_atomic;
+  reach_cl_spec sp = detail::quad_spec(plant, n, l, k_atomic, r, fp);
+  sp.ctl_steps = t_h;
+  reach::Gradient g;
+  g.g.assign(static_cast<size_t>(controller.param_count()), 0.0);
+  double lv = 0.0;
+  int32_t dc = 0;
+  ctx.check(reach_ctl_reach_loss(ctx.raw(), ctx.upload(from_reference(controller)), &sp,
+                                 static_cast<int32_t>(batch.size()), x0s.data(), r > 0 ? yr.data() : nullptr, eps, cap,
+                                 &lv, g.g.data(), &dc),
+            "ctl_reach_loss");
+  if (loss) *loss = lv;
+  if (diverged_count) *diverged_count = dc;
+  return g;
+}
+
+// reach::train_dt_dyn (training.hpp:333-382): the reference's loop, every loss and gradient on the device.
+inline reach::TrainResult train_dt_dyn(Context& ctx, const reach::MLPNet<double>& init, const reach::TrainConfig& cfg,
+                                       const std::vector<reach::Episode>& dataset) {
+  auto a = detail::episode_arrays(dataset);
+  std::vector<int32_t> dims, acts;
+  std::vector<double> params;
+  const MLPNet net = from_reference(init);
+  reach_net_desc d = detail::net_desc(net, dims, acts, params);
+  reach_train_config c = detail::train_config(cfg);
+  std::vector<double> out(params.size());
+  std::vector<reach_train_log_row> rows(static_cast<size_t>(std::max(cfg.iters, 1)));
+  const int rc = reach_train_dt_dyn(ctx.raw(), &d, &c, &a.set, out.data(), rows.data());
+  if (rc == REACH_E_NONFINITE) throw std::runtime_error(reach_ctx_last_error(ctx.raw()));
+  ctx.check(rc, "train_dt_dyn");
+  return reach::TrainResult{reach::net_with_params<double>(init, out), detail::train_log(rows)};
+}
+
+// reach::train_ct_ctl (training.hpp:389-442) with the quadrotor plant.
+inline reach::TrainResult train_ct_ctl(Context& ctx, const reach::MLPNet<double>& init, const reach::TrainConfig& cfg,
+                                       const std::vector<reach::Episode>& dataset,
+                                       const reach::QuadrotorParams& plant, int n, int l, double delta,
+                                       int k_atomic = 1, int rk4_substeps = 4,
+                                       const reach::FlowpipeParams& fp_base = {}) {
+  auto a = detail::episode_arrays(dataset);
+  std::vector<int32_t> dims, acts;
+  std::vector<double> params;
+  const MLPNet net = from_reference(init);
+  reach_net_desc d = detail::net_desc(net, dims, acts, params);
+  reach_train_config c = detail::train_config(cfg);
+  reach_cl_spec sp = detail::quad_spec(plant, n, l, k_atomic, a.set.ref_dim, fp_base);
+  std::vector<double> out(params.size());
+  std::vector<reach_train_log_row> rows(static_cast<size_t>(std::max(cfg.iters, 1)));
+  const int rc = reach_train_ct_ctl(ctx.raw(), &d, &c, &a.set, &sp, delta, rk4_substeps, out.data(), rows.data());
+  if (rc == REACH_E_NONFINITE) throw std::runtime_error(reach_ctx_last_error(ctx.raw()));
+  ctx.check(rc, "train_ct_ctl");
+  return reach::TrainResult{reach::net_with_params<double>(init, out), detail::train_log(rows)};
+}
+
 // reach::dt_interval_baseline (dt_reach.hpp:129-149)
 inline reach::ReachTube<double> dt_interval_baseline(Context& ctx, const reach::DTSystem<double>& sys,
                                                      const reach::IntervalBox<double>& x0,

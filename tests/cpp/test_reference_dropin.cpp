@@ -365,6 +365,77 @@ int main() {
       ++failures;
     }
   }
+  // certified training on the device: pred_loss gradient and the whole train_dt_dyn bit-identical;
+  // the ctl_reach_loss gradient (Dual through the CT engine) within 1e-9
+  {
+    Rng r8(21);
+    MLPNet<double> model = random_mlp(r8, 4, {16, 16}, 2, Act::Relu, 0.6);
+    auto step = [&](const Vec<double>& x, const Vec<double>& u) {
+      Vec<double> in = x;
+      in.insert(in.end(), u.begin(), u.end());
+      Vec<double> y = model.forward(in);
+      for (size_t i = 0; i < y.size(); ++i) y[i] = 0.5 * y[i] + 0.9 * x[i];
+      return y;
+    };
+    auto data = make_dt_dataset(step, 2, 2, 5, 5, 0.4, 0.5, r8);
+    const auto w = horizon_weights(3);
+    auto f = [&](const auto& p) {
+      using S = typename std::decay_t<decltype(p)>::value_type;
+      return pred_loss(net_with_params<S>(model, p), data, 3, w);
+    };
+    auto gref = grad_forward(f, net_params(model));
+    reach::Gradient ggot;
+    const double lp = reach_b200::pred_loss(gpu, model, data, 3, w, &ggot);
+    if (lp != pred_loss(model, data, 3, w) || gref.g != ggot.g) {
+      std::printf("pred_loss: mismatch\n");
+      ++failures;
+    }
+    TrainConfig cfg;
+    cfg.horizon_max = 3;
+    cfg.iters = 3;
+    cfg.batch = 2;
+    cfg.lambda = 0.5;
+    cfg.eps0 = 0.02;
+    cfg.eps_final = 0.005;
+    cfg.seed = 4;
+    auto tr = train_dt_dyn(model, cfg, data);
+    auto tg = reach_b200::train_dt_dyn(gpu, model, cfg, data);
+    if (tr.log.to_csv() != tg.log.to_csv() || net_params(tr.net) != net_params(tg.net)) {
+      std::printf("train_dt_dyn: mismatch\n%s---\n%s", tr.log.to_csv().c_str(), tg.log.to_csv().c_str());
+      ++failures;
+    }
+  }
+  {
+    Rng r9(3);
+    QuadrotorParams qp;
+    MLPNet<double> ctl = random_mlp(r9, 15, {8, 8}, 4, Act::Tanh, 0.4);
+    for (auto& w : ctl.layers.back().w.a) w *= 0.1;
+    ctl.layers.back().b[0] += qp.mass * qp.gravity;
+    std::vector<Episode> batch(2);
+    for (auto& ep : batch) {
+      Vec<double> x0(12, 0.0);
+      for (int d = 0; d < 6; ++d) x0[d] = r9.uniform(-0.05, 0.05);
+      ep.states.assign(3, x0);
+      ep.actions.assign(2, Vec<double>(4, 0.0));
+      ep.y_ref.assign(2, Vec<double>{0.1, 0.0, 0.0});
+    }
+    auto plant = [qp](const auto& x, const auto& u, auto& dx) { quadrotor_ode(x, u, qp, dx); };
+    auto f = [&](const auto& p) {
+      using S = typename std::decay_t<decltype(p)>::value_type;
+      return ctl_reach_loss(net_with_params<S>(ctl, p), plant, batch, 0.01, 2, 12, 4, 0.02, 2, 40.0);
+    };
+    auto gref = grad_forward(f, net_params(ctl));
+    auto ggot = reach_b200::ctl_reach_loss_gradient(gpu, ctl, qp, batch, 0.01, 2, 12, 4, 0.02, 2, 40.0);
+    double worst = 0.0, scale = 0.0;
+    for (size_t j = 0; j < gref.g.size(); ++j) {
+      worst = std::max(worst, std::fabs(gref.g[j] - ggot.g[j]));
+      scale = std::max(scale, std::fabs(gref.g[j]));
+    }
+    if (gref.g.size() != ggot.g.size() || worst > 1e-9 * scale) {
+      std::printf("ctl_reach_loss gradient: max err %.3g (scale %.3g)\n", worst, scale);
+      ++failures;
+    }
+  }
   std::printf(failures ? "FAIL (%d)\n" : "OK: reference drop-in parity\n", failures);
   return failures ? 1 : 0;
 }
