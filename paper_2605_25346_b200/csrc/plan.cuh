@@ -173,6 +173,111 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_objective_kernel(const P
   P.diverged[b] = P.status[b] != ST_OK ? 1 : 0;
 }
 
+// The same objective with every W_l^T resident in shared memory for the whole launch (staged once per
+// CTA, not per step and layer), up to 32 candidate warps per CTA persistent over the batch, and each
+// lane's up-to-4 output units of a layer accumulated side by side (independent chains, each in the
+// reference's j order) -- used whenever the network fits (C3: 157 KB).  Bit-identical to the above.
+constexpr int kPlanMaxWarps = 32;
+__global__ void __launch_bounds__(kPlanMaxWarps * 32) plan_objective_resident_kernel(const PlanParams P, int vec,
+                                                                                     int wtot) {
+  extern __shared__ __align__(16) double psm[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+  const DevNet& N = P.net;
+  const int n = P.n, m = P.m, H = P.H, L = N.L;
+  int woff[kMaxLayers];
+  {
+    int off = 0;
+    for (int l = 0; l < L; ++l) {
+      const int rows = N.dims[l + 1], cols = N.dims[l];
+      const double* wt = N.blob + N.wt_off[l];
+      const int ld = N.ldt[l];
+      for (int q = threadIdx.x; q < cols * rows; q += blockDim.x) {
+        const int j = q / rows, oo = q % rows;
+        psm[off + q] = __ldg(wt + static_cast<size_t>(j) * ld + oo);
+      }
+      woff[l] = off;
+      off += cols * rows;
+    }
+  }
+  __syncthreads();
+  double* vin = psm + wtot + static_cast<size_t>(warp) * 2 * vec;
+  double* vout = vin + vec;
+  for (int b = blockIdx.x * nwarps + warp; b < P.B; b += gridDim.x * nwarps) {
+    const double* acts = P.actions + static_cast<size_t>(b) * H * m;
+    double x_reg = (lane < n) ? P.x0[lane] : 0.0;
+    double obj = 0.0;
+    for (int t = 0; t < H; ++t) {
+      const double* u = acts + static_cast<size_t>(t) * m;
+      __syncwarp();
+      if (lane < n) vin[lane] = x_reg;
+      for (int j = lane; j < m; j += 32) vin[n + j] = u[j];
+      __syncwarp();
+      double* a = vin;
+      double* o = vout;
+      for (int l = 0; l < L; ++l) {
+        const int rows = N.dims[l + 1], cols = N.dims[l];
+        const double* wsm = psm + woff[l];
+        const double* bias = N.blob + N.b_off[l];
+        const int act = N.acts[l];
+        for (int o0 = lane; o0 < rows; o0 += 128) {
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int j = 0; j < cols; ++j) {
+            const double aj = a[j];
+            const double* wr = wsm + j * rows + o0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+              if (o0 + 32 * r < rows) acc[r] = add(acc[r], mul(wr[32 * r], aj));
+          }
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int oo = o0 + 32 * r;
+            if (oo < rows) {
+              double v = add(acc[r], __ldg(bias + oo));
+              if (act == 0) v = (v < 0.0) ? 0.0 : v;  // MLPNet::h_relu (neural.hpp:85-87)
+              else if (act == 1) v = tanh(v);
+              o[oo] = v;
+            }
+          }
+        }
+        __syncwarp();
+        double* tmp = a;
+        a = o;
+        o = tmp;
+      }
+      if (lane < n) x_reg = a[lane];
+      if (lane == 0) {  // stage costs (mpc.hpp:171-183)
+        for (int j = 0; j < m; ++j) obj = add(obj, mul(mul(P.r_w[j], u[j]), u[j]));
+        for (int j = 0; j < n; ++j) {
+          const double d = sub(a[j], P.x_goal[j]);
+          obj = add(obj, mul(mul(P.q_w[j], d), d));
+        }
+      }
+    }
+    if (lane == 0) {
+      const int nb = P.n_boxes[b];
+      for (int t = 1; t <= H; ++t) {
+        const double* lo = P.tube_lo + (static_cast<size_t>(b) * (H + 1) + t) * n;
+        const double* hi = P.tube_hi + (static_cast<size_t>(b) * (H + 1) + t) * n;
+        bool box_ok = t < nb;
+        if (box_ok)
+          for (int d = 0; d < n; ++d)
+            if (!(finite(lo[d]) && finite(hi[d]))) box_ok = false;
+        if (box_ok) {
+          for (int c = 0; c < P.n_con; ++c) {
+            const double g = con_margin(P, P.con[c], lo, hi);
+            const double ng = -g;
+            obj = add(obj, mul(P.penalty, (0.0 < ng) ? ng : 0.0));
+          }
+        } else if (P.n_con > 0) {
+          obj = add(obj, mul(mul(P.penalty, P.diverged_margin), static_cast<double>(P.n_con)));
+        }
+      }
+      P.objective[b] = obj;
+      P.diverged[b] = P.status[b] != ST_OK ? 1 : 0;
+    }
+  }
+}
+
 // plan_step_margin (mpc.hpp:211-215) of K boxes: min over the constraints of
 // Constraint::margin, folded with std::min's (b < a ? b : a) from +inf.
 __global__ void box_margin_kernel(const PlanParams P, const double* lo, const double* hi, int K, double* out) {

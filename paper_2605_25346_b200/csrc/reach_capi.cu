@@ -1043,6 +1043,28 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
   int wmax = 0;
   for (int l = 0; l < net->L; ++l) wmax = std::max(wmax, net->dims[l] * net->dims[l + 1]);
   wmax = (wmax + 1) & ~1;
+  // every layer resident in shared memory when it fits with >= 8 candidate warps (one persistent CTA per SM)
+  {
+    int wtot = 0;
+    int maxrows = 0;
+    for (int l = 0; l < net->L; ++l) {
+      wtot += net->dims[l] * net->dims[l + 1];
+      maxrows = std::max(maxrows, net->dims[l + 1]);
+    }
+    wtot = (wtot + 1) & ~1;
+    const long long room = static_cast<long long>(ctx->max_smem) - static_cast<long long>(wtot) * 8;
+    const int warps = room > 0 ? static_cast<int>(std::min<long long>(rb::kPlanMaxWarps, room / (2ll * vec * 8))) : 0;
+    if (warps >= 8 && maxrows <= 4096) {
+      const size_t rsmem = (static_cast<size_t>(wtot) + static_cast<size_t>(warps) * 2 * vec) * 8;
+      RB_CUDA(cudaFuncSetAttribute(rb::plan_objective_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(rsmem)));
+      const int grid = static_cast<int>(std::min<long long>((batch + warps - 1) / warps, ctx->num_sms));
+      rb::plan_objective_resident_kernel<<<grid, 32 * warps, rsmem, ctx->stream>>>(Q, vec, wtot);
+      RB_CUDA(cudaGetLastError());
+      ctx->launches += 2;
+      return REACH_OK;
+    }
+  }
   const size_t smem = (static_cast<size_t>(wmax) + static_cast<size_t>(rb::kPlanWarps) * 2 * vec) * 8;
   if (smem > static_cast<size_t>(ctx->max_smem))
     return fail(ctx, REACH_E_UNSUPPORTED, "plan_eval: layer too large for the staged rollout");
