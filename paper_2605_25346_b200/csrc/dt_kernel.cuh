@@ -96,7 +96,7 @@ struct DTParams {
   long long wws_stride;     // doubles per CTA
   int w_lds, w_rows;        // state row stride / rows (n + l)
   int w_nop, w_hw;          // Lambda^T row stride (odd), widest streamed row / unit count
-  int w_o_stage, w_o_relax, w_o_bf0, w_o_misc, w_o_int;  // shared-memory offsets (doubles)
+  int w_o_stage, w_o_relax, w_o_bf0, w_o_misc, w_o_int, w_o_bar;  // shared-memory offsets (doubles)
   unsigned long long* w_phase;  // optional per-phase cycle counters (RB_WIDE_PHASE=1), else null
 };
 

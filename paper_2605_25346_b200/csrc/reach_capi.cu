@@ -274,7 +274,10 @@ int plan_wide(reach_ctx* ctx, const reach_net* net, int n, int m, int window, lo
   const int nomax = std::max(n, l);
   off += n + n_i + 2 * n + 3 * nomax + std::max(l, 1) + n + 32;
   P.w_o_int = static_cast<int>(ev(off));
-  const size_t bytes = static_cast<size_t>(P.w_o_int) * 8 + 48 * 4 + static_cast<size_t>(std::max(lmax - 1, 1)) * 256;
+  // the ring mbarriers (8 x 8 B) after the int region (48 ints + the active-unit lists)
+  const size_t ints = 48 * 4 + static_cast<size_t>(std::max(lmax - 1, 1)) * 256;
+  P.w_o_bar = P.w_o_int + static_cast<int>((ints + 15) / 16 * 2);
+  const size_t bytes = static_cast<size_t>(P.w_o_bar) * 8 + 8 * 8;
   if (bytes > static_cast<size_t>(ctx->max_smem))
     return fail(ctx, REACH_E_UNSUPPORTED, "wide kernel working set exceeds shared memory");
   P.w_nop = nop;

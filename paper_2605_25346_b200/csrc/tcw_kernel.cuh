@@ -580,6 +580,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) dt_tcw_kernel(const DTParams 
   T.ebc = is + 48;
   T.ebn = T.ebc + tcw::kBRows;
   W.lists = reinterpret_cast<unsigned char*>(T.ebn + tcw::kBRows);
+  W.bars = nullptr;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + X.o_bar);
   tcw::Pipe pp;
   pp.aring = sm + tcw::kBBytes;

@@ -89,16 +89,69 @@ struct WideSmem {
   int* iv;          // [16] misc ints (pivot, flags)
   int* cnt;         // [kMaxLayers] active-unit counts
   unsigned char* lists;  // [L-1][256] active units
+  uint64_t* bars;        // [8] mbarriers of the bulk-copy rings (null: element-wise cp.async rings)
   int nop, hw;
 };
 
 // Streams rows list[0..nk) (identity when list == nullptr) of a row-major
 // global matrix -- `ncols` doubles from base + k * ld -- through a cp.async
 // ring of NS stages of RS rows and calls f(row_in_smem, k) on every thread, in order.
+//
+// With `bars` (and 16-byte aligned rows), each row of a chunk is one bulk copy (the TMA engine's 1-D
+// form, UBLKCP) completing on the stage's mbarrier: one lane per row issues, instead of every thread
+// issuing 8-byte cp.async per element (13 % of the C5 kernel's instructions).
 template <int NS = kWideNS, int RS = kWideRS, class F>
 __device__ __forceinline__ void stream_rows(double* stages, const double* base, long long ld,
-                                            const unsigned char* list, int nk, int ncols, F&& f) {
+                                            const unsigned char* list, int nk, int ncols, F&& f,
+                                            uint64_t* bars = nullptr) {
   const int nch = (nk + RS - 1) / RS;
+  static_assert(NS <= 8, "one mbarrier per stage");
+  if (bars && nch > 0 &&
+      ((reinterpret_cast<uintptr_t>(base) | static_cast<uintptr_t>(ld * 8) | static_cast<uintptr_t>(ncols * 8)) & 15u) ==
+          0) {
+    const int tid = threadIdx.x;
+    __syncthreads();  // the previous user of the barriers and of the stages is done
+    if (tid == 0) {
+      for (int q = 0; q < NS; ++q) mbar_init(bars + q, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t rowb = static_cast<uint32_t>(ncols) * 8u;
+    auto bissue = [&](int c) {  // warp 0: lane 0 arms the stage, lanes < nr copy one row each
+      if (c < nch && tid < 32) {
+        double* st = stages + (c % NS) * (RS * kWideSW);
+        const int t0 = c * RS;
+        const int nr = min(RS, nk - t0);
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive_expect_tx(bars + c % NS, rowb * static_cast<uint32_t>(nr));
+        }
+        __syncwarp();
+        for (int rr = tid; rr < nr; rr += 32) {
+          const int k = list ? static_cast<int>(list[t0 + rr]) : t0 + rr;
+          bulk_g2s(st + rr * kWideSW, base + static_cast<long long>(k) * ld, rowb, bars + c % NS);
+        }
+      }
+    };
+#pragma unroll
+    for (int c = 0; c < NS - 1; ++c) bissue(c);
+    for (int c = 0; c < nch; ++c) {
+      mbar_wait(bars + c % NS, (c / NS) & 1);
+      __syncthreads();  // every thread is past chunk c - 1: its stage can be refilled
+      bissue(c + NS - 1);
+      const double* st = stages + (c % NS) * (RS * kWideSW);
+      const int t0 = c * RS;
+      const int nr = min(RS, nk - t0);
+      if (nr == RS) {
+#pragma unroll kWideUnroll
+        for (int rr = 0; rr < RS; ++rr) f(st + rr * kWideSW, list ? static_cast<int>(list[t0 + rr]) : t0 + rr);
+      } else {
+        for (int rr = 0; rr < nr; ++rr) f(st + rr * kWideSW, list ? static_cast<int>(list[t0 + rr]) : t0 + rr);
+      }
+    }
+    __syncthreads();
+    return;
+  }
   auto issue = [&](int c) {
     if (c < nch) {
       double* st = stages + (c % NS) * (RS * kWideSW);
@@ -181,7 +234,8 @@ __device__ __forceinline__ double row_abs_sums_staged(const double* A, long long
 // rows k, each a sequential chain in stream order (linalg.hpp:53-63, i-k-j).
 template <int RPT, int CPL>
 __device__ __forceinline__ void wide_gemm(const double* LT, int nop, double* stages, const double* base, long long ld,
-                                          const unsigned char* list, int nk, int ncols, double (&acc)[RPT][CPL]) {
+                                          const unsigned char* list, int nk, int ncols, double (&acc)[RPT][CPL],
+                                          uint64_t* bars = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int r = 0; r < RPT; ++r)
@@ -198,17 +252,17 @@ __device__ __forceinline__ void wide_gemm(const double* LT, int nop, double* sta
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
       for (int c = 0; c < CPL; ++c) acc[r][c] = add(acc[r][c], mul(lam[r], w[c]));
-  });
+  }, bars);
 }
 
 // Lambda <- Lambda_s . W (ncols <= 256) written back into LT; returns true if any
 // entry is non-finite (the reference's remainder would be non-finite).
 template <int RPT, int CPL>
-__device__ __forceinline__ bool gemm_to_lt_t(double* LT, int nop, int n_o, double* stages, const double* W,
+__device__ __forceinline__ bool gemm_to_lt_t(uint64_t* bars, double* LT, int nop, int n_o, double* stages, const double* W,
                                              long long ldw, const unsigned char* list, int nk, int ncols) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double acc[RPT][CPL];
-  wide_gemm<RPT, CPL>(LT, nop, stages, W, ldw, list, nk, ncols, acc);
+  wide_gemm<RPT, CPL>(LT, nop, stages, W, ldw, list, nk, ncols, acc, bars);
   bool bad = false;
 #pragma unroll
   for (int r = 0; r < RPT; ++r)
@@ -224,19 +278,19 @@ __device__ __forceinline__ bool gemm_to_lt_t(double* LT, int nop, int n_o, doubl
 }
 
 template <int RPT>
-__device__ __forceinline__ bool gemm_to_lt(double* LT, int nop, int n_o, double* stages, const double* W, long long ldw,
+__device__ __forceinline__ bool gemm_to_lt(uint64_t* bars, double* LT, int nop, int n_o, double* stages, const double* W, long long ldw,
                                            const unsigned char* list, int nk, int ncols) {
-  if (ncols <= 64) return gemm_to_lt_t<RPT, 2>(LT, nop, n_o, stages, W, ldw, list, nk, ncols);
-  if (ncols <= 128) return gemm_to_lt_t<RPT, 4>(LT, nop, n_o, stages, W, ldw, list, nk, ncols);
-  return gemm_to_lt_t<RPT, 8>(LT, nop, n_o, stages, W, ldw, list, nk, ncols);
+  if (ncols <= 64) return gemm_to_lt_t<RPT, 2>(bars, LT, nop, n_o, stages, W, ldw, list, nk, ncols);
+  if (ncols <= 128) return gemm_to_lt_t<RPT, 4>(bars, LT, nop, n_o, stages, W, ldw, list, nk, ncols);
+  return gemm_to_lt_t<RPT, 8>(bars, LT, nop, n_o, stages, W, ldw, list, nk, ncols);
 }
 
 template <int RPT, int CPL>
-__device__ __forceinline__ void gemm_to_global_t(const double* LT, int nop, int n_o, double* stages, const double* A,
+__device__ __forceinline__ void gemm_to_global_t(uint64_t* bars, const double* LT, int nop, int n_o, double* stages, const double* A,
                                                  long long lda, int nk, int ncols, double* out, long long ldo) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double acc[RPT][CPL];
-  wide_gemm<RPT, CPL>(LT, nop, stages, A, lda, nullptr, nk, ncols, acc);
+  wide_gemm<RPT, CPL>(LT, nop, stages, A, lda, nullptr, nk, ncols, acc, bars);
 #pragma unroll
   for (int r = 0; r < RPT; ++r)
 #pragma unroll
@@ -248,13 +302,13 @@ __device__ __forceinline__ void gemm_to_global_t(const double* LT, int nop, int 
 
 // out[:, 0:nz) = Lambda (n_o x nk) . A (nk x nz), in column passes of <= 256.
 template <int RPT>
-__device__ __forceinline__ void gemm_to_global(const double* LT, int nop, int n_o, double* stages, const double* A,
+__device__ __forceinline__ void gemm_to_global(uint64_t* bars, const double* LT, int nop, int n_o, double* stages, const double* A,
                                                long long lda, int nk, int nz, double* out, long long ldo) {
   for (int col0 = 0; col0 < nz; col0 += kWideSW) {
     const int nc = min(kWideSW, nz - col0);
-    if (nc <= 64) gemm_to_global_t<RPT, 2>(LT, nop, n_o, stages, A + col0, lda, nk, nc, out + col0, ldo);
-    else if (nc <= 128) gemm_to_global_t<RPT, 4>(LT, nop, n_o, stages, A + col0, lda, nk, nc, out + col0, ldo);
-    else gemm_to_global_t<RPT, 8>(LT, nop, n_o, stages, A + col0, lda, nk, nc, out + col0, ldo);
+    if (nc <= 64) gemm_to_global_t<RPT, 2>(bars, LT, nop, n_o, stages, A + col0, lda, nk, nc, out + col0, ldo);
+    else if (nc <= 128) gemm_to_global_t<RPT, 4>(bars, LT, nop, n_o, stages, A + col0, lda, nk, nc, out + col0, ldo);
+    else gemm_to_global_t<RPT, 8>(bars, LT, nop, n_o, stages, A + col0, lda, nk, nc, out + col0, ldo);
   }
 }
 
@@ -345,9 +399,10 @@ __device__ int wide_certify(const DevNet& N, int n_i, int n_o, int nx, const dou
       }
     };
     if (deep_ring_fits(nop, W.hw))
-      stream_rows<kDeepNS, kDeepRS>(deep_ring(W.lt, W.hw), N.blob + N.wt_off[l], N.ldt[l], inlist, nk, width, ibp_row);
+      stream_rows<kDeepNS, kDeepRS>(deep_ring(W.lt, W.hw), N.blob + N.wt_off[l], N.ldt[l], inlist, nk, width, ibp_row,
+                                    W.bars);
     else
-      stream_rows(W.stages, N.blob + N.wt_off[l], N.ldt[l], inlist, nk, width, ibp_row);
+      stream_rows(W.stages, N.blob + N.wt_off[l], N.ldt[l], inlist, nk, width, ibp_row, W.bars);
     bool flag = false;
     if (o < width) {
       const double plo = add(alo, bfold), phi = add(ahi, bfold);
@@ -454,7 +509,7 @@ __device__ int wide_certify(const DevNet& N, int n_i, int n_o, int nx, const dou
     __syncthreads();
     ph.mark(pb + WP_GEMM);
     const int ncols = (l == 0) ? n_i : N.dims[l];
-    if (gemm_to_lt<RPT>(LT, nop, n_o, W.stages, N.blob + N.w_off[l], N.ldw[l], list, cnt, ncols)) return WC_CERT;
+    if (gemm_to_lt<RPT>(W.bars, LT, nop, n_o, W.stages, N.blob + N.w_off[l], N.ldw[l], list, cnt, ncols)) return WC_CERT;
   }
 
   // ---- prepended layer W = [A | I], b = c: shift chain, then Lambda . A
@@ -465,7 +520,7 @@ __device__ int wide_certify(const DevNet& N, int n_i, int n_o, int nx, const dou
     blo = add(blo, shift);
     bup = add(bup, shift);
   }
-  gemm_to_global<RPT>(LT, nop, n_o, W.stages, A, lda, n_i, nz, out, ldo);
+  gemm_to_global<RPT>(W.bars, LT, nop, n_o, W.stages, A, lda, n_i, nz, out, ldo);
   if (frad)
     for (int e = tid; e < n_o * n_i; e += kWideThreads) {
       const int i = e / n_i, jj = e - i * n_i;
@@ -566,11 +621,20 @@ static __device__ void wide_fold(double* S, long long lds, int n, int& base, int
         if ((d >> 5) == t) vp = x;
       }
       for (int i = lane; i < n; i += 32) pout[i] = (i == k) ? pin[piv] : (i == piv) ? pin[k] : pin[i];
+#if RB_FUSED
+      const double rvp = 1.0 / vp;  // fused mode: one reciprocal per pivot
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int i = k + lane + 32 * t;
+        if (i > k && i < n) fout[i] = (i == piv ? vk : v[t]) * rvp;
+      }
+#else
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int i = k + lane + 32 * t;
         if (i > k && i < n) fout[i] = __ddiv_rn(i == piv ? vk : v[t], vp);
       }
+#endif
       if (lane == 0) *bout = best;
     };
     if (warp == 0) {
@@ -642,6 +706,26 @@ static __device__ void wide_fold(double* S, long long lds, int n, int& base, int
       // register, the older x_k are read in blocks of 4 ahead of the chain
       for (int jc = tid; jc < w; jc += kWideThreads) {
         double xprev = 0.0;
+#if RB_FUSED
+        // fused mode: four partial sums per row (a different association; the chain length drops 4x)
+        for (int i = n - 1; i >= 0; --i) {
+          const double* mrow = M + Pf[i] * nc;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          int k = i + 2;
+          for (; k + 4 <= n; k += 4) {
+            s0 = fma(mrow[k], X[k * w + jc], s0);
+            s1 = fma(mrow[k + 1], X[(k + 1) * w + jc], s1);
+            s2 = fma(mrow[k + 2], X[(k + 2) * w + jc], s2);
+            s3 = fma(mrow[k + 3], X[(k + 3) * w + jc], s3);
+          }
+          for (; k < n; ++k) s0 = fma(mrow[k], X[k * w + jc], s0);
+          double acc = mrow[n + jc] - ((s0 + s1) + (s2 + s3));
+          if (i + 1 < n) acc = fma(-mrow[i + 1], xprev, acc);
+          xprev = acc / mrow[i];
+          X[i * w + jc] = xprev;
+        }
+        continue;
+#endif
         for (int i = n - 1; i >= 0; --i) {
           const double* mrow = M + Pf[i] * nc;
           double acc = mrow[n + jc];
@@ -765,6 +849,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) dt_wide_kernel(const DTParams
   W.iv = is + 16;
   W.cnt = is + 32;
   W.lists = reinterpret_cast<unsigned char*>(is + 48);
+  W.bars = reinterpret_cast<uint64_t*>(sd + P.w_o_bar);
 
   const long long lds = P.w_lds;
   double* buf0 = P.wws + static_cast<long long>(blockIdx.x) * P.wws_stride;
