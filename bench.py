@@ -581,16 +581,20 @@ def closed_loop_legs(args, ctx, world, rank, dev, barrier, stream):
     out["c5_closed_loop"] = c5
     if rank == 0:
         w1 = c1_closed_loop(batch=1)
-        for _ in range(3):
-            dt_closed_loop_batch(w1.dyn, w1.ctl, w1.n, w1.x0_lo, w1.x0_hi, w1.horizon, ctx=ctx)
-        lat = []
-        for _ in range(10):
-            t0 = time.perf_counter()
-            dt_closed_loop_batch(w1.dyn, w1.ctl, w1.n, w1.x0_lo, w1.x0_hi, w1.horizon, ctx=ctx)
-            lat.append(time.perf_counter() - t0)
+        lat_by = {}
+        for prec in ("fused", "exact"):
+            for _ in range(3):
+                dt_closed_loop_batch(w1.dyn, w1.ctl, w1.n, w1.x0_lo, w1.x0_hi, w1.horizon, ctx=ctx, precision=prec)
+            lat = []
+            for _ in range(10):
+                t0 = time.perf_counter()
+                dt_closed_loop_batch(w1.dyn, w1.ctl, w1.n, w1.x0_lo, w1.x0_hi, w1.horizon, ctx=ctx, precision=prec)
+                lat.append(time.perf_counter() - t0)
+            lat_by[prec] = 1e3 * float(np.median(lat))
         c1 = {"workload": "c1_closed_loop (BASELINE configs[0]): 4-D DT closed loop, 6->64x2->4 ReLU dynamics + "
                           "4->64x2->2 ReLU controller, one box, H=20",
-              "latency_ms_end_to_end": 1e3 * float(np.median(lat)),
+              "latency_ms_end_to_end": lat_by["fused"], "precision": "fused",
+              "latency_ms_end_to_end_exact": lat_by["exact"],
               "note": "batch 1 is latency-bound (SURVEY §8d): host call incl. copies, median of 10"}
         if not args.no_cpu_baseline:
             try:
