@@ -3,7 +3,9 @@
 // (refine.hpp:186-207) evaluates it -- one Dual pass of cl_reach (closed_loop.hpp:76-182) per seeded
 // parameter and episode.
 //
-// One warp (one CTA) per (pass p, episode e), its whole working set in shared memory (~170 KB):
+// One warp per (pass p, episode e); its working set (~200 KB) in global memory (L1 / L2 resident) with 8
+// persistent passes per SM (ctl_reach_loss_grad_kernel_g, the default: 2.9x the one-pass-per-SM
+// shared-memory variant ctl_reach_loss_grad_kernel, RB_CTD_SLOTS_PER_SM=0):
 //   * TMExpr<Dual> rows (taylor_model.hpp:197-445) with the generator columns lane-strided
 //     (lane L owns columns L, L+32, L+64); the scalar parts (c, at, the remainder interval) are
 //     computed by every lane alike and stored by lane 0; abs-sums are warp reductions;
@@ -747,10 +749,8 @@ struct CtlLossArgs {
 };
 
 // One Dual cl_reach (closed_loop.hpp:76-182) from box_from_center(x0_e, eps) per (pass, episode).
-__global__ void __launch_bounds__(32, 1) ctl_reach_loss_grad_kernel(const CtlLossArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Work& W = *reinterpret_cast<Work*>(smem_raw);
-  const int lane = threadIdx.x & 31, pass = blockIdx.x, ep = blockIdx.y;
+__device__ void ctl_pass(const CtlLossArgs& A, Work& W, int pass, int ep) {
+  const int lane = threadIdx.x & 31;
   const int n = A.n, l = A.l, na = n + l;
   dual::NetView net{A.net};
   if (A.seeded) dual::seed_param(net, A.poff, pass);
@@ -870,6 +870,21 @@ __global__ void __launch_bounds__(32, 1) ctl_reach_loss_grad_kernel(const CtlLos
     A.term_d[o] = term.d;
     if (pass == 0) A.diverged[ep] = failed ? 1 : 0;
   }
+  __syncwarp();
+}
+
+// Working set in shared memory: one pass per CTA (one warp per SM: the ~200 KB set fills it).
+__global__ void __launch_bounds__(32, 1) ctl_reach_loss_grad_kernel(const CtlLossArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ctl_pass(A, *reinterpret_cast<Work*>(smem_raw), blockIdx.x, blockIdx.y);
+}
+
+// Working set in global memory (L1 / L2 resident), one Work slot per CTA, CTAs persistent over the
+// (pass, episode) pairs: several latency-bound passes per SM instead of one.
+__global__ void __launch_bounds__(32) ctl_reach_loss_grad_kernel_g(const CtlLossArgs A, Work* ws, long long total) {
+  Work& W = ws[blockIdx.x];
+  for (long long q = blockIdx.x; q < total; q += gridDim.x)
+    ctl_pass(A, W, static_cast<int>(q / A.M), static_cast<int>(q % A.M));
 }
 
 }  // namespace ctd

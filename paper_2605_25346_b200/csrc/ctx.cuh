@@ -34,7 +34,9 @@ struct reach_ctx {
   // per-CTA symbolic-state buffers of the wide kernel family
   void* wws = nullptr;
   size_t wws_bytes = 0;
-  unsigned long long* wphase = nullptr;  // wide-kernel phase counters (RB_WIDE_PHASE=1)
+  unsigned long long* wphase = nullptr;
+  void* ctd_ws = nullptr;  // Dual CT working sets (ctl_reach_loss gradient), one per persistent CTA
+  size_t ctd_bytes = 0;  // wide-kernel phase counters (RB_WIDE_PHASE=1)
   // multi-GPU collectives (coll.cu): user callbacks or the built-in NCCL communicator
   reach_collectives coll{};
   bool has_coll = false;

@@ -447,6 +447,7 @@ int reach_ctx_destroy(reach_ctx* ctx) {
   if (ctx->pbuf) cudaFree(ctx->pbuf);
   if (ctx->wws) cudaFree(ctx->wws);
   if (ctx->wphase) cudaFree(ctx->wphase);
+  if (ctx->ctd_ws) cudaFree(ctx->ctd_ws);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
   for (auto& p : ctx->ev_used) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   for (auto& p : ctx->ev_free) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
@@ -2508,15 +2509,38 @@ int reach_ctl_reach_loss(reach_ctx* ctx, const reach_net* ctl, const reach_cl_sp
   A.term_d = Dp(o_d);
   A.diverged = reinterpret_cast<int*>(w + o_dv);
   const size_t smem = sizeof(cd::Work);
-  if (smem > static_cast<size_t>(ctx->max_smem))
-    return fail(ctx, REACH_E_UNSUPPORTED, "ctl_reach_loss: Dual working set exceeds shared memory");
-  RB_CUDA(cudaFuncSetAttribute(cd::ctl_reach_loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
+  // RB_CTD_SLOTS_PER_SM > 0: the working sets in global memory, that many persistent passes per SM
+  const int slots_per_sm = env_int("RB_CTD_SLOTS_PER_SM", 8, 0, 64);
   cudaEvent_t stop;
-  rc = timed_begin(ctx, &stop);
-  if (rc) return rc;
-  cd::ctl_reach_loss_grad_kernel<<<dim3(static_cast<unsigned>(P), static_cast<unsigned>(M)), 32, smem, ctx->stream>>>(A);
-  RB_CUDA(cudaGetLastError());
+  if (slots_per_sm > 0) {
+    const long long total = P * M;
+    const int grid = static_cast<int>(std::min<long long>(total, static_cast<long long>(slots_per_sm) * ctx->num_sms));
+    const size_t need = static_cast<size_t>(grid) * sizeof(cd::Work);
+    if (need > ctx->ctd_bytes) {
+      if (ctx->ctd_ws) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(ctx->ctd_ws);
+        ctx->ctd_ws = nullptr;
+        ctx->ctd_bytes = 0;
+      }
+      RB_CUDA(cudaMalloc(&ctx->ctd_ws, need));
+      ctx->ctd_bytes = need;
+    }
+    rc = timed_begin(ctx, &stop);
+    if (rc) return rc;
+    cd::ctl_reach_loss_grad_kernel_g<<<grid, 32, 0, ctx->stream>>>(A, static_cast<cd::Work*>(ctx->ctd_ws), total);
+    RB_CUDA(cudaGetLastError());
+  } else {
+    if (smem > static_cast<size_t>(ctx->max_smem))
+      return fail(ctx, REACH_E_UNSUPPORTED, "ctl_reach_loss: Dual working set exceeds shared memory");
+    RB_CUDA(cudaFuncSetAttribute(cd::ctl_reach_loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    rc = timed_begin(ctx, &stop);
+    if (rc) return rc;
+    cd::ctl_reach_loss_grad_kernel<<<dim3(static_cast<unsigned>(P), static_cast<unsigned>(M)), 32, smem,
+                                     ctx->stream>>>(A);
+    RB_CUDA(cudaGetLastError());
+  }
   rc = timed_end(ctx, stop);
   if (rc) return rc;
   ctx->launches += 1;
