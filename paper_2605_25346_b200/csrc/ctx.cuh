@@ -35,6 +35,8 @@ struct reach_ctx {
   void* wws = nullptr;
   size_t wws_bytes = 0;
   unsigned long long* wphase = nullptr;
+  cudaStream_t aux = nullptr;  // second stream: plan_eval's rollouts run beside its tube kernel
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* ctd_ws = nullptr;  // Dual CT working sets (ctl_reach_loss gradient), one per persistent CTA
   size_t ctd_bytes = 0;  // wide-kernel phase counters (RB_WIDE_PHASE=1)
   // multi-GPU collectives (coll.cu): user callbacks or the built-in NCCL communicator

@@ -173,13 +173,15 @@ __global__ void __launch_bounds__(kPlanWarps * 32) plan_objective_kernel(const P
   P.diverged[b] = P.status[b] != ST_OK ? 1 : 0;
 }
 
-// The same objective with every W_l^T resident in shared memory for the whole launch (staged once per
-// CTA, not per step and layer), up to 32 candidate warps per CTA persistent over the batch, and each
-// lane's up-to-4 output units of a layer accumulated side by side (independent chains, each in the
-// reference's j order) -- used whenever the network fits (C3: 157 KB).  Bit-identical to the above.
+// The objective's rollout part (nominal rollout + stage costs, mpc.hpp:170-184) with every W_l^T
+// resident in shared memory for the whole launch (staged once per CTA, not per step and layer), up to
+// 32 candidate warps per CTA persistent over the batch, and each lane's up-to-4 output units of a layer
+// accumulated side by side (independent chains, each in the reference's j order) -- used whenever the
+// network fits (C3: 157 KB).  It does not read the tube, so it runs concurrently with the tube kernel;
+// plan_penalty_kernel then adds the constraint terms.  Together bit-identical to the above.
 constexpr int kPlanMaxWarps = 32;
-__global__ void __launch_bounds__(kPlanMaxWarps * 32) plan_objective_resident_kernel(const PlanParams P, int vec,
-                                                                                     int wtot) {
+__global__ void __launch_bounds__(kPlanMaxWarps * 32) plan_rollout_resident_kernel(const PlanParams P, int vec,
+                                                                                   int wtot) {
   extern __shared__ __align__(16) double psm[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
   const DevNet& N = P.net;
@@ -253,29 +255,37 @@ __global__ void __launch_bounds__(kPlanMaxWarps * 32) plan_objective_resident_ke
         }
       }
     }
-    if (lane == 0) {
-      const int nb = P.n_boxes[b];
-      for (int t = 1; t <= H; ++t) {
-        const double* lo = P.tube_lo + (static_cast<size_t>(b) * (H + 1) + t) * n;
-        const double* hi = P.tube_hi + (static_cast<size_t>(b) * (H + 1) + t) * n;
-        bool box_ok = t < nb;
-        if (box_ok)
-          for (int d = 0; d < n; ++d)
-            if (!(finite(lo[d]) && finite(hi[d]))) box_ok = false;
-        if (box_ok) {
-          for (int c = 0; c < P.n_con; ++c) {
-            const double g = con_margin(P, P.con[c], lo, hi);
-            const double ng = -g;
-            obj = add(obj, mul(P.penalty, (0.0 < ng) ? ng : 0.0));
-          }
-        } else if (P.n_con > 0) {
-          obj = add(obj, mul(mul(P.penalty, P.diverged_margin), static_cast<double>(P.n_con)));
-        }
+    if (lane == 0) P.objective[b] = obj;  // rollout terms; plan_penalty_kernel adds the constraint terms
+  }
+}
+
+// Constraint penalties over the certified tube (mpc.hpp:187-200), one thread per candidate, added to the
+// rollout terms plan_rollout_resident_kernel left in P.objective.
+__global__ void plan_penalty_kernel(const PlanParams P) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B) return;
+  const int n = P.n, H = P.H;
+  double obj = P.objective[b];
+  const int nb = P.n_boxes[b];
+  for (int t = 1; t <= H; ++t) {
+    const double* lo = P.tube_lo + (static_cast<size_t>(b) * (H + 1) + t) * n;
+    const double* hi = P.tube_hi + (static_cast<size_t>(b) * (H + 1) + t) * n;
+    bool box_ok = t < nb;
+    if (box_ok)
+      for (int d = 0; d < n; ++d)
+        if (!(finite(lo[d]) && finite(hi[d]))) box_ok = false;
+    if (box_ok) {
+      for (int c = 0; c < P.n_con; ++c) {
+        const double g = con_margin(P, P.con[c], lo, hi);
+        const double ng = -g;
+        obj = add(obj, mul(P.penalty, (0.0 < ng) ? ng : 0.0));
       }
-      P.objective[b] = obj;
-      P.diverged[b] = P.status[b] != ST_OK ? 1 : 0;
+    } else if (P.n_con > 0) {
+      obj = add(obj, mul(mul(P.penalty, P.diverged_margin), static_cast<double>(P.n_con)));
     }
   }
+  P.objective[b] = obj;
+  P.diverged[b] = P.status[b] != ST_OK ? 1 : 0;
 }
 
 // plan_step_margin (mpc.hpp:211-215) of K boxes: min over the constraints of

@@ -448,6 +448,12 @@ int reach_ctx_destroy(reach_ctx* ctx) {
   if (ctx->wws) cudaFree(ctx->wws);
   if (ctx->wphase) cudaFree(ctx->wphase);
   if (ctx->ctd_ws) cudaFree(ctx->ctd_ws);
+  if (ctx->aux) {
+    cudaStreamSynchronize(ctx->aux);
+    cudaStreamDestroy(ctx->aux);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
+  }
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
   for (auto& p : ctx->ev_used) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   for (auto& p : ctx->ev_free) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
@@ -1001,12 +1007,6 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
   P.n_boxes = d_nb;
   P.failed_step = d_fs;
   P.status = d_st;
-  cudaEvent_t stop;
-  rc = timed_begin(ctx, &stop);
-  if (rc) return rc;
-  RB_CUDA(launch_dt(P, lay, batch, ctx->stream));
-  rc = timed_end(ctx, stop);
-  if (rc) return rc;
   // objective kernel: problem arrays staged after the tube in the plan workspace
   PlanBuffers pb;
   pack_problem(p, pb);
@@ -1047,7 +1047,10 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
   int wmax = 0;
   for (int l = 0; l < net->L; ++l) wmax = std::max(wmax, net->dims[l] * net->dims[l + 1]);
   wmax = (wmax + 1) & ~1;
-  // every layer resident in shared memory when it fits with >= 8 candidate warps (one persistent CTA per SM)
+  // every layer resident in shared memory when it fits with >= 8 candidate warps (one persistent CTA per
+  // SM): the nominal rollouts + stage costs do not read the tube, so they run on a second stream
+  // concurrently with the tube kernel (filling the SMs its last wave leaves idle); the penalty pass joins
+  // after both (plan_objective = rollout terms, then the constraint terms, in the reference's order).
   {
     int wtot = 0;
     int maxrows = 0;
@@ -1059,16 +1062,39 @@ int plan_eval_device(reach_ctx* ctx, const reach_net* net, const reach_plan_prob
     const long long room = static_cast<long long>(ctx->max_smem) - static_cast<long long>(wtot) * 8;
     const int warps = room > 0 ? static_cast<int>(std::min<long long>(rb::kPlanMaxWarps, room / (2ll * vec * 8))) : 0;
     if (warps >= 8 && maxrows <= 4096) {
+      if (!ctx->aux) {
+        RB_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+        RB_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        RB_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+      }
       const size_t rsmem = (static_cast<size_t>(wtot) + static_cast<size_t>(warps) * 2 * vec) * 8;
-      RB_CUDA(cudaFuncSetAttribute(rb::plan_objective_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      RB_CUDA(cudaFuncSetAttribute(rb::plan_rollout_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(rsmem)));
       const int grid = static_cast<int>(std::min<long long>((batch + warps - 1) / warps, ctx->num_sms));
-      rb::plan_objective_resident_kernel<<<grid, 32 * warps, rsmem, ctx->stream>>>(Q, vec, wtot);
+      RB_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+      RB_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+      rb::plan_rollout_resident_kernel<<<grid, 32 * warps, rsmem, ctx->aux>>>(Q, vec, wtot);
       RB_CUDA(cudaGetLastError());
-      ctx->launches += 2;
+      RB_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux));
+  cudaEvent_t stop;
+    rc = timed_begin(ctx, &stop);
+    if (rc) return rc;
+    RB_CUDA(launch_dt(P, lay, batch, ctx->stream));
+    rc = timed_end(ctx, stop);
+    if (rc) return rc;
+      RB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+      rb::plan_penalty_kernel<<<(batch + 255) / 256, 256, 0, ctx->stream>>>(Q);
+      RB_CUDA(cudaGetLastError());
+      ctx->launches += 3;
       return REACH_OK;
     }
   }
+  cudaEvent_t stop;
+  rc = timed_begin(ctx, &stop);
+  if (rc) return rc;
+  RB_CUDA(launch_dt(P, lay, batch, ctx->stream));
+  rc = timed_end(ctx, stop);
+  if (rc) return rc;
   const size_t smem = (static_cast<size_t>(wmax) + static_cast<size_t>(rb::kPlanWarps) * 2 * vec) * 8;
   if (smem > static_cast<size_t>(ctx->max_smem))
     return fail(ctx, REACH_E_UNSUPPORTED, "plan_eval: layer too large for the staged rollout");
