@@ -65,6 +65,10 @@ enum reach_tube_status {
 
 /* Flags for the batch entry points. */
 #define REACH_FLAG_DEVICE_PTRS 1 /* every pointer in args/out is a device pointer */
+/* The reference's outward-rounding mode (g_outward_rounding, interval.hpp:19): not supported by the
+ * device kernels (the reference's own worker threads ignore it too); requesting it
+ * returns REACH_E_UNSUPPORTED instead of silently computing in round-to-nearest. */
+#define REACH_FLAG_OUTWARD_ROUNDING 0x10
 /* Precision mode (flags bits 8..11) of the DT engines (reach_dt_batch, reach_dtcl_batch,
  * reach_split_hull).  REACH_PREC_EXACT (default): the reference's arithmetic, bit for bit.
  * REACH_PREC_TC: the CROWN contractions Lambda_s . W_l (neural.hpp:326) on the int8 tensor

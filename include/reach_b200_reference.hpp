@@ -67,10 +67,20 @@ inline reach::ReachTube<double> to_reference(const ReachTube& t) {
   return out;
 }
 
+namespace detail {
+// A caller that switched on the reference's outward rounding (reach::ScopedOutwardRounding,
+// interval.hpp:19-25) gets an error, not round-to-nearest results (C ABI: REACH_FLAG_OUTWARD_ROUNDING).
+inline void refuse_outward_rounding() {
+  if (reach::g_outward_rounding)
+    throw Error("outward rounding (g_outward_rounding) is not supported by the device kernels");
+}
+}  // namespace detail
+
 // reach::dt_reach_batch (dt_reach.hpp:108-125)
 inline std::vector<reach::ReachTube<double>> dt_reach_batch(
     Context& ctx, const reach::DTSystem<double>& sys, const std::vector<reach::IntervalBox<double>>& x0s,
     const std::vector<std::vector<reach::Vec<double>>>& action_seqs, const reach::DTReachParams& prm = {}) {
+  detail::refuse_outward_rounding();
   std::vector<Box> boxes;
   boxes.reserve(x0s.size());
   for (const auto& b : x0s) boxes.push_back(from_reference(b));
@@ -96,6 +106,7 @@ inline reach::ReachTube<double> reach_with_splitting_dt(Context& ctx, const reac
                                                         const reach::SplitPlan& plan,
                                                         const std::vector<reach::Vec<double>>& actions,
                                                         const reach::DTReachParams& prm = {}) {
+  detail::refuse_outward_rounding();
   plan.validate(x0.size());
   SplitPlan p{plan.counts};
   DTReachParams q{prm.window, prm.rebuild_from_box};
@@ -126,6 +137,7 @@ inline ClosedLoopSpec from_reference(const reach::ClosedLoopSpec<double>& spec, 
 
 inline reach::ReachTube<double> cl_reach(Context& ctx, const reach::ClosedLoopSpec<double>& spec,
                                          const reach::QuadrotorParams& plant, const reach::IntervalBox<double>& x0) {
+  detail::refuse_outward_rounding();
   return to_reference(cl_reach(ctx, from_reference(spec, plant), from_reference(x0)));
 }
 
@@ -134,6 +146,7 @@ inline reach::ReachTube<double> reach_with_splitting_cl(Context& ctx, const reac
                                                         const reach::QuadrotorParams& plant,
                                                         const reach::IntervalBox<double>& x0,
                                                         const reach::SplitPlan& plan) {
+  detail::refuse_outward_rounding();
   plan.validate(x0.size());
   return to_reference(reach_with_splitting_cl(ctx, from_reference(spec, plant), from_reference(x0), SplitPlan{plan.counts}));
 }
@@ -144,6 +157,7 @@ inline reach::ReachTube<double> reach_with_splitting_cl(Context& ctx, const reac
 // AnalyticField::rotation(w).
 inline reach::ReachTube<double> ct_reach(Context& ctx, const AnalyticField& f, const reach::IntervalBox<double>& x0,
                                          const reach::FlowpipeParams& prm) {
+  detail::refuse_outward_rounding();
   prm.validate();
   FlowpipeParams p{prm.h, prm.steps, prm.order, prm.eps_init, prm.refine_rounds, prm.enlargement,
                    prm.max_enlargements, prm.window};

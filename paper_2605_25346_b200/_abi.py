@@ -18,6 +18,7 @@ REACH_E_OOM = 5
 REACH_E_NONFINITE = 6
 
 REACH_FLAG_DEVICE_PTRS = 1
+REACH_FLAG_OUTWARD_ROUNDING = 0x10  # the reference's g_outward_rounding: refused (REACH_E_UNSUPPORTED)
 REACH_FLAG_PREC_MASK = 0xF00
 REACH_PREC_EXACT = 0x000
 REACH_PREC_TC = 0x100

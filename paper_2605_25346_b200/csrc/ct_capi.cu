@@ -335,6 +335,8 @@ int reach_cl_batch(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s,
                    const double* x0_hi, const reach_tube_out* out, int32_t flags) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !ctl || !s || !out) return REACH_E_INVALID_ARGUMENT;
+  if (flags & REACH_FLAG_OUTWARD_ROUNDING)
+    return fail(ctx, REACH_E_UNSUPPORTED, "outward rounding (g_outward_rounding) is not supported by the device kernels");
   if (batch < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "cl_reach: negative batch");
   int rc = validate_cl(ctx, ctl, s);
   if (rc) return rc;
@@ -423,6 +425,8 @@ int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spe
                         const reach_hull_out* out, int32_t flags) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !ctl || !s || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  if (flags & REACH_FLAG_OUTWARD_ROUNDING)
+    return fail(ctx, REACH_E_UNSUPPORTED, "outward rounding (g_outward_rounding) is not supported by the device kernels");
   int rc = validate_cl(ctx, ctl, s);
   if (rc) return rc;
   const int n = s->n;
@@ -574,6 +578,8 @@ int reach_ct_batch(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowp
                    const double* x0_lo, const double* x0_hi, const reach_tube_out* out, int32_t flags) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !fd || !fp || !out) return REACH_E_INVALID_ARGUMENT;
+  if (flags & REACH_FLAG_OUTWARD_ROUNDING)
+    return fail(ctx, REACH_E_UNSUPPORTED, "outward rounding (g_outward_rounding) is not supported by the device kernels");
   if (batch < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "ct_reach: negative batch");
   rb::ct::CTParams P{};
   int rc = ct_params(ctx, fd, fp, P);
@@ -650,6 +656,8 @@ int reach_ct_split_hull(reach_ctx* ctx, const reach_field_desc* fd, const reach_
                         const reach_cl_split_args* a, const reach_hull_out* out, int32_t flags) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !fd || !fp || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  if (flags & REACH_FLAG_OUTWARD_ROUNDING)
+    return fail(ctx, REACH_E_UNSUPPORTED, "outward rounding (g_outward_rounding) is not supported by the device kernels");
   rb::ct::CTParams P{};
   int rc = ct_params(ctx, fd, fp, P);
   if (rc) return rc;

@@ -747,6 +747,8 @@ int reach_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_dt_args* a,
                    int32_t flags) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  if (flags & REACH_FLAG_OUTWARD_ROUNDING)
+    return fail(ctx, REACH_E_UNSUPPORTED, "outward rounding (g_outward_rounding) is not supported by the device kernels");
   if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt_reach_batch: negative size");
   int rc = validate_system(ctx, net, a->n, a->m);
   if (rc) return rc;
@@ -757,6 +759,8 @@ int reach_dtcl_batch(reach_ctx* ctx, const reach_net* dyn, const reach_net* ctl,
                      const reach_tube_out* out, int32_t flags) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !dyn || !ctl || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  if (flags & REACH_FLAG_OUTWARD_ROUNDING)
+    return fail(ctx, REACH_E_UNSUPPORTED, "outward rounding (g_outward_rounding) is not supported by the device kernels");
   if (a->batch < 0 || a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt closed loop: negative size");
   if (a->m != 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "dt closed loop: actions come from the controller (m = 0)");
   const int l = ctl->dims[ctl->L];
@@ -793,6 +797,8 @@ int reach_split_hull(reach_ctx* ctx, const reach_net* net, const reach_split_arg
                      int32_t flags) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !a || !out) return REACH_E_INVALID_ARGUMENT;
+  if (flags & REACH_FLAG_OUTWARD_ROUNDING)
+    return fail(ctx, REACH_E_UNSUPPORTED, "outward rounding (g_outward_rounding) is not supported by the device kernels");
   int rc = validate_system(ctx, net, a->n, a->m);
   if (rc) return rc;
   if (a->horizon < 0) return fail(ctx, REACH_E_INVALID_ARGUMENT, "reach_with_splitting: negative horizon");
@@ -1317,6 +1323,8 @@ int reach_plan_eval_batch(reach_ctx* ctx, const reach_net* net, const reach_plan
                           const reach_tube_out* tubes, int32_t flags) {
   rbh::DeviceGuard device_guard_(ctx);
   if (!ctx || !net || !prob || !x0 || !objective || !diverged || batch < 0) return REACH_E_INVALID_ARGUMENT;
+  if (flags & REACH_FLAG_OUTWARD_ROUNDING)
+    return fail(ctx, REACH_E_UNSUPPORTED, "outward rounding (g_outward_rounding) is not supported by the device kernels");
   int rc = validate_problem(ctx, net, prob);
   if (rc) return rc;
   if (batch == 0) return REACH_OK;

@@ -436,6 +436,25 @@ int main() {
       ++failures;
     }
   }
+  // the reference's outward-rounding mode is refused, never silently ignored
+  {
+    reach::ScopedOutwardRounding on(true);
+    bool threw = false;
+    try {
+      Rng r10(1);
+      DTSystem<double> sys;
+      sys.n = 2;
+      sys.m = 0;
+      sys.step = random_mlp(r10, 2, {8}, 2, Act::Relu, 0.5);
+      reach_b200::dt_reach(gpu, sys, box_from_center<double>({0.1, 0.2}, 0.05), std::vector<Vec<double>>(3));
+    } catch (const std::exception&) {
+      threw = true;
+    }
+    if (!threw) {
+      std::printf("outward rounding: not refused\n");
+      ++failures;
+    }
+  }
   std::printf(failures ? "FAIL (%d)\n" : "OK: reference drop-in parity\n", failures);
   return failures ? 1 : 0;
 }

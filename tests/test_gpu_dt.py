@@ -197,3 +197,23 @@ def test_invalid_arguments_raise_value_error():
         dt_reach_batch_arrays(DTSystem(sys.step, 4, 3), lo[:, :4], hi[:, :4], acts, prm)
     with pytest.raises(ValueError):
         dt_reach_batch_arrays(sys, lo, hi, acts[:, :, :1], prm)
+
+
+def test_outward_rounding_flag_is_refused():
+    """REACH_FLAG_OUTWARD_ROUNDING (the reference's g_outward_rounding) is refused, never ignored."""
+    import ctypes as C
+    from paper_2605_25346_b200 import _abi as A
+    from paper_2605_25346_b200.api import default_context
+    rng = np.random.default_rng(2)
+    net = residual_relu_dynamics(rng, 2, 0, [8], dt=0.1)
+    sys = DTSystem(net, 2, 0)
+    ctx = default_context()
+    lo, hi = np.array([[0.0, 0.1]]), np.array([[0.1, 0.2]])
+    H = 3
+    out_lo, out_hi = np.zeros((1, H + 1, 2)), np.zeros((1, H + 1, 2))
+    nb, fs, st = np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1, np.int32)
+    args = A.DTArgs(1, H, 2, 0, 4, 0, A.dptr(lo), A.dptr(hi), A.dptr(np.zeros(1)), 0)
+    to = A.TubeOut(A.dptr(out_lo), A.dptr(out_hi), A.iptr(nb), A.iptr(fs), A.iptr(st))
+    rc = ctx._lib.reach_dt_batch(ctx.handle, ctx.upload(net), C.byref(args), C.byref(to), A.REACH_FLAG_OUTWARD_ROUNDING)
+    assert rc == A.REACH_E_UNSUPPORTED
+    assert "outward rounding" in ctx._lib.reach_ctx_last_error(ctx.handle).decode()
