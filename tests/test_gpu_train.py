@@ -109,3 +109,51 @@ def test_train_ct_ctl_matches_reference(lam):
     assert float(np.max(np.abs(du - de))) <= 1e-6 * float(np.max(np.abs(de)))
     if lam > 0:
         assert rows[-1].l_reach > 0
+
+
+def _tanh_case():
+    """The reference CLI's train-dt task shape (reach_cli.cpp:355-383): a tanh one-step model trained on a
+    damped rotation with a scalar forcing input."""
+    from paper_2605_25346_b200.api import Act, Episode
+    from paper_2605_25346_b200.workloads import random_mlp
+    rng = np.random.default_rng(4)
+    model = random_mlp(rng, 3, [16], 2, Act.Tanh, 0.5)
+    th, damp = 0.3, 0.95
+    data = []
+    for _ in range(6):
+        x = rng.uniform(-0.5, 0.5, 2)
+        xs, us = [x.copy()], []
+        for _ in range(4):
+            u = rng.uniform(-0.3, 0.3, 1)
+            x = np.array([damp * (x[0] * np.cos(th) - x[1] * np.sin(th)) + 0.1 * u[0],
+                          damp * (x[0] * np.sin(th) + x[1] * np.cos(th))])
+            xs.append(x.copy())
+            us.append(u)
+        data.append(Episode(xs, us))
+    return model, data
+
+
+def test_pred_loss_tanh_within_tolerance():
+    """tanh through CUDA's libm: values and gradients within 1e-12 / 1e-10 of the reference's."""
+    model, data = _tanh_case()
+    w = horizon_weights(3)
+    got, g = pred_loss(model, data, 3, w, with_grad=True)
+    exp, ge = ref_pred_loss(model, data, 3, w, with_grad=True)
+    assert abs(got - exp) <= 1e-12 * abs(exp)
+    assert float(np.max(np.abs(g - ge))) <= 1e-10 * float(np.max(np.abs(ge)))
+
+
+def test_train_dt_dyn_tanh_task_matches_reference():
+    """The CLI's bundled train-dt configuration (tanh model, lambda = 0.5 through the Dual tanh relaxations)."""
+    from paper_2605_25346_b200.api import TrainConfig
+    model, data = _tanh_case()
+    cfg = TrainConfig(horizon_max=3, eps0=0.1, eps_final=0.01, lambda_=0.5, iters=3, batch=4, lr=1e-3, seed=0)
+    net, rows = train_dt_dyn(model, cfg, data)
+    pe, rows_e, rc = ref_train_dt_dyn(model, cfg, data)
+    assert rc == 0 and len(rows) == len(rows_e)
+    for a, b in zip(rows, rows_e):
+        assert (a.iter, a.t_h, a.eps, a.diverged_count) == (b.iter, b.t_h, b.eps, b.diverged_count)
+        for x, y in ((a.l_pred, b.l_pred), (a.l_reach, b.l_reach), (a.l_total, b.l_total)):
+            assert abs(x - y) <= 1e-10 * max(abs(y), 1e-300)
+    du, de = net.params() - model.params(), pe - model.params()
+    assert float(np.max(np.abs(du - de))) <= 1e-6 * float(np.max(np.abs(de)))
