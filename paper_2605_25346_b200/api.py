@@ -281,7 +281,7 @@ def dt_interval_baseline(sys: DTSystem, x0, actions: Sequence, ctx: Optional[Con
 
 
 def dt_reach_batch(sys: DTSystem, x0s: Sequence, action_seqs: Sequence, prm: DTReachParams = DTReachParams(),
-                   ctx: Optional[Context] = None) -> List[ReachTube]:
+                   ctx: Optional[Context] = None, precision: str = "exact") -> List[ReachTube]:
     """dt_reach_batch (dt_reach.hpp:108-125): x0s = [(lo, hi), ...], action_seqs = [[u_0..u_{H-1}], ...]."""
     if len(x0s) != len(action_seqs):
         raise ValueError("dt_reach_batch: batch size mismatch")
@@ -292,13 +292,13 @@ def dt_reach_batch(sys: DTSystem, x0s: Sequence, action_seqs: Sequence, prm: DTR
     hi = np.array([np.asarray(b[1], np.float64) for b in x0s])
     H = len(action_seqs[0])
     acts = _actions_array(action_seqs, B, H, sys.m)
-    return dt_reach_batch_arrays(sys, lo, hi, acts, prm, ctx).tubes()
+    return dt_reach_batch_arrays(sys, lo, hi, acts, prm, ctx, precision=precision).tubes()
 
 
 def dt_reach(sys: DTSystem, x0, actions: Sequence, prm: DTReachParams = DTReachParams(),
-             ctx: Optional[Context] = None) -> ReachTube:
+             ctx: Optional[Context] = None, precision: str = "exact") -> ReachTube:
     """dt_reach (dt_reach.hpp:40-104): x0 = (lo, hi)."""
-    return dt_reach_batch(sys, [x0], [actions], prm, ctx)[0]
+    return dt_reach_batch(sys, [x0], [actions], prm, ctx, precision)[0]
 
 
 # ---------------------------------------------------------------------------
@@ -696,9 +696,9 @@ def reach_split_hull(sys: DTSystem, x0, plan: SplitPlan, actions, prm: DTReachPa
 
 
 def reach_with_splitting(sys: DTSystem, x0, plan: SplitPlan, actions, prm: DTReachParams = DTReachParams(),
-                         ctx: Optional[Context] = None) -> ReachTube:
+                         ctx: Optional[Context] = None, precision: str = "exact") -> ReachTube:
     """reach_with_splitting(dt_reach engine, x0, plan) (refine.hpp:121-160)."""
-    return reach_split_hull(sys, x0, plan, actions, prm, ctx=ctx).tube()
+    return reach_split_hull(sys, x0, plan, actions, prm, ctx=ctx, precision=precision).tube()
 
 
 # ---------------------------------------------------------------------------

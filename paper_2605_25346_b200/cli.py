@@ -148,11 +148,13 @@ def cmd_reach_dt(cfg: dict, out_dir: str) -> int:
     split = cfg.get("split", "")
     if baseline and split:
         raise ConfigError("--baseline interval with --split: the split engine is dt_reach on the device")
+    precision = cfg.get("precision", "exact")  # device precision mode (not a reference option)
     if baseline:
         tube = dt_interval_baseline(sys_, x0, actions)
+    elif split:
+        tube = reach_with_splitting(sys_, x0, make_split_plan(split, n), actions, precision=precision)
     else:
-        tube = dt_reach(sys_, x0, actions) if not split else reach_with_splitting(sys_, x0,
-                                                                                  make_split_plan(split, n), actions)
+        tube = dt_reach(sys_, x0, actions, precision=precision)
     out = Outputs()
     emit_tube(out, tube, False)
     return finish("reach-dt", cfg, out_dir, out, tube.diverged, tube.failure_reason)
@@ -288,6 +290,8 @@ def main(argv=None) -> int:
     c.add_argument("--net", required=True)
     c.add_argument("--actions", default="")
     c.add_argument("--baseline", default="")
+    c.add_argument("--precision", default="exact", choices=["exact", "fused", "tc"],
+                   help="device precision mode: exact (the reference bit for bit), fused (fp64 DFMA), tc (tensor cores)")
     common_reach(c, False)
     c = sub.add_parser("reach-cl")
     c.add_argument("--system", required=True)
@@ -350,6 +354,8 @@ def main(argv=None) -> int:
             raise ValueError("split requires --split")
         if name in ("reach-dt", "reach-cl", "refine"):
             cfg["net"] = F.read_json_file(a.net)
+            if getattr(a, "precision", "exact") != "exact":
+                cfg["precision"] = a.precision  # recorded in the manifest only when not the default
         if name == "reach-dt" and a.actions:
             cfg["actions"] = F.read_json_file(a.actions)
         if name == "reach-cl":

@@ -323,6 +323,9 @@ int plan_wide(reach_ctx* ctx, const reach_net* net, int n, int m, int window, lo
 // (RB_FORCE_WIDE=1 forces the wide family, for parity runs of both).
 int plan_dt(reach_ctx* ctx, const reach_net* net, int n, int m, int window, long long B, rb::DTParams& P,
             DTLayout& lay, const reach_net* ctl = nullptr, int prec = REACH_PREC_EXACT) {
+  // a network without a hidden layer has no Lambda.W contraction for the tensor cores (only the prepended
+  // [A | I] layer): the tensor-core mode is then the exact mode
+  if (prec == REACH_PREC_TC && net->L < 2 && (!ctl || ctl->L < 2)) prec = REACH_PREC_EXACT;
   if (prec == REACH_PREC_TC) {
     const int rc = plan_wide(ctx, net, n, m, window, B, P, lay, ctl);
     if (rc) return rc;

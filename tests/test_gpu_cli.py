@@ -101,3 +101,20 @@ def test_refine_subcommand_matches_reference(tmp_path):
         x = c if target == "center" else np.zeros(12)
         exp = ref_refine_tube_volume(sys_, c, 0.05, acts, 0 if target == "center" else 1, x - 0.5, x + 0.5, 5, x)
         assert rj["x"] == list(exp[0]) and rj["objective"] == exp[2] and rj["accepted_steps"] == exp[5]
+
+
+@pytest.mark.parametrize("precision", ["fused", "tc"])
+def test_reach_dt_precision_modes(tmp_path, precision):
+    """reach-dt --precision fused|tc: the golden example within rtol 1e-5 of the exact tube; the manifest
+    records the mode, and a rerun reproduces it byte for byte."""
+    a, b = str(tmp_path / "a"), str(tmp_path / "b")
+    args = ["reach-dt", "--net", golden_net(str(tmp_path)), "--x0-center", "0.5,0.5", "--eps", "0.125", "--steps", "8",
+            "--precision", precision, "--out", a]
+    assert run_cli(args, str(tmp_path)) == 0
+    got = np.array([[float(v) for v in line.split(",")] for line in read(os.path.join(a, "tube.csv")).splitlines()[1:]])
+    exp = np.array([[float(v) for v in line.split(",")] for line in golden_csv().splitlines()[1:]])
+    assert got.shape == exp.shape
+    assert float(np.max(np.abs(got - exp))) <= 1e-5 * float(np.max(np.abs(exp)))
+    assert json.loads(read(os.path.join(a, "manifest.json")))["config"]["precision"] == precision
+    assert run_cli(["rerun", "--manifest", os.path.join(a, "manifest.json"), "--out", b], str(tmp_path)) == 0
+    assert read(os.path.join(a, "tube.csv")) == read(os.path.join(b, "tube.csv"))
