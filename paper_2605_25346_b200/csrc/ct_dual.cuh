@@ -3,9 +3,9 @@
 // (refine.hpp:186-207) evaluates it -- one Dual pass of cl_reach (closed_loop.hpp:76-182) per seeded
 // parameter and episode.
 //
-// One warp per (pass p, episode e); its working set (~200 KB) in global memory (L1 / L2 resident) with 8
-// persistent passes per SM (ctl_reach_loss_grad_kernel_g, the default: 2.9x the one-pass-per-SM
-// shared-memory variant ctl_reach_loss_grad_kernel, RB_CTD_SLOTS_PER_SM=0):
+// One warp per (pass p, episode e); its working set (~200 KB) in global memory (L1 / L2 resident) with 12
+// persistent passes per SM (ctl_reach_loss_grad_kernel_g, the default: 3.6x the one-pass-per-SM
+// shared-memory variant ctl_reach_loss_grad_kernel, RB_CTD_SLOTS_PER_SM=0; swept 8 / 10 / 12 / 14 / 16 / 24):
 //   * TMExpr<Dual> rows (taylor_model.hpp:197-445) with the generator columns lane-strided
 //     (lane L owns columns L, L+32, L+64); the scalar parts (c, at, the remainder interval) are
 //     computed by every lane alike and stored by lane 0; abs-sums are warp reductions;
@@ -45,6 +45,9 @@ using dual::imid;
 using dual::irad;
 using dual::iscale;  // interval.hpp:80-84
 
+#ifndef RB_CTD_MIN_BLOCKS
+#define RB_CTD_MIN_BLOCKS 12  // passes per SM the global-memory variant is compiled for (<= 170 registers)
+#endif
 constexpr int MZ = 96;  // generator columns (n + l + window * (n + l) <= 96)
 constexpr int MR = 16;  // rows of the augmented state (n + l)
 constexpr int CW = 128; // widest controller layer
@@ -881,7 +884,7 @@ __global__ void __launch_bounds__(32, 1) ctl_reach_loss_grad_kernel(const CtlLos
 
 // Working set in global memory (L1 / L2 resident), one Work slot per CTA, CTAs persistent over the
 // (pass, episode) pairs: several latency-bound passes per SM instead of one.
-__global__ void __launch_bounds__(32) ctl_reach_loss_grad_kernel_g(const CtlLossArgs A, Work* ws, long long total) {
+__global__ void __launch_bounds__(32, RB_CTD_MIN_BLOCKS) ctl_reach_loss_grad_kernel_g(const CtlLossArgs A, Work* ws, long long total) {
   Work& W = ws[blockIdx.x];
   for (long long q = blockIdx.x; q < total; q += gridDim.x)
     ctl_pass(A, W, static_cast<int>(q / A.M), static_cast<int>(q % A.M));

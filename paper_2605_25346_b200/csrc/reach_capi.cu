@@ -2547,7 +2547,7 @@ int reach_ctl_reach_loss(reach_ctx* ctx, const reach_net* ctl, const reach_cl_sp
   A.diverged = reinterpret_cast<int*>(w + o_dv);
   const size_t smem = sizeof(cd::Work);
   // RB_CTD_SLOTS_PER_SM > 0: the working sets in global memory, that many persistent passes per SM
-  const int slots_per_sm = env_int("RB_CTD_SLOTS_PER_SM", 8, 0, 64);
+  const int slots_per_sm = env_int("RB_CTD_SLOTS_PER_SM", 12, 0, 64);
   cudaEvent_t stop;
   if (slots_per_sm > 0) {
     const long long total = P * M;
