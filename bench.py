@@ -174,6 +174,13 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout: float = 3.0):
+        """Block until nvidia-smi has produced its first sample, so the sampling covers the timed region
+        from its start (the tool takes a few hundred ms to come up; a short timed region could see none)."""
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+
     def stop(self):
         if self.proc is None:
             return None
@@ -742,6 +749,7 @@ def main():
     launches0 = ctx.launch_count
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.wait_first()
     step_ms = []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
