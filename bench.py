@@ -472,6 +472,22 @@ def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
     return out
 
 
+TC_INT8_PEAK_TOPS = 4500.0  # B200 dense int8 tensor-core peak (nominal; tools/mma_rate.py measures 8185 MAC/clk/SM)
+
+
+def tc_int8_macs_per_step(nets):
+    """int8 MACs the tensor-core mode (dt_tcw_kernel) issues per reach-step: for each certified net (dims,
+    output rows) ceil(n_o / 24) passes, each with ceil(dims[l] / 128) M tiles x ceil(dims[l+1] / 32) K
+    steps x 39 Ozaki slice pairs per contraction l = L-2 .. 0, every MMA 128 x 24 x 32."""
+    total = 0
+    for dims in nets:
+        L = len(dims) - 1
+        thirds = -(-dims[-1] // 24)
+        per = sum(-(-dims[l] // 128) * -(-dims[l + 1] // 32) for l in range(L - 1))
+        total += thirds * per * 39 * 128 * 24 * 32
+    return total
+
+
 def c5_flops_per_step():
     """SURVEY §8d formula for C5 (72-D, 3x256 ReLU dynamics + controller): controller
     certification over nz = 5n + 2l = 396 generators, dynamics certification over the stacked
@@ -542,6 +558,12 @@ def closed_loop_legs(args, ctx, world, rank, dev, barrier, stream):
                 a = fl * B * w.horizon / (ms / 1e3) / 1e12
                 modes[prec]["tflops"] = a
                 modes[prec]["frac_dfma_peak"] = a / tf_fma
+            else:
+                tops = 2.0 * tc_int8_macs_per_step([[int(x) for x in w.dyn.dims()], [int(x) for x in w.ctl.dims()]]) \
+                    * B * w.horizon / (ms / 1e3) / 1e12
+                modes[prec]["int8_tops"] = tops
+                modes[prec]["frac_int8_dense_peak"] = tops / TC_INT8_PEAK_TOPS
+                modes[prec]["peak_source"] = "B200 dense int8 nominal 4.5 POPS; ncu tensor pipe 3.2 % (profiles)"
         except Exception as ex:  # noqa: BLE001
             modes[prec] = {"error": str(ex)}
     c5["modes"] = modes
@@ -849,7 +871,10 @@ def main():
     if not args.no_tc:
         try:
             tc_ms, tc_tf = mode_time(A.REACH_PREC_TC, 1)
+            tops = 2.0 * tc_int8_macs_per_step([netdims]) * per_rank * H / (tc_ms / 1e3) / 1e12
             modes["tc"] = {"kernel_ms": tc_ms, "reach_steps_per_s": reach_steps / (tc_ms / 1e3), "tflops_fp64_equiv": tc_tf,
+                           "int8_tops": tops, "frac_int8_dense_peak": tops / TC_INT8_PEAK_TOPS,
+                           "peak_source": "B200 dense int8 nominal 4.5 POPS",
                            "kernel": "rb::dt_tcw_kernel (CTA per sub-box, tcgen05.mma kind::i8 Ozaki contractions)"}
         except Exception as ex:  # noqa: BLE001
             modes["tc"] = {"error": str(ex)}
