@@ -58,16 +58,15 @@ struct Program {
   std::vector<TOp> ops;
   double kc[rb::ct::kMaxKc] = {};
 };
-constexpr unsigned char P_(int i) { return static_cast<unsigned char>(i); }
-constexpr unsigned char T_(int i) { return static_cast<unsigned char>(rb::ct::SLOT_T + i); }
-constexpr unsigned char V_(int i) { return static_cast<unsigned char>(rb::ct::SLOT_V + i); }
-constexpr unsigned char C_(int i) { return static_cast<unsigned char>(rb::ct::SLOT_C + i); }
+using rb::ct::C_;
+using rb::ct::P_;
+using rb::ct::T_;
+using rb::ct::V_;
 
 // quadrotor_ode (systems.hpp:24-64) with the input rows u: the augmented rows
 // P12..15 (make_augmented_field, fields.hpp:96-107: cl_reach) or held
-// constants (quadrotor_field, fields.hpp:20-32,51-56: ct_reach).  Each dx_i is
-// consumed once neither P_i nor a view of it is read again, so the consumer
-// may overwrite P_i (poly_picard's in-place update).
+// constants (quadrotor_field, fields.hpp:20-32,51-56: ct_reach); the entries
+// are RB_CT_QUAD_OPS (ct_kernel.cuh), which the scalar-only replay compiles.
 Program quad_program(const double* prm, const double* u_held) {
   using namespace rb::ct;
   Program p;
@@ -87,43 +86,9 @@ Program quad_program(const double* prm, const double* u_held) {
       p.kc[8 + k] = u_held[k];
       o.push_back({OP_CONST, C_(k), 0, static_cast<unsigned char>(8 + k)});
     }
-  o.insert(o.end(), {
-      {OP_CONS, 0, P_(3), 0}, {OP_CONS, 1, P_(4), 0}, {OP_CONS, 2, P_(5), 0},  // dx0..2 = v
-      {OP_SIN, V_(0), P_(6), 0}, {OP_COS, V_(1), P_(6), 0},                     // sphi, cphi
-      {OP_SIN, V_(2), P_(7), 0}, {OP_COS, V_(3), P_(7), 0},                     // sth, cth
-      {OP_SIN, V_(4), P_(8), 0}, {OP_COS, V_(5), P_(8), 0},                     // spsi, cpsi
-      {OP_SCALE, V_(6), U(0), 0},                                               // a = u0 * (1/mass)
-      // independent products run in pairs (OP_MUL2 + the OP_MUL after it); the
-      // expression trees are unchanged, only their schedule
-      {OP_MUL2, T_(0), V_(1), V_(2)}, {OP_MUL, T_(1), V_(0), V_(4)},            // cs = cphi*sth, sphi*spsi
-      {OP_MUL2, T_(2), T_(0), V_(5)}, {OP_MUL, T_(3), T_(0), V_(4)},            // cs*cpsi, cs*spsi
-      {OP_ADD, T_(2), T_(2), T_(1)},                                            // b3x
-      {OP_MUL2, T_(1), V_(0), V_(5)}, {OP_MUL, T_(0), V_(1), V_(3)},            // sphi*cpsi, b3z = cphi*cth
-      {OP_SUB, T_(3), T_(3), T_(1)},                                            // b3y
-      {OP_MUL2, T_(1), V_(6), T_(2)}, {OP_MUL, T_(2), V_(6), T_(3)},            // dx3 = a*b3x, dx4 = a*b3y
-      {OP_CONS, 3, T_(1), 0}, {OP_CONS, 4, T_(2), 0},
-      {OP_INV, V_(7), V_(3), 0},                                                // tme_inv(cth)
-      {OP_MUL2, T_(3), V_(6), T_(0)}, {OP_MUL, T_(1), V_(2), V_(7)},            // a*b3z, tth = sth / cth
-      {OP_SUBK, T_(3), 0, 1},                                                   // - gravity
-      {OP_CONS, 5, T_(3), 0},
-      {OP_MUL2, T_(2), V_(0), T_(1)}, {OP_MUL, T_(3), V_(1), T_(1)},            // sphi*tth, cphi*tth
-      {OP_MUL2, T_(2), T_(2), P_(10)}, {OP_MUL, T_(3), T_(3), P_(11)},          // *q, *r
-      {OP_ADD, T_(2), P_(9), T_(2)},                                            // p + ...
-      {OP_ADD, T_(2), T_(2), T_(3)},                                            // dx6 (held)
-      {OP_MUL2, T_(0), V_(1), P_(10)}, {OP_MUL, T_(1), V_(0), P_(11)},          // cphi*q, sphi*r
-      {OP_SUB, T_(0), T_(0), T_(1)},                                            // dx7 (held)
-      {OP_MUL2, T_(1), V_(0), V_(7)}, {OP_MUL, T_(3), V_(1), V_(7)},            // sphi/cth, cphi/cth
-      {OP_MUL2, T_(1), T_(1), P_(10)}, {OP_MUL, T_(3), T_(3), P_(11)},          // *q, *r
-      {OP_ADD, T_(1), T_(1), T_(3)},                                            // dx8
-      // the views of P6 / P7 (sphi, cphi, 1/cth) are dead only now: consume rows 6..8
-      {OP_CONS, 6, T_(2), 0}, {OP_CONS, 7, T_(0), 0}, {OP_CONS, 8, T_(1), 0},
-      {OP_MUL2, T_(0), P_(10), P_(11)}, {OP_MUL, T_(1), P_(9), P_(11)},         // q*r, p*r
-      {OP_MUL, T_(2), P_(9), P_(10)},                                           // p*q
-      {OP_SCALE, V_(8), T_(0), 2}, {OP_SCALE, V_(9), U(1), 3}, {OP_ADD, T_(0), V_(8), V_(9)},  // dx9
-      {OP_SCALE, V_(8), T_(1), 4}, {OP_SCALE, V_(9), U(2), 5}, {OP_ADD, T_(1), V_(8), V_(9)},  // dx10
-      {OP_SCALE, V_(8), T_(2), 6}, {OP_SCALE, V_(9), U(3), 7}, {OP_ADD, T_(2), V_(8), V_(9)},  // dx11
-      {OP_CONS, 9, T_(0), 0}, {OP_CONS, 10, T_(1), 0}, {OP_CONS, 11, T_(2), 0},
-  });
+#define RB_CT_TOP(c, d, a, b) TOp{c, static_cast<unsigned char>(d), static_cast<unsigned char>(a), static_cast<unsigned char>(b)},
+  o.insert(o.end(), {RB_CT_QUAD_OPS(RB_CT_TOP, U(0), U(1), U(2), U(3))});
+#undef RB_CT_TOP
   if (!u_held)
     for (int i = 12; i < 16; ++i) o.push_back({OP_CONS0, static_cast<unsigned char>(i), 0, 0});  // udot = 0
   o.push_back({OP_END, 0, 0, 0});
@@ -175,6 +140,7 @@ struct ProgramStore {
   std::map<std::pair<int, int>, int> offset;  // (kind, n) -> first op
   std::mutex mu;
   std::vector<char> uploaded = std::vector<char>(256, 0);
+  bool too_long = false;  // a program exceeds the flow kernel's replay cache (FlowSmem::fc)
 };
 constexpr int kKindQuadAug = 100;
 ProgramStore& program_store() {
@@ -184,6 +150,7 @@ ProgramStore& program_store() {
     auto add = [&](int kind, int n, const Program& p) {
       st->offset[{kind, n}] = static_cast<int>(st->ops.size());
       st->ops.insert(st->ops.end(), p.ops.begin(), p.ops.end());
+      if (p.ops.size() > static_cast<size_t>(rb::ct::kFieldCache) + 1) st->too_long = true;  // + OP_END
     };
     add(kKindQuadAug, 16, quad_program(prm, nullptr));
     add(REACH_FIELD_QUADROTOR, 12, quad_program(prm, u));
@@ -203,6 +170,7 @@ int ensure_programs(reach_ctx* ctx) {
   if (ctx->device < 0 || ctx->device >= static_cast<int>(st.uploaded.size())) return REACH_E_INVALID_ARGUMENT;
   if (st.uploaded[ctx->device]) return REACH_OK;
   if (st.ops.size() > static_cast<size_t>(rb::ct::kProgCap)) return fail(ctx, REACH_E_UNSUPPORTED, "program store full");
+  if (st.too_long) return fail(ctx, REACH_E_UNSUPPORTED, "field program longer than the flow kernel's replay cache");
   RB_CUDA(cudaMemcpyToSymbol(rb::ct::kProgs, st.ops.data(), st.ops.size() * sizeof(TOp)));
   st.uploaded[ctx->device] = 1;
   return REACH_OK;
@@ -214,6 +182,7 @@ int ensure_programs(reach_ctx* ctx) {
 void load_program(const Program& p, int kind, int na, rb::ct::CTParams& P) {
   using namespace rb::ct;
   P.prog = program_store().offset.at({kind, na});
+  P.fast_prog = kind == kKindQuadAug ? 1 : kind == REACH_FIELD_QUADROTOR ? 2 : 0;  // compiled scalar replays
   for (int i = 0; i < kMaxKc; ++i) P.kc[i] = p.kc[i];
   bool read[16] = {};
   for (const TOp& op : p.ops) {

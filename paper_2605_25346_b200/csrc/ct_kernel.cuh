@@ -83,6 +83,7 @@ struct CTParams {
   double prm[8];
   double kc[kMaxKc];         // constants of the field program
   int prog;                  // offset of the field program in kProgs
+  int fast_prog;             // scalar-only replays: 0 interpreted, 1 / 2 quad_fast<false / true>
   signed char bzsrc[16];     // Picard bz row of row i: -1 own storage, -2 the zero row, j >= 0 the seed row j
   DevNet ctl;
   const double* y_ref;  // device [ctl_steps][ref_dim]
@@ -175,6 +176,7 @@ __device__ __forceinline__ double wsum(double a) {
 //   C0..3     constant rows (tme_const of a held input, fields.hpp:28).
 constexpr int NTF = 4;
 constexpr int NV = 10;
+constexpr int kFieldCache = 64;  // program entries (before OP_END) a field program may have (FlowSmem::fc)
 constexpr int NCST = 4;
 constexpr int SLOT_T = NA;
 constexpr int SLOT_V = NA + NTF;
@@ -203,6 +205,7 @@ struct __align__(128) FlowSmem {
   int pbz[NA];     // Picard bz row offset of row i
   int own[NA];     // row i owns its bz row
   int wid[8];      // queue block widths (square fold)
+  double2 fc[kFieldCache];  // per program entry: the result's (abs_z, abs_b) / a consumer's replay sum
   int na, off_zero, off_pbz, off_taz, off_tbz, pad;
   __device__ __forceinline__ double* coef() { return reinterpret_cast<double*>(this + 1); }
 };
@@ -260,7 +263,66 @@ enum : unsigned char {
   OP_MUL, OP_ADD, OP_SUB, OP_SUBK, OP_SCALE, OP_SIN, OP_COS, OP_INV, OP_CONS, OP_CONS0, OP_COPY, OP_CONST, OP_END,
   OP_MUL2  // two independent products: this op (dst = a * b) and the next program entry, one interleaved pass
 };
-enum : int { MODE_PICARD = 0, MODE_REPLAY = 1, MODE_ENDPOINT = 2 };
+// Between the last Picard iteration and the endpoint the field is evaluated on
+// the same Picard iterate p_k with different remainder candidates only
+// (remainder_picard's enlarge / shrink replays and the exact endpoint,
+// flowpipe_ct.hpp:144-263).  No coefficient of any intermediate row depends on
+// a remainder, so the first replay of a step (MODE_REPLAY) runs the full
+// coefficient passes, caches every produced row's abs-sums (and each
+// consumer's |Int f - p_k| sum) in FlowSmem::fc and writes the endpoint rows
+// seed + h (f + h/2 f') to HBM; every later replay and the endpoint itself
+// (MODE_REPLAY_FAST, MODE_ENDPOINT) are scalar-only: the warp-uniform interval
+// chains on the cached sums, no coefficient pass, no shuffle reduction.  The
+// cached values are the ones the full pass would recompute, bit for bit.
+enum : int { MODE_PICARD = 0, MODE_REPLAY = 1, MODE_REPLAY_FAST = 2, MODE_ENDPOINT = 3 };
+
+// Slot indices of the field programs (ct_capi.cu builds them; the quadrotor's
+// scalar-only replay below is compiled from the same list).
+__host__ __device__ constexpr unsigned char P_(int i) { return static_cast<unsigned char>(i); }
+__host__ __device__ constexpr unsigned char T_(int i) { return static_cast<unsigned char>(SLOT_T + i); }
+__host__ __device__ constexpr unsigned char V_(int i) { return static_cast<unsigned char>(SLOT_V + i); }
+__host__ __device__ constexpr unsigned char C_(int i) { return static_cast<unsigned char>(SLOT_C + i); }
+
+// quadrotor_ode (systems.hpp:24-64) as a field program, U0..U3 the input
+// rows (the augmented P12..15 of cl_reach or the held constants C0..3 of
+// ct_reach).  X(code, dst, a, b) per entry; constants: kc[0] = 1/mass,
+// kc[1] = g, kc[2..7] the inertia ratios.  Each dx_i is consumed once neither
+// P_i nor a view of it is read again, so the consumer may overwrite P_i
+// (poly_picard's in-place update); independent products run in pairs
+// (OP_MUL2 + the OP_MUL after it), the expression trees unchanged.
+#define RB_CT_QUAD_OPS(X, U0, U1, U2, U3)                                                       \
+  X(OP_CONS, 0, P_(3), 0) X(OP_CONS, 1, P_(4), 0) X(OP_CONS, 2, P_(5), 0) /* dx0..2 = v */     \
+  X(OP_SIN, V_(0), P_(6), 0) X(OP_COS, V_(1), P_(6), 0)                   /* sphi, cphi */     \
+  X(OP_SIN, V_(2), P_(7), 0) X(OP_COS, V_(3), P_(7), 0)                   /* sth, cth */       \
+  X(OP_SIN, V_(4), P_(8), 0) X(OP_COS, V_(5), P_(8), 0)                   /* spsi, cpsi */     \
+  X(OP_SCALE, V_(6), U0, 0)                                               /* a = u0 / mass */  \
+  X(OP_MUL2, T_(0), V_(1), V_(2)) X(OP_MUL, T_(1), V_(0), V_(4))         /* cphi*sth, sphi*spsi */ \
+  X(OP_MUL2, T_(2), T_(0), V_(5)) X(OP_MUL, T_(3), T_(0), V_(4))         /* cs*cpsi, cs*spsi */ \
+  X(OP_ADD, T_(2), T_(2), T_(1))                                          /* b3x */            \
+  X(OP_MUL2, T_(1), V_(0), V_(5)) X(OP_MUL, T_(0), V_(1), V_(3))         /* sphi*cpsi, b3z */ \
+  X(OP_SUB, T_(3), T_(3), T_(1))                                          /* b3y */            \
+  X(OP_MUL2, T_(1), V_(6), T_(2)) X(OP_MUL, T_(2), V_(6), T_(3))         /* dx3, dx4 */       \
+  X(OP_CONS, 3, T_(1), 0) X(OP_CONS, 4, T_(2), 0)                                              \
+  X(OP_INV, V_(7), V_(3), 0)                                              /* tme_inv(cth) */   \
+  X(OP_MUL2, T_(3), V_(6), T_(0)) X(OP_MUL, T_(1), V_(2), V_(7))         /* a*b3z, tth */     \
+  X(OP_SUBK, T_(3), 0, 1)                                                 /* - gravity */      \
+  X(OP_CONS, 5, T_(3), 0)                                                                      \
+  X(OP_MUL2, T_(2), V_(0), T_(1)) X(OP_MUL, T_(3), V_(1), T_(1))         /* sphi*tth, cphi*tth */ \
+  X(OP_MUL2, T_(2), T_(2), P_(10)) X(OP_MUL, T_(3), T_(3), P_(11))       /* *q, *r */         \
+  X(OP_ADD, T_(2), P_(9), T_(2))                                          /* p + ... */        \
+  X(OP_ADD, T_(2), T_(2), T_(3))                                          /* dx6 (held) */     \
+  X(OP_MUL2, T_(0), V_(1), P_(10)) X(OP_MUL, T_(1), V_(0), P_(11))       /* cphi*q, sphi*r */ \
+  X(OP_SUB, T_(0), T_(0), T_(1))                                          /* dx7 (held) */     \
+  X(OP_MUL2, T_(1), V_(0), V_(7)) X(OP_MUL, T_(3), V_(1), V_(7))         /* sphi/cth, cphi/cth */ \
+  X(OP_MUL2, T_(1), T_(1), P_(10)) X(OP_MUL, T_(3), T_(3), P_(11))       /* *q, *r */         \
+  X(OP_ADD, T_(1), T_(1), T_(3))                                          /* dx8 */            \
+  X(OP_CONS, 6, T_(2), 0) X(OP_CONS, 7, T_(0), 0) X(OP_CONS, 8, T_(1), 0) /* views of P6..8 dead */ \
+  X(OP_MUL2, T_(0), P_(10), P_(11)) X(OP_MUL, T_(1), P_(9), P_(11))      /* q*r, p*r */       \
+  X(OP_MUL, T_(2), P_(9), P_(10))                                         /* p*q */            \
+  X(OP_SCALE, V_(8), T_(0), 2) X(OP_SCALE, V_(9), U1, 3) X(OP_ADD, T_(0), V_(8), V_(9)) /* dx9 */  \
+  X(OP_SCALE, V_(8), T_(1), 4) X(OP_SCALE, V_(9), U2, 5) X(OP_ADD, T_(1), V_(8), V_(9)) /* dx10 */ \
+  X(OP_SCALE, V_(8), T_(2), 6) X(OP_SCALE, V_(9), U3, 7) X(OP_ADD, T_(2), V_(8), V_(9)) /* dx11 */ \
+  X(OP_CONS, 9, T_(0), 0) X(OP_CONS, 10, T_(1), 0) X(OP_CONS, 11, T_(2), 0)
 
 // Remainder of operator* (taylor_model.hpp:337-359): the excess terms bounded
 // over the domain and the remainder interactions, from the operands' scalars.
@@ -415,39 +477,98 @@ __device__ __forceinline__ void make_view(Slot& r, const Slot& u, double s) {
   }
 }
 
+// Scalar-only forms of the stored-row operations for the fast replays: the
+// result's scalars from its operands' scalars, its abs-sums from the cache.
+// Every operand scalar is read before the result is written (r may alias).
+__device__ __forceinline__ void mul_fast(Slot& r, const Slot& u, const Slot& v, double2 sums, double h) {
+  const double uc = u.c, vc = v.c, uat = u.at, vat = v.at;
+  const Iv rem = mul_rem(uc, vc, uat, vat, u.sz, v.sz, u.sb, v.sb, Iv{u.rlo, u.rhi}, Iv{v.rlo, v.rhi}, h);
+  set_scalars(r, uc * vc, uc * vat + vc * uat, rem, sums.x, sums.y);
+}
+__device__ __forceinline__ void mul2_fast(Slot& r, const Slot& u, const Slot& v, double2 rs, Slot& q, const Slot& x,
+                                          const Slot& y, double2 qs, double h) {
+  const double uc = u.c, vc = v.c, uat = u.at, vat = v.at, xc = x.c, yc = y.c, xat = x.at, yat = y.at;
+  const Iv rr = mul_rem(uc, vc, uat, vat, u.sz, v.sz, u.sb, v.sb, Iv{u.rlo, u.rhi}, Iv{v.rlo, v.rhi}, h);
+  const Iv qr = mul_rem(xc, yc, xat, yat, x.sz, y.sz, x.sb, y.sb, Iv{x.rlo, x.rhi}, Iv{y.rlo, y.rhi}, h);
+  set_scalars(r, uc * vc, uc * vat + vc * uat, rr, rs.x, rs.y);
+  set_scalars(q, xc * yc, xc * yat + yc * xat, qr, qs.x, qs.y);
+}
+__device__ __forceinline__ void addsub_fast(Slot& r, const Slot& a, const Slot& b, bool sub, double2 sums) {
+  const double c = sub ? a.c - b.c : a.c + b.c;
+  const double at = sub ? a.at - b.at : a.at + b.at;
+  const Iv rem = sub ? isub(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi}) : iadd(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi});
+  set_scalars(r, c, at, rem, sums.x, sums.y);
+}
+
 // The field program on the slots; `mode` selects what CONS does with dx_i:
-//   PICARD    g_i = seed_i + Int dx_i written over P_i (flowpipe_ct.hpp:130-133)
-//   REPLAY    I1_i = range(seed_i + Int dx_i - p_k,i) (:154-165)
-//   ENDPOINT  x(h)_i = seed_i + h (dx_i(0) + h/2 dx_i') to the state's HBM rows (:241-257)
+//   PICARD        g_i = seed_i + Int dx_i written over P_i (flowpipe_ct.hpp:130-133)
+//   REPLAY(_FAST) I1_i = range(seed_i + Int dx_i - p_k,i) (:154-165); the full
+//                 replay also writes x(h)_i's rows seed_i + h (dx_i + h/2 dx_i')
+//                 to the state's HBM rows (:241-257)
+//   ENDPOINT      x(h)_i's centre and remainder (scalar-only)
 // Returns the tme_inv "throw" (taylor_model.hpp:367-368).
 __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const Lane L, double* gM) {
   bool thrown = false;
   const double h = L.h;
   const int lane = L.lane;
+  const bool fast = mode >= MODE_REPLAY_FAST, record = mode == MODE_REPLAY;
   double* coef = W.coef();
+  double2* fc = W.fc;  // indexed by pc - prog
   TOp next = kProgs[prog];
   for (int pc = prog;; ++pc) {
     const TOp op = next;
     if (op.code == OP_END) break;
     next = kProgs[pc + 1];  // dispatch of the next op overlaps this one
     switch (op.code) {
-      case OP_MUL:
-        op_mul(coef, W.D[op.dst], W.D[op.a], W.D[op.b], L);
+      case OP_MUL: {
+        Slot& r = W.D[op.dst];
+        if (fast) {
+          mul_fast(r, W.D[op.a], W.D[op.b], fc[pc - prog], h);
+        } else {
+          op_mul(coef, r, W.D[op.a], W.D[op.b], L);
+          if (record && lane == 0) fc[pc - prog] = make_double2(r.sz, r.sb);
+        }
         break;
+      }
       case OP_MUL2: {  // this entry and the next one (an OP_MUL) as one pass
         const TOp o2 = next;
         ++pc;
         next = kProgs[pc + 1];
-        op_mul2(coef, W.D[op.dst], W.D[op.a], W.D[op.b], W.D[o2.dst], W.D[o2.a], W.D[o2.b], L);
+        Slot& r = W.D[op.dst];
+        Slot& q = W.D[o2.dst];
+        if (fast) {
+          mul2_fast(r, W.D[op.a], W.D[op.b], fc[pc - 1 - prog], q, W.D[o2.a], W.D[o2.b], fc[pc - prog], h);
+        } else {
+          op_mul2(coef, r, W.D[op.a], W.D[op.b], q, W.D[o2.a], W.D[o2.b], L);
+          if (record && lane == 0) {
+            fc[pc - 1 - prog] = make_double2(r.sz, r.sb);
+            fc[pc - prog] = make_double2(q.sz, q.sb);
+          }
+        }
         break;
       }
       case OP_ADD:
-      case OP_SUB:
-        op_addsub(coef, W.D[op.dst], W.D[op.a], W.D[op.b], op.code == OP_SUB, L);
+      case OP_SUB: {
+        Slot& r = W.D[op.dst];
+        if (fast) {
+          addsub_fast(r, W.D[op.a], W.D[op.b], op.code == OP_SUB, fc[pc - prog]);
+        } else {
+          op_addsub(coef, r, W.D[op.a], W.D[op.b], op.code == OP_SUB, L);
+          if (record && lane == 0) fc[pc - prog] = make_double2(r.sz, r.sb);
+        }
         break;
-      case OP_COPY:
-        op_copy(coef, W.D[op.dst], W.D[op.a], L);
+      }
+      case OP_COPY: {
+        Slot& r = W.D[op.dst];
+        if (fast) {
+          const Slot& a = W.D[op.a];
+          set_scalars(r, a.c, a.at, Iv{a.rlo, a.rhi}, fc[pc - prog].x, fc[pc - prog].y);
+        } else {
+          op_copy(coef, r, W.D[op.a], L);
+          if (record && lane == 0) fc[pc - prog] = make_double2(r.sz, r.sb);
+        }
         break;
+      }
       case OP_SUBK:
         W.D[op.dst].c = W.D[op.dst].c - W.kc[op.b];
         break;
@@ -509,21 +630,13 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
         const bool zero = op.code == OP_CONS0;
         const Slot& f = W.D[zero ? 0 : op.a];
         const Opnd F = opnd(coef, f);
-        const double fc = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at;
+        const double fc_ = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at;
         const double fsz = zero ? 0.0 : f.sz, fsb = zero ? 0.0 : f.sb;
         const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
         const double* S = coef + i * NZP;
         double* Pb = coef + W.pbz[i];
-        if (mode == MODE_ENDPOINT) {
-#pragma unroll
-          for (int k = 0; k < NZC; ++k) {
-            if (!L.act[k]) continue;
-            const int j = lane + 32 * k;
-            double fa = 0.0, fb = 0.0;
-            if (!zero) fetch(F, j, fa, fb);
-            gM[i * NZP + j] = S[j] + h * (fa + fb * h * 0.5);
-          }
-          W.ec[i] = W.sc[i] + h * (fc + fat * h * 0.5);
+        if (mode == MODE_ENDPOINT) {  // the rows were written by this step's full replay
+          W.ec[i] = W.sc[i] + h * (fc_ + fat * h * 0.5);
           W.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
           break;
         }
@@ -544,21 +657,28 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
               Pb[j] = fa;
             }
           }
-          set_scalars(W.D[i], W.sc[i], fc, rem, W.ssz[i], fsz);
+          set_scalars(W.D[i], W.sc[i], fc_, rem, W.ssz[i], fsz);
         } else {  // REPLAY: (seed + Int f) - p_k; its z part seed - p_k.az is exactly 0
-          double s2 = 0.0;
+          double s2;
+          if (fast) {
+            s2 = fc[pc - prog].x;
+          } else {
+            s2 = 0.0;
 #pragma unroll
-          for (int k = 0; k < NZC; ++k) {
-            if (!L.act[k]) continue;
-            const int j = lane + 32 * k;
-            double fa = 0.0, fb;
-            if (!zero) fetch(F, j, fa, fb);
-            s2 += fabs(fa - Pb[j]);
+            for (int k = 0; k < NZC; ++k) {
+              if (!L.act[k]) continue;
+              const int j = lane + 32 * k;
+              double fa = 0.0, fb = 0.0;
+              if (!zero) fetch(F, j, fa, fb);
+              s2 += fabs(fa - Pb[j]);
+              gM[i * NZP + j] = S[j] + h * (fa + fb * h * 0.5);  // the endpoint row (:241-257)
+            }
+            s2 = wsum(s2);
+            if (lane == 0) fc[pc - prog] = make_double2(s2, 0.0);
           }
-          s2 = wsum(s2);
           const Slot& pk = W.D[i];
           const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
-          W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc - pk.at, s2, h), rem);
+          W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, s2, h), rem);
         }
         break;
       }
@@ -566,6 +686,115 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
         break;
     }
   }
+  return thrown;
+}
+
+// The quadrotor program's scalar-only replay / endpoint (MODE_REPLAY_FAST,
+// MODE_ENDPOINT) compiled from RB_CT_QUAD_OPS instead of interpreted: the slot
+// scalars live in registers (compile-time slot indices) and the compiler
+// schedules the program's independent chains side by side (sin / cos of the
+// three angles, the two product trees, dx9..11) instead of one interpreted
+// operation after another.  Each operation is run_field's fast form, operand
+// order included; the abs-sums come from this step's full replay (FlowSmem::fc).
+struct FS {
+  double c, at, rlo, rhi, sz, sb;
+};
+template <int CODE, int DST, int A, int B>
+__device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, int pc, int mode, double h, bool& thrown) {
+  if constexpr (CODE == OP_MUL || CODE == OP_MUL2) {  // the pair's second entry follows as an OP_MUL
+    const FS u = D[A], v = D[B];
+    const double2 s = W.fc[pc];
+    const Iv rem = mul_rem(u.c, v.c, u.at, v.at, u.sz, v.sz, u.sb, v.sb, Iv{u.rlo, u.rhi}, Iv{v.rlo, v.rhi}, h);
+    D[DST] = FS{u.c * v.c, u.c * v.at + v.c * u.at, rem.lo, rem.hi, s.x, s.y};
+  } else if constexpr (CODE == OP_ADD || CODE == OP_SUB) {
+    const FS a = D[A], b = D[B];
+    const double2 s = W.fc[pc];
+    const bool sub = CODE == OP_SUB;
+    const Iv rem = sub ? isub(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi}) : iadd(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi});
+    D[DST] = FS{sub ? a.c - b.c : a.c + b.c, sub ? a.at - b.at : a.at + b.at, rem.lo, rem.hi, s.x, s.y};
+  } else if constexpr (CODE == OP_SUBK) {
+    D[DST].c = D[DST].c - W.kc[B];
+  } else if constexpr (CODE == OP_CONST) {
+    D[DST] = FS{W.kc[B], 0.0, 0.0, 0.0, 0.0, 0.0};
+  } else if constexpr (CODE == OP_SCALE) {
+    const FS u = D[A];
+    const double s = W.kc[B];
+    const Iv rem = iscale(s, Iv{u.rlo, u.rhi});
+    D[DST] = FS{u.c * s, u.at * s, rem.lo, rem.hi, fabs(s) * u.sz, fabs(s) * u.sb};
+  } else if constexpr (CODE == OP_SIN || CODE == OP_COS) {
+    const FS u = D[A];
+    const double m = u.c;
+    const Iv range = iadd(poly_range(u.c, u.sz, u.at, u.sb, h), Iv{u.rlo, u.rhi});
+    const double rad = smax(fabs(range.lo - m), fabs(range.hi - m));
+    const double err = rad * rad * 0.5;
+    double sm, cm;
+    sincos(m, &sm, &cm);
+    constexpr bool isc = CODE == OP_COS;
+    const double s = isc ? -sm : cm;
+    Iv rem = iscale(s, Iv{u.rlo, u.rhi});
+    rem = iadd(rem, Iv{-err, err});
+    D[DST] = FS{(m - m) * s + (isc ? cm : sm), u.at * s, rem.lo, rem.hi, fabs(s) * u.sz, fabs(s) * u.sb};
+  } else if constexpr (CODE == OP_INV) {
+    const FS v = D[A];
+    const Iv range = iadd(poly_range(v.c, v.sz, v.at, v.sb, h), Iv{v.rlo, v.rhi});
+    if (range.lo <= 0.0 && range.hi >= 0.0) thrown = true;
+    const double m = v.c, mm = m * m;
+    const double e_lo = 1.0 / range.lo - (2.0 / m - range.lo / mm);
+    const double e_hi = 1.0 / range.hi - (2.0 / m - range.hi / mm);
+    const Iv e{smin(smin(e_lo, e_hi), 0.0), smax(smax(e_lo, e_hi), 0.0)};
+    const double s = -1.0 / mm;
+    Iv rem = iscale(s, Iv{v.rlo, v.rhi});
+    rem = iadd(rem, e);
+    D[DST] = FS{v.c * s + 2.0 / m, v.at * s, rem.lo, rem.hi, fabs(s) * v.sz, fabs(s) * v.sb};
+  } else if constexpr (CODE == OP_CONS || CODE == OP_CONS0) {
+    constexpr int i = DST;
+    constexpr bool zero = CODE == OP_CONS0;
+    const FS f = D[zero ? 0 : A];
+    const double fc_ = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at, fsb = zero ? 0.0 : f.sb;
+    const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
+    if (mode == MODE_ENDPOINT) {
+      W.ec[i] = W.sc[i] + h * (fc_ + fat * h * 0.5);
+      W.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
+    } else {
+      const double half_at = fat * 0.5;
+      Iv rem = imul_0h(h * h, half_at);
+      const double bb = fsb * h * h * 0.5;
+      rem = iadd(rem, Iv{-bb, bb});
+      rem = iadd(rem, imul(fr, Iv{0.0, h}));
+      const FS pk = D[i];
+      const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
+      W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, W.fc[pc].x, h), rem);
+    }
+  }
+}
+
+// HELD: ct_reach's quadrotor field (inputs C0..3 from kc[8..11], four OP_CONST
+// entries first); else cl_reach's augmented field (inputs P12..15, udot = 0).
+template <bool HELD>
+__device__ __noinline__ bool quad_fast(FlowSmem& W, int mode, double h) {
+  FS D[NSLOT];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) {
+    const Slot& p = W.D[i];
+    D[i] = FS{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb};
+  }
+  bool thrown = false;
+  int pc = 0;
+#define RB_CT_FAST_OP(c, d, a, b) fast_op<c, d, a, b>(D, W, pc++, mode, h, thrown);
+  if constexpr (HELD) {
+    RB_CT_FAST_OP(OP_CONST, C_(0), 0, 8)
+    RB_CT_FAST_OP(OP_CONST, C_(1), 0, 9)
+    RB_CT_FAST_OP(OP_CONST, C_(2), 0, 10)
+    RB_CT_FAST_OP(OP_CONST, C_(3), 0, 11)
+    RB_CT_QUAD_OPS(RB_CT_FAST_OP, C_(0), C_(1), C_(2), C_(3))
+  } else {
+    RB_CT_QUAD_OPS(RB_CT_FAST_OP, P_(12), P_(13), P_(14), P_(15))
+    RB_CT_FAST_OP(OP_CONS0, 12, 0, 0)
+    RB_CT_FAST_OP(OP_CONS0, 13, 0, 0)
+    RB_CT_FAST_OP(OP_CONS0, 14, 0, 0)
+    RB_CT_FAST_OP(OP_CONS0, 15, 0, 0)
+  }
+#undef RB_CT_FAST_OP
   return thrown;
 }
 
@@ -952,12 +1181,21 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
       for (int i = 0; i < na; ++i)
         if (!isfinite(W.D[i].c)) fail = CT_PICARD;
     // remainder_picard (flowpipe_ct.hpp:144-276)
+    bool cached = false;  // this step's full replay has run (FlowSmem::fc, the endpoint rows in HBM)
+    auto fast_field = [&](int mode) {
+      if (Pm.fast_prog == 1) return quad_fast<false>(W, mode, h);
+      if (Pm.fast_prog == 2) return quad_fast<true>(W, mode, h);
+      return run_field(W, Pm.prog, mode, L, gM);
+    };
     auto replay = [&](const Iv* cand) {
       for (int i = 0; i < na; ++i) {
         W.D[i].rlo = cand[i].lo;
         W.D[i].rhi = cand[i].hi;
       }
-      return run_field(W, Pm.prog, MODE_REPLAY, L, gM);
+      const bool t = cached ? fast_field(MODE_REPLAY_FAST) : run_field(W, Pm.prog, MODE_REPLAY, L, gM);
+      __syncwarp();  // lane 0's cache stores before the next replay's reads
+      cached = true;
+      return t;
     };
     auto finite_box = [&](const Iv* x) {
       bool ok = true;
@@ -1004,7 +1242,7 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
         W.D[i].rlo = W.i1[i].lo;
         W.D[i].rhi = W.i1[i].hi;
       }
-      const bool threw = run_field(W, Pm.prog, MODE_ENDPOINT, L, gM);
+      const bool threw = fast_field(MODE_ENDPOINT);
       bool exact_ok = !threw && finite_box(W.erem);
       for (int i = 0; i < na; ++i) exact_ok = exact_ok && isfinite(W.ec[i]);
       // tm_eval_interval(segment, [0, h]) (taylor_model.hpp:73-97), before S changes
