@@ -153,6 +153,27 @@ __device__ __forceinline__ void wsum4(double& a, double& b, double& c, double& d
     d += __shfl_xor_sync(0xffffffffu, d, o);
   }
 }
+// Sixteen butterfly sums at once (a transposed reduction): lane L returns
+// the sum of v[row_of_wsum16(L)] over the warp.  Every level adds the same
+// lane pairs as wsum's butterfly, so each sum is bit-identical to wsum(v[r]);
+// 16 + 8 + 4 + 2 + 1 + 1 shuffles instead of 16 x 5.
+__device__ __forceinline__ int row_of_wsum16(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+__device__ __forceinline__ double wsum16_rows(double (&v)[16], int lane) {
+#pragma unroll
+  for (int o = 16, n = 8; o > 1; o >>= 1, n >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < n) {
+        const double got = __shfl_xor_sync(0xffffffffu, up ? v[k] : v[k + n], o);
+        v[k] = (up ? v[k + n] : v[k]) + got;
+      }
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
 __device__ __forceinline__ double wsum(double a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -1152,18 +1173,18 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
 #pragma unroll
     for (int k = 0; k < NZC; ++k) L.act[k] = (lane + 32 * k) < nz;
     // seed rows: abs_z (cached: the Picard rows share their z columns)
-    for (int i = 0; i < na; i += 2) {
-      double s1 = 0.0, s2 = 0.0;
+    {
+      double v[NA];
 #pragma unroll
-      for (int k = 0; k < NZC; ++k) {
-        if (!L.act[k]) continue;
-        const int j = lane + 32 * k;
-        s1 += fabs(coef[i * NZP + j]);
-        if (i + 1 < na) s2 += fabs(coef[(i + 1) * NZP + j]);
+      for (int i = 0; i < NA; ++i) {
+        v[i] = 0.0;
+#pragma unroll
+        for (int k = 0; k < NZC; ++k)
+          if (i < na && L.act[k]) v[i] += fabs(coef[i * NZP + lane + 32 * k]);
       }
-      wsum2(s1, s2);
-      W.ssz[i] = s1;
-      if (i + 1 < na) W.ssz[i + 1] = s2;
+      const double sum = wsum16_rows(v, lane);
+      if ((lane & 1) == 0 && row_of_wsum16(lane) < na) W.ssz[row_of_wsum16(lane)] = sum;
+      __syncwarp();
     }
     // poly_picard (flowpipe_ct.hpp:126-139): g_0 = seed (bz = 0, at = 0, rem = 0);
     // aliased rows are never read before their first update
@@ -1177,9 +1198,9 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     bool thrown = false;
     for (int it = 0; it < Pm.order && !thrown; ++it) thrown = run_field(W, Pm.prog, MODE_PICARD, L, gM);
     int fail = thrown ? CT_TME_INV : CT_OK;
-    if (fail == CT_OK)
-      for (int i = 0; i < na; ++i)
-        if (!isfinite(W.D[i].c)) fail = CT_PICARD;
+    // the per-row checks and updates of remainder_picard run lane-parallel (lane i: row i < na <= 16)
+    const bool row = lane < na;
+    if (fail == CT_OK && __any_sync(0xffffffffu, row && !isfinite(W.D[lane].c))) fail = CT_PICARD;
     // remainder_picard (flowpipe_ct.hpp:144-276)
     bool cached = false;  // this step's full replay has run (FlowSmem::fc, the endpoint rows in HBM)
     auto fast_field = [&](int mode) {
@@ -1188,81 +1209,74 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
       return run_field(W, Pm.prog, mode, L, gM);
     };
     auto replay = [&](const Iv* cand) {
-      for (int i = 0; i < na; ++i) {
-        W.D[i].rlo = cand[i].lo;
-        W.D[i].rhi = cand[i].hi;
+      if (row) {
+        W.D[lane].rlo = cand[lane].lo;
+        W.D[lane].rhi = cand[lane].hi;
       }
+      __syncwarp();
       const bool t = cached ? fast_field(MODE_REPLAY_FAST) : run_field(W, Pm.prog, MODE_REPLAY, L, gM);
       __syncwarp();  // lane 0's cache stores before the next replay's reads
       cached = true;
       return t;
     };
-    auto finite_box = [&](const Iv* x) {
-      bool ok = true;
-      for (int i = 0; i < na; ++i) ok = ok && ifin(x[i]);
-      return ok;
-    };
+    auto finite_box = [&](const Iv* x) { return __all_sync(0xffffffffu, !row || ifin(x[lane])); };
     auto subset = [&](const Iv* in, const Iv* out) {
-      bool ok = true;
-      for (int i = 0; i < na; ++i) ok = ok && (out[i].lo <= in[i].lo && in[i].hi <= out[i].hi);
-      return ok;
+      return __all_sync(0xffffffffu, !row || (out[lane].lo <= in[lane].lo && in[lane].hi <= out[lane].hi));
     };
     if (fail == CT_OK) {
-      for (int i = 0; i < na; ++i) {
-        W.i0[i] = Iv{-Pm.eps, Pm.eps};
-        W.i1[i] = Iv{0.0, 0.0};
+      if (row) {
+        W.i0[lane] = Iv{-Pm.eps, Pm.eps};
+        W.i1[lane] = Iv{0.0, 0.0};
       }
       bool accepted = false;
       for (int attempt = 0; attempt <= Pm.maxe; ++attempt) {
         const bool threw = replay(W.i0);
-        if (!threw)
-          for (int i = 0; i < na; ++i) W.i1[i] = W.nx[i];
+        if (!threw && row) W.i1[lane] = W.nx[lane];
         if (!threw && finite_box(W.i1) && subset(W.i1, W.i0)) {
           accepted = true;
           break;
         }
-        for (int i = 0; i < na; ++i) {  // per-dimension adaptive enlargement (:178-182)
-          const Iv ind = threw ? Iv{0.0, 0.0} : W.i1[i];
-          const Iv cur = W.i0[i];
+        if (row) {  // per-dimension adaptive enlargement (:178-182)
+          const Iv ind = threw ? Iv{0.0, 0.0} : W.i1[lane];
+          const Iv cur = W.i0[lane];
           const Iv hull = (ind.lo <= ind.hi) ? Iv{smin(cur.lo, ind.lo), smax(cur.hi, ind.hi)} : cur;
           const double mid = (hull.lo + hull.hi) * 0.5, rad = (hull.hi - hull.lo) * 0.5 * Pm.enl;
-          W.i0[i] = Iv{mid - rad, mid + rad};
+          W.i0[lane] = Iv{mid - rad, mid + rad};
         }
+        __syncwarp();
       }
+      __syncwarp();
       if (!accepted) fail = CT_REMAINDER;
     }
     if (fail == CT_OK) {
       for (int round = 0; round < Pm.refine; ++round) {  // shrink (:214-223)
         if (replay(W.i1)) break;
         if (!(finite_box(W.nx) && subset(W.nx, W.i1))) break;
-        for (int i = 0; i < na; ++i) W.i1[i] = W.nx[i];
+        if (row) W.i1[lane] = W.nx[lane];
       }
       // endpoint by exact integration at tau = h (:236-263) into the HBM state rows
-      for (int i = 0; i < na; ++i) {
-        W.D[i].rlo = W.i1[i].lo;
-        W.D[i].rhi = W.i1[i].hi;
+      if (row) {
+        W.D[lane].rlo = W.i1[lane].lo;
+        W.D[lane].rhi = W.i1[lane].hi;
       }
+      __syncwarp();
       const bool threw = fast_field(MODE_ENDPOINT);
-      bool exact_ok = !threw && finite_box(W.erem);
-      for (int i = 0; i < na; ++i) exact_ok = exact_ok && isfinite(W.ec[i]);
-      // tm_eval_interval(segment, [0, h]) (taylor_model.hpp:73-97), before S changes
-      bool fin = true;
+      const bool exact_ok = !threw && finite_box(W.erem) && __all_sync(0xffffffffu, !row || isfinite(W.ec[lane]));
+      // tm_eval_interval(segment, [0, h]) (taylor_model.hpp:73-97), before S changes; lane i: row i
       const int kbox = 1 + gstep;
       double blo = 0.0, bhi = 0.0;
-      for (int i = 0; i < na; ++i) {
-        const Slot& p = W.D[i];
+      if (row) {
+        const Slot& p = W.D[lane];
         Iv acc{p.c - p.sz, p.c + p.sz};
         acc = iadd(acc, iscale(p.at, Iv{0.0, h}));
         const double tau_mag = smax(0.0, h);
         acc = iadd(acc, Iv{-p.sb * tau_mag, p.sb * tau_mag});
-        acc = iadd(acc, W.i1[i]);
-        fin = fin && ifin(acc);
-        if (lane == i) {
-          blo = acc.lo;
-          bhi = acc.hi;
-        }
+        acc = iadd(acc, W.i1[lane]);
+        blo = acc.lo;
+        bhi = acc.hi;
       }
-      if (lane < na) emit_box(Pm, b, kbox, na, lane, blo, bhi);
+      const bool fin = __all_sync(0xffffffffu, !row || ifin(Iv{blo, bhi}));
+      if (row) emit_box(Pm, b, kbox, na, lane, blo, bhi);
       nboxes = kbox + 1;
       // new generator rows: the exact endpoint (HBM, L2-resident) or the
       // fallback p_k(h) = seed + B h (:264-274), via HBM so aliased bz rows
