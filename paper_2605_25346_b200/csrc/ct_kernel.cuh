@@ -819,6 +819,178 @@ __device__ __noinline__ bool quad_fast(FlowSmem& W, int mode, double h) {
   return thrown;
 }
 
+// The full-mode passes (MODE_PICARD, MODE_REPLAY) of the quadrotor program,
+// compiled from RB_CT_QUAD_OPS like quad_fast: slot scalars, view scales and
+// row offsets in registers, the coefficient rows in shared memory.  Each
+// operation is run_field's (operand order, excess folding, the abs-sum
+// butterflies), but with the program known to the compiler one operation's
+// scalar chain and shuffle reduction overlap the next operations' coefficient
+// passes instead of serializing through the interpreter's dispatch.
+struct FR {
+  double c, at, rlo, rhi, sz, sb;
+  double s;    // view scale (1 for a stored row)
+  int az, bz;  // coefficient rows (offsets into FlowSmem::coef())
+};
+struct FullCtx {
+  FlowSmem& W;
+  double* coef;
+  double* gM;
+  const Lane& L;
+  int mode;
+  int off_taz, off_tbz;
+};
+template <int CODE, int DST, int A, int B>
+__device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc, bool& thrown) {
+  FlowSmem& W = X.W;
+  double* coef = X.coef;
+  const Lane& L = X.L;
+  const double h = L.h;
+  const int lane = L.lane;
+  const bool record = X.mode == MODE_REPLAY;
+  if constexpr (CODE == OP_MUL || CODE == OP_MUL2 || CODE == OP_ADD || CODE == OP_SUB) {
+    static_assert(DST >= SLOT_T && DST < SLOT_V, "stored results go to temporaries");
+    const FR u = D[A], v = D[B];
+    const int raz = X.off_taz + (DST - SLOT_T) * NZP, rbz = X.off_tbz + (DST - SLOT_T) * NZP;
+    constexpr bool mul = CODE == OP_MUL || CODE == OP_MUL2, sub = CODE == OP_SUB;
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < NZC; ++k) {
+      if (!L.act[k]) continue;
+      const int j = lane + 32 * k;
+      // stored rows (P, T, C slots) have scale 1: x * 1.0 == x, so only views multiply
+      constexpr bool uv = A >= SLOT_V && A < SLOT_C, vv = B >= SLOT_V && B < SLOT_C;
+      const double ua = uv ? coef[u.az + j] * u.s : coef[u.az + j], ub = uv ? coef[u.bz + j] * u.s : coef[u.bz + j];
+      const double va = vv ? coef[v.az + j] * v.s : coef[v.az + j], vb = vv ? coef[v.bz + j] * v.s : coef[v.bz + j];
+      double ra, rb;
+      if constexpr (mul) {
+        ra = u.c * va + v.c * ua;
+        rb = u.c * vb + v.c * ub + u.at * va + v.at * ua;
+      } else {
+        ra = sub ? ua - va : ua + va;
+        rb = sub ? ub - vb : ub + vb;
+      }
+      coef[raz + j] = ra;
+      coef[rbz + j] = rb;
+      s1 += fabs(ra);
+      s2 += fabs(rb);
+    }
+    wsum2(s1, s2);
+    FR r;
+    if constexpr (mul) {
+      const Iv rem = mul_rem(u.c, v.c, u.at, v.at, u.sz, v.sz, u.sb, v.sb, Iv{u.rlo, u.rhi}, Iv{v.rlo, v.rhi}, h);
+      r = FR{u.c * v.c, u.c * v.at + v.c * u.at, rem.lo, rem.hi, s1, s2, 1.0, raz, rbz};
+    } else {
+      const Iv rem = sub ? isub(Iv{u.rlo, u.rhi}, Iv{v.rlo, v.rhi}) : iadd(Iv{u.rlo, u.rhi}, Iv{v.rlo, v.rhi});
+      r = FR{sub ? u.c - v.c : u.c + v.c, sub ? u.at - v.at : u.at + v.at, rem.lo, rem.hi, s1, s2, 1.0, raz, rbz};
+    }
+    D[DST] = r;
+    if (record && lane == 0) W.fc[pc] = make_double2(s1, s2);
+  } else if constexpr (CODE == OP_SUBK) {
+    D[DST].c = D[DST].c - W.kc[B];
+  } else if constexpr (CODE == OP_CONST) {
+    D[DST] = FR{W.kc[B], 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, W.off_zero, W.off_zero};
+  } else if constexpr (CODE == OP_SCALE) {
+    const FR u = D[A];
+    const double s = W.kc[B];
+    const Iv rem = iscale(s, Iv{u.rlo, u.rhi});
+    D[DST] = FR{u.c * s, u.at * s, rem.lo, rem.hi, fabs(s) * u.sz, fabs(s) * u.sb, u.s * s, u.az, u.bz};
+  } else if constexpr (CODE == OP_SIN || CODE == OP_COS) {
+    const FR u = D[A];
+    const double m = u.c;
+    const Iv range = iadd(poly_range(u.c, u.sz, u.at, u.sb, h), Iv{u.rlo, u.rhi});
+    const double rad = smax(fabs(range.lo - m), fabs(range.hi - m));
+    const double err = rad * rad * 0.5;
+    double sm, cm;
+    sincos(m, &sm, &cm);
+    constexpr bool isc = CODE == OP_COS;
+    const double s = isc ? -sm : cm;
+    Iv rem = iscale(s, Iv{u.rlo, u.rhi});
+    rem = iadd(rem, Iv{-err, err});
+    D[DST] = FR{(m - m) * s + (isc ? cm : sm), u.at * s, rem.lo, rem.hi, fabs(s) * u.sz, fabs(s) * u.sb, u.s * s,
+                u.az, u.bz};
+  } else if constexpr (CODE == OP_INV) {
+    const FR v = D[A];
+    const Iv range = iadd(poly_range(v.c, v.sz, v.at, v.sb, h), Iv{v.rlo, v.rhi});
+    if (range.lo <= 0.0 && range.hi >= 0.0) thrown = true;
+    const double m = v.c, mm = m * m;
+    const double e_lo = 1.0 / range.lo - (2.0 / m - range.lo / mm);
+    const double e_hi = 1.0 / range.hi - (2.0 / m - range.hi / mm);
+    const Iv e{smin(smin(e_lo, e_hi), 0.0), smax(smax(e_lo, e_hi), 0.0)};
+    const double s = -1.0 / mm;
+    Iv rem = iscale(s, Iv{v.rlo, v.rhi});
+    rem = iadd(rem, e);
+    D[DST] = FR{v.c * s + 2.0 / m, v.at * s, rem.lo, rem.hi, fabs(s) * v.sz, fabs(s) * v.sb, v.s * s, v.az, v.bz};
+  } else if constexpr (CODE == OP_CONS || CODE == OP_CONS0) {
+    constexpr int i = DST;
+    constexpr bool zero = CODE == OP_CONS0;
+    const FR f = D[zero ? 0 : A];
+    const double fc_ = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at, fsz = zero ? 0.0 : f.sz, fsb = zero ? 0.0 : f.sb;
+    const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
+    const double* S = coef + i * NZP;
+    double* Pb = coef + W.pbz[i];
+    const double half_at = fat * 0.5;
+    Iv rem = imul_0h(h * h, half_at);
+    const double bb = fsb * h * h * 0.5;
+    rem = iadd(rem, Iv{-bb, bb});
+    rem = iadd(rem, imul(fr, Iv{0.0, h}));
+    if (X.mode == MODE_PICARD) {
+      if (W.own[i]) {
+#pragma unroll
+        for (int k = 0; k < NZC; ++k) {
+          if (!L.act[k]) continue;
+          const int j = lane + 32 * k;
+          Pb[j] = zero ? 0.0 : coef[f.az + j] * f.s;
+        }
+      }
+      set_scalars(W.D[i], W.sc[i], fc_, rem, W.ssz[i], fsz);
+    } else {  // the step's full replay: range of (seed + Int f) - p_k, the endpoint rows, the cached sum
+      double s2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < NZC; ++k) {
+        if (!L.act[k]) continue;
+        const int j = lane + 32 * k;
+        const double fa = zero ? 0.0 : coef[f.az + j] * f.s, fb = zero ? 0.0 : coef[f.bz + j] * f.s;
+        s2 += fabs(fa - Pb[j]);
+        X.gM[i * NZP + j] = S[j] + h * (fa + fb * h * 0.5);
+      }
+      s2 = wsum(s2);
+      if (lane == 0) W.fc[pc] = make_double2(s2, 0.0);
+      const FR pk = D[i];
+      const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
+      W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, s2, h), rem);
+    }
+  }
+}
+
+template <bool HELD>
+__device__ __noinline__ bool quad_full(FlowSmem& W, int mode, const Lane L, double* gM) {
+  FR D[NSLOT];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) {
+    const Slot& p = W.D[i];
+    D[i] = FR{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb, 1.0, i * NZP, W.pbz[i]};
+  }
+  const FullCtx X{W, W.coef(), gM, L, mode, W.off_taz, W.off_tbz};
+  bool thrown = false;
+  int pc = 0;
+#define RB_CT_FULL_OP(c, d, a, b) full_op<c, d, a, b>(D, X, pc++, thrown);
+  if constexpr (HELD) {
+    RB_CT_FULL_OP(OP_CONST, C_(0), 0, 8)
+    RB_CT_FULL_OP(OP_CONST, C_(1), 0, 9)
+    RB_CT_FULL_OP(OP_CONST, C_(2), 0, 10)
+    RB_CT_FULL_OP(OP_CONST, C_(3), 0, 11)
+    RB_CT_QUAD_OPS(RB_CT_FULL_OP, C_(0), C_(1), C_(2), C_(3))
+  } else {
+    RB_CT_QUAD_OPS(RB_CT_FULL_OP, P_(12), P_(13), P_(14), P_(15))
+    RB_CT_FULL_OP(OP_CONS0, 12, 0, 0)
+    RB_CT_FULL_OP(OP_CONS0, 13, 0, 0)
+    RB_CT_FULL_OP(OP_CONS0, 14, 0, 0)
+    RB_CT_FULL_OP(OP_CONS0, 15, 0, 0)
+  }
+#undef RB_CT_FULL_OP
+  return thrown;
+}
+
 __device__ __forceinline__ void emit_box(const CTParams& P, long long b, int k, int na, int d, double lo, double hi) {
   if (!P.split) {
     const size_t o = (static_cast<size_t>(b) * P.T + k) * na + d;
@@ -1196,7 +1368,15 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
       set_scalars(W.D[i], W.sc[i], 0.0, Iv{0.0, 0.0}, W.ssz[i], 0.0);
     }
     bool thrown = false;
-    for (int it = 0; it < Pm.order && !thrown; ++it) thrown = run_field(W, Pm.prog, MODE_PICARD, L, gM);
+    auto full_field = [&](int mode) {
+      if (Pm.fast_prog == 1) return quad_full<false>(W, mode, L, gM);
+      if (Pm.fast_prog == 2) return quad_full<true>(W, mode, L, gM);
+      return run_field(W, Pm.prog, mode, L, gM);
+    };
+    for (int it = 0; it < Pm.order && !thrown; ++it) {
+      thrown = full_field(MODE_PICARD);
+      __syncwarp();
+    }
     int fail = thrown ? CT_TME_INV : CT_OK;
     // the per-row checks and updates of remainder_picard run lane-parallel (lane i: row i < na <= 16)
     const bool row = lane < na;
@@ -1214,7 +1394,7 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
         W.D[lane].rhi = cand[lane].hi;
       }
       __syncwarp();
-      const bool t = cached ? fast_field(MODE_REPLAY_FAST) : run_field(W, Pm.prog, MODE_REPLAY, L, gM);
+      const bool t = cached ? fast_field(MODE_REPLAY_FAST) : full_field(MODE_REPLAY);
       __syncwarp();  // lane 0's cache stores before the next replay's reads
       cached = true;
       return t;
@@ -1355,6 +1535,7 @@ struct __align__(16) CtlSmem {
 };
 
 constexpr int kCtlWarps = 4;
+constexpr int kCtlPrefetch = 16;  // controller weights loaded ahead of their accumulation chain
 
 __device__ __forceinline__ void relax_tanh_or_relu(int act, double l, double u, double& s, double& li, double& ui) {
   relax(act, l, u, s, li, ui);
@@ -1478,11 +1659,20 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     const int in_cols = (t == 0) ? n : rows;
     for (int u = lane; u < width; u += 32) {
       double lo = 0.0, hi = 0.0;
-      for (int j = 0; j < in_cols; ++j) {
-        const double w = blob[N.wt_off[t] + static_cast<size_t>(j) * N.ldt[t] + u];
-        const double xl = W.hb[cur][j][0], xh = W.hb[cur][j][1];
-        lo = lo + ((w >= 0.0) ? w * xl : w * xh);
-        hi = hi + ((w >= 0.0) ? w * xh : w * xl);
+      const double* wt = blob + N.wt_off[t] + u;
+      for (int j0 = 0; j0 < in_cols; j0 += kCtlPrefetch) {  // the chunk's weights in flight together (L2 latency)
+        double wv[kCtlPrefetch];
+#pragma unroll
+        for (int q = 0; q < kCtlPrefetch; ++q)
+          wv[q] = (j0 + q < in_cols) ? __ldg(wt + static_cast<size_t>(j0 + q) * N.ldt[t]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kCtlPrefetch; ++q) {
+          if (j0 + q >= in_cols) break;
+          const double w = wv[q];
+          const double xl = W.hb[cur][j0 + q][0], xh = W.hb[cur][j0 + q][1];
+          lo = lo + ((w >= 0.0) ? w * xl : w * xh);
+          hi = hi + ((w >= 0.0) ? w * xh : w * xl);
+        }
       }
       const double bias = (t == 0) ? W.bf0[u] : blob[N.b_off[t] + u];
       lo = lo + bias;
@@ -1554,11 +1744,19 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     // Lambda = Lambda . W_t (linalg.hpp:53-63, i-k-j order): lane = column
     for (int jc = lane; jc < cols; jc += 32) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int k = 0; k < width; ++k) {
-        const double w = blob[N.w_off[t] + static_cast<size_t>(k) * N.ldw[t] + jc];
+      const double* wc = blob + N.w_off[t] + jc;
+      for (int k0 = 0; k0 < width; k0 += kCtlPrefetch) {
+        double wv[kCtlPrefetch];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i < no) acc[i] = acc[i] + W.lam[lb][i][k] * w;
+        for (int q = 0; q < kCtlPrefetch; ++q)
+          wv[q] = (k0 + q < width) ? __ldg(wc + static_cast<size_t>(k0 + q) * N.ldw[t]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kCtlPrefetch; ++q) {
+          if (k0 + q >= width) break;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (i < no) acc[i] = acc[i] + W.lam[lb][i][k0 + q] * wv[q];
+        }
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
