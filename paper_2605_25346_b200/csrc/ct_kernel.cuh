@@ -1535,7 +1535,11 @@ struct __align__(16) CtlSmem {
 };
 
 constexpr int kCtlWarps = 4;
-constexpr int kCtlPrefetch = 16;  // controller weights loaded ahead of their accumulation chain
+constexpr int kCtlPrefetch = 16;  // controller weights loaded a chunk ahead of their accumulation chain
+__device__ __forceinline__ void ctl_chunk(double (&v)[kCtlPrefetch], const double* base, size_t ld, int j0, int n) {
+#pragma unroll
+  for (int q = 0; q < kCtlPrefetch; ++q) v[q] = (j0 + q < n) ? __ldg(base + static_cast<size_t>(j0 + q) * ld) : 0.0;
+}
 
 __device__ __forceinline__ void relax_tanh_or_relu(int act, double l, double u, double& s, double& li, double& ui) {
   relax(act, l, u, s, li, ui);
@@ -1623,8 +1627,21 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
   } else {
     nzx = n + nq * NA;
     nbw = nq;
-    for (int i = 0; i < n; ++i)
-      for (int j = lane; j < nzx; j += 32) W.xA[i * LDX + j] = gM[i * NZP + j];
+    double v[NX][NZC];  // every load in flight before the first store (n == NX for cl_reach)
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NZC; ++k) {
+        const int j = lane + 32 * k;
+        v[i][k] = (i < n && j < nzx) ? gM[i * NZP + j] : 0.0;
+      }
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+#pragma unroll
+      for (int k = 0; k < NZC; ++k) {
+        const int j = lane + 32 * k;
+        if (i < n && j < nzx) W.xA[i * LDX + j] = v[i][k];
+      }
     if (lane < n) W.xc[lane] = gc[lane];
   }
   __syncwarp();
@@ -1660,11 +1677,12 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     for (int u = lane; u < width; u += 32) {
       double lo = 0.0, hi = 0.0;
       const double* wt = blob + N.wt_off[t] + u;
-      for (int j0 = 0; j0 < in_cols; j0 += kCtlPrefetch) {  // the chunk's weights in flight together (L2 latency)
-        double wv[kCtlPrefetch];
-#pragma unroll
-        for (int q = 0; q < kCtlPrefetch; ++q)
-          wv[q] = (j0 + q < in_cols) ? __ldg(wt + static_cast<size_t>(j0 + q) * N.ldt[t]) : 0.0;
+      const size_t ldt = N.ldt[t];
+      double wv[kCtlPrefetch];
+      ctl_chunk(wv, wt, ldt, 0, in_cols);
+      for (int j0 = 0; j0 < in_cols; j0 += kCtlPrefetch) {  // the next chunk's weights in flight (L2 latency)
+        double wn[kCtlPrefetch];
+        ctl_chunk(wn, wt, ldt, j0 + kCtlPrefetch, in_cols);
 #pragma unroll
         for (int q = 0; q < kCtlPrefetch; ++q) {
           if (j0 + q >= in_cols) break;
@@ -1673,6 +1691,8 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
           lo = lo + ((w >= 0.0) ? w * xl : w * xh);
           hi = hi + ((w >= 0.0) ? w * xh : w * xl);
         }
+#pragma unroll
+        for (int q = 0; q < kCtlPrefetch; ++q) wv[q] = wn[q];
       }
       const double bias = (t == 0) ? W.bf0[u] : blob[N.b_off[t] + u];
       lo = lo + bias;
@@ -1745,11 +1765,12 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     for (int jc = lane; jc < cols; jc += 32) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       const double* wc = blob + N.w_off[t] + jc;
+      const size_t ldw = N.ldw[t];
+      double wv[kCtlPrefetch];
+      ctl_chunk(wv, wc, ldw, 0, width);
       for (int k0 = 0; k0 < width; k0 += kCtlPrefetch) {
-        double wv[kCtlPrefetch];
-#pragma unroll
-        for (int q = 0; q < kCtlPrefetch; ++q)
-          wv[q] = (k0 + q < width) ? __ldg(wc + static_cast<size_t>(k0 + q) * N.ldw[t]) : 0.0;
+        double wn[kCtlPrefetch];
+        ctl_chunk(wn, wc, ldw, k0 + kCtlPrefetch, width);
 #pragma unroll
         for (int q = 0; q < kCtlPrefetch; ++q) {
           if (k0 + q >= width) break;
@@ -1757,6 +1778,8 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
           for (int i = 0; i < 4; ++i)
             if (i < no) acc[i] = acc[i] + W.lam[lb][i][k0 + q] * wv[q];
         }
+#pragma unroll
+        for (int q = 0; q < kCtlPrefetch; ++q) wv[q] = wn[q];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
