@@ -720,88 +720,187 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
 struct FS {
   double c, at, rlo, rhi, sz, sb;
 };
-template <int CODE, int DST, int A, int B>
-__device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, int pc, int mode, double h, bool& thrown) {
+// Between two replays of a step only the remainders change, so everything
+// else each operation computes is recorded by the step's first scalar-only
+// replay (CACHED = false) into the temporaries' coefficient rows (dead until
+// the next step's Picard iteration; kFastK doubles per program entry), and
+// the later replays and the endpoint (CACHED = true) carry the remainders
+// only: operator* as base + pu * vr + pv * ur + ur * vr with base = the excess
+// interval + the tau^2 term and pu / pv the operands' polynomial ranges
+// (taylor_model.hpp:337-359, the same additions in the same order);
+// sin / cos / reciprocal from the cached range without the remainder and the
+// linearization point; the consumers from their cached constant parts.
+constexpr int kFastK = 6;
+template <int CODE, int DST, int A, int B, bool CACHED>
+__device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, double* K, int pc, int mode, double h,
+                                        bool& thrown, bool rec) {
+  double* k = K + pc * kFastK;
   if constexpr (CODE == OP_MUL || CODE == OP_MUL2) {  // the pair's second entry follows as an OP_MUL
     const FS u = D[A], v = D[B];
-    const double2 s = W.fc[pc];
-    const Iv rem = mul_rem(u.c, v.c, u.at, v.at, u.sz, v.sz, u.sb, v.sb, Iv{u.rlo, u.rhi}, Iv{v.rlo, v.rhi}, h);
-    D[DST] = FS{u.c * v.c, u.c * v.at + v.c * u.at, rem.lo, rem.hi, s.x, s.y};
+    const Iv ur{u.rlo, u.rhi}, vr{v.rlo, v.rhi};
+    Iv base, pu, pv;
+    if constexpr (CACHED) {
+      base = Iv{k[0], k[1]};
+      pu = Iv{k[2], k[3]};
+      pv = Iv{k[4], k[5]};
+    } else {  // mul_rem's constant part
+      const double uc = u.c, vc = v.c, uat = u.at, vat = v.at, au = u.sz, av = v.sz, bu = u.sb, bv = v.sb;
+      double sym = au * av;
+      sym += (au * bv + av * bu) * h;
+      sym += bu * bv * h * h;
+      sym += (fabs(uat) * bv + fabs(vat) * bu) * h * h;
+      base = iadd(Iv{-sym, sym}, imul_0h(h * h, uat * vat));
+      pu = poly_range(uc, au, uat, bu, h);
+      pv = poly_range(vc, av, vat, bv, h);
+      if (rec) {
+        k[0] = base.lo; k[1] = base.hi; k[2] = pu.lo; k[3] = pu.hi; k[4] = pv.lo; k[5] = pv.hi;
+      }
+    }
+    Iv rem = iadd(base, imul(pu, vr));
+    rem = iadd(rem, imul(pv, ur));
+    rem = iadd(rem, imul(ur, vr));
+    if constexpr (CACHED) {
+      D[DST].rlo = rem.lo;
+      D[DST].rhi = rem.hi;
+    } else {
+      const double2 s = W.fc[pc];
+      D[DST] = FS{u.c * v.c, u.c * v.at + v.c * u.at, rem.lo, rem.hi, s.x, s.y};
+    }
   } else if constexpr (CODE == OP_ADD || CODE == OP_SUB) {
     const FS a = D[A], b = D[B];
-    const double2 s = W.fc[pc];
-    const bool sub = CODE == OP_SUB;
+    constexpr bool sub = CODE == OP_SUB;
     const Iv rem = sub ? isub(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi}) : iadd(Iv{a.rlo, a.rhi}, Iv{b.rlo, b.rhi});
-    D[DST] = FS{sub ? a.c - b.c : a.c + b.c, sub ? a.at - b.at : a.at + b.at, rem.lo, rem.hi, s.x, s.y};
+    if constexpr (CACHED) {
+      D[DST].rlo = rem.lo;
+      D[DST].rhi = rem.hi;
+    } else {
+      const double2 s = W.fc[pc];
+      D[DST] = FS{sub ? a.c - b.c : a.c + b.c, sub ? a.at - b.at : a.at + b.at, rem.lo, rem.hi, s.x, s.y};
+    }
   } else if constexpr (CODE == OP_SUBK) {
-    D[DST].c = D[DST].c - W.kc[B];
+    if constexpr (!CACHED) D[DST].c = D[DST].c - W.kc[B];
   } else if constexpr (CODE == OP_CONST) {
     D[DST] = FS{W.kc[B], 0.0, 0.0, 0.0, 0.0, 0.0};
   } else if constexpr (CODE == OP_SCALE) {
     const FS u = D[A];
     const double s = W.kc[B];
     const Iv rem = iscale(s, Iv{u.rlo, u.rhi});
-    D[DST] = FS{u.c * s, u.at * s, rem.lo, rem.hi, fabs(s) * u.sz, fabs(s) * u.sb};
+    if constexpr (CACHED) {
+      D[DST].rlo = rem.lo;
+      D[DST].rhi = rem.hi;
+    } else {
+      D[DST] = FS{u.c * s, u.at * s, rem.lo, rem.hi, fabs(s) * u.sz, fabs(s) * u.sb};
+    }
   } else if constexpr (CODE == OP_SIN || CODE == OP_COS) {
     const FS u = D[A];
-    const double m = u.c;
-    const Iv range = iadd(poly_range(u.c, u.sz, u.at, u.sb, h), Iv{u.rlo, u.rhi});
+    Iv pr;
+    double m, s;
+    double sm = 0.0, cm = 0.0;
+    constexpr bool isc = CODE == OP_COS;
+    if constexpr (CACHED) {
+      pr = Iv{k[0], k[1]};
+      m = k[2];
+      s = k[3];
+    } else {
+      m = u.c;
+      pr = poly_range(u.c, u.sz, u.at, u.sb, h);
+      sincos(m, &sm, &cm);
+      s = isc ? -sm : cm;
+      if (rec) {
+        k[0] = pr.lo; k[1] = pr.hi; k[2] = m; k[3] = s;
+      }
+    }
+    const Iv range = iadd(pr, Iv{u.rlo, u.rhi});
     const double rad = smax(fabs(range.lo - m), fabs(range.hi - m));
     const double err = rad * rad * 0.5;
-    double sm, cm;
-    sincos(m, &sm, &cm);
-    constexpr bool isc = CODE == OP_COS;
-    const double s = isc ? -sm : cm;
     Iv rem = iscale(s, Iv{u.rlo, u.rhi});
     rem = iadd(rem, Iv{-err, err});
-    D[DST] = FS{(m - m) * s + (isc ? cm : sm), u.at * s, rem.lo, rem.hi, fabs(s) * u.sz, fabs(s) * u.sb};
+    if constexpr (CACHED) {
+      D[DST].rlo = rem.lo;
+      D[DST].rhi = rem.hi;
+    } else {
+      D[DST] = FS{(m - m) * s + (isc ? cm : sm), u.at * s, rem.lo, rem.hi, fabs(s) * u.sz, fabs(s) * u.sb};
+    }
   } else if constexpr (CODE == OP_INV) {
     const FS v = D[A];
-    const Iv range = iadd(poly_range(v.c, v.sz, v.at, v.sb, h), Iv{v.rlo, v.rhi});
+    Iv pr;
+    double m, mm;
+    if constexpr (CACHED) {
+      pr = Iv{k[0], k[1]};
+      m = k[2];
+      mm = k[3];
+    } else {
+      pr = poly_range(v.c, v.sz, v.at, v.sb, h);
+      m = v.c;
+      mm = m * m;
+      if (rec) {
+        k[0] = pr.lo; k[1] = pr.hi; k[2] = m; k[3] = mm;
+      }
+    }
+    const Iv range = iadd(pr, Iv{v.rlo, v.rhi});
     if (range.lo <= 0.0 && range.hi >= 0.0) thrown = true;
-    const double m = v.c, mm = m * m;
     const double e_lo = 1.0 / range.lo - (2.0 / m - range.lo / mm);
     const double e_hi = 1.0 / range.hi - (2.0 / m - range.hi / mm);
     const Iv e{smin(smin(e_lo, e_hi), 0.0), smax(smax(e_lo, e_hi), 0.0)};
     const double s = -1.0 / mm;
     Iv rem = iscale(s, Iv{v.rlo, v.rhi});
     rem = iadd(rem, e);
-    D[DST] = FS{v.c * s + 2.0 / m, v.at * s, rem.lo, rem.hi, fabs(s) * v.sz, fabs(s) * v.sb};
+    if constexpr (CACHED) {
+      D[DST].rlo = rem.lo;
+      D[DST].rhi = rem.hi;
+    } else {
+      D[DST] = FS{v.c * s + 2.0 / m, v.at * s, rem.lo, rem.hi, fabs(s) * v.sz, fabs(s) * v.sb};
+    }
   } else if constexpr (CODE == OP_CONS || CODE == OP_CONS0) {
     constexpr int i = DST;
     constexpr bool zero = CODE == OP_CONS0;
     const FS f = D[zero ? 0 : A];
-    const double fc_ = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at, fsb = zero ? 0.0 : f.sb;
     const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
-    if (mode == MODE_ENDPOINT) {
-      W.ec[i] = W.sc[i] + h * (fc_ + fat * h * 0.5);
-      W.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
+    Iv ca, cb;  // tme_integrate's constant part, the polynomial range of (seed + Int f) - p_k
+    double ec;
+    if constexpr (CACHED) {
+      ca = Iv{k[0], k[1]};
+      cb = Iv{k[2], k[3]};
+      ec = k[4];
     } else {
+      const double fc_ = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at, fsb = zero ? 0.0 : f.sb;
+      ec = W.sc[i] + h * (fc_ + fat * h * 0.5);
       const double half_at = fat * 0.5;
-      Iv rem = imul_0h(h * h, half_at);
       const double bb = fsb * h * h * 0.5;
-      rem = iadd(rem, Iv{-bb, bb});
-      rem = iadd(rem, imul(fr, Iv{0.0, h}));
+      ca = iadd(imul_0h(h * h, half_at), Iv{-bb, bb});
       const FS pk = D[i];
       const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
-      W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, W.fc[pc].x, h), rem);
+      cb = poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, W.fc[pc].x, h);
+      if (rec) {
+        k[0] = ca.lo; k[1] = ca.hi; k[2] = cb.lo; k[3] = cb.hi; k[4] = ec;
+      }
+    }
+    if (mode == MODE_ENDPOINT) {
+      W.ec[i] = ec;
+      W.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
+    } else {
+      const Iv rem = iadd(ca, imul(fr, Iv{0.0, h}));
+      W.nx[i] = iadd(cb, rem);
     }
   }
 }
 
 // HELD: ct_reach's quadrotor field (inputs C0..3 from kc[8..11], four OP_CONST
 // entries first); else cl_reach's augmented field (inputs P12..15, udot = 0).
-template <bool HELD>
-__device__ __noinline__ bool quad_fast(FlowSmem& W, int mode, double h) {
+// CACHED = false with rec: record the constants (lane 0) for the CACHED calls.
+template <bool HELD, bool CACHED>
+__device__ __noinline__ bool quad_fast(FlowSmem& W, int mode, double h, bool rec) {
   FS D[NSLOT];
 #pragma unroll
   for (int i = 0; i < NA; ++i) {
     const Slot& p = W.D[i];
     D[i] = FS{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb};
   }
+  double* K = W.coef() + W.off_taz;
+  rec = rec && (threadIdx.x & 31) == 0;
   bool thrown = false;
   int pc = 0;
-#define RB_CT_FAST_OP(c, d, a, b) fast_op<c, d, a, b>(D, W, pc++, mode, h, thrown);
+#define RB_CT_FAST_OP(c, d, a, b) fast_op<c, d, a, b, CACHED>(D, W, K, pc++, mode, h, thrown, rec);
   if constexpr (HELD) {
     RB_CT_FAST_OP(OP_CONST, C_(0), 0, 8)
     RB_CT_FAST_OP(OP_CONST, C_(1), 0, 9)
@@ -1383,10 +1482,17 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     if (fail == CT_OK && __any_sync(0xffffffffu, row && !isfinite(W.D[lane].c))) fail = CT_PICARD;
     // remainder_picard (flowpipe_ct.hpp:144-276)
     bool cached = false;  // this step's full replay has run (FlowSmem::fc, the endpoint rows in HBM)
+    int nrec = 0;  // 0: nothing recorded yet; 1: quad_fast's constants recorded (the temporaries' rows)
     auto fast_field = [&](int mode) {
-      if (Pm.fast_prog == 1) return quad_fast<false>(W, mode, h);
-      if (Pm.fast_prog == 2) return quad_fast<true>(W, mode, h);
-      return run_field(W, Pm.prog, mode, L, gM);
+      bool t;
+      if (Pm.fast_prog == 1)
+        t = nrec ? quad_fast<false, true>(W, mode, h, false) : quad_fast<false, false>(W, mode, h, true);
+      else if (Pm.fast_prog == 2)
+        t = nrec ? quad_fast<true, true>(W, mode, h, false) : quad_fast<true, false>(W, mode, h, true);
+      else
+        t = run_field(W, Pm.prog, mode, L, gM);
+      nrec = 1;
+      return t;
     };
     auto replay = [&](const Iv* cand) {
       if (row) {
