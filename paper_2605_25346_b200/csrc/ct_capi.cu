@@ -182,7 +182,7 @@ int ensure_programs(reach_ctx* ctx) {
 void load_program(const Program& p, int kind, int na, rb::ct::CTParams& P) {
   using namespace rb::ct;
   P.prog = program_store().offset.at({kind, na});
-  P.fast_prog = kind == kKindQuadAug ? 1 : kind == REACH_FIELD_QUADROTOR ? 2 : 0;  // compiled scalar replays
+  P.fast_prog = kind == kKindQuadAug ? 1 : kind == REACH_FIELD_QUADROTOR ? 2 : 0;  // the compiled programs
   for (int i = 0; i < kMaxKc; ++i) P.kc[i] = p.kc[i];
   bool read[16] = {};
   for (const TOp& op : p.ops) {
@@ -197,6 +197,17 @@ void load_program(const Program& p, int kind, int na, rb::ct::CTParams& P) {
   for (const TOp& op : p.ops) {
     if (op.code == OP_CONS0) P.bzsrc[op.dst] = -2;
     if (op.code == OP_CONS && op.a < NA && !read[op.dst]) P.bzsrc[op.dst] = static_cast<signed char>(op.a);
+  }
+  // the compiled quadrotor programs assume QuadLayout's rows; the interpreter serves anything else
+  if (P.fast_prog) {
+    const bool held = P.fast_prog == 2;
+    const int nrow = held ? NX : NA;
+    bool match = na == nrow;
+    for (int i = 0; i < nrow && match; ++i) {
+      const int want = i < 3 ? i + 3 : i < 12 ? -1 : -2;
+      match = P.bzsrc[i] == want;
+    }
+    if (!match) P.fast_prog = 0;
   }
 }
 

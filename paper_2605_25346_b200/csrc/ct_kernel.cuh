@@ -717,6 +717,27 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
 // three angles, the two product trees, dx9..11) instead of one interpreted
 // operation after another.  Each operation is run_field's fast form, operand
 // order included; the abs-sums come from this step's full replay (FlowSmem::fc).
+// The quadrotor programs' row layout as compile-time constants (what the
+// flow kernel derives from CTParams::bzsrc; the host selects the compiled
+// programs only when the two agree, ct_capi.cu): rows 0..2 integrate
+// P3..5 (bz = S3..5), rows 3..11 own their Picard bz rows, the input rows
+// 12..15 of the augmented field have udot = 0 (bz = the zero row).  Constant
+// row offsets let the compiler prove which shared-memory rows an operation
+// touches and move the next operations' loads ahead of this one's stores.
+template <bool HELD>
+struct QuadLayout {
+  static constexpr int na = HELD ? NX : NA;
+  static constexpr int off_zero = na * NZP;
+  static constexpr int off_pbz = off_zero + NZP;
+  static constexpr int npb = 9;
+  static constexpr int off_taz = off_pbz + npb * NZP;
+  static constexpr int off_tbz = off_taz + NTF * NZP;
+  __host__ __device__ static constexpr int pbz(int i) {
+    return i < 3 ? (i + 3) * NZP : i < 12 ? off_pbz + (i - 3) * NZP : off_zero;
+  }
+  __host__ __device__ static constexpr bool own(int i) { return i >= 3 && i < 12; }
+};
+
 struct FS {
   double c, at, rlo, rhi, sz, sb;
 };
@@ -896,7 +917,7 @@ __device__ __noinline__ bool quad_fast(FlowSmem& W, int mode, double h, bool rec
     const Slot& p = W.D[i];
     D[i] = FS{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb};
   }
-  double* K = W.coef() + W.off_taz;
+  double* K = W.coef() + QuadLayout<HELD>::off_taz;
   rec = rec && (threadIdx.x & 31) == 0;
   bool thrown = false;
   int pc = 0;
@@ -936,10 +957,10 @@ struct FullCtx {
   double* gM;
   const Lane& L;
   int mode;
-  int off_taz, off_tbz;
 };
-template <int CODE, int DST, int A, int B>
+template <int CODE, int DST, int A, int B, bool HELD>
 __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc, bool& thrown) {
+  using Q = QuadLayout<HELD>;
   FlowSmem& W = X.W;
   double* coef = X.coef;
   const Lane& L = X.L;
@@ -949,7 +970,7 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
   if constexpr (CODE == OP_MUL || CODE == OP_MUL2 || CODE == OP_ADD || CODE == OP_SUB) {
     static_assert(DST >= SLOT_T && DST < SLOT_V, "stored results go to temporaries");
     const FR u = D[A], v = D[B];
-    const int raz = X.off_taz + (DST - SLOT_T) * NZP, rbz = X.off_tbz + (DST - SLOT_T) * NZP;
+    constexpr int raz = Q::off_taz + (DST - SLOT_T) * NZP, rbz = Q::off_tbz + (DST - SLOT_T) * NZP;
     constexpr bool mul = CODE == OP_MUL || CODE == OP_MUL2, sub = CODE == OP_SUB;
     double s1 = 0.0, s2 = 0.0;
 #pragma unroll
@@ -987,7 +1008,7 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
   } else if constexpr (CODE == OP_SUBK) {
     D[DST].c = D[DST].c - W.kc[B];
   } else if constexpr (CODE == OP_CONST) {
-    D[DST] = FR{W.kc[B], 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, W.off_zero, W.off_zero};
+    D[DST] = FR{W.kc[B], 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, Q::off_zero, Q::off_zero};
   } else if constexpr (CODE == OP_SCALE) {
     const FR u = D[A];
     const double s = W.kc[B];
@@ -1026,14 +1047,14 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
     const double fc_ = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at, fsz = zero ? 0.0 : f.sz, fsb = zero ? 0.0 : f.sb;
     const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
     const double* S = coef + i * NZP;
-    double* Pb = coef + W.pbz[i];
+    double* Pb = coef + Q::pbz(i);
     const double half_at = fat * 0.5;
     Iv rem = imul_0h(h * h, half_at);
     const double bb = fsb * h * h * 0.5;
     rem = iadd(rem, Iv{-bb, bb});
     rem = iadd(rem, imul(fr, Iv{0.0, h}));
     if (X.mode == MODE_PICARD) {
-      if (W.own[i]) {
+      if constexpr (Q::own(i)) {
 #pragma unroll
         for (int k = 0; k < NZC; ++k) {
           if (!L.act[k]) continue;
@@ -1067,12 +1088,12 @@ __device__ __noinline__ bool quad_full(FlowSmem& W, int mode, const Lane L, doub
 #pragma unroll
   for (int i = 0; i < NA; ++i) {
     const Slot& p = W.D[i];
-    D[i] = FR{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb, 1.0, i * NZP, W.pbz[i]};
+    D[i] = FR{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb, 1.0, i * NZP, QuadLayout<HELD>::pbz(i)};
   }
-  const FullCtx X{W, W.coef(), gM, L, mode, W.off_taz, W.off_tbz};
+  const FullCtx X{W, W.coef(), gM, L, mode};
   bool thrown = false;
   int pc = 0;
-#define RB_CT_FULL_OP(c, d, a, b) full_op<c, d, a, b>(D, X, pc++, thrown);
+#define RB_CT_FULL_OP(c, d, a, b) full_op<c, d, a, b, HELD>(D, X, pc++, thrown);
   if constexpr (HELD) {
     RB_CT_FULL_OP(OP_CONST, C_(0), 0, 8)
     RB_CT_FULL_OP(OP_CONST, C_(1), 0, 9)
