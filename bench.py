@@ -443,7 +443,8 @@ def ct_sweep(args, ctx, world, rank, dev, barrier, stream):
            "roofline": {"bound": "fp64", "achieved": ach, "peak": tf_fma, "unit": "TFLOP/s", "frac": ach / tf_fma,
                         "flops_per_reach_step": fl,
                         "note": "algorithmic flops of the reference's TMExpr op sequence (bench.ct_flops_per_step); "
-                                "the kernel is issue/latency-bound (profiles/r01_c2_summary.md)"}}
+                                "the kernel is instruction-fetch/latency-bound and its replays skip most of that work "
+                                "(profiles/r02_c2_summary.md)"}}
     if rank == 0 and world == 1:
         try:
             from oracle_bind import oracle_cl_split_hull, ref_available, ref_cl_split_hull, ref_lib
