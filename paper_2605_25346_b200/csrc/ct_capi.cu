@@ -12,6 +12,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -209,6 +210,9 @@ void load_program(const Program& p, int kind, int na, rb::ct::CTParams& P) {
     }
     if (!match) P.fast_prog = 0;
   }
+  // RB_CT_INTERPRET=1 runs every program through the interpreter (tests compare the two implementations)
+  if (const char* v = std::getenv("RB_CT_INTERPRET"))
+    if (v[0] == '1') P.fast_prog = 0;
 }
 
 // ClosedLoopSpec::validate (closed_loop.hpp:30-43) + the device family's limits.

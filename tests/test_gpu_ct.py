@@ -61,6 +61,20 @@ def test_cl_split_hull_matches_oracle():
     assert _close(got.hi, exp.hi, exp.lo, exp.hi) <= CT_RTOL
 
 
+@pytest.mark.parametrize("case", ct_cases(), ids=lambda c: c[0])
+def test_compiled_program_matches_interpreter(case, monkeypatch):
+    """The quadrotor field runs as compiled straight-line code (quad_full / quad_fast, ct_kernel.cuh);
+    RB_CT_INTERPRET=1 routes the same program through the interpreter.  Both implement the same
+    operation sequence: statuses, failed steps and box counts identical, boxes within 1e-11."""
+    name, spec, lo, hi, _ = case
+    got = cl_reach_batch_arrays(spec, lo, hi)
+    monkeypatch.setenv("RB_CT_INTERPRET", "1")
+    ref = cl_reach_batch_arrays(spec, lo, hi)
+    monkeypatch.delenv("RB_CT_INTERPRET")
+    worst = assert_ct_close(got, ref, rtol=1e-11)
+    print(f"{name}: compiled vs interpreted max rel diff {worst:.3e}")
+
+
 def test_cl_batch_rows_independent():
     """A sub-box's tube does not depend on the batch around it (bit-identical)."""
     w = c2_quadrotor()

@@ -26,6 +26,19 @@ def test_ct_matches_oracle(case):
     assert bool((got.status != 0).any()) == expect_fail
 
 
+@pytest.mark.parametrize("case", [c for c in ct_open_cases() if c[0].startswith("quad")], ids=lambda c: c[0])
+def test_compiled_quadrotor_matches_interpreter(case, monkeypatch):
+    """The held-input quadrotor field's compiled program (quad_full / quad_fast<HELD>) against the
+    interpreter (RB_CT_INTERPRET=1) on the same inputs: codes identical, boxes within 1e-11."""
+    name, f, lo, hi, prm, _ = case
+    got = ct_reach_batch_arrays(f, lo, hi, prm)
+    monkeypatch.setenv("RB_CT_INTERPRET", "1")
+    ref = ct_reach_batch_arrays(f, lo, hi, prm)
+    monkeypatch.delenv("RB_CT_INTERPRET")
+    worst = assert_ct_close(got, ref, rtol=1e-11)
+    print(f"{name}: compiled vs interpreted max rel diff {worst:.3e}")
+
+
 def test_zero_field_keeps_x0():  # test_flowpipe_ct.cpp:146-160
     lo, hi = np.array([0.4, -0.45]), np.array([0.6, -0.05])
     t = ct_reach(zero_field(2), (lo, hi), FlowpipeParams(h=0.05, steps=10))
