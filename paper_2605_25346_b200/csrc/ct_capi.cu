@@ -267,10 +267,15 @@ int setup_params(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s, l
 }
 
 // Dynamic shared memory of the flow kernel: the fixed part + S, the zero row,
-// the own Picard bz rows and the temporaries.
+// the own Picard bz rows and the temporaries; the compact layout (cl_reach
+// under the compiled quadrotor program) has a shorter header, 76-column rows
+// and no zero row (ct_kernel.cuh, kCompactHdr).
+bool flow_compact(const rb::ct::CTParams& P) { return !P.square && P.fast_prog == 1 && P.side != nullptr; }
 size_t flow_smem_bytes(const rb::ct::CTParams& P) {
   int npb = 0;
   for (int i = 0; i < P.na; ++i) npb += (P.bzsrc[i] == -1);
+  if (flow_compact(P))
+    return rb::ct::kCompactHdr + static_cast<size_t>(P.na + npb + 2 * rb::ct::NTF) * rb::ct::kRowC * 8;
   return sizeof(rb::ct::FlowSmem) + static_cast<size_t>(P.na + 1 + npb + 2 * rb::ct::NTF) * rb::ct::NZP * 8;
 }
 
@@ -280,7 +285,9 @@ int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
   const size_t flow_smem = flow_smem_bytes(P);
   const size_t ctl_smem = rb::ct::kCtlWarps * (sizeof(rb::ct::CtlSmem) + static_cast<size_t>(P.ctl.L - 1) *
                                                                            rb::ct::kMaxCtlW * 2 * sizeof(double));
-  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const bool cmp = flow_compact(P);
+  auto* flow = cmp ? rb::ct::ct_flow_kernel<false, true> : rb::ct::ct_flow_kernel<false, false>;
+  RB_CUDA(cudaFuncSetAttribute(flow, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(flow_smem)));
   RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_ctl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(ctl_smem)));
@@ -292,7 +299,7 @@ int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
     P.ci = ci;
     rb::ct::ct_ctl_kernel<<<ctl_grid, 32 * rb::ct::kCtlWarps, ctl_smem, ctx->stream>>>(P);
     RB_CUDA(cudaGetLastError());
-    rb::ct::ct_flow_kernel<false><<<P.B, 32, flow_smem, ctx->stream>>>(P);
+    flow<<<P.B, 32, flow_smem, ctx->stream>>>(P);
     RB_CUDA(cudaGetLastError());
   }
   rc = timed_end(ctx, stop);
@@ -338,7 +345,8 @@ int reach_cl_batch(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s,
   const size_t box_bytes = B * T * NA * 8, i_bytes = B * 4, x_bytes = B * n * 8;
   Carve cv;
   const size_t o_c = cv.take(B * NA * 8), o_M = cv.take(B * NA * rb::ct::NZP * 8), o_meta = cv.take(B * 16),
-               o_y = cv.take(std::max<size_t>(static_cast<size_t>(s->ctl_steps) * s->ref_dim * 8, 8));
+               o_y = cv.take(std::max<size_t>(static_cast<size_t>(s->ctl_steps) * s->ref_dim * 8, 8)),
+               o_side = cv.take(B * rb::ct::kSideBytes);
   size_t o_xl = 0, o_xh = 0, o_ol = 0, o_oh = 0, o_nb = 0, o_fs = 0, o_st = 0;
   if (!dev) {
     o_xl = cv.take(x_bytes);
@@ -355,6 +363,7 @@ int reach_cl_batch(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spec* s,
   P.st_c = reinterpret_cast<double*>(w + o_c);
   P.st_M = reinterpret_cast<double*>(w + o_M);
   P.st_meta = reinterpret_cast<int*>(w + o_meta);
+  P.side = reinterpret_cast<unsigned char*>(w + o_side);
   P.y_ref = reinterpret_cast<double*>(w + o_y);
   if (s->ref_dim > 0)
     RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.y_ref), s->y_ref, static_cast<size_t>(s->ctl_steps) * s->ref_dim * 8,
@@ -442,7 +451,7 @@ int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spe
   Carve cv;
   const size_t o_c = cv.take(B * NA * 8), o_M = cv.take(B * NA * rb::ct::NZP * 8), o_meta = cv.take(B * 16),
                o_y = cv.take(std::max<size_t>(static_cast<size_t>(s->ctl_steps) * s->ref_dim * 8, 8)),
-               o_kl = cv.take(cnt * 8), o_kh = cv.take(cnt * 8), o_nan = cv.take(cnt * 8), o_div = cv.take(T * 4),
+               o_side = cv.take(B * rb::ct::kSideBytes), o_kl = cv.take(cnt * 8), o_kh = cv.take(cnt * 8), o_nan = cv.take(cnt * 8), o_div = cv.take(T * 4),
                o_nb = cv.take(4), o_key = cv.take(8), o_lo = cv.take(cnt * 8), o_hi = cv.take(cnt * 8);
   rc = ensure_ws(ctx, cv.off);
   if (rc) return rc;
@@ -450,6 +459,7 @@ int reach_cl_split_hull(reach_ctx* ctx, const reach_net* ctl, const reach_cl_spe
   P.st_c = reinterpret_cast<double*>(w + o_c);
   P.st_M = reinterpret_cast<double*>(w + o_M);
   P.st_meta = reinterpret_cast<int*>(w + o_meta);
+  P.side = reinterpret_cast<unsigned char*>(w + o_side);
   P.y_ref = reinterpret_cast<double*>(w + o_y);
   P.hull_lo = reinterpret_cast<unsigned long long*>(w + o_kl);
   P.hull_hi = reinterpret_cast<unsigned long long*>(w + o_kh);
@@ -541,12 +551,12 @@ int ct_params(reach_ctx* ctx, const reach_field_desc* fd, const reach_flowpipe_p
 
 int launch_ct(reach_ctx* ctx, const rb::ct::CTParams& P) {
   const size_t smem = flow_smem_bytes(P);
-  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_flow_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   cudaEvent_t stop;
   int rc = timed_begin(ctx, &stop);
   if (rc) return rc;
-  rb::ct::ct_flow_kernel<true><<<P.B, 32, smem, ctx->stream>>>(P);
+  rb::ct::ct_flow_kernel<true, false><<<P.B, 32, smem, ctx->stream>>>(P);
   RB_CUDA(cudaGetLastError());
   rc = timed_end(ctx, stop);
   if (rc) return rc;

@@ -41,6 +41,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 #include "dt_common.cuh"
@@ -99,6 +100,7 @@ struct CTParams {
   double* st_c;  // [B][NA]
   double* st_M;  // [B][NA][NZP]
   int* st_meta;  // [B][4]: nq, status, failed_step, n_boxes
+  unsigned char* side;  // [B][kSideBytes]: the compact layout's interval rows + replay cache
   // outputs
   int T;  // boxes per tube (1 + ctl_steps * K)
   double* out_lo;
@@ -217,20 +219,37 @@ struct Slot {
 // (cl_reach: 25.6 KB -> 8 sub-boxes per SM).  The Picard bz / temporary rows
 // double as the scratch of the square fold.
 struct __align__(128) FlowSmem {
-  Slot D[NSLOT];
   double sc[NA];   // seed centre
   double ssz[NA];  // abs_z of the seed rows
   double ec[NA];   // endpoint centre
   double kc[kMaxKc];
-  Iv erem[NA], i0[NA], i1[NA], nx[NA];
   int pbz[NA];     // Picard bz row offset of row i
   int own[NA];     // row i owns its bz row
   int wid[8];      // queue block widths (square fold)
-  double2 fc[kFieldCache];  // per program entry: the result's (abs_z, abs_b) / a consumer's replay sum
   int na, off_zero, off_pbz, off_taz, off_tbz, pad;
-  __device__ __forceinline__ double* coef() { return reinterpret_cast<double*>(this + 1); }
+  Slot D[NSLOT];   // the compact layout keeps D[0, NA) only: the P slots
+  // full layout only (the compact layout keeps these in HBM, CTParams::side)
+  Iv erem_s[NA], i0_s[NA], i1_s[NA], nx_s[NA];
+  double2 fc_s[kFieldCache];  // per program entry: the result's (abs_z, abs_b) / a consumer's replay sum
 };
 static_assert(sizeof(FlowSmem) % 128 == 0, "coefficient rows start on a 128-byte line: a warp's 256-byte row segment is two smem wavefronts, not three");
+// The compact layout (cl_reach under the compiled quadrotor program, ct_flow_kernel<false, true>): the
+// header ends after the P slots, the rows are kRowC = 76 columns (n + window (n + l) <= 76 for window
+// <= 4) and there is no zero row: 22.1 KB per sub-box -> 10 sub-boxes per SM instead of 8.
+constexpr int kRowC = NX + 4 * NA;
+constexpr int kNoRow = -(1 << 20);  // "the zero row" in the compact layout: reads give 0
+constexpr size_t kCompactHdr = (offsetof(FlowSmem, D) + NA * sizeof(Slot) + 127) / 128 * 128;
+template <bool CMP>
+__device__ __forceinline__ double* flow_coef(FlowSmem& W) {
+  return reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&W) + (CMP ? kCompactHdr : sizeof(FlowSmem)));
+}
+// Per-step interval rows and the replay cache: in shared memory (full layout) or in the sub-box's HBM
+// block (compact layout; kSideBytes per sub-box).
+struct Side {
+  Iv *erem, *i0, *i1, *nx;
+  double2* fc;
+};
+constexpr size_t kSideBytes = 4 * NA * sizeof(Iv) + kFieldCache * sizeof(double2);
 
 struct Lane {
   int lane;
@@ -533,8 +552,8 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
   const double h = L.h;
   const int lane = L.lane;
   const bool fast = mode >= MODE_REPLAY_FAST, record = mode == MODE_REPLAY;
-  double* coef = W.coef();
-  double2* fc = W.fc;  // indexed by pc - prog
+  double* coef = flow_coef<false>(W);
+  double2* fc = W.fc_s;  // indexed by pc - prog
   TOp next = kProgs[prog];
   for (int pc = prog;; ++pc) {
     const TOp op = next;
@@ -658,7 +677,7 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
         double* Pb = coef + W.pbz[i];
         if (mode == MODE_ENDPOINT) {  // the rows were written by this step's full replay
           W.ec[i] = W.sc[i] + h * (fc_ + fat * h * 0.5);
-          W.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
+          W.erem_s[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
           break;
         }
         // tme_integrate(dx_i) remainder (taylor_model.hpp:436-443)
@@ -699,7 +718,7 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
           }
           const Slot& pk = W.D[i];
           const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
-          W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, s2, h), rem);
+          W.nx_s[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, s2, h), rem);
         }
         break;
       }
@@ -724,19 +743,22 @@ __device__ __noinline__ bool run_field(FlowSmem& W, int prog, int mode, const La
 // 12..15 of the augmented field have udot = 0 (bz = the zero row).  Constant
 // row offsets let the compiler prove which shared-memory rows an operation
 // touches and move the next operations' loads ahead of this one's stores.
-template <bool HELD>
+template <bool HELD, bool CMP = false>
 struct QuadLayout {
+  static constexpr int rs = CMP ? kRowC : NZP;  // row stride
   static constexpr int na = HELD ? NX : NA;
-  static constexpr int off_zero = na * NZP;
-  static constexpr int off_pbz = off_zero + NZP;
+  static constexpr int off_zero = CMP ? kNoRow : na * rs;
+  static constexpr int off_pbz = na * rs + (CMP ? 0 : rs);
   static constexpr int npb = 9;
-  static constexpr int off_taz = off_pbz + npb * NZP;
-  static constexpr int off_tbz = off_taz + NTF * NZP;
+  static constexpr int off_taz = off_pbz + npb * rs;
+  static constexpr int off_tbz = off_taz + NTF * rs;
   __host__ __device__ static constexpr int pbz(int i) {
-    return i < 3 ? (i + 3) * NZP : i < 12 ? off_pbz + (i - 3) * NZP : off_zero;
+    return i < 3 ? (i + 3) * rs : i < 12 ? off_pbz + (i - 3) * rs : off_zero;
   }
   __host__ __device__ static constexpr bool own(int i) { return i >= 3 && i < 12; }
 };
+// a coefficient of row `row` (kNoRow: the zero row, absent in the compact layout)
+__device__ __forceinline__ double rowv(const double* coef, int row, int j) { return row < 0 ? 0.0 : coef[row + j]; }
 
 struct FS {
   double c, at, rlo, rhi, sz, sb;
@@ -753,8 +775,8 @@ struct FS {
 // linearization point; the consumers from their cached constant parts.
 constexpr int kFastK = 6;
 template <int CODE, int DST, int A, int B, bool CACHED>
-__device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, double* K, int pc, int mode, double h,
-                                        bool& thrown, bool rec) {
+__device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, const Side& X, double* K, int pc, int mode,
+                                        double h, bool& thrown, bool rec) {
   double* k = K + pc * kFastK;
   if constexpr (CODE == OP_MUL || CODE == OP_MUL2) {  // the pair's second entry follows as an OP_MUL
     const FS u = D[A], v = D[B];
@@ -784,7 +806,7 @@ __device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, double* K, 
       D[DST].rlo = rem.lo;
       D[DST].rhi = rem.hi;
     } else {
-      const double2 s = W.fc[pc];
+      const double2 s = X.fc[pc];
       D[DST] = FS{u.c * v.c, u.c * v.at + v.c * u.at, rem.lo, rem.hi, s.x, s.y};
     }
   } else if constexpr (CODE == OP_ADD || CODE == OP_SUB) {
@@ -795,7 +817,7 @@ __device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, double* K, 
       D[DST].rlo = rem.lo;
       D[DST].rhi = rem.hi;
     } else {
-      const double2 s = W.fc[pc];
+      const double2 s = X.fc[pc];
       D[DST] = FS{sub ? a.c - b.c : a.c + b.c, sub ? a.at - b.at : a.at + b.at, rem.lo, rem.hi, s.x, s.y};
     }
   } else if constexpr (CODE == OP_SUBK) {
@@ -891,17 +913,17 @@ __device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, double* K, 
       ca = iadd(imul_0h(h * h, half_at), Iv{-bb, bb});
       const FS pk = D[i];
       const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
-      cb = poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, W.fc[pc].x, h);
+      cb = poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, X.fc[pc].x, h);
       if (rec) {
         k[0] = ca.lo; k[1] = ca.hi; k[2] = cb.lo; k[3] = cb.hi; k[4] = ec;
       }
     }
     if (mode == MODE_ENDPOINT) {
       W.ec[i] = ec;
-      W.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
+      X.erem[i] = iadd(imul(Iv{h, h}, fr), Iv{0.0, 0.0});
     } else {
       const Iv rem = iadd(ca, imul(fr, Iv{0.0, h}));
-      W.nx[i] = iadd(cb, rem);
+      X.nx[i] = iadd(cb, rem);
     }
   }
 }
@@ -909,19 +931,19 @@ __device__ __forceinline__ void fast_op(FS (&D)[NSLOT], FlowSmem& W, double* K, 
 // HELD: ct_reach's quadrotor field (inputs C0..3 from kc[8..11], four OP_CONST
 // entries first); else cl_reach's augmented field (inputs P12..15, udot = 0).
 // CACHED = false with rec: record the constants (lane 0) for the CACHED calls.
-template <bool HELD, bool CACHED>
-__device__ __noinline__ bool quad_fast(FlowSmem& W, int mode, double h, bool rec) {
+template <bool HELD, bool CACHED, bool CMP = false>
+__device__ __noinline__ bool quad_fast(FlowSmem& W, const Side X, int mode, double h, bool rec) {
   FS D[NSLOT];
 #pragma unroll
   for (int i = 0; i < NA; ++i) {
     const Slot& p = W.D[i];
     D[i] = FS{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb};
   }
-  double* K = W.coef() + QuadLayout<HELD>::off_taz;
+  double* K = flow_coef<CMP>(W) + QuadLayout<HELD, CMP>::off_taz;
   rec = rec && (threadIdx.x & 31) == 0;
   bool thrown = false;
   int pc = 0;
-#define RB_CT_FAST_OP(c, d, a, b) fast_op<c, d, a, b, CACHED>(D, W, K, pc++, mode, h, thrown, rec);
+#define RB_CT_FAST_OP(c, d, a, b) fast_op<c, d, a, b, CACHED>(D, W, X, K, pc++, mode, h, thrown, rec);
   if constexpr (HELD) {
     RB_CT_FAST_OP(OP_CONST, C_(0), 0, 8)
     RB_CT_FAST_OP(OP_CONST, C_(1), 0, 9)
@@ -957,10 +979,11 @@ struct FullCtx {
   double* gM;
   const Lane& L;
   int mode;
+  Side sd;
 };
-template <int CODE, int DST, int A, int B, bool HELD>
+template <int CODE, int DST, int A, int B, bool HELD, bool CMP>
 __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc, bool& thrown) {
-  using Q = QuadLayout<HELD>;
+  using Q = QuadLayout<HELD, CMP>;
   FlowSmem& W = X.W;
   double* coef = X.coef;
   const Lane& L = X.L;
@@ -970,7 +993,7 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
   if constexpr (CODE == OP_MUL || CODE == OP_MUL2 || CODE == OP_ADD || CODE == OP_SUB) {
     static_assert(DST >= SLOT_T && DST < SLOT_V, "stored results go to temporaries");
     const FR u = D[A], v = D[B];
-    constexpr int raz = Q::off_taz + (DST - SLOT_T) * NZP, rbz = Q::off_tbz + (DST - SLOT_T) * NZP;
+    constexpr int raz = Q::off_taz + (DST - SLOT_T) * Q::rs, rbz = Q::off_tbz + (DST - SLOT_T) * Q::rs;
     constexpr bool mul = CODE == OP_MUL || CODE == OP_MUL2, sub = CODE == OP_SUB;
     double s1 = 0.0, s2 = 0.0;
 #pragma unroll
@@ -979,8 +1002,10 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
       const int j = lane + 32 * k;
       // stored rows (P, T, C slots) have scale 1: x * 1.0 == x, so only views multiply
       constexpr bool uv = A >= SLOT_V && A < SLOT_C, vv = B >= SLOT_V && B < SLOT_C;
-      const double ua = uv ? coef[u.az + j] * u.s : coef[u.az + j], ub = uv ? coef[u.bz + j] * u.s : coef[u.bz + j];
-      const double va = vv ? coef[v.az + j] * v.s : coef[v.az + j], vb = vv ? coef[v.bz + j] * v.s : coef[v.bz + j];
+      const double uaz = rowv(coef, u.az, j), ubz = rowv(coef, u.bz, j);
+      const double vaz = rowv(coef, v.az, j), vbz = rowv(coef, v.bz, j);
+      const double ua = uv ? uaz * u.s : uaz, ub = uv ? ubz * u.s : ubz;
+      const double va = vv ? vaz * v.s : vaz, vb = vv ? vbz * v.s : vbz;
       double ra, rb;
       if constexpr (mul) {
         ra = u.c * va + v.c * ua;
@@ -1004,7 +1029,7 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
       r = FR{sub ? u.c - v.c : u.c + v.c, sub ? u.at - v.at : u.at + v.at, rem.lo, rem.hi, s1, s2, 1.0, raz, rbz};
     }
     D[DST] = r;
-    if (record && lane == 0) W.fc[pc] = make_double2(s1, s2);
+    if (record && lane == 0) X.sd.fc[pc] = make_double2(s1, s2);
   } else if constexpr (CODE == OP_SUBK) {
     D[DST].c = D[DST].c - W.kc[B];
   } else if constexpr (CODE == OP_CONST) {
@@ -1046,8 +1071,8 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
     const FR f = D[zero ? 0 : A];
     const double fc_ = zero ? 0.0 : f.c, fat = zero ? 0.0 : f.at, fsz = zero ? 0.0 : f.sz, fsb = zero ? 0.0 : f.sb;
     const Iv fr = zero ? Iv{0.0, 0.0} : Iv{f.rlo, f.rhi};
-    const double* S = coef + i * NZP;
-    double* Pb = coef + Q::pbz(i);
+    const double* S = coef + i * Q::rs;
+    double* Pb = coef + (Q::pbz(i) < 0 ? 0 : Q::pbz(i));
     const double half_at = fat * 0.5;
     Iv rem = imul_0h(h * h, half_at);
     const double bb = fsb * h * h * 0.5;
@@ -1059,7 +1084,7 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
         for (int k = 0; k < NZC; ++k) {
           if (!L.act[k]) continue;
           const int j = lane + 32 * k;
-          Pb[j] = zero ? 0.0 : coef[f.az + j] * f.s;
+          Pb[j] = zero ? 0.0 : rowv(coef, f.az, j) * f.s;
         }
       }
       set_scalars(W.D[i], W.sc[i], fc_, rem, W.ssz[i], fsz);
@@ -1069,31 +1094,32 @@ __device__ __forceinline__ void full_op(FR (&D)[NSLOT], const FullCtx& X, int pc
       for (int k = 0; k < NZC; ++k) {
         if (!L.act[k]) continue;
         const int j = lane + 32 * k;
-        const double fa = zero ? 0.0 : coef[f.az + j] * f.s, fb = zero ? 0.0 : coef[f.bz + j] * f.s;
-        s2 += fabs(fa - Pb[j]);
+        const double fa = zero ? 0.0 : rowv(coef, f.az, j) * f.s, fb = zero ? 0.0 : rowv(coef, f.bz, j) * f.s;
+        s2 += fabs(fa - (Q::pbz(i) < 0 ? 0.0 : Pb[j]));
         X.gM[i * NZP + j] = S[j] + h * (fa + fb * h * 0.5);
       }
       s2 = wsum(s2);
-      if (lane == 0) W.fc[pc] = make_double2(s2, 0.0);
+      if (lane == 0) X.sd.fc[pc] = make_double2(s2, 0.0);
       const FR pk = D[i];
       const double zr = isfinite(W.ssz[i]) ? 0.0 : W.ssz[i] - W.ssz[i];
-      W.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, s2, h), rem);
+      X.sd.nx[i] = iadd(poly_range(W.sc[i] - pk.c, zr, fc_ - pk.at, s2, h), rem);
     }
   }
 }
 
-template <bool HELD>
-__device__ __noinline__ bool quad_full(FlowSmem& W, int mode, const Lane L, double* gM) {
+template <bool HELD, bool CMP = false>
+__device__ __noinline__ bool quad_full(FlowSmem& W, const Side sd, int mode, const Lane L, double* gM) {
+  using Q = QuadLayout<HELD, CMP>;
   FR D[NSLOT];
 #pragma unroll
   for (int i = 0; i < NA; ++i) {
     const Slot& p = W.D[i];
-    D[i] = FR{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb, 1.0, i * NZP, QuadLayout<HELD>::pbz(i)};
+    D[i] = FR{p.c, p.at, p.rlo, p.rhi, p.sz, p.sb, 1.0, i * Q::rs, Q::pbz(i)};
   }
-  const FullCtx X{W, W.coef(), gM, L, mode};
+  const FullCtx X{W, flow_coef<CMP>(W), gM, L, mode, sd};
   bool thrown = false;
   int pc = 0;
-#define RB_CT_FULL_OP(c, d, a, b) full_op<c, d, a, b, HELD>(D, X, pc++, thrown);
+#define RB_CT_FULL_OP(c, d, a, b) full_op<c, d, a, b, HELD, CMP>(D, X, pc++, thrown);
   if constexpr (HELD) {
     RB_CT_FULL_OP(OP_CONST, C_(0), 0, 8)
     RB_CT_FULL_OP(OP_CONST, C_(1), 0, 9)
@@ -1173,13 +1199,14 @@ __device__ __forceinline__ void x0_box(const CTParams& P, long long b, int d, do
 // The oldest block's row sums are taken first and the fresh block is written
 // after the shift, so rows never exceed nz columns: newest(i,i) = rad_i +
 // row_abs_sum(oldest, i), the reference's one addition.  Lane i sweeps row i.
+template <int RS>
 __device__ __forceinline__ void push_fresh_fold(double* S, const Iv* erem, int na, int p0, int& nz, int& nq, int cap,
                                                 int lane) {
   __syncwarp();
   const bool fold = nq + 1 > cap;
   double add = 0.0;
   if (fold && lane < na)
-    for (int j = 0; j < na; ++j) add += fabs(S[lane * NZP + p0 + j]);
+    for (int j = 0; j < na; ++j) add += fabs(S[lane * RS + p0 + j]);
   __syncwarp();
   if (fold) {
     for (int i = 0; i < na; ++i) {
@@ -1187,13 +1214,13 @@ __device__ __forceinline__ void push_fresh_fold(double* S, const Iv* erem, int n
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
         const int j = lane + 32 * k;
-        v[k] = (j >= p0 && j + na < nz) ? S[i * NZP + j + na] : 0.0;
+        v[k] = (j >= p0 && j + na < nz) ? S[i * RS + j + na] : 0.0;
       }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
         const int j = lane + 32 * k;
-        if (j >= p0 && j < nz) S[i * NZP + j] = v[k];
+        if (j >= p0 && j < nz) S[i * RS + j] = v[k];
       }
     }
     nz -= na;
@@ -1206,7 +1233,7 @@ __device__ __forceinline__ void push_fresh_fold(double* S, const Iv* erem, int n
 #pragma unroll
     for (int k = 0; k < NZC; ++k) {
       const int j = lane + 32 * k;
-      if (j >= nz && j < nz + na) S[i * NZP + j] = (j - nz == i) ? (fold ? rad + ai : rad) : 0.0;
+      if (j >= nz && j < nz + na) S[i * RS + j] = (j - nz == i) ? (fold ? rad + ai : rad) : 0.0;
     }
   }
   nz += na;
@@ -1377,11 +1404,16 @@ __device__ __noinline__ void push_fresh_fold_square(double* S, const Iv* erem, i
 // true).  Two instantiations: the square fold's shuffles otherwise cost the
 // cl_reach kernel the compiler's proof of warp convergence (collective
 // shuffle fallbacks everywhere, +35 % time).
-template <bool SQUARE>
-__global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
+#ifndef RB_CT_FLOW_MINB
+#define RB_CT_FLOW_MINB 10  // compact layout: 10 sub-boxes per SM (<= 200 registers)
+#endif
+template <bool SQUARE, bool CMP>
+__global__ void __launch_bounds__(32, CMP ? RB_CT_FLOW_MINB : 1) ct_flow_kernel(const CTParams Pm) {
   extern __shared__ __align__(16) unsigned char ct_smem[];
   FlowSmem& W = *reinterpret_cast<FlowSmem*>(ct_smem);
-  double* coef = W.coef();
+  static_assert(!(SQUARE && CMP), "the compact layout is cl_reach's");
+  constexpr int RS = CMP ? kRowC : NZP;  // shared-memory row stride (the HBM state keeps NZP)
+  double* coef = flow_coef<CMP>(W);
   const long long b = blockIdx.x;
   if (b >= Pm.B) return;
   const int lane = threadIdx.x;
@@ -1404,11 +1436,19 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
   const int cap = Pm.window > 0 ? Pm.window : 1;
   int nz = p0 + nq * Pm.bw;
   double* gM = Pm.st_M + static_cast<size_t>(b) * NA * NZP;
+  Side sd;
+  if constexpr (CMP) {
+    unsigned char* g = Pm.side + static_cast<size_t>(b) * kSideBytes;
+    sd = Side{reinterpret_cast<Iv*>(g), reinterpret_cast<Iv*>(g) + NA, reinterpret_cast<Iv*>(g) + 2 * NA,
+              reinterpret_cast<Iv*>(g) + 3 * NA, reinterpret_cast<double2*>(g + 4 * NA * sizeof(Iv))};
+  } else {
+    sd = Side{W.erem_s, W.i0_s, W.i1_s, W.nx_s, W.fc_s};
+  }
   // ---- the field program, its constants and the row layout
   int npb = 0;
   for (int i = 0; i < na; ++i) npb += (Pm.bzsrc[i] == -1);
-  const int off_zero = na * NZP, off_pbz = off_zero + NZP, off_taz = off_pbz + npb * NZP,
-            off_tbz = off_taz + NTF * NZP, coef_end = off_tbz + NTF * NZP;
+  const int off_zero = CMP ? kNoRow : na * RS, off_pbz = na * RS + (CMP ? 0 : RS), off_taz = off_pbz + npb * RS,
+            off_tbz = off_taz + NTF * RS, coef_end = off_tbz + NTF * RS;
   if (lane < kMaxKc) W.kc[lane] = Pm.kc[lane];
   if (lane == 0) {
     W.na = na;
@@ -1420,17 +1460,17 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     for (int i = 0; i < na; ++i) {
       const int src = Pm.bzsrc[i];
       W.own[i] = (src == -1);
-      W.pbz[i] = (src == -1) ? off_pbz + (q++) * NZP : (src == -2) ? off_zero : src * NZP;
+      W.pbz[i] = (src == -1) ? off_pbz + (q++) * RS : (src == -2) ? off_zero : src * RS;
     }
     for (int i = 0; i < 8; ++i) W.wid[i] = Pm.bw;
   }
-  for (int s = lane; s < NSLOT; s += 32) {
+  for (int s = lane; s < (CMP ? NA : NSLOT); s += 32) {  // the compact header holds the P slots only
     Slot& d = W.D[s];
     d.s1 = 1.0;
     d.s2 = 1.0;
     d.view = 0;
-    d.az = (s < SLOT_T) ? s * NZP : (s < SLOT_V) ? off_taz + (s - SLOT_T) * NZP : off_zero;
-    d.bz = (s < SLOT_V && s >= SLOT_T) ? off_tbz + (s - SLOT_T) * NZP : off_zero;
+    d.az = (s < SLOT_T) ? s * RS : (s < SLOT_V) ? off_taz + (s - SLOT_T) * RS : off_zero;
+    d.bz = (s < SLOT_V && s >= SLOT_T) ? off_tbz + (s - SLOT_T) * RS : off_zero;
   }
   // ---- the state: from X0 (ct_reach, init_symbolic_state, flowpipe_ct.hpp:302-309) or HBM
   for (int t = lane; t < coef_end; t += 32) coef[t] = 0.0;
@@ -1442,7 +1482,7 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     if (lane < na) {
       x0_box(Pm, b, lane, lo, hi);
       W.sc[lane] = (lo + hi) * 0.5;
-      coef[lane * NZP + lane] = (hi - lo) * 0.5;
+      coef[lane * RS + lane] = (hi - lo) * 0.5;
       emit_box(Pm, b, 0, na, lane, lo, hi);  // box 0 is X0 itself (flowpipe_ct.hpp:433)
     }
     nboxes = 1;
@@ -1451,7 +1491,7 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
 #pragma unroll
       for (int k = 0; k < NZC; ++k) {
         const int j = lane + 32 * k;
-        if (j < nz) coef[i * NZP + j] = gM[i * NZP + j];
+        if (j < nz) coef[i * RS + j] = gM[i * NZP + j];
       }
     if (lane < na) W.sc[lane] = Pm.st_c[b * NA + lane];
   }
@@ -1472,7 +1512,7 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
         v[i] = 0.0;
 #pragma unroll
         for (int k = 0; k < NZC; ++k)
-          if (i < na && L.act[k]) v[i] += fabs(coef[i * NZP + lane + 32 * k]);
+          if (i < na && L.act[k]) v[i] += fabs(coef[i * RS + lane + 32 * k]);
       }
       const double sum = wsum16_rows(v, lane);
       if ((lane & 1) == 0 && row_of_wsum16(lane) < na) W.ssz[row_of_wsum16(lane)] = sum;
@@ -1489,9 +1529,13 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     }
     bool thrown = false;
     auto full_field = [&](int mode) {
-      if (Pm.fast_prog == 1) return quad_full<false>(W, mode, L, gM);
-      if (Pm.fast_prog == 2) return quad_full<true>(W, mode, L, gM);
-      return run_field(W, Pm.prog, mode, L, gM);
+      if constexpr (CMP) {
+        return quad_full<false, true>(W, sd, mode, L, gM);
+      } else {
+        if (Pm.fast_prog == 1) return quad_full<false>(W, sd, mode, L, gM);
+        if (Pm.fast_prog == 2) return quad_full<true>(W, sd, mode, L, gM);
+        return run_field(W, Pm.prog, mode, L, gM);
+      }
     };
     for (int it = 0; it < Pm.order && !thrown; ++it) {
       thrown = full_field(MODE_PICARD);
@@ -1506,12 +1550,16 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     int nrec = 0;  // 0: nothing recorded yet; 1: quad_fast's constants recorded (the temporaries' rows)
     auto fast_field = [&](int mode) {
       bool t;
-      if (Pm.fast_prog == 1)
-        t = nrec ? quad_fast<false, true>(W, mode, h, false) : quad_fast<false, false>(W, mode, h, true);
-      else if (Pm.fast_prog == 2)
-        t = nrec ? quad_fast<true, true>(W, mode, h, false) : quad_fast<true, false>(W, mode, h, true);
-      else
-        t = run_field(W, Pm.prog, mode, L, gM);
+      if constexpr (CMP) {
+        t = nrec ? quad_fast<false, true, true>(W, sd, mode, h, false) : quad_fast<false, false, true>(W, sd, mode, h, true);
+      } else {
+        if (Pm.fast_prog == 1)
+          t = nrec ? quad_fast<false, true>(W, sd, mode, h, false) : quad_fast<false, false>(W, sd, mode, h, true);
+        else if (Pm.fast_prog == 2)
+          t = nrec ? quad_fast<true, true>(W, sd, mode, h, false) : quad_fast<true, false>(W, sd, mode, h, true);
+        else
+          t = run_field(W, Pm.prog, mode, L, gM);
+      }
       nrec = 1;
       return t;
     };
@@ -1532,23 +1580,23 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     };
     if (fail == CT_OK) {
       if (row) {
-        W.i0[lane] = Iv{-Pm.eps, Pm.eps};
-        W.i1[lane] = Iv{0.0, 0.0};
+        sd.i0[lane] = Iv{-Pm.eps, Pm.eps};
+        sd.i1[lane] = Iv{0.0, 0.0};
       }
       bool accepted = false;
       for (int attempt = 0; attempt <= Pm.maxe; ++attempt) {
-        const bool threw = replay(W.i0);
-        if (!threw && row) W.i1[lane] = W.nx[lane];
-        if (!threw && finite_box(W.i1) && subset(W.i1, W.i0)) {
+        const bool threw = replay(sd.i0);
+        if (!threw && row) sd.i1[lane] = sd.nx[lane];
+        if (!threw && finite_box(sd.i1) && subset(sd.i1, sd.i0)) {
           accepted = true;
           break;
         }
         if (row) {  // per-dimension adaptive enlargement (:178-182)
-          const Iv ind = threw ? Iv{0.0, 0.0} : W.i1[lane];
-          const Iv cur = W.i0[lane];
+          const Iv ind = threw ? Iv{0.0, 0.0} : sd.i1[lane];
+          const Iv cur = sd.i0[lane];
           const Iv hull = (ind.lo <= ind.hi) ? Iv{smin(cur.lo, ind.lo), smax(cur.hi, ind.hi)} : cur;
           const double mid = (hull.lo + hull.hi) * 0.5, rad = (hull.hi - hull.lo) * 0.5 * Pm.enl;
-          W.i0[lane] = Iv{mid - rad, mid + rad};
+          sd.i0[lane] = Iv{mid - rad, mid + rad};
         }
         __syncwarp();
       }
@@ -1557,18 +1605,18 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
     }
     if (fail == CT_OK) {
       for (int round = 0; round < Pm.refine; ++round) {  // shrink (:214-223)
-        if (replay(W.i1)) break;
-        if (!(finite_box(W.nx) && subset(W.nx, W.i1))) break;
-        if (row) W.i1[lane] = W.nx[lane];
+        if (replay(sd.i1)) break;
+        if (!(finite_box(sd.nx) && subset(sd.nx, sd.i1))) break;
+        if (row) sd.i1[lane] = sd.nx[lane];
       }
       // endpoint by exact integration at tau = h (:236-263) into the HBM state rows
       if (row) {
-        W.D[lane].rlo = W.i1[lane].lo;
-        W.D[lane].rhi = W.i1[lane].hi;
+        W.D[lane].rlo = sd.i1[lane].lo;
+        W.D[lane].rhi = sd.i1[lane].hi;
       }
       __syncwarp();
       const bool threw = fast_field(MODE_ENDPOINT);
-      const bool exact_ok = !threw && finite_box(W.erem) && __all_sync(0xffffffffu, !row || isfinite(W.ec[lane]));
+      const bool exact_ok = !threw && finite_box(sd.erem) && __all_sync(0xffffffffu, !row || isfinite(W.ec[lane]));
       // tm_eval_interval(segment, [0, h]) (taylor_model.hpp:73-97), before S changes; lane i: row i
       const int kbox = 1 + gstep;
       double blo = 0.0, bhi = 0.0;
@@ -1578,7 +1626,7 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
         acc = iadd(acc, iscale(p.at, Iv{0.0, h}));
         const double tau_mag = smax(0.0, h);
         acc = iadd(acc, Iv{-p.sb * tau_mag, p.sb * tau_mag});
-        acc = iadd(acc, W.i1[lane]);
+        acc = iadd(acc, sd.i1[lane]);
         blo = acc.lo;
         bhi = acc.hi;
       }
@@ -1594,10 +1642,10 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
           for (int k = 0; k < NZC; ++k) {
             if (!L.act[k]) continue;
             const int j = lane + 32 * k;
-            gM[i * NZP + j] = coef[i * NZP + j] + coef[W.pbz[i] + j] * h;
+            gM[i * NZP + j] = coef[i * RS + j] + rowv(coef, W.pbz[i], j) * h;
           }
           W.ec[i] = W.D[i].c + W.D[i].at * h;
-          W.erem[i] = W.i1[i];
+          sd.erem[i] = sd.i1[i];
         }
       }
       for (int i = 0; i < na; ++i)
@@ -1605,18 +1653,18 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
         for (int k = 0; k < NZC; ++k) {
           if (!L.act[k]) continue;
           const int j = lane + 32 * k;
-          coef[i * NZP + j] = gM[i * NZP + j];
+          coef[i * RS + j] = gM[i * NZP + j];
         }
       if (!fin) {
         fail = CT_BOX;
       } else {
         // symbolic_step (flowpipe_ct.hpp:378-409)
         double c_new = 0.0;
-        if (lane < na) c_new = W.ec[lane] + (W.erem[lane].lo + W.erem[lane].hi) * 0.5;
+        if (lane < na) c_new = W.ec[lane] + (sd.erem[lane].lo + sd.erem[lane].hi) * 0.5;
         if constexpr (SQUARE)
-          push_fresh_fold_square(coef, W.erem, na, nz, nq, cap, coef + off_pbz, lane);
+          push_fresh_fold_square(coef, sd.erem, na, nz, nq, cap, coef + off_pbz, lane);
         else
-          push_fresh_fold(coef, W.erem, na, p0, nz, nq, cap, lane);
+          push_fresh_fold<RS>(coef, sd.erem, na, p0, nz, nq, cap, lane);
         if (lane < na) W.sc[lane] = c_new;
         __syncwarp();
       }
@@ -1632,7 +1680,7 @@ __global__ void __launch_bounds__(32) ct_flow_kernel(const CTParams Pm) {
 #pragma unroll
     for (int k = 0; k < NZC; ++k) {
       const int j = lane + 32 * k;
-      if (j < NZP) gM[i * NZP + j] = (j < nz) ? coef[i * NZP + j] : 0.0;
+      if (j < NZP) gM[i * NZP + j] = (j < nz) ? coef[i * RS + j] : 0.0;
     }
   if (lane < na) Pm.st_c[b * NA + lane] = W.sc[lane];
   if (lane == 0) {
