@@ -1405,7 +1405,7 @@ __device__ __noinline__ void push_fresh_fold_square(double* S, const Iv* erem, i
 // cl_reach kernel the compiler's proof of warp convergence (collective
 // shuffle fallbacks everywhere, +35 % time).
 #ifndef RB_CT_FLOW_MINB
-#define RB_CT_FLOW_MINB 10  // compact layout: 10 sub-boxes per SM (<= 200 registers)
+#define RB_CT_FLOW_MINB 10  // compact layout: 10 sub-boxes per SM -> 3 warps per scheduler: <= 168 registers (16 K per SMSP)
 #endif
 template <bool SQUARE, bool CMP>
 __global__ void __launch_bounds__(32, CMP ? RB_CT_FLOW_MINB : 1) ct_flow_kernel(const CTParams Pm) {
