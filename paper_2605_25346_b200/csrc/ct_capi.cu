@@ -283,13 +283,17 @@ int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
   int prc = ensure_programs(ctx);
   if (prc) return prc;
   const size_t flow_smem = flow_smem_bytes(P);
-  const size_t ctl_smem = rb::ct::kCtlWarps * (sizeof(rb::ct::CtlSmem) + static_cast<size_t>(P.ctl.L - 1) *
-                                                                           rb::ct::kMaxCtlW * 2 * sizeof(double));
+  int cw = P.ctl.dims[0];  // widest controller layer (and input): the 64-wide buffers fit 12 warps per SM
+  for (int t = 1; t < P.ctl.L; ++t) cw = std::max(cw, P.ctl.dims[t]);
+  const bool narrow = cw <= 64;
+  auto* ctlk = narrow ? rb::ct::ct_ctl_kernel<64> : rb::ct::ct_ctl_kernel<rb::ct::kMaxCtlW>;
+  const size_t ctl_smem = rb::ct::kCtlWarps * (narrow ? rb::ct::ctl_warp_bytes<64>(P.ctl.L)
+                                                      : rb::ct::ctl_warp_bytes<rb::ct::kMaxCtlW>(P.ctl.L));
   const bool cmp = flow_compact(P);
   auto* flow = cmp ? rb::ct::ct_flow_kernel<false, true> : rb::ct::ct_flow_kernel<false, false>;
   RB_CUDA(cudaFuncSetAttribute(flow, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(flow_smem)));
-  RB_CUDA(cudaFuncSetAttribute(rb::ct::ct_ctl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RB_CUDA(cudaFuncSetAttribute(ctlk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(ctl_smem)));
   cudaEvent_t stop;
   int rc = timed_begin(ctx, &stop);
@@ -297,7 +301,7 @@ int launch_cl(reach_ctx* ctx, rb::ct::CTParams& P) {
   const int ctl_grid = (P.B + rb::ct::kCtlWarps - 1) / rb::ct::kCtlWarps;
   for (int ci = 0; ci < P.ctl_steps; ++ci) {
     P.ci = ci;
-    rb::ct::ct_ctl_kernel<<<ctl_grid, 32 * rb::ct::kCtlWarps, ctl_smem, ctx->stream>>>(P);
+    ctlk<<<ctl_grid, 32 * rb::ct::kCtlWarps, ctl_smem, ctx->stream>>>(P);
     RB_CUDA(cudaGetLastError());
     flow<<<P.B, 32, flow_smem, ctx->stream>>>(P);
     RB_CUDA(cudaGetLastError());

@@ -1697,17 +1697,25 @@ __global__ void __launch_bounds__(32, CMP ? RB_CT_FLOW_MINB : 1) ct_flow_kernel(
 // sub-box.  Weights are read from the uploaded blob (W row-major, W^T) through
 // L1/L2: the controller is small and certified once per control interval.
 // Per warp: this struct, then the preactivation boxes of the controller's
-// hidden layers, [L - 1][kMaxCtlW][2] (sized by the host: ctl_warp_bytes).
+// hidden layers, [L - 1][CW][2] (sized by the host).  CW is the widest
+// controller layer rounded up to 64 or 128: the C2 controller (3 x 64) takes
+// 18.8 KB per warp -> 12 sub-boxes per SM (8 with 128-wide buffers).
+template <int CW>
 struct __align__(16) CtlSmem {
+  static constexpr int LA = CW > NZP ? CW : NZP;  // Lambda rows double as the 4 x nzx Lambda_z scratch
   double xA[NX * LDX];           // state TM rows (n x nzx), stride LDX
   double xc[NX];
-  double hb[2][kMaxCtlW][2];     // IBP boxes
-  double lam[2][4][kMaxCtlW];    // Lambda (n_o x width), double buffered
-  double bf0[kMaxCtlW];          // frozen first-layer bias
+  double hb[2][CW][2];           // IBP boxes
+  double lam[2][4][LA];          // Lambda (n_o x width), double buffered
+  double bf0[CW];                // frozen first-layer bias
   double blo[4], bup[4];
   double uc[4];
   Iv urem[4];
 };
+template <int CW>
+__host__ __device__ constexpr size_t ctl_warp_bytes(int layers) {
+  return sizeof(CtlSmem<CW>) + static_cast<size_t>(layers - 1) * CW * 2 * sizeof(double);
+}
 
 constexpr int kCtlWarps = 4;
 constexpr int kCtlPrefetch = 16;  // controller weights loaded a chunk ahead of their accumulation chain
@@ -1720,12 +1728,13 @@ __device__ __forceinline__ void relax_tanh_or_relu(int act, double l, double u, 
   relax(act, l, u, s, li, ui);
 }
 
+template <int CW>
 __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams Pm) {
   extern __shared__ __align__(16) unsigned char ct_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t warp_bytes = sizeof(CtlSmem) + static_cast<size_t>(Pm.ctl.L - 1) * kMaxCtlW * 2 * sizeof(double);
-  CtlSmem& W = *reinterpret_cast<CtlSmem*>(ct_smem + warp * warp_bytes);
-  double* pre = reinterpret_cast<double*>(&W + 1);  // [L - 1][kMaxCtlW][2]
+  CtlSmem<CW>& W = *reinterpret_cast<CtlSmem<CW>*>(ct_smem + warp * ctl_warp_bytes<CW>(Pm.ctl.L));
+  double* pre = reinterpret_cast<double*>(&W + 1);  // [L - 1][CW][2]
+  constexpr int LA = CtlSmem<CW>::LA;
   const long long b = static_cast<long long>(blockIdx.x) * kCtlWarps + warp;
   if (b >= Pm.B) return;
   const int n = Pm.n, l = Pm.l;
@@ -1872,8 +1881,8 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
       const double bias = (t == 0) ? W.bf0[u] : blob[N.b_off[t] + u];
       lo = lo + bias;
       hi = hi + bias;
-      pre[(t * kMaxCtlW + u) * 2] = lo;
-      pre[(t * kMaxCtlW + u) * 2 + 1] = hi;
+      pre[(t * CW + u) * 2] = lo;
+      pre[(t * CW + u) * 2 + 1] = hi;
       W.hb[cur ^ 1][u][0] = act_apply(N.acts[t], lo);
       W.hb[cur ^ 1][u][1] = act_apply(N.acts[t], hi);
     }
@@ -1899,14 +1908,14 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     // relax_activation (neural.hpp:166-227) per unit; non-finite -> throw
     for (int u = lane; u < width; u += 32) {
       double s, li, ui;
-      const double pl = pre[(t * kMaxCtlW + u) * 2], ph = pre[(t * kMaxCtlW + u) * 2 + 1];
+      const double pl = pre[(t * CW + u) * 2], ph = pre[(t * CW + u) * 2 + 1];
       if (!(isfinite(pl) && isfinite(ph))) {
         bad = true;
         s = li = ui = 0.0;
       } else {
         relax(N.acts[t], pl, ph, s, li, ui);
       }
-      pre[(t * kMaxCtlW + u) * 2] = s;
+      pre[(t * CW + u) * 2] = s;
       W.hb[0][u][0] = li;
       W.hb[0][u][1] = ui;
     }
@@ -1926,7 +1935,7 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
           bl = bl + aij * ui;
           bu = bu + aij * li;
         }
-        W.lam[lb][lane][j] = aij * pre[(t * kMaxCtlW + j) * 2];
+        W.lam[lb][lane][j] = aij * pre[(t * CW + j) * 2];
       }
       // shift = Lambda . b (linalg.hpp:40-51), b += shift
       const double* bias = (t == 0) ? W.bf0 : blob + N.b_off[t];
@@ -1994,7 +2003,7 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (i < no) S[i * kMaxCtlW + jc] = acc[i];
+      if (i < no) S[i * LA + jc] = acc[i];
   }
   __syncwarp();
   bool ufin = true;
@@ -2014,7 +2023,7 @@ __global__ void __launch_bounds__(32 * kCtlWarps) ct_ctl_kernel(const CTParams P
   // (flowpipe_ct.hpp:347-348; G0 = (n + l) x n is never square) boxes the
   // oldest block (columns [n, n + NA)) into the fresh block's diagonal and
   // drops it, so the rows are written in their folded layout directly.
-  auto stacked = [&](int d, int j) { return (d < n) ? W.xA[d * LDX + j] : S[(d - n) * kMaxCtlW + j]; };
+  auto stacked = [&](int d, int j) { return (d < n) ? W.xA[d * LDX + j] : S[(d - n) * LA + j]; };
   const bool fold = nbw + 1 > cap;
   const int nz_keep = fold ? nzx - NA : nzx;
   const int nqn = fold ? nbw : nbw + 1;
