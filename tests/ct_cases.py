@@ -53,6 +53,10 @@ def ct_cases():
                           fp=FlowpipeParams(h=0.01))
     x0 = np.array([0.3] * 3 + [0.05] * 3 + [0.02] * 6)
     out.append(("ref_test_shape", spec, (-x0)[None], x0[None], False))
+    # a controller wider than 64 (the 128-wide certification buffers, ct_ctl_kernel<128>)
+    rng = np.random.default_rng(4242)
+    ctlw = quadrotor_controller(rng, hidden=(96, 80))
+    out.append(("wide_ctl", _with(short, controller=ctlw), lo[:2], hi[:2], False))
     # failures: remainder never contractive; tme_inv on a cos(theta) range through 0; blow-up
     out.append(("remainder_fail", _with(short, fp_eps_init=1e-14, fp_max_enlargements=0), lo[:2], hi[:2], True))
     tl, th = lo[:2].copy(), hi[:2].copy()
