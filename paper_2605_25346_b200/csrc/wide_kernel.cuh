@@ -595,23 +595,24 @@ static __device__ void wide_fold(double* S, long long lds, int n, int& base, int
           }
         }
       }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        const double ov = __shfl_down_sync(0xffffffffu, bv, off);
-        const int oi = __shfl_down_sync(0xffffffffu, bi, off);
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
+      {
+        // warp argmax on (|a|, -row) with three redux.sync (342 -> ~100 cycles against five
+        // shuffle rounds, tools/ubench/lat_chain.cu): |a| >= 0 orders as its IEEE bits; a lane
+        // without a candidate sends key 0 (= +0.0), which never beats |a_kk| either
+        const unsigned long long key =
+            (bv >= 0.0) ? static_cast<unsigned long long>(__double_as_longlong(bv)) : 0ull;
+        const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        bi = __reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? bi : 0x7fffffff);
+        bv = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
       }
       int piv = k;
       double best = fabs(vk);
-      if (lane == 0 && bv > best) {  // NaN |a_kk|: nothing beats it and the pivot test fails, as the reference
+      if (bv > best) {  // NaN |a_kk|: nothing beats it and the pivot test fails, as the reference
         best = bv;
         piv = bi;
       }
-      piv = __shfl_sync(0xffffffffu, piv, 0);
-      best = __shfl_sync(0xffffffffu, best, 0);
       // value of the pivot row (owner lane (piv - k) % 32, slot (piv - k) / 32)
       const int d = piv - k;
       double vp = 0.0;
