@@ -11,6 +11,8 @@ import ctypes as C
 import os
 import threading
 
+import numpy as np
+
 from . import _abi as A
 
 LIB_PATH = os.environ.get("REACH_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
@@ -125,6 +127,25 @@ def lib():
         return _lib
 
 
+def _layers_snapshot(net):
+    """Copies of an MLPNet's (w, b, act) per layer, or None for other net types."""
+    layers = getattr(net, "layers", None)
+    if layers is None:
+        return None
+    return [(np.array(L.w, dtype=np.float64, copy=True), np.array(L.b, dtype=np.float64, copy=True), L.act)
+            for L in layers]
+
+
+def _layers_equal(net, snap) -> bool:
+    layers = net.layers
+    if len(layers) != len(snap):
+        return False
+    for L, (w, b, act) in zip(layers, snap):
+        if L.act != act or not np.array_equal(L.w, w) or not np.array_equal(L.b, b):
+            return False
+    return True
+
+
 class Context:
     """reach_ctx: one CUDA device + stream + workspaces (one per host thread)."""
 
@@ -137,6 +158,7 @@ class Context:
         self.handle = h
         self.device = device
         self._nets = collections.OrderedDict()  # content key -> (net, handle), most recent last
+        self._net_memo = {}  # id(net) -> (net, layer snapshot, content key)
 
     def check(self, rc: int, what: str):
         if rc == A.REACH_OK:
@@ -241,9 +263,22 @@ class Context:
         bounded LRU: a weight-update loop uploads a new value every step, and the oldest
         handles are freed (reach_net_free) beyond MAX_CACHED_NETS."""
         import hashlib
+        # fast path for the same net object called again (the batch-1 latency case): compare its layers
+        # against the snapshot taken at upload (a memcmp per array) instead of re-hashing the whole net
+        memo = self._net_memo.get(id(net))
+        if memo is not None:
+            obj, snap, key = memo
+            if obj is net and key in self._nets and _layers_equal(net, snap):
+                self._nets.move_to_end(key)
+                return self._nets[key][1]
         desc, keep = net.desc()
         blob = b"".join(a.tobytes() for a in keep)
         key = hashlib.blake2b(blob, digest_size=16).digest() + len(blob).to_bytes(8, "little")
+        snap = _layers_snapshot(net)
+        if snap is not None:
+            if len(self._net_memo) >= 4 * self.MAX_CACHED_NETS:
+                self._net_memo.clear()
+            self._net_memo[id(net)] = (net, snap, key)
         hit = self._nets.get(key)
         if hit is not None:
             self._nets.move_to_end(key)
@@ -262,6 +297,7 @@ class Context:
             for _, (_, h) in list(self._nets.items()):
                 self._lib.reach_net_free(self.handle, h)
             self._nets.clear()
+            self._net_memo.clear()
             self._lib.reach_ctx_destroy(self.handle)
             self.handle = None
 

@@ -75,6 +75,9 @@ struct DTLayout {
 // (C4 sweep 116.7 -> 104.1 ms; measured sweep in profiles/r01_c4_summary.md).
 constexpr int kStageDoublesDefault = 6144;
 constexpr int kNStageDefault = 2;
+// host-pointer DT calls whose device workspace is at most this large stage through pinned memory (one
+// copy in, one copy out)
+constexpr size_t kSmallCallBytes = 1u << 20;
 
 // Weight-stream ring geometry; RB_NSTAGE / RB_STAGE_DOUBLES override it for tuning runs.
 int env_int(const char* name, int dflt, int lo, int hi) {
@@ -673,6 +676,8 @@ int run_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_net* ctl, con
   const size_t x_bytes = B * n * 8, act_bytes = (a->actions_shared ? 1 : B) * H * m * 8;
   const size_t box_bytes = B * (H + 1) * n * 8, i_bytes = B * 4;
   const bool dev = (flags & REACH_FLAG_DEVICE_PTRS) != 0;
+  bool small = false;
+  size_t o_out = 0, out_end = 0;
   if (dev) {
     P.x0_lo = a->x0_lo;
     P.x0_hi = a->x0_hi;
@@ -703,10 +708,25 @@ int run_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_net* ctl, con
     P.n_boxes = reinterpret_cast<int*>(w + o_nb);
     P.failed_step = reinterpret_cast<int*>(w + o_fs);
     P.status = reinterpret_cast<int*>(w + o_st);
-    RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.x0_lo), a->x0_lo, x_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.x0_hi), a->x0_hi, x_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    if (act_bytes)
-      RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.actions), a->actions, act_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    // small calls (the batch-1 latency case): every input in ONE copy and every output in ONE copy through
+    // the context's pinned staging, laid out as the device workspace
+    small = off <= kSmallCallBytes;
+    if (small) {
+      rc = ensure_pinned(ctx, off);
+      if (rc) return rc;
+      char* h = static_cast<char*>(ctx->hpin);
+      std::memcpy(h + o_xl, a->x0_lo, x_bytes);
+      std::memcpy(h + o_xh, a->x0_hi, x_bytes);
+      if (act_bytes) std::memcpy(h + o_a, a->actions, act_bytes);
+      RB_CUDA(cudaMemcpyAsync(w, h, o_ol, cudaMemcpyHostToDevice, ctx->stream));
+      o_out = o_ol;
+      out_end = off;
+    } else {
+      RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.x0_lo), a->x0_lo, x_bytes, cudaMemcpyHostToDevice, ctx->stream));
+      RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.x0_hi), a->x0_hi, x_bytes, cudaMemcpyHostToDevice, ctx->stream));
+      if (act_bytes)
+        RB_CUDA(cudaMemcpyAsync(const_cast<double*>(P.actions), a->actions, act_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    }
   }
   cudaEvent_t stop;
   rc = timed_begin(ctx, &stop);
@@ -715,7 +735,26 @@ int run_dt_batch(reach_ctx* ctx, const reach_net* net, const reach_net* ctl, con
   rc = timed_end(ctx, stop);
   if (rc) return rc;
   ctx->launches += 1;
-  if (!dev) {
+  if (!dev && small) {
+    // one read-back of the whole output region; boxes beyond n_boxes stay untouched in the caller's buffer
+    const char* h = static_cast<const char*>(ctx->hpin);
+    RB_CUDA(cudaMemcpyAsync(static_cast<char*>(ctx->hpin) + o_out, static_cast<const char*>(ctx->ws) + o_out,
+                            out_end - o_out, cudaMemcpyDeviceToHost, ctx->stream));
+    RB_CUDA(cudaStreamSynchronize(ctx->stream));
+    const char* base = static_cast<const char*>(ctx->ws);
+    auto host = [&](const void* dptr) { return h + (static_cast<const char*>(dptr) - base); };
+    std::memcpy(out->n_boxes, host(P.n_boxes), i_bytes);
+    std::memcpy(out->failed_step, host(P.failed_step), i_bytes);
+    std::memcpy(out->status, host(P.status), i_bytes);
+    const double* hl = reinterpret_cast<const double*>(host(P.out_lo));
+    const double* hh = reinterpret_cast<const double*>(host(P.out_hi));
+    for (size_t i = 0; i < B; ++i) {
+      const size_t o = i * (H + 1) * n, cnt = static_cast<size_t>(out->n_boxes[i]) * n * 8;
+      if (!cnt) continue;
+      std::memcpy(out->lo + o, hl + o, cnt);
+      std::memcpy(out->hi + o, hh + o, cnt);
+    }
+  } else if (!dev) {
     // boxes beyond n_boxes are untouched in the caller's buffer: copy only the
     // tube prefix per sample after reading n_boxes
     std::vector<int32_t> nb(B);

@@ -217,3 +217,26 @@ def test_outward_rounding_flag_is_refused():
     rc = ctx._lib.reach_dt_batch(ctx.handle, ctx.upload(net), C.byref(args), C.byref(to), A.REACH_FLAG_OUTWARD_ROUNDING)
     assert rc == A.REACH_E_UNSUPPORTED
     assert "outward rounding" in ctx._lib.reach_ctx_last_error(ctx.handle).decode()
+
+
+def test_net_cache_sees_in_place_weight_updates():
+    """Context.upload's same-object fast path: an unchanged net reuses its device handle, an in-place
+    weight update uploads the new value (and the results follow it), restoring it hits the cache again."""
+    from paper_2605_25346_b200 import Context
+    rng = np.random.default_rng(7)
+    net = residual_relu_dynamics(rng, 4, 0, [64, 64], dt=0.1)
+    sys_ = DTSystem(net, 4, 0)
+    ctx = Context(0)
+    h0 = ctx.upload(net).value
+    assert ctx.upload(net).value == h0
+    c = rng.uniform(-0.5, 0.5, size=(3, 4))
+    lo, hi = c - 0.01, c + 0.01
+    acts = np.zeros((3, 5, 0))
+    before = dt_reach_batch_arrays(sys_, lo, hi, acts, DTReachParams(), ctx=ctx)
+    net.layers[1].w[3, 5] += 0.25
+    assert ctx.upload(net).value != h0
+    after = dt_reach_batch_arrays(sys_, lo, hi, acts, DTReachParams(), ctx=ctx)
+    assert_tubes_equal(after, oracle_dt_batch(sys_, lo, hi, acts, DTReachParams()), exact=True)
+    assert not np.array_equal(after.lo, before.lo)
+    net.layers[1].w[3, 5] -= 0.25
+    assert ctx.upload(net).value == h0
