@@ -33,6 +33,10 @@ def main():
     wait = cyc[10]
     cyc = cyc[:10]
     tot = sum(cyc)
+    if tot == 0:
+        print(f"wall {dt*1e3:.1f} ms; the horizon kernel carries no phase marks in this build (they went away when "
+              "certify_tm_input became a device function; use the ncu source view, profiles/r02_c4_summary.md)")
+        return
     print(f"wall {dt*1e3:.1f} ms; warp-cycles {tot:.3e}")
     for nm, c in zip(NAMES, cyc):
         print(f"  {nm:9s} {100*c/tot:5.1f}%  {c/ (w.plan.total_parts() if not parts else parts) / w.horizon:9.0f} cyc/sample-step")
