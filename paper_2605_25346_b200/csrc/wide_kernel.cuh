@@ -772,24 +772,32 @@ static __device__ void wide_fold(double* S, long long lds, int n, int& base, int
     load_block(M, Sb, lds, n, nc);
     __syncthreads();
     if (folded) {
-      // E = G0 X - a (in place of a): two outputs per thread in flight
-      const int tot = n * w;
-      for (int e0 = tid; e0 < tot; e0 += 2 * kWideThreads) {
-        const int e1 = e0 + kWideThreads;
-        const int i0 = e0 / w, c0 = e0 - i0 * w;
-        const int e1c = e1 < tot ? e1 : e0;
-        const int i1 = e1c / w, c1 = e1c - i1 * w;
-        double acc0 = 0.0, acc1 = 0.0;
+      // E = G0 X - a (in place of a): a 2 x 2 output tile per thread (rows i, i + 1; columns c, c + w/2),
+      // four independent chains in flight, each in the reference's k order
+      const int wh = (w + 1) >> 1, nh = (n + 1) >> 1;
+      for (int t = tid; t < nh * wh; t += kWideThreads) {
+        const int ip = t / wh, cp = t - ip * wh;
+        const int i0 = 2 * ip, c0 = cp;
+        const bool vi = i0 + 1 < n, vc = cp + wh < w;
+        const int i1 = vi ? i0 + 1 : i0, c1 = vc ? cp + wh : cp;
+        double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
         const double* g0 = M + i0 * nc;
         const double* g1 = M + i1 * nc;
 #pragma unroll 4
         for (int k = 0; k < n; ++k) {
-          acc0 = add(acc0, mul(g0[k], X[k * w + c0]));
-          acc1 = add(acc1, mul(g1[k], X[k * w + c1]));
+          const double ga = g0[k], gb = g1[k], x0 = X[k * w + c0], x1 = X[k * w + c1];
+          a00 = add(a00, mul(ga, x0));
+          a01 = add(a01, mul(ga, x1));
+          a10 = add(a10, mul(gb, x0));
+          a11 = add(a11, mul(gb, x1));
         }
-        const double a0 = M[i0 * nc + n + c0], a1 = M[i1 * nc + n + c1];
-        M[i0 * nc + n + c0] = sub(acc0, a0);
-        if (e1 < tot) M[i1 * nc + n + c1] = sub(acc1, a1);
+        double* e0 = M + i0 * nc + n;
+        double* e1 = M + i1 * nc + n;
+        const double b00 = e0[c0], b01 = e0[c1], b10 = e1[c0], b11 = e1[c1];
+        e0[c0] = sub(a00, b00);
+        if (vc) e0[c1] = sub(a01, b01);
+        if (vi) e1[c0] = sub(a10, b10);
+        if (vi && vc) e1[c1] = sub(a11, b11);
       }
       __syncthreads();
     }
