@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) dt_tcw_kernel(const DTParams 
       __syncthreads();
       // ---- fold_overflow (flowpipe_ct.hpp:317-350)
       ph.mark(WP_FOLD);
-      wide_fold(cur, lds, n, base, nq, cap, W, ph);
+      wide_fold<72>(cur, lds, n, base, nq, cap, W, ph);
       // ---- symbolic_box (flowpipe_ct.hpp:413-424)
       ph.mark(WP_BOX);
       bool fin = true;

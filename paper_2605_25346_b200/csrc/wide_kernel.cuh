@@ -552,9 +552,49 @@ __device__ __forceinline__ void load_block(double* M, const double* Sb, long lon
   cp_wait<0>();
 }
 
+// Back substitution of mat_solve (linalg.hpp:125-131) with the solution column in registers: xb[q] = x_{n-1-q};
+// row r from the bottom (i = n - 1 - r) subtracts a_{i,k} x_k for k = i + 1 .. n - 1, i.e. q = r - 1 .. 0.
+// Fused mode: four partial sums over k >= i + 2 (as the generic fused loop), exact: the reference's chain
+// (used by the fused build only, see wide_fold).
+template <int NMAX>
+__device__ __forceinline__ void backsub_regs(const double* M, const int* Pf, double* X, int n, int nc, int w, int tid) {
+  for (int jc = tid; jc < w; jc += kWideThreads) {
+    double xb[NMAX];
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r) {
+      xb[r] = 0.0;
+      if (r < n) {
+        const int i = n - 1 - r;
+        const double* mr = M + Pf[i] * nc + (n - 1);  // mr[-q] = a_{i, n-1-q}
+        const double bi = mr[1 + jc];
+#if RB_FUSED
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int q = r - 2; q >= 0; q -= 4) {
+          s0 = fma(mr[-q], xb[q], s0);
+          if (q >= 1) s1 = fma(mr[-(q - 1)], xb[q - 1], s1);
+          if (q >= 2) s2 = fma(mr[-(q - 2)], xb[q - 2], s2);
+          if (q >= 3) s3 = fma(mr[-(q - 3)], xb[q - 3], s3);
+        }
+        double acc = bi - ((s0 + s1) + (s2 + s3));
+        if (r >= 1) acc = fma(-mr[-(r - 1)], xb[r - 1], acc);
+        xb[r] = acc / mr[-r];
+#else
+        double acc = bi;
+#pragma unroll
+        for (int q = r - 1; q >= 0; --q) acc = sub(acc, mul(mr[-q], xb[q]));
+        xb[r] = __ddiv_rn(acc, mr[-r]);
+#endif
+        X[i * w + jc] = xb[r];
+      }
+    }
+  }
+}
+
 // fold_overflow (flowpipe_ct.hpp:317-350) on the state in S (rows 0..n-1, row
 // stride lds, live columns [base, base + nz)).  Popping the oldest block moves
 // the (possibly rescaled) G0 right by its width instead of moving the queue.
+template <int NMAX>
 static __device__ void wide_fold(double* S, long long lds, int n, int& base, int& nq, int cap, const WideSmem& W,
                                  WPhase& ph) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -703,6 +743,14 @@ static __device__ void wide_fold(double* S, long long lds, int n, int& base, int
     bool folded = false;
     ph.mark(WP_FOLD_BACK);
     if (ok) {
+#if RB_FUSED
+      if constexpr (NMAX == 72) {
+        // fused mode, C5-class states (33 <= n <= 72): rows and products unrolled against the solution
+        // column held per thread (C5 fused back substitution 173 k -> 105 k cycles per reach-step; the
+        // exact mode's single subtraction chain measured slower this way, 165 k -> 201 k, and keeps the loop)
+        backsub_regs<NMAX>(M, Pf, X, n, nc, w, tid);
+      } else
+#endif
       // back substitution, one RHS column per thread; x_{i+1} stays in a
       // register, the older x_k are read in blocks of 4 ahead of the chain
       for (int jc = tid; jc < w; jc += kWideThreads) {
@@ -977,7 +1025,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) dt_wide_kernel(const DTParams
       __syncthreads();
       // ---- fold_overflow (flowpipe_ct.hpp:317-350)
       ph.mark(WP_FOLD);
-      wide_fold(cur, lds, n, base, nq, cap, W, ph);
+      wide_fold<8 * RD>(cur, lds, n, base, nq, cap, W, ph);
       ph.mark(WP_BOX);
       // ---- symbolic_box (flowpipe_ct.hpp:413-424)
       bool fin = true;
