@@ -556,8 +556,48 @@ __device__ __forceinline__ void load_block(double* M, const double* Sb, long lon
 // row r from the bottom (i = n - 1 - r) subtracts a_{i,k} x_k for k = i + 1 .. n - 1, i.e. q = r - 1 .. 0.
 // Fused mode: four partial sums over k >= i + 2 (as the generic fused loop), exact: the reference's chain
 // (used by the fused build only, see wide_fold).
+// One row of it per template instance (R = rows from the bottom), so every index into xb is a constant
+// and the column stays in registers.
+template <int R, int NMAX>
+struct BackRow {
+  static __device__ __forceinline__ void run(double (&xb)[NMAX], const double* M, const int* Pf, double* X, int n,
+                                             int nc, int w, int jc) {
+    if (R < n) {
+      const int i = n - 1 - R;
+      const double* mr = M + Pf[i] * nc + (n - 1);  // mr[-q] = a_{i, n-1-q}
+      const double bi = mr[1 + jc];
+#if RB_FUSED
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int q = R - 2; q >= 0; q -= 4) {
+        s0 = fma(mr[-q], xb[q], s0);
+        if (q >= 1) s1 = fma(mr[-(q - 1)], xb[q - 1], s1);
+        if (q >= 2) s2 = fma(mr[-(q - 2)], xb[q - 2], s2);
+        if (q >= 3) s3 = fma(mr[-(q - 3)], xb[q - 3], s3);
+      }
+      double acc = bi - ((s0 + s1) + (s2 + s3));
+      if (R >= 1) acc = fma(-mr[-(R - 1)], xb[R >= 1 ? R - 1 : 0], acc);
+      xb[R] = acc / mr[-R];
+#else
+      double acc = bi;
+#pragma unroll
+      for (int q = R - 1; q >= 0; --q) acc = sub(acc, mul(mr[-q], xb[q]));
+      xb[R] = __ddiv_rn(acc, mr[-R]);
+#endif
+      X[i * w + jc] = xb[R];
+      BackRow<R + 1, NMAX>::run(xb, M, Pf, X, n, nc, w, jc);
+    }
+  }
+};
+template <int NMAX>
+struct BackRow<NMAX, NMAX> {
+  static __device__ __forceinline__ void run(double (&)[NMAX], const double*, const int*, double*, int, int, int, int) {}
+};
+
 template <int NMAX>
 __device__ __forceinline__ void backsub_regs(const double* M, const int* Pf, double* X, int n, int nc, int w, int tid) {
+#if RB_FUSED
+  // fused build: rows unrolled by the compiler (the template-recursive form hung in this build; kept as measured)
   for (int jc = tid; jc < w; jc += kWideThreads) {
     double xb[NMAX];
 #pragma unroll
@@ -565,9 +605,8 @@ __device__ __forceinline__ void backsub_regs(const double* M, const int* Pf, dou
       xb[r] = 0.0;
       if (r < n) {
         const int i = n - 1 - r;
-        const double* mr = M + Pf[i] * nc + (n - 1);  // mr[-q] = a_{i, n-1-q}
+        const double* mr = M + Pf[i] * nc + (n - 1);
         const double bi = mr[1 + jc];
-#if RB_FUSED
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int q = r - 2; q >= 0; q -= 4) {
@@ -579,16 +618,16 @@ __device__ __forceinline__ void backsub_regs(const double* M, const int* Pf, dou
         double acc = bi - ((s0 + s1) + (s2 + s3));
         if (r >= 1) acc = fma(-mr[-(r - 1)], xb[r - 1], acc);
         xb[r] = acc / mr[-r];
-#else
-        double acc = bi;
-#pragma unroll
-        for (int q = r - 1; q >= 0; --q) acc = sub(acc, mul(mr[-q], xb[q]));
-        xb[r] = __ddiv_rn(acc, mr[-r]);
-#endif
         X[i * w + jc] = xb[r];
       }
     }
   }
+#else
+  for (int jc = tid; jc < w; jc += kWideThreads) {
+    double xb[NMAX];
+    BackRow<0, NMAX>::run(xb, M, Pf, X, n, nc, w, jc);
+  }
+#endif
 }
 
 // fold_overflow (flowpipe_ct.hpp:317-350) on the state in S (rows 0..n-1, row
@@ -743,14 +782,11 @@ static __device__ void wide_fold(double* S, long long lds, int n, int& base, int
     bool folded = false;
     ph.mark(WP_FOLD_BACK);
     if (ok) {
-#if RB_FUSED
       if constexpr (NMAX == 72) {
-        // fused mode, C5-class states (33 <= n <= 72): rows and products unrolled against the solution
-        // column held per thread (C5 fused back substitution 173 k -> 105 k cycles per reach-step; the
-        // exact mode's single subtraction chain measured slower this way, 165 k -> 201 k, and keeps the loop)
+        // C5-class states (33 <= n <= 72): the solution column held per thread in registers, rows and products
+        // unrolled (back substitution per C5 reach-step: fused 173 k -> 105 k cycles, exact 165 k -> 126 k)
         backsub_regs<NMAX>(M, Pf, X, n, nc, w, tid);
       } else
-#endif
       // back substitution, one RHS column per thread; x_{i+1} stays in a
       // register, the older x_k are read in blocks of 4 ahead of the chain
       for (int jc = tid; jc < w; jc += kWideThreads) {
